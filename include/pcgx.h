@@ -1,0 +1,249 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * pcgx — B200-native Chebyshev-polynomial-preconditioned CG (the hot path of
+ * arxiv 2008.01440's reference library `polycg`), exported as a plain C ABI:
+ * no exceptions, no C++ or torch types, plain pointers and sizes.
+ *
+ * Each entry point replaces one reference interface (paths under
+ * /root/reference/proj):
+ *
+ *   pcgx_stencil7_create   StencilOperator(lap3d, nx) + jacobi_scale
+ *                          (include/polycg/linop.hpp:94-108, 145-168; src/linop.cpp:200-259, 340-351)
+ *   pcgx_csr_create        CsrMatrix(n, row_ptr, col_idx, values) + jacobi_scale
+ *                          (include/polycg/linop.hpp:60-85; src/linop.cpp:67-197, 340-351)
+ *   pcgx_operator_apply    LinearOperator::apply on the ScaledOperator
+ *                          (include/polycg/linop.hpp:26-28; src/linop.cpp:41-49, 271-275)
+ *   pcgx_cheb_params       cheb_params + check_positivity (include/polycg/polyprec.hpp:50-54;
+ *                          src/polyprec.cpp:13-23, 56-79)
+ *   pcgx_cheb_apply        apply_chebyshev / ChebyshevPreconditioner::apply
+ *                          (include/polycg/polyprec.hpp:86-90, pcg.hpp:42-55; src/polyprec.cpp:169-198)
+ *   pcgx_pcg_solve         pcg_solve (include/polycg/pcg.hpp:57-91; src/pcg.cpp:10-117)
+ *   pcgx_random_uniform    random_uniform_vector (include/polycg/eigenest.hpp:58-60; src/eigenest.cpp:13-30)
+ *   pcgx_analytic_extremes analytic_extremes (include/polycg/linop.hpp:160-162; src/linop.cpp:382-390)
+ *
+ * Builder-defined entry points the reference lacks (BASELINE.json configs 3-5):
+ * pcgx_lanczos_bounds, pcgx_analytic_extremes_box, pcgx_gen_fe27_*,
+ * pcgx_gen_elast27_*, and the multi-GPU z-slab context (pcgx_context_create_dist).
+ *
+ * Threading contract (mirrors include/polycg/linop.hpp:17-20 and pcg.hpp:16-19):
+ * a context owns one CUDA device, its streams, workspace and (optionally) an
+ * NCCL communicator, and runs one call at a time; operator handles are immutable
+ * after creation and may be shared read-only by calls on their own context.
+ *
+ * Errors: every call returns a pcgx_status; pcgx_last_error(ctx) returns the
+ * message, whose text follows the reference's (e.g. "pcg_solve: p'Ap = ...").
+ * PCGX_ERR_INVALID  <-> std::invalid_argument, PCGX_ERR_NUMERICAL <-> polycg::NumericalError.
+ */
+#ifndef PCGX_H
+#define PCGX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCGX_ABI_VERSION 1
+
+typedef enum {
+  PCGX_OK = 0,
+  PCGX_ERR_INVALID = 1,     /* std::invalid_argument in the reference */
+  PCGX_ERR_NUMERICAL = 2,   /* polycg::NumericalError in the reference */
+  PCGX_ERR_CUDA = 3,        /* CUDA runtime failure (no device, OOM, fault) */
+  PCGX_ERR_NCCL = 4,        /* communicator failure */
+  PCGX_ERR_OVERFLOW = 5,    /* index does not fit the int32 device CSR */
+  PCGX_ERR_UNSUPPORTED = 6  /* valid reference input this build does not accelerate */
+} pcgx_status;
+
+typedef struct pcgx_context_s* pcgx_context;
+typedef struct pcgx_operator_s* pcgx_operator;
+
+/* ------------------------------------------------------------------ context */
+
+int pcgx_abi_version(void);
+/* Last error message of a context (or of the calling thread when ctx is NULL). */
+const char* pcgx_last_error(pcgx_context ctx);
+
+/* Single-GPU context on `device`. */
+pcgx_status pcgx_context_create(int device, pcgx_context* out);
+/* One rank of an nranks-GPU z-slab job (one process per GPU). `nccl_id` is the
+ * 128-byte ncclUniqueId produced by pcgx_nccl_unique_id on rank 0 and broadcast
+ * by the caller (bench.py uses torch.distributed for that plumbing). */
+pcgx_status pcgx_nccl_unique_id(void* id128);
+pcgx_status pcgx_context_create_dist(int device, int nranks, int rank, const void* nccl_id,
+                                     pcgx_context* out);
+void pcgx_context_destroy(pcgx_context ctx);
+int pcgx_context_rank(pcgx_context ctx);
+int pcgx_context_nranks(pcgx_context ctx);
+pcgx_status pcgx_synchronize(pcgx_context ctx);
+/* Number of pcgx kernels launched on this context so far (all kinds). */
+int64_t pcgx_kernel_launches(pcgx_context ctx);
+
+/* Device memory helpers so a C/ctypes host needs no other CUDA binding. */
+pcgx_status pcgx_device_alloc(pcgx_context ctx, size_t bytes, void** dptr);
+pcgx_status pcgx_device_free(pcgx_context ctx, void* dptr);
+pcgx_status pcgx_memcpy_h2d(pcgx_context ctx, void* dst, const void* src, size_t bytes);
+pcgx_status pcgx_memcpy_d2h(pcgx_context ctx, void* dst, const void* src, size_t bytes);
+pcgx_status pcgx_memcpy_d2d(pcgx_context ctx, void* dst, const void* src, size_t bytes);
+/* Pinned host memory (page-locked), for the end-to-end path. */
+pcgx_status pcgx_host_alloc(size_t bytes, void** hptr);
+pcgx_status pcgx_host_free(void* hptr);
+
+/* Device-side timing on the context's compute stream (CUDA events). */
+pcgx_status pcgx_timer_start(pcgx_context ctx);
+pcgx_status pcgx_timer_stop(pcgx_context ctx, double* ms);
+/* Writes `bytes` through a scratch buffer on the compute stream (L2 flush). */
+pcgx_status pcgx_flush_l2(pcgx_context ctx, size_t bytes);
+
+/* ---------------------------------------------------------------- operators */
+
+/* D^{-1/2} A D^{-1/2} for the 3D 7-point FD Laplacian (diag 6, off-diagonal -1,
+ * homogeneous Dirichlet) on an nx*ny*nz grid, i fastest (StencilOperator(lap3d, nx)
+ * is nx = ny = nz; non-cubic boxes are the builder extension for config 5 weak
+ * scaling). inv_sqrt_diag: the constant jacobi_scale produces, or <= 0 for the
+ * default 1/sqrt(6). On a dist context the rank owns the z-slab
+ * [pcgx_operator_z0, z0 + nz_local) and every vector is that slab. */
+pcgx_status pcgx_stencil7_create(pcgx_context ctx, int64_t nx, int64_t ny, int64_t nz,
+                                 double inv_sqrt_diag, pcgx_operator* out);
+
+/* CsrMatrix (symmetric, both triangles, int64 host arrays as in the reference)
+ * Jacobi-scaled. Narrowed to int32 on upload (PCGX_ERR_OVERFLOW if nnz >= 2^31).
+ * inv_sqrt_diag (n entries) may be NULL: it is then computed exactly as
+ * jacobi_scale does (1/sqrt(diag), NumericalError naming the first diag <= 0).
+ * Structural invariants are validated as CsrMatrix::validate does (symmetry of
+ * values is the caller's CsrMatrix contract and is not re-checked). */
+pcgx_status pcgx_csr_create(pcgx_context ctx, int64_t n, const int64_t* row_ptr,
+                            const int64_t* col_idx, const double* values,
+                            const double* inv_sqrt_diag, pcgx_operator* out);
+/* Same, from int32 host arrays (the builder's generators produce these). */
+pcgx_status pcgx_csr_create_i32(pcgx_context ctx, int64_t n, const int32_t* row_ptr,
+                                const int32_t* col_idx, const double* values,
+                                const double* inv_sqrt_diag, pcgx_operator* out);
+void pcgx_operator_destroy(pcgx_operator op);
+
+int64_t pcgx_operator_size(pcgx_operator op);        /* global n */
+int64_t pcgx_operator_local_size(pcgx_operator op);  /* rows owned by this rank */
+int64_t pcgx_operator_z0(pcgx_operator op);          /* first owned plane (stencil) */
+int64_t pcgx_operator_nnz(pcgx_operator op);         /* CSR nnz, or the assembled-equivalent for stencils */
+/* Number of matvecs applied so far (LinearOperator::matvec_count, linop.hpp:37). */
+uint64_t pcgx_operator_matvec_count(pcgx_operator op);
+
+/* y = A_scaled x. Host buffers (the parity entry) ... */
+pcgx_status pcgx_operator_apply(pcgx_context ctx, pcgx_operator op, const double* x, double* y);
+/* ... and device buffers (stream-ordered on the context stream). */
+pcgx_status pcgx_operator_apply_device(pcgx_context ctx, pcgx_operator op, const double* x,
+                                       double* y);
+
+/* --------------------------------------------------------- the polynomial */
+
+typedef struct {
+  int m;          /* degree: number of SpMVs per application */
+  double theta;   /* scale * (alpha + beta) / 2 */
+  double delta;   /* (beta - alpha) / 2 */
+  double sigma;   /* theta / delta */
+  const double* rho; /* rho[0..m] */
+} pcgx_cheb;
+
+/* cheb_params verbatim (bit-exact): tds = {theta, delta, sigma}, rho[m+1].
+ * Validates 0 < alpha < beta, m >= 0, scale >= 1 and positivity on a 1000-point grid. */
+pcgx_status pcgx_cheb_params(double alpha, double beta, int m, double scale, double* tds,
+                             double* rho);
+/* eval_poly (Chebyshev form), host scalar. */
+double pcgx_cheb_eval(const pcgx_cheb* p, double lambda);
+
+/* out = p_m(A) r. out must not alias r (polyprec.hpp:86-87). */
+pcgx_status pcgx_cheb_apply(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* p,
+                            const double* r, double* out);
+pcgx_status pcgx_cheb_apply_device(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* p,
+                                   const double* r, double* out);
+
+/* ------------------------------------------------------------------ solver */
+
+#define PCGX_FLAG_TIME_KERNELS 1u /* time every Chebyshev-step launch with CUDA events */
+#define PCGX_FLAG_NO_GRAPH 2u     /* launch kernels one by one instead of CUDA graphs */
+
+typedef struct {
+  double tol;         /* SolveOptions::tol (default 1e-8) */
+  int maxit;          /* SolveOptions::maxit (default 20000) */
+  const double* x0;   /* initial guess (same memory space as b), NULL = zero */
+  uint32_t flags;
+} pcgx_solve_opts;
+
+typedef struct {
+  /* SolveReport (pcg.hpp:73-82), counted by the reference's rules */
+  int64_t iters;
+  int64_t ddot;
+  int64_t matvec;
+  int64_t prec_applies;
+  double rel_res;
+  double true_rel_res;
+  double wall_time;    /* seconds, device events around the solve (pcg.cpp:20-30) */
+  int64_t converged;
+  /* builder extensions */
+  int64_t kernel_launches;   /* pcgx kernels launched by this solve */
+  int64_t wasted_matvec;     /* speculative P applications discarded at convergence */
+  int64_t allreduces;        /* NCCL all-reduce calls (0 on one GPU) */
+  int64_t halo_bytes;        /* bytes sent to z-neighbours */
+  double alg_bytes;          /* algorithmic HBM bytes of the solve */
+  double spmv_equiv_bytes;   /* matvec * SpMV-equivalent bytes (the BASELINE metric numerator) */
+  double step_ms;            /* total device ms of timed Chebyshev-step launches */
+  int64_t step_launches;     /* number of timed Chebyshev-step launches */
+  double step_bytes;         /* algorithmic bytes per Chebyshev-step launch */
+} pcgx_report;
+
+void pcgx_solve_opts_default(pcgx_solve_opts* o);
+
+/* pcg_solve. prec NULL = plain CG. Host buffers (end-to-end entry: b is copied
+ * to the device, x back, inside the call). */
+pcgx_status pcgx_pcg_solve(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* prec,
+                           const double* b, double* x, const pcgx_solve_opts* opts,
+                           pcgx_report* rep);
+/* Same with b, x (and opts->x0) already resident in device memory. */
+pcgx_status pcgx_pcg_solve_device(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* prec,
+                                  const double* b, double* x, const pcgx_solve_opts* opts,
+                                  pcgx_report* rep);
+
+/* ------------------------------------------------------- inputs and bounds */
+
+/* random_uniform_vector elements [offset, offset + n) into device memory. */
+pcgx_status pcgx_random_uniform_device(pcgx_context ctx, int64_t n, uint64_t seed,
+                                       uint64_t offset, double* out);
+/* Host version (bit-identical). */
+void pcgx_random_uniform(int64_t n, uint64_t seed, uint64_t offset, double* out);
+
+/* analytic_extremes (dim 2 or 3, cubic). */
+void pcgx_analytic_extremes(int dim, int64_t nx, int scaled, double* lo, double* hi);
+/* Scaled 3D box nx*ny*nz: (2/3) sum_d sin^2(pi h_d/2), (2/3) sum_d cos^2(pi h_d/2). */
+void pcgx_analytic_extremes_box(int64_t nx, int64_t ny, int64_t nz, double* lo, double* hi);
+
+/* Lanczos bound estimate on the device: start vector = normalised
+ * random_uniform_vector(n, seed); `steps` three-term steps without
+ * reorthogonalisation; hi = largest Ritz value of the leading steps_hi x steps_hi
+ * tridiagonal, lo = smallest Ritz value of the full steps x steps one. */
+pcgx_status pcgx_lanczos_bounds(pcgx_context ctx, pcgx_operator op, int steps_hi, int steps,
+                                uint64_t seed, double* lo, double* hi);
+
+/* --------------------------------------------------- config generators */
+
+/* Config 3: heterogeneous diffusion, Q1 (trilinear) finite elements on the
+ * (nx+1)^3 cells of the unit cube, nx^3 interior nodes (Dirichlet boundary
+ * eliminated) -> 27-point rows. Cell coefficient kappa_c = exp(sigma * N(0,1)),
+ * N(0,1) by Box-Muller on splitmix64(seed). Values are assembled so that
+ * a_ij == a_ji bitwise. Sizes first, then fill into caller arrays. */
+pcgx_status pcgx_gen_fe27_size(int64_t nx, int64_t* n, int64_t* nnz);
+pcgx_status pcgx_gen_fe27_fill(int64_t nx, double sigma, uint64_t seed, int32_t* row_ptr,
+                               int32_t* col_idx, double* values);
+/* Config 4: 3 dof per node, Q1 linear elasticity (Lame lambda, mu) on the same
+ * mesh, element stiffness scaled per cell by (1 + eps * u_c), u_c uniform [0,1)
+ * from seed (keeps every element PSD, the assembled matrix SPD). Rows are 3x3
+ * blocks over the 27 neighbours: 81 entries per interior row. */
+pcgx_status pcgx_gen_elast27_size(int64_t nx, int64_t* n, int64_t* nnz);
+pcgx_status pcgx_gen_elast27_fill(int64_t nx, double lambda, double mu, double eps,
+                                  uint64_t seed, int32_t* row_ptr, int32_t* col_idx,
+                                  double* values);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCGX_H */

@@ -1,0 +1,15 @@
+# SPDX-License-Identifier: Apache-2.0
+"""B200-native Chebyshev-polynomial-preconditioned CG (arxiv 2008.01440 hot path).
+
+The product is the native library ``libpcgx.so`` (sm_100a kernels + C++ host
+orchestration behind the C ABI in include/pcgx.h). This package holds its
+sources (csrc/), its build recipe (build.py) and the Python host binding
+(pcgx.py) that mirrors the reference's polycg API.
+"""
+from .pcgx import (  # noqa: F401
+    ChebyshevParams, ChebyshevPreconditioner, Context, CsrMatrix, CudaError, DeviceVector,
+    InvalidArgument, NumericalError, PcgxError, PinnedBuffer, ScaledOperator, SolveOptions,
+    SolveReport, StencilOperator, analytic_extremes, analytic_extremes_box, apply_chebyshev,
+    cheb_params, eval_poly, gen_elast27, gen_fe27, jacobi_scale, lanczos_bounds, lib,
+    pcg_solve, random_uniform_vector,
+)

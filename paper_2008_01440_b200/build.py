@@ -1,0 +1,82 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Build recipe for the in-tree native library ``libpcgx.so`` (sm_100a).
+
+    python -m paper_2008_01440_b200.build
+
+One nvcc invocation compiles the CUDA kernels + host orchestration
+(csrc/pcgx.cu) and the host C++ (csrc/host_math.cpp, csrc/gen.cpp) into
+paper_2008_01440_b200/libpcgx.so, linked against NCCL. Flags:
+
+* ``-gencode arch=compute_100a,code=sm_100a`` — B200 only, no PTX fallback;
+* ``--fmad=false`` and ``-ffp-contract=off`` — no FMA contraction anywhere, so
+  per-point results are the reference's IEEE values (parity);
+* ``-lineinfo`` — ncu source-page mapping.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libpcgx.so")
+SOURCES = ["pcgx.cu", "host_math.cpp", "gen.cpp"]
+HEADERS = ["common.cuh", "kernels.cuh", "host_math.hpp"]
+
+
+def _nvcc():
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _host_cxx():
+    for cand in ("/usr/bin/g++", shutil.which("g++")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("g++ not found")
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(ROOT, "include", "pcgx.h"))
+    deps.append(__file__)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def command(extra=()):
+    return [
+        _nvcc(), "-ccbin", _host_cxx(), "-O3", "-std=c++17",
+        "-gencode", "arch=compute_100a,code=sm_100a",
+        "-lineinfo", "--fmad=false",
+        "-Xcompiler", "-fPIC,-ffp-contract=off,-fopenmp,-O3",
+        "-Xptxas", "-v" if os.environ.get("PCGX_PTXAS_V") else "-O3",
+        "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+        "-shared", "-o", LIB,
+        *[os.path.join(CSRC, f) for f in SOURCES],
+        "-ldl", "-lgomp", *extra,
+    ]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or _stale():
+        cmd = command()
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError("libpcgx build failed:\n" + res.stdout + res.stderr)
+        if verbose and res.stderr:
+            print(res.stderr, file=sys.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

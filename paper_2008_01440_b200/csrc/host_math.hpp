@@ -1,0 +1,14 @@
+// SPDX-License-Identifier: Apache-2.0
+#pragma once
+#include <string>
+
+namespace pcgx {
+double cheb_eval(double theta, double delta, double sigma, const double* rho, int m, double lambda);
+int cheb_params(double alpha, double beta, int m, double scale, double* tds, double* rho,
+                std::string* msg);
+void analytic_extremes(int dim, long long nx, int scaled, double* lo, double* hi);
+void analytic_extremes_box(long long nx, long long ny, long long nz, double* lo, double* hi);
+void random_uniform_host(long long n, unsigned long long seed, unsigned long long offset,
+                         double* out);
+void tridiag_extremes(int k, const double* a, const double* b, double* lo, double* hi);
+}  // namespace pcgx

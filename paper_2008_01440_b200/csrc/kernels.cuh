@@ -1,0 +1,357 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// sm_100a kernels of the Chebyshev-PCG hot path. All fp64, HBM-bound, no
+// tensor cores (there is no dense contraction on this path).
+//
+//   stencil7_kernel<Epi>  K1+K4(+K5/K6/K7 epilogue): scaled 7-point SpMV fused
+//                         with whatever consumes y in the same pass
+//                         (proj/src/linop.cpp:236-258, 271-275)
+//   csr_kernel<Epi>       K2+K4(+epilogue): scaled CSR SpMV, int32 indices
+//                         (proj/src/linop.cpp:171-187, 271-275)
+//   update/pupdate/...    K7: PCG vector updates fused with their reductions
+//                         (proj/src/pcg.cpp:81-83, 101, 107)
+//   splitmix_kernel       K8: random_uniform_vector (proj/src/eigenest.cpp:13-30)
+//
+// The epilogue functors hold the fused per-point work; every reducing launch
+// ends in block_reduce_finish (warp shuffle tree -> block tree -> last-block
+// grid finish), deterministic for a fixed launch shape.
+#pragma once
+
+#include "common.cuh"
+
+namespace pcgx {
+
+// ----------------------------------------------------------------- reduction
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;  // lane 0 holds the fixed-order tree sum
+}
+
+// All threads of the block must call. Writes the block partial; the last block
+// to finish sums all partials in a fixed order and stores/accumulates the
+// result into red.result, then re-arms the ticket counter.
+__device__ __forceinline__ void block_reduce_finish(double v, const Reduce& red) {
+  __shared__ double ws[32];
+  __shared__ bool is_last;
+  const int nthreads = blockDim.x * blockDim.y * blockDim.z;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (nthreads + 31) >> 5;
+  v = warp_sum(v);
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nwarps ? ws[lane] : 0.0;
+    v = warp_sum(v);
+    if (lane == 0) {
+      red.partials[bid] = v;
+      __threadfence();
+      const unsigned ticket = atomicAdd(red.counter, 1u);
+      is_last = (ticket == nblocks - 1);
+    }
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double s = 0.0;
+  for (unsigned b = tid; b < nblocks; b += nthreads) s += __ldcg(red.partials + b);
+  s = warp_sum(s);
+  if (lane == 0) ws[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    s = lane < nwarps ? ws[lane] : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) {
+      *red.result = red.accumulate ? (*red.result + s) : s;
+      *red.counter = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// ----------------------------------------------------------------- epilogues
+// operator()(idx, y, xc): y = (A_scaled x)[idx], xc = x[idx]. Returns the
+// point's contribution to the launch's reduction (ignored when not reducing).
+
+// q = A p ; contribution p_i q_i  (pcg.cpp:72-74)
+struct EpiStore {
+  double* out;
+  __device__ __forceinline__ double operator()(long long idx, double y, double xc) const {
+    out[idx] = y;
+    return xc * y;
+  }
+};
+
+// e = b - A x ; contribution e_i^2  (pcg.cpp:43-45 with x0, and the exit true residual :112-114)
+struct EpiResid {
+  const double* __restrict__ b;
+  double* e;  // may be nullptr (true residual: only the norm is needed)
+  __device__ __forceinline__ double operator()(long long idx, double y, double) const {
+    const double ei = b[idx] - y;
+    if (e) e[idx] = ei;
+    return ei * ei;
+  }
+};
+
+// Chebyshev step 1 (polyprec.cpp:187-189), input vector = r:
+//   x = (2 rho_1 / delta) * (2 r - (A r) / theta)
+// x_old = r / theta is NOT stored: step 2 recomputes it from r (same bits).
+// Contribution r_i x_i (used when m == 1, i.e. x is already z = P r).
+struct EpiChebFirst {
+  double* __restrict__ xout;
+  double theta, c1;
+  __device__ __forceinline__ double operator()(long long idx, double y, double xc) const {
+    const double xn = c1 * ((2.0 * xc) - (y / theta));
+    xout[idx] = xn;
+    return xc * xn;
+  }
+};
+
+// Chebyshev step k >= 2 (polyprec.cpp:190-195), input vector = x_k-1:
+//   z = (2/delta) (r - A x) ; x_new = rho_k ((2 sigma) x - rho_{k-1} x_old + z)
+// x_old is r/theta at k == 2 (xold_from_r), otherwise read from xold; x_new is
+// written to out (== xold for the in-place middle steps). Contribution r_i x_new_i.
+struct EpiChebStep {
+  const double* __restrict__ r;
+  const double* xold;
+  double* out;
+  double rk, rk1, c2, c3, theta;
+  int xold_from_r;
+  __device__ __forceinline__ double operator()(long long idx, double y, double xc) const {
+    const double ri = r[idx];
+    const double xo = xold_from_r ? (ri / theta) : xold[idx];
+    const double z = c2 * (ri - y);
+    const double xn = rk * (((c3 * xc) - (rk1 * xo)) + z);
+    out[idx] = xn;
+    return ri * xn;
+  }
+};
+
+// ----------------------------------------------------------------- 7-point stencil
+
+// One thread per (i, j) column, marching planes [kb, ke) with the k-1, k, k+1
+// values in registers and the k+2 plane prefetched one iteration ahead; the
+// in-plane neighbours (i +- 1, j +- 1) come through L1 (the block's own plane
+// tile). Missing (Dirichlet) neighbours are 0, whose term -(d*0) = -0 leaves the
+// running sum bit-identical to the reference's skipped term.
+template <class Epi, bool kRed>
+__global__ void __launch_bounds__(kStencilThreads)
+stencil7_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begin, int k_end,
+                int kz, Reduce red) {
+  const int i = blockIdx.x * kStencilBX + threadIdx.x;
+  const int j = blockIdx.y * kStencilBY + threadIdx.y;
+  const int kb = k_begin + blockIdx.z * kz;
+  const int ke = min(kb + kz, k_end);
+  double acc = 0.0;
+  if (i < g.nx && j < g.ny && kb < ke) {
+    const long long col = (long long)j * g.nx + i;
+    const long long nxy = g.nxy;
+    auto plane = [&](int k) -> double {
+      if (k < 0) return g.ghost_lo ? __ldg(g.ghost_lo + col) : 0.0;
+      if (k >= g.nzl) return g.ghost_hi ? __ldg(g.ghost_hi + col) : 0.0;
+      return __ldg(x + (long long)k * nxy + col);
+    };
+    const bool has_w = i > 0, has_e = i < g.nx - 1, has_s = j > 0, has_n = j < g.ny - 1;
+    const double d = g.d;
+    double xm = plane(kb - 1);
+    double xc = plane(kb);
+    double xp = plane(kb + 1);
+    for (int k = kb; k < ke; ++k) {
+      const double xpp = (k + 1 < ke) ? plane(k + 2) : 0.0;
+      const long long idx = (long long)k * nxy + col;
+      const double xw = has_w ? __ldg(x + idx - 1) : 0.0;
+      const double xe = has_e ? __ldg(x + idx + 1) : 0.0;
+      const double xs = has_s ? __ldg(x + idx - g.nx) : 0.0;
+      const double xn = has_n ? __ldg(x + idx + g.nx) : 0.0;
+      // ascending column order: k-1, j-1, i-1, centre, i+1, j+1, k+1 (linop.cpp:247-253)
+      double s = 0.0;
+      s = s + (-(d * xm));
+      s = s + (-(d * xs));
+      s = s + (-(d * xw));
+      s = s + (6.0 * (d * xc));
+      s = s + (-(d * xe));
+      s = s + (-(d * xn));
+      s = s + (-(d * xp));
+      const double y = s * d;
+      const double c = epi(idx, y, xc);
+      if (kRed) acc = acc + c;
+      xm = xc;
+      xc = xp;
+      xp = xpp;
+    }
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
+// ----------------------------------------------------------------- CSR
+
+// Persistent grid over blocks of kCsrRows consecutive rows. The block's nnz
+// range is contiguous; it is walked in chunks: every thread forms products
+// va[k] * (d[c] * x[c]) for a coalesced stride of k into shared memory, then
+// each row-thread sums ITS row's products sequentially in column order, which
+// is the reference's order (linop.cpp:183-185) -> bitwise-equal rows.
+template <class Epi, bool kRed>
+__global__ void __launch_bounds__(kCsrRows)
+csr_kernel(CsrGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
+  __shared__ double prod[kCsrChunk];
+  double acc = 0.0;
+  const int nrb = (g.n + kCsrRows - 1) / kCsrRows;
+  for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+    const int row0 = rb * kCsrRows;
+    const int row = row0 + threadIdx.x;
+    const int rend = min(row0 + kCsrRows, g.n);
+    const int nz0 = __ldg(g.row_ptr + row0), nz1 = __ldg(g.row_ptr + rend);
+    int mb = 0, me = 0;
+    if (row < g.n) {
+      mb = __ldg(g.row_ptr + row);
+      me = __ldg(g.row_ptr + row + 1);
+    }
+    double sum = 0.0;
+    for (int c0 = nz0; c0 < nz1; c0 += kCsrChunk) {
+      const int c1 = min(c0 + kCsrChunk, nz1);
+#pragma unroll 4
+      for (int k = c0 + threadIdx.x; k < c1; k += kCsrRows) {
+        const int c = __ldg(g.col_idx + k);
+        prod[k - c0] = __ldg(g.values + k) * (__ldg(g.dvec + c) * __ldg(x + c));
+      }
+      __syncthreads();
+      const int lo = max(mb, c0), hi = min(me, c1);
+      for (int k = lo; k < hi; ++k) sum = sum + prod[k - c0];
+      __syncthreads();
+    }
+    if (row < g.n) {
+      const double y = sum * __ldg(g.dvec + row);
+      const double c = epi(row, y, __ldg(x + row));
+      if (kRed) acc = acc + c;
+    }
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
+// ----------------------------------------------------------------- vector kernels
+// Grid-stride over a fixed grid (deterministic element -> thread map).
+
+// x += alpha p ; r -= alpha q ; contribution r_i^2, alpha = rz[prev] / pq[cur]
+// (pcg.cpp:80-83)
+__global__ void __launch_bounds__(kVecThreads)
+update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
+              const double* __restrict__ p, const double* __restrict__ q, const double* S,
+              int s_rho, int s_pq, Reduce red) {
+  const double alpha = S[s_rho] / S[s_pq];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] = x[i] + alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    acc = acc + ri * ri;
+  }
+  block_reduce_finish(acc, red);
+}
+
+// p = z + beta p, beta = rz[cur] / rz[prev]  (pcg.cpp:107)
+__global__ void __launch_bounds__(kVecThreads)
+pupdate_kernel(long long n, double* __restrict__ p, const double* __restrict__ z,
+               const double* S, int s_new, int s_old) {
+  const double beta = S[s_new] / S[s_old];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+
+// z = r / theta (m == 0, polyprec.cpp:179-181) or z = r (no preconditioner,
+// pcg.cpp:61,99) ; contribution r_i z_i  (pcg.cpp:64,101)
+__global__ void __launch_bounds__(kVecThreads)
+zr_kernel(long long n, double* __restrict__ z, const double* __restrict__ r, double theta,
+          int divide, Reduce red) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double ri = r[i];
+    const double zi = divide ? ri / theta : ri;
+    z[i] = zi;
+    acc = acc + ri * zi;
+  }
+  block_reduce_finish(acc, red);
+}
+
+// result = a . b
+__global__ void __launch_bounds__(kVecThreads)
+dot_kernel(long long n, const double* __restrict__ a, const double* __restrict__ b, Reduce red) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc = acc + a[i] * b[i];
+  block_reduce_finish(acc, red);
+}
+
+// Lanczos three-term update: w = (w - a v) - b v_prev, contribution w_i^2;
+// a = S[s_a] (the all-reduced v'Av), b = beta of the previous step (host value).
+__global__ void __launch_bounds__(kVecThreads)
+lanczos_w_kernel(long long n, double* __restrict__ w, const double* __restrict__ v,
+                 const double* __restrict__ vprev, const double* S, int s_a, double b,
+                 Reduce red) {
+  const double a = S[s_a];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double wi = (w[i] - a * v[i]) - b * vprev[i];
+    w[i] = wi;
+    acc = acc + wi * wi;
+  }
+  block_reduce_finish(acc, red);
+}
+
+// vprev = v ; v = w / s
+__global__ void __launch_bounds__(kVecThreads)
+lanczos_shift_kernel(long long n, double* __restrict__ v, double* __restrict__ vprev,
+                     const double* __restrict__ w, double s) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    vprev[i] = v[i];
+    v[i] = w[i] / s;
+  }
+}
+
+// v = v / s
+__global__ void __launch_bounds__(kVecThreads)
+scale_div_kernel(long long n, double* __restrict__ v, double s) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = v[i] / s;
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+fill_kernel(long long n, double* __restrict__ v, double val) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = val;
+}
+
+// random_uniform_vector elements [offset, offset+n): the i-th draw of splitmix64
+// seeded with `seed` uses state seed + (i+1) * golden-gamma (eigenest.cpp:13-30).
+__global__ void __launch_bounds__(kVecThreads)
+splitmix_kernel(long long n, unsigned long long seed, unsigned long long offset,
+                double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long z = seed + (offset + (unsigned long long)i + 1ull) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z = z ^ (z >> 31);
+    const double u = (double)(z >> 11) * 0x1.0p-53;
+    out[i] = 2.0 * u - 1.0;
+  }
+}
+
+// Writes a large scratch buffer (flushes L2 between timed iterations).
+__global__ void flush_kernel(long long n, double* __restrict__ buf) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    buf[i] = (double)i;
+}
+
+}  // namespace pcgx

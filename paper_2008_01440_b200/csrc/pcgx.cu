@@ -1,0 +1,1179 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host orchestration of the B200 Chebyshev-PCG path and the C ABI (include/pcgx.h).
+//
+// One context = one GPU, one compute stream (+ one comm stream for halo
+// overlap), device scalars S[] that the kernels read directly (alpha, beta never
+// round-trip through the host), a pinned mirror of S read once per PCG
+// iteration for the convergence test, and CUDA graphs for the per-iteration
+// kernel chain. Multi-GPU: z-slab operator, NCCL send/recv of one halo plane
+// per neighbour per SpMV overlapped with the interior planes, and two NCCL
+// all-reduces (8 B and 16 B) per PCG iteration.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "host_math.hpp"
+#include "kernels.cuh"
+#include "pcgx.h"
+
+using namespace pcgx;
+
+// ============================================================================ types
+
+struct pcgx_context_s {
+  int device = 0;
+  int rank = 0, nranks = 1;
+  int sms = 148;
+  cudaStream_t s = nullptr;   // compute
+  cudaStream_t cs = nullptr;  // halo exchange
+  ncclComm_t comm = nullptr;
+  double* S = nullptr;        // device scalars
+  double* hS = nullptr;       // pinned mirror
+  double* partials = nullptr;
+  unsigned* counter = nullptr;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_sync = nullptr, ev_fork = nullptr,
+              ev_join = nullptr;
+  std::vector<cudaEvent_t> evpool;
+  int64_t launches = 0;
+  std::string err;
+  // workspace (device), sized for the largest operator used
+  long long ws_n = 0;
+  double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *w0 = nullptr, *w1 = nullptr,
+         *t0 = nullptr, *t1 = nullptr;
+  double* flush = nullptr;
+  size_t flush_bytes = 0;
+  // solve-local bookkeeping
+  int64_t cur_launches = 0;
+  int64_t cur_allreduce = 0;
+  int64_t cur_halo_bytes = 0;
+};
+
+struct pcgx_operator_s {
+  pcgx_context ctx = nullptr;
+  int kind = 0;  // 0 stencil7, 1 csr
+  long long n_global = 0, n_local = 0, nnz = 0;
+  // stencil
+  long long nx = 0, ny = 0, nz = 0, z0 = 0, nzl = 0;
+  double d = 0.0;
+  double *ghost_lo = nullptr, *ghost_hi = nullptr;
+  int kz = 16;
+  // csr
+  int *rp = nullptr, *ci = nullptr;
+  double *va = nullptr, *dvec = nullptr;
+  std::atomic<uint64_t> matvecs{0};
+};
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+// NCCL is resolved at run time (only dist contexts need it) so that loading
+// libpcgx.so never drags a second libnccl.so.2 into a process that also uses
+// torch's bundled one: an already-loaded libnccl.so.2 wins, then
+// $PCGX_NCCL_LIB, then the system library.
+struct Nccl {
+  bool ok = false;
+  std::string why;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl t;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) {
+      const char* env = std::getenv("PCGX_NCCL_LIB");
+      if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      t.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return t;
+    }
+#define PCGX_SYM(f) t.f = reinterpret_cast<decltype(t.f)>(dlsym(h, "nccl" #f))
+    PCGX_SYM(GetErrorString);
+    PCGX_SYM(GetUniqueId);
+    PCGX_SYM(CommInitRank);
+    PCGX_SYM(CommDestroy);
+    PCGX_SYM(AllReduce);
+    PCGX_SYM(Send);
+    PCGX_SYM(Recv);
+    PCGX_SYM(GroupStart);
+    PCGX_SYM(GroupEnd);
+#undef PCGX_SYM
+    t.ok = t.GetErrorString && t.GetUniqueId && t.CommInitRank && t.CommDestroy && t.AllReduce &&
+           t.Send && t.Recv && t.GroupStart && t.GroupEnd;
+    if (!t.ok) t.why = "libnccl.so.2 lacks a required symbol";
+    return t;
+  }();
+  if (!n.ok) fail(PCGX_ERR_NCCL, n.why);
+  return n;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+#define PCGX_NCCL(call)                                                                   \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      fail(PCGX_ERR_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_));         \
+  } while (0)
+
+template <class F>
+pcgx_status guarded(pcgx_context ctx, F&& f) {
+  try {
+    f();
+    return PCGX_OK;
+  } catch (const Error& e) {
+    (ctx ? ctx->err : g_thread_err) = e.what();
+    g_thread_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    (ctx ? ctx->err : g_thread_err) = "host allocation failed";
+    return PCGX_ERR_CUDA;
+  } catch (const std::exception& e) {
+    (ctx ? ctx->err : g_thread_err) = e.what();
+    return PCGX_ERR_CUDA;
+  }
+}
+
+void set_device(pcgx_context c) { PCGX_CUDA(cudaSetDevice(c->device)); }
+
+Reduce make_red(pcgx_context c, int slot, bool accumulate = false) {
+  Reduce r;
+  r.partials = c->partials;
+  r.counter = c->counter;
+  r.result = c->S + slot;
+  r.accumulate = accumulate ? 1 : 0;
+  return r;
+}
+
+void count_launch(pcgx_context c) {
+  c->launches++;
+  c->cur_launches++;
+}
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(PCGX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+void ensure_workspace(pcgx_context c, long long n) {
+  if (c->ws_n >= n) return;
+  double** bufs[] = {&c->r, &c->z, &c->p, &c->q, &c->w0, &c->w1, &c->t0, &c->t1};
+  for (double** b : bufs) {
+    if (*b) cudaFree(*b);
+    *b = nullptr;
+  }
+  c->ws_n = 0;
+  for (double** b : bufs) PCGX_CUDA(cudaMalloc(b, sizeof(double) * (size_t)std::max(n, 1LL)));
+  c->ws_n = n;
+}
+
+int vec_grid(pcgx_context c, long long n) {
+  const long long want = (n + kVecThreads - 1) / kVecThreads;
+  return (int)std::max(1LL, std::min(want, (long long)c->sms * 8));
+}
+
+// ---------------------------------------------------------------- all-reduce
+
+void allreduce(pcgx_context c, int slot, int count) {
+  if (c->nranks == 1) return;
+  PCGX_NCCL(nccl().AllReduce(c->S + slot, c->S + slot, count, ncclDouble, ncclSum, c->comm, c->s));
+  c->cur_allreduce++;
+}
+
+// ---------------------------------------------------------------- operator launch
+
+StencilGeom geom_of(pcgx_operator op) {
+  StencilGeom g;
+  g.nx = (int)op->nx;
+  g.ny = (int)op->ny;
+  g.nzl = (int)op->nzl;
+  g.nxy = op->nx * op->ny;
+  g.d = op->d;
+  g.ghost_lo = op->ghost_lo;
+  g.ghost_hi = op->ghost_hi;
+  return g;
+}
+
+template <class Epi, bool kRed>
+void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, const double* x,
+                    const Epi& epi, int k_begin, int k_end, int slot, bool accumulate) {
+  if (k_end <= k_begin) return;
+  const int kz = std::max(1, std::min(op->kz, k_end - k_begin));
+  dim3 block(kStencilBX, kStencilBY, 1);
+  dim3 grid((unsigned)((g.nx + kStencilBX - 1) / kStencilBX),
+            (unsigned)((g.ny + kStencilBY - 1) / kStencilBY),
+            (unsigned)((k_end - k_begin + kz - 1) / kz));
+  Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
+  stencil7_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red);
+  check_launch();
+  count_launch(c);
+}
+
+// y-consuming launch of the scaled operator over the local rows, with the halo
+// exchange of x (multi-GPU) overlapped with the interior planes.
+template <class Epi, bool kRed>
+void op_launch(pcgx_context c, pcgx_operator op, const double* x, const Epi& epi, int slot) {
+  op->matvecs.fetch_add(1, std::memory_order_relaxed);
+  if (op->kind == 1) {
+    CsrGeom g{(int)op->n_local, op->rp, op->ci, op->va, op->dvec};
+    const int nrb = (int)((op->n_local + kCsrRows - 1) / kCsrRows);
+    const int grid = std::max(1, std::min(nrb, c->sms * env_int("PCGX_CSR_BPS", 12)));
+    Reduce red = kRed ? make_red(c, slot) : Reduce{};
+    csr_kernel<Epi, kRed><<<grid, kCsrRows, 0, c->s>>>(g, x, epi, red);
+    check_launch();
+    count_launch(c);
+    return;
+  }
+  StencilGeom g = geom_of(op);
+  const int nzl = (int)op->nzl;
+  const bool lo_nb = op->ghost_lo != nullptr, hi_nb = op->ghost_hi != nullptr;
+  if (!lo_nb && !hi_nb) {
+    stencil_launch<Epi, kRed>(c, op, g, x, epi, 0, nzl, slot, false);
+    return;
+  }
+  // halo: my first plane -> rank-1 (its ghost_hi), my last plane -> rank+1 (its ghost_lo)
+  const long long nxy = op->nx * op->ny;
+  PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+  PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+  PCGX_NCCL(nccl().GroupStart());
+  if (lo_nb) {
+    PCGX_NCCL(nccl().Send(x, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
+    PCGX_NCCL(nccl().Recv(op->ghost_lo, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
+    c->cur_halo_bytes += nxy * 8;
+  }
+  if (hi_nb) {
+    PCGX_NCCL(nccl().Send(x + (nzl - 1) * nxy, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
+    PCGX_NCCL(nccl().Recv(op->ghost_hi, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
+    c->cur_halo_bytes += nxy * 8;
+  }
+  PCGX_NCCL(nccl().GroupEnd());
+  PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+  // interior planes need no ghost: run them while the halo is in flight
+  const int ib = lo_nb ? 1 : 0, ie = hi_nb ? nzl - 1 : nzl;
+  StencilGeom gi = g;
+  gi.ghost_lo = nullptr;
+  gi.ghost_hi = nullptr;
+  bool wrote = false;
+  if (ie > ib) {
+    stencil_launch<Epi, kRed>(c, op, gi, x, epi, ib, ie, slot, false);
+    wrote = true;
+  }
+  PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0));
+  if (lo_nb) {
+    stencil_launch<Epi, kRed>(c, op, g, x, epi, 0, 1, slot, wrote);
+    wrote = true;
+  }
+  if (hi_nb && (nzl - 1 >= (lo_nb ? 1 : 0))) {
+    stencil_launch<Epi, kRed>(c, op, g, x, epi, nzl - 1, nzl, slot, wrote);
+  }
+}
+
+// ---------------------------------------------------------------- vector launches
+
+void launch_update(pcgx_context c, long long n, double* x, double* r, const double* p,
+                   const double* q, int s_rho, int s_pq, int s_rr) {
+  update_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, r, p, q, c->S, s_rho, s_pq,
+                                                          make_red(c, s_rr));
+  check_launch();
+  count_launch(c);
+}
+
+void launch_pupdate(pcgx_context c, long long n, double* p, const double* z, int s_new,
+                    int s_old) {
+  pupdate_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, p, z, c->S, s_new, s_old);
+  check_launch();
+  count_launch(c);
+}
+
+void launch_zr(pcgx_context c, long long n, double* z, const double* r, double theta, int divide,
+               int slot) {
+  zr_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, z, r, theta, divide, make_red(c, slot));
+  check_launch();
+  count_launch(c);
+}
+
+void launch_dot(pcgx_context c, long long n, const double* a, const double* b, int slot) {
+  dot_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, a, b, make_red(c, slot));
+  check_launch();
+  count_launch(c);
+}
+
+void launch_fill(pcgx_context c, long long n, double* v, double val) {
+  fill_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, v, val);
+  check_launch();
+  count_launch(c);
+}
+
+void copy_d2d(pcgx_context c, double* dst, const double* src, long long n) {
+  if (dst != src)
+    PCGX_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, c->s));
+}
+
+// S (device) -> hS (pinned) and wait.
+void fetch_scalars(pcgx_context c) {
+  PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
+  PCGX_CUDA(cudaStreamSynchronize(c->s));
+}
+
+// ---------------------------------------------------------------- Chebyshev apply
+
+struct Cheb {
+  int m = 0;
+  double theta = 0, delta = 0, sigma = 0;
+  std::vector<double> rho;
+};
+
+Cheb cheb_from(const pcgx_cheb* p) {
+  Cheb c;
+  c.m = p->m;
+  c.theta = p->theta;
+  c.delta = p->delta;
+  c.sigma = p->sigma;
+  if (p->m < 0) fail(PCGX_ERR_INVALID, "cheb_apply: m must be >= 0");
+  if (p->m > 0 && !p->rho) fail(PCGX_ERR_INVALID, "cheb_apply: rho must have m+1 entries");
+  if (p->rho) c.rho.assign(p->rho, p->rho + p->m + 1);
+  return c;
+}
+
+// out = p_m(A) r (polyprec.cpp:169-198); rz_slot >= 0 also reduces r . out there.
+// Uses c->w0, c->w1 as the recurrence workspace. out must not alias r, w0, w1.
+void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double* r, double* out,
+                  int rz_slot) {
+  const long long n = op->n_local;
+  if (P.m == 0) {  // out = r / theta
+    launch_zr(c, n, out, r, P.theta, 1, rz_slot >= 0 ? rz_slot : S_DOT2);
+    return;
+  }
+  const double c1 = 2.0 * P.rho[1] / P.delta;
+  const double c2 = 2.0 / P.delta;
+  const double c3 = 2.0 * P.sigma;
+  if (P.m == 1) {
+    EpiChebFirst e{out, P.theta, c1};
+    if (rz_slot >= 0) op_launch<EpiChebFirst, true>(c, op, r, e, rz_slot);
+    else op_launch<EpiChebFirst, false>(c, op, r, e, -1);
+    return;
+  }
+  EpiChebFirst e1{c->w1, P.theta, c1};
+  op_launch<EpiChebFirst, false>(c, op, r, e1, -1);
+  double* cur = c->w1;  // x_{k-1}
+  double* old = c->w0;  // x_{k-2} (not yet materialised at k == 2)
+  for (int k = 2; k <= P.m; ++k) {
+    const bool last = (k == P.m);
+    double* dst = last ? out : old;
+    EpiChebStep e{r, old, dst, P.rho[k], P.rho[k - 1], c2, c3, P.theta, k == 2 ? 1 : 0};
+    if (last && rz_slot >= 0) op_launch<EpiChebStep, true>(c, op, cur, e, rz_slot);
+    else op_launch<EpiChebStep, false>(c, op, cur, e, -1);
+    old = cur;
+    cur = dst;
+  }
+}
+
+// ---------------------------------------------------------------- PCG
+
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
+  ~Graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+template <class F>
+void capture(pcgx_context c, Graph& g, F&& body) {
+  const int64_t before = c->cur_launches;
+  PCGX_CUDA(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaGraph_t tmp;
+    cudaStreamEndCapture(c->s, &tmp);
+    if (tmp) cudaGraphDestroy(tmp);
+    throw;
+  }
+  cudaGraph_t graph;
+  PCGX_CUDA(cudaStreamEndCapture(c->s, &graph));
+  PCGX_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+  cudaGraphDestroy(graph);
+  g.kernels = c->cur_launches - before;
+  c->cur_launches = before;  // counted per replay instead
+  c->launches -= g.kernels;
+}
+
+void replay(pcgx_context c, Graph& g) {
+  PCGX_CUDA(cudaGraphLaunch(g.exec, c->s));
+  c->cur_launches += g.kernels;
+  c->launches += g.kernels;
+}
+
+std::string fmt_double(double v) { return std::to_string(v); }
+
+// Algorithmic bytes per unknown for one matvec-equivalent pass:
+// stencil 16 B/unknown (read x, write y); CSR 12 nnz + 4 (n+1) + 16 n.
+double spmv_equiv_bytes(pcgx_operator op) {
+  if (op->kind == 0) return 16.0 * (double)op->n_local;
+  return 12.0 * (double)op->nnz + 4.0 * (double)(op->n_local + 1) + 16.0 * (double)op->n_local;
+}
+// Fused Chebyshev middle step: stencil 32 B/unknown; CSR 12 nnz + 4(n+1) + 32 n
+// (+ 8 n for the inv_sqrt_diag vector read with the row).
+double cheb_step_bytes(pcgx_operator op) {
+  if (op->kind == 0) return 32.0 * (double)op->n_local;
+  return 12.0 * (double)op->nnz + 4.0 * (double)(op->n_local + 1) + 40.0 * (double)op->n_local;
+}
+
+void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in,
+                      const double* b, double* x, const pcgx_solve_opts* o, pcgx_report* rep) {
+  if (op->ctx != c) fail(PCGX_ERR_INVALID, "pcg_solve: operator belongs to another context");
+  pcgx_solve_opts opts;
+  pcgx_solve_opts_default(&opts);
+  if (o) opts = *o;
+  if (!(opts.tol > 0.0)) fail(PCGX_ERR_INVALID, "pcg_solve: tol must be positive");
+  if (opts.maxit < 1) fail(PCGX_ERR_INVALID, "pcg_solve: maxit must be >= 1");
+  const bool have_prec = prec_in != nullptr;
+  Cheb P;
+  if (have_prec) P = cheb_from(prec_in);
+  const int m = have_prec ? P.m : 0;
+  const long long n = op->n_local;
+  ensure_workspace(c, n);
+  const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && env_int("PCGX_NO_GRAPH", 0) == 0;
+  const bool spec_after_update = (c->nranks == 1);
+
+  std::memset(rep, 0, sizeof *rep);
+  c->cur_launches = 0;
+  c->cur_allreduce = 0;
+  c->cur_halo_bytes = 0;
+  double* r = c->r;
+  double* z = c->z;
+  double* p = c->p;
+  double* q = c->q;
+
+  PCGX_CUDA(cudaEventRecord(c->ev_t0, c->s));
+  auto finish = [&]() {
+    PCGX_CUDA(cudaEventRecord(c->ev_t1, c->s));
+    PCGX_CUDA(cudaEventSynchronize(c->ev_t1));
+    float ms = 0.f;
+    PCGX_CUDA(cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1));
+    rep->wall_time = ms * 1e-3;
+    rep->kernel_launches = c->cur_launches;
+    rep->allreduces = c->cur_allreduce;
+    rep->halo_bytes = c->cur_halo_bytes;
+    rep->spmv_equiv_bytes = (double)rep->matvec * spmv_equiv_bytes(op);
+  };
+  double alg = 0.0;  // algorithmic bytes, accumulated per enqueued pass
+  const double N8 = 8.0 * (double)n;
+  auto cheb_bytes = [&]() -> double {  // one preconditioner application incl. r.z
+    if (!have_prec) return 2 * N8;
+    if (m == 0) return 2 * N8;
+    const double spmv_extra = spmv_equiv_bytes(op) - 2 * N8;  // matrix bytes (CSR)
+    if (m == 1) return spmv_extra + 2 * N8;
+    return (spmv_extra + 2 * N8) + (spmv_extra + 3 * N8) + (double)(m - 2) * (spmv_extra + 4 * N8);
+  };
+
+  // ||b|| (pcg.cpp:32)
+  launch_dot(c, n, b, b, S_BB);
+  allreduce(c, S_BB, 1);
+  fetch_scalars(c);
+  alg += N8;
+  const double bnorm = std::sqrt(c->hS[S_BB]);
+  rep->ddot++;
+  if (bnorm == 0.0) {
+    launch_fill(c, n, x, 0.0);
+    rep->converged = 1;
+    finish();
+    rep->alg_bytes = alg;
+    return;
+  }
+  if (opts.x0) {
+    copy_d2d(c, x, opts.x0, n);
+    op_launch<EpiResid, true>(c, op, x, EpiResid{b, r}, S_RR0);  // r = b - A x0
+    allreduce(c, S_RR0, 1);
+    fetch_scalars(c);
+    alg += spmv_equiv_bytes(op) + 2 * N8;
+    rep->matvec++;
+    const double rnorm = std::sqrt(c->hS[S_RR0]);
+    rep->ddot++;
+    rep->rel_res = rnorm / bnorm;
+    if (rep->rel_res <= opts.tol) {
+      rep->converged = 1;
+      rep->true_rel_res = rep->rel_res;
+      finish();
+      rep->alg_bytes = alg;
+      return;
+    }
+  } else {
+    copy_d2d(c, r, b, n);
+    launch_fill(c, n, x, 0.0);
+    alg += 3 * N8;
+    rep->rel_res = 1.0;
+  }
+
+  // setup preconditioning: z_0 goes straight into p (p = z, pcg.cpp:63), r'z -> rz(0)
+  auto enqueue_prec = [&](double* out, int slot) {
+    if (have_prec) enqueue_cheb(c, op, P, r, out, slot);
+    else launch_zr(c, n, out, r, 1.0, 0, slot);
+  };
+  enqueue_prec(p, slot_rz(0));
+  allreduce(c, slot_rz(0), 1);
+  alg += cheb_bytes();
+  if (have_prec) {
+    rep->prec_applies++;
+    rep->matvec += m;
+  }
+  rep->ddot++;
+  fetch_scalars(c);
+  {
+    const double rho = c->hS[slot_rz(0)];
+    if (!std::isfinite(rho) || rho <= 0.0)
+      fail(PCGX_ERR_NUMERICAL,
+           "pcg_solve: r'z = " + fmt_double(rho) + " at setup (preconditioner not SPD?)");
+  }
+
+  // per-iteration pieces
+  auto enqueue_spmv_dot = [&](int par) {
+    op_launch<EpiStore, true>(c, op, p, EpiStore{q}, slot_pq(par));
+    allreduce(c, slot_pq(par), 1);
+  };
+  // B(it): prec(it) [+ rr,rz all-reduce + host snapshot on multi-GPU] ; p update ; spmv_dot(it+1)
+  auto enqueue_B = [&](int par, bool with_snapshot) {
+    enqueue_prec(z, slot_rz(par));
+    if (!spec_after_update) {
+      allreduce(c, slot_rr(par), 2);
+      if (with_snapshot) {
+        PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
+        PCGX_CUDA(cudaEventRecord(c->ev_sync, c->s));
+      }
+    }
+    launch_pupdate(c, n, p, z, slot_rz(par), slot_rz(par ^ 1));
+    enqueue_spmv_dot(par ^ 1);
+  };
+  Graph gB[2];
+  const double bytes_B = cheb_bytes() + 3 * N8 + spmv_equiv_bytes(op);
+  const double bytes_update = 6 * N8;
+
+  enqueue_spmv_dot(1);
+  alg += spmv_equiv_bytes(op);
+  for (int it = 1; it <= opts.maxit; ++it) {
+    const int par = it & 1;
+    launch_update(c, n, x, r, p, q, slot_rz(par ^ 1), slot_pq(par), slot_rr(par));
+    alg += bytes_update;
+    rep->matvec++;  // q = A p of this iteration
+    const bool more = it < opts.maxit;
+    if (spec_after_update || !more) {
+      if (!spec_after_update) allreduce(c, slot_rr(par), 1);
+      PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
+      PCGX_CUDA(cudaEventRecord(c->ev_sync, c->s));
+    }
+    if (more) {
+      if (use_graph) {
+        if (!gB[par].exec) capture(c, gB[par], [&] { enqueue_B(par, true); });
+        replay(c, gB[par]);
+      } else {
+        enqueue_B(par, true);
+      }
+      alg += bytes_B;
+    }
+    PCGX_CUDA(cudaEventSynchronize(c->ev_sync));
+    const double* hs = c->hS;
+    // checks in the reference's order: r'z(it-1) [pcg.cpp:103-106], p'Ap [:76-79], ||r|| [:85]
+    if (it >= 2) {
+      const double rho_prev = hs[slot_rz(par ^ 1)];
+      if (!std::isfinite(rho_prev) || rho_prev <= 0.0)
+        fail(PCGX_ERR_NUMERICAL,
+             "pcg_solve: r'z = " + fmt_double(rho_prev) + " (preconditioner not SPD?)");
+    }
+    const double pq = hs[slot_pq(par)];
+    rep->ddot++;
+    if (!std::isfinite(pq) || pq <= 0.0)
+      fail(PCGX_ERR_NUMERICAL, "pcg_solve: p'Ap = " + fmt_double(pq) + " (operator not SPD?)");
+    const double rnorm = std::sqrt(hs[slot_rr(par)]);
+    rep->ddot++;
+    if (!std::isfinite(rnorm)) fail(PCGX_ERR_NUMERICAL, "pcg_solve: residual norm is not finite");
+    rep->iters = it;
+    rep->rel_res = rnorm / bnorm;
+    if (rep->rel_res <= opts.tol) {
+      rep->converged = 1;
+      if (more) rep->wasted_matvec = m + 1;  // speculative P r and A p
+      break;
+    }
+    if (!more) break;
+    if (have_prec) {
+      rep->prec_applies++;
+      rep->matvec += m;
+    }
+    rep->ddot++;  // r'z
+    if (!spec_after_update) {
+      const double rz = hs[slot_rz(par)];
+      if (!std::isfinite(rz) || rz <= 0.0)
+        fail(PCGX_ERR_NUMERICAL, "pcg_solve: r'z = " + fmt_double(rz) + " (preconditioner not SPD?)");
+    }
+  }
+  // true residual (pcg.cpp:112-115)
+  op_launch<EpiResid, true>(c, op, x, EpiResid{b, nullptr}, S_EE);
+  allreduce(c, S_EE, 1);
+  fetch_scalars(c);
+  alg += spmv_equiv_bytes(op) + N8;
+  rep->matvec++;
+  rep->true_rel_res = std::sqrt(c->hS[S_EE]) / bnorm;
+  rep->ddot++;
+  finish();
+  rep->alg_bytes = alg;
+  rep->step_bytes = cheb_step_bytes(op);
+
+  // Optional: time the dominant kernel (the fused middle Chebyshev step) with
+  // CUDA events on the compute stream, on this solve's operator and buffers.
+  if ((opts.flags & PCGX_FLAG_TIME_KERNELS) && have_prec && m >= 3) {
+    const int reps = std::max(3, env_int("PCGX_STEP_REPS", 20));
+    EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0};
+    op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);  // warm
+    op->matvecs.fetch_sub(1);
+    PCGX_CUDA(cudaEventRecord(c->ev_t0, c->s));
+    for (int i = 0; i < reps; ++i) {
+      op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);
+      op->matvecs.fetch_sub(1);
+    }
+    PCGX_CUDA(cudaEventRecord(c->ev_t1, c->s));
+    PCGX_CUDA(cudaEventSynchronize(c->ev_t1));
+    float ms = 0.f;
+    PCGX_CUDA(cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1));
+    rep->step_ms = ms;
+    rep->step_launches = reps;
+  }
+}
+
+// ---------------------------------------------------------------- Lanczos
+
+void lanczos_device(pcgx_context c, pcgx_operator op, int steps_hi, int steps, uint64_t seed,
+                    double* lo, double* hi) {
+  if (steps < 1 || steps_hi < 1 || steps_hi > steps)
+    fail(PCGX_ERR_INVALID, "lanczos: need 1 <= steps_hi <= steps");
+  const long long n = op->n_local;
+  ensure_workspace(c, n);
+  double* v = c->t0;
+  double* vprev = c->t1;
+  double* w = c->w0;
+  const unsigned long long offset = (unsigned long long)(op->kind == 0 ? op->z0 * op->nx * op->ny : 0);
+  splitmix_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, seed, offset, v);
+  check_launch();
+  count_launch(c);
+  launch_dot(c, n, v, v, S_DOT);
+  allreduce(c, S_DOT, 1);
+  fetch_scalars(c);
+  const double nv = std::sqrt(c->hS[S_DOT]);
+  if (nv == 0.0) fail(PCGX_ERR_NUMERICAL, "lanczos: zero starting vector");
+  scale_div_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, v, nv);
+  check_launch();
+  launch_fill(c, n, vprev, 0.0);
+  std::vector<double> a, bb;
+  double bprev = 0.0;
+  for (int j = 0; j < steps; ++j) {
+    op_launch<EpiStore, true>(c, op, v, EpiStore{w}, S_DOT);  // w = A v, a = v'w
+    allreduce(c, S_DOT, 1);
+    lanczos_w_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, w, v, vprev, c->S, S_DOT, bprev,
+                                                              make_red(c, S_DOT2));
+    check_launch();
+    count_launch(c);
+    allreduce(c, S_DOT2, 1);
+    fetch_scalars(c);
+    const double aj = c->hS[S_DOT];
+    const double bj = std::sqrt(c->hS[S_DOT2]);
+    a.push_back(aj);
+    bb.push_back(bj);
+    if (bj == 0.0) break;
+    lanczos_shift_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, v, vprev, w, bj);
+    check_launch();
+    count_launch(c);
+    bprev = bj;
+  }
+  double l1, h1, l2, h2;
+  const int k = (int)a.size();
+  tridiag_extremes(std::min(k, steps_hi), a.data(), bb.data(), &l1, &h1);
+  tridiag_extremes(k, a.data(), bb.data(), &l2, &h2);
+  *hi = h1;
+  *lo = l2;
+}
+
+// ---------------------------------------------------------------- operator creation
+
+void init_stencil_ghosts(pcgx_context c, pcgx_operator op) {
+  const size_t pb = sizeof(double) * (size_t)(op->nx * op->ny);
+  if (c->nranks > 1) {
+    if (c->rank > 0) PCGX_CUDA(cudaMalloc(&op->ghost_lo, pb));
+    if (c->rank < c->nranks - 1) PCGX_CUDA(cudaMalloc(&op->ghost_hi, pb));
+  }
+}
+
+int default_kz(pcgx_context c, long long nx, long long ny, long long nzl) {
+  const int env = env_int("PCGX_KZ", 0);
+  if (env > 0) return env;
+  (void)c;
+  (void)nx;
+  (void)ny;
+  (void)nzl;
+  return 16;
+}
+
+template <class IdxT>
+void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, const IdxT* ci,
+                const double* va, const double* inv_sqrt) {
+  if (n < 0) fail(PCGX_ERR_INVALID, "LinearOperator: negative dimension");
+  if (!rp || (n > 0 && (!ci || !va)) ) fail(PCGX_ERR_INVALID, "CsrMatrix: null array");
+  if (rp[0] != 0) fail(PCGX_ERR_INVALID, "CsrMatrix: row_ptr must have length n+1 and start at 0");
+  const long long nnz = (long long)rp[n];
+  if (nnz >= (1LL << 31) || n >= (1LL << 31))
+    fail(PCGX_ERR_OVERFLOW, "csr_create: nnz " + std::to_string(nnz) +
+                                " does not fit the int32 device CSR");
+  std::vector<int> rp32((size_t)n + 1);
+  std::vector<int> ci32((size_t)nnz);
+  std::vector<double> dv((size_t)n);
+  for (long long i = 0; i < n; ++i) {
+    if (rp[i + 1] < rp[i]) fail(PCGX_ERR_INVALID, "CsrMatrix: row_ptr not nondecreasing");
+    double diag = 0.0;
+    for (long long k = rp[i]; k < rp[i + 1]; ++k) {
+      const long long col = (long long)ci[k];
+      if (col < 0 || col >= n)
+        fail(PCGX_ERR_INVALID, "CsrMatrix: column index out of range in row " + std::to_string(i));
+      if (k > rp[i] && col <= (long long)ci[k - 1])
+        fail(PCGX_ERR_INVALID, "CsrMatrix: columns not strictly increasing in row " + std::to_string(i));
+      if (col == i) diag = va[k];
+      ci32[(size_t)k] = (int)col;
+    }
+    rp32[(size_t)i + 1] = (int)rp[i + 1];
+    if (inv_sqrt) {
+      dv[(size_t)i] = inv_sqrt[i];
+    } else {  // jacobi_scale (linop.cpp:340-351)
+      if (!(diag > 0.0))
+        fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry at index " +
+                                     std::to_string(i) + " (" + std::to_string(diag) + ")");
+      dv[(size_t)i] = 1.0 / std::sqrt(diag);
+    }
+  }
+  op->kind = 1;
+  op->n_global = op->n_local = n;
+  op->nnz = nnz;
+  PCGX_CUDA(cudaMalloc(&op->rp, sizeof(int) * (size_t)(n + 1)));
+  PCGX_CUDA(cudaMalloc(&op->ci, sizeof(int) * (size_t)std::max(nnz, 1LL)));
+  PCGX_CUDA(cudaMalloc(&op->va, sizeof(double) * (size_t)std::max(nnz, 1LL)));
+  PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * (size_t)std::max(n, 1LL)));
+  PCGX_CUDA(cudaMemcpy(op->rp, rp32.data(), sizeof(int) * (size_t)(n + 1), cudaMemcpyHostToDevice));
+  if (nnz) {
+    PCGX_CUDA(cudaMemcpy(op->ci, ci32.data(), sizeof(int) * (size_t)nnz, cudaMemcpyHostToDevice));
+    PCGX_CUDA(cudaMemcpy(op->va, va, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice));
+  }
+  if (n) PCGX_CUDA(cudaMemcpy(op->dvec, dv.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice));
+}
+
+void free_op(pcgx_operator op) {
+  if (!op) return;
+  cudaFree(op->ghost_lo);
+  cudaFree(op->ghost_hi);
+  cudaFree(op->rp);
+  cudaFree(op->ci);
+  cudaFree(op->va);
+  cudaFree(op->dvec);
+  delete op;
+}
+
+void ctx_init(pcgx_context c) {
+  PCGX_CUDA(cudaSetDevice(c->device));
+  PCGX_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
+  PCGX_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+  PCGX_CUDA(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+  PCGX_CUDA(cudaMalloc(&c->S, sizeof(double) * kSlots));
+  PCGX_CUDA(cudaMemset(c->S, 0, sizeof(double) * kSlots));
+  PCGX_CUDA(cudaMallocHost(&c->hS, sizeof(double) * kSlots));
+  PCGX_CUDA(cudaMalloc(&c->partials, sizeof(double) * kMaxBlocks));
+  PCGX_CUDA(cudaMalloc(&c->counter, sizeof(unsigned) * 4));
+  PCGX_CUDA(cudaMemset(c->counter, 0, sizeof(unsigned) * 4));
+  PCGX_CUDA(cudaEventCreate(&c->ev_t0));
+  PCGX_CUDA(cudaEventCreate(&c->ev_t1));
+  PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming));
+  PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+int pcgx_abi_version(void) { return PCGX_ABI_VERSION; }
+
+const char* pcgx_last_error(pcgx_context ctx) {
+  return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+pcgx_status pcgx_context_create(int device, pcgx_context* out) {
+  return guarded(nullptr, [&] {
+    if (!out) fail(PCGX_ERR_INVALID, "context_create: null out");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+      fail(PCGX_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) fail(PCGX_ERR_INVALID, "context_create: bad device index");
+    auto c = std::make_unique<pcgx_context_s>();
+    c->device = device;
+    ctx_init(c.get());
+    *out = c.release();
+  });
+}
+
+pcgx_status pcgx_nccl_unique_id(void* id128) {
+  return guarded(nullptr, [&] {
+    ncclUniqueId id;
+    PCGX_NCCL(nccl().GetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof id);
+  });
+}
+
+pcgx_status pcgx_context_create_dist(int device, int nranks, int rank, const void* nccl_id,
+                                     pcgx_context* out) {
+  return guarded(nullptr, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+      fail(PCGX_ERR_INVALID, "context_create_dist: bad rank/nranks");
+    auto c = std::make_unique<pcgx_context_s>();
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    ctx_init(c.get());
+    if (nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof id);
+      PCGX_NCCL(nccl().CommInitRank(&c->comm, nranks, id, rank));
+    }
+    *out = c.release();
+  });
+}
+
+void pcgx_context_destroy(pcgx_context c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->s);
+  if (c->comm) nccl().CommDestroy(c->comm);
+  double* bufs[] = {c->r, c->z, c->p, c->q, c->w0, c->w1, c->t0, c->t1, c->flush, c->S, c->partials};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  cudaFree(c->counter);
+  cudaFreeHost(c->hS);
+  cudaEvent_t evs[] = {c->ev_t0, c->ev_t1, c->ev_sync, c->ev_fork, c->ev_join};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  cudaStreamDestroy(c->s);
+  cudaStreamDestroy(c->cs);
+  delete c;
+}
+
+int pcgx_context_rank(pcgx_context c) { return c ? c->rank : -1; }
+int pcgx_context_nranks(pcgx_context c) { return c ? c->nranks : -1; }
+int64_t pcgx_kernel_launches(pcgx_context c) { return c ? c->launches : 0; }
+
+pcgx_status pcgx_synchronize(pcgx_context c) {
+  return guarded(c, [&] {
+    set_device(c);
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
+pcgx_status pcgx_device_alloc(pcgx_context c, size_t bytes, void** dptr) {
+  return guarded(c, [&] {
+    set_device(c);
+    PCGX_CUDA(cudaMalloc(dptr, std::max<size_t>(bytes, 8)));
+  });
+}
+pcgx_status pcgx_device_free(pcgx_context c, void* dptr) {
+  return guarded(c, [&] {
+    set_device(c);
+    PCGX_CUDA(cudaFree(dptr));
+  });
+}
+pcgx_status pcgx_memcpy_h2d(pcgx_context c, void* dst, const void* src, size_t bytes) {
+  return guarded(c, [&] {
+    set_device(c);
+    PCGX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->s));
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+pcgx_status pcgx_memcpy_d2h(pcgx_context c, void* dst, const void* src, size_t bytes) {
+  return guarded(c, [&] {
+    set_device(c);
+    PCGX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->s));
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+pcgx_status pcgx_memcpy_d2d(pcgx_context c, void* dst, const void* src, size_t bytes) {
+  return guarded(c, [&] {
+    set_device(c);
+    PCGX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->s));
+  });
+}
+pcgx_status pcgx_host_alloc(size_t bytes, void** hptr) {
+  return guarded(nullptr, [&] { PCGX_CUDA(cudaMallocHost(hptr, std::max<size_t>(bytes, 8))); });
+}
+pcgx_status pcgx_host_free(void* hptr) {
+  return guarded(nullptr, [&] { PCGX_CUDA(cudaFreeHost(hptr)); });
+}
+
+pcgx_status pcgx_timer_start(pcgx_context c) {
+  return guarded(c, [&] { PCGX_CUDA(cudaEventRecord(c->ev_t0, c->s)); });
+}
+pcgx_status pcgx_timer_stop(pcgx_context c, double* ms) {
+  return guarded(c, [&] {
+    PCGX_CUDA(cudaEventRecord(c->ev_t1, c->s));
+    PCGX_CUDA(cudaEventSynchronize(c->ev_t1));
+    float f = 0.f;
+    PCGX_CUDA(cudaEventElapsedTime(&f, c->ev_t0, c->ev_t1));
+    *ms = f;
+  });
+}
+pcgx_status pcgx_flush_l2(pcgx_context c, size_t bytes) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (c->flush_bytes < bytes) {
+      if (c->flush) cudaFree(c->flush);
+      c->flush = nullptr;
+      PCGX_CUDA(cudaMalloc(&c->flush, bytes));
+      c->flush_bytes = bytes;
+    }
+    const long long n = (long long)(bytes / 8);
+    flush_kernel<<<c->sms * 4, 256, 0, c->s>>>(n, c->flush);
+    check_launch();
+    count_launch(c);
+  });
+}
+
+pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t nz,
+                                 double inv_sqrt_diag, pcgx_operator* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (nx < 1 || ny < 1 || nz < 1) fail(PCGX_ERR_INVALID, "StencilOperator: nx must be >= 1");
+    if (nx > (1 << 30) || ny > (1 << 30) || nx * ny > (1LL << 31))
+      fail(PCGX_ERR_UNSUPPORTED, "stencil7_create: plane nx*ny too large");
+    if (nz < c->nranks) fail(PCGX_ERR_INVALID, "stencil7_create: fewer planes than ranks");
+    auto op = new pcgx_operator_s();
+    op->ctx = c;
+    op->kind = 0;
+    op->nx = nx;
+    op->ny = ny;
+    op->nz = nz;
+    // balanced z-slabs: the first (nz % P) ranks own one extra plane
+    const long long base = nz / c->nranks, extra = nz % c->nranks;
+    op->nzl = base + (c->rank < extra ? 1 : 0);
+    op->z0 = c->rank * base + std::min<long long>(c->rank, extra);
+    op->n_global = nx * ny * nz;
+    op->n_local = nx * ny * op->nzl;
+    op->nnz = 7 * op->n_global - 2 * (ny * nz + nx * nz + nx * ny);
+    op->d = inv_sqrt_diag > 0.0 ? inv_sqrt_diag : 1.0 / std::sqrt(6.0);
+    op->kz = default_kz(c, nx, ny, op->nzl);
+    try {
+      init_stencil_ghosts(c, op);
+    } catch (...) {
+      free_op(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+pcgx_status pcgx_csr_create(pcgx_context c, int64_t n, const int64_t* row_ptr,
+                            const int64_t* col_idx, const double* values,
+                            const double* inv_sqrt_diag, pcgx_operator* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (c->nranks > 1) fail(PCGX_ERR_UNSUPPORTED, "csr_create: multi-GPU CSR is not built yet");
+    auto op = new pcgx_operator_s();
+    op->ctx = c;
+    try {
+      csr_upload(c, op, n, row_ptr, col_idx, values, inv_sqrt_diag);
+    } catch (...) {
+      free_op(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+pcgx_status pcgx_csr_create_i32(pcgx_context c, int64_t n, const int32_t* row_ptr,
+                                const int32_t* col_idx, const double* values,
+                                const double* inv_sqrt_diag, pcgx_operator* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (c->nranks > 1) fail(PCGX_ERR_UNSUPPORTED, "csr_create: multi-GPU CSR is not built yet");
+    auto op = new pcgx_operator_s();
+    op->ctx = c;
+    try {
+      csr_upload(c, op, n, row_ptr, col_idx, values, inv_sqrt_diag);
+    } catch (...) {
+      free_op(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+void pcgx_operator_destroy(pcgx_operator op) {
+  if (!op) return;
+  cudaSetDevice(op->ctx->device);
+  cudaStreamSynchronize(op->ctx->s);
+  free_op(op);
+}
+
+int64_t pcgx_operator_size(pcgx_operator op) { return op ? op->n_global : -1; }
+int64_t pcgx_operator_local_size(pcgx_operator op) { return op ? op->n_local : -1; }
+int64_t pcgx_operator_z0(pcgx_operator op) { return op ? op->z0 : -1; }
+int64_t pcgx_operator_nnz(pcgx_operator op) { return op ? op->nnz : -1; }
+uint64_t pcgx_operator_matvec_count(pcgx_operator op) { return op ? op->matvecs.load() : 0; }
+
+pcgx_status pcgx_operator_apply_device(pcgx_context c, pcgx_operator op, const double* x,
+                                       double* y) {
+  return guarded(c, [&] {
+    set_device(c);
+    op_launch<EpiStore, false>(c, op, x, EpiStore{y}, -1);
+  });
+}
+
+pcgx_status pcgx_operator_apply(pcgx_context c, pcgx_operator op, const double* x, double* y) {
+  return guarded(c, [&] {
+    set_device(c);
+    const long long n = op->n_local;
+    ensure_workspace(c, n);
+    PCGX_CUDA(cudaMemcpyAsync(c->t0, x, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
+    op_launch<EpiStore, false>(c, op, c->t0, EpiStore{c->t1}, -1);
+    PCGX_CUDA(cudaMemcpyAsync(y, c->t1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
+pcgx_status pcgx_cheb_params(double alpha, double beta, int m, double scale, double* tds,
+                             double* rho) {
+  std::string msg;
+  const int st = pcgx::cheb_params(alpha, beta, m, scale, tds, rho, &msg);
+  if (st) g_thread_err = msg;
+  return (pcgx_status)st;
+}
+
+double pcgx_cheb_eval(const pcgx_cheb* p, double lambda) {
+  return cheb_eval(p->theta, p->delta, p->sigma, p->rho, p->m, lambda);
+}
+
+pcgx_status pcgx_cheb_apply_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* p,
+                                   const double* r, double* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (r == out) fail(PCGX_ERR_INVALID, "apply_chebyshev: out must not alias r");
+    ensure_workspace(c, op->n_local);
+    Cheb P = cheb_from(p);
+    enqueue_cheb(c, op, P, r, out, -1);
+  });
+}
+
+pcgx_status pcgx_cheb_apply(pcgx_context c, pcgx_operator op, const pcgx_cheb* p, const double* r,
+                            double* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    const long long n = op->n_local;
+    ensure_workspace(c, n);
+    Cheb P = cheb_from(p);
+    PCGX_CUDA(cudaMemcpyAsync(c->t0, r, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
+    enqueue_cheb(c, op, P, c->t0, c->t1, -1);
+    PCGX_CUDA(cudaMemcpyAsync(out, c->t1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
+void pcgx_solve_opts_default(pcgx_solve_opts* o) {
+  o->tol = 1e-8;
+  o->maxit = 20000;
+  o->x0 = nullptr;
+  o->flags = 0;
+}
+
+pcgx_status pcgx_pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec,
+                                  const double* b, double* x, const pcgx_solve_opts* opts,
+                                  pcgx_report* rep) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (!rep) fail(PCGX_ERR_INVALID, "pcg_solve: null report");
+    pcg_solve_device(c, op, prec, b, x, opts, rep);
+  });
+}
+
+pcgx_status pcgx_pcg_solve(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec,
+                           const double* b, double* x, const pcgx_solve_opts* opts,
+                           pcgx_report* rep) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (!rep) fail(PCGX_ERR_INVALID, "pcg_solve: null report");
+    const long long n = op->n_local;
+    ensure_workspace(c, n);
+    // b and x live in t0 / t1 for the call (the solver uses r z p q w0 w1)
+    PCGX_CUDA(cudaMemcpyAsync(c->t0, b, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
+    pcgx_solve_opts o;
+    pcgx_solve_opts_default(&o);
+    if (opts) o = *opts;
+    if (o.x0) {
+      PCGX_CUDA(cudaMemcpyAsync(c->t1, o.x0, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
+      o.x0 = c->t1;
+    }
+    pcg_solve_device(c, op, prec, c->t0, c->t1, &o, rep);
+    PCGX_CUDA(cudaMemcpyAsync(x, c->t1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
+pcgx_status pcgx_random_uniform_device(pcgx_context c, int64_t n, uint64_t seed, uint64_t offset,
+                                       double* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    splitmix_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, seed, offset, out);
+    check_launch();
+    count_launch(c);
+  });
+}
+
+void pcgx_random_uniform(int64_t n, uint64_t seed, uint64_t offset, double* out) {
+  random_uniform_host(n, seed, offset, out);
+}
+
+void pcgx_analytic_extremes(int dim, int64_t nx, int scaled, double* lo, double* hi) {
+  analytic_extremes(dim, nx, scaled, lo, hi);
+}
+
+void pcgx_analytic_extremes_box(int64_t nx, int64_t ny, int64_t nz, double* lo, double* hi) {
+  analytic_extremes_box(nx, ny, nz, lo, hi);
+}
+
+pcgx_status pcgx_lanczos_bounds(pcgx_context c, pcgx_operator op, int steps_hi, int steps,
+                                uint64_t seed, double* lo, double* hi) {
+  return guarded(c, [&] {
+    set_device(c);
+    lanczos_device(c, op, steps_hi, steps, seed, lo, hi);
+  });
+}
+
+}  // extern "C"

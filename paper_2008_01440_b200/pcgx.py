@@ -1,0 +1,649 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Python host binding of the B200 Chebyshev-PCG library (ctypes over include/pcgx.h).
+
+This mirrors the reference's public C++ API (/root/reference/proj/include/polycg)
+name for name so that parity tests read like the reference's own tests:
+
+================================  =============================================
+reference (polycg)                here
+================================  =============================================
+StencilOperator(lap3d, nx)        ``StencilOperator(nx, ny=None, nz=None)``
+CsrMatrix(n, rp, ci, va)          ``CsrMatrix(n, row_ptr, col_idx, values)``
+jacobi_scale(op)                  ``jacobi_scale(op, ctx) -> (ScaledOperator, d)``
+LinearOperator::apply             ``ScaledOperator.apply(x)``
+cheb_params / eval_poly           ``cheb_params`` / ``eval_poly``
+apply_chebyshev                   ``apply_chebyshev(params, op, r)``
+ChebyshevPreconditioner           ``ChebyshevPreconditioner(params)``
+SolveOptions / SolveReport        ``SolveOptions`` / ``SolveReport``
+pcg_solve(op, b, opts, prec)      ``pcg_solve(op, b, opts, prec)``
+random_uniform_vector(n, seed)    ``random_uniform_vector(n, seed)``
+analytic_extremes(kind, nx, s)    ``analytic_extremes(dim, nx, scaled)``
+std::invalid_argument             ``InvalidArgument`` (a ``ValueError``)
+polycg::NumericalError            ``NumericalError``
+================================  =============================================
+
+Every compute call runs the sm_100a kernels in ``libpcgx.so``; there is no CPU
+fallback. Importing works without a GPU (host-only helpers such as
+``cheb_params`` and the generators are usable); creating a ``Context`` on a
+machine without a CUDA device raises ``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpcgx.so")
+
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+_vp = C.c_void_p
+
+
+class PcgxError(RuntimeError):
+    status = -1
+
+
+class InvalidArgument(PcgxError, ValueError):
+    status = 1
+
+
+class NumericalError(PcgxError):
+    status = 2
+
+
+class CudaError(PcgxError):
+    status = 3
+
+
+class NcclError(PcgxError):
+    status = 4
+
+
+class OverflowError_(PcgxError):
+    status = 5
+
+
+class Unsupported(PcgxError):
+    status = 6
+
+
+_ERRS = {1: InvalidArgument, 2: NumericalError, 3: CudaError, 4: NcclError, 5: OverflowError_,
+         6: Unsupported}
+
+
+class _Cheb(C.Structure):
+    _fields_ = [("m", C.c_int), ("theta", C.c_double), ("delta", C.c_double),
+                ("sigma", C.c_double), ("rho", _dp)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("maxit", C.c_int), ("x0", _vp), ("flags", C.c_uint32)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("iters", C.c_int64), ("ddot", C.c_int64), ("matvec", C.c_int64),
+                ("prec_applies", C.c_int64), ("rel_res", C.c_double),
+                ("true_rel_res", C.c_double), ("wall_time", C.c_double),
+                ("converged", C.c_int64), ("kernel_launches", C.c_int64),
+                ("wasted_matvec", C.c_int64), ("allreduces", C.c_int64),
+                ("halo_bytes", C.c_int64), ("alg_bytes", C.c_double),
+                ("spmv_equiv_bytes", C.c_double), ("step_ms", C.c_double),
+                ("step_launches", C.c_int64), ("step_bytes", C.c_double)]
+
+
+FLAG_TIME_KERNELS = 1
+FLAG_NO_GRAPH = 2
+
+# Exported symbols of include/pcgx.h (tests check the .so exports all of them).
+SYMBOLS = [
+    "pcgx_abi_version", "pcgx_last_error", "pcgx_context_create", "pcgx_nccl_unique_id",
+    "pcgx_context_create_dist", "pcgx_context_destroy", "pcgx_context_rank",
+    "pcgx_context_nranks", "pcgx_synchronize", "pcgx_kernel_launches", "pcgx_device_alloc",
+    "pcgx_device_free", "pcgx_memcpy_h2d", "pcgx_memcpy_d2h", "pcgx_memcpy_d2d",
+    "pcgx_host_alloc", "pcgx_host_free", "pcgx_timer_start", "pcgx_timer_stop",
+    "pcgx_flush_l2", "pcgx_stencil7_create", "pcgx_csr_create", "pcgx_csr_create_i32",
+    "pcgx_operator_destroy", "pcgx_operator_size", "pcgx_operator_local_size",
+    "pcgx_operator_z0", "pcgx_operator_nnz", "pcgx_operator_matvec_count",
+    "pcgx_operator_apply", "pcgx_operator_apply_device", "pcgx_cheb_params", "pcgx_cheb_eval",
+    "pcgx_cheb_apply", "pcgx_cheb_apply_device", "pcgx_solve_opts_default", "pcgx_pcg_solve",
+    "pcgx_pcg_solve_device", "pcgx_random_uniform_device", "pcgx_random_uniform",
+    "pcgx_analytic_extremes", "pcgx_analytic_extremes_box", "pcgx_lanczos_bounds",
+    "pcgx_gen_fe27_size", "pcgx_gen_fe27_fill", "pcgx_gen_elast27_size",
+    "pcgx_gen_elast27_fill",
+]
+
+_lib = None
+
+
+def lib():
+    """Load libpcgx.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2008_01440_b200.build` "
+                          "(there is no CPU fallback)")
+    if not os.environ.get("PCGX_NCCL_LIB"):
+        # prefer the NCCL torch ships (same process may import torch later)
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            cand = os.path.join(base, "nccl", "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["PCGX_NCCL_LIB"] = cand
+                break
+    L = C.CDLL(LIB_PATH)
+    ctx = C.c_void_p
+    op = C.c_void_p
+    sig = {
+        "pcgx_abi_version": (C.c_int, []),
+        "pcgx_last_error": (C.c_char_p, [ctx]),
+        "pcgx_context_create": (C.c_int, [C.c_int, C.POINTER(ctx)]),
+        "pcgx_nccl_unique_id": (C.c_int, [C.c_void_p]),
+        "pcgx_context_create_dist": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                               C.POINTER(ctx)]),
+        "pcgx_context_destroy": (None, [ctx]),
+        "pcgx_context_rank": (C.c_int, [ctx]),
+        "pcgx_context_nranks": (C.c_int, [ctx]),
+        "pcgx_synchronize": (C.c_int, [ctx]),
+        "pcgx_kernel_launches": (C.c_int64, [ctx]),
+        "pcgx_device_alloc": (C.c_int, [ctx, C.c_size_t, C.POINTER(C.c_void_p)]),
+        "pcgx_device_free": (C.c_int, [ctx, C.c_void_p]),
+        "pcgx_memcpy_h2d": (C.c_int, [ctx, C.c_void_p, C.c_void_p, C.c_size_t]),
+        "pcgx_memcpy_d2h": (C.c_int, [ctx, C.c_void_p, C.c_void_p, C.c_size_t]),
+        "pcgx_memcpy_d2d": (C.c_int, [ctx, C.c_void_p, C.c_void_p, C.c_size_t]),
+        "pcgx_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+        "pcgx_host_free": (C.c_int, [C.c_void_p]),
+        "pcgx_timer_start": (C.c_int, [ctx]),
+        "pcgx_timer_stop": (C.c_int, [ctx, _dp]),
+        "pcgx_flush_l2": (C.c_int, [ctx, C.c_size_t]),
+        "pcgx_stencil7_create": (C.c_int, [ctx, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                                           C.POINTER(op)]),
+        "pcgx_csr_create": (C.c_int, [ctx, C.c_int64, _i64p, _i64p, _dp, _dp, C.POINTER(op)]),
+        "pcgx_csr_create_i32": (C.c_int, [ctx, C.c_int64, _i32p, _i32p, _dp, _dp,
+                                          C.POINTER(op)]),
+        "pcgx_operator_destroy": (None, [op]),
+        "pcgx_operator_size": (C.c_int64, [op]),
+        "pcgx_operator_local_size": (C.c_int64, [op]),
+        "pcgx_operator_z0": (C.c_int64, [op]),
+        "pcgx_operator_nnz": (C.c_int64, [op]),
+        "pcgx_operator_matvec_count": (C.c_uint64, [op]),
+        "pcgx_operator_apply": (C.c_int, [ctx, op, _dp, _dp]),
+        "pcgx_operator_apply_device": (C.c_int, [ctx, op, C.c_void_p, C.c_void_p]),
+        "pcgx_cheb_params": (C.c_int, [C.c_double, C.c_double, C.c_int, C.c_double, _dp, _dp]),
+        "pcgx_cheb_eval": (C.c_double, [C.POINTER(_Cheb), C.c_double]),
+        "pcgx_cheb_apply": (C.c_int, [ctx, op, C.POINTER(_Cheb), _dp, _dp]),
+        "pcgx_cheb_apply_device": (C.c_int, [ctx, op, C.POINTER(_Cheb), C.c_void_p, C.c_void_p]),
+        "pcgx_solve_opts_default": (None, [C.POINTER(_Opts)]),
+        "pcgx_pcg_solve": (C.c_int, [ctx, op, C.POINTER(_Cheb), _dp, _dp, C.POINTER(_Opts),
+                                     C.POINTER(_Report)]),
+        "pcgx_pcg_solve_device": (C.c_int, [ctx, op, C.POINTER(_Cheb), C.c_void_p, C.c_void_p,
+                                            C.POINTER(_Opts), C.POINTER(_Report)]),
+        "pcgx_random_uniform_device": (C.c_int, [ctx, C.c_int64, C.c_uint64, C.c_uint64,
+                                                 C.c_void_p]),
+        "pcgx_random_uniform": (None, [C.c_int64, C.c_uint64, C.c_uint64, _dp]),
+        "pcgx_analytic_extremes": (None, [C.c_int, C.c_int64, C.c_int, _dp, _dp]),
+        "pcgx_analytic_extremes_box": (None, [C.c_int64, C.c_int64, C.c_int64, _dp, _dp]),
+        "pcgx_lanczos_bounds": (C.c_int, [ctx, op, C.c_int, C.c_int, C.c_uint64, _dp, _dp]),
+        "pcgx_gen_fe27_size": (C.c_int, [C.c_int64, _i64p, _i64p]),
+        "pcgx_gen_fe27_fill": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, _i32p, _i32p, _dp]),
+        "pcgx_gen_elast27_size": (C.c_int, [C.c_int64, _i64p, _i64p]),
+        "pcgx_gen_elast27_fill": (C.c_int, [C.c_int64, C.c_double, C.c_double, C.c_double,
+                                            C.c_uint64, _i32p, _i32p, _dp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    if L.pcgx_abi_version() != 1:
+        raise ImportError("libpcgx ABI mismatch")
+    _lib = L
+    return L
+
+
+def _ptr(a, t=_dp):
+    return a.ctypes.data_as(t)
+
+
+def _check(status, ctx_handle=None):
+    if status == 0:
+        return
+    msg = lib().pcgx_last_error(ctx_handle).decode(errors="replace")
+    raise _ERRS.get(status, PcgxError)(msg)
+
+
+# ============================================================================ context
+
+class Context:
+    """One GPU (optionally one rank of a z-slab NCCL job). Mirrors the
+    one-Preconditioner-per-solve ownership rule (pcg.hpp:16-19): a context runs
+    one call at a time."""
+
+    def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, nccl_id=None):
+        L = lib()
+        h = C.c_void_p()
+        if nranks == 1:
+            _check(L.pcgx_context_create(device, C.byref(h)))
+        else:
+            buf = C.create_string_buffer(bytes(nccl_id), 128)
+            _check(L.pcgx_context_create_dist(device, nranks, rank, buf, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().pcgx_nccl_unique_id(buf))
+        return buf.raw
+
+    @property
+    def rank(self):
+        return lib().pcgx_context_rank(self.h)
+
+    @property
+    def nranks(self):
+        return lib().pcgx_context_nranks(self.h)
+
+    @property
+    def kernel_launches(self) -> int:
+        return lib().pcgx_kernel_launches(self.h)
+
+    def synchronize(self):
+        _check(lib().pcgx_synchronize(self.h), self.h)
+
+    def timer_start(self):
+        _check(lib().pcgx_timer_start(self.h), self.h)
+
+    def timer_stop(self) -> float:
+        ms = C.c_double()
+        _check(lib().pcgx_timer_stop(self.h, C.byref(ms)), self.h)
+        return ms.value
+
+    def flush_l2(self, nbytes=256 << 20):
+        _check(lib().pcgx_flush_l2(self.h, nbytes), self.h)
+
+    def close(self):
+        if self.h:
+            lib().pcgx_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class DeviceVector:
+    """fp64 vector in HBM owned by a context."""
+
+    def __init__(self, ctx: Context, n: int):
+        self.ctx, self.n = ctx, int(n)
+        p = C.c_void_p()
+        _check(lib().pcgx_device_alloc(ctx.h, 8 * max(self.n, 1), C.byref(p)), ctx.h)
+        self.ptr = p.value
+
+    @classmethod
+    def from_numpy(cls, ctx, a):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        v = cls(ctx, a.size)
+        _check(lib().pcgx_memcpy_h2d(ctx.h, v.ptr, a.ctypes.data, 8 * a.size), ctx.h)
+        return v
+
+    def numpy(self):
+        out = np.empty(self.n)
+        _check(lib().pcgx_memcpy_d2h(self.ctx.h, out.ctypes.data, self.ptr, 8 * self.n), self.ctx.h)
+        return out
+
+    def copy_from(self, other: "DeviceVector"):
+        _check(lib().pcgx_memcpy_d2d(self.ctx.h, self.ptr, other.ptr, 8 * self.n), self.ctx.h)
+
+    def free(self):
+        if self.ptr:
+            lib().pcgx_device_free(self.ctx.h, self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            if self.ptr and self.ctx.h:
+                self.free()
+        except Exception:
+            pass
+
+
+class PinnedBuffer:
+    """Page-locked host fp64 buffer (numpy view) for the end-to-end path."""
+
+    def __init__(self, n):
+        p = C.c_void_p()
+        _check(lib().pcgx_host_alloc(8 * max(int(n), 1), C.byref(p)))
+        self.ptr = p.value
+        self.array = np.ctypeslib.as_array(C.cast(p, _dp), shape=(int(n),))
+
+    def free(self):
+        if self.ptr:
+            lib().pcgx_host_free(self.ptr)
+            self.ptr = None
+
+
+# ============================================================================ operators
+
+@dataclass
+class StencilOperator:
+    """StencilOperator(lap3d, nx) (proj/include/polycg/linop.hpp:94-108); ny, nz
+    default to nx (the builder allows boxes for config 5 weak scaling)."""
+    nx: int
+    ny: int | None = None
+    nz: int | None = None
+
+    def dims(self):
+        return self.nx, self.ny or self.nx, self.nz or self.nx
+
+    def size(self):
+        a, b, c = self.dims()
+        return a * b * c
+
+    def diagonal(self):
+        return np.full(self.size(), 6.0)
+
+
+@dataclass
+class CsrMatrix:
+    """CsrMatrix(n, row_ptr, col_idx, values) (linop.hpp:60-85), host arrays."""
+    n: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    def size(self):
+        return self.n
+
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+    def diagonal(self):
+        rows = np.repeat(np.arange(self.n), np.diff(self.row_ptr))
+        d = np.zeros(self.n)
+        m = self.col_idx == rows
+        d[rows[m]] = self.values[m]
+        return d
+
+
+class ScaledOperator:
+    """Device-resident D^{-1/2} A D^{-1/2} (ScaledOperator, linop.hpp:112-126)."""
+
+    def __init__(self, ctx: Context, handle, inner):
+        self.ctx, self.h, self.inner = ctx, handle, inner
+
+    def size(self):
+        return lib().pcgx_operator_size(self.h)
+
+    def local_size(self):
+        return lib().pcgx_operator_local_size(self.h)
+
+    def z0(self):
+        return lib().pcgx_operator_z0(self.h)
+
+    def nnz(self):
+        return lib().pcgx_operator_nnz(self.h)
+
+    def matvec_count(self):
+        return lib().pcgx_operator_matvec_count(self.h)
+
+    def apply(self, x):
+        """y = A x. numpy in/out (host) or DeviceVector in/out (device)."""
+        if isinstance(x, DeviceVector):
+            y = DeviceVector(self.ctx, self.local_size())
+            _check(lib().pcgx_operator_apply_device(self.ctx.h, self.h, x.ptr, y.ptr), self.ctx.h)
+            return y
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.size != self.local_size():
+            raise InvalidArgument(f"apply: vector length {x.size} does not match operator "
+                                  f"dimension {self.local_size()}")
+        y = np.empty(self.local_size())
+        _check(lib().pcgx_operator_apply(self.ctx.h, self.h, _ptr(x), _ptr(y)), self.ctx.h)
+        return y
+
+    def close(self):
+        if self.h:
+            lib().pcgx_operator_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def jacobi_scale(op, ctx: Context):
+    """jacobi_scale (proj/src/linop.cpp:340-351): returns (ScaledOperator, inv_sqrt_diag)."""
+    L = lib()
+    h = C.c_void_p()
+    if isinstance(op, StencilOperator):
+        nx, ny, nz = op.dims()
+        _check(L.pcgx_stencil7_create(ctx.h, nx, ny, nz, 0.0, C.byref(h)), ctx.h)
+        return ScaledOperator(ctx, h, op), None
+    if isinstance(op, CsrMatrix):
+        rp, ci = np.asarray(op.row_ptr), np.asarray(op.col_idx)
+        va = np.ascontiguousarray(op.values, dtype=np.float64)
+        if rp.dtype == np.int32 and ci.dtype == np.int32:
+            _check(L.pcgx_csr_create_i32(ctx.h, op.n, _ptr(np.ascontiguousarray(rp), _i32p),
+                                         _ptr(np.ascontiguousarray(ci), _i32p), _ptr(va), None,
+                                         C.byref(h)), ctx.h)
+        else:
+            rp = np.ascontiguousarray(rp, dtype=np.int64)
+            ci = np.ascontiguousarray(ci, dtype=np.int64)
+            _check(L.pcgx_csr_create(ctx.h, op.n, _ptr(rp, _i64p), _ptr(ci, _i64p), _ptr(va),
+                                     None, C.byref(h)), ctx.h)
+        return ScaledOperator(ctx, h, op), None
+    raise InvalidArgument("jacobi_scale: unsupported operator type")
+
+
+# ============================================================================ polynomial
+
+@dataclass
+class ChebyshevParams:
+    """ChebyshevParams (polyprec.hpp:36-45)."""
+    m: int
+    alpha: float
+    beta: float
+    scale: float
+    theta: float
+    delta: float
+    sigma: float
+    rho: np.ndarray = field(repr=False)
+
+    def _c(self):
+        s = _Cheb()
+        s.m, s.theta, s.delta, s.sigma = self.m, self.theta, self.delta, self.sigma
+        self._rho_keep = np.ascontiguousarray(self.rho, dtype=np.float64)
+        s.rho = _ptr(self._rho_keep)
+        return s
+
+
+def cheb_params(alpha, beta, m, scale=1.0) -> ChebyshevParams:
+    """cheb_params (polyprec.cpp:56-79), bit-exact, with the positivity check."""
+    tds = np.zeros(3)
+    rho = np.zeros(max(int(m), 0) + 1)
+    st = lib().pcgx_cheb_params(alpha, beta, int(m), scale, _ptr(tds), _ptr(rho))
+    _check(st, None)
+    return ChebyshevParams(int(m), alpha, beta, scale, tds[0], tds[1], tds[2], rho)
+
+
+def eval_poly(params: ChebyshevParams, lam: float) -> float:
+    return lib().pcgx_cheb_eval(C.byref(params._c()), lam)
+
+
+class ChebyshevPreconditioner:
+    """ChebyshevPreconditioner (pcg.hpp:42-55)."""
+
+    def __init__(self, params: ChebyshevParams):
+        self._params = params
+
+    def params(self):
+        return self._params
+
+    def degree(self):
+        return self._params.m
+
+    def apply(self, op: ScaledOperator, r):
+        return apply_chebyshev(self._params, op, r)
+
+
+def apply_chebyshev(params: ChebyshevParams, op: ScaledOperator, r):
+    """out = p_m(A) r (polyprec.cpp:169-198) on the device."""
+    cp = params._c()
+    if isinstance(r, DeviceVector):
+        out = DeviceVector(op.ctx, op.local_size())
+        _check(lib().pcgx_cheb_apply_device(op.ctx.h, op.h, C.byref(cp), r.ptr, out.ptr), op.ctx.h)
+        return out
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    if r.size != op.local_size():
+        raise InvalidArgument("apply_chebyshev: vector length mismatch")
+    out = np.empty(op.local_size())
+    _check(lib().pcgx_cheb_apply(op.ctx.h, op.h, C.byref(cp), _ptr(r), _ptr(out)), op.ctx.h)
+    return out
+
+
+# ============================================================================ solver
+
+@dataclass
+class SolveOptions:
+    """SolveOptions (pcg.hpp:57-64). on_iterate is not supported on the device path."""
+    tol: float = 1e-8
+    maxit: int = 20000
+    x0: object = None
+    flags: int = 0
+
+
+@dataclass
+class SolveReport:
+    """SolveReport (pcg.hpp:73-82) + device extensions."""
+    iters: int = 0
+    ddot: int = 0
+    matvec: int = 0
+    prec_applies: int = 0
+    rel_res: float = 0.0
+    true_rel_res: float = 0.0
+    wall_time: float = 0.0
+    converged: bool = False
+    kernel_launches: int = 0
+    wasted_matvec: int = 0
+    allreduces: int = 0
+    halo_bytes: int = 0
+    alg_bytes: float = 0.0
+    spmv_equiv_bytes: float = 0.0
+    step_ms: float = 0.0
+    step_launches: int = 0
+    step_bytes: float = 0.0
+
+    @classmethod
+    def _from(cls, r: _Report):
+        d = {f: getattr(r, f) for f, _ in _Report._fields_}
+        d["converged"] = bool(d["converged"])
+        return cls(**d)
+
+
+def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
+              prec: ChebyshevPreconditioner | None = None, x_out=None):
+    """pcg_solve (pcg.cpp:10-117) on the GPU.
+
+    b numpy -> host entry (b copied in, x copied out inside the call; returns
+    numpy x). b DeviceVector -> device entry (returns a DeviceVector x, or
+    writes into x_out).
+    """
+    opts = opts or SolveOptions()
+    L = lib()
+    o = _Opts()
+    L.pcgx_solve_opts_default(C.byref(o))
+    o.tol, o.maxit, o.flags = opts.tol, opts.maxit, opts.flags
+    rep = _Report()
+    cp = C.byref(prec.params()._c()) if prec is not None else None
+    if isinstance(b, DeviceVector):
+        x = x_out or DeviceVector(op.ctx, op.local_size())
+        if opts.x0 is not None:
+            o.x0 = opts.x0.ptr
+        _check(L.pcgx_pcg_solve_device(op.ctx.h, op.h, cp, b.ptr, x.ptr, C.byref(o),
+                                       C.byref(rep)), op.ctx.h)
+        return x, SolveReport._from(rep)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.size != op.local_size():
+        raise InvalidArgument("pcg_solve: rhs length mismatch")
+    x = np.empty(op.local_size()) if x_out is None else x_out
+    x0 = None
+    if opts.x0 is not None:
+        x0 = np.ascontiguousarray(opts.x0, dtype=np.float64)
+        if x0.size != b.size:
+            raise InvalidArgument("pcg_solve: x0 length mismatch")
+        o.x0 = x0.ctypes.data
+    _check(L.pcgx_pcg_solve(op.ctx.h, op.h, cp, _ptr(b), x.ctypes.data_as(_dp), C.byref(o),
+                            C.byref(rep)), op.ctx.h)
+    return x, SolveReport._from(rep)
+
+
+def lanczos_bounds(op: ScaledOperator, steps_hi=20, steps=30, seed=20240801):
+    lo, hi = C.c_double(), C.c_double()
+    _check(lib().pcgx_lanczos_bounds(op.ctx.h, op.h, steps_hi, steps, seed, C.byref(lo),
+                                     C.byref(hi)), op.ctx.h)
+    return lo.value, hi.value
+
+
+# ============================================================================ inputs
+
+def random_uniform_vector(n, seed, offset=0, ctx: Context | None = None):
+    """random_uniform_vector (eigenest.cpp:22-30). Host numpy, or a DeviceVector
+    generated on the GPU when ctx is given (bit-identical)."""
+    if ctx is None:
+        out = np.empty(int(n))
+        lib().pcgx_random_uniform(int(n), seed, offset, _ptr(out))
+        return out
+    v = DeviceVector(ctx, n)
+    _check(lib().pcgx_random_uniform_device(ctx.h, int(n), seed, offset, v.ptr), ctx.h)
+    return v
+
+
+def analytic_extremes(dim, nx, scaled=True):
+    lo, hi = C.c_double(), C.c_double()
+    lib().pcgx_analytic_extremes(dim, nx, int(scaled), C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
+
+
+def analytic_extremes_box(nx, ny, nz):
+    lo, hi = C.c_double(), C.c_double()
+    lib().pcgx_analytic_extremes_box(nx, ny, nz, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
+
+
+def gen_fe27(nx, sigma=1.0, seed=20240801) -> CsrMatrix:
+    """Config 3 matrix (int32 CSR): Q1 heterogeneous diffusion, lognormal cells."""
+    n, nnz = C.c_int64(), C.c_int64()
+    _check(lib().pcgx_gen_fe27_size(nx, C.byref(n), C.byref(nnz)))
+    rp = np.empty(n.value + 1, dtype=np.int32)
+    ci = np.empty(nnz.value, dtype=np.int32)
+    va = np.empty(nnz.value)
+    _check(lib().pcgx_gen_fe27_fill(nx, sigma, seed, _ptr(rp, _i32p), _ptr(ci, _i32p), _ptr(va)))
+    return CsrMatrix(n.value, rp, ci, va)
+
+
+def gen_elast27(nx, lam=1.0, mu=0.5, eps=0.1, seed=20240801) -> CsrMatrix:
+    """Config 4 matrix (int32 CSR): 3-dof Q1 elasticity, 3x3 blocks, per-cell scaling."""
+    n, nnz = C.c_int64(), C.c_int64()
+    _check(lib().pcgx_gen_elast27_size(nx, C.byref(n), C.byref(nnz)))
+    rp = np.empty(n.value + 1, dtype=np.int32)
+    ci = np.empty(nnz.value, dtype=np.int32)
+    va = np.empty(nnz.value)
+    _check(lib().pcgx_gen_elast27_fill(nx, lam, mu, eps, seed, _ptr(rp, _i32p), _ptr(ci, _i32p),
+                                       _ptr(va)))
+    return CsrMatrix(n.value, rp, ci, va)

@@ -1,0 +1,368 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden outputs and the C oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): polynomial coefficients bit-exact; P_k(A) r per
+degree step within 1e-12 relative (here: BITWISE, the kernels reproduce the
+reference's per-point IEEE operations); PCG iterations within +-1; relative
+residual and solution within 1e-10 relative of the oracle's.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleOp
+from tests._util import fh, fhs, lap3d_csr, rel_norm, sha
+
+pytestmark = pytest.mark.gpu
+SEED = 20240801
+
+
+@pytest.fixture(scope="module")
+def P(pcgx):
+    return pcgx
+
+
+def stencil(P, ctx, nx, ny=None, nz=None):
+    op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
+    return op
+
+
+def csr(P, ctx, rp, ci, va):
+    op, _ = P.jacobi_scale(P.CsrMatrix(len(rp) - 1, np.asarray(rp), np.asarray(ci),
+                                       np.asarray(va)), ctx)
+    return op
+
+
+# ------------------------------------------------------------------ operators
+
+def test_stencil_apply_bitwise_vs_reference(P, ctx, golden):
+    for c in golden["stencil_apply"]:
+        nx = c["nx"]
+        x = P.random_uniform_vector(nx ** 3, c["x_seed"])
+        y = stencil(P, ctx, nx).apply(x)
+        assert sha(y) == c["sha256"], nx
+
+
+@pytest.mark.parametrize("dims", [(33, 17, 5), (1, 1, 1), (2, 3, 4), (40, 8, 70), (100, 100, 3)])
+def test_stencil_box_bitwise_vs_oracle(P, ctx, oracle, dims):
+    nx, ny, nz = dims
+    n = nx * ny * nz
+    x = oracle.random_uniform(n, 99)
+    y = stencil(P, ctx, nx, ny, nz).apply(x)
+    yo = oracle.apply(OracleOp("lap3d", nx=nx, ny=ny, nz=nz), x)
+    assert np.array_equal(y, yo)
+
+
+@pytest.mark.parametrize("kz", [1, 3, 16, 64])
+def test_stencil_kz_chunking_invariant(P, ctx, oracle, kz, monkeypatch):
+    monkeypatch.setenv("PCGX_KZ", str(kz))
+    nx = 21
+    x = oracle.random_uniform(nx ** 3, 5)
+    y = stencil(P, ctx, nx).apply(x)
+    assert np.array_equal(y, oracle.apply(OracleOp("lap3d", nx=nx), x))
+
+
+def test_csr_apply_bitwise_vs_reference(P, ctx, golden):
+    g = golden["csr_apply"]
+    n = len(g["row_ptr"]) - 1
+    x = P.random_uniform_vector(n, g["x_seed"])
+    va = fhs(g["values"])
+    y64 = csr(P, ctx, np.array(g["row_ptr"], np.int64), np.array(g["col_idx"], np.int64), va).apply(x)
+    y32 = csr(P, ctx, np.array(g["row_ptr"], np.int32), np.array(g["col_idx"], np.int32), va).apply(x)
+    assert np.array_equal(y64, fhs(g["y"]))
+    assert np.array_equal(y32, fhs(g["y"]))
+
+
+@pytest.mark.parametrize("nx", [2, 3, 5, 9, 16])
+def test_stencil_and_assembled_agree_bitwise(P, ctx, nx):
+    # test_linop.cpp:67-79
+    rp, ci, va = lap3d_csr(nx)
+    st, cs = stencil(P, ctx, nx), csr(P, ctx, rp, ci, va)
+    for trial in range(5):
+        x = P.random_uniform_vector(nx ** 3, 7000 + 100 * trial + nx)
+        assert np.array_equal(st.apply(x), cs.apply(x))
+
+
+def test_matvec_counter(P, ctx):
+    # test_linop.cpp:216-223 ; apply_chebyshev costs exactly m matvecs (test_polyprec.cpp:279-294)
+    op = stencil(P, ctx, 6)
+    x = np.ones(op.size())
+    c0 = op.matvec_count()
+    op.apply(x)
+    op.apply(x)
+    assert op.matvec_count() - c0 == 2
+    for m in (0, 1, 2, 5, 12):
+        c0 = op.matvec_count()
+        P.apply_chebyshev(P.cheb_params(0.1, 1.9, m, 1.0), op, x)
+        assert op.matvec_count() - c0 == m
+
+
+def test_apply_rejects_mismatched_length(P, ctx):
+    op = stencil(P, ctx, 4)
+    with pytest.raises(P.InvalidArgument):
+        op.apply(np.ones(3))
+
+
+def test_jacobi_scale_nonpositive_diagonal(P, ctx):
+    # test_linop.cpp:95-99: NumericalError naming the first nonpositive index
+    rp = np.array([0, 1, 2, 3], np.int64)
+    ci = np.array([0, 1, 2], np.int64)
+    va = np.array([1.0, -2.0, 3.0])
+    with pytest.raises(P.NumericalError, match="index 1"):
+        csr(P, ctx, rp, ci, va)
+
+
+def test_csr_structural_validation(P, ctx):
+    with pytest.raises(P.InvalidArgument, match="strictly increasing"):
+        csr(P, ctx, np.array([0, 2, 3], np.int64), np.array([1, 0, 1], np.int64), np.ones(3))
+    with pytest.raises(P.InvalidArgument, match="out of range"):
+        csr(P, ctx, np.array([0, 1, 2], np.int64), np.array([0, 5], np.int64), np.ones(2))
+
+
+# ------------------------------------------------------------------ polynomial
+
+def test_cheb_apply_per_degree_step_bitwise(P, ctx, golden):
+    for c in golden["apply_chebyshev"]:
+        nx = c["nx"]
+        op = stencil(P, ctx, nx)
+        a, b = P.analytic_extremes(3, nx)
+        r = P.random_uniform_vector(nx ** 3, c["r_seed"])
+        if "steps" in c:
+            for st in c["steps"]:
+                out = P.apply_chebyshev(P.cheb_params(a, b, st["m"], fh(c["scale"])), op, r)
+                assert sha(out) == st["sha256"], (nx, st["m"])
+        else:
+            out = P.apply_chebyshev(P.cheb_params(a, b, 5, fh(c["scale"])), op, r)
+            assert np.array_equal(out, fhs(c["m5_out"]))
+
+
+def test_cheb_apply_csr_bitwise(P, ctx, golden):
+    g, c = golden["csr_apply"], golden["apply_chebyshev_csr"]
+    op = csr(P, ctx, np.array(g["row_ptr"]), np.array(g["col_idx"]), fhs(g["values"]))
+    x = P.random_uniform_vector(len(g["row_ptr"]) - 1, c["x_seed"])
+    p = P.cheb_params(fh(c["alpha"]), fh(c["beta"]), c["m"], fh(c["scale"]))
+    assert sha(P.apply_chebyshev(p, op, x)) == c["sha256"]
+
+
+def test_cheb_apply_hand_values(P, ctx):
+    # test_polyprec.cpp:86-101 needs diag(1,3); a 2x2 CSR gives it
+    op = csr(P, ctx, np.array([0, 1, 2]), np.array([0, 1]), np.array([1.0, 1.0]))
+    # scaled operator of diag(1,1) is I; use the m=0 case: r / theta bitwise (test_polyprec.cpp:103-110)
+    p = P.cheb_params(1.0, 3.0, 0, 1.0)
+    r = np.array([2.0, -4.0])
+    assert np.array_equal(P.apply_chebyshev(p, op, r), r / 2.0)
+
+
+def test_cheb_apply_large_degree_vs_oracle(P, ctx, oracle):
+    nx = 24
+    a, b = P.analytic_extremes(3, nx)
+    r = oracle.random_uniform(nx ** 3, 3)
+    for m in (20, 40, 80):
+        out = P.apply_chebyshev(P.cheb_params(a, b, m, 1.001), stencil(P, ctx, nx), r)
+        ref = oracle.apply_chebyshev(OracleOp("lap3d", nx=nx), oracle.cheb_params(a, b, m, 1.001), r)
+        assert np.array_equal(out, ref), m
+
+
+# ------------------------------------------------------------------ inputs
+
+def test_random_uniform_device_bitwise(P, ctx, golden):
+    g = golden["random_uniform"]
+    v = P.random_uniform_vector(g["n"], g["seed"], ctx=ctx).numpy()
+    assert sha(v) == g["sha256"]
+    w = P.random_uniform_vector(1000, g["seed"], offset=4321, ctx=ctx).numpy()
+    assert np.array_equal(w, v[4321:5321])
+
+
+def test_lanczos_device_vs_oracle(P, ctx, oracle):
+    nx = 20
+    op = stencil(P, ctx, nx)
+    lo, hi = P.lanczos_bounds(op, 20, 30, SEED)
+    olo, ohi, al, be = oracle.lanczos(OracleOp("lap3d", nx=nx), 30, SEED)
+    _, ohi20 = oracle.tridiag_extremes(al[:20], be[:20])
+    assert lo == pytest.approx(olo, rel=1e-9)
+    assert hi == pytest.approx(ohi20, rel=1e-9)
+    a, b = P.analytic_extremes(3, nx)
+    assert a <= lo and hi <= b
+
+
+# ------------------------------------------------------------------ PCG
+
+def _golden_case(golden, tag):
+    return next(s for s in golden["pcg_solve"] if s["tag"] == tag)
+
+
+def _check_solve(P, oracle, c, op_gpu, op_or, n, form="host"):
+    xt = P.random_uniform_vector(n, SEED)
+    b = op_gpu.apply(xt)
+    assert sha(b) == c["b_sha256"]  # bitwise identical right-hand side
+    prm = None if c["m"] < 0 else P.cheb_params(fh(c["alpha"]), fh(c["beta"]), c["m"], fh(c["scale"]))
+    prec = None if prm is None else P.ChebyshevPreconditioner(prm)
+    opts = P.SolveOptions(tol=c["tol"], maxit=c["maxit"])
+    if form == "host":
+        x, rep = P.pcg_solve(op_gpu, b, opts, prec)
+    else:
+        bd = P.DeviceVector.from_numpy(op_gpu.ctx, b)
+        xd, rep = P.pcg_solve(op_gpu, bd, opts, prec)
+        x = xd.numpy()
+    g = c["report"]
+    # iteration count within +-1 (observed: identical) and the reference's counter rules
+    assert abs(rep.iters - g["iters"]) <= 1
+    m = max(c["m"], 0)
+    if rep.converged:
+        assert rep.ddot == 3 * rep.iters + 2
+        assert rep.matvec == rep.iters * (m + 1) + 1
+    assert rep.converged == bool(g["converged"])
+    # solution and residuals vs the oracle run on the same b
+    opr = None if prm is None else oracle.cheb_params(fh(c["alpha"]), fh(c["beta"]), c["m"], fh(c["scale"]))
+    xo, ro = oracle.pcg_solve(op_or, opr, b, tol=c["tol"], maxit=c["maxit"])
+    if rep.iters == ro["iters"]:
+        assert rel_norm(x, xo) <= 1e-10
+        assert abs(rep.rel_res - ro["rel_res"]) <= 1e-10 * ro["rel_res"] + 1e-300
+        assert abs(rep.true_rel_res - ro["true_rel_res"]) <= 1e-10 * max(ro["true_rel_res"], 1e-12)
+    err = rel_norm(x, xt)
+    assert err == pytest.approx(fh(c["err"]), rel=1e-6, abs=1e-12)
+    return rep
+
+
+@pytest.mark.parametrize("tag", ["lap24_m0", "lap24_m1", "lap24_m5", "lap24_m10", "lap24_m20",
+                                 "lap24_m40", "lap24_cg", "lap24_maxit", "lap32_m80"])
+def test_pcg_solve_stencil_vs_oracle(P, ctx, oracle, golden, tag):
+    c = _golden_case(golden, tag)
+    nx = c["nx"]
+    _check_solve(P, oracle, c, stencil(P, ctx, nx), OracleOp("lap3d", nx=nx), nx ** 3)
+
+
+def test_pcg_solve_cfg1_assembled_csr(P, ctx, oracle, golden):
+    """Config 1: 100^3 7-point CSR (int32 on the device), k=20, s=1.001 -> 19 iterations."""
+    c = _golden_case(golden, "cfg1")
+    rp, ci, va = lap3d_csr(100)
+    rep = _check_solve(P, oracle, c, csr(P, ctx, rp.astype(np.int32), ci.astype(np.int32), va),
+                       OracleOp("lap3d", nx=100), 100 ** 3)
+    assert (rep.iters, rep.ddot, rep.matvec, rep.prec_applies) == (19, 59, 400, 19)
+
+
+def test_pcg_solve_cfg1_stencil_device_entry(P, ctx, oracle, golden):
+    c = _golden_case(golden, "cfg1")
+    rep = _check_solve(P, oracle, c, stencil(P, ctx, 100), OracleOp("lap3d", nx=100), 100 ** 3,
+                       form="device")
+    assert rep.iters == 19 and rep.kernel_launches > 0
+
+
+def test_pcg_solve_csr300(P, ctx, oracle, golden):
+    g = golden["csr_apply"]
+    c = _golden_case(golden, "csr300_m7")
+    rp, ci, va = np.array(g["row_ptr"]), np.array(g["col_idx"]), fhs(g["values"])
+    _check_solve(P, oracle, c, csr(P, ctx, rp, ci, va),
+                 OracleOp("csr", row_ptr=rp, col_idx=ci, values=va), len(rp) - 1)
+
+
+def test_pcg_solve_x0_and_zero_rhs(P, ctx, oracle):
+    nx = 16
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    prm = P.cheb_params(a, b, 5, 1.001)
+    xt = P.random_uniform_vector(nx ** 3, SEED)
+    rhs = op.apply(xt)
+    x0 = P.random_uniform_vector(nx ** 3, 1)
+    x, rep = P.pcg_solve(op, rhs, P.SolveOptions(x0=x0), P.ChebyshevPreconditioner(prm))
+    xo, ro = oracle.pcg_solve(OracleOp("lap3d", nx=nx), oracle.cheb_params(a, b, 5, 1.001), rhs, x0=x0)
+    assert rep.iters == ro["iters"] and rep.matvec == ro["matvec"] and rep.ddot == ro["ddot"]
+    assert rel_norm(x, xo) <= 1e-10
+    # x0 already converged -> zero iterations, true_rel_res = rel_res (pcg.cpp:46-50)
+    x2, r2 = P.pcg_solve(op, rhs, P.SolveOptions(x0=x, tol=1e-3), P.ChebyshevPreconditioner(prm))
+    assert r2.iters == 0 and r2.converged and r2.true_rel_res == r2.rel_res
+    # b = 0 -> x = 0, converged, one ddot (pcg.cpp:32-37)
+    z, r3 = P.pcg_solve(op, np.zeros(nx ** 3), None, P.ChebyshevPreconditioner(prm))
+    assert r3.converged and r3.ddot == 1 and np.all(z == 0)
+
+
+def test_pcg_solve_invalid_options(P, ctx):
+    op = stencil(P, ctx, 4)
+    with pytest.raises(P.InvalidArgument, match="tol must be positive"):
+        P.pcg_solve(op, np.ones(64), P.SolveOptions(tol=0.0))
+    with pytest.raises(P.InvalidArgument, match="maxit must be >= 1"):
+        P.pcg_solve(op, np.ones(64), P.SolveOptions(maxit=0))
+    with pytest.raises(P.InvalidArgument, match="rhs length"):
+        P.pcg_solve(op, np.ones(5))
+
+
+def test_pcg_solve_indefinite_raises_numerical(P, ctx):
+    # symmetric, positive diagonal, indefinite: [[1, 2], [2, 1]] -> p'Ap <= 0 or r'z <= 0
+    op = csr(P, ctx, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([1.0, 2.0, 2.0, 1.0]))
+    with pytest.raises(P.NumericalError, match="pcg_solve: p'Ap"):
+        P.pcg_solve(op, np.array([1.0, -1.0]))
+
+
+def test_no_graph_path_identical(P, ctx):
+    nx = 20
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, 10, 1.001))
+    rhs = op.apply(P.random_uniform_vector(nx ** 3, SEED))
+    x1, r1 = P.pcg_solve(op, rhs, P.SolveOptions(), prec)
+    x2, r2 = P.pcg_solve(op, rhs, P.SolveOptions(flags=P.pcgx.FLAG_NO_GRAPH), prec)
+    assert np.array_equal(x1, x2) and r1.iters == r2.iters
+    assert r1.kernel_launches == r2.kernel_launches
+
+
+def test_determinism_run_to_run(P, ctx):
+    nx = 30
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, 20, 1.001))
+    rhs = op.apply(P.random_uniform_vector(nx ** 3, SEED))
+    xs = [P.pcg_solve(op, rhs, None, prec)[0] for _ in range(3)]
+    assert all(np.array_equal(xs[0], x) for x in xs[1:])
+
+
+# ------------------------------------------------------------------ builder configs 3/4 (small)
+
+def test_fe27_small_vs_oracle(P, ctx, oracle):
+    A = P.gen_fe27(14, sigma=1.0, seed=SEED)
+    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    lo, hi = P.lanczos_bounds(op, 20, 30, SEED)
+    opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    xt = P.random_uniform_vector(A.n, SEED)
+    rhs = op.apply(xt)
+    assert np.array_equal(rhs, oracle.apply(opo, xt))
+    prm = P.cheb_params(lo, hi, 40, 1.001)
+    x, rep = P.pcg_solve(op, rhs, None, P.ChebyshevPreconditioner(prm))
+    xo, ro = oracle.pcg_solve(opo, oracle.cheb_params(lo, hi, 40, 1.001), rhs)
+    assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
+    if rep.iters == ro["iters"]:
+        assert rel_norm(x, xo) <= 1e-10
+
+
+def test_elast27_small_vs_oracle(P, ctx, oracle):
+    A = P.gen_elast27(8, 1.0, 0.5, 0.1, seed=SEED)
+    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    lo, hi = P.lanczos_bounds(op, 20, 30, SEED)
+    opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    xt = P.random_uniform_vector(A.n, SEED)
+    rhs = op.apply(xt)
+    assert np.array_equal(rhs, oracle.apply(opo, xt))
+    prm = P.cheb_params(lo, hi, 30, 1.001)
+    x, rep = P.pcg_solve(op, rhs, P.SolveOptions(maxit=5000), P.ChebyshevPreconditioner(prm))
+    xo, ro = oracle.pcg_solve(opo, oracle.cheb_params(lo, hi, 30, 1.001), rhs, maxit=5000)
+    assert rep.converged == bool(ro["converged"]) and abs(rep.iters - ro["iters"]) <= 1
+    if rep.iters == ro["iters"]:
+        assert rel_norm(x, xo) <= 1e-10
+
+
+# ------------------------------------------------------------------ full size (BASELINE sizes)
+
+@pytest.mark.slow
+def test_cfg2_320_k20_known_answer(P, ctx):
+    """320^3 matrix-free, k=20, s=1.001: the reference measured 39 iterations, ddot 119,
+    matvec 820, rel_res = true_rel_res = 7.515e-9, error 1.513e-6."""
+    nx = 320
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    xt = P.random_uniform_vector(nx ** 3, SEED, ctx=ctx)
+    rhs = op.apply(xt)
+    x, rep = P.pcg_solve(op, rhs, None, P.ChebyshevPreconditioner(P.cheb_params(a, b, 20, 1.001)))
+    assert abs(rep.iters - 39) <= 1 and rep.converged
+    assert rep.rel_res == pytest.approx(7.515e-9, rel=1e-3)
+    assert rep.true_rel_res == pytest.approx(rep.rel_res, rel=1e-3)
+    xh, xth = x.numpy(), xt.numpy()
+    assert rel_norm(xh, xth) == pytest.approx(1.513e-6, rel=1e-3)

@@ -1,0 +1,150 @@
+# SPDX-License-Identifier: Apache-2.0
+"""CPU-only checks of the native library: it builds, loads, exports every symbol
+include/pcgx.h declares, and its host-side math and generators are right.
+No kernel is launched here (no GPU in the build container)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests._util import fh, fhs, sha
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_header_symbols_exported(pcgx):
+    hdr = open(os.path.join(ROOT, "include", "pcgx.h")).read()
+    declared = set(re.findall(r"\b(pcgx_[a-z0-9_]+)\s*\(", hdr))
+    declared -= {"pcgx_context_s", "pcgx_operator_s"}
+    L = C.CDLL(pcgx.LIB_PATH)
+    missing = [s for s in sorted(declared) if not hasattr(L, s)]
+    assert not missing, missing
+    assert declared == set(pcgx.SYMBOLS)
+
+
+def test_library_is_sm100a(pcgx):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", pcgx.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_context_without_gpu_fails_loudly(pcgx):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(pcgx.CudaError):
+        pcgx.Context(0)
+
+
+def test_cheb_params_bitwise(pcgx, golden):
+    for c in golden["cheb_params"]:
+        p = pcgx.cheb_params(fh(c["alpha"]), fh(c["beta"]), c["m"], fh(c["scale"]))
+        assert (p.theta, p.delta, p.sigma) == (fh(c["theta"]), fh(c["delta"]), fh(c["sigma"]))
+        assert np.array_equal(p.rho, fhs(c["rho"]))
+
+
+def test_cheb_params_errors_match_reference(pcgx, golden):
+    for e in golden["cheb_params_errors"]:
+        a, b, m, s = e["args"]
+        if e["error"] is None:
+            pcgx.cheb_params(a, b, m, s)
+            continue
+        exc = pcgx.InvalidArgument if e["error"] == "invalid_argument" else pcgx.NumericalError
+        with pytest.raises(exc) as ei:
+            pcgx.cheb_params(a, b, m, s)
+        assert str(ei.value) == e["msg"]
+
+
+def test_eval_poly_bitwise(pcgx, golden):
+    g = golden["eval_poly"]
+    for key, vals in g["by_m"].items():
+        m, s = key.split(":")
+        p = pcgx.cheb_params(fh(g["alpha"]), fh(g["beta"]), int(m), float(s))
+        got = np.array([pcgx.eval_poly(p, l) for l in fhs(g["lams"])])
+        assert np.array_equal(got, fhs(vals))
+
+
+def test_positivity_grid(pcgx):
+    # test_polyprec.cpp:296-306
+    for s in (1.0, 1.01, 1.1):
+        for m in (0, 1, 3, 7, 15, 31, 63):
+            p = pcgx.cheb_params(7.9064e-4, 1.99921, m, s)
+            lam = np.linspace(7.9064e-4, 1.99921, 2001)
+            assert all(pcgx.eval_poly(p, l) > 0 for l in lam)
+
+
+def test_optimality(pcgx):
+    # test_polyprec.cpp:173-188: max |1 - lambda p(lambda)| = 1 / T_{m+1}(sigma)
+    for a, b in ((7.9064e-4, 1.99921), (1e-3, 1.0), (0.02, 2.0)):
+        for m in (1, 3, 7, 15, 31):
+            p = pcgx.cheb_params(a, b, m, 1.0)
+            lam = a + (b - a) * np.arange(20001) / 20000
+            gm = max(abs(1 - l * pcgx.eval_poly(p, l)) for l in lam)
+            exp = 1.0 / np.cosh((m + 1) * np.arccosh(p.sigma))
+            assert gm == pytest.approx(exp, rel=1e-10)
+
+
+def test_analytic_extremes_bitwise(pcgx, golden):
+    for c in golden["analytic_extremes"]:
+        lo, hi = pcgx.analytic_extremes(c["dim"], c["nx"])
+        assert lo == fh(c["lo"]) and hi == fh(c["hi"])
+
+
+def test_random_uniform_host_bitwise(pcgx, golden):
+    g = golden["random_uniform"]
+    v = pcgx.random_uniform_vector(g["n"], g["seed"])
+    assert sha(v) == g["sha256"]
+    assert np.array_equal(pcgx.random_uniform_vector(100, g["seed"], offset=777), v[777:877])
+
+
+def _check_sym_spd(A, n, dense_ok=True):
+    rp, ci, va = A.row_ptr, A.col_idx, A.values
+    assert rp[0] == 0 and rp[-1] == len(ci)
+    assert np.all(np.diff(rp) >= 0)
+    for i in range(n):
+        row = ci[rp[i]:rp[i + 1]]
+        assert np.all(np.diff(row) > 0)
+    # bitwise symmetry: CsrMatrix(..., sym_tol = 0) contract
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    key = rows.astype(np.int64) * n + ci
+    keyT = ci.astype(np.int64) * n + rows
+    order = np.argsort(key)
+    orderT = np.argsort(keyT)
+    assert np.array_equal(key[order], keyT[orderT])
+    assert np.array_equal(va[order].view(np.uint64), va[orderT].view(np.uint64))
+    if dense_ok:
+        D = np.zeros((n, n))
+        D[rows, ci] = va
+        assert np.linalg.eigvalsh(D).min() > 0
+
+
+@pytest.mark.parametrize("nx", [1, 2, 4, 6])
+def test_gen_fe27(pcgx, nx):
+    A = pcgx.gen_fe27(nx, sigma=1.0, seed=5)
+    assert A.n == nx ** 3 and A.nnz() == (3 * nx - 2) ** 3
+    assert np.all(np.diff(A.row_ptr) <= 27)
+    _check_sym_spd(A, A.n)
+    # every one of the 27 couplings is nonzero (anisotropic Q1 element)
+    assert np.count_nonzero(A.values) == A.nnz()
+    # deterministic
+    B = pcgx.gen_fe27(nx, sigma=1.0, seed=5)
+    assert sha(A.values) == sha(B.values)
+
+
+@pytest.mark.parametrize("nx", [1, 2, 4])
+def test_gen_elast27(pcgx, nx):
+    A = pcgx.gen_elast27(nx, 1.0, 0.5, 0.1, seed=9)
+    assert A.n == 3 * nx ** 3 and A.nnz() == 9 * (3 * nx - 2) ** 3
+    assert np.all(np.diff(A.row_ptr) <= 81)
+    _check_sym_spd(A, A.n)
+
+
+def test_gen_sizes_at_configs(pcgx):
+    n, nnz = C.c_int64(), C.c_int64()
+    pcgx.lib().pcgx_gen_fe27_size(256, C.byref(n), C.byref(nnz))
+    assert (n.value, nnz.value) == (16_777_216, 449_455_096)
+    pcgx.lib().pcgx_gen_elast27_size(160, C.byref(n), C.byref(nnz))
+    assert (n.value, nnz.value) == (12_288_000, 982_938_168)
