@@ -1,0 +1,415 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Benchmark of the B200 Chebyshev-PCG hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config cfg2|cfg5s|cfg5w|cfg1|cfg3|cfg4] [--no-cpu-baseline]
+
+Default workload (N=1) is BASELINE.json configs[1] ("cfg2"): the 7-point
+Laplacian matrix-free on 320^3 (32.8M unknowns), fp64, Jacobi-scaled,
+x_true = random_uniform_vector(n, 20240801) (U(-1,1)), b = A x_true, x0 = 0,
+analytic bounds with theta-scale s = 1.001, PCG to ||r||/||b|| <= 1e-8, one
+solve per degree k in {0, 5, 10, 20, 40, 80}. One "step" = that whole degree
+sweep. Under torchrun (N > 1) every rank owns a 320x320x320 z-slab of a
+320 x 320 x (320 N) grid (weak scaling; NCCL halo planes + all-reduces).
+
+value = SpMV-equivalent GB/s of the whole job = sum_k matvec_k * 16 B * n /
+(sum_k time-to-1e-8_k), device-timed (CUDA events, max over ranks), inputs
+resident in HBM; e2e = the same metric through the host-buffer C-ABI call
+(pinned b copied in, x copied out, per solve). Vectors (262 MB) exceed the
+126 MB L2, so no flush is needed between timed solves.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 20240801
+METRIC = "Cheb-PCG time-to-1e-8 and SpMV-equiv GB/s vs HBM peak at 1/2/4/8 B200"
+SWEEP = [0, 5, 10, 20, 40, 80]
+SCALE = 1.001
+TOL = 1e-8
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- distributed plumbing
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Dist:
+    def __init__(self, ws, rank, local):
+        self.ws, self.rank, self.local = ws, rank, local
+        self.pg = None
+        if ws > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend="cpu:gloo,cuda:nccl")
+            self.dist = dist
+            self.torch = torch
+
+    def bcast_bytes(self, b):
+        if self.ws == 1:
+            return b
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def barrier(self):
+        if self.ws > 1:
+            self.dist.barrier()
+
+    def max(self, v):
+        if self.ws == 1:
+            return v
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v):
+        if self.ws == 1:
+            return v
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.ws > 1:
+            self.dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------- workloads
+
+def workload(config, ws):
+    """(dims, degrees, description) per config; dims = global (nx, ny, nz)."""
+    if config == "cfg2":
+        return (320, 320, 320 * ws), SWEEP, "7-pt matrix-free 320^3 per GPU, degree sweep"
+    if config == "cfg5s":
+        return (640, 640, 640), [40], "7-pt matrix-free 640^3 strong scaling, k=40"
+    if config == "cfg5w":
+        return (512, 512, 512 * ws), [40], "7-pt matrix-free 512x512x(512P) weak scaling, k=40"
+    raise SystemExit(f"unknown stencil config {config}")
+
+
+def run_gpu(args):
+    import paper_2008_01440_b200 as P
+    from paper_2008_01440_b200 import build as B
+    ws, rank, local = dist_env()
+    if ws != args.gpus:
+        if args.gpus > 1 and ws == 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one rank per GPU)")
+    B.build()
+    D = Dist(ws, rank, local)
+    if ws > 1:
+        nid = D.bcast_bytes(P.Context.nccl_unique_id() if rank == 0 else None)
+        ctx = P.Context(local, nranks=ws, rank=rank, nccl_id=nid)
+    else:
+        ctx = P.Context(0)
+    (nx, ny, nz), degrees, desc = workload(args.config, ws)
+    if args.degrees:
+        degrees = [int(v) for v in args.degrees.split(",")]
+    op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
+    n_loc = op.local_size()
+    n_glob = op.size()
+    if nx == ny == nz:
+        alpha, beta = P.analytic_extremes(3, nx)
+    else:
+        alpha, beta = P.analytic_extremes_box(nx, ny, nz)
+    xt = P.random_uniform_vector(n_loc, SEED, offset=op.z0() * nx * ny, ctx=ctx)
+    b = op.apply(xt)
+    x = P.DeviceVector(ctx, n_loc)
+    precs = {k: P.ChebyshevPreconditioner(P.cheb_params(alpha, beta, k, SCALE)) for k in degrees}
+    opts = P.SolveOptions(tol=TOL, maxit=100000)
+
+    def sweep(record=None):
+        tot_t, tot_mv, out = 0.0, 0, []
+        for k in degrees:
+            _, rep = P.pcg_solve(op, b, opts, precs[k], x_out=x)
+            t = D.max(rep.wall_time)
+            tot_t += t
+            tot_mv += rep.matvec
+            out.append((k, rep, t))
+        return tot_t, tot_mv, out
+
+    log(f"[bench] rank {rank}/{ws}: {desc}, n_local={n_loc}, warmup {args.warmup}")
+    for _ in range(args.warmup):
+        sweep()
+    ctx.synchronize()
+    D.barrier()
+    l0 = ctx.kernel_launches
+    times, mvs, reps = [], [], None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            D.barrier()
+            ctx.synchronize()
+            t, mv, reps = sweep()
+            times.append(t)
+            mvs.append(mv)
+    launches = ctx.kernel_launches - l0
+    clocks = clk.summary()
+    spmv_bytes = 16.0 * n_glob
+    t_step = float(np.mean(times))
+    value = float(np.mean(mvs)) * spmv_bytes / t_step / 1e9
+
+    # dominant kernel: fused Chebyshev middle step, CUDA-event timed on the compute stream
+    kbig = max(k for k in degrees)
+    _, rprof = P.pcg_solve(op, b, P.SolveOptions(tol=TOL, maxit=100000,
+                                                 flags=P.pcgx.FLAG_TIME_KERNELS), precs[kbig], x_out=x)
+    step_ms = D.max(rprof.step_ms / max(rprof.step_launches, 1))
+    step_bytes = 32.0 * n_loc
+    peak, peak_kind = peaks()
+    achieved = step_bytes / (step_ms * 1e-3) / 1e9
+
+    # end to end: host (pinned) b in, x out, through the host-buffer C-ABI entry
+    hb = P.PinnedBuffer(n_loc)
+    hx = P.PinnedBuffer(n_loc)
+    hb.array[:] = b.numpy()
+    e2e_t = []
+    e2e_mv = []
+    for i in range(max(1, min(args.steps, 2)) + 1):
+        D.barrier()
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        mv = 0
+        for k in degrees:
+            _, rep = P.pcg_solve(op, hb.array, opts, precs[k], x_out=hx.array)
+            mv += rep.matvec
+        ctx.synchronize()
+        dt = D.max(time.perf_counter() - t0)
+        if i > 0:  # first pass warms the host path
+            e2e_t.append(dt)
+            e2e_mv.append(mv)
+    e2e_value = float(np.mean(e2e_mv)) * spmv_bytes / float(np.mean(e2e_t)) / 1e9
+
+    per_k = []
+    for k, rep, t in reps:
+        per_k.append({"k": k, "iters": rep.iters, "ddot": rep.ddot, "matvec": rep.matvec,
+                      "time_to_1e8_s": round(t, 6), "rel_res": rep.rel_res,
+                      "true_rel_res": rep.true_rel_res, "converged": rep.converged,
+                      "alg_GBps": round(D.sum(rep.alg_bytes) / t / 1e9, 1),
+                      "spmv_equiv_GBps": round(rep.matvec * spmv_bytes / t / 1e9, 1)})
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            td = json.load(f)
+        if td.get("n") == n_loc:
+            traffic = td.get("dram_bytes_per_launch")
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample()
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded x_true ~ U(-1,1), b = A x_true)",
+        "config": {"workload": args.config, "desc": desc, "grid": [nx, ny, nz],
+                   "n_global": n_glob, "degrees": degrees, "theta_scale": SCALE, "tol": TOL,
+                   "bounds": "analytic", "parallelism": f"z-slab x{ws}",
+                   "l2": "inputs larger than L2 (262 MB vectors vs 126 MB L2); no flush"},
+        "per_k": per_k,
+        "time_to_1e8_s": {str(k): round(t, 6) for k, _, t in reps},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "stencil7_kernel<EpiChebStep> (fused SpMV + Chebyshev step)",
+                     "bytes_per_launch": step_bytes, "avg_launch_ms": round(step_ms, 5),
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
+                     "frac_of_8TBs_spec": round(achieved / 8000.0, 4)},
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s",
+                "h2d_bytes_per_step": 8 * n_loc * len(degrees) * ws,
+                "d2h_bytes_per_step": 8 * n_loc * len(degrees) * ws},
+        "gpu_launches": int(D.sum(launches)),
+        "clocks": clocks,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    hb.free()
+    hx.free()
+    D.barrier()
+    ctx.close()
+    D.close()
+
+
+# ----------------------------------------------------------------- CPU reference arm
+
+CPU_SAMPLE_NX = 320
+CPU_SAMPLE_K = 20
+CPU_SAMPLE_MAXIT = 2
+
+
+def _ref_lib():
+    """The reference library itself (oracle/_ref, compiled from /root/reference/proj
+    sources by oracle/Makefile); falls back to the C restatement if absent."""
+    from oracle.oracle import Oracle, RefLib
+    try:
+        return "reference", RefLib()
+    except FileNotFoundError:
+        return "port", Oracle()
+
+
+def cpu_sample(kind, L, threads):
+    """One bounded sample: reference pcg_solve on 320^3 matrix-free, k=20,
+    s=1.001, maxit=2 (setup P r + 2 iterations + exit residual = 63 SpMVs)."""
+    nx = CPU_SAMPLE_NX
+    n = nx ** 3
+    if kind == "reference":
+        L.set_threads(threads)
+        a, b = L.analytic_extremes(3, nx)
+        _, _, rep = L.pcg_solve("lap3d", a, b, CPU_SAMPLE_K, SCALE, nx=nx, seed=SEED, tol=TOL,
+                                maxit=CPU_SAMPLE_MAXIT, want_x=False)
+    else:
+        from oracle.oracle import OracleOp
+        op = OracleOp("lap3d", nx=nx)
+        a, b = L.analytic_extremes(3, nx)
+        rhs = L.apply(op, L.random_uniform(n, SEED))
+        _, rep = L.pcg_solve(op, L.cheb_params(a, b, CPU_SAMPLE_K, SCALE), rhs, tol=TOL,
+                             maxit=CPU_SAMPLE_MAXIT)
+    gbps = rep["matvec"] * 16.0 * n / rep["wall_time"] / 1e9
+    return gbps, rep
+
+
+def cpu_baseline_sample():
+    kind, L = _ref_lib()
+    threads = os.cpu_count() or 1
+    try:
+        gbps, rep = cpu_sample(kind, L, threads)
+    except Exception as e:  # never let the baseline kill the GPU line
+        return {"value": None, "unit": "GB/s", "cores": threads, "kind": kind, "error": str(e)}
+    return {"value": round(gbps, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": (f"reference pcg_solve on 320^3 matrix-free (cfg2 shape), k={CPU_SAMPLE_K}, "
+                       f"s={SCALE}, maxit={CPU_SAMPLE_MAXIT}: {rep['matvec']} SpMVs in "
+                       f"{rep['wall_time']:.2f} s; OpenMP apply_impl threads={threads}, Eigen "
+                       "vector ops single-threaded as in the reference"),
+            "wall_time_s": round(rep["wall_time"], 3)}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    kind, L = _ref_lib()
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        gbps, rep = cpu_sample(kind, L, threads)
+        if i >= args.warmup:
+            vals.append((gbps, rep["wall_time"]))
+    value = float(np.mean([v for v, _ in vals]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(float(np.mean([t for _, t in vals])) * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded x_true ~ U(-1,1), b = A x_true)",
+        "config": {"workload": args.config, "grid": [CPU_SAMPLE_NX] * 3, "degrees": [CPU_SAMPLE_K],
+                   "theta_scale": SCALE, "tol": TOL, "maxit": CPU_SAMPLE_MAXIT},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": f"320^3 k={CPU_SAMPLE_K} maxit={CPU_SAMPLE_MAXIT} per step"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pcgx", choices=["pcgx", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg5s", "cfg5w"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--degrees", default=None, help="override the degree list (profiling)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "pcgx":
+        log("[bench] note: fewer than 3 warm-up steps requested")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -31,6 +31,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -234,6 +235,7 @@ class Context:
             _check(L.pcgx_context_create_dist(device, nranks, rank, buf, C.byref(h)))
         self.h = h
         self.device = device
+        self._children = weakref.WeakSet()  # operators / vectors to release before the context
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -269,6 +271,8 @@ class Context:
 
     def close(self):
         if self.h:
+            for ch in list(self._children):
+                ch.close()
             lib().pcgx_context_destroy(self.h)
             self.h = None
 
@@ -293,6 +297,7 @@ class DeviceVector:
         p = C.c_void_p()
         _check(lib().pcgx_device_alloc(ctx.h, 8 * max(self.n, 1), C.byref(p)), ctx.h)
         self.ptr = p.value
+        ctx._children.add(self)
 
     @classmethod
     def from_numpy(cls, ctx, a):
@@ -310,14 +315,15 @@ class DeviceVector:
         _check(lib().pcgx_memcpy_d2d(self.ctx.h, self.ptr, other.ptr, 8 * self.n), self.ctx.h)
 
     def free(self):
-        if self.ptr:
+        if self.ptr and self.ctx.h:
             lib().pcgx_device_free(self.ctx.h, self.ptr)
-            self.ptr = None
+        self.ptr = None
+
+    close = free
 
     def __del__(self):
         try:
-            if self.ptr and self.ctx.h:
-                self.free()
+            self.free()
         except Exception:
             pass
 
@@ -385,6 +391,7 @@ class ScaledOperator:
 
     def __init__(self, ctx: Context, handle, inner):
         self.ctx, self.h, self.inner = ctx, handle, inner
+        ctx._children.add(self)
 
     def size(self):
         return lib().pcgx_operator_size(self.h)
@@ -416,9 +423,9 @@ class ScaledOperator:
         return y
 
     def close(self):
-        if self.h:
+        if self.h and self.ctx.h:
             lib().pcgx_operator_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
