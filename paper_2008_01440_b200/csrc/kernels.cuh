@@ -73,26 +73,55 @@ __device__ __forceinline__ void block_reduce_finish(double v, const Reduce& red)
 }
 
 // ----------------------------------------------------------------- epilogues
-// operator()(idx, y, xc): y = (A_scaled x)[idx], xc = x[idx]. Returns the
-// point's contribution to the launch's reduction (ignored when not reducing).
+// Two-phase interface so the marching kernels can prefetch the epilogue's own
+// operand vectors one plane ahead:
+//   ld(idx, v)  / ld2(idx, v)          load the per-point operands (scalar / double2)
+//   st(idx, y, xc, v) / st2(...)        consume y = (A_scaled x)[idx] and xc = x[idx],
+//                                       write outputs, return the point's contribution
+//                                       to the launch's reduction.
+
+__device__ __forceinline__ double2 ldg2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ void st2(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
 
 // q = A p ; contribution p_i q_i  (pcg.cpp:72-74)
 struct EpiStore {
   double* out;
-  __device__ __forceinline__ double operator()(long long idx, double y, double xc) const {
+  __device__ __forceinline__ void ld(long long, double (&)[2]) const {}
+  __device__ __forceinline__ void ld2(long long, double2 (&)[2]) const {}
+  __device__ __forceinline__ double st(long long idx, double y, double xc, const double (&)[2]) const {
     out[idx] = y;
     return xc * y;
   }
+  __device__ __forceinline__ double st2(long long idx, double y0, double y1, double2 xc,
+                                        const double2 (&)[2]) const {
+    pcgx::st2(out + idx, y0, y1);
+    return xc.x * y0 + xc.y * y1;
+  }
 };
 
-// e = b - A x ; contribution e_i^2  (pcg.cpp:43-45 with x0, and the exit true residual :112-114)
+// e = b - A x ; contribution e_i^2  (pcg.cpp:43-45 with x0, exit true residual :112-114)
 struct EpiResid {
   const double* __restrict__ b;
   double* e;  // may be nullptr (true residual: only the norm is needed)
-  __device__ __forceinline__ double operator()(long long idx, double y, double) const {
-    const double ei = b[idx] - y;
+  __device__ __forceinline__ void ld(long long idx, double (&v)[2]) const { v[0] = __ldg(b + idx); }
+  __device__ __forceinline__ void ld2(long long idx, double2 (&v)[2]) const { v[0] = ldg2(b + idx); }
+  __device__ __forceinline__ double st(long long idx, double y, double, const double (&v)[2]) const {
+    const double ei = v[0] - y;
     if (e) e[idx] = ei;
     return ei * ei;
+  }
+  __device__ __forceinline__ double st2(long long idx, double y0, double y1, double2,
+                                        const double2 (&v)[2]) const {
+    const double e0 = v[0].x - y0, e1 = v[0].y - y1;
+    if (e) pcgx::st2(e + idx, e0, e1);
+    return e0 * e0 + e1 * e1;
   }
 };
 
@@ -103,34 +132,79 @@ struct EpiResid {
 struct EpiChebFirst {
   double* __restrict__ xout;
   double theta, c1;
-  __device__ __forceinline__ double operator()(long long idx, double y, double xc) const {
-    const double xn = c1 * ((2.0 * xc) - (y / theta));
+  __device__ __forceinline__ void ld(long long, double (&)[2]) const {}
+  __device__ __forceinline__ void ld2(long long, double2 (&)[2]) const {}
+  __device__ __forceinline__ double f(double y, double xc) const {
+    return c1 * ((2.0 * xc) - (y / theta));
+  }
+  __device__ __forceinline__ double st(long long idx, double y, double xc, const double (&)[2]) const {
+    const double xn = f(y, xc);
     xout[idx] = xn;
     return xc * xn;
   }
+  __device__ __forceinline__ double st2(long long idx, double y0, double y1, double2 xc,
+                                        const double2 (&)[2]) const {
+    const double a = f(y0, xc.x), b = f(y1, xc.y);
+    pcgx::st2(xout + idx, a, b);
+    return xc.x * a + xc.y * b;
+  }
 };
 
-// Chebyshev step k >= 2 (polyprec.cpp:190-195), input vector = x_k-1:
+// Chebyshev step k >= 2 (polyprec.cpp:190-195), input vector = x_{k-1}:
 //   z = (2/delta) (r - A x) ; x_new = rho_k ((2 sigma) x - rho_{k-1} x_old + z)
 // x_old is r/theta at k == 2 (xold_from_r), otherwise read from xold; x_new is
-// written to out (== xold for the in-place middle steps). Contribution r_i x_new_i.
+// written to out (== xold for the in-place middle steps: each point's x_old is
+// read by its own thread before it is overwritten). Contribution r_i x_new_i.
 struct EpiChebStep {
   const double* __restrict__ r;
   const double* xold;
   double* out;
   double rk, rk1, c2, c3, theta;
   int xold_from_r;
-  __device__ __forceinline__ double operator()(long long idx, double y, double xc) const {
-    const double ri = r[idx];
-    const double xo = xold_from_r ? (ri / theta) : xold[idx];
+  __device__ __forceinline__ void ld(long long idx, double (&v)[2]) const {
+    v[0] = __ldg(r + idx);
+    v[1] = xold_from_r ? 0.0 : xold[idx];
+  }
+  __device__ __forceinline__ void ld2(long long idx, double2 (&v)[2]) const {
+    v[0] = ldg2(r + idx);
+    v[1] = xold_from_r ? make_double2(0.0, 0.0) : pcgx::ld2(xold + idx);
+  }
+  __device__ __forceinline__ double f(double y, double xc, double ri, double xo_in) const {
+    const double xo = xold_from_r ? (ri / theta) : xo_in;
     const double z = c2 * (ri - y);
-    const double xn = rk * (((c3 * xc) - (rk1 * xo)) + z);
+    return rk * (((c3 * xc) - (rk1 * xo)) + z);
+  }
+  __device__ __forceinline__ double st(long long idx, double y, double xc, const double (&v)[2]) const {
+    const double xn = f(y, xc, v[0], v[1]);
     out[idx] = xn;
-    return ri * xn;
+    return v[0] * xn;
+  }
+  __device__ __forceinline__ double st2(long long idx, double y0, double y1, double2 xc,
+                                        const double2 (&v)[2]) const {
+    const double a = f(y0, xc.x, v[0].x, v[1].x), b = f(y1, xc.y, v[0].y, v[1].y);
+    pcgx::st2(out + idx, a, b);
+    return v[0].x * a + v[0].y * b;
   }
 };
 
 // ----------------------------------------------------------------- 7-point stencil
+
+// Scaled 7-point row: terms in ascending column order k-1, j-1, i-1, centre,
+// i+1, j+1, k+1 (linop.cpp:247-253), t = d*x per neighbour (linop.cpp:272),
+// y = s*d (linop.cpp:274). A missing (Dirichlet) neighbour is passed as 0: its
+// term -(d*0) = -0 leaves the running sum bit-identical to the skipped term.
+__device__ __forceinline__ double stencil_point(double d, double xm, double xs, double xw,
+                                                double xc, double xe, double xn, double xp) {
+  double s = 0.0;
+  s = s + (-(d * xm));
+  s = s + (-(d * xs));
+  s = s + (-(d * xw));
+  s = s + (6.0 * (d * xc));
+  s = s + (-(d * xe));
+  s = s + (-(d * xn));
+  s = s + (-(d * xp));
+  return s * d;
+}
 
 // One thread per (i, j) column, marching planes [kb, ke) with the k-1, k, k+1
 // values in registers and the k+2 plane prefetched one iteration ahead; the
@@ -159,28 +233,91 @@ stencil7_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begi
     double xm = plane(kb - 1);
     double xc = plane(kb);
     double xp = plane(kb + 1);
+    double ev[2] = {0.0, 0.0};
+    epi.ld((long long)kb * nxy + col, ev);
     for (int k = kb; k < ke; ++k) {
-      const double xpp = (k + 1 < ke) ? plane(k + 2) : 0.0;
       const long long idx = (long long)k * nxy + col;
+      const bool more = k + 1 < ke;
+      const double xpp = more ? plane(k + 2) : 0.0;
+      double evn[2] = {0.0, 0.0};
+      if (more) epi.ld(idx + nxy, evn);
       const double xw = has_w ? __ldg(x + idx - 1) : 0.0;
       const double xe = has_e ? __ldg(x + idx + 1) : 0.0;
       const double xs = has_s ? __ldg(x + idx - g.nx) : 0.0;
       const double xn = has_n ? __ldg(x + idx + g.nx) : 0.0;
-      // ascending column order: k-1, j-1, i-1, centre, i+1, j+1, k+1 (linop.cpp:247-253)
-      double s = 0.0;
-      s = s + (-(d * xm));
-      s = s + (-(d * xs));
-      s = s + (-(d * xw));
-      s = s + (6.0 * (d * xc));
-      s = s + (-(d * xe));
-      s = s + (-(d * xn));
-      s = s + (-(d * xp));
-      const double y = s * d;
-      const double c = epi(idx, y, xc);
+      const double y = stencil_point(d, xm, xs, xw, xc, xe, xn, xp);
+      const double c = epi.st(idx, y, xc, ev);
       if (kRed) acc = acc + c;
       xm = xc;
       xc = xp;
       xp = xpp;
+      ev[0] = evn[0];
+      ev[1] = evn[1];
+    }
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
+
+// Vectorised variant for even nx (all BASELINE grids): each lane owns TWO
+// consecutive i (one 16-byte load per vector per plane), a warp spans 64 i; the
+// i-1 / i+1 neighbours come from the adjacent lanes by shuffle (lane 0 / 31
+// load the one value outside the warp), j+-1 through L1. The next plane of x
+// and of the epilogue operands is prefetched one iteration ahead, so each thread
+// keeps 3-4 independent 16-byte HBM loads in flight across the dependent march.
+template <class Epi, bool kRed>
+__global__ void __launch_bounds__(kStencilThreads)
+stencil7v2_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begin, int k_end,
+                  int kz, Reduce red) {
+  const int lane = threadIdx.x;
+  const int i0 = blockIdx.x * 64 + 2 * lane;
+  const int j = blockIdx.y * kStencilBY + threadIdx.y;
+  const int kb = k_begin + blockIdx.z * kz;
+  const int ke = min(kb + kz, k_end);
+  double acc = 0.0;
+  if (j < g.ny && kb < ke) {  // warp-uniform: every lane of the warp runs the march
+    const bool valid = i0 < g.nx;
+    const long long col = (long long)j * g.nx + i0;
+    const long long nxy = g.nxy;
+    const double2 zero2 = make_double2(0.0, 0.0);
+    auto plane = [&](int k) -> double2 {
+      if (!valid) return zero2;
+      if (k < 0) return g.ghost_lo ? ldg2(g.ghost_lo + col) : zero2;
+      if (k >= g.nzl) return g.ghost_hi ? ldg2(g.ghost_hi + col) : zero2;
+      return ldg2(x + (long long)k * nxy + col);
+    };
+    const bool has_s = valid && j > 0, has_n = valid && j < g.ny - 1;
+    const bool edge_w = lane == 0, edge_e = lane == 31;
+    const bool has_w = valid && i0 > 0, has_e = valid && i0 + 2 < g.nx;
+    const double d = g.d;
+    double2 xm = plane(kb - 1);
+    double2 xc = plane(kb);
+    double2 xp = plane(kb + 1);
+    double2 ev[2] = {zero2, zero2};
+    if (valid) epi.ld2((long long)kb * nxy + col, ev);
+    for (int k = kb; k < ke; ++k) {
+      const long long idx = (long long)k * nxy + col;
+      const bool more = k + 1 < ke;
+      const double2 xpp = more ? plane(k + 2) : zero2;
+      double2 evn[2] = {zero2, zero2};
+      if (more && valid) epi.ld2(idx + nxy, evn);
+      const double2 xs = has_s ? ldg2(x + idx - g.nx) : zero2;
+      const double2 xn = has_n ? ldg2(x + idx + g.nx) : zero2;
+      double xw = __shfl_up_sync(0xffffffffu, xc.y, 1);
+      double xe = __shfl_down_sync(0xffffffffu, xc.x, 1);
+      if (edge_w) xw = has_w ? __ldg(x + idx - 1) : 0.0;
+      if (edge_e) xe = has_e ? __ldg(x + idx + 2) : 0.0;
+      const double y0 = stencil_point(d, xm.x, xs.x, xw, xc.x, xc.y, xn.x, xp.x);
+      const double y1 = stencil_point(d, xm.y, xs.y, xc.x, xc.y, xe, xn.y, xp.y);
+      if (valid) {
+        const double c = epi.st2(idx, y0, y1, xc, ev);
+        if (kRed) acc = acc + c;
+      }
+      xm = xc;
+      xc = xp;
+      xp = xpp;
+      ev[0] = evn[0];
+      ev[1] = evn[1];
     }
   }
   if (kRed) block_reduce_finish(acc, red);
@@ -223,8 +360,10 @@ csr_kernel(CsrGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
       __syncthreads();
     }
     if (row < g.n) {
+      double ev[2] = {0.0, 0.0};
+      epi.ld(row, ev);
       const double y = sum * __ldg(g.dvec + row);
-      const double c = epi(row, y, __ldg(x + row));
+      const double c = epi.st(row, y, __ldg(x + row), ev);
       if (kRed) acc = acc + c;
     }
   }

@@ -69,6 +69,7 @@ struct pcgx_operator_s {
   double d = 0.0;
   double *ghost_lo = nullptr, *ghost_hi = nullptr;
   int kz = 16;
+  bool vec2 = false;  // even nx -> stencil7v2_kernel
   // csr
   int *rp = nullptr, *ci = nullptr;
   double *va = nullptr, *dvec = nullptr;
@@ -227,11 +228,16 @@ void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, cons
   if (k_end <= k_begin) return;
   const int kz = std::max(1, std::min(op->kz, k_end - k_begin));
   dim3 block(kStencilBX, kStencilBY, 1);
-  dim3 grid((unsigned)((g.nx + kStencilBX - 1) / kStencilBX),
-            (unsigned)((g.ny + kStencilBY - 1) / kStencilBY),
-            (unsigned)((k_end - k_begin + kz - 1) / kz));
   Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
-  stencil7_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red);
+  const unsigned gy = (unsigned)((g.ny + kStencilBY - 1) / kStencilBY);
+  const unsigned gz = (unsigned)((k_end - k_begin + kz - 1) / kz);
+  if (op->vec2) {  // even nx: two points per lane, 16-byte loads
+    dim3 grid((unsigned)((g.nx + 63) / 64), gy, gz);
+    stencil7v2_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red);
+  } else {
+    dim3 grid((unsigned)((g.nx + kStencilBX - 1) / kStencilBX), gy, gz);
+    stencil7_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red);
+  }
   check_launch();
   count_launch(c);
 }
@@ -990,6 +996,7 @@ pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t
     op->nnz = 7 * op->n_global - 2 * (ny * nz + nx * nz + nx * ny);
     op->d = inv_sqrt_diag > 0.0 ? inv_sqrt_diag : 1.0 / std::sqrt(6.0);
     op->kz = default_kz(c, nx, ny, op->nzl);
+    op->vec2 = (nx % 2 == 0) && env_int("PCGX_STENCIL_SCALAR", 0) == 0;
     try {
       init_stencil_ghosts(c, op);
     } catch (...) {

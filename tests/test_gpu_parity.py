@@ -303,7 +303,7 @@ def test_no_graph_path_identical(P, ctx):
     prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, 10, 1.001))
     rhs = op.apply(P.random_uniform_vector(nx ** 3, SEED))
     x1, r1 = P.pcg_solve(op, rhs, P.SolveOptions(), prec)
-    x2, r2 = P.pcg_solve(op, rhs, P.SolveOptions(flags=P.pcgx.FLAG_NO_GRAPH), prec)
+    x2, r2 = P.pcg_solve(op, rhs, P.SolveOptions(flags=P.FLAG_NO_GRAPH), prec)
     assert np.array_equal(x1, x2) and r1.iters == r2.iters
     assert r1.kernel_launches == r2.kernel_launches
 
