@@ -19,6 +19,10 @@
 
 #include "common.cuh"
 
+#ifndef PCGX_V2_MINB
+#define PCGX_V2_MINB 4
+#endif
+
 namespace pcgx {
 
 // ----------------------------------------------------------------- reduction
@@ -89,10 +93,14 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 __device__ __forceinline__ void st2(double* p, double a, double b) {
   *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 // q = A p ; contribution p_i q_i  (pcg.cpp:72-74)
 struct EpiStore {
   double* out;
+  __device__ __forceinline__ void pf(long long) const {}
   __device__ __forceinline__ void ld(long long, double (&)[2]) const {}
   __device__ __forceinline__ void ld2(long long, double2 (&)[2]) const {}
   __device__ __forceinline__ double st(long long idx, double y, double xc, const double (&)[2]) const {
@@ -110,6 +118,7 @@ struct EpiStore {
 struct EpiResid {
   const double* __restrict__ b;
   double* e;  // may be nullptr (true residual: only the norm is needed)
+  __device__ __forceinline__ void pf(long long idx) const { prefetch_l2(b + idx); }
   __device__ __forceinline__ void ld(long long idx, double (&v)[2]) const { v[0] = __ldg(b + idx); }
   __device__ __forceinline__ void ld2(long long idx, double2 (&v)[2]) const { v[0] = ldg2(b + idx); }
   __device__ __forceinline__ double st(long long idx, double y, double, const double (&v)[2]) const {
@@ -132,6 +141,7 @@ struct EpiResid {
 struct EpiChebFirst {
   double* __restrict__ xout;
   double theta, c1;
+  __device__ __forceinline__ void pf(long long) const {}
   __device__ __forceinline__ void ld(long long, double (&)[2]) const {}
   __device__ __forceinline__ void ld2(long long, double2 (&)[2]) const {}
   __device__ __forceinline__ double f(double y, double xc) const {
@@ -161,6 +171,10 @@ struct EpiChebStep {
   double* out;
   double rk, rk1, c2, c3, theta;
   int xold_from_r;
+  __device__ __forceinline__ void pf(long long idx) const {
+    prefetch_l2(r + idx);
+    if (!xold_from_r) prefetch_l2(xold + idx);
+  }
   __device__ __forceinline__ void ld(long long idx, double (&v)[2]) const {
     v[0] = __ldg(r + idx);
     v[1] = xold_from_r ? 0.0 : xold[idx];
@@ -266,9 +280,9 @@ stencil7_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begi
 // and of the epilogue operands is prefetched one iteration ahead, so each thread
 // keeps 3-4 independent 16-byte HBM loads in flight across the dependent march.
 template <class Epi, bool kRed>
-__global__ void __launch_bounds__(kStencilThreads)
+__global__ void __launch_bounds__(kStencilThreads, PCGX_V2_MINB)
 stencil7v2_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begin, int k_end,
-                  int kz, Reduce red) {
+                  int kz, Reduce red, int pfd) {
   const int lane = threadIdx.x;
   const int i0 = blockIdx.x * 64 + 2 * lane;
   const int j = blockIdx.y * kStencilBY + threadIdx.y;
@@ -301,6 +315,11 @@ stencil7v2_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_be
       const double2 xpp = more ? plane(k + 2) : zero2;
       double2 evn[2] = {zero2, zero2};
       if (more && valid) epi.ld2(idx + nxy, evn);
+      if (pfd > 0 && valid && k + pfd < ke) {  // L2 prefetch pfd planes ahead (no registers)
+        const long long pidx = idx + (long long)pfd * nxy;
+        if (k + pfd + 1 < g.nzl) prefetch_l2(x + pidx + nxy);
+        epi.pf(pidx);
+      }
       const double2 xs = has_s ? ldg2(x + idx - g.nx) : zero2;
       const double2 xn = has_n ? ldg2(x + idx + g.nx) : zero2;
       double xw = __shfl_up_sync(0xffffffffu, xc.y, 1);

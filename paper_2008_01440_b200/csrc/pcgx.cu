@@ -70,6 +70,7 @@ struct pcgx_operator_s {
   double *ghost_lo = nullptr, *ghost_hi = nullptr;
   int kz = 16;
   bool vec2 = false;  // even nx -> stencil7v2_kernel
+  int pfd = 0;        // L2 prefetch distance (planes) of the v2 march
   // csr
   int *rp = nullptr, *ci = nullptr;
   double *va = nullptr, *dvec = nullptr;
@@ -233,7 +234,8 @@ void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, cons
   const unsigned gz = (unsigned)((k_end - k_begin + kz - 1) / kz);
   if (op->vec2) {  // even nx: two points per lane, 16-byte loads
     dim3 grid((unsigned)((g.nx + 63) / 64), gy, gz);
-    stencil7v2_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red);
+    stencil7v2_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red,
+                                                            op->pfd);
   } else {
     dim3 grid((unsigned)((g.nx + kStencilBX - 1) / kStencilBX), gy, gz);
     stencil7_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red);
@@ -997,6 +999,7 @@ pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t
     op->d = inv_sqrt_diag > 0.0 ? inv_sqrt_diag : 1.0 / std::sqrt(6.0);
     op->kz = default_kz(c, nx, ny, op->nzl);
     op->vec2 = (nx % 2 == 0) && env_int("PCGX_STENCIL_SCALAR", 0) == 0;
+    op->pfd = env_int("PCGX_PFD", 2);
     try {
       init_stencil_ghosts(c, op);
     } catch (...) {

@@ -37,7 +37,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpcgx.so")
+LIB_PATH = os.environ.get("PCGX_LIB") or os.path.join(_HERE, "libpcgx.so")
 
 _dp = C.POINTER(C.c_double)
 _i64p = C.POINTER(C.c_int64)
