@@ -1,0 +1,81 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// TEST: the reference-side C++ binding (include/polycg_gpu/adapter.hpp) used
+// exactly as a maintainer would, against the reference library itself
+// (oracle/_ref objects, built from /root/reference/proj/src). Built by
+// `make -C oracle adapter_test`; run by tests/test_adapter.py on a GPU box.
+//
+// For each case the SAME ScaledOperator, rhs and ChebyshevPreconditioner go to
+// polycg::pcg_solve (CPU reference) and polycg::gpu::pcg_solve (B200), and the
+// program prints one JSON line per case with both reports and the solution
+// difference; exit code 0 iff every case meets the parity bar.
+#include <cmath>
+#include <cstdio>
+#include <memory>
+#include <string>
+
+#include "polycg/eigenest.hpp"
+#include "polycg/linop.hpp"
+#include "polycg/pcg.hpp"
+#include "polycg/polyprec.hpp"
+#include "polycg_gpu/adapter.hpp"
+
+using namespace polycg;
+
+static int run_case(const char* tag, const LinearOperator& inner, Index nx, int m, double s,
+                    polycg::gpu::Session& sess) {
+  auto [scaled, inv_sqrt] = jacobi_scale(inner);
+  const auto [a0, b0] = analytic_extremes(StencilKind::lap3d, nx, true);
+  const Vector exact = random_uniform_vector(scaled.size(), 20240801);
+  const Vector b = scaled.apply(exact);
+  SolveOptions opts;
+  ChebyshevPreconditioner p_cpu(cheb_params(a0, b0, m, s));
+  ChebyshevPreconditioner p_gpu(cheb_params(a0, b0, m, s));
+  auto [x_ref, r_ref] = pcg_solve(scaled, b, opts, &p_cpu);
+  polycg::gpu::DeviceOperator dop(sess, scaled);
+  auto [x_gpu, r_gpu] = polycg::gpu::pcg_solve(sess, dop, scaled, b, opts, &p_gpu);
+  double dn = 0.0, xn = 0.0;
+  for (Index i = 0; i < x_ref.size(); ++i) {
+    dn += (x_gpu[i] - x_ref[i]) * (x_gpu[i] - x_ref[i]);
+    xn += x_ref[i] * x_ref[i];
+  }
+  const double rel = std::sqrt(dn / xn);
+  // per-step Chebyshev parity through the adapter (bitwise expected)
+  Vector r0 = random_uniform_vector(scaled.size(), 4242), o_cpu, o_gpu;
+  o_cpu = apply_chebyshev(cheb_params(a0, b0, 7, s), scaled, r0);
+  polycg::gpu::apply_chebyshev(sess, dop, cheb_params(a0, b0, 7, s), r0, o_gpu);
+  bool bitwise = true;
+  for (Index i = 0; i < r0.size(); ++i) bitwise = bitwise && (o_cpu[i] == o_gpu[i]);
+  const bool ok = std::abs(r_gpu.iters - r_ref.iters) <= 1 && rel <= 1e-10 && bitwise &&
+                  r_gpu.ddot == r_ref.ddot && r_gpu.matvec == r_ref.matvec &&
+                  r_gpu.converged == r_ref.converged;
+  std::printf(
+      "{\"case\": \"%s\", \"ok\": %s, \"iters\": [%d, %d], \"ddot\": [%llu, %llu], "
+      "\"matvec\": [%llu, %llu], \"rel_res\": [%.17g, %.17g], \"x_rel_diff\": %.3e, "
+      "\"cheb7_bitwise\": %s, \"wall_time\": [%.6f, %.6f]}\n",
+      tag, ok ? "true" : "false", r_ref.iters, r_gpu.iters, (unsigned long long)r_ref.ddot,
+      (unsigned long long)r_gpu.ddot, (unsigned long long)r_ref.matvec,
+      (unsigned long long)r_gpu.matvec, r_ref.rel_res, r_gpu.rel_res, rel,
+      bitwise ? "true" : "false", r_ref.wall_time, r_gpu.wall_time);
+  return ok ? 0 : 1;
+}
+
+int main() {
+  set_apply_threads(8);
+  polycg::gpu::Session sess(0);
+  int bad = 0;
+  const StencilOperator st40(StencilKind::lap3d, 40);
+  bad += run_case("stencil40_m10", st40, 40, 10, 1.001, sess);
+  const CsrMatrix cs30 = assemble_laplacian(StencilKind::lap3d, 30);
+  bad += run_case("csr30_m20", cs30, 30, 20, 1.001, sess);
+  // error path: a non-Chebyshev preconditioner is rejected like a bad argument
+  try {
+    auto [scaled, d] = jacobi_scale(st40);
+    NewtonPreconditioner np(newton_params(0.1, 1.9, 2, 1.0));
+    polycg::gpu::pcg_solve(scaled, Vector::Ones(scaled.size()), {}, &np);
+    bad += 1;
+  } catch (const std::invalid_argument&) {
+    std::printf("{\"case\": \"reject_newton\", \"ok\": true}\n");
+  }
+  return bad == 0 ? 0 : 1;
+}
