@@ -114,15 +114,24 @@ def dist_env():
 
 
 class Dist:
-    def __init__(self, ws, rank, local):
+    """torch.distributed plumbing: rendezvous, the NCCL unique-id broadcast and
+    max-over-ranks timing. The data path (halo planes, all-reduces) is NCCL
+    inside libpcgx. backend None -> "cpu:gloo,cuda:nccl" on a GPU box, "gloo"
+    without CUDA (the CPU tests drive this class with world_size 2)."""
+
+    def __init__(self, ws, rank, local, backend=None):
         self.ws, self.rank, self.local = ws, rank, local
         self.pg = None
         if ws > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(local)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend="cpu:gloo,cuda:nccl")
+            if backend is None:
+                backend = "cpu:gloo,cuda:nccl" if torch.cuda.is_available() else "gloo"
+            if torch.cuda.is_available():
+                torch.cuda.set_device(local)
+            if not dist.is_initialized():
+                dist.init_process_group(backend=backend, rank=rank, world_size=ws)
             self.dist = dist
             self.torch = torch
 

@@ -73,6 +73,12 @@ pcgx_status pcgx_context_create(int device, pcgx_context* out);
 pcgx_status pcgx_nccl_unique_id(void* id128);
 pcgx_status pcgx_context_create_dist(int device, int nranks, int rank, const void* nccl_id,
                                      pcgx_context* out);
+/* P ranks of a z-slab job inside ONE process (devices[r] per rank, NULL = all
+ * on device 0): halo planes move by stream-ordered copies and scalars are
+ * reduced in rank order; each context must be driven by its own host thread
+ * (every rank calls the same sequence, as with NCCL). Used to exercise the
+ * multi-rank slab path on a single GPU. */
+pcgx_status pcgx_local_group_create(int nranks, const int* devices, pcgx_context* out);
 void pcgx_context_destroy(pcgx_context ctx);
 int pcgx_context_rank(pcgx_context ctx);
 int pcgx_context_nranks(pcgx_context ctx);
@@ -106,6 +112,9 @@ pcgx_status pcgx_flush_l2(pcgx_context ctx, size_t bytes);
  * [pcgx_operator_z0, z0 + nz_local) and every vector is that slab. */
 pcgx_status pcgx_stencil7_create(pcgx_context ctx, int64_t nx, int64_t ny, int64_t nz,
                                  double inv_sqrt_diag, pcgx_operator* out);
+/* The z-slab partition every rank uses (host-only): rank r of P owns planes
+ * [z0, z0 + nz_local), balanced, the first nz % P ranks one plane more. */
+void pcgx_slab_partition(int64_t nz, int nranks, int rank, int64_t* z0, int64_t* nz_local);
 
 /* CsrMatrix (symmetric, both triangles, int64 host arrays as in the reference)
  * Jacobi-scaled. Narrowed to int32 on upload (PCGX_ERR_OVERFLOW if nnz >= 2^31).

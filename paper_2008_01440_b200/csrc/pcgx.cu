@@ -15,6 +15,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -39,6 +41,7 @@ struct pcgx_context_s {
   cudaStream_t s = nullptr;   // compute
   cudaStream_t cs = nullptr;  // halo exchange
   ncclComm_t comm = nullptr;
+  struct CommBase* cm = nullptr;  // nullptr on a single-GPU context
   double* S = nullptr;        // device scalars
   double* hS = nullptr;       // pinned mirror
   double* partials = nullptr;
@@ -201,15 +204,153 @@ int vec_grid(pcgx_context c, long long n) {
   return (int)std::max(1LL, std::min(want, (long long)c->sms * 8));
 }
 
-// ---------------------------------------------------------------- all-reduce
+// ---------------------------------------------------------------- communication
+//
+// CommBase is the only place ranks meet. NcclComm: one process per GPU, NCCL
+// over NVLink/NVSwitch (the production path). LocalGroup: P ranks as P
+// contexts in ONE process (one host thread each, any devices), exchanging halo
+// planes with stream-ordered cudaMemcpyAsync and reducing scalars in rank
+// order; no kernel ever waits on another kernel (dependencies are CUDA events
+// plus a host barrier), so the multi-rank slab logic can be exercised on a
+// single GPU. Both are collective: every rank calls them at the same point.
+
+}  // namespace
+struct CommBase {
+  virtual ~CommBase() = default;
+  virtual void allreduce(pcgx_context c, int slot, int count) = 0;
+  // Start exchanging x's first/last owned plane into the neighbours' ghosts.
+  virtual void halo_begin(pcgx_context c, pcgx_operator op, const double* x) = 0;
+  // Make c->s wait until this rank's ghost planes hold the neighbours' planes.
+  virtual void halo_wait(pcgx_context c) = 0;
+  virtual bool graph_capturable() const = 0;
+};
+namespace {
+
+struct NcclComm : CommBase {
+  void allreduce(pcgx_context c, int slot, int count) override {
+    PCGX_NCCL(nccl().AllReduce(c->S + slot, c->S + slot, count, ncclDouble, ncclSum, c->comm, c->s));
+  }
+  void halo_begin(pcgx_context c, pcgx_operator op, const double* x) override;
+  void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
+  bool graph_capturable() const override { return true; }
+};
+
+class HostBarrier {
+ public:
+  explicit HostBarrier(int n) : n_(n) {}
+  void wait() {
+    std::unique_lock<std::mutex> lk(m_);
+    const long gen = gen_;
+    if (++count_ == n_) {
+      count_ = 0;
+      ++gen_;
+      cv_.notify_all();
+    } else {
+      cv_.wait(lk, [&] { return gen != gen_; });
+    }
+  }
+
+ private:
+  std::mutex m_;
+  std::condition_variable cv_;
+  int n_, count_ = 0;
+  long gen_ = 0;
+};
+
+// rank-ordered sum of the group's contributions into every rank's slots
+__global__ void group_sum_kernel(const double* contrib, int nranks, int slot, int count, double* S) {
+  const int i = threadIdx.x;
+  if (i < count) {
+    double s = 0.0;
+    for (int q = 0; q < nranks; ++q) s += contrib[q * kSlots + slot + i];
+    S[slot + i] = s;
+  }
+}
+
+struct LocalGroup {
+  int nranks;
+  HostBarrier bar;
+  std::vector<pcgx_context> ctx;
+  std::vector<double*> ghost_lo, ghost_hi;
+  std::vector<cudaEvent_t> ev_ar;   // rank's contribution copied
+  std::vector<cudaEvent_t> ev_done; // rank finished reading contributions
+  double* contrib = nullptr;        // nranks * kSlots doubles on the first rank's device
+  std::atomic<int> refs{0};
+  explicit LocalGroup(int n) : nranks(n), bar(n), ctx(n), ghost_lo(n), ghost_hi(n), ev_ar(n), ev_done(n) {}
+};
+
+struct LocalComm : CommBase {
+  std::shared_ptr<LocalGroup> g;
+  int rank;
+  LocalComm(std::shared_ptr<LocalGroup> grp, int r) : g(std::move(grp)), rank(r) {}
+  void allreduce(pcgx_context c, int slot, int count) override {
+    // previous allreduce fully consumed by every rank before contrib is reused
+    for (int q = 0; q < g->nranks; ++q) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ev_done[q], 0));
+    PCGX_CUDA(cudaMemcpyAsync(g->contrib + rank * kSlots + slot, c->S + slot, sizeof(double) * count,
+                              cudaMemcpyDefault, c->s));
+    PCGX_CUDA(cudaEventRecord(g->ev_ar[rank], c->s));
+    g->bar.wait();
+    for (int q = 0; q < g->nranks; ++q) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ev_ar[q], 0));
+    group_sum_kernel<<<1, 32, 0, c->s>>>(g->contrib, g->nranks, slot, count, c->S);
+    check_launch();
+    PCGX_CUDA(cudaEventRecord(g->ev_done[rank], c->s));
+    g->bar.wait();
+  }
+  void halo_begin(pcgx_context c, pcgx_operator op, const double* x) override;
+  void halo_wait(pcgx_context c) override {
+    if (rank > 0) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[rank - 1]->ev_join, 0));
+    if (rank < g->nranks - 1) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[rank + 1]->ev_join, 0));
+  }
+  bool graph_capturable() const override { return false; }
+};
 
 void allreduce(pcgx_context c, int slot, int count) {
-  if (c->nranks == 1) return;
-  PCGX_NCCL(nccl().AllReduce(c->S + slot, c->S + slot, count, ncclDouble, ncclSum, c->comm, c->s));
+  if (c->nranks == 1 || !c->cm) return;
+  c->cm->allreduce(c, slot, count);
   c->cur_allreduce++;
 }
 
 // ---------------------------------------------------------------- operator launch
+
+void NcclComm::halo_begin(pcgx_context c, pcgx_operator op, const double* x) {
+  const long long nxy = op->nx * op->ny;
+  const long long nzl = op->nzl;
+  PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+  PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+  PCGX_NCCL(nccl().GroupStart());
+  if (op->ghost_lo) {
+    PCGX_NCCL(nccl().Send(x, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
+    PCGX_NCCL(nccl().Recv(op->ghost_lo, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
+  }
+  if (op->ghost_hi) {
+    PCGX_NCCL(nccl().Send(x + (nzl - 1) * nxy, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
+    PCGX_NCCL(nccl().Recv(op->ghost_hi, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
+  }
+  PCGX_NCCL(nccl().GroupEnd());
+  PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+}
+
+void LocalComm::halo_begin(pcgx_context c, pcgx_operator op, const double* x) {
+  const long long nxy = op->nx * op->ny;
+  const long long nzl = op->nzl;
+  g->ghost_lo[rank] = op->ghost_lo;
+  g->ghost_hi[rank] = op->ghost_hi;
+  // ev_fork: my x is final AND my previous boundary kernels (ghost readers) are queued before it
+  PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+  g->bar.wait();
+  PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+  const size_t pb = sizeof(double) * (size_t)nxy;
+  if (rank > 0) {  // my first plane -> ghost_hi of rank-1, once rank-1 no longer reads it
+    PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[rank - 1]->ev_fork, 0));
+    PCGX_CUDA(cudaMemcpyAsync(g->ghost_hi[rank - 1], x, pb, cudaMemcpyDefault, c->cs));
+  }
+  if (rank < g->nranks - 1) {  // my last plane -> ghost_lo of rank+1
+    PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[rank + 1]->ev_fork, 0));
+    PCGX_CUDA(cudaMemcpyAsync(g->ghost_lo[rank + 1], x + (nzl - 1) * nxy, pb, cudaMemcpyDefault, c->cs));
+  }
+  PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+  g->bar.wait();  // every rank's ev_join recorded before anyone waits on it
+}
 
 StencilGeom geom_of(pcgx_operator op) {
   StencilGeom g;
@@ -267,22 +408,9 @@ void op_launch(pcgx_context c, pcgx_operator op, const double* x, const Epi& epi
     return;
   }
   // halo: my first plane -> rank-1 (its ghost_hi), my last plane -> rank+1 (its ghost_lo)
+  c->cm->halo_begin(c, op, x);
   const long long nxy = op->nx * op->ny;
-  PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
-  PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
-  PCGX_NCCL(nccl().GroupStart());
-  if (lo_nb) {
-    PCGX_NCCL(nccl().Send(x, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
-    PCGX_NCCL(nccl().Recv(op->ghost_lo, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
-    c->cur_halo_bytes += nxy * 8;
-  }
-  if (hi_nb) {
-    PCGX_NCCL(nccl().Send(x + (nzl - 1) * nxy, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
-    PCGX_NCCL(nccl().Recv(op->ghost_hi, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
-    c->cur_halo_bytes += nxy * 8;
-  }
-  PCGX_NCCL(nccl().GroupEnd());
-  PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+  c->cur_halo_bytes += ((lo_nb ? 1 : 0) + (hi_nb ? 1 : 0)) * nxy * 8;
   // interior planes need no ghost: run them while the halo is in flight
   const int ib = lo_nb ? 1 : 0, ie = hi_nb ? nzl - 1 : nzl;
   StencilGeom gi = g;
@@ -293,7 +421,7 @@ void op_launch(pcgx_context c, pcgx_operator op, const double* x, const Epi& epi
     stencil_launch<Epi, kRed>(c, op, gi, x, epi, ib, ie, slot, false);
     wrote = true;
   }
-  PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0));
+  c->cm->halo_wait(c);
   if (lo_nb) {
     stencil_launch<Epi, kRed>(c, op, g, x, epi, 0, 1, slot, wrote);
     wrote = true;
@@ -469,7 +597,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   const int m = have_prec ? P.m : 0;
   const long long n = op->n_local;
   ensure_workspace(c, n);
-  const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && env_int("PCGX_NO_GRAPH", 0) == 0;
+  const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && env_int("PCGX_NO_GRAPH", 0) == 0 &&
+                         (!c->cm || c->cm->graph_capturable());
   const bool spec_after_update = (c->nranks == 1);
 
   std::memset(rep, 0, sizeof *rep);
@@ -874,8 +1003,35 @@ pcgx_status pcgx_context_create_dist(int device, int nranks, int rank, const voi
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof id);
       PCGX_NCCL(nccl().CommInitRank(&c->comm, nranks, id, rank));
+      c->cm = new NcclComm();
     }
     *out = c.release();
+  });
+}
+
+pcgx_status pcgx_local_group_create(int nranks, const int* devices, pcgx_context* out) {
+  return guarded(nullptr, [&] {
+    if (nranks < 1 || !out) fail(PCGX_ERR_INVALID, "local_group_create: bad nranks");
+    auto grp = std::make_shared<LocalGroup>(nranks);
+    std::vector<std::unique_ptr<pcgx_context_s>> made;
+    for (int r = 0; r < nranks; ++r) {
+      auto c = std::make_unique<pcgx_context_s>();
+      c->device = devices ? devices[r] : 0;
+      c->rank = r;
+      c->nranks = nranks;
+      ctx_init(c.get());
+      PCGX_CUDA(cudaEventCreateWithFlags(&grp->ev_ar[r], cudaEventDisableTiming));
+      PCGX_CUDA(cudaEventCreateWithFlags(&grp->ev_done[r], cudaEventDisableTiming));
+      grp->ctx[r] = c.get();
+      made.push_back(std::move(c));
+    }
+    PCGX_CUDA(cudaSetDevice(grp->ctx[0]->device));
+    PCGX_CUDA(cudaMalloc(&grp->contrib, sizeof(double) * kSlots * nranks));
+    PCGX_CUDA(cudaMemset(grp->contrib, 0, sizeof(double) * kSlots * nranks));
+    for (int r = 0; r < nranks; ++r) {
+      made[r]->cm = new LocalComm(grp, r);
+      out[r] = made[r].release();
+    }
   });
 }
 
@@ -884,6 +1040,7 @@ void pcgx_context_destroy(pcgx_context c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->s);
   if (c->comm) nccl().CommDestroy(c->comm);
+  delete c->cm;
   double* bufs[] = {c->r, c->z, c->p, c->q, c->w0, c->w1, c->t0, c->t1, c->flush, c->S, c->partials};
   for (double* b : bufs)
     if (b) cudaFree(b);
@@ -975,6 +1132,13 @@ pcgx_status pcgx_flush_l2(pcgx_context c, size_t bytes) {
   });
 }
 
+// balanced z-slabs: the first (nz % P) ranks own one extra plane
+void pcgx_slab_partition(int64_t nz, int nranks, int rank, int64_t* z0, int64_t* nz_local) {
+  const int64_t base = nz / nranks, extra = nz % nranks;
+  *nz_local = base + (rank < extra ? 1 : 0);
+  *z0 = rank * base + std::min<int64_t>(rank, extra);
+}
+
 pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t nz,
                                  double inv_sqrt_diag, pcgx_operator* out) {
   return guarded(c, [&] {
@@ -989,10 +1153,10 @@ pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t
     op->nx = nx;
     op->ny = ny;
     op->nz = nz;
-    // balanced z-slabs: the first (nz % P) ranks own one extra plane
-    const long long base = nz / c->nranks, extra = nz % c->nranks;
-    op->nzl = base + (c->rank < extra ? 1 : 0);
-    op->z0 = c->rank * base + std::min<long long>(c->rank, extra);
+    int64_t z0 = 0, nzl = 0;
+    pcgx_slab_partition(nz, c->nranks, c->rank, &z0, &nzl);
+    op->nzl = nzl;
+    op->z0 = z0;
     op->n_global = nx * ny * nz;
     op->n_local = nx * ny * op->nzl;
     op->nnz = 7 * op->n_global - 2 * (ny * nz + nx * nz + nx * ny);

@@ -103,11 +103,11 @@ FLAG_NO_GRAPH = 2
 # Exported symbols of include/pcgx.h (tests check the .so exports all of them).
 SYMBOLS = [
     "pcgx_abi_version", "pcgx_last_error", "pcgx_context_create", "pcgx_nccl_unique_id",
-    "pcgx_context_create_dist", "pcgx_context_destroy", "pcgx_context_rank",
+    "pcgx_context_create_dist", "pcgx_local_group_create", "pcgx_context_destroy", "pcgx_context_rank",
     "pcgx_context_nranks", "pcgx_synchronize", "pcgx_kernel_launches", "pcgx_device_alloc",
     "pcgx_device_free", "pcgx_memcpy_h2d", "pcgx_memcpy_d2h", "pcgx_memcpy_d2d",
     "pcgx_host_alloc", "pcgx_host_free", "pcgx_timer_start", "pcgx_timer_stop",
-    "pcgx_flush_l2", "pcgx_stencil7_create", "pcgx_csr_create", "pcgx_csr_create_i32",
+    "pcgx_flush_l2", "pcgx_stencil7_create", "pcgx_slab_partition", "pcgx_csr_create", "pcgx_csr_create_i32",
     "pcgx_operator_destroy", "pcgx_operator_size", "pcgx_operator_local_size",
     "pcgx_operator_z0", "pcgx_operator_nnz", "pcgx_operator_matvec_count",
     "pcgx_operator_apply", "pcgx_operator_apply_device", "pcgx_cheb_params", "pcgx_cheb_eval",
@@ -148,6 +148,7 @@ def lib():
         "pcgx_nccl_unique_id": (C.c_int, [C.c_void_p]),
         "pcgx_context_create_dist": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p,
                                                C.POINTER(ctx)]),
+        "pcgx_local_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(ctx)]),
         "pcgx_context_destroy": (None, [ctx]),
         "pcgx_context_rank": (C.c_int, [ctx]),
         "pcgx_context_nranks": (C.c_int, [ctx]),
@@ -168,6 +169,7 @@ def lib():
         "pcgx_csr_create": (C.c_int, [ctx, C.c_int64, _i64p, _i64p, _dp, _dp, C.POINTER(op)]),
         "pcgx_csr_create_i32": (C.c_int, [ctx, C.c_int64, _i32p, _i32p, _dp, _dp,
                                           C.POINTER(op)]),
+        "pcgx_slab_partition": (None, [C.c_int64, C.c_int, C.c_int, _i64p, _i64p]),
         "pcgx_operator_destroy": (None, [op]),
         "pcgx_operator_size": (C.c_int64, [op]),
         "pcgx_operator_local_size": (C.c_int64, [op]),
@@ -225,10 +227,13 @@ class Context:
     one-Preconditioner-per-solve ownership rule (pcg.hpp:16-19): a context runs
     one call at a time."""
 
-    def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, nccl_id=None):
+    def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, nccl_id=None,
+                 _handle=None):
         L = lib()
         h = C.c_void_p()
-        if nranks == 1:
+        if _handle is not None:
+            h = _handle
+        elif nranks == 1:
             _check(L.pcgx_context_create(device, C.byref(h)))
         else:
             buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -236,6 +241,14 @@ class Context:
         self.h = h
         self.device = device
         self._children = weakref.WeakSet()  # operators / vectors to release before the context
+
+    @classmethod
+    def local_group(cls, nranks: int, devices=None):
+        """P z-slab ranks in this process (drive each from its own thread)."""
+        hs = (C.c_void_p * nranks)()
+        devs = None if devices is None else (C.c_int * nranks)(*devices)
+        _check(lib().pcgx_local_group_create(nranks, devs, hs))
+        return [cls(devices[r] if devices else 0, _handle=C.c_void_p(hs[r])) for r in range(nranks)]
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -619,6 +632,13 @@ def random_uniform_vector(n, seed, offset=0, ctx: Context | None = None):
     v = DeviceVector(ctx, n)
     _check(lib().pcgx_random_uniform_device(ctx.h, int(n), seed, offset, v.ptr), ctx.h)
     return v
+
+
+def slab_partition(nz, nranks, rank):
+    """(z0, nz_local) of rank's z-slab (the partition every pcgx rank uses)."""
+    z0, nl = C.c_int64(), C.c_int64()
+    lib().pcgx_slab_partition(nz, nranks, rank, C.byref(z0), C.byref(nl))
+    return z0.value, nl.value
 
 
 def analytic_extremes(dim, nx, scaled=True):

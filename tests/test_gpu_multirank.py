@@ -1,0 +1,93 @@
+# SPDX-License-Identifier: Apache-2.0
+"""The multi-rank z-slab path on ONE GPU: P ranks as P contexts of a
+pcgx_local_group (one host thread each; halo planes by stream-ordered copies,
+scalars reduced in rank order). Everything but the NCCL calls themselves runs:
+slab partition, ghost planes, interior/boundary split with accumulated
+reductions, merged [r'r, r'z] all-reduce, per-rank RNG offsets.
+
+Elementwise work is exact, so SpMV and every Chebyshev step must be BITWISE equal
+to the single-domain oracle; the solve must match within the PCG parity bar."""
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleOp
+from tests._util import rel_norm
+
+pytestmark = pytest.mark.gpu
+SEED = 20240801
+
+
+def run_ranks(P, fn):
+    with ThreadPoolExecutor(max_workers=len(P)) as ex:
+        futs = [ex.submit(fn, r, c) for r, c in enumerate(P)]
+        return [f.result(timeout=600) for f in futs]
+
+
+@pytest.mark.parametrize("nranks,dims,m", [(2, (24, 24, 24), 10), (3, (20, 16, 26), 5),
+                                           (4, (32, 32, 30), 20), (4, (30, 30, 4), 3)])
+def test_slab_solve_matches_single_domain(pcgx, oracle, nranks, dims, m):
+    P = pcgx
+    nx, ny, nz = dims
+    ctxs = P.Context.local_group(nranks)
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+    opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
+    xt_full = oracle.random_uniform(nx * ny * nz, SEED)
+    b_full = oracle.apply(opo, xt_full)
+    prm_o = oracle.cheb_params(a, b, m, 1.001)
+    x_full, rep_o = oracle.pcg_solve(opo, prm_o, b_full)
+    r_full = oracle.random_uniform(nx * ny * nz, 77)
+    z_full = oracle.apply_chebyshev(opo, prm_o, r_full)
+
+    def rank(r, ctx):
+        op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
+        z0 = op.z0()
+        nl = op.local_size()
+        assert (z0, nl // (nx * ny)) == P.slab_partition(nz, nranks, r)
+        lo, hi = z0 * nx * ny, z0 * nx * ny + nl
+        xt = P.random_uniform_vector(nl, SEED, offset=lo)
+        bl = op.apply(xt)                                  # halo exchange inside
+        zl = P.apply_chebyshev(P.cheb_params(a, b, m, 1.001), op, r_full[lo:hi])
+        x, rep = P.pcg_solve(op, bl, P.SolveOptions(),
+                             P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001)))
+        return lo, hi, bl, zl, x, rep
+
+    outs = run_ranks(ctxs, rank)
+    b_g = np.concatenate([o[2] for o in outs])
+    z_g = np.concatenate([o[3] for o in outs])
+    x_g = np.concatenate([o[4] for o in outs])
+    assert np.array_equal(b_g, b_full)          # SpMV across slabs: bitwise
+    assert np.array_equal(z_g, z_full)          # P_m(A) r across slabs: bitwise
+    reps = [o[5] for o in outs]
+    assert all(r.iters == reps[0].iters for r in reps)
+    assert abs(reps[0].iters - rep_o["iters"]) <= 1
+    assert reps[0].converged
+    if reps[0].iters == rep_o["iters"]:
+        assert rel_norm(x_g, x_full) <= 1e-10
+    assert reps[0].ddot == rep_o["ddot"] and reps[0].matvec == rep_o["matvec"]
+    # two all-reduces per iteration (+ setup/exit ones), halos on every SpMV
+    assert reps[0].allreduces <= 2 * reps[0].iters + 4
+    assert all(r.halo_bytes > 0 for r in reps)
+    for c in ctxs:
+        c.close()
+
+
+def test_slab_lanczos_matches_single_domain(pcgx):
+    P = pcgx
+    nx, nz = 20, 22
+    single = P.Context(0)
+    op1, _ = P.jacobi_scale(P.StencilOperator(nx, nx, nz), single)
+    lo1, hi1 = P.lanczos_bounds(op1, 20, 30, SEED)
+    ctxs = P.Context.local_group(2)
+
+    def rank(r, ctx):
+        op, _ = P.jacobi_scale(P.StencilOperator(nx, nx, nz), ctx)
+        return P.lanczos_bounds(op, 20, 30, SEED)
+
+    res = run_ranks(ctxs, rank)
+    for lo, hi in res:
+        assert lo == pytest.approx(lo1, rel=1e-9) and hi == pytest.approx(hi1, rel=1e-9)
+    for c in ctxs:
+        c.close()
+    single.close()
