@@ -25,6 +25,7 @@
 #include <string>
 #include <vector>
 
+#include "cheb2.cuh"
 #include "common.cuh"
 #include "host_math.hpp"
 #include "kernels.cuh"
@@ -54,7 +55,7 @@ struct pcgx_context_s {
   // workspace (device), sized for the largest operator used
   long long ws_n = 0;
   double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *w0 = nullptr, *w1 = nullptr,
-         *t0 = nullptr, *t1 = nullptr;
+         *w2 = nullptr, *w3 = nullptr, *t0 = nullptr, *t1 = nullptr;
   double* flush = nullptr;
   size_t flush_bytes = 0;
   // solve-local bookkeeping
@@ -74,6 +75,10 @@ struct pcgx_operator_s {
   int kz = 16;
   bool vec2 = false;  // even nx -> stencil7v2_kernel
   int pfd = 0;        // L2 prefetch distance (planes) of the v2 march
+  bool cheb2 = false; // two Chebyshev steps per pass (stencil7_cheb2_kernel, TMA)
+  int kz2 = 32;       // z-chunk of the two-step kernel
+  struct TmaPair { const double* ptr; CUtensorMap a, e; };
+  std::vector<TmaPair> tmaps;  // per-buffer tensor maps (A box 68x12, B/R box 68x10)
   // csr
   int *rp = nullptr, *ci = nullptr;
   double *va = nullptr, *dvec = nullptr;
@@ -189,7 +194,7 @@ void check_launch() {
 
 void ensure_workspace(pcgx_context c, long long n) {
   if (c->ws_n >= n) return;
-  double** bufs[] = {&c->r, &c->z, &c->p, &c->q, &c->w0, &c->w1, &c->t0, &c->t1};
+  double** bufs[] = {&c->r, &c->z, &c->p, &c->q, &c->w0, &c->w1, &c->w2, &c->w3, &c->t0, &c->t1};
   for (double** b : bufs) {
     if (*b) cudaFree(*b);
     *b = nullptr;
@@ -478,6 +483,66 @@ void fetch_scalars(pcgx_context c) {
   PCGX_CUDA(cudaStreamSynchronize(c->s));
 }
 
+// ---------------------------------------------------------------- TMA tensor maps
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  if (!fn) fail(PCGX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map(pcgx_operator op, const double* ptr, int bx, int by) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {(cuuint64_t)op->nx, (cuuint64_t)op->ny, (cuuint64_t)op->nzl};
+  const cuuint64_t strides[2] = {(cuuint64_t)op->nx * 8, (cuuint64_t)(op->nx * op->ny) * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr),
+                                    dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(PCGX_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+const pcgx_operator_s::TmaPair& tmaps_for(pcgx_operator op, const double* ptr) {
+  for (auto& t : op->tmaps)
+    if (t.ptr == ptr) return t;
+  op->tmaps.push_back({ptr, make_map(op, ptr, kC2AX, kC2AY), make_map(op, ptr, kC2BX, kC2BY)});
+  return op->tmaps.back();
+}
+
+template <bool kFirst, bool kRed>
+void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const double* B,
+                  const double* R, const Cheb2Params& prm, int slot) {
+  PCGX_CUDA(cudaFuncSetAttribute(stencil7_cheb2_kernel<kFirst, kRed>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2Smem));
+  // copies: a later tmaps_for() may grow the cache and move its elements
+  const CUtensorMap ma = tmaps_for(op, A).a;
+  const CUtensorMap mb = tmaps_for(op, B ? B : A).e;
+  const CUtensorMap mr = tmaps_for(op, R).e;
+  const int kz = std::max(1, std::min(op->kz2, (int)op->nzl));
+  dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
+            (unsigned)((op->nzl + kz - 1) / kz));
+  Reduce red = kRed ? make_red(c, slot) : Reduce{};
+  stencil7_cheb2_kernel<kFirst, kRed><<<grid, kC2Threads, kC2Smem, c->s>>>(ma, mb, mr, prm, kz, red);
+  check_launch();
+  count_launch(c);
+  op->matvecs.fetch_add(2, std::memory_order_relaxed);
+}
+
 // ---------------------------------------------------------------- Chebyshev apply
 
 struct Cheb {
@@ -514,6 +579,52 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
     EpiChebFirst e{out, P.theta, c1};
     if (rz_slot >= 0) op_launch<EpiChebFirst, true>(c, op, r, e, rz_slot);
     else op_launch<EpiChebFirst, false>(c, op, r, e, -1);
+    return;
+  }
+  if (op->kind == 0 && op->cheb2) {
+    // two steps per pass: (1,2), (3,4), ...; an odd last step runs single-step
+    Cheb2Params q{};
+    q.nx = (int)op->nx;
+    q.ny = (int)op->ny;
+    q.nzl = (int)op->nzl;
+    q.nxy = op->nx * op->ny;
+    q.d = op->d;
+    q.theta = P.theta;
+    q.c1 = c1;
+    q.c2 = c2;
+    q.c3 = c3;
+    double* bufs[4] = {c->w0, c->w1, c->w2, c->w3};
+    const bool last12 = (P.m == 2);
+    q.rk2 = P.rho[2];
+    q.rk2m1 = P.rho[1];
+    q.outC = bufs[0];
+    q.outE = last12 ? out : bufs[1];
+    if (last12 && rz_slot >= 0) cheb2_launch<true, true>(c, op, r, nullptr, r, q, rz_slot);
+    else cheb2_launch<true, false>(c, op, r, nullptr, r, q, -1);
+    if (last12) return;
+    int iold = 0, icur = 1;  // x_{k-2}, x_{k-1} buffer indices
+    int k = 3;
+    for (; k + 1 <= P.m; k += 2) {
+      const bool last = (k + 1 == P.m);
+      int fc = -1, fe = -1;
+      for (int b = 0; b < 4; ++b)
+        if (b != iold && b != icur) (fc < 0 ? fc : fe) = b;
+      q.rk1 = P.rho[k];
+      q.rk1m1 = P.rho[k - 1];
+      q.rk2 = P.rho[k + 1];
+      q.rk2m1 = P.rho[k];
+      q.outC = bufs[fc];
+      q.outE = last ? out : bufs[fe];
+      if (last && rz_slot >= 0) cheb2_launch<false, true>(c, op, bufs[icur], bufs[iold], r, q, rz_slot);
+      else cheb2_launch<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1);
+      iold = fc;
+      icur = fe;
+    }
+    if (k == P.m) {  // odd remainder: x_m = step(x_{m-1}, x_{m-2}) -> out
+      EpiChebStep e{r, bufs[iold], out, P.rho[k], P.rho[k - 1], c2, c3, P.theta, 0};
+      if (rz_slot >= 0) op_launch<EpiChebStep, true>(c, op, bufs[icur], e, rz_slot);
+      else op_launch<EpiChebStep, false>(c, op, bufs[icur], e, -1);
+    }
     return;
   }
   EpiChebFirst e1{c->w1, P.theta, c1};
@@ -1041,7 +1152,7 @@ void pcgx_context_destroy(pcgx_context c) {
   cudaStreamSynchronize(c->s);
   if (c->comm) nccl().CommDestroy(c->comm);
   delete c->cm;
-  double* bufs[] = {c->r, c->z, c->p, c->q, c->w0, c->w1, c->t0, c->t1, c->flush, c->S, c->partials};
+  double* bufs[] = {c->r, c->z, c->p, c->q, c->w0, c->w1, c->w2, c->w3, c->t0, c->t1, c->flush, c->S, c->partials};
   for (double* b : bufs)
     if (b) cudaFree(b);
   cudaFree(c->counter);
@@ -1164,6 +1275,8 @@ pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t
     op->kz = default_kz(c, nx, ny, op->nzl);
     op->vec2 = (nx % 2 == 0) && env_int("PCGX_STENCIL_SCALAR", 0) == 0;
     op->pfd = env_int("PCGX_PFD", 2);
+    op->cheb2 = op->vec2 && c->nranks == 1 && env_int("PCGX_CHEB2", 0) != 0;
+    op->kz2 = env_int("PCGX_KZ2", 32);
     try {
       init_stencil_ghosts(c, op);
     } catch (...) {
