@@ -243,7 +243,7 @@ def run_gpu(args):
     _, rprof = P.pcg_solve(op, b, P.SolveOptions(tol=TOL, maxit=100000,
                                                  flags=P.pcgx.FLAG_TIME_KERNELS), precs[kbig], x_out=x)
     step_ms = D.max(rprof.step_ms / max(rprof.step_launches, 1))
-    step_bytes = 32.0 * n_loc
+    step_bytes = rprof.step_bytes
     peak, peak_kind = peaks()
     achieved = step_bytes / (step_ms * 1e-3) / 1e9
 
@@ -300,7 +300,9 @@ def run_gpu(args):
         "time_to_1e8_s": {str(k): round(t, 6) for k, _, t in reps},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "stencil7_kernel<EpiChebStep> (fused SpMV + Chebyshev step)",
+                     "kernel": ("stencil7_cheb2_kernel (TMA, two fused SpMV + Chebyshev steps "
+                                "per pass, 40 B/unknown)" if step_bytes == 40.0 * n_loc else
+                                "stencil7v2_kernel<EpiChebStep> (fused SpMV + Chebyshev step, 32 B/unknown)"),
                      "bytes_per_launch": step_bytes, "avg_launch_ms": round(step_ms, 5),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
                      "frac_of_8TBs_spec": round(achieved / 8000.0, 4)},

@@ -11,11 +11,10 @@
 // uses x_old = x_0 = r/theta.
 //
 // One CTA owns a 64 x 8 (i x j) output tile and marches a z-chunk. Per plane it
-// TMA-loads A with a 2-deep halo (68 x 12 box), B and R with a 1-deep halo
-// (66 x 10); out-of-domain box elements arrive zero-filled, which is exactly the
-// homogeneous Dirichlet boundary. (B and R use 68 x 10 boxes from i0-2.) Stage 1 computes C on the 66 x 10 extended
-// tile (the halo redundantly) into a 3-plane shared ring; stage 2 reads C from
-// there. HBM traffic per point per TWO steps: read A, B, R + write C, E = 40 B
+// TMA-loads A with a 2-deep j halo (68 x 12 box), B and R with a 1-deep one
+// (68 x 10); out-of-domain box elements arrive zero-filled (the homogeneous
+// Dirichlet boundary). Stage 1 computes C on the 66 x 10 extended tile (the halo
+// redundantly) into a 3-plane shared ring; stage 2 reads C from there. HBM traffic per point per TWO steps: read A, B, R + write C, E = 40 B
 // (vs 64 B for two single-step passes); halo re-reads are served by L2.
 // Loads run D = 3 planes ahead through a ring of mbarriers; one elected thread
 // issues them. Per-point arithmetic is the single-step kernel's (bitwise parity).
@@ -27,22 +26,25 @@
 
 namespace pcgx {
 
-constexpr int kC2TX = 64, kC2TY = 8;                 // output tile
-constexpr int kC2AX = kC2TX + 4, kC2AY = kC2TY + 4;  // A box (2-halo)
-constexpr int kC2EX = kC2TX + 2, kC2EY = kC2TY + 2;  // extended tile (1-halo)
-// B and R boxes start at i0-2 (not i0-1): the innermost TMA box coordinate must
-// be 16-byte aligned, i.e. even for fp64 (tools/tma_probe: odd -> illegal instruction).
-constexpr int kC2BX = kC2TX + 4, kC2BY = kC2TY + 2;
+constexpr int kC2TX = 64, kC2TY = 8;                 // output tile (i x j)
+constexpr int kC2W = kC2TX + 4;                      // row width of every smem plane (tile-i t <-> col t+2)
+constexpr int kC2AY = kC2TY + 4;                     // A box rows (2-halo in j)
+constexpr int kC2BY = kC2TY + 2;                     // B, R boxes and the C ring: 1-halo rows
+// Every TMA box starts at i0-2: the innermost box coordinate must be 16-byte
+// aligned, i.e. even for fp64 (tools/tma_probe: an odd origin is an illegal
+// instruction on sm_100a). A box 68 x 12 (6528 B), B/R boxes 68 x 10 (5440 B).
+constexpr int kC2AX = kC2W, kC2BX = kC2W;
 constexpr int kC2D = 3;                              // prefetch distance (planes)
 constexpr int kC2NA = kC2D + 2, kC2NB = kC2D, kC2NR = kC2D + 1, kC2NC = 3;
-constexpr int kC2APlane = kC2AX * kC2AY;             // doubles (6528 B = 51 x 128 B)
-constexpr int kC2EPlane = kC2EX * kC2EY;             // doubles used per extended plane
-constexpr int kC2EStride = 688;                      // slot stride: 5504 B = 43 x 128 B (TMA dst alignment)
-constexpr int kC2BPlane = kC2BX * kC2BY;             // doubles loaded per B / R plane (5440 B)
-constexpr int kC2Threads = 256;
-constexpr size_t kC2Smem =
-    sizeof(double) * (size_t)(kC2NA * kC2APlane + (kC2NB + kC2NR + kC2NC) * kC2EStride) +
-    16 * (kC2D + 1) + 128;
+constexpr int kC2APlane = kC2W * kC2AY;              // 816 doubles = 51 x 128 B
+constexpr int kC2BPlane = kC2W * kC2BY;              // 680 doubles
+constexpr int kC2EStride = 688;                      // B/R slot stride: 5504 B = 43 x 128 B (TMA dst alignment)
+constexpr int kC2CStride = kC2BPlane;                // C ring slot (plain shared stores)
+constexpr int kC2Warps = kC2TY + 2;                  // one warp per extended row in stage 1
+constexpr int kC2Threads = 32 * kC2Warps;            // 320
+constexpr size_t kC2Smem = sizeof(double) * (size_t)(kC2NA * kC2APlane + (kC2NB + kC2NR) * kC2EStride +
+                                                     kC2NC * kC2CStride) +
+                           16 * (kC2D + 1) + 128;
 
 struct Cheb2Params {
   int nx, ny, nzl;          // local grid
@@ -88,7 +90,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// grid: (ceil(nx/64), ceil(ny/8), ceil(nzl/kz)); block: 256 threads; dynamic smem kC2Smem.
+// grid: (ceil(nx/64), ceil(ny/8), ceil(nzl/kz)); block: 320 threads; dynamic smem kC2Smem.
+//
+// Stage 1: warp w owns extended row w (tile row w-1); lane l owns the point
+// pair tile-i (2l, 2l+1). Stage 2: warp w < 8 owns tile row w, lane l the pair
+// (2l, 2l+1); meanwhile warps 8 and 9 compute the two halo columns (tile-i -1
+// and 64) of C for the plane stage 1 just produced (they are first read by
+// stage 2 one iteration later). The k-1 / k+1 neighbours of the pairs live in
+// per-lane register queues, i-1 / i+1 come by shuffle, only j-1 / j+1 and the
+// operands are read from shared memory (16-byte LDS). Ring slots rotate by
+// one per plane and are tracked with incremented indices (no modulo).
 template <bool kFirst, bool kRed>
 __global__ void __launch_bounds__(kC2Threads, 2)
 stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 box)
@@ -96,19 +107,18 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
                       const __grid_constant__ CUtensorMap mapR,  // R (68 x 10 box)
                       Cheb2Params p, int kz, Reduce red) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sA = reinterpret_cast<double*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // 128-byte aligned base, kept as a shared-space pointer (LDS, not generic LD)
+  double* sA = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   double* sB = sA + kC2NA * kC2APlane;
   double* sR = sB + kC2NB * kC2EStride;
   double* sC = sR + kC2NR * kC2EStride;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kC2NC * kC2EStride);  // kC2D unit bars + 1 prologue
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kC2NC * kC2CStride);  // kC2D unit bars + 1 prologue
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = blockIdx.x * kC2TX, j0 = blockIdx.y * kC2TY;
   const int kb = blockIdx.z * kz;
   const int ke = min(kb + kz, p.nzl);
-  const unsigned bytesA = kC2APlane * 8, bytesE = kC2BPlane * 8;
-  const unsigned unit_bytes = kFirst ? bytesA : bytesA + 2 * bytesE;
+  const unsigned bytesA = kC2APlane * 8, bytesB = kC2BPlane * 8;
 
   if (tid == 0) {
     for (int q = 0; q <= kC2D; ++q) mbar_init(&bars[q], 1);
@@ -116,16 +126,14 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
   }
   __syncthreads();
 
-  // load unit u (stage-1 plane u): A[u+1], B[u], R[u]. Planes outside [0, nzl)
-  // are never loaded (a box lying wholly outside the tensor faults on sm_100a
-  // instead of zero-filling); their few readers substitute 0 = Dirichlet.
+  // Load unit u (stage-1 plane u): A[u+1], B[u], R[u]. Planes outside [0, nzl)
+  // are never loaded (their readers substitute 0 = Dirichlet).
   auto in_z = [&](int z) { return z >= 0 && z < p.nzl; };
   auto issue_unit = [&](int u) {
     uint64_t* bar = &bars[(u - (kb - 1)) % kC2D];
     const bool la = in_z(u + 1), lbr = !kFirst && in_z(u);
-    mbar_expect_tx(bar, (la ? bytesA : 0u) + (lbr ? 2 * bytesE : 0u));
-    if (la)
-      tma_load_3d(sA + ((u + 1 - (kb - 2)) % kC2NA) * kC2APlane, &mapA, i0 - 2, j0 - 2, u + 1, bar);
+    mbar_expect_tx(bar, (la ? bytesA : 0u) + (lbr ? 2 * bytesB : 0u));
+    if (la) tma_load_3d(sA + ((u + 1 - (kb - 2)) % kC2NA) * kC2APlane, &mapA, i0 - 2, j0 - 2, u + 1, bar);
     if (lbr) {
       tma_load_3d(sB + ((u - (kb - 1)) % kC2NB) * kC2EStride, &mapB, i0 - 2, j0 - 1, u, bar);
       tma_load_3d(sR + ((u - (kb - 1)) % kC2NR) * kC2EStride, &mapR, i0 - 2, j0 - 1, u, bar);
@@ -135,84 +143,140 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
   if (tid == 0) {
     uint64_t* pb = &bars[kC2D];
     mbar_expect_tx(pb, (in_z(kb - 2) ? bytesA : 0u) + (in_z(kb - 1) ? bytesA : 0u));
-    if (in_z(kb - 2)) tma_load_3d(sA + 0 * kC2APlane, &mapA, i0 - 2, j0 - 2, kb - 2, pb);
-    if (in_z(kb - 1)) tma_load_3d(sA + 1 * kC2APlane, &mapA, i0 - 2, j0 - 2, kb - 1, pb);
+    if (in_z(kb - 2)) tma_load_3d(sA, &mapA, i0 - 2, j0 - 2, kb - 2, pb);
+    if (in_z(kb - 1)) tma_load_3d(sA + kC2APlane, &mapA, i0 - 2, j0 - 2, kb - 1, pb);
     for (int u = kb - 1; u < kb - 1 + kC2D && u <= u_last; ++u) issue_unit(u);
   }
   mbar_wait(&bars[kC2D], 0);
 
   const double d = p.d;
+  const double2 zero2 = make_double2(0.0, 0.0);
+  const int col = 2 * lane + 2;                    // smem column of the lane's pair
+  const int gi = i0 + 2 * lane;                    // global i of the pair's first point
+  const bool pair_in = gi < p.nx;                  // nx even: both points or none
+  // stage 1 (extended row `warp`)
+  const int gj1 = j0 - 1 + warp;
+  const bool row1_in = gj1 >= 0 && gj1 < p.ny;
+  const bool do1 = row1_in && pair_in;
+  const int offA1 = (warp + 1) * kC2W + col;       // A-box offset of the pair
+  const int offB1 = warp * kC2W + col;             // B/R/C offset of the pair
+  const bool c_interior = warp >= 1 && warp <= kC2TY;
+  double* gC = p.outC + (long long)gj1 * p.nx + gi;  // + u * nxy
+  // stage 2 (tile row `warp` for warps 0..7)
+  const bool stage2 = warp < kC2TY;
+  const int gj2 = j0 + warp;
+  const bool do2 = stage2 && gj2 < p.ny && pair_in;
+  const int offC2 = (warp + 1) * kC2W + col;
+  const int offA2 = (warp + 2) * kC2W + col;
+  double* gE = p.outE + (long long)gj2 * p.nx + gi;  // + v * nxy
+  // halo columns (warps 8, 9, lanes 0..9): column tile-i -1 (warp 8) or 64 (warp 9)
+  const bool do_h = warp >= kC2TY && lane < kC2BY;
+  const int hcol = warp == kC2TY ? 1 : kC2TX + 2;
+  const int hgi = warp == kC2TY ? i0 - 1 : i0 + kC2TX;
+  const int hgj = j0 - 1 + lane;
+  const bool h_in = do_h && hgi >= 0 && hgi < p.nx && hgj >= 0 && hgj < p.ny;
+  const int offAh = (lane + 1) * kC2W + hcol, offBh = lane * kC2W + hcol;
+
+  // ring slot indices of plane u (A: u-(kb-2), B/R: u-(kb-1), C: u), advanced by one per plane
+  int sa = 1;                         // slot of A[u] at u = kb-1
+  int sb = 0, sr = 0;                 // slots of B[u], R[u]
+  int sc = (((kb - 1) % kC2NC) + kC2NC) % kC2NC;  // slot of C[u]
+  auto wrap_inc = [](int x, int n) { return x + 1 == n ? 0 : x + 1; };
+  auto wrap_dec = [](int x, int n) { return x == 0 ? n - 1 : x - 1; };
+
+  double2 am = in_z(kb - 2) ? *reinterpret_cast<const double2*>(sA + offA1) : zero2;
+  double2 ac = in_z(kb - 1) ? *reinterpret_cast<const double2*>(sA + kC2APlane + offA1) : zero2;
+  double2 cm = zero2, cc = zero2;     // stage-2 C centres of planes v-1, v
   double acc = 0.0;
+
   for (int u = kb - 1; u <= u_last; ++u) {
     const int ui = u - (kb - 1);
     mbar_wait(&bars[ui % kC2D], (ui / kC2D) & 1);
-    // ---------------- stage 1: C[u] on the 66 x 10 extended tile
-    const double* Am = sA + ((u - 1 - (kb - 2)) % kC2NA) * kC2APlane;
-    const double* Ac = sA + ((u - (kb - 2)) % kC2NA) * kC2APlane;
-    const double* Ap = sA + ((u + 1 - (kb - 2)) % kC2NA) * kC2APlane;
-    const double* Bs = sB + (ui % kC2NB) * kC2EStride;
-    const double* Rs = sR + (ui % kC2NR) * kC2EStride;
-    double* Cs = sC + (((u % kC2NC) + kC2NC) % kC2NC) * kC2EStride;
-    const bool write_c = (u >= kb) && (u < ke);  // halo planes belong to the neighbouring chunks
-    const bool plane_in = (u >= 0) && (u < p.nzl);
-    const bool has_m = u - 1 >= 0, has_p = u + 1 < p.nzl;
-    for (int e = tid; e < kC2EPlane; e += kC2Threads) {
-      const int ii = e % kC2EX, jj = e / kC2EX;
-      const int gi = i0 - 1 + ii, gj = j0 - 1 + jj;
-      double cval = 0.0;
-      if (plane_in && gi >= 0 && gi < p.nx && gj >= 0 && gj < p.ny) {
-        const int a = (jj + 1) * kC2AX + (ii + 1);  // centre in A-box coordinates
-        const double xc = Ac[a];
-        const double y = stencil_point(d, has_m ? Am[a] : 0.0, Ac[a - kC2AX], Ac[a - 1], xc,
-                                       Ac[a + 1], Ac[a + kC2AX], has_p ? Ap[a] : 0.0);
+    const double* Au = sA + sa * kC2APlane;
+    const double* Ap = sA + wrap_inc(sa, kC2NA) * kC2APlane;
+    const double* Bu = sB + sb * kC2EStride;
+    const double* Ru = sR + sr * kC2EStride;
+    double* Cu = sC + sc * kC2CStride;
+    const bool plane_in = in_z(u), has_p = in_z(u + 1);
+    // ---------------- stage 1: C[u] pairs of the extended tile
+    {
+      const double2 ap = has_p ? *reinterpret_cast<const double2*>(Ap + offA1) : zero2;
+      double aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
+      double ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
+      if (lane == 0) aw = Au[offA1 - 1];
+      if (lane == 31) ae = Au[offA1 + 2];
+      double2 cv = zero2;
+      if (plane_in && do1) {
+        const double2 as = *reinterpret_cast<const double2*>(Au + offA1 - kC2W);
+        const double2 an = *reinterpret_cast<const double2*>(Au + offA1 + kC2W);
+        const double y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
+        const double y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
         if (kFirst) {
-          cval = p.c1 * ((2.0 * xc) - (y / p.theta));
+          cv.x = p.c1 * ((2.0 * ac.x) - (y0 / p.theta));
+          cv.y = p.c1 * ((2.0 * ac.y) - (y1 / p.theta));
         } else {
-          const int be = jj * kC2BX + ii + 1;  // B/R box coordinates
-          const double ri = Rs[be];
-          const double z = p.c2 * (ri - y);
-          cval = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * Bs[be])) + z);
+          const double2 bb = *reinterpret_cast<const double2*>(Bu + offB1);
+          const double2 rr = *reinterpret_cast<const double2*>(Ru + offB1);
+          cv.x = p.rk1 * (((p.c3 * ac.x) - (p.rk1m1 * bb.x)) + p.c2 * (rr.x - y0));
+          cv.y = p.rk1 * (((p.c3 * ac.y) - (p.rk1m1 * bb.y)) + p.c2 * (rr.y - y1));
         }
-        if (write_c && ii >= 1 && ii <= kC2TX && jj >= 1 && jj <= kC2TY)
-          p.outC[(long long)u * p.nxy + (long long)gj * p.nx + gi] = cval;
+        if (c_interior && u >= kb && u < ke) st2(gC + (long long)u * p.nxy, cv.x, cv.y);
       }
-      Cs[e] = cval;
+      *reinterpret_cast<double2*>(Cu + offB1) = cv;
+      am = ac;
+      ac = ap;
     }
     __syncthreads();
-    // ---------------- stage 2: E[u-1] on the 64 x 8 tile
-    const int v = u - 1;
-    if (v >= kb) {
-      const double* Cm = sC + ((((v - 1) % kC2NC) + kC2NC) % kC2NC) * kC2EStride;
-      const double* Cc = sC + (((v % kC2NC) + kC2NC) % kC2NC) * kC2EStride;
-      const double* Cp = Cs;
-      const double* Aold = sA + ((v - (kb - 2)) % kC2NA) * kC2APlane;    // A[v]
-      const double* Rv = sR + ((v - (kb - 1)) % kC2NR) * kC2EStride;     // R[v]
-      for (int e = tid; e < kC2TX * kC2TY; e += kC2Threads) {
-        const int ii = e % kC2TX, jj = e / kC2TX;
-        const int gi = i0 + ii, gj = j0 + jj;
-        if (gi < p.nx && gj < p.ny) {
-          const int c = (jj + 1) * kC2EX + (ii + 1);  // centre in extended-tile coordinates
-          const double xc = Cc[c];
-          const double y = stencil_point(d, Cm[c], Cc[c - kC2EX], Cc[c - 1], xc, Cc[c + 1],
-                                         Cc[c + kC2EX], Cp[c]);
-          const int a = (jj + 2) * kC2AX + (ii + 2);
-          double ri, xo;
-          if (kFirst) {
-            ri = Aold[a];            // A == R == r
-            xo = ri / p.theta;       // x_0 = r / theta
-          } else {
-            ri = Rv[(jj + 1) * kC2BX + ii + 2];
-            xo = Aold[a];            // x_{k-1}
-          }
-          const double z = p.c2 * (ri - y);
-          const double xn = p.rk2 * (((p.c3 * xc) - (p.rk2m1 * xo)) + z);
-          p.outE[(long long)v * p.nxy + (long long)gj * p.nx + gi] = xn;
-          if (kRed) acc = acc + ri * xn;
+    // ---------------- stage 2: E[u-1] on the tile (warps 0..7) | halo columns of C[u] (warps 8, 9)
+    if (stage2) {
+      const int v = u - 1;
+      const double2 cp = *reinterpret_cast<const double2*>(Cu + offC2);
+      const double* Cv = sC + wrap_dec(sc, kC2NC) * kC2CStride;
+      double cw = __shfl_up_sync(0xffffffffu, cc.y, 1);
+      double ce = __shfl_down_sync(0xffffffffu, cc.x, 1);
+      if (lane == 0) cw = Cv[offC2 - 1];
+      if (lane == 31) ce = Cv[offC2 + 2];
+      if (v >= kb && do2) {
+        const double2 cs = *reinterpret_cast<const double2*>(Cv + offC2 - kC2W);
+        const double2 cn = *reinterpret_cast<const double2*>(Cv + offC2 + kC2W);
+        const double y0 = stencil_point(d, cm.x, cs.x, cw, cc.x, cc.y, cn.x, cp.x);
+        const double y1 = stencil_point(d, cm.y, cs.y, cc.x, cc.y, ce, cn.y, cp.y);
+        const double* Av = sA + wrap_dec(sa, kC2NA) * kC2APlane;  // A[v] = A[u-1]
+        const double2 av = *reinterpret_cast<const double2*>(Av + offA2);
+        double2 rv, xo;
+        if (kFirst) {
+          rv = av;  // A == R == r
+          xo = make_double2(av.x / p.theta, av.y / p.theta);  // x_0 = r / theta
+        } else {
+          rv = *reinterpret_cast<const double2*>(sR + wrap_dec(sr, kC2NR) * kC2EStride + offC2);
+          xo = av;  // x_{k-1}
         }
+        const double e0 = p.rk2 * (((p.c3 * cc.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
+        const double e1 = p.rk2 * (((p.c3 * cc.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
+        st2(gE + (long long)v * p.nxy, e0, e1);
+        if (kRed) acc = acc + (rv.x * e0 + rv.y * e1);
       }
+      cm = cc;
+      cc = cp;
+    } else if (do_h) {
+      double cx = 0.0;
+      if (plane_in && h_in) {
+        const double* Am = sA + wrap_dec(sa, kC2NA) * kC2APlane;
+        const double xc = Au[offAh];
+        const double y = stencil_point(d, in_z(u - 1) ? Am[offAh] : 0.0, Au[offAh - kC2W],
+                                       Au[offAh - 1], xc, Au[offAh + 1], Au[offAh + kC2W],
+                                       has_p ? Ap[offAh] : 0.0);
+        if (kFirst) cx = p.c1 * ((2.0 * xc) - (y / p.theta));
+        else cx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * Bu[offBh])) + p.c2 * (Ru[offBh] - y));
+      }
+      Cu[offBh] = cx;
     }
     __syncthreads();
     if (tid == 0 && u + kC2D <= u_last) issue_unit(u + kC2D);
+    sa = wrap_inc(sa, kC2NA);
+    sb = wrap_inc(sb, kC2NB);
+    sr = wrap_inc(sr, kC2NR);
+    sc = wrap_inc(sc, kC2NC);
   }
   if (kRed) block_reduce_finish(acc, red);
 }

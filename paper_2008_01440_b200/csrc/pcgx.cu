@@ -740,6 +740,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
     if (m == 0) return 2 * N8;
     const double spmv_extra = spmv_equiv_bytes(op) - 2 * N8;  // matrix bytes (CSR)
     if (m == 1) return spmv_extra + 2 * N8;
+    if (op->kind == 0 && op->cheb2)  // (1,2): read r, write x1 x2; pairs: 3 reads 2 writes; odd tail: 4
+      return 3 * N8 + (double)((m - 2) / 2) * 5 * N8 + ((m % 2) ? 4 * N8 : 0.0);
     return (spmv_extra + 2 * N8) + (spmv_extra + 3 * N8) + (double)(m - 2) * (spmv_extra + 4 * N8);
   };
 
@@ -893,24 +895,46 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   rep->alg_bytes = alg;
   rep->step_bytes = cheb_step_bytes(op);
 
-  // Optional: time the dominant kernel (the fused middle Chebyshev step) with
-  // CUDA events on the compute stream, on this solve's operator and buffers.
-  if ((opts.flags & PCGX_FLAG_TIME_KERNELS) && have_prec && m >= 3) {
+  // Optional: time the dominant kernel with CUDA events on the compute stream, on
+  // this solve's operator and buffers: the two-step pass (stencil, cheb2) or the
+  // fused single middle step.
+  if ((opts.flags & PCGX_FLAG_TIME_KERNELS) && have_prec && m >= 4) {
     const int reps = std::max(3, env_int("PCGX_STEP_REPS", 20));
-    EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0};
-    op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);  // warm
-    op->matvecs.fetch_sub(1);
-    PCGX_CUDA(cudaEventRecord(c->ev_t0, c->s));
-    for (int i = 0; i < reps; ++i) {
-      op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);
-      op->matvecs.fetch_sub(1);
+    const bool two = (op->kind == 0 && op->cheb2);
+    Cheb2Params q{};
+    if (two) {
+      q.nx = (int)op->nx;
+      q.ny = (int)op->ny;
+      q.nzl = (int)op->nzl;
+      q.nxy = op->nx * op->ny;
+      q.d = op->d;
+      q.theta = P.theta;
+      q.c2 = 2.0 / P.delta;
+      q.c3 = 2.0 * P.sigma;
+      q.rk1 = P.rho[3];
+      q.rk1m1 = P.rho[2];
+      q.rk2 = P.rho[4];
+      q.rk2m1 = P.rho[3];
+      q.outC = c->w2;
+      q.outE = c->w3;
     }
+    EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0};
+    auto launch = [&] {
+      if (two) cheb2_launch<false, false>(c, op, c->w1, c->w0, r, q, -1);
+      else op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);
+    };
+    const uint64_t mv0 = op->matvecs.load();
+    launch();  // warm
+    PCGX_CUDA(cudaEventRecord(c->ev_t0, c->s));
+    for (int i = 0; i < reps; ++i) launch();
     PCGX_CUDA(cudaEventRecord(c->ev_t1, c->s));
     PCGX_CUDA(cudaEventSynchronize(c->ev_t1));
+    op->matvecs.store(mv0);
     float ms = 0.f;
     PCGX_CUDA(cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1));
     rep->step_ms = ms;
     rep->step_launches = reps;
+    rep->step_bytes = two ? 40.0 * (double)op->n_local : cheb_step_bytes(op);
   }
 }
 
@@ -1275,7 +1299,7 @@ pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t
     op->kz = default_kz(c, nx, ny, op->nzl);
     op->vec2 = (nx % 2 == 0) && env_int("PCGX_STENCIL_SCALAR", 0) == 0;
     op->pfd = env_int("PCGX_PFD", 2);
-    op->cheb2 = op->vec2 && c->nranks == 1 && env_int("PCGX_CHEB2", 0) != 0;
+    op->cheb2 = op->vec2 && c->nranks == 1 && env_int("PCGX_CHEB2", 1) != 0;
     op->kz2 = env_int("PCGX_KZ2", 32);
     try {
       init_stencil_ghosts(c, op);
