@@ -168,14 +168,69 @@ class Dist:
 # ----------------------------------------------------------------- workloads
 
 def workload(config, ws):
-    """(dims, degrees, description) per config; dims = global (nx, ny, nz)."""
+    """(kind, dims, degrees, description) per BASELINE.json config; dims = global grid."""
     if config == "cfg2":
-        return (320, 320, 320 * ws), SWEEP, "7-pt matrix-free 320^3 per GPU, degree sweep"
+        return "stencil", (320, 320, 320 * ws), SWEEP, "7-pt matrix-free 320^3 per GPU, degree sweep"
     if config == "cfg5s":
-        return (640, 640, 640), [40], "7-pt matrix-free 640^3 strong scaling, k=40"
+        return "stencil", (640, 640, 640), [40], "7-pt matrix-free 640^3 strong scaling, k=40"
     if config == "cfg5w":
-        return (512, 512, 512 * ws), [40], "7-pt matrix-free 512x512x(512P) weak scaling, k=40"
-    raise SystemExit(f"unknown stencil config {config}")
+        return "stencil", (512, 512, 512 * ws), [40], "7-pt matrix-free 512x512x(512P) weak scaling, k=40"
+    if config == "cfg1":
+        return "lap_csr", (100, 100, 100), [20], "7-pt assembled CSR (int32) 100^3, k=20"
+    if config == "cfg3":
+        return "fe27", (256, 256, 256), [40], ("27-pt Q1 FE heterogeneous diffusion 256^3, lognormal "
+                                              "sigma=1, Lanczos bounds, k=40")
+    if config == "cfg4":
+        return "elast27", (160, 160, 160), [30], ("3-dof Q1 elasticity 160^3 (3x3 blocks, 27 nodes), "
+                                                 "Lanczos bounds, k=30")
+    raise SystemExit(f"unknown config {config}")
+
+
+def lap3d_csr_i32(nx):
+    """assemble_laplacian(lap3d, nx) (proj/src/linop.cpp:299-331) as int32 CSR."""
+    n = nx ** 3
+    nxy = nx * nx
+    r = np.arange(n, dtype=np.int64)
+    i, j, k = r % nx, (r // nx) % nx, r // nxy
+    ones = np.ones(n, bool)
+    mask = np.stack([k > 0, j > 0, i > 0, ones, i < nx - 1, j < nx - 1, k < nx - 1], axis=1)
+    offs = np.array([-nxy, -nx, -1, 0, 1, nx, nxy])
+    vals = np.array([-1.0, -1.0, -1.0, 6.0, -1.0, -1.0, -1.0])
+    rp = np.zeros(n + 1, dtype=np.int32)
+    rp[1:] = np.cumsum(mask.sum(1))
+    ci = (r[:, None] + offs[None, :])[mask].astype(np.int32)
+    va = np.broadcast_to(vals, (n, 7))[mask].astype(np.float64)
+    return rp, ci, va
+
+
+def build_operator(P, ctx, kind, dims):
+    """-> (op, alpha, beta, bytes_per_spmv_equiv (global), bounds_desc)"""
+    nx, ny, nz = dims
+    if kind == "stencil":
+        op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
+        if nx == ny == nz:
+            a, b = P.analytic_extremes(3, nx)
+        else:
+            a, b = P.analytic_extremes_box(nx, ny, nz)
+        return op, a, b, 16.0 * op.size(), "analytic"
+    if kind == "lap_csr":
+        rp, ci, va = lap3d_csr_i32(nx)
+        A = P.CsrMatrix(nx ** 3, rp, ci, va)
+        a, b = P.analytic_extremes(3, nx)
+        bounds = "analytic"
+    elif kind == "fe27":
+        A = P.gen_fe27(nx, sigma=1.0, seed=SEED)
+        bounds = "lanczos"
+    elif kind == "elast27":
+        A = P.gen_elast27(nx, 1.0, 0.5, 0.1, seed=SEED)
+        bounds = "lanczos"
+    op, _ = P.jacobi_scale(A, ctx)
+    nnz, n = A.nnz(), A.n
+    del A
+    if bounds == "lanczos":
+        a, b = P.lanczos_bounds(op, 20, 30, SEED)  # lambda_max: 20 steps, lambda_min: 30 steps
+    # SpMV-equivalent bytes (int32 CSR): 12 nnz + 4 (n+1) + 16 n
+    return op, a, b, 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n, bounds
 
 
 def run_gpu(args):
@@ -192,17 +247,18 @@ def run_gpu(args):
         ctx = P.Context(local, nranks=ws, rank=rank, nccl_id=nid)
     else:
         ctx = P.Context(0)
-    (nx, ny, nz), degrees, desc = workload(args.config, ws)
+    kind, (nx, ny, nz), degrees, desc = workload(args.config, ws)
     if args.degrees:
         degrees = [int(v) for v in args.degrees.split(",")]
-    op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
+    if kind != "stencil" and ws > 1:
+        raise SystemExit("multi-GPU CSR is not built yet (SURVEY 8f.1); CSR configs run on 1 GPU")
+    t_setup = time.perf_counter()
+    op, alpha, beta, spmv_bytes, bounds = build_operator(P, ctx, kind, (nx, ny, nz))
+    t_setup = time.perf_counter() - t_setup
     n_loc = op.local_size()
     n_glob = op.size()
-    if nx == ny == nz:
-        alpha, beta = P.analytic_extremes(3, nx)
-    else:
-        alpha, beta = P.analytic_extremes_box(nx, ny, nz)
-    xt = P.random_uniform_vector(n_loc, SEED, offset=op.z0() * nx * ny, ctx=ctx)
+    xt = P.random_uniform_vector(n_loc, SEED, offset=(op.z0() * nx * ny if kind == "stencil" else 0),
+                                 ctx=ctx)
     b = op.apply(xt)
     x = P.DeviceVector(ctx, n_loc)
     precs = {k: P.ChebyshevPreconditioner(P.cheb_params(alpha, beta, k, SCALE)) for k in degrees}
@@ -234,12 +290,14 @@ def run_gpu(args):
             mvs.append(mv)
     launches = ctx.kernel_launches - l0
     clocks = clk.summary()
-    spmv_bytes = 16.0 * n_glob
     t_step = float(np.mean(times))
     value = float(np.mean(mvs)) * spmv_bytes / t_step / 1e9
 
     # dominant kernel: fused Chebyshev middle step, CUDA-event timed on the compute stream
     kbig = max(k for k in degrees)
+    if kbig < 4:
+        kbig = 20
+        precs[kbig] = P.ChebyshevPreconditioner(P.cheb_params(alpha, beta, kbig, SCALE))
     _, rprof = P.pcg_solve(op, b, P.SolveOptions(tol=TOL, maxit=100000,
                                                  flags=P.pcgx.FLAG_TIME_KERNELS), precs[kbig], x_out=x)
     step_ms = D.max(rprof.step_ms / max(rprof.step_launches, 1))
@@ -284,7 +342,7 @@ def run_gpu(args):
             traffic = td.get("dram_bytes_per_launch")
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.config == "cfg2":
         cpu = cpu_baseline_sample()
 
     line = {
@@ -294,13 +352,18 @@ def run_gpu(args):
         "data": "synthetic (seeded x_true ~ U(-1,1), b = A x_true)",
         "config": {"workload": args.config, "desc": desc, "grid": [nx, ny, nz],
                    "n_global": n_glob, "degrees": degrees, "theta_scale": SCALE, "tol": TOL,
-                   "bounds": "analytic", "parallelism": f"z-slab x{ws}",
-                   "l2": "inputs larger than L2 (262 MB vectors vs 126 MB L2); no flush"},
+                   "bounds": bounds, "alpha": alpha, "beta": beta,
+                   "parallelism": f"z-slab x{ws}", "setup_s": round(t_setup, 2),
+                   "spmv_equiv_bytes": spmv_bytes,
+                   "l2": ("inputs larger than L2 (126 MB); no flush" if 8 * n_glob > 126e6 else
+                          "vectors L2-resident (8 MB at 100^3): L2-bound, not an HBM roofline claim")},
         "per_k": per_k,
         "time_to_1e8_s": {str(k): round(t, 6) for k, _, t in reps},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": ("stencil7_cheb2_kernel (TMA, two fused SpMV + Chebyshev steps "
+                     "kernel": ("csr_kernel<EpiChebStep> (fused int32 CSR SpMV + Chebyshev step, "
+                                "12 nnz + 4(n+1) + 40 n bytes)" if kind != "stencil" else
+                                "stencil7_cheb2_kernel (TMA, two fused SpMV + Chebyshev steps "
                                 "per pass, 40 B/unknown)" if step_bytes == 40.0 * n_loc else
                                 "stencil7v2_kernel<EpiChebStep> (fused SpMV + Chebyshev step, 32 B/unknown)"),
                      "bytes_per_launch": step_bytes, "avg_launch_ms": round(step_ms, 5),
@@ -410,7 +473,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="pcgx", choices=["pcgx", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg5s", "cfg5w"])
+    ap.add_argument("--config", default="cfg2",
+                    choices=["cfg2", "cfg5s", "cfg5w", "cfg1", "cfg3", "cfg4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--degrees", default=None, help="override the degree list (profiling)")
     args = ap.parse_args()
