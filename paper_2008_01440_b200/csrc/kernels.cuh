@@ -365,13 +365,38 @@ csr_kernel(CsrGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
       mb = __ldg(g.row_ptr + row);
       me = __ldg(g.row_ptr + row + 1);
     }
+    // the row's own epilogue operands are independent of the chunk loop: issue them first
+    double ev[2] = {0.0, 0.0};
+    double xr = 0.0, dr = 0.0;
+    if (row < g.n) {
+      epi.ld(row, ev);
+      xr = __ldg(x + row);
+      dr = __ldg(g.dvec + row);
+    }
     double sum = 0.0;
+    constexpr int kPer = kCsrChunk / kCsrRows;  // products per thread per chunk
     for (int c0 = nz0; c0 < nz1; c0 += kCsrChunk) {
       const int c1 = min(c0 + kCsrChunk, nz1);
-#pragma unroll 4
-      for (int k = c0 + threadIdx.x; k < c1; k += kCsrRows) {
-        const int c = __ldg(g.col_idx + k);
-        prod[k - c0] = __ldg(g.values + k) * (__ldg(g.dvec + c) * __ldg(x + c));
+      // all index/value loads of the chunk first, then all gathers, then the
+      // products: two dependent memory round trips per chunk, kPer-way MLP each
+      int cidx[kPer];
+      double val[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int k = c0 + threadIdx.x + q * kCsrRows;
+        cidx[q] = k < c1 ? __ldg(g.col_idx + k) : 0;
+        val[q] = k < c1 ? __ldg(g.values + k) : 0.0;
+      }
+      double dx[kPer], xx[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        dx[q] = __ldg(g.dvec + cidx[q]);
+        xx[q] = __ldg(x + cidx[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int k = c0 + threadIdx.x + q * kCsrRows;
+        if (k < c1) prod[k - c0] = val[q] * (dx[q] * xx[q]);
       }
       __syncthreads();
       const int lo = max(mb, c0), hi = min(me, c1);
@@ -379,10 +404,212 @@ csr_kernel(CsrGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
       __syncthreads();
     }
     if (row < g.n) {
-      double ev[2] = {0.0, 0.0};
+      const double y = sum * dr;
+      const double c = epi.st(row, y, xr, ev);
+      if (kRed) acc = acc + c;
+    }
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
+
+// ----------------------------------------------------------------- CSR, TMA-pipelined
+
+// Tiles of <= kCsr2Rows consecutive rows whose nnz fit kCsr2Nnz (host-built
+// table). A persistent CTA double-buffers tiles: one elected thread bulk-copies
+// (cp.async.bulk, TMA) the next tile's values and column indices into shared
+// memory while the CTA works on the current one; each row-thread then sums
+// va[k] * (d[c] * x[c]) over its row sequentially in column order
+// (linop.cpp:183-185 -> bitwise rows), with the gathers issued in batches, and
+// runs the epilogue.
+constexpr int kCsr2Rows = 128;
+constexpr int kCsr2Nnz = 3072;                 // nnz budget per tile
+constexpr int kCsr2Buf = kCsr2Nnz + 8;         // + alignment slack (copies start at k & ~3)
+constexpr int kCsr2Batch = 8;
+constexpr size_t kCsr2Smem = 2 * ((size_t)kCsr2Buf * 8 + (size_t)kCsr2Buf * 4) + 2 * 8 + 128;
+
+struct Csr2Geom {
+  int n;
+  int ntiles;
+  const int* tile_row;   // ntiles + 1
+  const int* row_ptr;
+  const int* col_idx;    // padded by >= 8 entries
+  const double* values;  // padded by >= 8 entries
+  const double* dvec;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init2(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(b)))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx2(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(b))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait2(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra W_%=;\n}\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(b))),
+      "r"(parity)
+      : "memory");
+}
+
+template <class Epi, bool kRed>
+__global__ void __launch_bounds__(kCsr2Rows, 2)
+csr2_kernel(Csr2Geom g, const double* __restrict__ x, Epi epi, Reduce red) {
+  extern __shared__ __align__(128) unsigned char smem2[];
+  unsigned char* base = smem2 + ((128u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem2)) & 127u)) & 127u);
+  // stage st: values at base + st * kCsr2Buf * 8, column indices after both value stages
+  auto sva = [&](int st) { return reinterpret_cast<double*>(base + (size_t)st * kCsr2Buf * 8); };
+  auto sci = [&](int st) {
+    return reinterpret_cast<int*>(base + 2 * (size_t)kCsr2Buf * 8 + (size_t)st * kCsr2Buf * 4);
+  };
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 2 * (size_t)kCsr2Buf * 12);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init2(&bar[0]);
+    mbar_init2(&bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int t, int st) {
+    const int r0 = __ldg(g.tile_row + t), r1 = __ldg(g.tile_row + t + 1);
+    const int k0 = __ldg(g.row_ptr + r0) & ~3, k1 = __ldg(g.row_ptr + r1);
+    const int len = (k1 - k0 + 3) & ~3;  // multiple of 4 entries: 16-byte multiple for both arrays
+    mbar_arrive_tx2(&bar[st], (unsigned)len * 12u);
+    bulk_g2s(sva(st), g.values + k0, (unsigned)len * 8u, &bar[st]);
+    bulk_g2s(sci(st), g.col_idx + k0, (unsigned)len * 4u, &bar[st]);
+  };
+  double acc = 0.0;
+  int it = 0;
+  if (tid == 0 && (int)blockIdx.x < g.ntiles) issue(blockIdx.x, 0);
+  for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++it) {
+    const int st = it & 1;
+    if (tid == 0 && t + (int)gridDim.x < g.ntiles) issue(t + gridDim.x, st ^ 1);
+    const int r0 = __ldg(g.tile_row + t), r1 = __ldg(g.tile_row + t + 1);
+    const int nz0 = __ldg(g.row_ptr + r0), nz1 = __ldg(g.row_ptr + r1);
+    const int kb = nz0 & ~3;
+    const int row = r0 + tid;
+    // the row's own operands first (independent of the tile data)
+    double ev[2] = {0.0, 0.0};
+    double xr = 0.0, dr = 0.0;
+    int mb = 0, me = 0;
+    if (row < r1) {
       epi.ld(row, ev);
-      const double y = sum * __ldg(g.dvec + row);
-      const double c = epi.st(row, y, __ldg(x + row), ev);
+      xr = __ldg(x + row);
+      dr = __ldg(g.dvec + row);
+      mb = __ldg(g.row_ptr + row);
+      me = __ldg(g.row_ptr + row + 1);
+    }
+    mbar_wait2(&bar[st], (unsigned)(it >> 1) & 1u);
+    const double* va = sva(st) - kb;  // index by global k
+    const int* ci = sci(st) - kb;
+    // each row-thread walks its own row in column order: column indices and
+    // values from shared memory, the x / d gathers in batches (coalesced across
+    // the warp for stencil-structured rows), the sum strictly sequential
+    if (row < r1) {
+      double sum = 0.0;
+      for (int k = mb; k < me; k += kCsr2Batch) {
+        double dxv[kCsr2Batch], xv[kCsr2Batch], vv[kCsr2Batch];
+#pragma unroll
+        for (int q = 0; q < kCsr2Batch; ++q) {
+          const int kk = k + q;
+          const int c = kk < me ? ci[kk] : 0;
+          vv[q] = kk < me ? va[kk] : 0.0;
+          dxv[q] = __ldg(g.dvec + c);
+          xv[q] = __ldg(x + c);
+        }
+#pragma unroll
+        for (int q = 0; q < kCsr2Batch; ++q)
+          if (k + q < me) sum = sum + vv[q] * (dxv[q] * xv[q]);
+      }
+      const double y = sum * dr;
+      const double cst = epi.st(row, y, xr, ev);
+      if (kRed) acc = acc + cst;
+    }
+    __syncthreads();  // stage st free for reuse
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
+
+// ----------------------------------------------------------------- SELL-32 (sliced ELLPACK)
+
+// The CSR matrix re-laid out at upload as slices of 32 rows (one warp): within
+// slice s, entry k of lane (= row) l lives at slice_ptr[s] + 32 k + l, rows
+// shorter than the slice's longest are padded. A thread owns one row and walks
+// it in column order (k ascending = the reference's CSR order, linop.cpp:183-185),
+// so each row's sum is bitwise the reference's; every value / index load is a
+// coalesced 256 B / 128 B warp access, the x and d gathers are coalesced for
+// stencil-structured rows, and padded slots are skipped by predicate (never
+// added: a +0 product could flip a -0 sum).
+struct SellGeom {
+  int n;
+  int nslices;
+  const long long* slice_ptr;  // nslices + 1 (entries)
+  const int* rowlen;           // n
+  const int* col;              // padded
+  const double* val;           // padded
+  const double* dvec;
+};
+
+#ifndef PCGX_SELL_BATCH
+#define PCGX_SELL_BATCH 8
+#endif
+#ifndef PCGX_SELL_MINB
+#define PCGX_SELL_MINB 4
+#endif
+constexpr int kSellBatch = PCGX_SELL_BATCH;
+
+template <class Epi, bool kRed>
+__global__ void __launch_bounds__(256, PCGX_SELL_MINB)
+sell_kernel(SellGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  double acc = 0.0;
+  for (int s = blockIdx.x * wpb + (threadIdx.x >> 5); s < g.nslices; s += gridDim.x * wpb) {
+    const int row = s * 32 + lane;
+    const long long base = __ldg(g.slice_ptr + s) + lane;
+    const int L = (int)((__ldg(g.slice_ptr + s + 1) - __ldg(g.slice_ptr + s)) >> 5);
+    const bool live = row < g.n;
+    const int len = live ? __ldg(g.rowlen + row) : 0;
+    double ev[2] = {0.0, 0.0};
+    double xr = 0.0, dr = 0.0;
+    if (live) {
+      epi.ld(row, ev);
+      xr = __ldg(x + row);
+      dr = __ldg(g.dvec + row);
+    }
+    double sum = 0.0;
+    for (int k = 0; k < L; k += kSellBatch) {
+      double vv[kSellBatch], dv[kSellBatch], xv[kSellBatch];
+#pragma unroll
+      for (int q = 0; q < kSellBatch; ++q) {
+        const bool on = (k + q) < len;
+        const long long e = base + (long long)(k + q) * 32;
+        const int c = on ? __ldg(g.col + e) : 0;
+        vv[q] = on ? __ldg(g.val + e) : 0.0;
+        dv[q] = on ? __ldg(g.dvec + c) : 0.0;
+        xv[q] = on ? __ldg(x + c) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kSellBatch; ++q)
+        if (k + q < len) sum = sum + vv[q] * (dv[q] * xv[q]);
+    }
+    if (live) {
+      const double y = sum * dr;
+      const double c = epi.st(row, y, xr, ev);
       if (kRed) acc = acc + c;
     }
   }

@@ -80,6 +80,15 @@ struct pcgx_operator_s {
   struct TmaPair { const double* ptr; CUtensorMap a, e; };
   std::vector<TmaPair> tmaps;  // per-buffer tensor maps (A box 68x12, B/R box 68x10)
   // csr
+  int* tile_row = nullptr;  // csr2 tiles (ntiles + 1), nullptr -> csr_kernel
+  // SELL-32 layout (sell_kernel, the default CSR path)
+  long long* sell_ptr = nullptr;
+  int* sell_len = nullptr;
+  int* sell_col = nullptr;
+  double* sell_val = nullptr;
+  int nslices = 0;
+  long long sell_padded = 0;
+  int ntiles = 0;
   int *rp = nullptr, *ci = nullptr;
   double *va = nullptr, *dvec = nullptr;
   std::atomic<uint64_t> matvecs{0};
@@ -395,6 +404,29 @@ void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, cons
 template <class Epi, bool kRed>
 void op_launch(pcgx_context c, pcgx_operator op, const double* x, const Epi& epi, int slot) {
   op->matvecs.fetch_add(1, std::memory_order_relaxed);
+  if (op->kind == 1 && op->sell_ptr) {
+    SellGeom g{(int)op->n_local, op->nslices, op->sell_ptr, op->sell_len, op->sell_col, op->sell_val,
+               op->dvec};
+    const int wpb = 8;
+    const int want = (op->nslices + wpb - 1) / wpb;
+    const int grid = std::max(1, std::min(want, c->sms * env_int("PCGX_SELL_BPS", 8)));
+    Reduce red = kRed ? make_red(c, slot) : Reduce{};
+    sell_kernel<Epi, kRed><<<grid, 32 * wpb, 0, c->s>>>(g, x, epi, red);
+    check_launch();
+    count_launch(c);
+    return;
+  }
+  if (op->kind == 1 && op->tile_row) {
+    Csr2Geom g{(int)op->n_local, op->ntiles, op->tile_row, op->rp, op->ci, op->va, op->dvec};
+    PCGX_CUDA(cudaFuncSetAttribute(csr2_kernel<Epi, kRed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kCsr2Smem));
+    const int grid = std::max(1, std::min(op->ntiles, c->sms * env_int("PCGX_CSR2_BPS", 2)));
+    Reduce red = kRed ? make_red(c, slot) : Reduce{};
+    csr2_kernel<Epi, kRed><<<grid, kCsr2Rows, kCsr2Smem, c->s>>>(g, x, epi, red);
+    check_launch();
+    count_launch(c);
+    return;
+  }
   if (op->kind == 1) {
     CsrGeom g{(int)op->n_local, op->rp, op->ci, op->va, op->dvec};
     const int nrb = (int)((op->n_local + kCsrRows - 1) / kCsrRows);
@@ -1049,8 +1081,11 @@ void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, c
   op->n_global = op->n_local = n;
   op->nnz = nnz;
   PCGX_CUDA(cudaMalloc(&op->rp, sizeof(int) * (size_t)(n + 1)));
-  PCGX_CUDA(cudaMalloc(&op->ci, sizeof(int) * (size_t)std::max(nnz, 1LL)));
-  PCGX_CUDA(cudaMalloc(&op->va, sizeof(double) * (size_t)std::max(nnz, 1LL)));
+  // +8 entries of padding: the TMA tile copies round their length up to 4 entries
+  PCGX_CUDA(cudaMalloc(&op->ci, sizeof(int) * (size_t)(nnz + 8)));
+  PCGX_CUDA(cudaMalloc(&op->va, sizeof(double) * (size_t)(nnz + 8)));
+  PCGX_CUDA(cudaMemset(op->ci, 0, sizeof(int) * (size_t)(nnz + 8)));
+  PCGX_CUDA(cudaMemset(op->va, 0, sizeof(double) * (size_t)(nnz + 8)));
   PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * (size_t)std::max(n, 1LL)));
   PCGX_CUDA(cudaMemcpy(op->rp, rp32.data(), sizeof(int) * (size_t)(n + 1), cudaMemcpyHostToDevice));
   if (nnz) {
@@ -1058,6 +1093,72 @@ void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, c
     PCGX_CUDA(cudaMemcpy(op->va, va, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice));
   }
   if (n) PCGX_CUDA(cudaMemcpy(op->dvec, dv.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice));
+  const int ckern = env_int("PCGX_CSR_KERNEL", 0);  // 0 sell (default), 1 tma tiles, 2 chunked
+  if (ckern == 0 && n > 0) {
+    const long long ns = (n + 31) / 32;
+    std::vector<long long> sp((size_t)ns + 1, 0);
+    std::vector<int> rl((size_t)n);
+    for (long long sI = 0; sI < ns; ++sI) {
+      int L = 0;
+      for (long long r = sI * 32; r < std::min(n, sI * 32 + 32); ++r) {
+        rl[(size_t)r] = rp32[(size_t)r + 1] - rp32[(size_t)r];
+        L = std::max(L, rl[(size_t)r]);
+      }
+      sp[(size_t)sI + 1] = sp[(size_t)sI] + 32LL * L;
+    }
+    const long long tot = sp[(size_t)ns];
+    std::vector<int> scol((size_t)tot, 0);
+    std::vector<double> sval((size_t)tot, 0.0);
+#pragma omp parallel for schedule(static)
+    for (long long sI = 0; sI < ns; ++sI)
+      for (long long r = sI * 32; r < std::min(n, sI * 32 + 32); ++r) {
+        const long long lane = r - sI * 32;
+        for (int k = 0; k < rl[(size_t)r]; ++k) {
+          const long long src = rp32[(size_t)r] + k;
+          const long long dst = sp[(size_t)sI] + 32LL * k + lane;
+          scol[(size_t)dst] = ci32[(size_t)src];
+          sval[(size_t)dst] = va[src];
+        }
+      }
+    op->nslices = (int)ns;
+    PCGX_CUDA(cudaMalloc(&op->sell_ptr, sizeof(long long) * sp.size()));
+    PCGX_CUDA(cudaMalloc(&op->sell_len, sizeof(int) * (size_t)n));
+    PCGX_CUDA(cudaMalloc(&op->sell_col, sizeof(int) * (size_t)std::max(tot, 1LL)));
+    PCGX_CUDA(cudaMalloc(&op->sell_val, sizeof(double) * (size_t)std::max(tot, 1LL)));
+    PCGX_CUDA(cudaMemcpy(op->sell_ptr, sp.data(), sizeof(long long) * sp.size(), cudaMemcpyHostToDevice));
+    PCGX_CUDA(cudaMemcpy(op->sell_len, rl.data(), sizeof(int) * (size_t)n, cudaMemcpyHostToDevice));
+    if (tot) {
+      PCGX_CUDA(cudaMemcpy(op->sell_col, scol.data(), sizeof(int) * (size_t)tot, cudaMemcpyHostToDevice));
+      PCGX_CUDA(cudaMemcpy(op->sell_val, sval.data(), sizeof(double) * (size_t)tot, cudaMemcpyHostToDevice));
+    }
+    op->sell_padded = tot;
+    // the SELL copy replaces the CSR value/index arrays on the device
+    cudaFree(op->ci);
+    cudaFree(op->va);
+    op->ci = nullptr;
+    op->va = nullptr;
+  }
+  // csr2 tiles: greedy, <= kCsr2Rows rows and <= kCsr2Nnz nnz (+3 alignment) each
+  if (ckern == 1 && n > 0) {
+    std::vector<int> tiles{0};
+    bool ok = true;
+    long long r = 0;
+    while (r < n) {
+      const long long start = r;
+      const long long k0 = (long long)rp32[(size_t)start] & ~3LL;
+      while (r < n && r - start < kCsr2Rows && (long long)rp32[(size_t)r + 1] - k0 <= kCsr2Nnz) ++r;
+      if (r == start) {  // one row longer than the tile budget: keep the chunked kernel
+        ok = false;
+        break;
+      }
+      tiles.push_back((int)r);
+    }
+    if (ok) {
+      op->ntiles = (int)tiles.size() - 1;
+      PCGX_CUDA(cudaMalloc(&op->tile_row, sizeof(int) * tiles.size()));
+      PCGX_CUDA(cudaMemcpy(op->tile_row, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice));
+    }
+  }
 }
 
 void free_op(pcgx_operator op) {
@@ -1068,6 +1169,11 @@ void free_op(pcgx_operator op) {
   cudaFree(op->ci);
   cudaFree(op->va);
   cudaFree(op->dvec);
+  cudaFree(op->tile_row);
+  cudaFree(op->sell_ptr);
+  cudaFree(op->sell_len);
+  cudaFree(op->sell_col);
+  cudaFree(op->sell_val);
   delete op;
 }
 
