@@ -84,8 +84,6 @@ struct StencilGeom {
   int nzl;              // planes owned by this rank
   long long nxy;        // nx * ny
   double d;             // inv_sqrt_diag (constant)
-  const double* ghost_lo;  // plane z0-1 of the input vector, or nullptr (Dirichlet)
-  const double* ghost_hi;  // plane z0+nzl of the input vector, or nullptr
 };
 
 struct CsrGeom {

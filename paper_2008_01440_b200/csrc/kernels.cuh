@@ -76,6 +76,61 @@ __device__ __forceinline__ void block_reduce_finish(double v, const Reduce& red)
   }
 }
 
+// Two values reduced together (partials[2 b], partials[2 b + 1]) into
+// result[0], result[1]: the [r'r, r'z] pair of one iteration.
+__device__ __forceinline__ void block_reduce_finish2(double v0, double v1, const Reduce& red) {
+  __shared__ double ws0[32], ws1[32];
+  __shared__ bool is_last2;
+  const int nthreads = blockDim.x * blockDim.y * blockDim.z;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (nthreads + 31) >> 5;
+  v0 = warp_sum(v0);
+  v1 = warp_sum(v1);
+  if (lane == 0) {
+    ws0[warp] = v0;
+    ws1[warp] = v1;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    v0 = warp_sum(lane < nwarps ? ws0[lane] : 0.0);
+    v1 = warp_sum(lane < nwarps ? ws1[lane] : 0.0);
+    if (lane == 0) {
+      red.partials[2 * bid] = v0;
+      red.partials[2 * bid + 1] = v1;
+      __threadfence();
+      const unsigned ticket = atomicAdd(red.counter, 1u);
+      is_last2 = (ticket == nblocks - 1);
+    }
+  }
+  __syncthreads();
+  if (!is_last2) return;
+  __threadfence();
+  double s0 = 0.0, s1 = 0.0;
+  for (unsigned b = tid; b < nblocks; b += nthreads) {
+    s0 += __ldcg(red.partials + 2 * b);
+    s1 += __ldcg(red.partials + 2 * b + 1);
+  }
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  if (lane == 0) {
+    ws0[warp] = s0;
+    ws1[warp] = s1;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    s0 = warp_sum(lane < nwarps ? ws0[lane] : 0.0);
+    s1 = warp_sum(lane < nwarps ? ws1[lane] : 0.0);
+    if (lane == 0) {
+      red.result[0] = s0;
+      red.result[1] = s1;
+      *red.counter = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // ----------------------------------------------------------------- epilogues
 // Two-phase interface so the marching kernels can prefetch the epilogue's own
 // operand vectors one plane ahead:
@@ -203,6 +258,91 @@ struct EpiChebStep {
 
 // ----------------------------------------------------------------- 7-point stencil
 
+// ----------------------------------------------------------------- operator inputs
+// The operator kernels read their input vector through an `In` policy:
+//   InVec  : x itself;
+//   InComb : the PCG direction update fused into the SpMV that consumes it,
+//            p_new = z + beta p_old with beta = S[s_new] / S[s_old]
+//            (pcg.cpp:107; `first`: p = z, pcg.cpp:63), evaluated per loaded
+//            element with the reference's rounding (z + (beta * p)), so the
+//            values are bitwise those of a separate update pass; the epilogue
+//            writes p_new once at the centre point (EpiStoreP).
+// Ghost planes (z-slab neighbours) hold the raw vectors; In combines them too.
+
+struct InVec {
+  const double* __restrict__ x;
+  const double* glo;  // ghost plane below the slab (or nullptr: Dirichlet)
+  const double* ghi;
+  __device__ __forceinline__ void init() {}
+  __device__ __forceinline__ double ld1(long long i) const { return __ldg(x + i); }
+  __device__ __forceinline__ double2 ld2(long long i) const { return ldg2(x + i); }
+  __device__ __forceinline__ void pf(long long i) const { prefetch_l2(x + i); }
+  __device__ __forceinline__ double glo1(long long c) const { return glo ? __ldg(glo + c) : 0.0; }
+  __device__ __forceinline__ double ghi1(long long c) const { return ghi ? __ldg(ghi + c) : 0.0; }
+  __device__ __forceinline__ double2 glo2(long long c) const {
+    return glo ? ldg2(glo + c) : make_double2(0.0, 0.0);
+  }
+  __device__ __forceinline__ double2 ghi2(long long c) const {
+    return ghi ? ldg2(ghi + c) : make_double2(0.0, 0.0);
+  }
+};
+
+struct InComb {
+  const double* __restrict__ z;
+  const double* __restrict__ p;
+  const double* S;
+  int s_new, s_old, first;
+  const double *zlo, *zhi, *plo, *phi;  // ghost planes of z and p_old
+  double beta;
+  __device__ __forceinline__ void init() { beta = first ? 0.0 : S[s_new] / S[s_old]; }
+  __device__ __forceinline__ double f(double zv, double pv) const {
+    return first ? zv : zv + beta * pv;
+  }
+  __device__ __forceinline__ double ld1(long long i) const { return f(__ldg(z + i), first ? 0.0 : __ldg(p + i)); }
+  __device__ __forceinline__ double2 ld2(long long i) const {
+    const double2 a = ldg2(z + i);
+    if (first) return a;
+    const double2 b = ldg2(p + i);
+    return make_double2(a.x + beta * b.x, a.y + beta * b.y);
+  }
+  __device__ __forceinline__ void pf(long long i) const {
+    prefetch_l2(z + i);
+    if (!first) prefetch_l2(p + i);
+  }
+  __device__ __forceinline__ double glo1(long long c) const {
+    return zlo ? f(__ldg(zlo + c), first ? 0.0 : __ldg(plo + c)) : 0.0;
+  }
+  __device__ __forceinline__ double ghi1(long long c) const {
+    return zhi ? f(__ldg(zhi + c), first ? 0.0 : __ldg(phi + c)) : 0.0;
+  }
+  __device__ __forceinline__ double2 glo2(long long c) const {
+    return zlo ? make_double2(glo1(c), glo1(c + 1)) : make_double2(0.0, 0.0);
+  }
+  __device__ __forceinline__ double2 ghi2(long long c) const {
+    return zhi ? make_double2(ghi1(c), ghi1(c + 1)) : make_double2(0.0, 0.0);
+  }
+};
+
+// q = A p_new ; writes p_new (the input at the centre) ; contribution p_new_i q_i
+struct EpiStoreP {
+  double* q;
+  double* pout;
+  __device__ __forceinline__ void pf(long long) const {}
+  __device__ __forceinline__ void ld(long long, double (&)[2]) const {}
+  __device__ __forceinline__ void ld2(long long, double2 (&)[2]) const {}
+  __device__ __forceinline__ double st(long long idx, double y, double xc, const double (&)[2]) const {
+    q[idx] = y;
+    pout[idx] = xc;
+    return xc * y;
+  }
+  __device__ __forceinline__ double st2(long long idx, double y0, double y1, double2 xc,
+                                        const double2 (&)[2]) const {
+    pcgx::st2(q + idx, y0, y1);
+    pcgx::st2(pout + idx, xc.x, xc.y);
+    return xc.x * y0 + xc.y * y1;
+  }
+};
+
 // Scaled 7-point row: terms in ascending column order k-1, j-1, i-1, centre,
 // i+1, j+1, k+1 (linop.cpp:247-253), t = d*x per neighbour (linop.cpp:272),
 // y = s*d (linop.cpp:274). A missing (Dirichlet) neighbour is passed as 0: its
@@ -225,10 +365,10 @@ __device__ __forceinline__ double stencil_point(double d, double xm, double xs, 
 // in-plane neighbours (i +- 1, j +- 1) come through L1 (the block's own plane
 // tile). Missing (Dirichlet) neighbours are 0, whose term -(d*0) = -0 leaves the
 // running sum bit-identical to the reference's skipped term.
-template <class Epi, bool kRed>
+template <class In, class Epi, bool kRed>
 __global__ void __launch_bounds__(kStencilThreads)
-stencil7_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begin, int k_end,
-                int kz, Reduce red) {
+stencil7_kernel(StencilGeom g, In in, Epi epi, int k_begin, int k_end, int kz, Reduce red) {
+  in.init();
   const int i = blockIdx.x * kStencilBX + threadIdx.x;
   const int j = blockIdx.y * kStencilBY + threadIdx.y;
   const int kb = k_begin + blockIdx.z * kz;
@@ -238,9 +378,9 @@ stencil7_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begi
     const long long col = (long long)j * g.nx + i;
     const long long nxy = g.nxy;
     auto plane = [&](int k) -> double {
-      if (k < 0) return g.ghost_lo ? __ldg(g.ghost_lo + col) : 0.0;
-      if (k >= g.nzl) return g.ghost_hi ? __ldg(g.ghost_hi + col) : 0.0;
-      return __ldg(x + (long long)k * nxy + col);
+      if (k < 0) return in.glo1(col);
+      if (k >= g.nzl) return in.ghi1(col);
+      return in.ld1((long long)k * nxy + col);
     };
     const bool has_w = i > 0, has_e = i < g.nx - 1, has_s = j > 0, has_n = j < g.ny - 1;
     const double d = g.d;
@@ -255,10 +395,10 @@ stencil7_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begi
       const double xpp = more ? plane(k + 2) : 0.0;
       double evn[2] = {0.0, 0.0};
       if (more) epi.ld(idx + nxy, evn);
-      const double xw = has_w ? __ldg(x + idx - 1) : 0.0;
-      const double xe = has_e ? __ldg(x + idx + 1) : 0.0;
-      const double xs = has_s ? __ldg(x + idx - g.nx) : 0.0;
-      const double xn = has_n ? __ldg(x + idx + g.nx) : 0.0;
+      const double xw = has_w ? in.ld1(idx - 1) : 0.0;
+      const double xe = has_e ? in.ld1(idx + 1) : 0.0;
+      const double xs = has_s ? in.ld1(idx - g.nx) : 0.0;
+      const double xn = has_n ? in.ld1(idx + g.nx) : 0.0;
       const double y = stencil_point(d, xm, xs, xw, xc, xe, xn, xp);
       const double c = epi.st(idx, y, xc, ev);
       if (kRed) acc = acc + c;
@@ -279,10 +419,11 @@ stencil7_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begi
 // load the one value outside the warp), j+-1 through L1. The next plane of x
 // and of the epilogue operands is prefetched one iteration ahead, so each thread
 // keeps 3-4 independent 16-byte HBM loads in flight across the dependent march.
-template <class Epi, bool kRed>
+template <class In, class Epi, bool kRed>
 __global__ void __launch_bounds__(kStencilThreads, PCGX_V2_MINB)
-stencil7v2_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_begin, int k_end,
-                  int kz, Reduce red, int pfd) {
+stencil7v2_kernel(StencilGeom g, In in, Epi epi, int k_begin, int k_end, int kz, Reduce red,
+                  int pfd) {
+  in.init();
   const int lane = threadIdx.x;
   const int i0 = blockIdx.x * 64 + 2 * lane;
   const int j = blockIdx.y * kStencilBY + threadIdx.y;
@@ -296,9 +437,9 @@ stencil7v2_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_be
     const double2 zero2 = make_double2(0.0, 0.0);
     auto plane = [&](int k) -> double2 {
       if (!valid) return zero2;
-      if (k < 0) return g.ghost_lo ? ldg2(g.ghost_lo + col) : zero2;
-      if (k >= g.nzl) return g.ghost_hi ? ldg2(g.ghost_hi + col) : zero2;
-      return ldg2(x + (long long)k * nxy + col);
+      if (k < 0) return in.glo2(col);
+      if (k >= g.nzl) return in.ghi2(col);
+      return in.ld2((long long)k * nxy + col);
     };
     const bool has_s = valid && j > 0, has_n = valid && j < g.ny - 1;
     const bool edge_w = lane == 0, edge_e = lane == 31;
@@ -317,15 +458,15 @@ stencil7v2_kernel(StencilGeom g, const double* __restrict__ x, Epi epi, int k_be
       if (more && valid) epi.ld2(idx + nxy, evn);
       if (pfd > 0 && valid && k + pfd < ke) {  // L2 prefetch pfd planes ahead (no registers)
         const long long pidx = idx + (long long)pfd * nxy;
-        if (k + pfd + 1 < g.nzl) prefetch_l2(x + pidx + nxy);
+        if (k + pfd + 1 < g.nzl) in.pf(pidx + nxy);
         epi.pf(pidx);
       }
-      const double2 xs = has_s ? ldg2(x + idx - g.nx) : zero2;
-      const double2 xn = has_n ? ldg2(x + idx + g.nx) : zero2;
+      const double2 xs = has_s ? in.ld2(idx - g.nx) : zero2;
+      const double2 xn = has_n ? in.ld2(idx + g.nx) : zero2;
       double xw = __shfl_up_sync(0xffffffffu, xc.y, 1);
       double xe = __shfl_down_sync(0xffffffffu, xc.x, 1);
-      if (edge_w) xw = has_w ? __ldg(x + idx - 1) : 0.0;
-      if (edge_e) xe = has_e ? __ldg(x + idx + 2) : 0.0;
+      if (edge_w) xw = has_w ? in.ld1(idx - 1) : 0.0;
+      if (edge_e) xe = has_e ? in.ld1(idx + 2) : 0.0;
       const double y0 = stencil_point(d, xm.x, xs.x, xw, xc.x, xc.y, xn.x, xp.x);
       const double y1 = stencil_point(d, xm.y, xs.y, xc.x, xc.y, xe, xn.y, xp.y);
       if (valid) {
@@ -572,9 +713,10 @@ struct SellGeom {
 #endif
 constexpr int kSellBatch = PCGX_SELL_BATCH;
 
-template <class Epi, bool kRed>
+template <class In, class Epi, bool kRed>
 __global__ void __launch_bounds__(256, PCGX_SELL_MINB)
-sell_kernel(SellGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
+sell_kernel(SellGeom g, In in, Epi epi, Reduce red) {
+  in.init();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   double acc = 0.0;
@@ -588,7 +730,7 @@ sell_kernel(SellGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
     double xr = 0.0, dr = 0.0;
     if (live) {
       epi.ld(row, ev);
-      xr = __ldg(x + row);
+      xr = in.ld1(row);
       dr = __ldg(g.dvec + row);
     }
     double sum = 0.0;
@@ -601,7 +743,7 @@ sell_kernel(SellGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
         const int c = on ? __ldg(g.col + e) : 0;
         vv[q] = on ? __ldg(g.val + e) : 0.0;
         dv[q] = on ? __ldg(g.dvec + c) : 0.0;
-        xv[q] = on ? __ldg(x + c) : 0.0;
+        xv[q] = on ? in.ld1(c) : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < kSellBatch; ++q)
@@ -620,31 +762,42 @@ sell_kernel(SellGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
 // Grid-stride over a fixed grid (deterministic element -> thread map).
 
 // x += alpha p ; r -= alpha q ; contribution r_i^2, alpha = rz[prev] / pq[cur]
-// (pcg.cpp:80-83)
+// (pcg.cpp:80-83). zmode 1 (m = 0, polyprec.cpp:179-181): also z = r / theta
+// and r'z (pcg.cpp:101) in the same pass; zmode 2 (no preconditioner, z = r):
+// r'z = r'r. zmode > 0 reduces the adjacent pair [r'r, r'z] (red.result[0..1]).
 __global__ void __launch_bounds__(kVecThreads)
 update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
               const double* __restrict__ p, const double* __restrict__ q, const double* S,
-              int s_rho, int s_pq, Reduce red) {
+              int s_rho, int s_pq, Reduce red, int zmode, double theta, double* __restrict__ z) {
   const double alpha = S[s_rho] / S[s_pq];
-  double acc = 0.0;
+  double acc = 0.0, acc2 = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     x[i] = x[i] + alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
     acc = acc + ri * ri;
+    if (zmode == 1) {
+      const double zi = ri / theta;
+      z[i] = zi;
+      acc2 = acc2 + ri * zi;
+    } else if (zmode == 2) {
+      acc2 = acc2 + ri * ri;
+    }
   }
-  block_reduce_finish(acc, red);
+  if (zmode) block_reduce_finish2(acc, acc2, red);
+  else block_reduce_finish(acc, red);
 }
 
-// p = z + beta p, beta = rz[cur] / rz[prev]  (pcg.cpp:107)
+// p_new = z + beta p_old, beta = rz[cur] / rz[prev] (pcg.cpp:107); first: p = z
+// (pcg.cpp:63). Out of place (the direction buffers ping-pong per iteration).
 __global__ void __launch_bounds__(kVecThreads)
-pupdate_kernel(long long n, double* __restrict__ p, const double* __restrict__ z,
-               const double* S, int s_new, int s_old) {
-  const double beta = S[s_new] / S[s_old];
+pupdate_kernel(long long n, double* __restrict__ pnew, const double* __restrict__ pold,
+               const double* __restrict__ z, const double* S, int s_new, int s_old, int first) {
+  const double beta = first ? 0.0 : S[s_new] / S[s_old];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    p[i] = z[i] + beta * p[i];
+    pnew[i] = first ? z[i] : z[i] + beta * pold[i];
 }
 
 // z = r / theta (m == 0, polyprec.cpp:179-181) or z = r (no preconditioner,

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "cheb2.cuh"
@@ -54,14 +55,15 @@ struct pcgx_context_s {
   std::string err;
   // workspace (device), sized for the largest operator used
   long long ws_n = 0;
-  double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *w0 = nullptr, *w1 = nullptr,
-         *w2 = nullptr, *w3 = nullptr, *t0 = nullptr, *t1 = nullptr;
+  double *r = nullptr, *z = nullptr, *p = nullptr, *p2 = nullptr, *q = nullptr, *w0 = nullptr,
+         *w1 = nullptr, *w2 = nullptr, *w3 = nullptr, *t0 = nullptr, *t1 = nullptr;
   double* flush = nullptr;
   size_t flush_bytes = 0;
   // solve-local bookkeeping
   int64_t cur_launches = 0;
   int64_t cur_allreduce = 0;
   int64_t cur_halo_bytes = 0;
+  bool capturing = false;
 };
 
 struct pcgx_operator_s {
@@ -71,7 +73,8 @@ struct pcgx_operator_s {
   // stencil
   long long nx = 0, ny = 0, nz = 0, z0 = 0, nzl = 0;
   double d = 0.0;
-  double *ghost_lo = nullptr, *ghost_hi = nullptr;
+  double *ghost_lo = nullptr, *ghost_hi = nullptr;    // ghost planes of the SpMV input
+  double *ghost_lo2 = nullptr, *ghost_hi2 = nullptr;  // second set (fused p = z + beta p: p_old)
   int kz = 16;
   bool vec2 = false;  // even nx -> stencil7v2_kernel
   int pfd = 0;        // L2 prefetch distance (planes) of the v2 march
@@ -203,7 +206,7 @@ void check_launch() {
 
 void ensure_workspace(pcgx_context c, long long n) {
   if (c->ws_n >= n) return;
-  double** bufs[] = {&c->r, &c->z, &c->p, &c->q, &c->w0, &c->w1, &c->w2, &c->w3, &c->t0, &c->t1};
+  double** bufs[] = {&c->r, &c->z, &c->p, &c->p2, &c->q, &c->w0, &c->w1, &c->w2, &c->w3, &c->t0, &c->t1};
   for (double** b : bufs) {
     if (*b) cudaFree(*b);
     *b = nullptr;
@@ -232,8 +235,9 @@ int vec_grid(pcgx_context c, long long n) {
 struct CommBase {
   virtual ~CommBase() = default;
   virtual void allreduce(pcgx_context c, int slot, int count) = 0;
-  // Start exchanging x's first/last owned plane into the neighbours' ghosts.
-  virtual void halo_begin(pcgx_context c, pcgx_operator op, const double* x) = 0;
+  // Start exchanging the first/last owned plane of each of the nv vectors into
+  // the neighbours' ghost set v (v = 0: ghost_lo/hi, v = 1: ghost_lo2/hi2).
+  virtual void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) = 0;
   // Make c->s wait until this rank's ghost planes hold the neighbours' planes.
   virtual void halo_wait(pcgx_context c) = 0;
   virtual bool graph_capturable() const = 0;
@@ -244,7 +248,7 @@ struct NcclComm : CommBase {
   void allreduce(pcgx_context c, int slot, int count) override {
     PCGX_NCCL(nccl().AllReduce(c->S + slot, c->S + slot, count, ncclDouble, ncclSum, c->comm, c->s));
   }
-  void halo_begin(pcgx_context c, pcgx_operator op, const double* x) override;
+  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override;
   void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
   bool graph_capturable() const override { return true; }
 };
@@ -285,12 +289,14 @@ struct LocalGroup {
   int nranks;
   HostBarrier bar;
   std::vector<pcgx_context> ctx;
-  std::vector<double*> ghost_lo, ghost_hi;
+  std::vector<double*> ghost_lo, ghost_hi, ghost_lo2, ghost_hi2;
   std::vector<cudaEvent_t> ev_ar;   // rank's contribution copied
   std::vector<cudaEvent_t> ev_done; // rank finished reading contributions
   double* contrib = nullptr;        // nranks * kSlots doubles on the first rank's device
   std::atomic<int> refs{0};
-  explicit LocalGroup(int n) : nranks(n), bar(n), ctx(n), ghost_lo(n), ghost_hi(n), ev_ar(n), ev_done(n) {}
+  explicit LocalGroup(int n)
+      : nranks(n), bar(n), ctx(n), ghost_lo(n), ghost_hi(n), ghost_lo2(n), ghost_hi2(n), ev_ar(n),
+        ev_done(n) {}
 };
 
 struct LocalComm : CommBase {
@@ -310,7 +316,7 @@ struct LocalComm : CommBase {
     PCGX_CUDA(cudaEventRecord(g->ev_done[rank], c->s));
     g->bar.wait();
   }
-  void halo_begin(pcgx_context c, pcgx_operator op, const double* x) override;
+  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override;
   void halo_wait(pcgx_context c) override {
     if (rank > 0) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[rank - 1]->ev_join, 0));
     if (rank < g->nranks - 1) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[rank + 1]->ev_join, 0));
@@ -326,41 +332,51 @@ void allreduce(pcgx_context c, int slot, int count) {
 
 // ---------------------------------------------------------------- operator launch
 
-void NcclComm::halo_begin(pcgx_context c, pcgx_operator op, const double* x) {
+void NcclComm::halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) {
   const long long nxy = op->nx * op->ny;
   const long long nzl = op->nzl;
   PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
   PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
   PCGX_NCCL(nccl().GroupStart());
-  if (op->ghost_lo) {
-    PCGX_NCCL(nccl().Send(x, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
-    PCGX_NCCL(nccl().Recv(op->ghost_lo, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
-  }
-  if (op->ghost_hi) {
-    PCGX_NCCL(nccl().Send(x + (nzl - 1) * nxy, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
-    PCGX_NCCL(nccl().Recv(op->ghost_hi, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
+  for (int v = 0; v < nv; ++v) {
+    const double* x = xs[v];
+    double* glo = v ? op->ghost_lo2 : op->ghost_lo;
+    double* ghi = v ? op->ghost_hi2 : op->ghost_hi;
+    if (glo) {
+      PCGX_NCCL(nccl().Send(x, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
+      PCGX_NCCL(nccl().Recv(glo, (size_t)nxy, ncclDouble, c->rank - 1, c->comm, c->cs));
+    }
+    if (ghi) {
+      PCGX_NCCL(nccl().Send(x + (nzl - 1) * nxy, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
+      PCGX_NCCL(nccl().Recv(ghi, (size_t)nxy, ncclDouble, c->rank + 1, c->comm, c->cs));
+    }
   }
   PCGX_NCCL(nccl().GroupEnd());
   PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
 }
 
-void LocalComm::halo_begin(pcgx_context c, pcgx_operator op, const double* x) {
+void LocalComm::halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) {
   const long long nxy = op->nx * op->ny;
   const long long nzl = op->nzl;
   g->ghost_lo[rank] = op->ghost_lo;
   g->ghost_hi[rank] = op->ghost_hi;
-  // ev_fork: my x is final AND my previous boundary kernels (ghost readers) are queued before it
+  g->ghost_lo2[rank] = op->ghost_lo2;
+  g->ghost_hi2[rank] = op->ghost_hi2;
+  // ev_fork: my vectors are final AND my previous boundary kernels (ghost readers) are queued before it
   PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
   g->bar.wait();
   PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
   const size_t pb = sizeof(double) * (size_t)nxy;
-  if (rank > 0) {  // my first plane -> ghost_hi of rank-1, once rank-1 no longer reads it
-    PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[rank - 1]->ev_fork, 0));
-    PCGX_CUDA(cudaMemcpyAsync(g->ghost_hi[rank - 1], x, pb, cudaMemcpyDefault, c->cs));
-  }
-  if (rank < g->nranks - 1) {  // my last plane -> ghost_lo of rank+1
-    PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[rank + 1]->ev_fork, 0));
-    PCGX_CUDA(cudaMemcpyAsync(g->ghost_lo[rank + 1], x + (nzl - 1) * nxy, pb, cudaMemcpyDefault, c->cs));
+  if (rank > 0) PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[rank - 1]->ev_fork, 0));
+  if (rank < g->nranks - 1) PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[rank + 1]->ev_fork, 0));
+  for (int v = 0; v < nv; ++v) {
+    const double* x = xs[v];
+    if (rank > 0)  // my first plane -> ghost_hi of rank-1, once rank-1 no longer reads it
+      PCGX_CUDA(cudaMemcpyAsync(v ? g->ghost_hi2[rank - 1] : g->ghost_hi[rank - 1], x, pb,
+                                cudaMemcpyDefault, c->cs));
+    if (rank < g->nranks - 1)  // my last plane -> ghost_lo of rank+1
+      PCGX_CUDA(cudaMemcpyAsync(v ? g->ghost_lo2[rank + 1] : g->ghost_lo[rank + 1],
+                                x + (nzl - 1) * nxy, pb, cudaMemcpyDefault, c->cs));
   }
   PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
   g->bar.wait();  // every rank's ev_join recorded before anyone waits on it
@@ -373,13 +389,11 @@ StencilGeom geom_of(pcgx_operator op) {
   g.nzl = (int)op->nzl;
   g.nxy = op->nx * op->ny;
   g.d = op->d;
-  g.ghost_lo = op->ghost_lo;
-  g.ghost_hi = op->ghost_hi;
   return g;
 }
 
-template <class Epi, bool kRed>
-void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, const double* x,
+template <class In, class Epi, bool kRed>
+void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, const In& in,
                     const Epi& epi, int k_begin, int k_end, int slot, bool accumulate) {
   if (k_end <= k_begin) return;
   const int kz = std::max(1, std::min(op->kz, k_end - k_begin));
@@ -389,20 +403,59 @@ void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, cons
   const unsigned gz = (unsigned)((k_end - k_begin + kz - 1) / kz);
   if (op->vec2) {  // even nx: two points per lane, 16-byte loads
     dim3 grid((unsigned)((g.nx + 63) / 64), gy, gz);
-    stencil7v2_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red,
-                                                            op->pfd);
+    stencil7v2_kernel<In, Epi, kRed><<<grid, block, 0, c->s>>>(g, in, epi, k_begin, k_end, kz, red,
+                                                                op->pfd);
   } else {
     dim3 grid((unsigned)((g.nx + kStencilBX - 1) / kStencilBX), gy, gz);
-    stencil7_kernel<Epi, kRed><<<grid, block, 0, c->s>>>(g, x, epi, k_begin, k_end, kz, red);
+    stencil7_kernel<In, Epi, kRed><<<grid, block, 0, c->s>>>(g, in, epi, k_begin, k_end, kz, red);
   }
   check_launch();
   count_launch(c);
 }
 
+// Input policies with the operator's ghost planes attached (or stripped for the
+// interior planes of a slab, which need none).
+InVec in_of(pcgx_operator op, const double* x, bool ghosts) {
+  return InVec{x, ghosts ? op->ghost_lo : nullptr, ghosts ? op->ghost_hi : nullptr};
+}
+InComb in_of(pcgx_operator op, const double* z, const double* p, const double* S, int s_new,
+             int s_old, int first, bool ghosts) {
+  InComb in{};
+  in.z = z;
+  in.p = p;
+  in.S = S;
+  in.s_new = s_new;
+  in.s_old = s_old;
+  in.first = first;
+  in.zlo = ghosts ? op->ghost_lo : nullptr;
+  in.zhi = ghosts ? op->ghost_hi : nullptr;
+  in.plo = ghosts ? op->ghost_lo2 : nullptr;
+  in.phi = ghosts ? op->ghost_hi2 : nullptr;
+  return in;
+}
+InVec strip(const InVec& in) { return InVec{in.x, nullptr, nullptr}; }
+InComb strip(const InComb& in) {
+  InComb o = in;
+  o.zlo = o.zhi = o.plo = o.phi = nullptr;
+  return o;
+}
+int halo_vecs(const InVec& in, const double** xs) {
+  xs[0] = in.x;
+  return 1;
+}
+int halo_vecs(const InComb& in, const double** xs) {
+  xs[0] = in.z;
+  xs[1] = in.p;
+  return in.first ? 1 : 2;
+}
+
+// Whether the operator's kernels accept the fused direction-update input.
+bool fuses_dir_update(pcgx_operator op) { return op->kind == 0 || op->sell_ptr != nullptr; }
+
 // y-consuming launch of the scaled operator over the local rows, with the halo
-// exchange of x (multi-GPU) overlapped with the interior planes.
-template <class Epi, bool kRed>
-void op_launch(pcgx_context c, pcgx_operator op, const double* x, const Epi& epi, int slot) {
+// exchange of the input (multi-GPU) overlapped with the interior planes.
+template <class In, class Epi, bool kRed>
+void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi, int slot) {
   op->matvecs.fetch_add(1, std::memory_order_relaxed);
   if (op->kind == 1 && op->sell_ptr) {
     SellGeom g{(int)op->n_local, op->nslices, op->sell_ptr, op->sell_len, op->sell_col, op->sell_val,
@@ -411,79 +464,72 @@ void op_launch(pcgx_context c, pcgx_operator op, const double* x, const Epi& epi
     const int want = (op->nslices + wpb - 1) / wpb;
     const int grid = std::max(1, std::min(want, c->sms * env_int("PCGX_SELL_BPS", 8)));
     Reduce red = kRed ? make_red(c, slot) : Reduce{};
-    sell_kernel<Epi, kRed><<<grid, 32 * wpb, 0, c->s>>>(g, x, epi, red);
+    sell_kernel<In, Epi, kRed><<<grid, 32 * wpb, 0, c->s>>>(g, in, epi, red);
     check_launch();
     count_launch(c);
     return;
   }
-  if (op->kind == 1 && op->tile_row) {
-    Csr2Geom g{(int)op->n_local, op->ntiles, op->tile_row, op->rp, op->ci, op->va, op->dvec};
-    PCGX_CUDA(cudaFuncSetAttribute(csr2_kernel<Epi, kRed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kCsr2Smem));
-    const int grid = std::max(1, std::min(op->ntiles, c->sms * env_int("PCGX_CSR2_BPS", 2)));
-    Reduce red = kRed ? make_red(c, slot) : Reduce{};
-    csr2_kernel<Epi, kRed><<<grid, kCsr2Rows, kCsr2Smem, c->s>>>(g, x, epi, red);
-    check_launch();
-    count_launch(c);
-    return;
-  }
-  if (op->kind == 1) {
-    CsrGeom g{(int)op->n_local, op->rp, op->ci, op->va, op->dvec};
-    const int nrb = (int)((op->n_local + kCsrRows - 1) / kCsrRows);
-    const int grid = std::max(1, std::min(nrb, c->sms * env_int("PCGX_CSR_BPS", 12)));
-    Reduce red = kRed ? make_red(c, slot) : Reduce{};
-    csr_kernel<Epi, kRed><<<grid, kCsrRows, 0, c->s>>>(g, x, epi, red);
-    check_launch();
-    count_launch(c);
-    return;
+  if constexpr (std::is_same_v<In, InVec>) {
+    if (op->kind == 1 && op->tile_row) {
+      Csr2Geom g{(int)op->n_local, op->ntiles, op->tile_row, op->rp, op->ci, op->va, op->dvec};
+      PCGX_CUDA(cudaFuncSetAttribute(csr2_kernel<Epi, kRed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kCsr2Smem));
+      const int grid = std::max(1, std::min(op->ntiles, c->sms * env_int("PCGX_CSR2_BPS", 2)));
+      Reduce red = kRed ? make_red(c, slot) : Reduce{};
+      csr2_kernel<Epi, kRed><<<grid, kCsr2Rows, kCsr2Smem, c->s>>>(g, in.x, epi, red);
+      check_launch();
+      count_launch(c);
+      return;
+    }
+    if (op->kind == 1) {
+      CsrGeom g{(int)op->n_local, op->rp, op->ci, op->va, op->dvec};
+      const int nrb = (int)((op->n_local + kCsrRows - 1) / kCsrRows);
+      const int grid = std::max(1, std::min(nrb, c->sms * env_int("PCGX_CSR_BPS", 12)));
+      Reduce red = kRed ? make_red(c, slot) : Reduce{};
+      csr_kernel<Epi, kRed><<<grid, kCsrRows, 0, c->s>>>(g, in.x, epi, red);
+      check_launch();
+      count_launch(c);
+      return;
+    }
+  } else {
+    if (op->kind == 1) fail(PCGX_ERR_UNSUPPORTED, "fused direction update needs the SELL CSR kernel");
   }
   StencilGeom g = geom_of(op);
   const int nzl = (int)op->nzl;
   const bool lo_nb = op->ghost_lo != nullptr, hi_nb = op->ghost_hi != nullptr;
   if (!lo_nb && !hi_nb) {
-    stencil_launch<Epi, kRed>(c, op, g, x, epi, 0, nzl, slot, false);
+    stencil_launch<In, Epi, kRed>(c, op, g, in, epi, 0, nzl, slot, false);
     return;
   }
-  // halo: my first plane -> rank-1 (its ghost_hi), my last plane -> rank+1 (its ghost_lo)
-  c->cm->halo_begin(c, op, x);
+  // halo: my first plane -> rank-1 (its ghosts), my last plane -> rank+1
+  const double* xs[2];
+  const int nv = halo_vecs(in, xs);
+  c->cm->halo_begin(c, op, xs, nv);
   const long long nxy = op->nx * op->ny;
-  c->cur_halo_bytes += ((lo_nb ? 1 : 0) + (hi_nb ? 1 : 0)) * nxy * 8;
+  c->cur_halo_bytes += (long long)nv * ((lo_nb ? 1 : 0) + (hi_nb ? 1 : 0)) * nxy * 8;
   // interior planes need no ghost: run them while the halo is in flight
   const int ib = lo_nb ? 1 : 0, ie = hi_nb ? nzl - 1 : nzl;
-  StencilGeom gi = g;
-  gi.ghost_lo = nullptr;
-  gi.ghost_hi = nullptr;
   bool wrote = false;
   if (ie > ib) {
-    stencil_launch<Epi, kRed>(c, op, gi, x, epi, ib, ie, slot, false);
+    stencil_launch<In, Epi, kRed>(c, op, g, strip(in), epi, ib, ie, slot, false);
     wrote = true;
   }
   c->cm->halo_wait(c);
   if (lo_nb) {
-    stencil_launch<Epi, kRed>(c, op, g, x, epi, 0, 1, slot, wrote);
+    stencil_launch<In, Epi, kRed>(c, op, g, in, epi, 0, 1, slot, wrote);
     wrote = true;
   }
   if (hi_nb && (nzl - 1 >= (lo_nb ? 1 : 0))) {
-    stencil_launch<Epi, kRed>(c, op, g, x, epi, nzl - 1, nzl, slot, wrote);
+    stencil_launch<In, Epi, kRed>(c, op, g, in, epi, nzl - 1, nzl, slot, wrote);
   }
 }
 
+template <class Epi, bool kRed>
+void op_launch(pcgx_context c, pcgx_operator op, const double* x, const Epi& epi, int slot) {
+  op_launch_in<InVec, Epi, kRed>(c, op, in_of(op, x, true), epi, slot);
+}
+
 // ---------------------------------------------------------------- vector launches
-
-void launch_update(pcgx_context c, long long n, double* x, double* r, const double* p,
-                   const double* q, int s_rho, int s_pq, int s_rr) {
-  update_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, r, p, q, c->S, s_rho, s_pq,
-                                                          make_red(c, s_rr));
-  check_launch();
-  count_launch(c);
-}
-
-void launch_pupdate(pcgx_context c, long long n, double* p, const double* z, int s_new,
-                    int s_old) {
-  pupdate_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, p, z, c->S, s_new, s_old);
-  check_launch();
-  count_launch(c);
-}
 
 void launch_zr(pcgx_context c, long long n, double* z, const double* r, double theta, int divide,
                int slot) {
@@ -688,9 +734,12 @@ template <class F>
 void capture(pcgx_context c, Graph& g, F&& body) {
   const int64_t before = c->cur_launches;
   PCGX_CUDA(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
+  c->capturing = true;
   try {
     body();
+    c->capturing = false;
   } catch (...) {
+    c->capturing = false;
     cudaGraph_t tmp;
     cudaStreamEndCapture(c->s, &tmp);
     if (tmp) cudaGraphDestroy(tmp);
@@ -742,7 +791,10 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   ensure_workspace(c, n);
   const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && env_int("PCGX_NO_GRAPH", 0) == 0 &&
                          (!c->cm || c->cm->graph_capturable());
-  const bool spec_after_update = (c->nranks == 1);
+  // one GPU: snapshot r'r right after the update and overlap the host check with
+  // the speculative P r; multi-GPU: merge [r'r, r'z] into one all-reduce after P r
+  // (PCGX_MERGED=1 forces the multi-GPU schedule on one GPU, for tests)
+  const bool spec_after_update = (c->nranks == 1) && env_int("PCGX_MERGED", 0) == 0;
 
   std::memset(rep, 0, sizeof *rep);
   c->cur_launches = 0;
@@ -815,12 +867,17 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
     rep->rel_res = 1.0;
   }
 
-  // setup preconditioning: z_0 goes straight into p (p = z, pcg.cpp:63), r'z -> rz(0)
-  auto enqueue_prec = [&](double* out, int slot) {
-    if (have_prec) enqueue_cheb(c, op, P, r, out, slot);
-    else launch_zr(c, n, out, r, 1.0, 0, slot);
-  };
-  enqueue_prec(p, slot_rz(0));
+  // zmode: 0 = Chebyshev m >= 1 (z from the fused recurrence), 1 = m == 0 (z = r/theta
+  // written by the update kernel), 2 = no preconditioner (z is r itself).
+  const int zm = !have_prec ? 2 : (m == 0 ? 1 : 0);
+  const double* zvec = (zm == 2) ? r : z;
+  double* Pd[2] = {p, c->p2};  // direction ping-pong: p(it) lives in Pd[it & 1]
+  const bool fuse = fuses_dir_update(op) && env_int("PCGX_NO_FUSE_P", 0) == 0;
+
+  // setup: z_0 = P r_0 and rho_0 = r'z -> rz(0) (pcg.cpp:57-64)
+  if (zm == 0) enqueue_cheb(c, op, P, r, z, slot_rz(0));
+  else if (zm == 1) launch_zr(c, n, z, r, P.theta, 1, slot_rz(0));
+  else launch_dot(c, n, r, r, slot_rz(0));
   allreduce(c, slot_rz(0), 1);
   alg += cheb_bytes();
   if (have_prec) {
@@ -836,54 +893,79 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
            "pcg_solve: r'z = " + fmt_double(rho) + " at setup (preconditioner not SPD?)");
   }
 
-  // per-iteration pieces
-  auto enqueue_spmv_dot = [&](int par) {
-    op_launch<EpiStore, true>(c, op, p, EpiStore{q}, slot_pq(par));
+  // dir_spmv(it): p(it) = z + beta p(it-1) (p(1) = z), q = A p(it), p'q -> pq(par); the
+  // direction update is fused into the SpMV's input (InComb) where the kernels allow it.
+  auto enqueue_dir_spmv = [&](int it) {
+    const int par = it & 1;
+    double* pnew = Pd[par];
+    const double* pold = Pd[par ^ 1];
+    const int first = (it == 1) ? 1 : 0;
+    if (fuse) {
+      op_launch_in<InComb, EpiStoreP, true>(
+          c, op, in_of(op, zvec, pold, c->S, slot_rz(par ^ 1), slot_rz(par), first, true),
+          EpiStoreP{q, pnew}, slot_pq(par));
+    } else {
+      pupdate_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, pnew, pold, zvec, c->S,
+                                                                slot_rz(par ^ 1), slot_rz(par), first);
+      check_launch();
+      count_launch(c);
+      op_launch<EpiStore, true>(c, op, pnew, EpiStore{q}, slot_pq(par));
+    }
     allreduce(c, slot_pq(par), 1);
   };
-  // B(it): prec(it) [+ rr,rz all-reduce + host snapshot on multi-GPU] ; p update ; spmv_dot(it+1)
-  auto enqueue_B = [&](int par, bool with_snapshot) {
-    enqueue_prec(z, slot_rz(par));
-    if (!spec_after_update) {
-      allreduce(c, slot_rr(par), 2);
-      if (with_snapshot) {
-        PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
-        PCGX_CUDA(cudaEventRecord(c->ev_sync, c->s));
+  const double bytes_dir = fuse ? spmv_equiv_bytes(op) + 2 * N8 : spmv_equiv_bytes(op) + 3 * N8;
+  auto snapshot = [&]() {  // External: when captured, the graph records ev_sync on every replay
+    PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
+    if (c->capturing) PCGX_CUDA(cudaEventRecordWithFlags(c->ev_sync, c->s, cudaEventRecordExternal));
+    else PCGX_CUDA(cudaEventRecord(c->ev_sync, c->s));
+  };
+  // snapshot right after the update when r'r (and r'z for zmode > 0) are final there
+  const bool snap_after_update = spec_after_update || zm > 0;
+  // B(it): [prec(it) -> z, r'z ; multi-GPU: all-reduce (r'r, r'z) + snapshot] ; dir_spmv(it+1)
+  auto enqueue_B = [&](int it) {
+    const int par = it & 1;
+    if (zm == 0) {
+      enqueue_cheb(c, op, P, r, z, slot_rz(par));
+      if (!spec_after_update) {
+        allreduce(c, slot_rr(par), 2);
+        snapshot();
       }
     }
-    launch_pupdate(c, n, p, z, slot_rz(par), slot_rz(par ^ 1));
-    enqueue_spmv_dot(par ^ 1);
+    enqueue_dir_spmv(it + 1);
   };
   Graph gB[2];
-  const double bytes_B = cheb_bytes() + 3 * N8 + spmv_equiv_bytes(op);
-  const double bytes_update = 6 * N8;
+  const double bytes_B = (zm == 0 ? cheb_bytes() : 0.0) + bytes_dir;
+  const double bytes_update = 6 * N8 + (zm == 1 ? N8 : 0.0);
 
-  enqueue_spmv_dot(1);
-  alg += spmv_equiv_bytes(op);
+  enqueue_dir_spmv(1);
+  alg += bytes_dir;
   for (int it = 1; it <= opts.maxit; ++it) {
     const int par = it & 1;
-    launch_update(c, n, x, r, p, q, slot_rz(par ^ 1), slot_pq(par), slot_rr(par));
+    update_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, r, Pd[par], q, c->S,
+                                                            slot_rz(par ^ 1), slot_pq(par),
+                                                            make_red(c, slot_rr(par)), zm,
+                                                            zm == 1 ? P.theta : 1.0, z);
+    check_launch();
+    count_launch(c);
     alg += bytes_update;
     rep->matvec++;  // q = A p of this iteration
     const bool more = it < opts.maxit;
-    if (spec_after_update || !more) {
-      if (!spec_after_update) allreduce(c, slot_rr(par), 1);
-      PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
-      PCGX_CUDA(cudaEventRecord(c->ev_sync, c->s));
-    }
+    if (!spec_after_update && (zm > 0 || !more)) allreduce(c, slot_rr(par), zm > 0 ? 2 : 1);
+    if (snap_after_update || !more) snapshot();
     if (more) {
       if (use_graph) {
-        if (!gB[par].exec) capture(c, gB[par], [&] { enqueue_B(par, true); });
+        if (!gB[par].exec) capture(c, gB[par], [&] { enqueue_B(it); });
         replay(c, gB[par]);
       } else {
-        enqueue_B(par, true);
+        enqueue_B(it);
       }
       alg += bytes_B;
     }
     PCGX_CUDA(cudaEventSynchronize(c->ev_sync));
     const double* hs = c->hS;
     // checks in the reference's order: r'z(it-1) [pcg.cpp:103-106], p'Ap [:76-79], ||r|| [:85]
-    if (it >= 2) {
+    const bool rz_now = !spec_after_update || zm > 0;  // r'z(it) is in this snapshot
+    if (it >= 2 && !rz_now) {
       const double rho_prev = hs[slot_rz(par ^ 1)];
       if (!std::isfinite(rho_prev) || rho_prev <= 0.0)
         fail(PCGX_ERR_NUMERICAL,
@@ -900,7 +982,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
     rep->rel_res = rnorm / bnorm;
     if (rep->rel_res <= opts.tol) {
       rep->converged = 1;
-      if (more) rep->wasted_matvec = m + 1;  // speculative P r and A p
+      if (more) rep->wasted_matvec = (zm == 0 ? m : 0) + 1;  // speculative P r and A p
       break;
     }
     if (!more) break;
@@ -909,7 +991,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
       rep->matvec += m;
     }
     rep->ddot++;  // r'z
-    if (!spec_after_update) {
+    if (rz_now) {
       const double rz = hs[slot_rz(par)];
       if (!std::isfinite(rz) || rz <= 0.0)
         fail(PCGX_ERR_NUMERICAL, "pcg_solve: r'z = " + fmt_double(rz) + " (preconditioner not SPD?)");
@@ -1027,8 +1109,14 @@ void lanczos_device(pcgx_context c, pcgx_operator op, int steps_hi, int steps, u
 void init_stencil_ghosts(pcgx_context c, pcgx_operator op) {
   const size_t pb = sizeof(double) * (size_t)(op->nx * op->ny);
   if (c->nranks > 1) {
-    if (c->rank > 0) PCGX_CUDA(cudaMalloc(&op->ghost_lo, pb));
-    if (c->rank < c->nranks - 1) PCGX_CUDA(cudaMalloc(&op->ghost_hi, pb));
+    if (c->rank > 0) {
+      PCGX_CUDA(cudaMalloc(&op->ghost_lo, pb));
+      PCGX_CUDA(cudaMalloc(&op->ghost_lo2, pb));
+    }
+    if (c->rank < c->nranks - 1) {
+      PCGX_CUDA(cudaMalloc(&op->ghost_hi, pb));
+      PCGX_CUDA(cudaMalloc(&op->ghost_hi2, pb));
+    }
   }
 }
 
@@ -1165,6 +1253,8 @@ void free_op(pcgx_operator op) {
   if (!op) return;
   cudaFree(op->ghost_lo);
   cudaFree(op->ghost_hi);
+  cudaFree(op->ghost_lo2);
+  cudaFree(op->ghost_hi2);
   cudaFree(op->rp);
   cudaFree(op->ci);
   cudaFree(op->va);
@@ -1282,7 +1372,7 @@ void pcgx_context_destroy(pcgx_context c) {
   cudaStreamSynchronize(c->s);
   if (c->comm) nccl().CommDestroy(c->comm);
   delete c->cm;
-  double* bufs[] = {c->r, c->z, c->p, c->q, c->w0, c->w1, c->w2, c->w3, c->t0, c->t1, c->flush, c->S, c->partials};
+  double* bufs[] = {c->r, c->z, c->p, c->p2, c->q, c->w0, c->w1, c->w2, c->w3, c->t0, c->t1, c->flush, c->S, c->partials};
   for (double* b : bufs)
     if (b) cudaFree(b);
   cudaFree(c->counter);

@@ -405,3 +405,40 @@ def test_cheb2_matches_single_step_path(P, ctx, monkeypatch):
     # last step is taken over a different launch shape -> last-bit differences
     assert r1.iters == r0.iters and rel_norm(x1, x0) <= 1e-12
     assert r1.kernel_launches < r0.kernel_launches
+
+
+# ------------------------------------------------------------------ PCG schedule variants
+
+@pytest.mark.parametrize("env", [{"PCGX_MERGED": "1"}, {"PCGX_NO_FUSE_P": "1"},
+                                 {"PCGX_MERGED": "1", "PCGX_NO_GRAPH": "1"}, {"PCGX_CHEB2": "0"}])
+@pytest.mark.parametrize("m", [-1, 0, 1, 6, 15])
+def test_pcg_schedules_agree(P, ctx, oracle, env, m, monkeypatch):
+    """The multi-GPU schedule (merged [r'r, r'z] reduction, snapshot inside the
+    CUDA graph), the unfused direction update and the single-step preconditioner
+    must give the oracle's iterations and solution."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    nx = 22
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    xt = P.random_uniform_vector(nx ** 3, SEED)
+    rhs = op.apply(xt)
+    prec = None if m < 0 else P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001))
+    x, rep = P.pcg_solve(op, rhs, None, prec)
+    po = None if m < 0 else oracle.cheb_params(a, b, m, 1.001)
+    xo, ro = oracle.pcg_solve(OracleOp("lap3d", nx=nx), po, rhs)
+    assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
+    assert rep.ddot == ro["ddot"] and rep.matvec == ro["matvec"]
+    if rep.iters == ro["iters"]:
+        assert rel_norm(x, xo) <= 1e-10
+
+
+def test_pcg_csr_fallback_kernels(P, ctx, oracle, golden, monkeypatch):
+    """csr2 (TMA tiles) and the chunked CSR kernel: not fused with the direction update."""
+    c = _golden_case(golden, "csr300_m7")
+    g = golden["csr_apply"]
+    rp, ci, va = np.array(g["row_ptr"]), np.array(g["col_idx"]), fhs(g["values"])
+    for kern in ("1", "2"):
+        monkeypatch.setenv("PCGX_CSR_KERNEL", kern)
+        _check_solve(P, oracle, c, csr(P, ctx, rp, ci, va),
+                     OracleOp("csr", row_ptr=rp, col_idx=ci, values=va), len(rp) - 1)
