@@ -48,6 +48,10 @@ constexpr size_t kC2Smem = sizeof(double) * (size_t)(kC2NA * kC2APlane + (kC2NB 
 
 struct Cheb2Params {
   int nx, ny, nzl;          // local grid
+  // z-slabs: loaded planes must lie in [a_lo, a_hi) (A, B, R; the slab plus the
+  // neighbours' planes exchanged into the vectors' padding), C is computed on
+  // [c_lo, c_hi) and is 0 (Dirichlet) elsewhere; tensor z = plane + zoff.
+  int a_lo, a_hi, c_lo, c_hi, zoff;
   long long nxy;
   double d;                 // inv sqrt diag
   double theta;
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(kC2Threads, 2)
 stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 box)
                       const __grid_constant__ CUtensorMap mapB,  // B (68 x 10 box)
                       const __grid_constant__ CUtensorMap mapR,  // R (68 x 10 box)
-                      Cheb2Params p, int kz, Reduce red) {
+                      Cheb2Params p, int k_begin, int k_end, int kz, Reduce red) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 128-byte aligned base, kept as a shared-space pointer (LDS, not generic LD)
   double* sA = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
@@ -116,8 +120,8 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = blockIdx.x * kC2TX, j0 = blockIdx.y * kC2TY;
-  const int kb = blockIdx.z * kz;
-  const int ke = min(kb + kz, p.nzl);
+  const int kb = k_begin + blockIdx.z * kz;
+  const int ke = min(kb + kz, k_end);
   const unsigned bytesA = kC2APlane * 8, bytesB = kC2BPlane * 8;
 
   if (tid == 0) {
@@ -128,23 +132,24 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
 
   // Load unit u (stage-1 plane u): A[u+1], B[u], R[u]. Planes outside [0, nzl)
   // are never loaded (their readers substitute 0 = Dirichlet).
-  auto in_z = [&](int z) { return z >= 0 && z < p.nzl; };
+  auto in_z = [&](int z) { return z >= p.a_lo && z < p.a_hi; };
+  const int zo = p.zoff;
   auto issue_unit = [&](int u) {
     uint64_t* bar = &bars[(u - (kb - 1)) % kC2D];
     const bool la = in_z(u + 1), lbr = !kFirst && in_z(u);
     mbar_expect_tx(bar, (la ? bytesA : 0u) + (lbr ? 2 * bytesB : 0u));
-    if (la) tma_load_3d(sA + ((u + 1 - (kb - 2)) % kC2NA) * kC2APlane, &mapA, i0 - 2, j0 - 2, u + 1, bar);
+    if (la) tma_load_3d(sA + ((u + 1 - (kb - 2)) % kC2NA) * kC2APlane, &mapA, i0 - 2, j0 - 2, u + 1 + zo, bar);
     if (lbr) {
-      tma_load_3d(sB + ((u - (kb - 1)) % kC2NB) * kC2EStride, &mapB, i0 - 2, j0 - 1, u, bar);
-      tma_load_3d(sR + ((u - (kb - 1)) % kC2NR) * kC2EStride, &mapR, i0 - 2, j0 - 1, u, bar);
+      tma_load_3d(sB + ((u - (kb - 1)) % kC2NB) * kC2EStride, &mapB, i0 - 2, j0 - 1, u + zo, bar);
+      tma_load_3d(sR + ((u - (kb - 1)) % kC2NR) * kC2EStride, &mapR, i0 - 2, j0 - 1, u + zo, bar);
     }
   };
   const int u_last = ke;  // stage 1 runs u = kb-1 .. ke
   if (tid == 0) {
     uint64_t* pb = &bars[kC2D];
     mbar_expect_tx(pb, (in_z(kb - 2) ? bytesA : 0u) + (in_z(kb - 1) ? bytesA : 0u));
-    if (in_z(kb - 2)) tma_load_3d(sA, &mapA, i0 - 2, j0 - 2, kb - 2, pb);
-    if (in_z(kb - 1)) tma_load_3d(sA + kC2APlane, &mapA, i0 - 2, j0 - 2, kb - 1, pb);
+    if (in_z(kb - 2)) tma_load_3d(sA, &mapA, i0 - 2, j0 - 2, kb - 2 + zo, pb);
+    if (in_z(kb - 1)) tma_load_3d(sA + kC2APlane, &mapA, i0 - 2, j0 - 2, kb - 1 + zo, pb);
     for (int u = kb - 1; u < kb - 1 + kC2D && u <= u_last; ++u) issue_unit(u);
   }
   mbar_wait(&bars[kC2D], 0);
@@ -197,7 +202,7 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
     const double* Bu = sB + sb * kC2EStride;
     const double* Ru = sR + sr * kC2EStride;
     double* Cu = sC + sc * kC2CStride;
-    const bool plane_in = in_z(u), has_p = in_z(u + 1);
+    const bool plane_in = u >= p.c_lo && u < p.c_hi, has_p = in_z(u + 1);
     // ---------------- stage 1: C[u] pairs of the extended tile
     {
       const double2 ap = has_p ? *reinterpret_cast<const double2*>(Ap + offA1) : zero2;

@@ -54,7 +54,7 @@ struct pcgx_context_s {
   int64_t launches = 0;
   std::string err;
   // workspace (device), sized for the largest operator used
-  long long ws_n = 0;
+  long long ws_n = 0, ws_pad = 0;
   double *r = nullptr, *z = nullptr, *p = nullptr, *p2 = nullptr, *q = nullptr, *w0 = nullptr,
          *w1 = nullptr, *w2 = nullptr, *w3 = nullptr, *t0 = nullptr, *t1 = nullptr;
   double* flush = nullptr;
@@ -79,6 +79,7 @@ struct pcgx_operator_s {
   bool vec2 = false;  // even nx -> stencil7v2_kernel
   int pfd = 0;        // L2 prefetch distance (planes) of the v2 march
   bool cheb2 = false; // two Chebyshev steps per pass (stencil7_cheb2_kernel, TMA)
+  int zpad = 0;       // ghost planes per side in the workspace vectors (z-slab + cheb2: 2)
   int kz2 = 32;       // z-chunk of the two-step kernel
   struct TmaPair { const double* ptr; CUtensorMap a, e; };
   std::vector<TmaPair> tmaps;  // per-buffer tensor maps (A box 68x12, B/R box 68x10)
@@ -204,16 +205,27 @@ void check_launch() {
   if (e != cudaSuccess) fail(PCGX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
 }
 
-void ensure_workspace(pcgx_context c, long long n) {
-  if (c->ws_n >= n) return;
+long long ws_pad_of(pcgx_operator op) { return op->zpad * op->nx * op->ny; }
+
+// Workspace vectors carry `pad` zeroed elements before and after (z-slab ranks:
+// two ghost planes per side that the two-step kernel reads through TMA).
+void ensure_workspace(pcgx_context c, long long n, long long pad = 0) {
+  if (c->ws_n >= n && c->ws_pad == pad) return;
   double** bufs[] = {&c->r, &c->z, &c->p, &c->p2, &c->q, &c->w0, &c->w1, &c->w2, &c->w3, &c->t0, &c->t1};
   for (double** b : bufs) {
-    if (*b) cudaFree(*b);
+    if (*b) cudaFree(*b - c->ws_pad);
     *b = nullptr;
   }
   c->ws_n = 0;
-  for (double** b : bufs) PCGX_CUDA(cudaMalloc(b, sizeof(double) * (size_t)std::max(n, 1LL)));
+  for (double** b : bufs) {
+    double* raw = nullptr;
+    const size_t tot = (size_t)std::max(n, 1LL) + 2 * (size_t)pad;
+    PCGX_CUDA(cudaMalloc(&raw, sizeof(double) * tot));
+    if (pad) PCGX_CUDA(cudaMemset(raw, 0, sizeof(double) * tot));
+    *b = raw + pad;
+  }
   c->ws_n = n;
+  c->ws_pad = pad;
 }
 
 int vec_grid(pcgx_context c, long long n) {
@@ -240,6 +252,17 @@ struct CommBase {
   virtual void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) = 0;
   // Make c->s wait until this rank's ghost planes hold the neighbours' planes.
   virtual void halo_wait(pcgx_context c) = 0;
+  // Generic plane exchange (two-step kernel): for each item my bottom `count`
+  // elements go to rank-1's recv_hi and my top ones to rank+1's recv_lo; I
+  // receive into my recv_lo / recv_hi. Completes like halo_begin (halo_wait).
+  struct PlaneX {
+    const double* send_lo;
+    double* recv_lo;
+    const double* send_hi;
+    double* recv_hi;
+    long long count;
+  };
+  virtual void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) = 0;
   virtual bool graph_capturable() const = 0;
 };
 namespace {
@@ -250,6 +273,7 @@ struct NcclComm : CommBase {
   }
   void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override;
   void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
+  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override;
   bool graph_capturable() const override { return true; }
 };
 
@@ -290,13 +314,14 @@ struct LocalGroup {
   HostBarrier bar;
   std::vector<pcgx_context> ctx;
   std::vector<double*> ghost_lo, ghost_hi, ghost_lo2, ghost_hi2;
+  std::vector<std::vector<double*>> xrecv_lo, xrecv_hi;  // per rank, per xchg item
   std::vector<cudaEvent_t> ev_ar;   // rank's contribution copied
   std::vector<cudaEvent_t> ev_done; // rank finished reading contributions
   double* contrib = nullptr;        // nranks * kSlots doubles on the first rank's device
   std::atomic<int> refs{0};
   explicit LocalGroup(int n)
-      : nranks(n), bar(n), ctx(n), ghost_lo(n), ghost_hi(n), ghost_lo2(n), ghost_hi2(n), ev_ar(n),
-        ev_done(n) {}
+      : nranks(n), bar(n), ctx(n), ghost_lo(n), ghost_hi(n), ghost_lo2(n), ghost_hi2(n),
+        xrecv_lo(n), xrecv_hi(n), ev_ar(n), ev_done(n) {}
 };
 
 struct LocalComm : CommBase {
@@ -321,6 +346,7 @@ struct LocalComm : CommBase {
     if (rank > 0) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[rank - 1]->ev_join, 0));
     if (rank < g->nranks - 1) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[rank + 1]->ev_join, 0));
   }
+  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override;
   bool graph_capturable() const override { return false; }
 };
 
@@ -380,6 +406,51 @@ void LocalComm::halo_begin(pcgx_context c, pcgx_operator op, const double* const
   }
   PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
   g->bar.wait();  // every rank's ev_join recorded before anyone waits on it
+}
+
+void NcclComm::xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) {
+  const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
+  PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+  PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+  PCGX_NCCL(nccl().GroupStart());
+  for (int i = 0; i < n; ++i) {
+    const PlaneX& it = items[i];
+    if (lo) {
+      PCGX_NCCL(nccl().Send(it.send_lo, (size_t)it.count, ncclDouble, c->rank - 1, c->comm, c->cs));
+      PCGX_NCCL(nccl().Recv(it.recv_lo, (size_t)it.count, ncclDouble, c->rank - 1, c->comm, c->cs));
+    }
+    if (hi) {
+      PCGX_NCCL(nccl().Send(it.send_hi, (size_t)it.count, ncclDouble, c->rank + 1, c->comm, c->cs));
+      PCGX_NCCL(nccl().Recv(it.recv_hi, (size_t)it.count, ncclDouble, c->rank + 1, c->comm, c->cs));
+    }
+  }
+  PCGX_NCCL(nccl().GroupEnd());
+  PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+}
+
+void LocalComm::xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) {
+  (void)op;
+  g->xrecv_lo[rank].assign((size_t)n, nullptr);
+  g->xrecv_hi[rank].assign((size_t)n, nullptr);
+  for (int i = 0; i < n; ++i) {
+    g->xrecv_lo[rank][(size_t)i] = items[i].recv_lo;
+    g->xrecv_hi[rank][(size_t)i] = items[i].recv_hi;
+  }
+  PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+  g->bar.wait();
+  PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+  if (rank > 0) PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[rank - 1]->ev_fork, 0));
+  if (rank < g->nranks - 1) PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[rank + 1]->ev_fork, 0));
+  for (int i = 0; i < n; ++i) {
+    const PlaneX& it = items[i];
+    const size_t b = sizeof(double) * (size_t)it.count;
+    if (rank > 0)
+      PCGX_CUDA(cudaMemcpyAsync(g->xrecv_hi[rank - 1][(size_t)i], it.send_lo, b, cudaMemcpyDefault, c->cs));
+    if (rank < g->nranks - 1)
+      PCGX_CUDA(cudaMemcpyAsync(g->xrecv_lo[rank + 1][(size_t)i], it.send_hi, b, cudaMemcpyDefault, c->cs));
+  }
+  PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+  g->bar.wait();
 }
 
 StencilGeom geom_of(pcgx_operator op) {
@@ -583,7 +654,10 @@ EncodeTiledFn encode_tiled() {
 
 CUtensorMap make_map(pcgx_operator op, const double* ptr, int bx, int by) {
   CUtensorMap m;
-  const cuuint64_t dims[3] = {(cuuint64_t)op->nx, (cuuint64_t)op->ny, (cuuint64_t)op->nzl};
+  // padded workspace (z-slab ranks): the map spans the zpad ghost planes on each side
+  ptr -= (long long)op->zpad * op->nx * op->ny;
+  const cuuint64_t dims[3] = {(cuuint64_t)op->nx, (cuuint64_t)op->ny,
+                              (cuuint64_t)(op->nzl + 2 * op->zpad)};
   const cuuint64_t strides[2] = {(cuuint64_t)op->nx * 8, (cuuint64_t)(op->nx * op->ny) * 8};
   const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
@@ -604,21 +678,65 @@ const pcgx_operator_s::TmaPair& tmaps_for(pcgx_operator op, const double* ptr) {
 
 template <bool kFirst, bool kRed>
 void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const double* B,
-                  const double* R, const Cheb2Params& prm, int slot) {
+                  const double* R, const Cheb2Params& prm, int slot, int k_begin, int k_end, int kz,
+                  bool accumulate) {
+  if (k_end <= k_begin) return;
   PCGX_CUDA(cudaFuncSetAttribute(stencil7_cheb2_kernel<kFirst, kRed>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2Smem));
   // copies: a later tmaps_for() may grow the cache and move its elements
   const CUtensorMap ma = tmaps_for(op, A).a;
   const CUtensorMap mb = tmaps_for(op, B ? B : A).e;
   const CUtensorMap mr = tmaps_for(op, R).e;
-  const int kz = std::max(1, std::min(op->kz2, (int)op->nzl));
+  kz = std::max(1, std::min(kz, k_end - k_begin));
   dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
-            (unsigned)((op->nzl + kz - 1) / kz));
-  Reduce red = kRed ? make_red(c, slot) : Reduce{};
-  stencil7_cheb2_kernel<kFirst, kRed><<<grid, kC2Threads, kC2Smem, c->s>>>(ma, mb, mr, prm, kz, red);
+            (unsigned)((k_end - k_begin + kz - 1) / kz));
+  Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
+  stencil7_cheb2_kernel<kFirst, kRed><<<grid, kC2Threads, kC2Smem, c->s>>>(ma, mb, mr, prm, k_begin,
+                                                                           k_end, kz, red);
   check_launch();
   count_launch(c);
+}
+
+// One two-step pass over the local slab. On a z-slab rank the neighbours' two
+// A planes (one B plane) per side are first exchanged into the vectors'
+// padding; the chunks that do not read them run while the planes travel.
+template <bool kFirst, bool kRed>
+void cheb2_pass(pcgx_context c, pcgx_operator op, const double* A, const double* B,
+                const double* R, Cheb2Params prm, int slot) {
   op->matvecs.fetch_add(2, std::memory_order_relaxed);
+  const int nzl = (int)op->nzl;
+  const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
+  prm.zoff = op->zpad;
+  prm.a_lo = lo ? -2 : 0;
+  prm.a_hi = hi ? nzl + 2 : nzl;
+  prm.c_lo = lo ? -1 : 0;
+  prm.c_hi = hi ? nzl + 1 : nzl;
+  if (!lo && !hi) {
+    cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, 0, nzl, op->kz2, false);
+    return;
+  }
+  const long long nxy = op->nx * op->ny;
+  CommBase::PlaneX items[2];
+  int ni = 0;
+  items[ni++] = {A, const_cast<double*>(A) - 2 * nxy, A + (long long)(nzl - 2) * nxy,
+                 const_cast<double*>(A) + (long long)nzl * nxy, 2 * nxy};
+  if (!kFirst)
+    items[ni++] = {B, const_cast<double*>(B) - nxy, B + (long long)(nzl - 1) * nxy,
+                   const_cast<double*>(B) + (long long)nzl * nxy, nxy};
+  c->cm->xchg(c, op, items, ni);
+  c->cur_halo_bytes += (long long)((lo ? 1 : 0) + (hi ? 1 : 0)) * (2 + (kFirst ? 0 : 1)) * nxy * 8;
+  const int ib = lo ? std::min(2, nzl) : 0, ie = hi ? std::max(ib, nzl - 2) : nzl;
+  bool wrote = false;
+  if (ie > ib) {
+    cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, ib, ie, op->kz2, false);
+    wrote = true;
+  }
+  c->cm->halo_wait(c);
+  if (ib > 0) {
+    cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, 0, ib, 2, wrote);
+    wrote = true;
+  }
+  if (ie < nzl) cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, ie, nzl, 2, wrote);
 }
 
 // ---------------------------------------------------------------- Chebyshev apply
@@ -677,8 +795,8 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
     q.rk2m1 = P.rho[1];
     q.outC = bufs[0];
     q.outE = last12 ? out : bufs[1];
-    if (last12 && rz_slot >= 0) cheb2_launch<true, true>(c, op, r, nullptr, r, q, rz_slot);
-    else cheb2_launch<true, false>(c, op, r, nullptr, r, q, -1);
+    if (last12 && rz_slot >= 0) cheb2_pass<true, true>(c, op, r, nullptr, r, q, rz_slot);
+    else cheb2_pass<true, false>(c, op, r, nullptr, r, q, -1);
     if (last12) return;
     int iold = 0, icur = 1;  // x_{k-2}, x_{k-1} buffer indices
     int k = 3;
@@ -693,8 +811,8 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
       q.rk2m1 = P.rho[k];
       q.outC = bufs[fc];
       q.outE = last ? out : bufs[fe];
-      if (last && rz_slot >= 0) cheb2_launch<false, true>(c, op, bufs[icur], bufs[iold], r, q, rz_slot);
-      else cheb2_launch<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1);
+      if (last && rz_slot >= 0) cheb2_pass<false, true>(c, op, bufs[icur], bufs[iold], r, q, rz_slot);
+      else cheb2_pass<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1);
       iold = fc;
       icur = fe;
     }
@@ -788,7 +906,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   if (have_prec) P = cheb_from(prec_in);
   const int m = have_prec ? P.m : 0;
   const long long n = op->n_local;
-  ensure_workspace(c, n);
+  ensure_workspace(c, n, ws_pad_of(op));
   const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && env_int("PCGX_NO_GRAPH", 0) == 0 &&
                          (!c->cm || c->cm->graph_capturable());
   // one GPU: snapshot r'r right after the update and overlap the host check with
@@ -1034,7 +1152,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
     }
     EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0};
     auto launch = [&] {
-      if (two) cheb2_launch<false, false>(c, op, c->w1, c->w0, r, q, -1);
+      if (two) cheb2_pass<false, false>(c, op, c->w1, c->w0, r, q, -1);
       else op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);
     };
     const uint64_t mv0 = op->matvecs.load();
@@ -1059,7 +1177,7 @@ void lanczos_device(pcgx_context c, pcgx_operator op, int steps_hi, int steps, u
   if (steps < 1 || steps_hi < 1 || steps_hi > steps)
     fail(PCGX_ERR_INVALID, "lanczos: need 1 <= steps_hi <= steps");
   const long long n = op->n_local;
-  ensure_workspace(c, n);
+  ensure_workspace(c, n, ws_pad_of(op));
   double* v = c->t0;
   double* vprev = c->t1;
   double* w = c->w0;
@@ -1372,7 +1490,10 @@ void pcgx_context_destroy(pcgx_context c) {
   cudaStreamSynchronize(c->s);
   if (c->comm) nccl().CommDestroy(c->comm);
   delete c->cm;
-  double* bufs[] = {c->r, c->z, c->p, c->p2, c->q, c->w0, c->w1, c->w2, c->w3, c->t0, c->t1, c->flush, c->S, c->partials};
+  double* ws[] = {c->r, c->z, c->p, c->p2, c->q, c->w0, c->w1, c->w2, c->w3, c->t0, c->t1};
+  for (double* b : ws)
+    if (b) cudaFree(b - c->ws_pad);
+  double* bufs[] = {c->flush, c->S, c->partials};
   for (double* b : bufs)
     if (b) cudaFree(b);
   cudaFree(c->counter);
@@ -1495,10 +1616,12 @@ pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t
     op->kz = default_kz(c, nx, ny, op->nzl);
     op->vec2 = (nx % 2 == 0) && env_int("PCGX_STENCIL_SCALAR", 0) == 0;
     op->pfd = env_int("PCGX_PFD", 2);
-    op->cheb2 = op->vec2 && c->nranks == 1 && env_int("PCGX_CHEB2", 1) != 0;
+    op->cheb2 = op->vec2 && env_int("PCGX_CHEB2", 1) != 0;
     op->kz2 = env_int("PCGX_KZ2", 32);
     try {
       init_stencil_ghosts(c, op);
+      if (c->nranks > 1 && op->nzl < 2) op->cheb2 = false;  // 2-plane halos need >= 2 planes
+      op->zpad = (op->cheb2 && c->nranks > 1) ? 2 : 0;
     } catch (...) {
       free_op(op);
       throw;
@@ -1568,7 +1691,7 @@ pcgx_status pcgx_operator_apply(pcgx_context c, pcgx_operator op, const double* 
   return guarded(c, [&] {
     set_device(c);
     const long long n = op->n_local;
-    ensure_workspace(c, n);
+    ensure_workspace(c, n, ws_pad_of(op));
     PCGX_CUDA(cudaMemcpyAsync(c->t0, x, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
     op_launch<EpiStore, false>(c, op, c->t0, EpiStore{c->t1}, -1);
     PCGX_CUDA(cudaMemcpyAsync(y, c->t1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
@@ -1593,8 +1716,12 @@ pcgx_status pcgx_cheb_apply_device(pcgx_context c, pcgx_operator op, const pcgx_
   return guarded(c, [&] {
     set_device(c);
     if (r == out) fail(PCGX_ERR_INVALID, "apply_chebyshev: out must not alias r");
-    ensure_workspace(c, op->n_local);
+    ensure_workspace(c, op->n_local, ws_pad_of(op));
     Cheb P = cheb_from(p);
+    if (op->zpad) {  // the two-step kernel reads r's neighbour planes from padding
+      copy_d2d(c, c->t0, r, op->n_local);
+      r = c->t0;
+    }
     enqueue_cheb(c, op, P, r, out, -1);
   });
 }
@@ -1604,7 +1731,7 @@ pcgx_status pcgx_cheb_apply(pcgx_context c, pcgx_operator op, const pcgx_cheb* p
   return guarded(c, [&] {
     set_device(c);
     const long long n = op->n_local;
-    ensure_workspace(c, n);
+    ensure_workspace(c, n, ws_pad_of(op));
     Cheb P = cheb_from(p);
     PCGX_CUDA(cudaMemcpyAsync(c->t0, r, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
     enqueue_cheb(c, op, P, c->t0, c->t1, -1);
@@ -1637,7 +1764,7 @@ pcgx_status pcgx_pcg_solve(pcgx_context c, pcgx_operator op, const pcgx_cheb* pr
     set_device(c);
     if (!rep) fail(PCGX_ERR_INVALID, "pcg_solve: null report");
     const long long n = op->n_local;
-    ensure_workspace(c, n);
+    ensure_workspace(c, n, ws_pad_of(op));
     // b and x live in t0 / t1 for the call (the solver uses r z p q w0 w1)
     PCGX_CUDA(cudaMemcpyAsync(c->t0, b, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
     pcgx_solve_opts o;
