@@ -338,7 +338,9 @@ def run_gpu(args):
     if os.path.exists(tp):
         with open(tp) as f:
             td = json.load(f)
-        if td.get("n") == n_loc:
+        same_kernel = (td.get("kernel", "").startswith("stencil7_cheb2") ==
+                       (step_bytes == 40.0 * n_loc and kind == "stencil"))
+        if td.get("n") == n_loc and same_kernel:
             traffic = td.get("dram_bytes_per_launch")
 
     cpu = None
