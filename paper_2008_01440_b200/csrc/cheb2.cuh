@@ -34,7 +34,13 @@ constexpr int kC2BY = kC2TY + 2;                     // B, R boxes and the C rin
 // aligned, i.e. even for fp64 (tools/tma_probe: an odd origin is an illegal
 // instruction on sm_100a). A box 68 x 12 (6528 B), B/R boxes 68 x 10 (5440 B).
 constexpr int kC2AX = kC2W, kC2BX = kC2W;
-constexpr int kC2D = 3;                              // prefetch distance (planes)
+#ifndef PCGX_C2D
+#define PCGX_C2D 3
+#endif
+#ifndef PCGX_C2MINB
+#define PCGX_C2MINB 2
+#endif
+constexpr int kC2D = PCGX_C2D;                       // prefetch distance (planes)
 constexpr int kC2NA = kC2D + 2, kC2NB = kC2D, kC2NR = kC2D + 1, kC2NC = 3;
 constexpr int kC2APlane = kC2W * kC2AY;              // 816 doubles = 51 x 128 B
 constexpr int kC2BPlane = kC2W * kC2BY;              // 680 doubles
@@ -105,7 +111,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 // operands are read from shared memory (16-byte LDS). Ring slots rotate by
 // one per plane and are tracked with incremented indices (no modulo).
 template <bool kFirst, bool kRed>
-__global__ void __launch_bounds__(kC2Threads, 2)
+__global__ void __launch_bounds__(kC2Threads, PCGX_C2MINB)
 stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 box)
                       const __grid_constant__ CUtensorMap mapB,  // B (68 x 10 box)
                       const __grid_constant__ CUtensorMap mapR,  // R (68 x 10 box)
@@ -182,12 +188,25 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
   const bool h_in = do_h && hgi >= 0 && hgi < p.nx && hgj >= 0 && hgj < p.ny;
   const int offAh = (lane + 1) * kC2W + hcol, offBh = lane * kC2W + hcol;
 
-  // ring slot indices of plane u (A: u-(kb-2), B/R: u-(kb-1), C: u), advanced by one per plane
-  int sa = 1;                         // slot of A[u] at u = kb-1
-  int sb = 0, sr = 0;                 // slots of B[u], R[u]
-  int sc = (((kb - 1) % kC2NC) + kC2NC) % kC2NC;  // slot of C[u]
-  auto wrap_inc = [](int x, int n) { return x + 1 == n ? 0 : x + 1; };
-  auto wrap_dec = [](int x, int n) { return x == 0 ? n - 1 : x - 1; };
+  // Ring slots of plane u, as rotating shared pointers (one add + select per ring
+  // per plane): A[u-1], A[u], A[u+1]; B[u]; R[u-1], R[u]; C[u-1], C[u].
+  const double* const sAend = sA + kC2NA * kC2APlane;
+  const double* const sBend = sB + kC2NB * kC2EStride;
+  const double* const sRend = sR + kC2NR * kC2EStride;
+  double* const sCend = sC + kC2NC * kC2CStride;
+  const double* pAm = sA;                      // A[kb-2]
+  const double* pAu = sA + kC2APlane;          // A[kb-1]
+  const double* pAp = sA + 2 * kC2APlane;      // A[kb]
+  const double* pBu = sB;                      // B[kb-1]
+  const double* pRu = sR;                      // R[kb-1]
+  const double* pRm = sR + (kC2NR - 1) * kC2EStride;  // R[kb-2] (never read)
+  const int sc0 = (((kb - 1) % kC2NC) + kC2NC) % kC2NC;
+  double* pCu = sC + sc0 * kC2CStride;         // C[kb-1]
+  double* pCm = sC + ((sc0 + kC2NC - 1) % kC2NC) * kC2CStride;
+  int bslot = 0;                               // unit barrier of plane u
+  unsigned bphase = 0;
+  double* gCu = gC + (long long)(kb - 1) * p.nxy;  // this lane's C pair at plane u
+  double* gEv = gE + (long long)(kb - 2) * p.nxy;  // this lane's E pair at plane u-1
 
   double2 am = in_z(kb - 2) ? *reinterpret_cast<const double2*>(sA + offA1) : zero2;
   double2 ac = in_z(kb - 1) ? *reinterpret_cast<const double2*>(sA + kC2APlane + offA1) : zero2;
@@ -195,13 +214,12 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
   double acc = 0.0;
 
   for (int u = kb - 1; u <= u_last; ++u) {
-    const int ui = u - (kb - 1);
-    mbar_wait(&bars[ui % kC2D], (ui / kC2D) & 1);
-    const double* Au = sA + sa * kC2APlane;
-    const double* Ap = sA + wrap_inc(sa, kC2NA) * kC2APlane;
-    const double* Bu = sB + sb * kC2EStride;
-    const double* Ru = sR + sr * kC2EStride;
-    double* Cu = sC + sc * kC2CStride;
+    mbar_wait(&bars[bslot], bphase);
+    const double* Au = pAu;
+    const double* Ap = pAp;
+    const double* Bu = pBu;
+    const double* Ru = pRu;
+    double* Cu = pCu;
     const bool plane_in = u >= p.c_lo && u < p.c_hi, has_p = in_z(u + 1);
     // ---------------- stage 1: C[u] pairs of the extended tile
     {
@@ -225,7 +243,7 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
           cv.x = p.rk1 * (((p.c3 * ac.x) - (p.rk1m1 * bb.x)) + p.c2 * (rr.x - y0));
           cv.y = p.rk1 * (((p.c3 * ac.y) - (p.rk1m1 * bb.y)) + p.c2 * (rr.y - y1));
         }
-        if (c_interior && u >= kb && u < ke) st2(gC + (long long)u * p.nxy, cv.x, cv.y);
+        if (c_interior && u >= kb && u < ke) st2(gCu, cv.x, cv.y);
       }
       *reinterpret_cast<double2*>(Cu + offB1) = cv;
       am = ac;
@@ -236,7 +254,7 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
     if (stage2) {
       const int v = u - 1;
       const double2 cp = *reinterpret_cast<const double2*>(Cu + offC2);
-      const double* Cv = sC + wrap_dec(sc, kC2NC) * kC2CStride;
+      const double* Cv = pCm;
       double cw = __shfl_up_sync(0xffffffffu, cc.y, 1);
       double ce = __shfl_down_sync(0xffffffffu, cc.x, 1);
       if (lane == 0) cw = Cv[offC2 - 1];
@@ -246,19 +264,18 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
         const double2 cn = *reinterpret_cast<const double2*>(Cv + offC2 + kC2W);
         const double y0 = stencil_point(d, cm.x, cs.x, cw, cc.x, cc.y, cn.x, cp.x);
         const double y1 = stencil_point(d, cm.y, cs.y, cc.x, cc.y, ce, cn.y, cp.y);
-        const double* Av = sA + wrap_dec(sa, kC2NA) * kC2APlane;  // A[v] = A[u-1]
-        const double2 av = *reinterpret_cast<const double2*>(Av + offA2);
+        const double2 av = *reinterpret_cast<const double2*>(pAm + offA2);  // A[v] = A[u-1]
         double2 rv, xo;
         if (kFirst) {
           rv = av;  // A == R == r
           xo = make_double2(av.x / p.theta, av.y / p.theta);  // x_0 = r / theta
         } else {
-          rv = *reinterpret_cast<const double2*>(sR + wrap_dec(sr, kC2NR) * kC2EStride + offC2);
+          rv = *reinterpret_cast<const double2*>(pRm + offC2);  // R[v]
           xo = av;  // x_{k-1}
         }
         const double e0 = p.rk2 * (((p.c3 * cc.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
         const double e1 = p.rk2 * (((p.c3 * cc.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
-        st2(gE + (long long)v * p.nxy, e0, e1);
+        st2(gEv, e0, e1);
         if (kRed) acc = acc + (rv.x * e0 + rv.y * e1);
       }
       cm = cc;
@@ -266,9 +283,8 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
     } else if (do_h) {
       double cx = 0.0;
       if (plane_in && h_in) {
-        const double* Am = sA + wrap_dec(sa, kC2NA) * kC2APlane;
         const double xc = Au[offAh];
-        const double y = stencil_point(d, in_z(u - 1) ? Am[offAh] : 0.0, Au[offAh - kC2W],
+        const double y = stencil_point(d, in_z(u - 1) ? pAm[offAh] : 0.0, Au[offAh - kC2W],
                                        Au[offAh - 1], xc, Au[offAh + 1], Au[offAh + kC2W],
                                        has_p ? Ap[offAh] : 0.0);
         if (kFirst) cx = p.c1 * ((2.0 * xc) - (y / p.theta));
@@ -278,10 +294,21 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
     }
     __syncthreads();
     if (tid == 0 && u + kC2D <= u_last) issue_unit(u + kC2D);
-    sa = wrap_inc(sa, kC2NA);
-    sb = wrap_inc(sb, kC2NB);
-    sr = wrap_inc(sr, kC2NR);
-    sc = wrap_inc(sc, kC2NC);
+    // rotate the rings and global pointers by one plane
+    pAm = pAu;
+    pAu = pAp;
+    pAp = (pAp + kC2APlane == sAend) ? sA : pAp + kC2APlane;
+    pBu = (pBu + kC2EStride == sBend) ? sB : pBu + kC2EStride;
+    pRm = pRu;
+    pRu = (pRu + kC2EStride == sRend) ? sR : pRu + kC2EStride;
+    pCm = pCu;
+    pCu = (pCu + kC2CStride == sCend) ? sC : pCu + kC2CStride;
+    if (++bslot == kC2D) {
+      bslot = 0;
+      bphase ^= 1u;
+    }
+    gCu += p.nxy;
+    gEv += p.nxy;
   }
   if (kRed) block_reduce_finish(acc, red);
 }
