@@ -242,9 +242,11 @@ def run_gpu(args):
             raise SystemExit("--gpus N > 1 must be launched with torchrun (one rank per GPU)")
     B.build()
     D = Dist(ws, rank, local)
-    if ws > 1:
+    # PCGX_BENCH_DIST=1: take the multi-GPU code path even at world size 1 (a
+    # 1-rank NCCL communicator; with PCGX_FORCE_NCCL=1 its all-reduces go through NCCL)
+    if ws > 1 or os.environ.get("PCGX_BENCH_DIST") == "1":
         nid = D.bcast_bytes(P.Context.nccl_unique_id() if rank == 0 else None)
-        ctx = P.Context(local, nranks=ws, rank=rank, nccl_id=nid)
+        ctx = P.Context(local, nranks=ws, rank=rank, nccl_id=nid, dist=True)
     else:
         ctx = P.Context(0)
     kind, (nx, ny, nz), degrees, desc = workload(args.config, ws)

@@ -351,7 +351,7 @@ struct LocalComm : CommBase {
 };
 
 void allreduce(pcgx_context c, int slot, int count) {
-  if (c->nranks == 1 || !c->cm) return;
+  if (!c->cm) return;
   c->cm->allreduce(c, slot, count);
   c->cur_allreduce++;
 }
@@ -843,6 +843,7 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
 struct Graph {
   cudaGraphExec_t exec = nullptr;
   int64_t kernels = 0;
+  int64_t allreduces = 0;
   ~Graph() {
     if (exec) cudaGraphExecDestroy(exec);
   }
@@ -851,6 +852,7 @@ struct Graph {
 template <class F>
 void capture(pcgx_context c, Graph& g, F&& body) {
   const int64_t before = c->cur_launches;
+  const int64_t before_ar = c->cur_allreduce;
   PCGX_CUDA(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
   c->capturing = true;
   try {
@@ -870,12 +872,15 @@ void capture(pcgx_context c, Graph& g, F&& body) {
   g.kernels = c->cur_launches - before;
   c->cur_launches = before;  // counted per replay instead
   c->launches -= g.kernels;
+  g.allreduces = c->cur_allreduce - before_ar;
+  c->cur_allreduce = before_ar;
 }
 
 void replay(pcgx_context c, Graph& g) {
   PCGX_CUDA(cudaGraphLaunch(g.exec, c->s));
   c->cur_launches += g.kernels;
   c->launches += g.kernels;
+  c->cur_allreduce += g.allreduces;
 }
 
 std::string fmt_double(double v) { return std::to_string(v); }
@@ -912,7 +917,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   // one GPU: snapshot r'r right after the update and overlap the host check with
   // the speculative P r; multi-GPU: merge [r'r, r'z] into one all-reduce after P r
   // (PCGX_MERGED=1 forces the multi-GPU schedule on one GPU, for tests)
-  const bool spec_after_update = (c->nranks == 1) && env_int("PCGX_MERGED", 0) == 0;
+  const bool spec_after_update = !c->cm && env_int("PCGX_MERGED", 0) == 0;
 
   std::memset(rep, 0, sizeof *rep);
   c->cur_launches = 0;
@@ -1448,7 +1453,9 @@ pcgx_status pcgx_context_create_dist(int device, int nranks, int rank, const voi
     c->rank = rank;
     c->nranks = nranks;
     ctx_init(c.get());
-    if (nranks > 1) {
+    // a 1-rank job has nothing to communicate; PCGX_FORCE_NCCL=1 still routes its
+    // all-reduces through a 1-rank NCCL communicator (exercises the NCCL path on one GPU)
+    if (nranks > 1 || env_int("PCGX_FORCE_NCCL", 0)) {
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof id);
       PCGX_NCCL(nccl().CommInitRank(&c->comm, nranks, id, rank));

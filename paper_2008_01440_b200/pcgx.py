@@ -228,12 +228,12 @@ class Context:
     one call at a time."""
 
     def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, nccl_id=None,
-                 _handle=None):
+                 dist: bool = False, _handle=None):
         L = lib()
         h = C.c_void_p()
         if _handle is not None:
             h = _handle
-        elif nranks == 1:
+        elif nranks == 1 and not dist:
             _check(L.pcgx_context_create(device, C.byref(h)))
         else:
             buf = C.create_string_buffer(bytes(nccl_id), 128)
