@@ -442,3 +442,24 @@ def test_pcg_csr_fallback_kernels(P, ctx, oracle, golden, monkeypatch):
         monkeypatch.setenv("PCGX_CSR_KERNEL", kern)
         _check_solve(P, oracle, c, csr(P, ctx, rp, ci, va),
                      OracleOp("csr", row_ptr=rp, col_idx=ci, values=va), len(rp) - 1)
+
+
+@pytest.mark.parametrize("k,iters,ddot,matvec,rel_res,err", [
+    (80, 8, 26, 649, 3.318e-9, 1.327e-7), (40, 14, 44, 575, 4.795e-9, 1.805e-7),
+    (20, 26, 80, 547, 6.173e-9, 2.144e-7), (10, 48, 146, 529, 9.230e-9, 2.850e-7),
+    (5, 87, 263, 523, 9.113e-9, 3.021e-7), (0, 380, 1142, 381, 9.798e-9, 2.000e-6)])
+def test_160_sweep_reference_known_answers(P, ctx, k, iters, ddot, matvec, rel_res, err):
+    """the reference itself on 160^3 matrix-free, s = 1.001,
+    x_true seed 20240801 (k-sweep table). Counters exact, iterations +-1."""
+    nx = 160
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    xt = P.random_uniform_vector(nx ** 3, SEED, ctx=ctx)
+    rhs = op.apply(xt)
+    x, rep = P.pcg_solve(op, rhs, None, P.ChebyshevPreconditioner(P.cheb_params(a, b, k, 1.001)))
+    assert abs(rep.iters - iters) <= 1 and rep.converged
+    if rep.iters == iters:
+        assert (rep.ddot, rep.matvec) == (ddot, matvec)
+        assert rep.rel_res == pytest.approx(rel_res, rel=2e-3)
+        assert rep.true_rel_res == pytest.approx(rel_res, rel=2e-3)
+        assert rel_norm(x.numpy(), xt.numpy()) == pytest.approx(err, rel=2e-3)
