@@ -252,15 +252,12 @@ def run_gpu(args):
     kind, (nx, ny, nz), degrees, desc = workload(args.config, ws)
     if args.degrees:
         degrees = [int(v) for v in args.degrees.split(",")]
-    if kind != "stencil" and ws > 1:
-        raise SystemExit("multi-GPU CSR is not built yet (SURVEY 8f.1); CSR configs run on 1 GPU")
     t_setup = time.perf_counter()
     op, alpha, beta, spmv_bytes, bounds = build_operator(P, ctx, kind, (nx, ny, nz))
     t_setup = time.perf_counter() - t_setup
     n_loc = op.local_size()
     n_glob = op.size()
-    xt = P.random_uniform_vector(n_loc, SEED, offset=(op.z0() * nx * ny if kind == "stencil" else 0),
-                                 ctx=ctx)
+    xt = P.random_uniform_vector(n_loc, SEED, offset=op.row0(), ctx=ctx)
     b = op.apply(xt)
     x = P.DeviceVector(ctx, n_loc)
     precs = {k: P.ChebyshevPreconditioner(P.cheb_params(alpha, beta, k, SCALE)) for k in degrees}
@@ -357,7 +354,8 @@ def run_gpu(args):
         "config": {"workload": args.config, "desc": desc, "grid": [nx, ny, nz],
                    "n_global": n_glob, "degrees": degrees, "theta_scale": SCALE, "tol": TOL,
                    "bounds": bounds, "alpha": alpha, "beta": beta,
-                   "parallelism": f"z-slab x{ws}", "setup_s": round(t_setup, 2),
+                   "parallelism": (f"z-slab x{ws}" if kind == "stencil" else f"block rows x{ws}"),
+                   "setup_s": round(t_setup, 2),
                    "spmv_equiv_bytes": spmv_bytes,
                    "l2": ("inputs larger than L2 (126 MB); no flush" if 8 * n_glob > 126e6 else
                           "vectors L2-resident (8 MB at 100^3): L2-bound, not an HBM roofline claim")},

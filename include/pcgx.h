@@ -118,6 +118,9 @@ void pcgx_slab_partition(int64_t nz, int nranks, int rank, int64_t* z0, int64_t*
 
 /* CsrMatrix (symmetric, both triangles, int64 host arrays as in the reference)
  * Jacobi-scaled. Narrowed to int32 on upload (PCGX_ERR_OVERFLOW if nnz >= 2^31).
+ * On a multi-rank context every rank passes the FULL matrix and keeps the block
+ * of rows [pcgx_operator_row0, + local_size) (balanced; vectors are that block);
+ * the columns other ranks own travel as a per-neighbour halo before each SpMV.
  * inv_sqrt_diag (n entries) may be NULL: it is then computed exactly as
  * jacobi_scale does (1/sqrt(diag), NumericalError naming the first diag <= 0).
  * Structural invariants are validated as CsrMatrix::validate does (symmetry of
@@ -134,6 +137,7 @@ void pcgx_operator_destroy(pcgx_operator op);
 int64_t pcgx_operator_size(pcgx_operator op);        /* global n */
 int64_t pcgx_operator_local_size(pcgx_operator op);  /* rows owned by this rank */
 int64_t pcgx_operator_z0(pcgx_operator op);          /* first owned plane (stencil) */
+int64_t pcgx_operator_row0(pcgx_operator op);        /* first owned global row (any kind) */
 int64_t pcgx_operator_nnz(pcgx_operator op);         /* CSR nnz, or the assembled-equivalent for stencils */
 /* Number of matvecs applied so far (LinearOperator::matvec_count, linop.hpp:37). */
 uint64_t pcgx_operator_matvec_count(pcgx_operator op);

@@ -273,8 +273,13 @@ struct InVec {
   const double* __restrict__ x;
   const double* glo;  // ghost plane below the slab (or nullptr: Dirichlet)
   const double* ghi;
+  const double* gx;   // CSR block rows: values of the ghost columns (index - nloc)
+  long long nloc;
   __device__ __forceinline__ void init() {}
   __device__ __forceinline__ double ld1(long long i) const { return __ldg(x + i); }
+  __device__ __forceinline__ double ldc(long long c) const {
+    return c < nloc ? __ldg(x + c) : __ldg(gx + (c - nloc));
+  }
   __device__ __forceinline__ double2 ld2(long long i) const { return ldg2(x + i); }
   __device__ __forceinline__ void pf(long long i) const { prefetch_l2(x + i); }
   __device__ __forceinline__ double glo1(long long c) const { return glo ? __ldg(glo + c) : 0.0; }
@@ -293,12 +298,18 @@ struct InComb {
   const double* S;
   int s_new, s_old, first;
   const double *zlo, *zhi, *plo, *phi;  // ghost planes of z and p_old
+  const double *gz, *gp;                // CSR block rows: ghost columns of z and p_old
+  long long nloc;
   double beta;
   __device__ __forceinline__ void init() { beta = first ? 0.0 : S[s_new] / S[s_old]; }
   __device__ __forceinline__ double f(double zv, double pv) const {
     return first ? zv : zv + beta * pv;
   }
   __device__ __forceinline__ double ld1(long long i) const { return f(__ldg(z + i), first ? 0.0 : __ldg(p + i)); }
+  __device__ __forceinline__ double ldc(long long c) const {
+    if (c < nloc) return ld1(c);
+    return f(__ldg(gz + (c - nloc)), first ? 0.0 : __ldg(gp + (c - nloc)));
+  }
   __device__ __forceinline__ double2 ld2(long long i) const {
     const double2 a = ldg2(z + i);
     if (first) return a;
@@ -698,6 +709,7 @@ csr2_kernel(Csr2Geom g, const double* __restrict__ x, Epi epi, Reduce red) {
 struct SellGeom {
   int n;
   int nslices;
+  int s_begin, s_end;          // slices of this launch
   const long long* slice_ptr;  // nslices + 1 (entries)
   const int* rowlen;           // n
   const int* col;              // padded
@@ -720,7 +732,7 @@ sell_kernel(SellGeom g, In in, Epi epi, Reduce red) {
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   double acc = 0.0;
-  for (int s = blockIdx.x * wpb + (threadIdx.x >> 5); s < g.nslices; s += gridDim.x * wpb) {
+  for (int s = g.s_begin + blockIdx.x * wpb + (threadIdx.x >> 5); s < g.s_end; s += gridDim.x * wpb) {
     const int row = s * 32 + lane;
     const long long base = __ldg(g.slice_ptr + s) + lane;
     const int L = (int)((__ldg(g.slice_ptr + s + 1) - __ldg(g.slice_ptr + s)) >> 5);
@@ -742,8 +754,8 @@ sell_kernel(SellGeom g, In in, Epi epi, Reduce red) {
         const long long e = base + (long long)(k + q) * 32;
         const int c = on ? __ldg(g.col + e) : 0;
         vv[q] = on ? __ldg(g.val + e) : 0.0;
-        dv[q] = on ? __ldg(g.dvec + c) : 0.0;
-        xv[q] = on ? in.ld1(c) : 0.0;
+        dv[q] = on ? __ldg(g.dvec + c) : 0.0;  // dvec spans the ghost columns too
+        xv[q] = on ? in.ldc(c) : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < kSellBatch; ++q)
@@ -883,6 +895,15 @@ splitmix_kernel(long long n, unsigned long long seed, unsigned long long offset,
     const double u = (double)(z >> 11) * 0x1.0p-53;
     out[i] = 2.0 * u - 1.0;
   }
+}
+
+// out[k] = x[idx[k]] (send buffers of the CSR block-row halo)
+__global__ void __launch_bounds__(kVecThreads)
+pack_kernel(long long n, const int* __restrict__ idx, const double* __restrict__ x,
+            double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = x[idx[i]];
 }
 
 // Writes a large scratch buffer (flushes L2 between timed iterations).

@@ -92,6 +92,14 @@ struct pcgx_operator_s {
   double* sell_val = nullptr;
   int nslices = 0;
   long long sell_padded = 0;
+  // CSR block rows on a multi-rank context: this rank owns rows [row0, row0 + n_local);
+  // columns >= n_local index the ghost array (values of other ranks' rows)
+  long long row0 = 0, nghost = 0, nsend = 0;
+  int* send_idx = nullptr;                 // concatenated per-neighbour send lists (local rows)
+  double *sbuf_z = nullptr, *sbuf_p = nullptr, *ghost_z = nullptr, *ghost_p = nullptr;
+  std::vector<int> nb_rank;                // neighbours with traffic
+  std::vector<long long> send_off, send_cnt, recv_off, recv_cnt;
+  int sl_b0 = 0, sl_b1 = 0;                // slices [sl_b0, sl_b1) read no ghost column
   int ntiles = 0;
   int *rp = nullptr, *ci = nullptr;
   double *va = nullptr, *dvec = nullptr;
@@ -263,6 +271,10 @@ struct CommBase {
     long long count;
   };
   virtual void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) = 0;
+  // CSR block rows: send nv packed buffers' per-neighbour segments, receive the
+  // neighbours' segments into the ghost arrays (op->nb_rank / send_* / recv_*).
+  virtual void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
+                           double* const* gbuf) = 0;
   virtual bool graph_capturable() const = 0;
 };
 namespace {
@@ -274,6 +286,8 @@ struct NcclComm : CommBase {
   void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override;
   void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
   void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override;
+  void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
+                   double* const* gbuf) override;
   bool graph_capturable() const override { return true; }
 };
 
@@ -315,13 +329,14 @@ struct LocalGroup {
   std::vector<pcgx_context> ctx;
   std::vector<double*> ghost_lo, ghost_hi, ghost_lo2, ghost_hi2;
   std::vector<std::vector<double*>> xrecv_lo, xrecv_hi;  // per rank, per xchg item
+  std::vector<std::vector<double*>> srecv;               // [rank][v * nranks + src] ghost destination
   std::vector<cudaEvent_t> ev_ar;   // rank's contribution copied
   std::vector<cudaEvent_t> ev_done; // rank finished reading contributions
   double* contrib = nullptr;        // nranks * kSlots doubles on the first rank's device
   std::atomic<int> refs{0};
   explicit LocalGroup(int n)
       : nranks(n), bar(n), ctx(n), ghost_lo(n), ghost_hi(n), ghost_lo2(n), ghost_hi2(n),
-        xrecv_lo(n), xrecv_hi(n), ev_ar(n), ev_done(n) {}
+        xrecv_lo(n), xrecv_hi(n), srecv(n), ev_ar(n), ev_done(n) {}
 };
 
 struct LocalComm : CommBase {
@@ -342,11 +357,13 @@ struct LocalComm : CommBase {
     g->bar.wait();
   }
   void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override;
-  void halo_wait(pcgx_context c) override {
-    if (rank > 0) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[rank - 1]->ev_join, 0));
-    if (rank < g->nranks - 1) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[rank + 1]->ev_join, 0));
+  void halo_wait(pcgx_context c) override {  // my ghosts are written by the other ranks' copies
+    for (int q = 0; q < g->nranks; ++q)
+      if (q != rank) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[q]->ev_join, 0));
   }
   void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override;
+  void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
+                   double* const* gbuf) override;
   bool graph_capturable() const override { return false; }
 };
 
@@ -453,6 +470,47 @@ void LocalComm::xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int 
   g->bar.wait();
 }
 
+void NcclComm::sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
+                           double* const* gbuf) {
+  PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+  PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+  PCGX_NCCL(nccl().GroupStart());
+  for (int v = 0; v < nv; ++v)
+    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
+      const int q = op->nb_rank[i];
+      if (op->send_cnt[i])
+        PCGX_NCCL(nccl().Send(sbuf[v] + op->send_off[i], (size_t)op->send_cnt[i], ncclDouble, q, c->comm, c->cs));
+      if (op->recv_cnt[i])
+        PCGX_NCCL(nccl().Recv(gbuf[v] + op->recv_off[i], (size_t)op->recv_cnt[i], ncclDouble, q, c->comm, c->cs));
+    }
+  PCGX_NCCL(nccl().GroupEnd());
+  PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+}
+
+void LocalComm::sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
+                            double* const* gbuf) {
+  const int P = g->nranks;
+  auto& mine = g->srecv[rank];
+  mine.assign((size_t)nv * P, nullptr);
+  for (int v = 0; v < nv; ++v)
+    for (size_t i = 0; i < op->nb_rank.size(); ++i)
+      mine[(size_t)v * P + op->nb_rank[i]] = gbuf[v] + op->recv_off[i];
+  PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+  g->bar.wait();
+  PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+  for (size_t i = 0; i < op->nb_rank.size(); ++i)  // the receiver no longer reads its ghosts
+    PCGX_CUDA(cudaStreamWaitEvent(c->cs, g->ctx[op->nb_rank[i]]->ev_fork, 0));
+  for (int v = 0; v < nv; ++v)
+    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
+      if (!op->send_cnt[i]) continue;
+      const int q = op->nb_rank[i];
+      PCGX_CUDA(cudaMemcpyAsync(g->srecv[q][(size_t)v * P + rank], sbuf[v] + op->send_off[i],
+                                sizeof(double) * (size_t)op->send_cnt[i], cudaMemcpyDefault, c->cs));
+    }
+  PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+  g->bar.wait();
+}
+
 StencilGeom geom_of(pcgx_operator op) {
   StencilGeom g;
   g.nx = (int)op->nx;
@@ -487,7 +545,8 @@ void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, cons
 // Input policies with the operator's ghost planes attached (or stripped for the
 // interior planes of a slab, which need none).
 InVec in_of(pcgx_operator op, const double* x, bool ghosts) {
-  return InVec{x, ghosts ? op->ghost_lo : nullptr, ghosts ? op->ghost_hi : nullptr};
+  return InVec{x, ghosts ? op->ghost_lo : nullptr, ghosts ? op->ghost_hi : nullptr, op->ghost_z,
+               op->n_local};
 }
 InComb in_of(pcgx_operator op, const double* z, const double* p, const double* S, int s_new,
              int s_old, int first, bool ghosts) {
@@ -502,9 +561,16 @@ InComb in_of(pcgx_operator op, const double* z, const double* p, const double* S
   in.zhi = ghosts ? op->ghost_hi : nullptr;
   in.plo = ghosts ? op->ghost_lo2 : nullptr;
   in.phi = ghosts ? op->ghost_hi2 : nullptr;
+  in.gz = op->ghost_z;
+  in.gp = op->ghost_p;
+  in.nloc = op->n_local;
   return in;
 }
-InVec strip(const InVec& in) { return InVec{in.x, nullptr, nullptr}; }
+InVec strip(const InVec& in) {
+  InVec o = in;
+  o.glo = o.ghi = nullptr;
+  return o;
+}
 InComb strip(const InComb& in) {
   InComb o = in;
   o.zlo = o.zhi = o.plo = o.phi = nullptr;
@@ -529,15 +595,42 @@ template <class In, class Epi, bool kRed>
 void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi, int slot) {
   op->matvecs.fetch_add(1, std::memory_order_relaxed);
   if (op->kind == 1 && op->sell_ptr) {
-    SellGeom g{(int)op->n_local, op->nslices, op->sell_ptr, op->sell_len, op->sell_col, op->sell_val,
-               op->dvec};
-    const int wpb = 8;
-    const int want = (op->nslices + wpb - 1) / wpb;
-    const int grid = std::max(1, std::min(want, c->sms * env_int("PCGX_SELL_BPS", 8)));
-    Reduce red = kRed ? make_red(c, slot) : Reduce{};
-    sell_kernel<In, Epi, kRed><<<grid, 32 * wpb, 0, c->s>>>(g, in, epi, red);
-    check_launch();
-    count_launch(c);
+    auto sell = [&](int s0, int s1, bool accumulate) {
+      if (s1 <= s0) return;
+      SellGeom g{(int)op->n_local, op->nslices, s0, s1, op->sell_ptr, op->sell_len, op->sell_col,
+                 op->sell_val, op->dvec};
+      const int wpb = 8;
+      const int want = (s1 - s0 + wpb - 1) / wpb;
+      const int grid = std::max(1, std::min(want, c->sms * env_int("PCGX_SELL_BPS", 8)));
+      Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
+      sell_kernel<In, Epi, kRed><<<grid, 32 * wpb, 0, c->s>>>(g, in, epi, red);
+      check_launch();
+      count_launch(c);
+    };
+    if (op->nb_rank.empty()) {
+      sell(0, op->nslices, false);
+      return;
+    }
+    // block-row halo: pack the rows other ranks reference, exchange, overlap the
+    // ghost-free slices with the transfer, then the slices that read ghost columns
+    const double* src[2];
+    const int nv = halo_vecs(in, src);
+    const double* sb[2] = {op->sbuf_z, op->sbuf_p};
+    double* gb[2] = {op->ghost_z, op->ghost_p};
+    for (int v = 0; v < nv; ++v) {
+      if (!op->nsend) break;
+      pack_kernel<<<vec_grid(c, op->nsend), kVecThreads, 0, c->s>>>(op->nsend, op->send_idx, src[v],
+                                                                     const_cast<double*>(sb[v]));
+      check_launch();
+      count_launch(c);
+    }
+    c->cm->sparse_xchg(c, op, nv, sb, gb);
+    c->cur_halo_bytes += (long long)nv * op->nsend * 8;
+    sell(op->sl_b0, op->sl_b1, false);
+    const bool wrote = op->sl_b1 > op->sl_b0;
+    c->cm->halo_wait(c);
+    sell(0, op->sl_b0, wrote);
+    sell(op->sl_b1, op->nslices, wrote || op->sl_b0 > 0);
     return;
   }
   if constexpr (std::is_same_v<In, InVec>) {
@@ -1186,7 +1279,7 @@ void lanczos_device(pcgx_context c, pcgx_operator op, int steps_hi, int steps, u
   double* v = c->t0;
   double* vprev = c->t1;
   double* w = c->w0;
-  const unsigned long long offset = (unsigned long long)(op->kind == 0 ? op->z0 * op->nx * op->ny : 0);
+  const unsigned long long offset = (unsigned long long)pcgx_operator_row0(op);
   splitmix_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, seed, offset, v);
   check_launch();
   count_launch(c);
@@ -1253,6 +1346,195 @@ int default_kz(pcgx_context c, long long nx, long long ny, long long nzl) {
   return 16;
 }
 
+void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
+                const std::vector<int>& ci32, const double* va);
+
+// CSR block rows (the paper's MPI block-row SpMV): this rank
+// keeps rows [row0, row0 + nloc) with columns remapped to the local space:
+// owned columns -> [0, nloc), others -> nloc + (position in the ascending list
+// of ghost columns). Entries keep their order (the reference's summation order).
+// Each rank holds the full matrix on the host, so the send lists (the rows of
+// mine other ranks' rows reference) are computed without communication.
+void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::vector<int>& rp32,
+                      const std::vector<int>& ci32, const double* va, const std::vector<double>& dv) {
+  const int P = c->nranks, me = c->rank;
+  std::vector<long long> start(P + 1);
+  for (int q = 0; q < P; ++q) {
+    int64_t z0, nl;
+    pcgx_slab_partition(n, P, q, &z0, &nl);
+    start[(size_t)q] = z0;
+  }
+  start[(size_t)P] = n;
+  auto owner = [&](long long col) {
+    return (int)(std::upper_bound(start.begin(), start.end(), col) - start.begin()) - 1;
+  };
+  const long long r0 = start[(size_t)me], r1 = start[(size_t)me + 1], nloc = r1 - r0;
+  if (nloc < 1) fail(PCGX_ERR_INVALID, "csr_create: fewer rows than ranks");
+  // ghost columns of my rows, ascending (hence grouped by owner)
+  std::vector<int> ghosts;
+  for (long long i = r0; i < r1; ++i)
+    for (int k = rp32[(size_t)i]; k < rp32[(size_t)i + 1]; ++k) {
+      const int col = ci32[(size_t)k];
+      if (col < r0 || col >= r1) ghosts.push_back(col);
+    }
+  std::sort(ghosts.begin(), ghosts.end());
+  ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+  // local CSR
+  const long long k0 = rp32[(size_t)r0];
+  std::vector<int> lrp((size_t)nloc + 1), lci((size_t)(rp32[(size_t)r1] - k0));
+  for (long long i = r0; i <= r1; ++i) lrp[(size_t)(i - r0)] = (int)(rp32[(size_t)i] - k0);
+  for (long long k = k0; k < rp32[(size_t)r1]; ++k) {
+    const int col = ci32[(size_t)k];
+    lci[(size_t)(k - k0)] = (col >= r0 && col < r1)
+                                ? (int)(col - r0)
+                                : (int)(nloc + (std::lower_bound(ghosts.begin(), ghosts.end(), col) -
+                                                ghosts.begin()));
+  }
+  // per-neighbour traffic: recv = my ghosts owned by q; send = my rows q's rows reference
+  op->nb_rank.clear();
+  op->send_off.clear();
+  op->send_cnt.clear();
+  op->recv_off.clear();
+  op->recv_cnt.clear();
+  std::vector<int> send_idx;
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    const long long lo = std::lower_bound(ghosts.begin(), ghosts.end(), (int)start[(size_t)q]) - ghosts.begin();
+    const long long hi = std::lower_bound(ghosts.begin(), ghosts.end(), (int)start[(size_t)q + 1]) - ghosts.begin();
+    std::vector<int> need;  // rows of mine referenced by q's rows, ascending
+    for (long long i = start[(size_t)q]; i < start[(size_t)q + 1]; ++i)
+      for (int k = rp32[(size_t)i]; k < rp32[(size_t)i + 1]; ++k) {
+        const int col = ci32[(size_t)k];
+        if (col >= r0 && col < r1) need.push_back(col);
+      }
+    std::sort(need.begin(), need.end());
+    need.erase(std::unique(need.begin(), need.end()), need.end());
+    if (hi == lo && need.empty()) continue;
+    op->nb_rank.push_back(q);
+    op->recv_off.push_back(lo);
+    op->recv_cnt.push_back(hi - lo);
+    op->send_off.push_back((long long)send_idx.size());
+    op->send_cnt.push_back((long long)need.size());
+    for (int col : need) send_idx.push_back((int)(col - r0));
+  }
+  op->row0 = r0;
+  op->n_local = nloc;
+  op->nghost = (long long)ghosts.size();
+  op->nsend = (long long)send_idx.size();
+  std::vector<double> dext((size_t)(nloc + op->nghost));
+  for (long long i = 0; i < nloc; ++i) dext[(size_t)i] = dv[(size_t)(r0 + i)];
+  for (long long g = 0; g < op->nghost; ++g) dext[(size_t)(nloc + g)] = dv[(size_t)ghosts[(size_t)g]];
+  PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * dext.size()));
+  PCGX_CUDA(cudaMemcpy(op->dvec, dext.data(), sizeof(double) * dext.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMalloc(&op->rp, sizeof(int) * lrp.size()));
+  PCGX_CUDA(cudaMemcpy(op->rp, lrp.data(), sizeof(int) * lrp.size(), cudaMemcpyHostToDevice));
+  const size_t ng = (size_t)std::max(op->nghost, 1LL), nsd = (size_t)std::max(op->nsend, 1LL);
+  PCGX_CUDA(cudaMalloc(&op->send_idx, sizeof(int) * nsd));
+  if (op->nsend)
+    PCGX_CUDA(cudaMemcpy(op->send_idx, send_idx.data(), sizeof(int) * send_idx.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMalloc(&op->sbuf_z, sizeof(double) * nsd));
+  PCGX_CUDA(cudaMalloc(&op->sbuf_p, sizeof(double) * nsd));
+  PCGX_CUDA(cudaMalloc(&op->ghost_z, sizeof(double) * ng));
+  PCGX_CUDA(cudaMalloc(&op->ghost_p, sizeof(double) * ng));
+  build_sell(op, nloc, lrp, lci, va + k0);
+}
+
+// SELL-32 arrays of an int32 CSR (n rows, local column space) -> op (see sell_kernel).
+void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
+                const std::vector<int>& ci32, const double* va) {
+  const long long ns = (n + 31) / 32;
+  std::vector<long long> sp((size_t)ns + 1, 0);
+  std::vector<int> rl((size_t)std::max(n, 1LL));
+  for (long long sI = 0; sI < ns; ++sI) {
+    int L = 0;
+    for (long long r = sI * 32; r < std::min(n, sI * 32 + 32); ++r) {
+      rl[(size_t)r] = rp32[(size_t)r + 1] - rp32[(size_t)r];
+      L = std::max(L, rl[(size_t)r]);
+    }
+    sp[(size_t)sI + 1] = sp[(size_t)sI] + 32LL * L;
+  }
+  const long long tot = sp[(size_t)ns];
+  std::vector<int> scol((size_t)std::max(tot, 1LL), 0);
+  std::vector<double> sval((size_t)std::max(tot, 1LL), 0.0);
+#pragma omp parallel for schedule(static)
+  for (long long sI = 0; sI < ns; ++sI)
+    for (long long r = sI * 32; r < std::min(n, sI * 32 + 32); ++r) {
+      const long long lane = r - sI * 32;
+      for (int k = 0; k < rl[(size_t)r]; ++k) {
+        const long long src = rp32[(size_t)r] + k;
+        const long long dst = sp[(size_t)sI] + 32LL * k + lane;
+        scol[(size_t)dst] = ci32[(size_t)src];
+        sval[(size_t)dst] = va[src];
+      }
+    }
+  op->nslices = (int)ns;
+  PCGX_CUDA(cudaMalloc(&op->sell_ptr, sizeof(long long) * sp.size()));
+  PCGX_CUDA(cudaMalloc(&op->sell_len, sizeof(int) * rl.size()));
+  PCGX_CUDA(cudaMalloc(&op->sell_col, sizeof(int) * scol.size()));
+  PCGX_CUDA(cudaMalloc(&op->sell_val, sizeof(double) * sval.size()));
+  PCGX_CUDA(cudaMemcpy(op->sell_ptr, sp.data(), sizeof(long long) * sp.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMemcpy(op->sell_len, rl.data(), sizeof(int) * rl.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMemcpy(op->sell_col, scol.data(), sizeof(int) * scol.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMemcpy(op->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice));
+  op->sell_padded = tot;
+  // slices that touch no ghost column (local columns are < n): run while the halo travels
+  int b0 = (int)ns, b1 = 0;
+  for (long long sI = 0; sI < ns; ++sI) {
+    bool ghost = false;
+    for (long long r = sI * 32; r < std::min(n, sI * 32 + 32) && !ghost; ++r)
+      for (int k = rp32[(size_t)r]; k < rp32[(size_t)r + 1]; ++k)
+        if (ci32[(size_t)k] >= n) {
+          ghost = true;
+          break;
+        }
+    if (ghost) {
+      b0 = std::min(b0, (int)sI);
+      b1 = std::max(b1, (int)sI + 1);
+    }
+  }
+  if (b0 >= b1) {  // no ghost anywhere
+    op->sl_b0 = 0;
+    op->sl_b1 = (int)ns;
+  } else {  // ghost slices are a prefix and a suffix for block rows: interior in between
+    int lead = 0;
+    while (lead < (int)ns) {
+      bool ghost = false;
+      for (long long r = (long long)lead * 32; r < std::min(n, (long long)lead * 32 + 32) && !ghost; ++r)
+        for (int k = rp32[(size_t)r]; k < rp32[(size_t)r + 1]; ++k)
+          if (ci32[(size_t)k] >= n) {
+            ghost = true;
+            break;
+          }
+      if (!ghost) break;
+      ++lead;
+    }
+    int trail = (int)ns;
+    while (trail > lead) {
+      bool ghost = false;
+      const long long sI = trail - 1;
+      for (long long r = sI * 32; r < std::min(n, sI * 32 + 32) && !ghost; ++r)
+        for (int k = rp32[(size_t)r]; k < rp32[(size_t)r + 1]; ++k)
+          if (ci32[(size_t)k] >= n) {
+            ghost = true;
+            break;
+          }
+      if (!ghost) break;
+      --trail;
+    }
+    // any ghost slice strictly inside [lead, trail) forces the whole range after the halo
+    bool inner_ghost = false;
+    for (long long sI = lead; sI < trail && !inner_ghost; ++sI)
+      for (long long r = sI * 32; r < std::min(n, sI * 32 + 32) && !inner_ghost; ++r)
+        for (int k = rp32[(size_t)r]; k < rp32[(size_t)r + 1]; ++k)
+          if (ci32[(size_t)k] >= n) {
+            inner_ghost = true;
+            break;
+          }
+    op->sl_b0 = inner_ghost ? 0 : lead;
+    op->sl_b1 = inner_ghost ? 0 : trail;
+  }
+}
+
 template <class IdxT>
 void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, const IdxT* ci,
                 const double* va, const double* inv_sqrt) {
@@ -1265,7 +1547,7 @@ void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, c
                                 " does not fit the int32 device CSR");
   std::vector<int> rp32((size_t)n + 1);
   std::vector<int> ci32((size_t)nnz);
-  std::vector<double> dv((size_t)n);
+  std::vector<double> dv((size_t)std::max(n, 1LL));
   for (long long i = 0; i < n; ++i) {
     if (rp[i + 1] < rp[i]) fail(PCGX_ERR_INVALID, "CsrMatrix: row_ptr not nondecreasing");
     double diag = 0.0;
@@ -1289,8 +1571,13 @@ void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, c
     }
   }
   op->kind = 1;
-  op->n_global = op->n_local = n;
+  op->n_global = n;
   op->nnz = nnz;
+  if (c->nranks > 1) {
+    csr_upload_block(c, op, n, rp32, ci32, va, dv);
+    return;
+  }
+  op->n_local = n;
   PCGX_CUDA(cudaMalloc(&op->rp, sizeof(int) * (size_t)(n + 1)));
   // +8 entries of padding: the TMA tile copies round their length up to 4 entries
   PCGX_CUDA(cudaMalloc(&op->ci, sizeof(int) * (size_t)(nnz + 8)));
@@ -1306,43 +1593,7 @@ void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, c
   if (n) PCGX_CUDA(cudaMemcpy(op->dvec, dv.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice));
   const int ckern = env_int("PCGX_CSR_KERNEL", 0);  // 0 sell (default), 1 tma tiles, 2 chunked
   if (ckern == 0 && n > 0) {
-    const long long ns = (n + 31) / 32;
-    std::vector<long long> sp((size_t)ns + 1, 0);
-    std::vector<int> rl((size_t)n);
-    for (long long sI = 0; sI < ns; ++sI) {
-      int L = 0;
-      for (long long r = sI * 32; r < std::min(n, sI * 32 + 32); ++r) {
-        rl[(size_t)r] = rp32[(size_t)r + 1] - rp32[(size_t)r];
-        L = std::max(L, rl[(size_t)r]);
-      }
-      sp[(size_t)sI + 1] = sp[(size_t)sI] + 32LL * L;
-    }
-    const long long tot = sp[(size_t)ns];
-    std::vector<int> scol((size_t)tot, 0);
-    std::vector<double> sval((size_t)tot, 0.0);
-#pragma omp parallel for schedule(static)
-    for (long long sI = 0; sI < ns; ++sI)
-      for (long long r = sI * 32; r < std::min(n, sI * 32 + 32); ++r) {
-        const long long lane = r - sI * 32;
-        for (int k = 0; k < rl[(size_t)r]; ++k) {
-          const long long src = rp32[(size_t)r] + k;
-          const long long dst = sp[(size_t)sI] + 32LL * k + lane;
-          scol[(size_t)dst] = ci32[(size_t)src];
-          sval[(size_t)dst] = va[src];
-        }
-      }
-    op->nslices = (int)ns;
-    PCGX_CUDA(cudaMalloc(&op->sell_ptr, sizeof(long long) * sp.size()));
-    PCGX_CUDA(cudaMalloc(&op->sell_len, sizeof(int) * (size_t)n));
-    PCGX_CUDA(cudaMalloc(&op->sell_col, sizeof(int) * (size_t)std::max(tot, 1LL)));
-    PCGX_CUDA(cudaMalloc(&op->sell_val, sizeof(double) * (size_t)std::max(tot, 1LL)));
-    PCGX_CUDA(cudaMemcpy(op->sell_ptr, sp.data(), sizeof(long long) * sp.size(), cudaMemcpyHostToDevice));
-    PCGX_CUDA(cudaMemcpy(op->sell_len, rl.data(), sizeof(int) * (size_t)n, cudaMemcpyHostToDevice));
-    if (tot) {
-      PCGX_CUDA(cudaMemcpy(op->sell_col, scol.data(), sizeof(int) * (size_t)tot, cudaMemcpyHostToDevice));
-      PCGX_CUDA(cudaMemcpy(op->sell_val, sval.data(), sizeof(double) * (size_t)tot, cudaMemcpyHostToDevice));
-    }
-    op->sell_padded = tot;
+    build_sell(op, n, rp32, ci32, va);
     // the SELL copy replaces the CSR value/index arrays on the device
     cudaFree(op->ci);
     cudaFree(op->va);
@@ -1387,6 +1638,11 @@ void free_op(pcgx_operator op) {
   cudaFree(op->sell_len);
   cudaFree(op->sell_col);
   cudaFree(op->sell_val);
+  cudaFree(op->send_idx);
+  cudaFree(op->sbuf_z);
+  cudaFree(op->sbuf_p);
+  cudaFree(op->ghost_z);
+  cudaFree(op->ghost_p);
   delete op;
 }
 
@@ -1642,7 +1898,6 @@ pcgx_status pcgx_csr_create(pcgx_context c, int64_t n, const int64_t* row_ptr,
                             const double* inv_sqrt_diag, pcgx_operator* out) {
   return guarded(c, [&] {
     set_device(c);
-    if (c->nranks > 1) fail(PCGX_ERR_UNSUPPORTED, "csr_create: multi-GPU CSR is not built yet");
     auto op = new pcgx_operator_s();
     op->ctx = c;
     try {
@@ -1660,7 +1915,6 @@ pcgx_status pcgx_csr_create_i32(pcgx_context c, int64_t n, const int32_t* row_pt
                                 const double* inv_sqrt_diag, pcgx_operator* out) {
   return guarded(c, [&] {
     set_device(c);
-    if (c->nranks > 1) fail(PCGX_ERR_UNSUPPORTED, "csr_create: multi-GPU CSR is not built yet");
     auto op = new pcgx_operator_s();
     op->ctx = c;
     try {
@@ -1683,6 +1937,10 @@ void pcgx_operator_destroy(pcgx_operator op) {
 int64_t pcgx_operator_size(pcgx_operator op) { return op ? op->n_global : -1; }
 int64_t pcgx_operator_local_size(pcgx_operator op) { return op ? op->n_local : -1; }
 int64_t pcgx_operator_z0(pcgx_operator op) { return op ? op->z0 : -1; }
+int64_t pcgx_operator_row0(pcgx_operator op) {
+  if (!op) return -1;
+  return op->kind == 0 ? op->z0 * op->nx * op->ny : op->row0;
+}
 int64_t pcgx_operator_nnz(pcgx_operator op) { return op ? op->nnz : -1; }
 uint64_t pcgx_operator_matvec_count(pcgx_operator op) { return op ? op->matvecs.load() : 0; }
 

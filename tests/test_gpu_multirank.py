@@ -91,3 +91,56 @@ def test_slab_lanczos_matches_single_domain(pcgx):
     for c in ctxs:
         c.close()
     single.close()
+
+
+@pytest.mark.parametrize("nranks,gen,m", [(2, "fe27", 6), (3, "elast27", 4), (4, "lap", 5)])
+def test_csr_block_rows_match_single_domain(pcgx, oracle, nranks, gen, m):
+    """Multi-rank CSR (block rows + per-neighbour halo, SELL kernel): SpMV and P_m(A) r
+    bitwise equal to the single-domain oracle, the solve within the PCG bar."""
+    P = pcgx
+    if gen == "fe27":
+        A = P.gen_fe27(10, 1.0, SEED)
+    elif gen == "elast27":
+        A = P.gen_elast27(6, 1.0, 0.5, 0.1, SEED)
+    else:
+        from tests._util import lap3d_csr
+        rp, ci, va = lap3d_csr(11)
+        A = P.CsrMatrix(11 ** 3, rp, ci, va)
+    n = A.n
+    opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    a, b = 0.005, 2.5
+    xt_full = oracle.random_uniform(n, SEED)
+    b_full = oracle.apply(opo, xt_full)
+    prm_o = oracle.cheb_params(a, b, m, 1.001)
+    x_full, rep_o = oracle.pcg_solve(opo, prm_o, b_full)
+    r_full = oracle.random_uniform(n, 77)
+    z_full = oracle.apply_chebyshev(opo, prm_o, r_full)
+    ctxs = P.Context.local_group(nranks)
+
+    def rank(r, ctx):
+        op, _ = P.jacobi_scale(A, ctx)
+        lo = op.row0()
+        hi = lo + op.local_size()
+        assert (lo, op.local_size()) == P.slab_partition(n, nranks, r)
+        bl = op.apply(P.random_uniform_vector(op.local_size(), SEED, offset=lo))
+        zl = P.apply_chebyshev(P.cheb_params(a, b, m, 1.001), op, r_full[lo:hi])
+        x, rep = P.pcg_solve(op, bl, P.SolveOptions(),
+                             P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001)))
+        lo2, hi2 = P.lanczos_bounds(op, 10, 15, SEED)
+        return bl, zl, x, rep, (lo2, hi2)
+
+    outs = run_ranks(ctxs, rank)
+    assert np.array_equal(np.concatenate([o[0] for o in outs]), b_full)
+    assert np.array_equal(np.concatenate([o[1] for o in outs]), z_full)
+    reps = [o[3] for o in outs]
+    assert all(r.iters == reps[0].iters for r in reps) and reps[0].converged
+    assert abs(reps[0].iters - rep_o["iters"]) <= 1
+    if reps[0].iters == rep_o["iters"]:
+        assert rel_norm(np.concatenate([o[2] for o in outs]), x_full) <= 1e-10
+    assert all(r.halo_bytes > 0 for r in reps)
+    olo, _, al, be = oracle.lanczos(opo, 15, SEED)
+    _, ohi = oracle.tridiag_extremes(al[:10], be[:10])
+    for o in outs:
+        assert o[4][0] == pytest.approx(olo, rel=1e-8) and o[4][1] == pytest.approx(ohi, rel=1e-8)
+    for c in ctxs:
+        c.close()
