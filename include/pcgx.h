@@ -237,6 +237,16 @@ void pcgx_analytic_extremes_box(int64_t nx, int64_t ny, int64_t nz, double* lo, 
 pcgx_status pcgx_lanczos_bounds(pcgx_context ctx, pcgx_operator op, int steps_hi, int steps,
                                 uint64_t seed, double* lo, double* hi);
 
+/* power_method and dacg_smallest (include/polycg/eigenest.hpp:29-45;
+ * src/eigenest.cpp:48-167) on the device: same iteration and stopping rules,
+ * the seeded start vector of random_uniform_vector; out4 = {value, iters,
+ * matvecs, converged} (EigResult). Errors as the reference (NumericalError on
+ * an indefinite operator). */
+pcgx_status pcgx_power_method(pcgx_context ctx, pcgx_operator op, double tol, int maxit,
+                              uint64_t seed, double* out4);
+pcgx_status pcgx_dacg_smallest(pcgx_context ctx, pcgx_operator op, double tol, int maxit,
+                               uint64_t seed, double* out4);
+
 /* --------------------------------------------------- config generators */
 
 /* Config 3: heterogeneous diffusion, Q1 (trilinear) finite elements on the

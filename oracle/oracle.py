@@ -141,6 +141,8 @@ class Oracle:
                                    C.c_int, _dp, C.POINTER(Report)]
         L.or_lanczos.argtypes = [C.POINTER(_OrOp), C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
         L.or_tridiag_extremes.argtypes = [C.c_int, _dp, _dp, _dp, _dp]
+        L.or_power_method.argtypes = [C.POINTER(_OrOp), C.c_double, C.c_int, C.c_uint64, _dp]
+        L.or_dacg_smallest.argtypes = [C.POINTER(_OrOp), C.c_double, C.c_int, C.c_uint64, _dp]
 
     def _chk(self, code):
         if code:
@@ -226,6 +228,18 @@ class Oracle:
                                     _ptr(a), _ptr(b)))
         return lo.value, hi.value, a, b
 
+    def _eig(self, fn, op, tol, maxit, seed):
+        out = np.zeros(4)
+        self._chk(getattr(self.L, fn)(C.byref(op.s), tol, maxit, seed, _ptr(out)))
+        return {"value": out[0], "iters": int(out[1]), "matvecs": int(out[2]),
+                "converged": bool(out[3])}
+
+    def power_method(self, op, tol=1e-4, maxit=200, seed=20240801):
+        return self._eig("or_power_method", op, tol, maxit, seed)
+
+    def dacg_smallest(self, op, tol=1e-2, maxit=5000, seed=20240801):
+        return self._eig("or_dacg_smallest", op, tol, maxit, seed)
+
     def tridiag_extremes(self, a, b):
         a = np.ascontiguousarray(a, dtype=np.float64)
         b = np.ascontiguousarray(b, dtype=np.float64)
@@ -266,6 +280,9 @@ class RefLib:
         L.ref_spectrum_table.argtypes = [C.c_int64, C.POINTER(C.c_int), C.c_int, C.c_double,
                                          C.c_int, C.c_uint64, _dp]
         L.ref_set_threads.argtypes = [C.c_int]
+        for fn in ("ref_power_method", "ref_dacg_smallest"):
+            getattr(L, fn).argtypes = [C.c_int, C.c_int64, C.c_int64, _i64p, _i64p, _dp, C.c_double,
+                                       C.c_int, C.c_uint64, _dp]
 
     def _chk(self, code):
         if code:
@@ -355,6 +372,19 @@ class RefLib:
                                        _ptr(bp), seed, tol, maxit, _ptr(x), _ptr(b_out),
                                        C.byref(rep)))
         return x, (b_out if b is None else bp), rep.as_dict()
+
+    def _eig(self, fn, kind, tol, maxit, seed, nx=0, csr=None):
+        n, rp, ci, va, keep = self._csr(csr)
+        out = np.zeros(4)
+        self._chk(getattr(self.L, fn)(REF_KIND[kind], nx, n, rp, ci, va, tol, maxit, seed, _ptr(out)))
+        return {"value": out[0], "iters": int(out[1]), "matvecs": int(out[2]),
+                "converged": bool(out[3])}
+
+    def power_method(self, kind, tol=1e-4, maxit=200, seed=20240801, nx=0, csr=None):
+        return self._eig("ref_power_method", kind, tol, maxit, seed, nx, csr)
+
+    def dacg_smallest(self, kind, tol=1e-2, maxit=5000, seed=20240801, nx=0, csr=None):
+        return self._eig("ref_dacg_smallest", kind, tol, maxit, seed, nx, csr)
 
     def spectrum_table(self, nx, degrees, scale, solution="ones", seed=20240801):
         deg = (C.c_int * len(degrees))(*degrees)

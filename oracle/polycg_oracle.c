@@ -470,3 +470,175 @@ int or_lanczos(const or_op* op, int steps, uint64_t seed, double* lo, double* hi
   free(w);
   return OR_OK;
 }
+
+/* ---------------------------------------------------------------- power / DACG */
+
+/* start_vector (eigenest.cpp:35-46): seeded uniform, normalised; seed+1 once if zero */
+static int start_vector(const or_op* op, uint64_t seed, const char* who, double* v) {
+  const int64_t n = op_n(op);
+  or_random_uniform(n, seed, 0, v);
+  double nrm = sqrt(dot(n, v, v));
+  if (nrm == 0.0) {
+    or_random_uniform(n, seed + 1, 0, v);
+    nrm = sqrt(dot(n, v, v));
+    if (nrm == 0.0) {
+      snprintf(g_err, sizeof g_err, "%s: zero starting vector", who);
+      return OR_NUMERICAL;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) v[i] = v[i] / nrm;
+  return OR_OK;
+}
+
+/* power_method, eigenest.cpp:48-79 */
+int or_power_method(const or_op* op, double tol, int maxit, uint64_t seed, double* out) {
+  const int64_t n = op_n(op);
+  if (!(tol > 0.0)) return fail(OR_INVALID, "power_method: tol must be positive");
+  double* v = (double*)malloc(sizeof(double) * (size_t)n);
+  double* w = (double*)malloc(sizeof(double) * (size_t)n);
+  double value = 0.0, matvecs = 0.0;
+  int iters = 0, conv = 0, st = start_vector(op, seed, "power_method", v);
+  double beta_old = 0.0;
+  for (int it = 1; st == OR_OK && it <= maxit; ++it) {
+    or_apply(op, v, w);
+    matvecs += 1.0;
+    const double beta = dot(n, v, w);
+    value = beta;
+    iters = it;
+    if (it > 1 && fabs(beta - beta_old) <= tol * fabs(beta)) {
+      conv = 1;
+      break;
+    }
+    beta_old = beta;
+    const double wnorm = sqrt(dot(n, w, w));
+    if (wnorm == 0.0) {
+      st = start_vector(op, seed + 1, "power_method", v);
+      if (st) break;
+      or_apply(op, v, w);
+      matvecs += 1.0;
+      if (sqrt(dot(n, w, w)) == 0.0) {
+        st = fail(OR_NUMERICAL, "power_method: operator annihilates the start vector");
+        break;
+      }
+    }
+    const double wn = sqrt(dot(n, w, w));
+    for (int64_t i = 0; i < n; ++i) v[i] = w[i] / wn;
+  }
+  out[0] = value;
+  out[1] = iters;
+  out[2] = matvecs;
+  out[3] = conv;
+  free(v);
+  free(w);
+  return st;
+}
+
+/* dacg_smallest, eigenest.cpp:81-167 */
+int or_dacg_smallest(const or_op* op, double tol, int maxit, uint64_t seed, double* out) {
+  const int64_t n = op_n(op);
+  if (!(tol > 0.0)) return fail(OR_INVALID, "dacg_smallest: tol must be positive");
+  double* x = (double*)malloc(sizeof(double) * (size_t)n);
+  double* ax = (double*)malloc(sizeof(double) * (size_t)n);
+  double* p = (double*)calloc((size_t)n, sizeof(double));
+  double* ap = (double*)malloc(sizeof(double) * (size_t)n);
+  double* g = (double*)malloc(sizeof(double) * (size_t)n);
+  double* e = (double*)malloc(sizeof(double) * (size_t)n);
+  double value = 0.0, matvecs = 0.0;
+  int iters = 0, conv = 0;
+  int st = start_vector(op, seed, "dacg_smallest", x);
+  if (st) goto done;
+  or_apply(op, x, ax);
+  matvecs += 1.0;
+  double q = dot(n, x, ax);
+  if (!(q > 0.0)) {
+    st = fail(OR_NUMERICAL, "dacg_smallest: x'Ax <= 0, operator not positive definite");
+    goto done;
+  }
+  double g_old_sq = 0.0;
+  int have_p = 0;
+  for (int it = 0; it <= maxit; ++it) {
+    value = q;
+    iters = it;
+    for (int64_t i = 0; i < n; ++i) {
+      e[i] = ax[i] - q * x[i];
+      g[i] = 2.0 * e[i];
+    }
+    const double resid = sqrt(dot(n, e, e)) / q;
+    if (resid <= tol) {
+      conv = 1;
+      break;
+    }
+    if (it == maxit) break;
+    const double gsq = dot(n, g, g);
+    if (!have_p || it % 50 == 0) {
+      for (int64_t i = 0; i < n; ++i) p[i] = -g[i];
+    } else {
+      const double c = gsq / g_old_sq;
+      for (int64_t i = 0; i < n; ++i) p[i] = -g[i] + c * p[i];
+    }
+    have_p = 1;
+    g_old_sq = gsq;
+    or_apply(op, p, ap);
+    matvecs += 1.0;
+    const double hxx = q, hxp = dot(n, x, ap), hpp = dot(n, p, ap);
+    const double mxx = 1.0, mxp = dot(n, x, p), mpp = dot(n, p, p);
+    if (!(hpp > 0.0)) {
+      st = fail(OR_NUMERICAL, "dacg_smallest: p'Ap <= 0, operator not positive definite");
+      goto done;
+    }
+    const double a2 = mxx * mpp - mxp * mxp;
+    const double a1 = -((hxx * mpp + hpp * mxx) - 2.0 * hxp * mxp);
+    const double a0 = hxx * hpp - hxp * hxp;
+    const double disc = sqrt(fmax(0.0, a1 * a1 - 4.0 * a2 * a0));
+    const double lambda = (-a1 - disc) / (2.0 * a2);
+    const double r11 = hxx - lambda * mxx, r12 = hxp - lambda * mxp;
+    const double r22 = hpp - lambda * mpp;
+    double cx, cp;
+    if (fabs(r12) + fabs(r22) > fabs(r11) + fabs(r12)) {
+      cx = -r22;
+      cp = r12;
+    } else {
+      cx = -r12;
+      cp = r11;
+    }
+    if (cx == 0.0 && cp == 0.0) {
+      cx = 1.0;
+      cp = 0.0;
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      x[i] = cx * x[i] + cp * p[i];
+      ax[i] = cx * ax[i] + cp * ap[i];
+    }
+    const double xnorm = sqrt(dot(n, x, x));
+    if (xnorm == 0.0) {
+      st = fail(OR_NUMERICAL, "dacg_smallest: line search collapsed");
+      goto done;
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      x[i] = x[i] / xnorm;
+      ax[i] = ax[i] / xnorm;
+    }
+    const double q_prev = q;
+    q = dot(n, x, ax);
+    if (!(q > 0.0)) {
+      st = fail(OR_NUMERICAL, "dacg_smallest: x'Ax <= 0, operator not positive definite");
+      goto done;
+    }
+    if (q > q_prev * (1.0 + 1e-12)) {
+      st = fail(OR_NUMERICAL, "dacg_smallest: Rayleigh quotient increased");
+      goto done;
+    }
+  }
+done:
+  out[0] = value;
+  out[1] = iters;
+  out[2] = matvecs;
+  out[3] = conv;
+  free(x);
+  free(ax);
+  free(p);
+  free(ap);
+  free(g);
+  free(e);
+  return st;
+}

@@ -230,6 +230,34 @@ int ref_pcg_solve(int kind, std::int64_t nx, std::int64_t n, const std::int64_t*
   });
 }
 
+// power_method / dacg_smallest (eigenest.cpp:48-167) on the scaled operator.
+// out: {value, iters, matvecs, converged}
+int ref_power_method(int kind, std::int64_t nx, std::int64_t n, const std::int64_t* rp,
+                     const std::int64_t* ci, const double* va, double tol, int maxit,
+                     std::uint64_t seed, double* out) {
+  return guarded([&] {
+    RefProblem p = make_problem(kind, nx, n, rp, ci, va);
+    const EigResult r = power_method(*p.scaled, EigOptions{tol, maxit, seed});
+    out[0] = r.value;
+    out[1] = r.iters;
+    out[2] = static_cast<double>(r.matvecs);
+    out[3] = r.converged ? 1.0 : 0.0;
+  });
+}
+
+int ref_dacg_smallest(int kind, std::int64_t nx, std::int64_t n, const std::int64_t* rp,
+                      const std::int64_t* ci, const double* va, double tol, int maxit,
+                      std::uint64_t seed, double* out) {
+  return guarded([&] {
+    RefProblem p = make_problem(kind, nx, n, rp, ci, va);
+    const EigResult r = dacg_smallest(*p.scaled, EigOptions{tol, maxit, seed});
+    out[0] = r.value;
+    out[1] = r.iters;
+    out[2] = static_cast<double>(r.matvecs);
+    out[3] = r.converged ? 1.0 : 0.0;
+  });
+}
+
 // rows: 6 doubles each {m, iters, mu_max, mu_min, l, kappa}; solution 0 ones, 1 flat, 2 random
 int ref_spectrum_table(std::int64_t nx, const int* degrees, int nd, double scale, int solution,
                        std::uint64_t seed, double* rows) {

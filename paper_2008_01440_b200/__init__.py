@@ -11,5 +11,6 @@ from .pcgx import (  # noqa: F401
     InvalidArgument, NumericalError, PcgxError, PinnedBuffer, ScaledOperator, SolveOptions,
     SolveReport, StencilOperator, analytic_extremes, analytic_extremes_box, apply_chebyshev,
     FLAG_NO_GRAPH, FLAG_TIME_KERNELS, cheb_params, eval_poly, gen_elast27, gen_fe27, jacobi_scale, lanczos_bounds, lib,
-    pcg_solve, random_uniform_vector, slab_partition,
+    pcg_solve, random_uniform_vector, slab_partition, EigOptions, EigResult, power_method,
+    dacg_smallest, estimate_bounds,
 )

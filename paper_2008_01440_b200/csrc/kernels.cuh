@@ -131,6 +131,60 @@ __device__ __forceinline__ void block_reduce_finish2(double v0, double v1, const
   }
 }
 
+// N values reduced together into red.result[0..N) (partials[N b + k]).
+template <int N>
+__device__ __forceinline__ void block_reduce_finishN(const double (&vin)[N], const Reduce& red) {
+  __shared__ double wsn[N][32];
+  __shared__ bool is_lastn;
+  const int nthreads = blockDim.x * blockDim.y * blockDim.z;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const unsigned nblocks = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (nthreads + 31) >> 5;
+  double v[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    v[k] = warp_sum(vin[k]);
+    if (lane == 0) wsn[k][warp] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = warp_sum(lane < nwarps ? wsn[k][lane] : 0.0);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) red.partials[N * bid + k] = v[k];
+      __threadfence();
+      const unsigned ticket = atomicAdd(red.counter, 1u);
+      is_lastn = (ticket == nblocks - 1);
+    }
+  }
+  __syncthreads();
+  if (!is_lastn) return;
+  __threadfence();
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = 0.0;
+  for (unsigned b = tid; b < nblocks; b += nthreads)
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] += __ldcg(red.partials + N * b + k);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    v[k] = warp_sum(v[k]);
+    if (lane == 0) wsn[k][warp] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = warp_sum(lane < nwarps ? wsn[k][lane] : 0.0);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) red.result[k] = v[k];
+      *red.counter = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // ----------------------------------------------------------------- epilogues
 // Two-phase interface so the marching kernels can prefetch the epilogue's own
 // operand vectors one plane ahead:
@@ -904,6 +958,89 @@ pack_kernel(long long n, const int* __restrict__ idx, const double* __restrict__
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     out[i] = x[idx[i]];
+}
+
+// ---- power method / DACG (eigenest.cpp:48-167), elementwise in the reference's order
+
+// v = w / s  (power_method: v = w / w.norm())
+__global__ void __launch_bounds__(kVecThreads)
+div_copy_kernel(long long n, double* __restrict__ v, const double* __restrict__ w, double s) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = w[i] / s;
+}
+
+// e = ax - q x, g = 2 e: reduces [e'e, g'g]
+__global__ void __launch_bounds__(kVecThreads)
+dacg_g_kernel(long long n, const double* __restrict__ x, const double* __restrict__ ax, double q,
+              Reduce red) {
+  double v[2] = {0.0, 0.0};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double e = ax[i] - q * x[i];
+    const double g = 2.0 * e;
+    v[0] = v[0] + e * e;
+    v[1] = v[1] + g * g;
+  }
+  block_reduce_finishN<2>(v, red);
+}
+
+// p = -g (restart) or p = -g + c p, g = 2 (ax - q x) recomputed
+__global__ void __launch_bounds__(kVecThreads)
+dacg_p_kernel(long long n, const double* __restrict__ x, const double* __restrict__ ax, double q,
+              double* __restrict__ p, double c, int restart) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double g = 2.0 * (ax[i] - q * x[i]);
+    p[i] = restart ? -g : -g + c * p[i];
+  }
+}
+
+// [x'ap, x'p, p'p]
+__global__ void __launch_bounds__(kVecThreads)
+dot3_kernel(long long n, const double* __restrict__ x, const double* __restrict__ p,
+            const double* __restrict__ ap, Reduce red) {
+  double v[3] = {0.0, 0.0, 0.0};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double xi = x[i], pi = p[i];
+    v[0] = v[0] + xi * ap[i];
+    v[1] = v[1] + xi * pi;
+    v[2] = v[2] + pi * pi;
+  }
+  block_reduce_finishN<3>(v, red);
+}
+
+// x = cx x + cp p ; ax = cx ax + cp ap ; reduces x'x
+__global__ void __launch_bounds__(kVecThreads)
+dacg_x_kernel(long long n, double* __restrict__ x, double* __restrict__ ax,
+              const double* __restrict__ p, const double* __restrict__ ap, double cx, double cp,
+              Reduce red) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double xi = cx * x[i] + cp * p[i];
+    x[i] = xi;
+    ax[i] = cx * ax[i] + cp * ap[i];
+    acc = acc + xi * xi;
+  }
+  block_reduce_finish(acc, red);
+}
+
+// x /= s ; ax /= s ; reduces x'ax
+__global__ void __launch_bounds__(kVecThreads)
+dacg_norm_kernel(long long n, double* __restrict__ x, double* __restrict__ ax, double s,
+                 Reduce red) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double xi = x[i] / s;
+    const double ai = ax[i] / s;
+    x[i] = xi;
+    ax[i] = ai;
+    acc = acc + xi * ai;
+  }
+  block_reduce_finish(acc, red);
 }
 
 // Writes a large scratch buffer (flushes L2 between timed iterations).

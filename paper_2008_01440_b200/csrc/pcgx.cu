@@ -1268,6 +1268,181 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   }
 }
 
+// ---------------------------------------------------------------- power method / DACG
+// Device restatements of the reference's bound estimators (eigenest.cpp:35-167):
+// same iteration, same elementwise rounding, deterministic tree reductions; the
+// host reads the reduced scalars once or twice per iteration and runs the
+// scalar logic (convergence, restart, the 2x2 pencil) exactly as the reference.
+
+// start_vector (eigenest.cpp:35-46) into v (this rank's rows).
+void start_vector_device(pcgx_context c, pcgx_operator op, uint64_t seed, const char* who, double* v) {
+  const long long n = op->n_local;
+  const unsigned long long off = (unsigned long long)pcgx_operator_row0(op);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    splitmix_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, seed + (uint64_t)attempt, off, v);
+    check_launch();
+    count_launch(c);
+    launch_dot(c, n, v, v, S_DOT);
+    allreduce(c, S_DOT, 1);
+    fetch_scalars(c);
+    const double nrm = std::sqrt(c->hS[S_DOT]);
+    if (nrm != 0.0) {
+      scale_div_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, v, nrm);
+      check_launch();
+      count_launch(c);
+      return;
+    }
+  }
+  fail(PCGX_ERR_NUMERICAL, std::string(who) + ": zero starting vector");
+}
+
+// out = {value, iters, matvecs, converged}
+void power_method_device(pcgx_context c, pcgx_operator op, double tol, int maxit, uint64_t seed,
+                         double* out) {
+  if (!(tol > 0.0)) fail(PCGX_ERR_INVALID, "power_method: tol must be positive");
+  const long long n = op->n_local;
+  ensure_workspace(c, n, ws_pad_of(op));
+  double* v = c->t0;
+  double* w = c->t1;
+  double value = 0.0, matvecs = 0.0;
+  int iters = 0, conv = 0;
+  start_vector_device(c, op, seed, "power_method", v);
+  double beta_old = 0.0;
+  for (int it = 1; it <= maxit; ++it) {
+    op_launch<EpiStore, true>(c, op, v, EpiStore{w}, S_DOT);  // w = A v, beta = v'w
+    allreduce(c, S_DOT, 1);
+    launch_dot(c, n, w, w, S_DOT2);
+    allreduce(c, S_DOT2, 1);
+    fetch_scalars(c);
+    matvecs += 1.0;
+    const double beta = c->hS[S_DOT];
+    value = beta;
+    iters = it;
+    if (it > 1 && std::abs(beta - beta_old) <= tol * std::abs(beta)) {
+      conv = 1;
+      break;
+    }
+    beta_old = beta;
+    double wn = std::sqrt(c->hS[S_DOT2]);
+    if (wn == 0.0) {  // A v = 0 exactly: restart from seed + 1 (eigenest.cpp:67-75)
+      start_vector_device(c, op, seed + 1, "power_method", v);
+      op_launch<EpiStore, false>(c, op, v, EpiStore{w}, -1);
+      matvecs += 1.0;
+      launch_dot(c, n, w, w, S_DOT2);
+      allreduce(c, S_DOT2, 1);
+      fetch_scalars(c);
+      wn = std::sqrt(c->hS[S_DOT2]);
+      if (wn == 0.0) fail(PCGX_ERR_NUMERICAL, "power_method: operator annihilates the start vector");
+    }
+    div_copy_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, v, w, wn);
+    check_launch();
+    count_launch(c);
+  }
+  out[0] = value;
+  out[1] = iters;
+  out[2] = matvecs;
+  out[3] = conv;
+}
+
+void dacg_device(pcgx_context c, pcgx_operator op, double tol, int maxit, uint64_t seed,
+                 double* out) {
+  if (!(tol > 0.0)) fail(PCGX_ERR_INVALID, "dacg_smallest: tol must be positive");
+  constexpr int kRestart = 50;
+  const long long n = op->n_local;
+  ensure_workspace(c, n, ws_pad_of(op));
+  double* x = c->t0;
+  double* ax = c->t1;
+  double* p = c->w0;
+  double* ap = c->w1;
+  double value = 0.0, matvecs = 0.0;
+  int iters = 0, conv = 0;
+  start_vector_device(c, op, seed, "dacg_smallest", x);
+  op_launch<EpiStore, true>(c, op, x, EpiStore{ax}, S_DOT);  // ax = A x, q = x'ax
+  allreduce(c, S_DOT, 1);
+  fetch_scalars(c);
+  matvecs += 1.0;
+  double q = c->hS[S_DOT];
+  if (!(q > 0.0)) fail(PCGX_ERR_NUMERICAL, "dacg_smallest: x'Ax <= 0, operator not positive definite");
+  double g_old_sq = 0.0;
+  bool have_p = false;
+  const int grid = vec_grid(c, n);
+  for (int it = 0; it <= maxit; ++it) {
+    value = q;
+    iters = it;
+    dacg_g_kernel<<<grid, kVecThreads, 0, c->s>>>(n, x, ax, q, make_red(c, S_E0));
+    check_launch();
+    count_launch(c);
+    allreduce(c, S_E0, 2);
+    fetch_scalars(c);
+    const double resid = std::sqrt(c->hS[S_E0]) / q;
+    if (resid <= tol) {
+      conv = 1;
+      break;
+    }
+    if (it == maxit) break;
+    const double gsq = c->hS[S_E1];
+    const bool restart = !have_p || it % kRestart == 0;
+    dacg_p_kernel<<<grid, kVecThreads, 0, c->s>>>(n, x, ax, q, p, restart ? 0.0 : gsq / g_old_sq,
+                                                  restart ? 1 : 0);
+    check_launch();
+    count_launch(c);
+    have_p = true;
+    g_old_sq = gsq;
+    op_launch<EpiStore, true>(c, op, p, EpiStore{ap}, S_DOT);  // ap = A p, hpp = p'ap
+    allreduce(c, S_DOT, 1);
+    dot3_kernel<<<grid, kVecThreads, 0, c->s>>>(n, x, p, ap, make_red(c, S_E0));
+    check_launch();
+    count_launch(c);
+    allreduce(c, S_E0, 3);
+    fetch_scalars(c);
+    matvecs += 1.0;
+    const double hxx = q, hxp = c->hS[S_E0], hpp = c->hS[S_DOT];
+    const double mxx = 1.0, mxp = c->hS[S_E1], mpp = c->hS[S_E2];
+    if (!(hpp > 0.0))
+      fail(PCGX_ERR_NUMERICAL, "dacg_smallest: p'Ap <= 0, operator not positive definite");
+    const double a2 = mxx * mpp - mxp * mxp;
+    const double a1 = -(hxx * mpp + hpp * mxx - 2.0 * hxp * mxp);
+    const double a0 = hxx * hpp - hxp * hxp;
+    const double disc = std::sqrt(std::max(0.0, a1 * a1 - 4.0 * a2 * a0));
+    const double lambda = (-a1 - disc) / (2.0 * a2);
+    const double r11 = hxx - lambda * mxx, r12 = hxp - lambda * mxp;
+    const double r22 = hpp - lambda * mpp;
+    double cx, cp;
+    if (std::abs(r12) + std::abs(r22) > std::abs(r11) + std::abs(r12)) {
+      cx = -r22;
+      cp = r12;
+    } else {
+      cx = -r12;
+      cp = r11;
+    }
+    if (cx == 0.0 && cp == 0.0) {
+      cx = 1.0;
+      cp = 0.0;
+    }
+    dacg_x_kernel<<<grid, kVecThreads, 0, c->s>>>(n, x, ax, p, ap, cx, cp, make_red(c, S_DOT2));
+    check_launch();
+    count_launch(c);
+    allreduce(c, S_DOT2, 1);
+    fetch_scalars(c);
+    const double xnorm = std::sqrt(c->hS[S_DOT2]);
+    if (xnorm == 0.0) fail(PCGX_ERR_NUMERICAL, "dacg_smallest: line search collapsed");
+    dacg_norm_kernel<<<grid, kVecThreads, 0, c->s>>>(n, x, ax, xnorm, make_red(c, S_DOT));
+    check_launch();
+    count_launch(c);
+    allreduce(c, S_DOT, 1);
+    fetch_scalars(c);
+    const double q_prev = q;
+    q = c->hS[S_DOT];
+    if (!(q > 0.0))
+      fail(PCGX_ERR_NUMERICAL, "dacg_smallest: x'Ax <= 0, operator not positive definite");
+    if (q > q_prev * (1.0 + 1e-12)) fail(PCGX_ERR_NUMERICAL, "dacg_smallest: Rayleigh quotient increased");
+  }
+  out[0] = value;
+  out[1] = iters;
+  out[2] = matvecs;
+  out[3] = conv;
+}
+
 // ---------------------------------------------------------------- Lanczos
 
 void lanczos_device(pcgx_context c, pcgx_operator op, int steps_hi, int steps, uint64_t seed,
@@ -2065,6 +2240,22 @@ void pcgx_analytic_extremes(int dim, int64_t nx, int scaled, double* lo, double*
 
 void pcgx_analytic_extremes_box(int64_t nx, int64_t ny, int64_t nz, double* lo, double* hi) {
   analytic_extremes_box(nx, ny, nz, lo, hi);
+}
+
+pcgx_status pcgx_power_method(pcgx_context c, pcgx_operator op, double tol, int maxit,
+                              uint64_t seed, double* out4) {
+  return guarded(c, [&] {
+    set_device(c);
+    power_method_device(c, op, tol, maxit, seed, out4);
+  });
+}
+
+pcgx_status pcgx_dacg_smallest(pcgx_context c, pcgx_operator op, double tol, int maxit,
+                               uint64_t seed, double* out4) {
+  return guarded(c, [&] {
+    set_device(c);
+    dacg_device(c, op, tol, maxit, seed, out4);
+  });
 }
 
 pcgx_status pcgx_lanczos_bounds(pcgx_context c, pcgx_operator op, int steps_hi, int steps,

@@ -114,6 +114,7 @@ SYMBOLS = [
     "pcgx_cheb_apply", "pcgx_cheb_apply_device", "pcgx_solve_opts_default", "pcgx_pcg_solve",
     "pcgx_pcg_solve_device", "pcgx_random_uniform_device", "pcgx_random_uniform",
     "pcgx_analytic_extremes", "pcgx_analytic_extremes_box", "pcgx_lanczos_bounds",
+    "pcgx_power_method", "pcgx_dacg_smallest",
     "pcgx_gen_fe27_size", "pcgx_gen_fe27_fill", "pcgx_gen_elast27_size",
     "pcgx_gen_elast27_fill",
 ]
@@ -194,6 +195,8 @@ def lib():
         "pcgx_analytic_extremes": (None, [C.c_int, C.c_int64, C.c_int, _dp, _dp]),
         "pcgx_analytic_extremes_box": (None, [C.c_int64, C.c_int64, C.c_int64, _dp, _dp]),
         "pcgx_lanczos_bounds": (C.c_int, [ctx, op, C.c_int, C.c_int, C.c_uint64, _dp, _dp]),
+        "pcgx_power_method": (C.c_int, [ctx, op, C.c_double, C.c_int, C.c_uint64, _dp]),
+        "pcgx_dacg_smallest": (C.c_int, [ctx, op, C.c_double, C.c_int, C.c_uint64, _dp]),
         "pcgx_gen_fe27_size": (C.c_int, [C.c_int64, _i64p, _i64p]),
         "pcgx_gen_fe27_fill": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, _i32p, _i32p, _dp]),
         "pcgx_gen_elast27_size": (C.c_int, [C.c_int64, _i64p, _i64p]),
@@ -623,6 +626,49 @@ def lanczos_bounds(op: ScaledOperator, steps_hi=20, steps=30, seed=20240801):
     _check(lib().pcgx_lanczos_bounds(op.ctx.h, op.h, steps_hi, steps, seed, C.byref(lo),
                                      C.byref(hi)), op.ctx.h)
     return lo.value, hi.value
+
+
+@dataclass
+class EigResult:
+    """EigResult (eigenest.hpp:21-30; the per-iteration trace is not kept)."""
+    value: float
+    iters: int
+    matvecs: int
+    converged: bool
+
+
+@dataclass
+class EigOptions:
+    """EigOptions (eigenest.hpp:15-19)."""
+    tol: float = 1e-4
+    maxit: int = 200
+    seed: int = 20240801
+
+
+def _eig(fn, op, opts):
+    out = np.zeros(4)
+    _check(getattr(lib(), fn)(op.ctx.h, op.h, opts.tol, opts.maxit, opts.seed, _ptr(out)), op.ctx.h)
+    return EigResult(float(out[0]), int(out[1]), int(out[2]), bool(out[3]))
+
+
+def power_method(op: ScaledOperator, opts: EigOptions | None = None) -> EigResult:
+    """power_method (eigenest.cpp:48-79) on the device."""
+    return _eig("pcgx_power_method", op, opts or EigOptions())
+
+
+def dacg_smallest(op: ScaledOperator, opts: EigOptions | None = None) -> EigResult:
+    """dacg_smallest (eigenest.cpp:81-167) on the device."""
+    return _eig("pcgx_dacg_smallest", op, opts or EigOptions(tol=1e-2, maxit=5000))
+
+
+def estimate_bounds(op: ScaledOperator, power_opts: EigOptions | None = None,
+                    dacg_opts: EigOptions | None = None):
+    """estimate_bounds (eigenest.cpp:169-185): (alpha0, beta0, power result, dacg result)."""
+    hi = power_method(op, power_opts)
+    lo = dacg_smallest(op, dacg_opts)
+    if not (lo.value > 0.0) or lo.value > hi.value:
+        raise NumericalError("estimate_bounds: estimates violate 0 < alpha0 <= beta0")
+    return lo.value, hi.value, hi, lo
 
 
 # ============================================================================ inputs

@@ -203,6 +203,21 @@ def main():
             t1[f"{sol}:{s}"] = [[int(r[0]), int(r[1]), hx(r[2]), hx(r[3]), int(r[4]), hx(r[5])] for r in rows]
     out["table1"] = t1
 
+    # ---- bound estimators (eigenest.cpp:48-167) ----------------------------------------
+    eig = []
+    for tag, kind, nx, csr, ptol, pmax, dtol, dmax in [
+            ("lap10_default", "lap3d", 10, None, 1e-4, 200, 1e-2, 5000),
+            ("lap24_tight", "lap3d", 24, None, 1e-8, 2000, 1e-4, 5000),
+            ("csr300_default", "csr", 0, (rp, ci, va), 1e-4, 200, 1e-2, 5000)]:
+        pm = R.power_method(kind, tol=ptol, maxit=pmax, nx=nx, csr=csr)
+        dg = R.dacg_smallest(kind, tol=dtol, maxit=dmax, nx=nx, csr=csr)
+        eig.append({"tag": tag, "kind": kind, "nx": nx, "power": {"tol": ptol, "maxit": pmax,
+                    "value": hx(pm["value"]), "iters": pm["iters"], "matvecs": pm["matvecs"],
+                    "converged": pm["converged"]},
+                    "dacg": {"tol": dtol, "maxit": dmax, "value": hx(dg["value"]), "iters": dg["iters"],
+                             "matvecs": dg["matvecs"], "converged": dg["converged"]}})
+    out["eigen_estimators"] = eig
+
     with open(os.path.join(HERE, "reference_golden.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", os.path.join(HERE, "reference_golden.json"))

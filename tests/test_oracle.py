@@ -226,3 +226,25 @@ def test_lanczos_bounds_bracket_analytic(oracle):
     assert hi == pytest.approx(hi_a, rel=2e-2)
     lo20, hi20 = oracle.tridiag_extremes(al[:20], be[:20])
     assert hi20 <= hi + 1e-15
+
+
+def _eig_op(oracle, golden, c):
+    if c["kind"] == "lap3d":
+        return OracleOp("lap3d", nx=c["nx"])
+    g = golden["csr_apply"]
+    return OracleOp("csr", row_ptr=g["row_ptr"], col_idx=g["col_idx"], values=fhs(g["values"]))
+
+
+def test_power_dacg_bitwise_vs_reference(oracle, golden):
+    """power_method / dacg_smallest (eigenest.cpp:48-167) restated in C: same value
+    bits, iterations and matvec counts as the reference itself."""
+    for c in golden["eigen_estimators"]:
+        op = _eig_op(oracle, golden, c)
+        pm = oracle.power_method(op, tol=c["power"]["tol"], maxit=c["power"]["maxit"], seed=SEED)
+        assert pm["value"] == fh(c["power"]["value"]), c["tag"]
+        assert (pm["iters"], pm["matvecs"], pm["converged"]) == (
+            c["power"]["iters"], c["power"]["matvecs"], c["power"]["converged"])
+        dg = oracle.dacg_smallest(op, tol=c["dacg"]["tol"], maxit=c["dacg"]["maxit"], seed=SEED)
+        assert dg["value"] == fh(c["dacg"]["value"]), c["tag"]
+        assert (dg["iters"], dg["matvecs"], dg["converged"]) == (
+            c["dacg"]["iters"], c["dacg"]["matvecs"], c["dacg"]["converged"])
