@@ -16,8 +16,8 @@
 // Dirichlet boundary). Stage 1 computes C on the 66 x 10 extended tile (the halo
 // redundantly) into a 3-plane shared ring; stage 2 reads C from there. HBM traffic per point per TWO steps: read A, B, R + write C, E = 40 B
 // (vs 64 B for two single-step passes); halo re-reads are served by L2.
-// Loads run D = 3 planes ahead through a ring of mbarriers; one elected thread
-// issues them. Per-point arithmetic is the single-step kernel's (bitwise parity).
+// Loads run D = 4 planes ahead through a ring of mbarriers; one elected thread
+// issues them. One block barrier per plane (the ring refill rides on it). Per-point arithmetic is the single-step kernel's (bitwise parity).
 #pragma once
 
 #include <cuda.h>
@@ -35,7 +35,7 @@ constexpr int kC2BY = kC2TY + 2;                     // B, R boxes and the C rin
 // instruction on sm_100a). A box 68 x 12 (6528 B), B/R boxes 68 x 10 (5440 B).
 constexpr int kC2AX = kC2W, kC2BX = kC2W;
 #ifndef PCGX_C2D
-#define PCGX_C2D 3
+#define PCGX_C2D 4
 #endif
 #ifndef PCGX_C2MINB
 #define PCGX_C2MINB 2
@@ -250,6 +250,11 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
       ac = ap;
     }
     __syncthreads();
+    // Refill the ring slots of unit u-1 with unit u-1+D: every warp is past
+    // stage 2 / the halo of iteration u-1, the last readers of A[u-2], B[u-1],
+    // R[u-2]. This is the only block barrier of the iteration: a warp runs on
+    // from its stage 2 of u into stage 1 of u+1 without waiting for the others.
+    if (tid == 0 && u >= kb && u - 1 + kC2D <= u_last) issue_unit(u - 1 + kC2D);
     // ---------------- stage 2: E[u-1] on the tile (warps 0..7) | halo columns of C[u] (warps 8, 9)
     if (stage2) {
       const int v = u - 1;
@@ -292,8 +297,6 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
       }
       Cu[offBh] = cx;
     }
-    __syncthreads();
-    if (tid == 0 && u + kC2D <= u_last) issue_unit(u + kC2D);
     // rotate the rings and global pointers by one plane
     pAm = pAu;
     pAu = pAp;
