@@ -171,6 +171,28 @@ pcgx_status pcgx_cheb_apply(pcgx_context ctx, pcgx_operator op, const pcgx_cheb*
 pcgx_status pcgx_cheb_apply_device(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* p,
                                    const double* r, double* out);
 
+/* Newton form (polyprec.hpp:22-31): degree 2^nlev - 1, zeta[0..nlev]. */
+typedef struct {
+  int nlev;
+  const double* zeta; /* zeta[0..nlev] */
+} pcgx_newton;
+
+/* newton_params verbatim (polyprec.cpp:27-54, bit-exact): zeta[nlev+1].
+ * Validates 0 < alpha0 <= beta0, nlev >= 0, scale >= 1 and positivity. */
+pcgx_status pcgx_newton_params(double alpha0, double beta0, int nlev, double scale,
+                               double* zeta);
+/* eval_poly, Newton form (polyprec.cpp:81-87). */
+double pcgx_newton_eval(const pcgx_newton* p, double lambda);
+/* chi_sequence (polyprec.cpp:102-123): chi[nlev], 0 <= nlev <= 30. */
+pcgx_status pcgx_chi_sequence(double alpha, double beta, int nlev, double* chi);
+/* out = P_nlev(A) r by the reference's depth-nlev recursion (apply_newton,
+ * polyprec.cpp:135-160): exactly 2^nlev - 1 matvecs, bitwise the reference's
+ * per-element values. out must not alias r. */
+pcgx_status pcgx_newton_apply(pcgx_context ctx, pcgx_operator op, const pcgx_newton* p,
+                              const double* r, double* out);
+pcgx_status pcgx_newton_apply_device(pcgx_context ctx, pcgx_operator op, const pcgx_newton* p,
+                                     const double* r, double* out);
+
 /* ------------------------------------------------------------------ solver */
 
 #define PCGX_FLAG_TIME_KERNELS 1u /* time every Chebyshev-step launch with CUDA events */
@@ -216,6 +238,15 @@ pcgx_status pcgx_pcg_solve(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* 
 pcgx_status pcgx_pcg_solve_device(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* prec,
                                   const double* b, double* x, const pcgx_solve_opts* opts,
                                   pcgx_report* rep);
+
+/* pcg_solve with a NewtonPreconditioner (pcg.hpp:27-40); counters as above with
+ * degree 2^nlev - 1. */
+pcgx_status pcgx_pcg_solve_newton(pcgx_context ctx, pcgx_operator op, const pcgx_newton* prec,
+                                  const double* b, double* x, const pcgx_solve_opts* opts,
+                                  pcgx_report* rep);
+pcgx_status pcgx_pcg_solve_newton_device(pcgx_context ctx, pcgx_operator op,
+                                         const pcgx_newton* prec, const double* b, double* x,
+                                         const pcgx_solve_opts* opts, pcgx_report* rep);
 
 /* ------------------------------------------------------- inputs and bounds */
 

@@ -12,7 +12,8 @@
 // Supported inputs — exactly what the hot path covers:
 //   op   : ScaledOperator over StencilOperator(lap3d, nx) or CsrMatrix
 //          (what jacobi_scale returns, src/linop.cpp:340-351)
-//   prec : ChebyshevPreconditioner (pcg.hpp:42-55) or nullptr (plain CG)
+//   prec : ChebyshevPreconditioner (pcg.hpp:42-55), NewtonPreconditioner
+//          (pcg.hpp:27-40) or nullptr (plain CG)
 // Anything else throws std::invalid_argument (there is no silent CPU fallback).
 //
 // Depends on the reference's headers (polycg/linop.hpp, polycg/pcg.hpp) and on
@@ -105,16 +106,25 @@ inline std::pair<Vector, SolveReport> pcg_solve(const Session& s, const DeviceOp
     throw std::invalid_argument("gpu::pcg_solve: on_iterate is not supported on the device path");
   pcgx_cheb cheb{};
   const pcgx_cheb* cp = nullptr;
+  pcgx_newton newton{};
+  const pcgx_newton* np = nullptr;
   if (prec) {
-    auto* c = dynamic_cast<ChebyshevPreconditioner*>(prec);
-    if (!c) throw std::invalid_argument("gpu::pcg_solve: only ChebyshevPreconditioner is accelerated");
-    const ChebyshevParams& p = c->params();
-    cheb.m = p.m;
-    cheb.theta = p.theta;
-    cheb.delta = p.delta;
-    cheb.sigma = p.sigma;
-    cheb.rho = p.rho.data();
-    cp = &cheb;
+    if (auto* c = dynamic_cast<ChebyshevPreconditioner*>(prec)) {
+      const ChebyshevParams& p = c->params();
+      cheb.m = p.m;
+      cheb.theta = p.theta;
+      cheb.delta = p.delta;
+      cheb.sigma = p.sigma;
+      cheb.rho = p.rho.data();
+      cp = &cheb;
+    } else if (auto* nw = dynamic_cast<NewtonPreconditioner*>(prec)) {
+      newton.nlev = nw->params().nlev;
+      newton.zeta = nw->params().zeta.data();
+      np = &newton;
+    } else {
+      throw std::invalid_argument(
+          "gpu::pcg_solve: only ChebyshevPreconditioner and NewtonPreconditioner are accelerated");
+    }
   }
   pcgx_solve_opts o;
   pcgx_solve_opts_default(&o);
@@ -123,7 +133,8 @@ inline std::pair<Vector, SolveReport> pcg_solve(const Session& s, const DeviceOp
   o.x0 = opts.x0 ? opts.x0->data() : nullptr;
   pcgx_report r{};
   Vector x(n);
-  check(pcgx_pcg_solve(s.get(), dop.get(), cp, b.data(), x.data(), &o, &r), s.get());
+  if (np) check(pcgx_pcg_solve_newton(s.get(), dop.get(), np, b.data(), x.data(), &o, &r), s.get());
+  else check(pcgx_pcg_solve(s.get(), dop.get(), cp, b.data(), x.data(), &o, &r), s.get());
   SolveReport rep;
   rep.iters = static_cast<int>(r.iters);
   rep.ddot = static_cast<std::uint64_t>(r.ddot);
@@ -151,6 +162,14 @@ inline void apply_chebyshev(const Session& s, const DeviceOperator& dop,
   const pcgx_cheb cheb{p.m, p.theta, p.delta, p.sigma, p.rho.data()};
   out.resize(r.size());
   check(pcgx_cheb_apply(s.get(), dop.get(), &cheb, r.data(), out.data()), s.get());
+}
+
+// out = P_nlev(A) r on the device (apply_newton, src/polyprec.cpp:148-160).
+inline void apply_newton(const Session& s, const DeviceOperator& dop, const NewtonParams& p,
+                         const Vector& r, Vector& out) {
+  const pcgx_newton nw{p.nlev, p.zeta.data()};
+  out.resize(r.size());
+  check(pcgx_newton_apply(s.get(), dop.get(), &nw, r.data(), out.data()), s.get());
 }
 
 }  // namespace polycg::gpu

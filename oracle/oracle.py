@@ -139,6 +139,8 @@ class Oracle:
         L.or_apply_newton.argtypes = [C.POINTER(_OrOp), _dp, C.c_int, _dp, _dp]
         L.or_pcg_solve.argtypes = [C.POINTER(_OrOp), _dp, _dp, C.c_int, _dp, _dp, C.c_double,
                                    C.c_int, _dp, C.POINTER(Report)]
+        L.or_pcg_solve_newton.argtypes = [C.POINTER(_OrOp), _dp, C.c_int, _dp, _dp, C.c_double,
+                                          C.c_int, _dp, C.POINTER(Report)]
         L.or_lanczos.argtypes = [C.POINTER(_OrOp), C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
         L.or_tridiag_extremes.argtypes = [C.c_int, _dp, _dp, _dp, _dp]
         L.or_power_method.argtypes = [C.POINTER(_OrOp), C.c_double, C.c_int, C.c_uint64, _dp]
@@ -220,6 +222,17 @@ class Oracle:
                                       _ptr(x0p), tol, maxit, _ptr(x), C.byref(rep)))
         return x, rep.as_dict()
 
+    def pcg_solve_newton(self, op: OracleOp, zeta, b, tol=1e-8, maxit=20000, x0=None):
+        """pcg_solve with a NewtonPreconditioner (pcg.hpp:27-40)."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        zeta = np.ascontiguousarray(zeta, dtype=np.float64)
+        x = np.empty(op.n)
+        rep = Report()
+        x0p = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        self._chk(self.L.or_pcg_solve_newton(C.byref(op.s), _ptr(zeta), len(zeta) - 1, _ptr(b),
+                                             _ptr(x0p), tol, maxit, _ptr(x), C.byref(rep)))
+        return x, rep.as_dict()
+
     def lanczos(self, op: OracleOp, steps, seed):
         a = np.zeros(steps)
         b = np.zeros(steps)
@@ -277,6 +290,7 @@ class RefLib:
         L.ref_pcg_solve.argtypes = [C.c_int, C.c_int64, C.c_int64, _i64p, _i64p, _dp, C.c_double,
                                     C.c_double, C.c_int, C.c_double, _dp, C.c_uint64, C.c_double,
                                     C.c_int, _dp, _dp, C.POINTER(Report)]
+        L.ref_pcg_solve_newton.argtypes = L.ref_pcg_solve.argtypes
         L.ref_spectrum_table.argtypes = [C.c_int64, C.POINTER(C.c_int), C.c_int, C.c_double,
                                          C.c_int, C.c_uint64, _dp]
         L.ref_set_threads.argtypes = [C.c_int]
@@ -371,6 +385,20 @@ class RefLib:
         self._chk(self.L.ref_pcg_solve(REF_KIND[kind], nx, n, rp, ci, va, alpha, beta, m, scale,
                                        _ptr(bp), seed, tol, maxit, _ptr(x), _ptr(b_out),
                                        C.byref(rep)))
+        return x, (b_out if b is None else bp), rep.as_dict()
+
+    def pcg_solve_newton(self, kind, alpha, beta, nlev, scale, nx=0, csr=None, b=None,
+                         seed=20240801, tol=1e-8, maxit=20000):
+        """pcg_solve with NewtonPreconditioner(newton_params(alpha, beta, nlev, scale))."""
+        n, rp, ci, va, keep = self._csr(csr)
+        N = self._n(kind, nx, csr)
+        x = np.empty(N)
+        b_out = np.empty(N) if b is None else None
+        bp = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
+        rep = Report()
+        self._chk(self.L.ref_pcg_solve_newton(REF_KIND[kind], nx, n, rp, ci, va, alpha, beta,
+                                              nlev, scale, _ptr(bp), seed, tol, maxit, _ptr(x),
+                                              _ptr(b_out), C.byref(rep)))
         return x, (b_out if b is None else bp), rep.as_dict()
 
     def _eig(self, fn, kind, tol, maxit, seed, nx=0, csr=None):

@@ -288,13 +288,46 @@ static double now_s(void) {
   return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
 }
 
+/* The preconditioner of a solve: Chebyshev (pcg.hpp:42-55) or Newton form
+ * (pcg.hpp:27-40); m < 0 = none. */
+typedef struct {
+  int newton;
+  const double* tds;
+  const double* rho;
+  const double* zeta;
+  int m;  /* Chebyshev degree, or Newton nlev */
+} prec_t;
+
+static void prec_apply(const or_op* op, const prec_t* P, const double* r, double* z) {
+  if (P->newton) or_apply_newton(op, P->zeta, P->m, r, z);
+  else or_apply_chebyshev(op, P->tds, P->rho, P->m, r, z);
+}
+
+static int pcg_solve_impl(const or_op* op, const prec_t* P, const double* b, const double* x0,
+                          double tol, int maxit, double* x, or_report* rep);
+
 /* pcg_solve, pcg.cpp:10-117 (counters at :33,41,44,58-59,65,73,75,84,96-97,102,113,115) */
 int or_pcg_solve(const or_op* op, const double* tds, const double* rho_c, int m, const double* b,
                  const double* x0, double tol, int maxit, double* x, or_report* rep) {
+  const prec_t P = {0, tds, rho_c, NULL, m};
+  return pcg_solve_impl(op, &P, b, x0, tol, maxit, x, rep);
+}
+
+/* pcg_solve with a NewtonPreconditioner (degree 2^nlev - 1). */
+int or_pcg_solve_newton(const or_op* op, const double* zeta, int nlev, const double* b,
+                        const double* x0, double tol, int maxit, double* x, or_report* rep) {
+  if (nlev < 0) return fail(OR_INVALID, "apply_newton: nlev must be >= 0");
+  const prec_t P = {1, NULL, NULL, zeta, nlev};
+  return pcg_solve_impl(op, &P, b, x0, tol, maxit, x, rep);
+}
+
+static int pcg_solve_impl(const or_op* op, const prec_t* P, const double* b, const double* x0,
+                          double tol, int maxit, double* x, or_report* rep) {
+  const int m = P->m;
   const int64_t n = op_n(op);
   if (!(tol > 0.0)) return fail(OR_INVALID, "pcg_solve: tol must be positive");
   if (maxit < 1) return fail(OR_INVALID, "pcg_solve: maxit must be >= 1");
-  const int mdeg = m < 0 ? 0 : m;
+  const int mdeg = m < 0 ? 0 : (P->newton ? (1 << m) - 1 : m);
   const double t0 = now_s();
   memset(rep, 0, sizeof *rep);
   double* r = (double*)malloc(sizeof(double) * (size_t)n);
@@ -329,7 +362,7 @@ int or_pcg_solve(const or_op* op, const double* tds, const double* rho_c, int m,
     rep->rel_res = 1.0;
   }
   if (m >= 0) {
-    or_apply_chebyshev(op, tds, rho_c, m, r, z);
+    prec_apply(op, P, r, z);
     rep->prec_applies++;
     rep->matvec += mdeg;
   } else {
@@ -370,7 +403,7 @@ int or_pcg_solve(const or_op* op, const double* tds, const double* rho_c, int m,
     }
     if (it == maxit) break;
     if (m >= 0) {
-      or_apply_chebyshev(op, tds, rho_c, m, r, z);
+      prec_apply(op, P, r, z);
       rep->prec_applies++;
       rep->matvec += mdeg;
     } else {

@@ -79,6 +79,10 @@ int or_apply_newton(const or_op* op, const double* zeta, int nlev, const double*
 int or_pcg_solve(const or_op* op, const double* tds, const double* rho, int m, const double* b,
                  const double* x0, double tol, int maxit, double* x, or_report* rep);
 
+/* pcg_solve with a NewtonPreconditioner (pcg.hpp:27-40): zeta[nlev+1]. */
+int or_pcg_solve_newton(const or_op* op, const double* zeta, int nlev, const double* b,
+                        const double* x0, double tol, int maxit, double* x, or_report* rep);
+
 /* power_method / dacg_smallest (eigenest.cpp:48-167): out = {value, iters,
  * matvecs, converged}. */
 int or_power_method(const or_op* op, double tol, int maxit, uint64_t seed, double* out);

@@ -17,6 +17,7 @@
 //   ref_apply_chebyshev   -> polycg::apply_chebyshev      (proj/src/polyprec.cpp:169-198)
 //   ref_apply_newton      -> polycg::apply_newton         (proj/src/polyprec.cpp:148-160)
 //   ref_pcg_solve         -> polycg::pcg_solve            (proj/src/pcg.cpp:10-117)
+//   ref_pcg_solve_newton  -> polycg::pcg_solve with NewtonPreconditioner (pcg.hpp:27-40)
 //   ref_spectrum_table    -> polycg::spectrum_table       (proj/src/spectrum.cpp:59-88)
 //
 // Operators: kind 0 = StencilOperator(lap3d, nx), kind 1 = StencilOperator(lap2d, nx),
@@ -197,10 +198,33 @@ struct RefReport {
 
 // m < 0 -> no preconditioner (plain CG). b may be NULL -> b = A x_true with
 // x_true = random_uniform_vector(n, seed) (tools/polycg.cpp:266-278,375-376).
+// newton = 0: ChebyshevPreconditioner(cheb_params(alpha, beta, m, scale)), m < 0 none;
+// newton = 1: NewtonPreconditioner(newton_params(alpha, beta, m = nlev, scale)).
+int ref_pcg_solve_prec(int kind, std::int64_t nx, std::int64_t n, const std::int64_t* rp,
+                       const std::int64_t* ci, const double* va, double alpha, double beta, int m,
+                       double scale, int newton, const double* b, std::uint64_t seed, double tol,
+                       int maxit, double* x_out, double* b_out, RefReport* rep);
+
 int ref_pcg_solve(int kind, std::int64_t nx, std::int64_t n, const std::int64_t* rp,
                   const std::int64_t* ci, const double* va, double alpha, double beta, int m,
                   double scale, const double* b, std::uint64_t seed, double tol, int maxit,
                   double* x_out, double* b_out, RefReport* rep) {
+  return ref_pcg_solve_prec(kind, nx, n, rp, ci, va, alpha, beta, m, scale, 0, b, seed, tol, maxit,
+                            x_out, b_out, rep);
+}
+
+int ref_pcg_solve_newton(int kind, std::int64_t nx, std::int64_t n, const std::int64_t* rp,
+                         const std::int64_t* ci, const double* va, double alpha, double beta,
+                         int nlev, double scale, const double* b, std::uint64_t seed, double tol,
+                         int maxit, double* x_out, double* b_out, RefReport* rep) {
+  return ref_pcg_solve_prec(kind, nx, n, rp, ci, va, alpha, beta, nlev, scale, 1, b, seed, tol,
+                            maxit, x_out, b_out, rep);
+}
+
+int ref_pcg_solve_prec(int kind, std::int64_t nx, std::int64_t n, const std::int64_t* rp,
+                       const std::int64_t* ci, const double* va, double alpha, double beta, int m,
+                       double scale, int newton, const double* b, std::uint64_t seed, double tol,
+                       int maxit, double* x_out, double* b_out, RefReport* rep) {
   return guarded([&] {
     RefProblem p = make_problem(kind, nx, n, rp, ci, va);
     const Index N = p.scaled->size();
@@ -215,8 +239,9 @@ int ref_pcg_solve(int kind, std::int64_t nx, std::int64_t n, const std::int64_t*
     SolveOptions opts;
     opts.tol = tol;
     opts.maxit = maxit;
-    std::unique_ptr<ChebyshevPreconditioner> prec;
-    if (m >= 0) prec = std::make_unique<ChebyshevPreconditioner>(cheb_params(alpha, beta, m, scale));
+    std::unique_ptr<Preconditioner> prec;
+    if (newton) prec = std::make_unique<NewtonPreconditioner>(newton_params(alpha, beta, m, scale));
+    else if (m >= 0) prec = std::make_unique<ChebyshevPreconditioner>(cheb_params(alpha, beta, m, scale));
     auto [x, report] = pcg_solve(*p.scaled, bv, opts, prec.get());
     if (x_out) std::memcpy(x_out, x.data(), sizeof(double) * static_cast<std::size_t>(N));
     rep->iters = report.iters;

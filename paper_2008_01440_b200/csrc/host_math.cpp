@@ -65,6 +65,76 @@ int cheb_params(double alpha, double beta, int m, double scale, double* tds, dou
   return 0;
 }
 
+// eval_poly, Newton form (polyprec.cpp:81-87): the scalar mirror of the recursion.
+double newton_eval(const double* zeta, int nlev, double lambda) {
+  double r = zeta[0];
+  for (int j = 1; j <= nlev; ++j) r = zeta[j] * (2.0 * r - lambda * r * r);
+  return r;
+}
+
+// newton_params (polyprec.cpp:27-54): zeta[0..nlev]; same validation and
+// positivity check (1000-point grid on [alpha0, beta0]) as the reference.
+int newton_params(double alpha0, double beta0, int nlev, double scale, double* zeta,
+                  std::string* msg) {
+  if (!(alpha0 > 0.0) || !(beta0 >= alpha0)) {
+    *msg = "newton_params: need 0 < alpha0 <= beta0";
+    return PCGX_ERR_INVALID;
+  }
+  if (nlev < 0) {
+    *msg = "newton_params: nlev must be >= 0";
+    return PCGX_ERR_INVALID;
+  }
+  if (!(scale >= 1.0)) {
+    *msg = "newton_params: scale must be >= 1";
+    return PCGX_ERR_INVALID;
+  }
+  const double theta = 0.5 * (alpha0 + beta0);
+  const double delta = 0.5 * (beta0 - alpha0);
+  zeta[0] = 1.0 / (scale * theta);
+  if (nlev >= 1) {
+    const double t = (scale * theta - delta) * zeta[0];
+    zeta[1] = 2.0 / (1.0 + 2.0 * t - t * t);
+    for (int j = 2; j <= nlev; ++j) {
+      const double z = zeta[j - 1];
+      zeta[j] = 2.0 / (1.0 + 2.0 * z - z * z);
+    }
+  }
+  constexpr int kGrid = 1000;
+  for (int g = 0; g < kGrid; ++g) {
+    const double lam = alpha0 + (beta0 - alpha0) * static_cast<double>(g) / (kGrid - 1);
+    if (!(newton_eval(zeta, nlev, lam) > 0.0)) {
+      *msg = "polynomial preconditioner not positive at lambda = " + std::to_string(lam);
+      return PCGX_ERR_NUMERICAL;
+    }
+  }
+  return 0;
+}
+
+// chi_sequence (polyprec.cpp:102-123): chi_j = 2 sigma_k^2 / sigma_{2k}.
+int chi_sequence(double alpha, double beta, int nlev, double* chi, std::string* msg) {
+  if (!(alpha > 0.0) || !(beta > alpha)) {
+    *msg = "chi_sequence: need 0 < alpha < beta";
+    return PCGX_ERR_INVALID;
+  }
+  if (nlev < 0 || nlev > 30) {
+    *msg = "chi_sequence: nlev must be in [0, 30]";
+    return PCGX_ERR_INVALID;
+  }
+  double sigma_k = (alpha + beta) / (beta - alpha);
+  bool huge = false;
+  for (int j = 0; j < nlev; ++j) {
+    if (huge || sigma_k > 1e150) {  // 2 sigma_k^2 would overflow; chi is 1 from here on
+      huge = true;
+      chi[j] = 1.0;
+      continue;
+    }
+    const double sigma_2k = 2.0 * sigma_k * sigma_k - 1.0;
+    chi[j] = 2.0 * sigma_k * sigma_k / sigma_2k;
+    sigma_k = sigma_2k;
+  }
+  return 0;
+}
+
 // linop.cpp:382-390
 void analytic_extremes(int dim, long long nx, int scaled, double* lo, double* hi) {
   const double pi = 3.141592653589793238462643383279502884;

@@ -310,6 +310,63 @@ struct EpiChebStep {
   }
 };
 
+// Newton form (polyprec.cpp:135-160), one SpMV of the recursion fused with the
+// element-wise steps that follow it in the reference's order:
+//   nchain == 0 : out = zeta0 * (A x)                    (the next level-0 scale)
+//   nchain >= 1 : t = zeta0 * (A x); t = zeta1 * ((2 x) - t)    [u = L0 = x]
+//                 t = zeta2 * ((2 L1) - t); t = zeta3 * ((2 L2) - t)   (nchain 2, 3)
+// u1, u2 = L1, L2 (per-point operands v[0], v[1]); with a reduction the
+// operand slot after the chain's holds r and the contribution is r_i out_i.
+struct EpiNewton {
+  double* out;
+  const double* u1;
+  const double* u2;
+  double z0, z1, z2, z3;
+  int nchain;
+  __device__ __forceinline__ void pf(long long idx) const {
+    if (u1) prefetch_l2(u1 + idx);
+    if (u2) prefetch_l2(u2 + idx);
+  }
+  __device__ __forceinline__ void ld(long long idx, double (&v)[2]) const {
+    v[0] = u1 ? __ldg(u1 + idx) : 0.0;
+    v[1] = u2 ? __ldg(u2 + idx) : 0.0;
+  }
+  __device__ __forceinline__ void ld2(long long idx, double2 (&v)[2]) const {
+    v[0] = u1 ? ldg2(u1 + idx) : make_double2(0.0, 0.0);
+    v[1] = u2 ? ldg2(u2 + idx) : make_double2(0.0, 0.0);
+  }
+  __device__ __forceinline__ double f(double y, double xc, double a, double b) const {
+    double t = z0 * y;
+    if (nchain >= 1) t = z1 * ((2.0 * xc) - t);
+    if (nchain >= 2) t = z2 * ((2.0 * a) - t);
+    if (nchain >= 3) t = z3 * ((2.0 * b) - t);
+    return t;
+  }
+  // reduction operand: the slot after the chain's operands
+  __device__ __forceinline__ double rr(double a, double b) const { return nchain >= 2 ? b : a; }
+  __device__ __forceinline__ double st(long long idx, double y, double xc, const double (&v)[2]) const {
+    const double t = f(y, xc, v[0], v[1]);
+    out[idx] = t;
+    return rr(v[0], v[1]) * t;
+  }
+  __device__ __forceinline__ double st2(long long idx, double y0, double y1, double2 xc,
+                                        const double2 (&v)[2]) const {
+    const double a = f(y0, xc.x, v[0].x, v[1].x), b = f(y1, xc.y, v[0].y, v[1].y);
+    pcgx::st2(out + idx, a, b);
+    return rr(v[0].x, v[1].x) * a + rr(v[0].y, v[1].y) * b;
+  }
+};
+
+// The rest of a Newton chain that did not fit the SpMV epilogue, element-wise:
+// out = zeta[j] * ((2 L[j-1]) - out) for j = j0 .. j1 (polyprec.cpp:145);
+// optional contribution r_i out_i.
+constexpr int kNewtonMaxLev = 24;
+struct NewtonChain {
+  int j0, j1;
+  double zeta[kNewtonMaxLev + 1];
+  const double* L[kNewtonMaxLev];
+};
+
 // ----------------------------------------------------------------- 7-point stencil
 
 // ----------------------------------------------------------------- operator inputs
@@ -880,6 +937,37 @@ zr_kernel(long long n, double* __restrict__ z, const double* __restrict__ r, dou
     acc = acc + ri * zi;
   }
   block_reduce_finish(acc, red);
+}
+
+// Newton level 0 (polyprec.cpp:139-141): out = zeta0 * in; contribution in_i out_i.
+template <bool kRed>
+__global__ void __launch_bounds__(kVecThreads)
+nscale_kernel(long long n, double* __restrict__ out, const double* __restrict__ in, double z0,
+              Reduce red) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = in[i];
+    const double o = z0 * v;
+    out[i] = o;
+    if (kRed) acc = acc + v * o;
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
+template <bool kRed>
+__global__ void __launch_bounds__(kVecThreads)
+nchain_kernel(long long n, double* __restrict__ out, const NewtonChain ch,
+              const double* __restrict__ r, Reduce red) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double t = out[i];
+    for (int j = ch.j0; j <= ch.j1; ++j) t = ch.zeta[j] * ((2.0 * __ldg(ch.L[j - 1] + i)) - t);
+    out[i] = t;
+    if (kRed) acc = acc + __ldg(r + i) * t;
+  }
+  if (kRed) block_reduce_finish(acc, red);
 }
 
 // result = a . b

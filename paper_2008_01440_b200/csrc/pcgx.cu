@@ -59,6 +59,9 @@ struct pcgx_context_s {
          *w1 = nullptr, *w2 = nullptr, *w3 = nullptr, *t0 = nullptr, *t1 = nullptr;
   double* flush = nullptr;
   size_t flush_bytes = 0;
+  // Newton-form level vectors L[0..nlev-1] (NewtonWorkspace, polyprec.hpp:69-71)
+  std::vector<double*> nl;
+  long long nl_n = 0;
   // solve-local bookkeeping
   int64_t cur_launches = 0;
   int64_t cur_allreduce = 0;
@@ -931,6 +934,171 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
   }
 }
 
+// ---------------------------------------------------------------- Newton form
+
+struct Newton {
+  int nlev = 0;
+  std::vector<double> zeta;
+};
+
+Newton newton_from(const pcgx_newton* p) {
+  if (!p) fail(PCGX_ERR_INVALID, "apply_newton: null parameters");
+  if (p->nlev < 0) fail(PCGX_ERR_INVALID, "apply_newton: nlev must be >= 0");
+  if (p->nlev > kNewtonMaxLev)
+    fail(PCGX_ERR_UNSUPPORTED, "apply_newton: nlev > " + std::to_string(kNewtonMaxLev));
+  if (!p->zeta) fail(PCGX_ERR_INVALID, "apply_newton: zeta must have nlev+1 entries");
+  Newton N;
+  N.nlev = p->nlev;
+  N.zeta.assign(p->zeta, p->zeta + p->nlev + 1);
+  return N;
+}
+
+void ensure_newton_ws(pcgx_context c, long long n, int nlev) {
+  if (c->nl_n < n) {
+    for (double* b : c->nl) cudaFree(b);
+    c->nl.clear();
+    c->nl_n = n;
+  }
+  while ((int)c->nl.size() < nlev) {
+    double* b = nullptr;
+    PCGX_CUDA(cudaMalloc(&b, sizeof(double) * (size_t)std::max(n, 1LL)));
+    c->nl.push_back(b);
+  }
+}
+
+// The reference recursion (newton_rec, polyprec.cpp:135-147) unrolled into its
+// element-wise op sequence. Vector ids: -1 = r, -2 = out, k >= 0 = L[k].
+struct NOp {
+  int kind;  // 0: out = zeta0 * in ; 1: out = A in ; 2: out = zeta_j ((2 L[j-1]) - out)
+  int out, in, j;
+};
+void newton_ops(int j, int in, int out, std::vector<NOp>& v) {
+  if (j == 0) {
+    v.push_back({0, out, in, 0});
+    return;
+  }
+  newton_ops(j - 1, in, j - 1, v);  // L[j-1] = P_{j-1} in
+  v.push_back({1, out, j - 1, 0});  // out = A L[j-1]
+  newton_ops(j - 1, out, out, v);   // out = P_{j-1} out
+  v.push_back({2, out, j - 1, j});  // out = zeta_j (2 L[j-1] - out)
+}
+
+// out = P_nlev(A) r; rz_slot >= 0 also reduces r . out. Every SpMV is fused with
+// the element-wise ops that follow it: the level-0 scale of its output (written
+// straight to L[0] when the output itself is dead) and the chain of combine
+// steps on it (up to three in the epilogue, the rest in one element-wise pass).
+// Same ops in the same order per element: bitwise the reference's values.
+void enqueue_newton(pcgx_context c, pcgx_operator op, const Newton& N, const double* r,
+                    double* out, int rz_slot) {
+  const long long n = op->n_local;
+  ensure_newton_ws(c, n, N.nlev);
+  std::vector<NOp> ops;
+  newton_ops(N.nlev, -1, -2, ops);
+  auto vec = [&](int id) -> double* {
+    return id == -1 ? const_cast<double*>(r) : id == -2 ? out : c->nl[(size_t)id];
+  };
+  const double* z = N.zeta.data();
+  const bool red = rz_slot >= 0;
+  size_t i = 0;
+  while (i < ops.size()) {
+    const NOp& o = ops[i];
+    if (o.kind == 0) {  // the first op (level-0 scale of r), or the whole apply at nlev 0
+      const bool rd = red && i + 1 == ops.size();
+      if (rd) nscale_kernel<true><<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, vec(o.out), vec(o.in), z[0], make_red(c, rz_slot));
+      else nscale_kernel<false><<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, vec(o.out), vec(o.in), z[0], Reduce{});
+      check_launch();
+      count_launch(c);
+      ++i;
+      continue;
+    }
+    if (o.kind != 1 || i + 1 >= ops.size() || ops[i + 1].kind != 0 || ops[i + 1].in != o.out)
+      fail(PCGX_ERR_INVALID, "apply_newton: unexpected op sequence");
+    const NOp& sc = ops[i + 1];
+    if (sc.out != o.out) {  // out dead after its level-0 scale: write zeta0 * (A x) to L[0]
+      EpiNewton e{vec(sc.out), nullptr, nullptr, z[0], 0.0, 0.0, 0.0, 0};
+      op_launch<EpiNewton, false>(c, op, vec(o.in), e, -1);
+      i += 2;
+      continue;
+    }
+    size_t k = i + 2;
+    int J = 0;
+    while (k < ops.size() && ops[k].kind == 2 && ops[k].out == o.out) {
+      if (ops[k].j != J + 1 || ops[k].in != J) fail(PCGX_ERR_INVALID, "apply_newton: bad chain");
+      ++J;
+      ++k;
+    }
+    if (J < 1 || o.in != 0) fail(PCGX_ERR_INVALID, "apply_newton: bad chain head");
+    const bool rd = red && k == ops.size();
+    const int jf = std::min(J, rd ? 2 : 3);
+    EpiNewton e{vec(o.out), nullptr, nullptr, z[0], z[1], jf >= 2 ? z[2] : 0.0, jf >= 3 ? z[3] : 0.0, jf};
+    if (jf >= 2) e.u1 = c->nl[1];
+    if (jf >= 3) e.u2 = c->nl[2];
+    const bool rd_here = rd && jf == J;
+    if (rd_here) (jf <= 1 ? e.u1 : e.u2) = r;
+    if (rd_here) op_launch<EpiNewton, true>(c, op, vec(o.in), e, rz_slot);
+    else op_launch<EpiNewton, false>(c, op, vec(o.in), e, -1);
+    if (J > jf) {
+      NewtonChain ch{};
+      ch.j0 = jf + 1;
+      ch.j1 = J;
+      for (int j = 0; j <= J; ++j) ch.zeta[j] = z[j];
+      for (int j = 1; j <= J; ++j) ch.L[j - 1] = c->nl[(size_t)(j - 1)];
+      if (rd) nchain_kernel<true><<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, vec(o.out), ch, r, make_red(c, rz_slot));
+      else nchain_kernel<false><<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, vec(o.out), ch, r, Reduce{});
+      check_launch();
+      count_launch(c);
+    }
+    i = k;
+  }
+}
+
+double spmv_equiv_bytes(pcgx_operator op);
+
+// Algorithmic bytes of one Newton application (same plan as enqueue_newton).
+double newton_bytes(pcgx_operator op, int nlev, bool red) {
+  std::vector<NOp> ops;
+  newton_ops(nlev, -1, -2, ops);
+  const double N8 = 8.0 * (double)op->n_local;
+  const double spmv = spmv_equiv_bytes(op);
+  double b = 0.0;
+  size_t i = 0;
+  while (i < ops.size()) {
+    if (ops[i].kind == 0) {
+      b += 2 * N8;
+      ++i;
+      continue;
+    }
+    if (ops[i + 1].out != ops[i].out) {
+      b += spmv;
+      i += 2;
+      continue;
+    }
+    size_t k = i + 2;
+    int J = 0;
+    while (k < ops.size() && ops[k].kind == 2 && ops[k].out == ops[i].out) ++J, ++k;
+    const bool rd = red && k == ops.size();
+    const int jf = std::min(J, rd ? 2 : 3);
+    b += spmv + (double)(jf - 1) * N8 + ((rd && jf == J) ? N8 : 0.0);
+    if (J > jf) b += (double)(2 + (J - jf) + (rd ? 1 : 0)) * N8;
+    i = k;
+  }
+  return b;
+}
+
+// The preconditioner of a solve: none (plain CG), Chebyshev or Newton form.
+struct Prec {
+  int kind = 0;  // 0 none, 1 Chebyshev, 2 Newton
+  Cheb cheb;
+  Newton newton;
+  int degree() const { return kind == 1 ? cheb.m : kind == 2 ? (1 << newton.nlev) - 1 : 0; }
+};
+
+void enqueue_prec(pcgx_context c, pcgx_operator op, const Prec& P, const double* r, double* out,
+                  int rz_slot) {
+  if (P.kind == 1) enqueue_cheb(c, op, P.cheb, r, out, rz_slot);
+  else enqueue_newton(c, op, P.newton, r, out, rz_slot);
+}
+
 // ---------------------------------------------------------------- PCG
 
 struct Graph {
@@ -991,18 +1159,17 @@ double cheb_step_bytes(pcgx_operator op) {
   return 12.0 * (double)op->nnz + 4.0 * (double)(op->n_local + 1) + 40.0 * (double)op->n_local;
 }
 
-void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in,
-                      const double* b, double* x, const pcgx_solve_opts* o, pcgx_report* rep) {
+void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const double* b,
+                      double* x, const pcgx_solve_opts* o, pcgx_report* rep) {
   if (op->ctx != c) fail(PCGX_ERR_INVALID, "pcg_solve: operator belongs to another context");
   pcgx_solve_opts opts;
   pcgx_solve_opts_default(&opts);
   if (o) opts = *o;
   if (!(opts.tol > 0.0)) fail(PCGX_ERR_INVALID, "pcg_solve: tol must be positive");
   if (opts.maxit < 1) fail(PCGX_ERR_INVALID, "pcg_solve: maxit must be >= 1");
-  const bool have_prec = prec_in != nullptr;
-  Cheb P;
-  if (have_prec) P = cheb_from(prec_in);
-  const int m = have_prec ? P.m : 0;
+  const bool have_prec = prec.kind != 0;
+  const Cheb& P = prec.cheb;
+  const int m = prec.degree();
   const long long n = op->n_local;
   ensure_workspace(c, n, ws_pad_of(op));
   const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && env_int("PCGX_NO_GRAPH", 0) == 0 &&
@@ -1037,6 +1204,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   const double N8 = 8.0 * (double)n;
   auto cheb_bytes = [&]() -> double {  // one preconditioner application incl. r.z
     if (!have_prec) return 2 * N8;
+    if (prec.kind == 2) return newton_bytes(op, prec.newton.nlev, true);
     if (m == 0) return 2 * N8;
     const double spmv_extra = spmv_equiv_bytes(op) - 2 * N8;  // matrix bytes (CSR)
     if (m == 1) return spmv_extra + 2 * N8;
@@ -1085,13 +1253,13 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
 
   // zmode: 0 = Chebyshev m >= 1 (z from the fused recurrence), 1 = m == 0 (z = r/theta
   // written by the update kernel), 2 = no preconditioner (z is r itself).
-  const int zm = !have_prec ? 2 : (m == 0 ? 1 : 0);
+  const int zm = !have_prec ? 2 : (prec.kind == 1 && m == 0 ? 1 : 0);
   const double* zvec = (zm == 2) ? r : z;
   double* Pd[2] = {p, c->p2};  // direction ping-pong: p(it) lives in Pd[it & 1]
   const bool fuse = fuses_dir_update(op) && env_int("PCGX_NO_FUSE_P", 0) == 0;
 
   // setup: z_0 = P r_0 and rho_0 = r'z -> rz(0) (pcg.cpp:57-64)
-  if (zm == 0) enqueue_cheb(c, op, P, r, z, slot_rz(0));
+  if (zm == 0) enqueue_prec(c, op, prec, r, z, slot_rz(0));
   else if (zm == 1) launch_zr(c, n, z, r, P.theta, 1, slot_rz(0));
   else launch_dot(c, n, r, r, slot_rz(0));
   allreduce(c, slot_rz(0), 1);
@@ -1141,7 +1309,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   auto enqueue_B = [&](int it) {
     const int par = it & 1;
     if (zm == 0) {
-      enqueue_cheb(c, op, P, r, z, slot_rz(par));
+      enqueue_prec(c, op, prec, r, z, slot_rz(par));
       if (!spec_after_update) {
         allreduce(c, slot_rr(par), 2);
         snapshot();
@@ -1228,7 +1396,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec_in
   // Optional: time the dominant kernel with CUDA events on the compute stream, on
   // this solve's operator and buffers: the two-step pass (stencil, cheb2) or the
   // fused single middle step.
-  if ((opts.flags & PCGX_FLAG_TIME_KERNELS) && have_prec && m >= 4) {
+  if ((opts.flags & PCGX_FLAG_TIME_KERNELS) && prec.kind == 1 && m >= 4) {
     const int reps = std::max(3, env_int("PCGX_STEP_REPS", 20));
     const bool two = (op->kind == 0 && op->cheb2);
     Cheb2Params q{};
@@ -1934,6 +2102,7 @@ void pcgx_context_destroy(pcgx_context c) {
   double* bufs[] = {c->flush, c->S, c->partials};
   for (double* b : bufs)
     if (b) cudaFree(b);
+  for (double* b : c->nl) cudaFree(b);
   cudaFree(c->counter);
   cudaFreeHost(c->hS);
   cudaEvent_t evs[] = {c->ev_t0, c->ev_t1, c->ev_sync, c->ev_fork, c->ev_join};
@@ -2180,6 +2349,49 @@ pcgx_status pcgx_cheb_apply(pcgx_context c, pcgx_operator op, const pcgx_cheb* p
   });
 }
 
+pcgx_status pcgx_newton_params(double alpha0, double beta0, int nlev, double scale,
+                               double* zeta) {
+  std::string msg;
+  const int st = pcgx::newton_params(alpha0, beta0, nlev, scale, zeta, &msg);
+  if (st) g_thread_err = msg;
+  return (pcgx_status)st;
+}
+
+double pcgx_newton_eval(const pcgx_newton* p, double lambda) {
+  return newton_eval(p->zeta, p->nlev, lambda);
+}
+
+pcgx_status pcgx_chi_sequence(double alpha, double beta, int nlev, double* chi) {
+  std::string msg;
+  const int st = pcgx::chi_sequence(alpha, beta, nlev, chi, &msg);
+  if (st) g_thread_err = msg;
+  return (pcgx_status)st;
+}
+
+pcgx_status pcgx_newton_apply_device(pcgx_context c, pcgx_operator op, const pcgx_newton* p,
+                                     const double* r, double* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (r == out) fail(PCGX_ERR_INVALID, "apply_newton: out must not alias r");
+    Newton N = newton_from(p);
+    enqueue_newton(c, op, N, r, out, -1);
+  });
+}
+
+pcgx_status pcgx_newton_apply(pcgx_context c, pcgx_operator op, const pcgx_newton* p,
+                              const double* r, double* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    const long long n = op->n_local;
+    ensure_workspace(c, n, ws_pad_of(op));
+    Newton N = newton_from(p);
+    PCGX_CUDA(cudaMemcpyAsync(c->t0, r, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
+    enqueue_newton(c, op, N, c->t0, c->t1, -1);
+    PCGX_CUDA(cudaMemcpyAsync(out, c->t1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
 void pcgx_solve_opts_default(pcgx_solve_opts* o) {
   o->tol = 1e-8;
   o->maxit = 20000;
@@ -2187,37 +2399,75 @@ void pcgx_solve_opts_default(pcgx_solve_opts* o) {
   o->flags = 0;
 }
 
+namespace {
+Prec prec_of_cheb(const pcgx_cheb* p) {
+  Prec P;
+  if (p) {
+    P.kind = 1;
+    P.cheb = cheb_from(p);
+  }
+  return P;
+}
+Prec prec_of_newton(const pcgx_newton* p) {
+  Prec P;
+  if (p) {
+    P.kind = 2;
+    P.newton = newton_from(p);
+  }
+  return P;
+}
+
+pcgx_status solve_device_entry(pcgx_context c, pcgx_operator op, const Prec& P, const double* b,
+                               double* x, const pcgx_solve_opts* opts, pcgx_report* rep) {
+  set_device(c);
+  if (!rep) fail(PCGX_ERR_INVALID, "pcg_solve: null report");
+  pcg_solve_device(c, op, P, b, x, opts, rep);
+  return PCGX_OK;
+}
+
+// Host-buffer entry: b and x live in t0 / t1 for the call (the solver uses r z p q w0..w3).
+void solve_host_entry(pcgx_context c, pcgx_operator op, const Prec& P, const double* b, double* x,
+                      const pcgx_solve_opts* opts, pcgx_report* rep) {
+  set_device(c);
+  if (!rep) fail(PCGX_ERR_INVALID, "pcg_solve: null report");
+  const long long n = op->n_local;
+  ensure_workspace(c, n, ws_pad_of(op));
+  PCGX_CUDA(cudaMemcpyAsync(c->t0, b, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
+  pcgx_solve_opts o;
+  pcgx_solve_opts_default(&o);
+  if (opts) o = *opts;
+  if (o.x0) {
+    PCGX_CUDA(cudaMemcpyAsync(c->t1, o.x0, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
+    o.x0 = c->t1;
+  }
+  pcg_solve_device(c, op, P, c->t0, c->t1, &o, rep);
+  PCGX_CUDA(cudaMemcpyAsync(x, c->t1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
+  PCGX_CUDA(cudaStreamSynchronize(c->s));
+}
+}  // namespace
+
 pcgx_status pcgx_pcg_solve_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec,
                                   const double* b, double* x, const pcgx_solve_opts* opts,
                                   pcgx_report* rep) {
-  return guarded(c, [&] {
-    set_device(c);
-    if (!rep) fail(PCGX_ERR_INVALID, "pcg_solve: null report");
-    pcg_solve_device(c, op, prec, b, x, opts, rep);
-  });
+  return guarded(c, [&] { solve_device_entry(c, op, prec_of_cheb(prec), b, x, opts, rep); });
+}
+
+pcgx_status pcgx_pcg_solve_newton_device(pcgx_context c, pcgx_operator op,
+                                         const pcgx_newton* prec, const double* b, double* x,
+                                         const pcgx_solve_opts* opts, pcgx_report* rep) {
+  return guarded(c, [&] { solve_device_entry(c, op, prec_of_newton(prec), b, x, opts, rep); });
+}
+
+pcgx_status pcgx_pcg_solve_newton(pcgx_context c, pcgx_operator op, const pcgx_newton* prec,
+                                  const double* b, double* x, const pcgx_solve_opts* opts,
+                                  pcgx_report* rep) {
+  return guarded(c, [&] { solve_host_entry(c, op, prec_of_newton(prec), b, x, opts, rep); });
 }
 
 pcgx_status pcgx_pcg_solve(pcgx_context c, pcgx_operator op, const pcgx_cheb* prec,
                            const double* b, double* x, const pcgx_solve_opts* opts,
                            pcgx_report* rep) {
-  return guarded(c, [&] {
-    set_device(c);
-    if (!rep) fail(PCGX_ERR_INVALID, "pcg_solve: null report");
-    const long long n = op->n_local;
-    ensure_workspace(c, n, ws_pad_of(op));
-    // b and x live in t0 / t1 for the call (the solver uses r z p q w0 w1)
-    PCGX_CUDA(cudaMemcpyAsync(c->t0, b, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
-    pcgx_solve_opts o;
-    pcgx_solve_opts_default(&o);
-    if (opts) o = *opts;
-    if (o.x0) {
-      PCGX_CUDA(cudaMemcpyAsync(c->t1, o.x0, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
-      o.x0 = c->t1;
-    }
-    pcg_solve_device(c, op, prec, c->t0, c->t1, &o, rep);
-    PCGX_CUDA(cudaMemcpyAsync(x, c->t1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
-    PCGX_CUDA(cudaStreamSynchronize(c->s));
-  });
+  return guarded(c, [&] { solve_host_entry(c, op, prec_of_cheb(prec), b, x, opts, rep); });
 }
 
 pcgx_status pcgx_random_uniform_device(pcgx_context c, int64_t n, uint64_t seed, uint64_t offset,

@@ -14,6 +14,9 @@ LinearOperator::apply             ``ScaledOperator.apply(x)``
 cheb_params / eval_poly           ``cheb_params`` / ``eval_poly``
 apply_chebyshev                   ``apply_chebyshev(params, op, r)``
 ChebyshevPreconditioner           ``ChebyshevPreconditioner(params)``
+newton_params / chi_sequence      ``newton_params`` / ``chi_sequence``
+apply_newton                      ``apply_newton(params, op, r)``
+NewtonPreconditioner              ``NewtonPreconditioner(params)``
 SolveOptions / SolveReport        ``SolveOptions`` / ``SolveReport``
 pcg_solve(op, b, opts, prec)      ``pcg_solve(op, b, opts, prec)``
 random_uniform_vector(n, seed)    ``random_uniform_vector(n, seed)``
@@ -82,6 +85,10 @@ class _Cheb(C.Structure):
                 ("sigma", C.c_double), ("rho", _dp)]
 
 
+class _Newton(C.Structure):
+    _fields_ = [("nlev", C.c_int), ("zeta", _dp)]
+
+
 class _Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("maxit", C.c_int), ("x0", _vp), ("flags", C.c_uint32)]
 
@@ -116,7 +123,9 @@ SYMBOLS = [
     "pcgx_analytic_extremes", "pcgx_analytic_extremes_box", "pcgx_lanczos_bounds",
     "pcgx_power_method", "pcgx_dacg_smallest",
     "pcgx_gen_fe27_size", "pcgx_gen_fe27_fill", "pcgx_gen_elast27_size",
-    "pcgx_gen_elast27_fill",
+    "pcgx_gen_elast27_fill", "pcgx_newton_params", "pcgx_newton_eval", "pcgx_chi_sequence",
+    "pcgx_newton_apply", "pcgx_newton_apply_device", "pcgx_pcg_solve_newton",
+    "pcgx_pcg_solve_newton_device",
 ]
 
 _lib = None
@@ -184,6 +193,17 @@ def lib():
         "pcgx_cheb_eval": (C.c_double, [C.POINTER(_Cheb), C.c_double]),
         "pcgx_cheb_apply": (C.c_int, [ctx, op, C.POINTER(_Cheb), _dp, _dp]),
         "pcgx_cheb_apply_device": (C.c_int, [ctx, op, C.POINTER(_Cheb), C.c_void_p, C.c_void_p]),
+        "pcgx_newton_params": (C.c_int, [C.c_double, C.c_double, C.c_int, C.c_double, _dp]),
+        "pcgx_newton_eval": (C.c_double, [C.POINTER(_Newton), C.c_double]),
+        "pcgx_chi_sequence": (C.c_int, [C.c_double, C.c_double, C.c_int, _dp]),
+        "pcgx_newton_apply": (C.c_int, [ctx, op, C.POINTER(_Newton), _dp, _dp]),
+        "pcgx_newton_apply_device": (C.c_int, [ctx, op, C.POINTER(_Newton), C.c_void_p,
+                                               C.c_void_p]),
+        "pcgx_pcg_solve_newton": (C.c_int, [ctx, op, C.POINTER(_Newton), _dp, _dp,
+                                            C.POINTER(_Opts), C.POINTER(_Report)]),
+        "pcgx_pcg_solve_newton_device": (C.c_int, [ctx, op, C.POINTER(_Newton), C.c_void_p,
+                                                   C.c_void_p, C.POINTER(_Opts),
+                                                   C.POINTER(_Report)]),
         "pcgx_solve_opts_default": (None, [C.POINTER(_Opts)]),
         "pcgx_pcg_solve": (C.c_int, [ctx, op, C.POINTER(_Cheb), _dp, _dp, C.POINTER(_Opts),
                                      C.POINTER(_Report)]),
@@ -510,8 +530,45 @@ def cheb_params(alpha, beta, m, scale=1.0) -> ChebyshevParams:
     return ChebyshevParams(int(m), alpha, beta, scale, tds[0], tds[1], tds[2], rho)
 
 
-def eval_poly(params: ChebyshevParams, lam: float) -> float:
+def eval_poly(params, lam: float) -> float:
+    """eval_poly (polyprec.cpp:81-100), Chebyshev or Newton form."""
+    if isinstance(params, NewtonParams):
+        return lib().pcgx_newton_eval(C.byref(params._c()), lam)
     return lib().pcgx_cheb_eval(C.byref(params._c()), lam)
+
+
+@dataclass
+class NewtonParams:
+    """NewtonParams (polyprec.hpp:22-31)."""
+    nlev: int
+    alpha0: float
+    beta0: float
+    scale: float
+    zeta: np.ndarray = field(repr=False)
+
+    def degree(self):
+        return (1 << self.nlev) - 1
+
+    def _c(self):
+        s = _Newton()
+        s.nlev = self.nlev
+        self._zeta_keep = np.ascontiguousarray(self.zeta, dtype=np.float64)
+        s.zeta = _ptr(self._zeta_keep)
+        return s
+
+
+def newton_params(alpha0, beta0, nlev, scale=1.0) -> NewtonParams:
+    """newton_params (polyprec.cpp:27-54), bit-exact, with the positivity check."""
+    zeta = np.zeros(max(int(nlev), 0) + 1)
+    _check(lib().pcgx_newton_params(alpha0, beta0, int(nlev), scale, _ptr(zeta)), None)
+    return NewtonParams(int(nlev), alpha0, beta0, scale, zeta)
+
+
+def chi_sequence(alpha, beta, nlev) -> np.ndarray:
+    """chi_sequence (polyprec.cpp:102-123)."""
+    chi = np.zeros(max(int(nlev), 0))
+    _check(lib().pcgx_chi_sequence(alpha, beta, int(nlev), _ptr(chi)), None)
+    return chi
 
 
 class ChebyshevPreconditioner:
@@ -542,6 +599,38 @@ def apply_chebyshev(params: ChebyshevParams, op: ScaledOperator, r):
         raise InvalidArgument("apply_chebyshev: vector length mismatch")
     out = np.empty(op.local_size())
     _check(lib().pcgx_cheb_apply(op.ctx.h, op.h, C.byref(cp), _ptr(r), _ptr(out)), op.ctx.h)
+    return out
+
+
+class NewtonPreconditioner:
+    """NewtonPreconditioner (pcg.hpp:27-40)."""
+
+    def __init__(self, params: NewtonParams):
+        self._params = params
+
+    def params(self):
+        return self._params
+
+    def degree(self):
+        return self._params.degree()
+
+    def apply(self, op: ScaledOperator, r):
+        return apply_newton(self._params, op, r)
+
+
+def apply_newton(params: NewtonParams, op: ScaledOperator, r):
+    """out = P_nlev(A) r (polyprec.cpp:135-160) on the device: 2^nlev - 1 matvecs."""
+    cp = params._c()
+    if isinstance(r, DeviceVector):
+        out = DeviceVector(op.ctx, op.local_size())
+        _check(lib().pcgx_newton_apply_device(op.ctx.h, op.h, C.byref(cp), r.ptr, out.ptr),
+               op.ctx.h)
+        return out
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    if r.size != op.local_size():
+        raise InvalidArgument("apply_newton: vector length mismatch")
+    out = np.empty(op.local_size())
+    _check(lib().pcgx_newton_apply(op.ctx.h, op.h, C.byref(cp), _ptr(r), _ptr(out)), op.ctx.h)
     return out
 
 
@@ -585,7 +674,7 @@ class SolveReport:
 
 
 def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
-              prec: ChebyshevPreconditioner | None = None, x_out=None):
+              prec: ChebyshevPreconditioner | NewtonPreconditioner | None = None, x_out=None):
     """pcg_solve (pcg.cpp:10-117) on the GPU.
 
     b numpy -> host entry (b copied in, x copied out inside the call; returns
@@ -598,13 +687,15 @@ def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
     L.pcgx_solve_opts_default(C.byref(o))
     o.tol, o.maxit, o.flags = opts.tol, opts.maxit, opts.flags
     rep = _Report()
+    newton = isinstance(prec, NewtonPreconditioner)
     cp = C.byref(prec.params()._c()) if prec is not None else None
+    f_dev = L.pcgx_pcg_solve_newton_device if newton else L.pcgx_pcg_solve_device
+    f_host = L.pcgx_pcg_solve_newton if newton else L.pcgx_pcg_solve
     if isinstance(b, DeviceVector):
         x = x_out or DeviceVector(op.ctx, op.local_size())
         if opts.x0 is not None:
             o.x0 = opts.x0.ptr
-        _check(L.pcgx_pcg_solve_device(op.ctx.h, op.h, cp, b.ptr, x.ptr, C.byref(o),
-                                       C.byref(rep)), op.ctx.h)
+        _check(f_dev(op.ctx.h, op.h, cp, b.ptr, x.ptr, C.byref(o), C.byref(rep)), op.ctx.h)
         return x, SolveReport._from(rep)
     b = np.ascontiguousarray(b, dtype=np.float64)
     if b.size != op.local_size():
@@ -616,8 +707,8 @@ def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
         if x0.size != b.size:
             raise InvalidArgument("pcg_solve: x0 length mismatch")
         o.x0 = x0.ctypes.data
-    _check(L.pcgx_pcg_solve(op.ctx.h, op.h, cp, _ptr(b), x.ctypes.data_as(_dp), C.byref(o),
-                            C.byref(rep)), op.ctx.h)
+    _check(f_host(op.ctx.h, op.h, cp, _ptr(b), x.ctypes.data_as(_dp), C.byref(o), C.byref(rep)),
+           op.ctx.h)
     return x, SolveReport._from(rep)
 
 

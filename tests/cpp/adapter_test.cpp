@@ -68,14 +68,45 @@ int main() {
   bad += run_case("stencil40_m10", st40, 40, 10, 1.001, sess);
   const CsrMatrix cs30 = assemble_laplacian(StencilKind::lap3d, 30);
   bad += run_case("csr30_m20", cs30, 30, 20, 1.001, sess);
-  // error path: a non-Chebyshev preconditioner is rejected like a bad argument
+  // NewtonPreconditioner (pcg.hpp:27-40): same call, same answer
+  {
+    auto [scaled, d] = jacobi_scale(st40);
+    const auto [a0, b0] = analytic_extremes(StencilKind::lap3d, 40, true);
+    const Vector b = scaled.apply(random_uniform_vector(scaled.size(), 20240801));
+    NewtonPreconditioner p_cpu(newton_params(a0, b0, 3, 1.001));
+    NewtonPreconditioner p_gpu(newton_params(a0, b0, 3, 1.001));
+    auto [x_ref, r_ref] = pcg_solve(scaled, b, {}, &p_cpu);
+    polycg::gpu::DeviceOperator dop(sess, scaled);
+    auto [x_gpu, r_gpu] = polycg::gpu::pcg_solve(sess, dop, scaled, b, {}, &p_gpu);
+    double dn = 0.0, xn = 0.0;
+    for (Index i = 0; i < x_ref.size(); ++i) {
+      dn += (x_gpu[i] - x_ref[i]) * (x_gpu[i] - x_ref[i]);
+      xn += x_ref[i] * x_ref[i];
+    }
+    const double rel = std::sqrt(dn / xn);
+    Vector r0 = random_uniform_vector(scaled.size(), 4242), o_gpu;
+    const Vector o_cpu = apply_newton(newton_params(a0, b0, 4, 1.001), scaled, r0);
+    polycg::gpu::apply_newton(sess, dop, newton_params(a0, b0, 4, 1.001), r0, o_gpu);
+    bool bitwise = true;
+    for (Index i = 0; i < r0.size(); ++i) bitwise = bitwise && (o_cpu[i] == o_gpu[i]);
+    const bool ok = std::abs(r_gpu.iters - r_ref.iters) <= 1 && rel <= 1e-10 && bitwise &&
+                    r_gpu.ddot == r_ref.ddot && r_gpu.matvec == r_ref.matvec;
+    std::printf("{\"case\": \"stencil40_newton3\", \"ok\": %s, \"iters\": [%d, %d], "
+                "\"x_rel_diff\": %.3e, \"newton4_bitwise\": %s}\n",
+                ok ? "true" : "false", r_ref.iters, r_gpu.iters, rel, bitwise ? "true" : "false");
+    bad += ok ? 0 : 1;
+  }
+  // error path: an unknown preconditioner type is rejected like a bad argument
+  struct Half : Preconditioner {
+    void apply(const LinearOperator&, const Vector& r, Vector& z) override { z = 0.5 * r; }
+    int degree() const override { return 0; }
+  } half;
   try {
     auto [scaled, d] = jacobi_scale(st40);
-    NewtonPreconditioner np(newton_params(0.1, 1.9, 2, 1.0));
-    polycg::gpu::pcg_solve(scaled, Vector::Ones(scaled.size()), {}, &np);
+    polycg::gpu::pcg_solve(scaled, Vector::Ones(scaled.size()), {}, &half);
     bad += 1;
   } catch (const std::invalid_argument&) {
-    std::printf("{\"case\": \"reject_newton\", \"ok\": true}\n");
+    std::printf("{\"case\": \"reject_custom_prec\", \"ok\": true}\n");
   }
   return bad == 0 ? 0 : 1;
 }

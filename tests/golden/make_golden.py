@@ -195,6 +195,23 @@ def main():
     rec_solve("csr300_m7", "csr", 0, 7, 1.01, csr=(rp, ci, va), bounds=(0.05, 1.9))
     out["pcg_solve"] = solves
 
+    # ---- pcg_solve with NewtonPreconditioner (pcg.hpp:27-40) ---------------------------------
+    nsolves = []
+    for tag, kind, nx, nlev, scale, csr, bounds in [
+            ("lap24_n3", "lap3d", 24, 3, 1.001, None, None),
+            ("lap24_n5", "lap3d", 24, 5, 1.001, None, None),
+            ("lap24_n0", "lap3d", 24, 0, 1.0, None, None),
+            ("csr300_n3", "csr", 0, 3, 1.01, (rp, ci, va), (0.05, 1.9))]:
+        a, b = bounds if bounds else R.analytic_extremes(3, nx)
+        x, bvec, rep = R.pcg_solve_newton(kind, a, b, nlev, scale, nx=nx, csr=csr, seed=SEED)
+        nsolves.append({"tag": tag, "kind": kind, "nx": nx, "nlev": nlev, "scale": hx(scale),
+                        "alpha": hx(a), "beta": hx(b),
+                        "report": {k: (hx(v) if isinstance(v, float) else v) for k, v in rep.items()
+                                   if k != "wall_time"},
+                        "x_sha256": h(x), "b_sha256": h(bvec)})
+        print(tag, rep["iters"], rep["ddot"], rep["matvec"], rep["rel_res"], file=sys.stderr)
+    out["pcg_solve_newton"] = nsolves
+
     # ---- Table 1 (spectrum.cpp:59-88) ------------------------------------
     t1 = {}
     for sol in ("ones", "random"):

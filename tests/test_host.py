@@ -87,6 +87,64 @@ def test_optimality(pcgx):
             assert gm == pytest.approx(exp, rel=1e-10)
 
 
+def test_newton_params_bitwise(pcgx, golden):
+    for c in golden["newton_params"]:
+        p = pcgx.newton_params(fh(c["alpha"]), fh(c["beta"]), c["nlev"], fh(c["scale"]))
+        assert np.array_equal(p.zeta, fhs(c["zeta"]))
+        assert p.degree() == 2 ** c["nlev"] - 1
+
+
+def test_newton_params_hand_values_and_errors(pcgx):
+    # test_polyprec.cpp:19-36, 55-60
+    p = pcgx.newton_params(1.0, 1.0, 4, 1.0)
+    assert p.zeta == pytest.approx([1.0] * 5, rel=1e-15)
+    p = pcgx.newton_params(1.0, 3.0, 2, 1.0)
+    assert p.zeta == pytest.approx([0.5, 8.0 / 7.0, 98.0 / 97.0], rel=1e-15)
+    p = pcgx.newton_params(7.9064e-4, 1.99921, 1, 1.0)
+    assert p.zeta[1] == pytest.approx(1.99684, rel=1e-5)
+    for args, msg in [((0.0, 1.0, 1, 1.0), "newton_params: need 0 < alpha0 <= beta0"),
+                      ((-1.0, 1.0, 1, 1.0), "newton_params: need 0 < alpha0 <= beta0"),
+                      ((1.0, 2.0, -1, 1.0), "newton_params: nlev must be >= 0"),
+                      ((1.0, 2.0, 1, 0.5), "newton_params: scale must be >= 1")]:
+        with pytest.raises(pcgx.InvalidArgument) as ei:
+            pcgx.newton_params(*args)
+        assert str(ei.value) == msg
+
+
+def test_newton_eval_and_forms_agree(pcgx):
+    # test_polyprec.cpp:38-43, 155-170: eval at the fixed point; the scalar forms agree
+    for nlev in (0, 2, 5):
+        assert pcgx.eval_poly(pcgx.newton_params(1.0, 1.0, nlev, 1.0), 1.0) == pytest.approx(1.0, rel=1e-15)
+    for s in (1.0, 1.01):
+        for nlev in (0, 1, 3, 6):
+            pn = pcgx.newton_params(0.01, 1.99, nlev, s)
+            pc = pcgx.cheb_params(0.01, 1.99, pn.degree(), s)
+            for g in range(101):
+                lam = 0.01 + (1.99 - 0.01) * g / 100.0
+                assert pcgx.eval_poly(pn, lam) == pytest.approx(pcgx.eval_poly(pc, lam), rel=1e-12)
+    # the scalar mirror of the recursion (polyprec.cpp:81-87), restated
+    p = pcgx.newton_params(0.02, 1.95, 4, 1.001)
+    for lam in (0.02, 0.5, 1.3, 1.95):
+        r = p.zeta[0]
+        for j in range(1, 5):
+            r = p.zeta[j] * (2.0 * r - lam * r * r)
+        assert pcgx.eval_poly(p, lam) == r
+
+
+def test_chi_sequence(pcgx):
+    # test_polyprec.cpp:308-321, and chi == zeta[1:] of newton_params at scale 1
+    chi = pcgx.chi_sequence(1.0, 3.0, 2)
+    assert chi == pytest.approx([8.0 / 7.0, 98.0 / 97.0], rel=1e-15)
+    tight = pcgx.chi_sequence(1.0, 1.0 + 1e-9, 30)
+    assert len(tight) == 30 and all(abs(c - 1.0) <= 1e-15 for c in tight[5:])
+    z = pcgx.newton_params(0.01, 1.99, 6, 1.0).zeta
+    assert pcgx.chi_sequence(0.01, 1.99, 6) == pytest.approx(z[1:], rel=1e-12)
+    with pytest.raises(pcgx.InvalidArgument):
+        pcgx.chi_sequence(1.0, 1.0, 1)
+    with pytest.raises(pcgx.InvalidArgument):
+        pcgx.chi_sequence(1.0, 2.0, 31)
+
+
 def test_analytic_extremes_bitwise(pcgx, golden):
     for c in golden["analytic_extremes"]:
         lo, hi = pcgx.analytic_extremes(c["dim"], c["nx"])

@@ -248,3 +248,26 @@ def test_power_dacg_bitwise_vs_reference(oracle, golden):
         assert dg["value"] == fh(c["dacg"]["value"]), c["tag"]
         assert (dg["iters"], dg["matvecs"], dg["converged"]) == (
             c["dacg"]["iters"], c["dacg"]["matvecs"], c["dacg"]["converged"])
+
+
+@pytest.mark.parametrize("tag", ["lap24_n0", "lap24_n3", "lap24_n5", "csr300_n3"])
+def test_pcg_solve_newton_bitwise_vs_reference(oracle, golden, tag):
+    """pcg_solve with NewtonPreconditioner (pcg.hpp:27-40): counters, residuals, x."""
+    c = next(s for s in golden["pcg_solve_newton"] if s["tag"] == tag)
+    if c["kind"] == "csr":
+        g = golden["csr_apply"]
+        op = OracleOp("csr", row_ptr=g["row_ptr"], col_idx=g["col_idx"], values=fhs(g["values"]))
+        n = len(g["row_ptr"]) - 1
+    else:
+        op = OracleOp("lap3d", nx=c["nx"])
+        n = c["nx"] ** 3
+    b = oracle.apply(op, oracle.random_uniform(n, SEED))
+    assert sha(b) == c["b_sha256"]
+    z = oracle.newton_params(fh(c["alpha"]), fh(c["beta"]), c["nlev"], fh(c["scale"]))
+    x, rep = oracle.pcg_solve_newton(op, z, b)
+    g = c["report"]
+    for k in ("iters", "ddot", "matvec", "prec_applies", "converged"):
+        assert rep[k] == g[k], k
+    assert rep["rel_res"] == fh(g["rel_res"])
+    assert rep["true_rel_res"] == fh(g["true_rel_res"])
+    assert sha(x) == c["x_sha256"]
