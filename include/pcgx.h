@@ -53,7 +53,8 @@ typedef enum {
   PCGX_ERR_CUDA = 3,        /* CUDA runtime failure (no device, OOM, fault) */
   PCGX_ERR_NCCL = 4,        /* communicator failure */
   PCGX_ERR_OVERFLOW = 5,    /* index does not fit the int32 device CSR */
-  PCGX_ERR_UNSUPPORTED = 6  /* valid reference input this build does not accelerate */
+  PCGX_ERR_UNSUPPORTED = 6, /* valid reference input this build does not accelerate */
+  PCGX_ERR_PARSE = 7        /* polycg::ParseError (MatrixMarket input), message has file:line */
 } pcgx_status;
 
 typedef struct pcgx_context_s* pcgx_context;
@@ -247,6 +248,34 @@ pcgx_status pcgx_pcg_solve_newton(pcgx_context ctx, pcgx_operator op, const pcgx
 pcgx_status pcgx_pcg_solve_newton_device(pcgx_context ctx, pcgx_operator op,
                                          const pcgx_newton* prec, const double* b, double* x,
                                          const pcgx_solve_opts* opts, pcgx_report* rep);
+
+/* ------------------------------------------------------- MatrixMarket files */
+
+/* Host CSR arrays (int64, as CsrMatrix stores them, linop.hpp:72-74), owned by
+ * the library: release with pcgx_csr_host_free. */
+typedef struct {
+  int64_t n, nnz;
+  int64_t* row_ptr; /* n+1 */
+  int64_t* col_idx; /* nnz */
+  double* values;   /* nnz */
+} pcgx_csr_host;
+
+/* load_matrix_market(path) (matrix_market.cpp:55-59, 61-166): coordinate real,
+ * symmetric (lower triangle) or general with symmetric content, 1-based; the
+ * symmetrised CSR with both triangles. Errors: PCGX_ERR_PARSE with the
+ * reference's "name:line: what" message. Multithreaded parse. */
+pcgx_status pcgx_mm_load(const char* path, pcgx_csr_host* out);
+/* load_matrix_market(istream, name): the same from an in-memory text. */
+pcgx_status pcgx_mm_load_text(const char* text, size_t len, const char* name, pcgx_csr_host* out);
+void pcgx_csr_host_free(pcgx_csr_host* m);
+/* save_matrix_market (matrix_market.cpp:172-199): lower triangle, "%.16e" values,
+ * byte-identical to the reference's output; load(save(m)) == m. */
+pcgx_status pcgx_mm_save(const char* path, int64_t n, const int64_t* row_ptr,
+                         const int64_t* col_idx, const double* values);
+/* ... into a library-owned text buffer (release with pcgx_free_text). */
+pcgx_status pcgx_mm_save_text(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                              const double* values, char** text, size_t* len);
+void pcgx_free_text(char* text);
 
 /* ------------------------------------------------------- inputs and bounds */
 

@@ -49,7 +49,13 @@ class NumericalError(OracleError):
     pass
 
 
+class ParseError(OracleError):
+    pass
+
+
 def _raise(code, msg):
+    if code == 7:
+        raise ParseError(code, msg)
     if code == 1:
         raise InvalidArgument(code, msg)
     if code == 2:
@@ -291,6 +297,12 @@ class RefLib:
                                     C.c_double, C.c_int, C.c_double, _dp, C.c_uint64, C.c_double,
                                     C.c_int, _dp, _dp, C.POINTER(Report)]
         L.ref_pcg_solve_newton.argtypes = L.ref_pcg_solve.argtypes
+        L.ref_mm_load_text.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, _i64p, _i64p]
+        L.ref_mm_load_file.argtypes = [C.c_char_p, _i64p, _i64p]
+        L.ref_mm_fetch.argtypes = [_i64p, _i64p, _dp]
+        L.ref_mm_fetch.restype = None
+        L.ref_mm_save_text.argtypes = [C.c_int64, _i64p, _i64p, _dp, C.POINTER(C.c_char_p),
+                                       _i64p]
         L.ref_spectrum_table.argtypes = [C.c_int64, C.POINTER(C.c_int), C.c_int, C.c_double,
                                          C.c_int, C.c_uint64, _dp]
         L.ref_set_threads.argtypes = [C.c_int]
@@ -400,6 +412,31 @@ class RefLib:
                                               nlev, scale, _ptr(bp), seed, tol, maxit, _ptr(x),
                                               _ptr(b_out), C.byref(rep)))
         return x, (b_out if b is None else bp), rep.as_dict()
+
+    def mm_load(self, source, name=None):
+        """load_matrix_market: text (with name) or a path -> (n, row_ptr, col_idx, values)."""
+        n, nnz = C.c_int64(), C.c_int64()
+        if name is not None:
+            data = source.encode() if isinstance(source, str) else source
+            self._chk(self.L.ref_mm_load_text(data, len(data), name.encode(), C.byref(n),
+                                              C.byref(nnz)))
+        else:
+            self._chk(self.L.ref_mm_load_file(os.fsencode(source), C.byref(n), C.byref(nnz)))
+        rp = np.empty(n.value + 1, dtype=np.int64)
+        ci = np.empty(nnz.value, dtype=np.int64)
+        va = np.empty(nnz.value)
+        self.L.ref_mm_fetch(rp.ctypes.data_as(_i64p), ci.ctypes.data_as(_i64p), _ptr(va))
+        return n.value, rp, ci, va
+
+    def mm_save(self, n, rp, ci, va):
+        """save_matrix_market(CsrMatrix(n, rp, ci, va), ostream) -> text."""
+        rp = np.ascontiguousarray(rp, dtype=np.int64)
+        ci = np.ascontiguousarray(ci, dtype=np.int64)
+        va = np.ascontiguousarray(va, dtype=np.float64)
+        t, ln = C.c_char_p(), C.c_int64()
+        self._chk(self.L.ref_mm_save_text(n, rp.ctypes.data_as(_i64p), ci.ctypes.data_as(_i64p),
+                                          _ptr(va), C.byref(t), C.byref(ln)))
+        return C.string_at(t, ln.value).decode()
 
     def _eig(self, fn, kind, tol, maxit, seed, nx=0, csr=None):
         n, rp, ci, va, keep = self._csr(csr)

@@ -27,6 +27,7 @@
 
 #include "polycg/eigenest.hpp"
 #include "polycg/linop.hpp"
+#include "polycg/matrix_market.hpp"
 #include "polycg/pcg.hpp"
 #include "polycg/polyprec.hpp"
 #include "polycg/spectrum.hpp"
@@ -35,6 +36,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -53,6 +55,9 @@ int guarded(F&& f) {
   } catch (const NumericalError& e) {
     g_err = e.what();
     return 2;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    return 7;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return 1;
@@ -102,6 +107,48 @@ Vector to_vec(const double* p, std::int64_t n) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// load_matrix_market(istream, name) (matrix_market.cpp:61-166) / (path) (:55-59):
+// sizes now, arrays by ref_mm_fetch (the matrix is kept per thread in between).
+thread_local std::unique_ptr<CsrMatrix> g_mm;
+int ref_mm_load_text(const char* text, std::int64_t len, const char* name, std::int64_t* n,
+                     std::int64_t* nnz) {
+  return guarded([&] {
+    std::istringstream in(std::string(text, static_cast<std::size_t>(len)));
+    g_mm = std::make_unique<CsrMatrix>(load_matrix_market(in, name));
+    *n = g_mm->size();
+    *nnz = g_mm->nnz();
+  });
+}
+int ref_mm_load_file(const char* path, std::int64_t* n, std::int64_t* nnz) {
+  return guarded([&] {
+    g_mm = std::make_unique<CsrMatrix>(load_matrix_market(std::string(path)));
+    *n = g_mm->size();
+    *nnz = g_mm->nnz();
+  });
+}
+void ref_mm_fetch(std::int64_t* rp, std::int64_t* ci, double* va) {
+  std::memcpy(rp, g_mm->row_ptr().data(), sizeof(std::int64_t) * g_mm->row_ptr().size());
+  std::memcpy(ci, g_mm->col_idx().data(), sizeof(std::int64_t) * g_mm->col_idx().size());
+  std::memcpy(va, g_mm->values().data(), sizeof(double) * g_mm->values().size());
+  g_mm.reset();
+}
+// save_matrix_market(m, ostream) (matrix_market.cpp:178-199); the text stays valid
+// until the next call on this thread.
+thread_local std::string g_mm_text;
+int ref_mm_save_text(std::int64_t n, const std::int64_t* rp, const std::int64_t* ci,
+                     const double* va, const char** text, std::int64_t* len) {
+  return guarded([&] {
+    const std::int64_t nnz = rp[n];
+    CsrMatrix m(n, std::vector<Index>(rp, rp + n + 1), std::vector<Index>(ci, ci + nnz),
+                std::vector<double>(va, va + nnz));
+    std::ostringstream out;
+    save_matrix_market(m, out);
+    g_mm_text = out.str();
+    *text = g_mm_text.c_str();
+    *len = static_cast<std::int64_t>(g_mm_text.size());
+  });
+}
 
 void ref_set_threads(int t) { set_apply_threads(t); }
 int ref_get_threads() { return apply_threads(); }

@@ -13,5 +13,5 @@ from .pcgx import (  # noqa: F401
     FLAG_NO_GRAPH, FLAG_TIME_KERNELS, cheb_params, eval_poly, gen_elast27, gen_fe27, jacobi_scale, lanczos_bounds, lib,
     pcg_solve, random_uniform_vector, slab_partition, EigOptions, EigResult, power_method,
     dacg_smallest, estimate_bounds, NewtonParams, NewtonPreconditioner, apply_newton,
-    newton_params, chi_sequence,
+    newton_params, chi_sequence, ParseError, load_matrix_market, save_matrix_market,
 )

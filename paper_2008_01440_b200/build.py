@@ -23,7 +23,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpcgx.so")
-SOURCES = ["pcgx.cu", "host_math.cpp", "gen.cpp"]
+SOURCES = ["pcgx.cu", "host_math.cpp", "gen.cpp", "mm.cpp"]
 HEADERS = ["common.cuh", "kernels.cuh", "cheb2.cuh", "host_math.hpp"]
 
 

@@ -2392,6 +2392,82 @@ pcgx_status pcgx_newton_apply(pcgx_context c, pcgx_operator op, const pcgx_newto
   });
 }
 
+pcgx_status pcgx_mm_load(const char* path, pcgx_csr_host* out) {
+  if (!path || !out) {
+    g_thread_err = "load_matrix_market: null argument";
+    return PCGX_ERR_INVALID;
+  }
+  std::string msg;
+  const int st = pcgx::mm_load(path, out, &msg);
+  if (st) g_thread_err = msg;
+  return (pcgx_status)st;
+}
+
+pcgx_status pcgx_mm_load_text(const char* text, size_t len, const char* name, pcgx_csr_host* out) {
+  if ((!text && len) || !out) {
+    g_thread_err = "load_matrix_market: null argument";
+    return PCGX_ERR_INVALID;
+  }
+  std::string msg;
+  const int st = pcgx::mm_load_text(text, len, name, out, &msg);
+  if (st) g_thread_err = msg;
+  return (pcgx_status)st;
+}
+
+void pcgx_csr_host_free(pcgx_csr_host* m) {
+  if (!m) return;
+  std::free(m->row_ptr);
+  std::free(m->col_idx);
+  std::free(m->values);
+  m->row_ptr = m->col_idx = nullptr;
+  m->values = nullptr;
+  m->n = m->nnz = 0;
+}
+
+pcgx_status pcgx_mm_save_text(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+                              char** text, size_t* len) {
+  if (n < 0 || !rp || !text || !len) {
+    g_thread_err = "save_matrix_market: invalid argument";
+    return PCGX_ERR_INVALID;
+  }
+  std::string s;
+  pcgx::mm_save_text(n, rp, ci, va, &s);
+  char* buf = (char*)std::malloc(s.size() + 1);
+  if (!buf) {
+    g_thread_err = "save_matrix_market: out of memory";
+    return PCGX_ERR_INVALID;
+  }
+  std::memcpy(buf, s.data(), s.size());
+  buf[s.size()] = '\0';
+  *text = buf;
+  *len = s.size();
+  return PCGX_OK;
+}
+
+void pcgx_free_text(char* text) { std::free(text); }
+
+pcgx_status pcgx_mm_save(const char* path, int64_t n, const int64_t* rp, const int64_t* ci,
+                         const double* va) {
+  if (!path || n < 0 || !rp) {
+    g_thread_err = "save_matrix_market: invalid argument";
+    return PCGX_ERR_INVALID;
+  }
+  std::string s;
+  pcgx::mm_save_text(n, rp, ci, va, &s);
+  FILE* f = std::fopen(path, "wb");
+  if (!f) {
+    g_thread_err = std::string(path) + ": cannot open file for writing";
+    return PCGX_ERR_PARSE;
+  }
+  const size_t w = std::fwrite(s.data(), 1, s.size(), f);
+  std::fclose(f);
+  if (w != s.size()) {
+    g_thread_err = std::string(path) + ": write failed";
+    return PCGX_ERR_PARSE;
+  }
+  return PCGX_OK;
+}
+
 void pcgx_solve_opts_default(pcgx_solve_opts* o) {
   o->tol = 1e-8;
   o->maxit = 20000;

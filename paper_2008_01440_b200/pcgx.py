@@ -21,8 +21,10 @@ SolveOptions / SolveReport        ``SolveOptions`` / ``SolveReport``
 pcg_solve(op, b, opts, prec)      ``pcg_solve(op, b, opts, prec)``
 random_uniform_vector(n, seed)    ``random_uniform_vector(n, seed)``
 analytic_extremes(kind, nx, s)    ``analytic_extremes(dim, nx, scaled)``
+load/save_matrix_market           ``load_matrix_market`` / ``save_matrix_market``
 std::invalid_argument             ``InvalidArgument`` (a ``ValueError``)
 polycg::NumericalError            ``NumericalError``
+polycg::ParseError                ``ParseError``
 ================================  =============================================
 
 Every compute call runs the sm_100a kernels in ``libpcgx.so``; there is no CPU
@@ -76,8 +78,18 @@ class Unsupported(PcgxError):
     status = 6
 
 
+class ParseError(PcgxError):
+    """polycg::ParseError (types.hpp:16-21): unparsable input, message has file:line."""
+    status = 7
+
+
 _ERRS = {1: InvalidArgument, 2: NumericalError, 3: CudaError, 4: NcclError, 5: OverflowError_,
-         6: Unsupported}
+         6: Unsupported, 7: ParseError}
+
+
+class _CsrHost(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("row_ptr", C.POINTER(C.c_int64)),
+                ("col_idx", C.POINTER(C.c_int64)), ("values", C.POINTER(C.c_double))]
 
 
 class _Cheb(C.Structure):
@@ -125,7 +137,8 @@ SYMBOLS = [
     "pcgx_gen_fe27_size", "pcgx_gen_fe27_fill", "pcgx_gen_elast27_size",
     "pcgx_gen_elast27_fill", "pcgx_newton_params", "pcgx_newton_eval", "pcgx_chi_sequence",
     "pcgx_newton_apply", "pcgx_newton_apply_device", "pcgx_pcg_solve_newton",
-    "pcgx_pcg_solve_newton_device",
+    "pcgx_pcg_solve_newton_device", "pcgx_mm_load", "pcgx_mm_load_text", "pcgx_csr_host_free",
+    "pcgx_mm_save", "pcgx_mm_save_text", "pcgx_free_text",
 ]
 
 _lib = None
@@ -204,6 +217,13 @@ def lib():
         "pcgx_pcg_solve_newton_device": (C.c_int, [ctx, op, C.POINTER(_Newton), C.c_void_p,
                                                    C.c_void_p, C.POINTER(_Opts),
                                                    C.POINTER(_Report)]),
+        "pcgx_mm_load": (C.c_int, [C.c_char_p, C.POINTER(_CsrHost)]),
+        "pcgx_mm_load_text": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.POINTER(_CsrHost)]),
+        "pcgx_csr_host_free": (None, [C.POINTER(_CsrHost)]),
+        "pcgx_mm_save": (C.c_int, [C.c_char_p, C.c_int64, _i64p, _i64p, _dp]),
+        "pcgx_mm_save_text": (C.c_int, [C.c_int64, _i64p, _i64p, _dp, C.POINTER(C.c_void_p),
+                                        C.POINTER(C.c_size_t)]),
+        "pcgx_free_text": (None, [C.c_void_p]),
         "pcgx_solve_opts_default": (None, [C.POINTER(_Opts)]),
         "pcgx_pcg_solve": (C.c_int, [ctx, op, C.POINTER(_Cheb), _dp, _dp, C.POINTER(_Opts),
                                      C.POINTER(_Report)]),
@@ -421,6 +441,54 @@ class CsrMatrix:
         m = self.col_idx == rows
         d[rows[m]] = self.values[m]
         return d
+
+
+def _csr_from_host(h: _CsrHost) -> CsrMatrix:
+    n, nnz = int(h.n), int(h.nnz)
+    rp = np.ctypeslib.as_array(h.row_ptr, shape=(n + 1,)).copy()
+    ci = np.ctypeslib.as_array(h.col_idx, shape=(max(nnz, 1),))[:nnz].copy()
+    va = np.ctypeslib.as_array(h.values, shape=(max(nnz, 1),))[:nnz].copy()
+    return CsrMatrix(n, rp, ci, va)
+
+
+def load_matrix_market(source, name: str | None = None) -> CsrMatrix:
+    """load_matrix_market (matrix_market.cpp:55-166): a path, or (bytes/str) text with
+    ``name`` used in messages like the reference's istream overload. Raises ParseError."""
+    L = lib()
+    h = _CsrHost()
+    if isinstance(source, (bytes, str)) and name is not None:
+        data = source.encode() if isinstance(source, str) else source
+        st = L.pcgx_mm_load_text(data, len(data), name.encode(), C.byref(h))
+    else:
+        st = L.pcgx_mm_load(os.fsencode(source), C.byref(h))
+    try:
+        _check(st, None)
+        return _csr_from_host(h)
+    finally:
+        L.pcgx_csr_host_free(C.byref(h))
+
+
+def _csr_arrays(m: CsrMatrix):
+    rp = np.ascontiguousarray(m.row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(m.col_idx, dtype=np.int64)
+    va = np.ascontiguousarray(m.values, dtype=np.float64)
+    return rp, ci, va
+
+
+def save_matrix_market(m: CsrMatrix, path=None):
+    """save_matrix_market (matrix_market.cpp:172-199). path None: return the text."""
+    L = lib()
+    rp, ci, va = _csr_arrays(m)
+    args = (int(m.n), rp.ctypes.data_as(_i64p), ci.ctypes.data_as(_i64p), _ptr(va))
+    if path is not None:
+        _check(L.pcgx_mm_save(os.fsencode(path), *args), None)
+        return None
+    buf, ln = C.c_void_p(), C.c_size_t()
+    _check(L.pcgx_mm_save_text(*args, C.byref(buf), C.byref(ln)), None)
+    try:
+        return C.string_at(buf, ln.value).decode()
+    finally:
+        L.pcgx_free_text(buf)
 
 
 class ScaledOperator:

@@ -21,7 +21,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
 
-from oracle.oracle import RefLib, NumericalError, InvalidArgument  # noqa: E402
+from oracle.oracle import RefLib, NumericalError, InvalidArgument, OracleError  # noqa: E402
 
 SEED = 20240801
 
@@ -234,6 +234,21 @@ def main():
                     "dacg": {"tol": dtol, "maxit": dmax, "value": hx(dg["value"]), "iters": dg["iters"],
                              "matvecs": dg["matvecs"], "converged": dg["converged"]}})
     out["eigen_estimators"] = eig
+
+    # ---- load_matrix_market / save_matrix_market (matrix_market.cpp:55-199) ------------------
+    from tests.golden.mm_cases import cases as mm_cases  # noqa: E402
+    mm = {}
+    for name, text in mm_cases().items():
+        try:
+            n, rp, ci, va = R.mm_load(text, "<" + name + ">")
+        except OracleError as e:
+            mm[name] = {"error": str(e)}
+            continue
+        saved = R.mm_save(n, rp, ci, va)
+        mm[name] = {"n": int(n), "nnz": int(len(va)), "row_ptr": hashlib.sha256(rp.astype("<i8").tobytes()).hexdigest(),
+                    "col_idx": hashlib.sha256(ci.astype("<i8").tobytes()).hexdigest(), "values": h(va),
+                    "save_sha256": hashlib.sha256(saved.encode()).hexdigest()}
+    out["matrix_market"] = mm
 
     with open(os.path.join(HERE, "reference_golden.json"), "w") as f:
         json.dump(out, f, indent=1)

@@ -497,3 +497,25 @@ def test_dacg_rejects_indefinite(P, ctx):
     op = csr(P, ctx, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([1.0, 2.0, 2.0, 1.0]))
     with pytest.raises(P.NumericalError, match="dacg_smallest"):
         P.dacg_smallest(op)
+
+
+# ------------------------------------------------------------------ MatrixMarket -> device CSR
+
+def test_matrix_market_ingest_solve(P, ctx, oracle, tmp_path):
+    """A .mtx file through the native loader straight into the int32 device CSR,
+    then Chebyshev-PCG: the same solve as the oracle on the loaded arrays."""
+    A = P.gen_fe27(12, sigma=1.0, seed=SEED)
+    m = P.CsrMatrix(A.n, A.row_ptr.astype(np.int64), A.col_idx.astype(np.int64), A.values)
+    path = tmp_path / "fe27_12.mtx"
+    P.save_matrix_market(m, str(path))
+    L = P.load_matrix_market(str(path))
+    assert np.array_equal(L.values, m.values) and np.array_equal(L.col_idx, m.col_idx)
+    op = csr(P, ctx, L.row_ptr, L.col_idx, L.values)
+    opo = OracleOp("csr", row_ptr=L.row_ptr, col_idx=L.col_idx, values=L.values)
+    lo, hi = P.lanczos_bounds(op, 20, 30, SEED)
+    rhs = op.apply(P.random_uniform_vector(L.n, SEED))
+    x, rep = P.pcg_solve(op, rhs, None, P.ChebyshevPreconditioner(P.cheb_params(lo, hi, 20, 1.001)))
+    xo, ro = oracle.pcg_solve(opo, oracle.cheb_params(lo, hi, 20, 1.001), rhs)
+    assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
+    if rep.iters == ro["iters"]:
+        assert rel_norm(x, xo) <= 1e-10
