@@ -346,6 +346,21 @@ def run_gpu(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.config == "cfg2":
         cpu = cpu_baseline_sample()
 
+    # working set of one pass: the operand vectors (x, y, r, x_old) plus the matrix
+    ws_bytes = 4 * 8 * n_loc + (0 if kind == "stencil" else 12 * op.nnz())
+    l2_note = (f"working set {ws_bytes / 1e6:.0f} MB per GPU > L2 (126 MB); no flush" if ws_bytes > 126e6
+               else f"working set {ws_bytes / 1e6:.0f} MB fits L2 (126 MB): L2-bound, not an HBM roofline claim")
+    storage = op.storage()
+    kdesc = {
+        "stencil": ("stencil7_cheb2_kernel (TMA, two fused SpMV + Chebyshev steps per pass, 40 B/unknown)"
+                    if step_bytes == 40.0 * n_loc else
+                    "stencil7v2_kernel<EpiChebStep> (fused SpMV + Chebyshev step, 32 B/unknown)"),
+        "sell32": "sell_kernel<EpiChebStep> (SELL-32 int32 CSR SpMV + Chebyshev step, 12 nnz + 4(n+1) + 40 n bytes)",
+        "bsr3": "bsr3_kernel<EpiChebStep> (3x3-block SELL-32 SpMV + Chebyshev step, 8 nnz + 4 nnz/9 + 4(n/3+1) + 40 n bytes)",
+        "csr_tiles": "csr2_kernel<EpiChebStep> (TMA row tiles, 12 nnz + 4(n+1) + 40 n bytes)",
+        "csr_chunked": "csr_kernel<EpiChebStep> (chunked CSR, 12 nnz + 4(n+1) + 40 n bytes)",
+    }[storage]
+
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 3),
@@ -357,17 +372,13 @@ def run_gpu(args):
                    "parallelism": (f"z-slab x{ws}" if kind == "stencil" else f"block rows x{ws}"),
                    "setup_s": round(t_setup, 2),
                    "spmv_equiv_bytes": spmv_bytes,
-                   "l2": ("inputs larger than L2 (126 MB); no flush" if 8 * n_glob > 126e6 else
-                          "vectors L2-resident (8 MB at 100^3): L2-bound, not an HBM roofline claim")},
+                   "storage": op.storage(),
+                   "l2": l2_note},
         "per_k": per_k,
         "time_to_1e8_s": {str(k): round(t, 6) for k, _, t in reps},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": ("csr_kernel<EpiChebStep> (fused int32 CSR SpMV + Chebyshev step, "
-                                "12 nnz + 4(n+1) + 40 n bytes)" if kind != "stencil" else
-                                "stencil7_cheb2_kernel (TMA, two fused SpMV + Chebyshev steps "
-                                "per pass, 40 B/unknown)" if step_bytes == 40.0 * n_loc else
-                                "stencil7v2_kernel<EpiChebStep> (fused SpMV + Chebyshev step, 32 B/unknown)"),
+                     "kernel": kdesc,
                      "bytes_per_launch": step_bytes, "avg_launch_ms": round(step_ms, 5),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
                      "frac_of_8TBs_spec": round(achieved / 8000.0, 4)},

@@ -881,6 +881,96 @@ sell_kernel(SellGeom g, In in, Epi epi, Reduce red) {
   if (kRed) block_reduce_finish(acc, red);
 }
 
+// ----------------------------------------------------------------- 3x3 block CSR
+// A CSR matrix whose rows come in aligned triples with a shared pattern of full
+// 3x3 blocks (3 dof per node: the elasticity family, cfg4) is stored as BSR-3 in
+// the SELL-32 arrangement over BLOCK rows: per slice of 32 block rows, step k
+// holds one block column index per lane (128 B) and the 9 block values as nine
+// coalesced 256-byte rows (q = 3c + d, val[(slot0 + 32k) * 9 + 32 q + lane]).
+// Matrix bytes per nnz: 8 + 4/9 (vs 12 for the int32 CSR). One thread owns a
+// block row = three CSR rows with three sums; each sum takes its terms in the
+// CSR row's column order (blocks ascending, d = 0..2), v * (d_c * x_c), so every
+// row is bitwise the scalar CSR kernel's (linop.cpp:171-187, 271-275).
+struct Bsr3Geom {
+  int nb;                      // block rows (n / 3)
+  int s_begin, s_end;          // slices of this launch
+  const long long* slice_ptr;  // nslices + 1 (blocks; multiples of 32)
+  const int* blen;             // nb: blocks per block row
+  const int* bcol;             // padded: block column J (column 3J .. 3J+2)
+  const double* val;           // padded: 9 per block (see above)
+  const double* dvec;
+};
+
+#ifndef PCGX_BSR_BATCH
+#define PCGX_BSR_BATCH 1
+#endif
+constexpr int kBsrBatch = PCGX_BSR_BATCH;
+
+template <class In, class Epi, bool kRed>
+__global__ void __launch_bounds__(256, 4)
+bsr3_kernel(Bsr3Geom g, In in, Epi epi, Reduce red) {
+  in.init();
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  double acc = 0.0;
+  for (int s = g.s_begin + blockIdx.x * wpb + (threadIdx.x >> 5); s < g.s_end; s += gridDim.x * wpb) {
+    const int br = s * 32 + lane;
+    const long long base = __ldg(g.slice_ptr + s);
+    const int L = (int)((__ldg(g.slice_ptr + s + 1) - base) >> 5);
+    const bool live = br < g.nb;
+    const int len = live ? __ldg(g.blen + br) : 0;
+    const long long r0 = 3LL * br;
+    double ev[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    double xr[3] = {0.0, 0.0, 0.0}, dr[3] = {0.0, 0.0, 0.0};
+    if (live) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        epi.ld(r0 + c, ev[c]);
+        xr[c] = in.ld1(r0 + c);
+        dr[c] = __ldg(g.dvec + r0 + c);
+      }
+    }
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < L; k += kBsrBatch) {
+      double v[kBsrBatch][9], t[kBsrBatch][3];
+#pragma unroll
+      for (int q = 0; q < kBsrBatch; ++q) {
+        const bool on = (k + q) < len;
+        const long long slot = base + 32LL * (k + q);
+        const int J = on ? __ldg(g.bcol + slot + lane) : 0;
+        const double* vp = g.val + slot * 9 + lane;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) v[q][e] = on ? __ldg(vp + 32 * e) : 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const long long cidx = 3LL * J + d;
+          t[q][d] = on ? __ldg(g.dvec + cidx) * in.ldc(cidx) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kBsrBatch; ++q)
+        if (k + q < len) {
+          s0 = s0 + v[q][0] * t[q][0];
+          s0 = s0 + v[q][1] * t[q][1];
+          s0 = s0 + v[q][2] * t[q][2];
+          s1 = s1 + v[q][3] * t[q][0];
+          s1 = s1 + v[q][4] * t[q][1];
+          s1 = s1 + v[q][5] * t[q][2];
+          s2 = s2 + v[q][6] * t[q][0];
+          s2 = s2 + v[q][7] * t[q][1];
+          s2 = s2 + v[q][8] * t[q][2];
+        }
+    }
+    if (live) {
+      const double c0 = epi.st(r0, s0 * dr[0], xr[0], ev[0]);
+      const double c1 = epi.st(r0 + 1, s1 * dr[1], xr[1], ev[1]);
+      const double c2 = epi.st(r0 + 2, s2 * dr[2], xr[2], ev[2]);
+      if (kRed) acc = acc + ((c0 + c1) + c2);
+    }
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
 // ----------------------------------------------------------------- vector kernels
 // Grid-stride over a fixed grid (deterministic element -> thread map).
 

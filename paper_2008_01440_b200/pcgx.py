@@ -128,7 +128,7 @@ SYMBOLS = [
     "pcgx_host_alloc", "pcgx_host_free", "pcgx_timer_start", "pcgx_timer_stop",
     "pcgx_flush_l2", "pcgx_stencil7_create", "pcgx_slab_partition", "pcgx_csr_create", "pcgx_csr_create_i32",
     "pcgx_operator_destroy", "pcgx_operator_size", "pcgx_operator_local_size",
-    "pcgx_operator_z0", "pcgx_operator_row0", "pcgx_operator_nnz", "pcgx_operator_matvec_count",
+    "pcgx_operator_z0", "pcgx_operator_row0", "pcgx_operator_nnz", "pcgx_operator_storage", "pcgx_operator_matvec_count",
     "pcgx_operator_apply", "pcgx_operator_apply_device", "pcgx_cheb_params", "pcgx_cheb_eval",
     "pcgx_cheb_apply", "pcgx_cheb_apply_device", "pcgx_solve_opts_default", "pcgx_pcg_solve",
     "pcgx_pcg_solve_device", "pcgx_random_uniform_device", "pcgx_random_uniform",
@@ -199,6 +199,7 @@ def lib():
         "pcgx_operator_z0": (C.c_int64, [op]),
         "pcgx_operator_row0": (C.c_int64, [op]),
         "pcgx_operator_nnz": (C.c_int64, [op]),
+        "pcgx_operator_storage": (C.c_int, [op]),
         "pcgx_operator_matvec_count": (C.c_uint64, [op]),
         "pcgx_operator_apply": (C.c_int, [ctx, op, _dp, _dp]),
         "pcgx_operator_apply_device": (C.c_int, [ctx, op, C.c_void_p, C.c_void_p]),
@@ -510,6 +511,12 @@ class ScaledOperator:
     def row0(self):
         """First global row owned by this rank (slab / block rows)."""
         return lib().pcgx_operator_row0(self.h)
+
+    STORAGE = {0: "stencil", 1: "sell32", 2: "bsr3", 3: "csr_tiles", 4: "csr_chunked"}
+
+    def storage(self) -> str:
+        """Device storage of the operator (pcgx_operator_storage)."""
+        return self.STORAGE[lib().pcgx_operator_storage(self.h)]
 
     def nnz(self):
         return lib().pcgx_operator_nnz(self.h)

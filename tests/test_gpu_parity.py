@@ -519,3 +519,51 @@ def test_matrix_market_ingest_solve(P, ctx, oracle, tmp_path):
     assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
     if rep.iters == ro["iters"]:
         assert rel_norm(x, xo) <= 1e-10
+
+
+# ------------------------------------------------------------------ 3x3-block storage (cfg4 family)
+
+@pytest.mark.parametrize("nx", [3, 8, 11])
+def test_bsr3_detected_and_bitwise(P, ctx, oracle, nx, monkeypatch):
+    """The 3-dof elasticity matrices are stored as BSR-3 automatically; SpMV and
+    every Chebyshev step stay bitwise the reference's CSR row sums."""
+    A = P.gen_elast27(nx, 1.0, 0.5, 0.1, seed=SEED)
+    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op.storage() == "bsr3"
+    opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    x = oracle.random_uniform(A.n, 17)
+    assert np.array_equal(op.apply(x), oracle.apply(opo, x))
+    for m in (1, 2, 5):
+        prm = P.cheb_params(0.01, 2.9, m, 1.001)
+        assert np.array_equal(P.apply_chebyshev(prm, op, x),
+                              oracle.apply_chebyshev(opo, oracle.cheb_params(0.01, 2.9, m, 1.001), x))
+    monkeypatch.setenv("PCGX_BSR", "0")
+    op_s = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op_s.storage() == "sell32"
+    assert np.array_equal(op_s.apply(x), op.apply(x))
+
+
+def test_bsr3_solve_vs_oracle(P, ctx, oracle):
+    A = P.gen_elast27(10, 1.0, 0.5, 0.1, seed=SEED)
+    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op.storage() == "bsr3"
+    opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    lo, hi = P.lanczos_bounds(op, 20, 30, SEED)
+    rhs = op.apply(P.random_uniform_vector(A.n, SEED))
+    for prec in (P.ChebyshevPreconditioner(P.cheb_params(lo, hi, 30, 1.001)),
+                 P.NewtonPreconditioner(P.newton_params(lo, hi, 4, 1.001))):
+        x, rep = P.pcg_solve(op, rhs, P.SolveOptions(maxit=5000), prec)
+        if isinstance(prec, P.NewtonPreconditioner):
+            xo, ro = oracle.pcg_solve_newton(opo, prec.params().zeta, rhs, maxit=5000)
+        else:
+            xo, ro = oracle.pcg_solve(opo, oracle.cheb_params(lo, hi, 30, 1.001), rhs, maxit=5000)
+        assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
+        if rep.iters == ro["iters"]:
+            assert rel_norm(x, xo) <= 1e-10
+
+
+def test_non_block_matrices_keep_sell(P, ctx):
+    A = P.gen_fe27(9, sigma=1.0, seed=SEED)          # n = 729 = 3 * 243, scalar pattern
+    assert csr(P, ctx, A.row_ptr, A.col_idx, A.values).storage() == "sell32"
+    rp, ci, va = lap3d_csr(6)                          # n = 216, 7-point pattern
+    assert csr(P, ctx, rp, ci, va).storage() == "sell32"
