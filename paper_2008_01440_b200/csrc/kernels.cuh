@@ -971,6 +971,54 @@ bsr3_kernel(Bsr3Geom g, In in, Epi epi, Reduce red) {
   if (kRed) block_reduce_finish(acc, red);
 }
 
+// ----------------------------------------------------------------- diagonal (offset) storage
+// A CSR matrix whose column offsets (col - row) come from a small fixed set (K <= 32:
+// the 27-point FE stencils of cfg3, the assembled 7-point Laplacian) is stored by
+// offset: val[k * ld + i] = a(i, i + off[k]) (coalesced across rows) plus one
+// presence mask per row. No column indices: 8 B per stored entry + 4 B per row
+// (vs 12 B per nnz). Terms are taken in ascending offset = ascending column order,
+// only where the mask bit is set, v * (d_c * x_c): bitwise the CSR row sum.
+constexpr int kDiaMax = 32;
+
+struct DiaGeom {
+  int n, K;
+  long long ld;
+  int off[kDiaMax];
+  const double* val;
+  const unsigned* mask;
+  const double* dvec;
+};
+
+#ifndef PCGX_DIA_MINB
+#define PCGX_DIA_MINB 8
+#endif
+template <class In, class Epi, bool kRed>
+__global__ void __launch_bounds__(256, PCGX_DIA_MINB)
+dia_kernel(DiaGeom g, In in, Epi epi, Reduce red) {
+  in.init();
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double ev[2];
+    epi.ld(i, ev);
+    const double xr = in.ld1(i);
+    const double dr = __ldg(g.dvec + i);
+    const unsigned msk = __ldg(g.mask + i);
+    double sum = 0.0;
+#pragma unroll 9
+    for (int k = 0; k < g.K; ++k) {
+      if (msk & (1u << k)) {
+        const long long c = i + g.off[k];
+        sum = sum + __ldg(g.val + k * g.ld + i) * (__ldg(g.dvec + c) * in.ldc(c));
+      }
+    }
+    const double y = sum * dr;
+    const double cc = epi.st(i, y, xr, ev);
+    if (kRed) acc = acc + cc;
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
 // ----------------------------------------------------------------- vector kernels
 // Grid-stride over a fixed grid (deterministic element -> thread map).
 

@@ -104,6 +104,12 @@ struct pcgx_operator_s {
   int bsr_slices = 0;
   long long bsr_blocks = 0;     // stored (unpadded) blocks = nnz / 9
   long long bsr_padded = 0;     // blocks incl. slice padding
+  // offset (diagonal) storage (dia_kernel): K fixed column offsets, values by offset
+  double* dia_val = nullptr;
+  unsigned* dia_mask = nullptr;
+  int dia_k = 0;
+  int dia_off[32] = {0};
+  long long dia_ld = 0;
   // CSR block rows on a multi-rank context: this rank owns rows [row0, row0 + n_local);
   // columns >= n_local index the ghost array (values of other ranks' rows)
   long long row0 = 0, nghost = 0, nsend = 0;
@@ -600,7 +606,8 @@ int halo_vecs(const InComb& in, const double** xs) {
 
 // Whether the operator's kernels accept the fused direction-update input.
 bool fuses_dir_update(pcgx_operator op) {
-  return op->kind == 0 || op->sell_ptr != nullptr || op->bsr_ptr != nullptr;
+  return op->kind == 0 || op->sell_ptr != nullptr || op->bsr_ptr != nullptr ||
+         op->dia_val != nullptr;
 }
 
 // y-consuming launch of the scaled operator over the local rows, with the halo
@@ -608,12 +615,37 @@ bool fuses_dir_update(pcgx_operator op) {
 template <class In, class Epi, bool kRed>
 void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi, int slot) {
   op->matvecs.fetch_add(1, std::memory_order_relaxed);
+  if (op->kind == 1 && op->dia_val) {
+    DiaGeom g{};
+    g.n = (int)op->n_local;
+    g.K = op->dia_k;
+    g.ld = op->dia_ld;
+    for (int k = 0; k < op->dia_k; ++k) g.off[k] = op->dia_off[k];
+    g.val = op->dia_val;
+    g.mask = op->dia_mask;
+    g.dvec = op->dvec;
+    // one full wave of resident blocks, grid-stride over the rows (a partial second
+    // wave would leave SMs idle at the tail)
+    static int occ = 0;
+    if (!occ) {
+      PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dia_kernel<In, Epi, kRed>, 256, 0));
+      occ = std::max(occ, 1);
+    }
+    const long long want = (op->n_local + 255) / 256;
+    const int bps = env_int("PCGX_DIA_BPS", 0);
+    const int grid = (int)std::max(1LL, std::min(want, (long long)c->sms * (bps > 0 ? bps : occ)));
+    Reduce red = kRed ? make_red(c, slot) : Reduce{};
+    dia_kernel<In, Epi, kRed><<<grid, 256, 0, c->s>>>(g, in, epi, red);
+    check_launch();
+    count_launch(c);
+    return;
+  }
   if (op->kind == 1 && op->bsr_ptr) {
     Bsr3Geom g{(int)(op->n_local / 3), 0, op->bsr_slices, op->bsr_ptr, op->bsr_len, op->bsr_col,
                op->bsr_val, op->dvec};
     const int wpb = 8;
     const int want = (op->bsr_slices + wpb - 1) / wpb;
-    const int grid = std::max(1, std::min(want, c->sms * env_int("PCGX_BSR_BPS", 8)));
+    const int grid = std::max(1, std::min(want, c->sms * env_int("PCGX_BSR_BPS", 16)));
     Reduce red = kRed ? make_red(c, slot) : Reduce{};
     bsr3_kernel<In, Epi, kRed><<<grid, 32 * wpb, 0, c->s>>>(g, in, epi, red);
     check_launch();
@@ -1175,6 +1207,7 @@ double matrix_bytes(pcgx_operator op) {
   if (op->kind == 0) return 0.0;
   if (op->bsr_ptr)
     return 8.0 * (double)op->nnz + 4.0 * (double)op->bsr_blocks + 4.0 * (double)(op->n_local / 3 + 1);
+  if (op->dia_val) return 8.0 * (double)op->dia_k * (double)op->n_local + 4.0 * (double)op->n_local;
   return 12.0 * (double)op->nnz + 4.0 * (double)(op->n_local + 1);
 }
 // SpMV-equivalent bytes, the BASELINE metric's numerator: stencil
@@ -1935,6 +1968,60 @@ bool is_bsr3(long long n, const std::vector<int>& rp, const std::vector<int>& ci
   return ok != 0;
 }
 
+// The sorted set of column offsets (col - row) if it has at most kDiaMax members.
+bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>& ci,
+                 std::vector<int>& off) {
+  off.clear();
+  // rows mostly repeat their neighbour's offset pattern: only new patterns are merged
+  int pa = 0, pb = 0;  // previous row's entries [pa, pb) and its row index
+  long long prow = -1;
+  for (long long i = 0; i < n; ++i) {
+    const int a = rp[(size_t)i], b = rp[(size_t)i + 1];
+    bool same = prow >= 0 && b - a == pb - pa;
+    for (int k = 0; k < b - a && same; ++k)
+      same = (long long)ci[(size_t)(a + k)] - i == (long long)ci[(size_t)(pa + k)] - prow;
+    if (!same)
+      for (int k = a; k < b; ++k) {
+        const long long o = (long long)ci[(size_t)k] - i;
+        if (std::find(off.begin(), off.end(), (int)o) == off.end()) {
+          if ((int)off.size() == kDiaMax) return false;
+          off.push_back((int)o);
+        }
+      }
+    pa = a;
+    pb = b;
+    prow = i;
+  }
+  std::sort(off.begin(), off.end());
+  return !off.empty();
+}
+
+// Offset-storage arrays (see dia_kernel).
+void build_dia(pcgx_operator op, long long n, const std::vector<int>& rp32,
+               const std::vector<int>& ci32, const double* va, const std::vector<int>& off) {
+  const int K = (int)off.size();
+  const long long ld = (n + 31) / 32 * 32;  // rows incl. the last slice's padding
+  std::vector<double> val((size_t)(ld * K), 0.0);
+  std::vector<unsigned> mask((size_t)n, 0u);
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < n; ++i) {
+    int q = 0;
+    for (int k = rp32[(size_t)i]; k < rp32[(size_t)i + 1]; ++k) {
+      const int o = (int)((long long)ci32[(size_t)k] - i);
+      while (off[(size_t)q] != o) ++q;  // both ascending
+      val[(size_t)(q * ld + i)] = va[k];
+      mask[(size_t)i] |= 1u << q;
+    }
+  }
+  op->dia_k = K;
+  op->dia_ld = ld;
+  for (int k = 0; k < K; ++k) op->dia_off[k] = off[(size_t)k];
+  PCGX_CUDA(cudaMalloc(&op->dia_val, sizeof(double) * val.size()));
+  PCGX_CUDA(cudaMalloc(&op->dia_mask, sizeof(unsigned) * mask.size()));
+  PCGX_CUDA(cudaMemcpy(op->dia_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMemcpy(op->dia_mask, mask.data(), sizeof(unsigned) * mask.size(), cudaMemcpyHostToDevice));
+}
+
 // BSR-3 / SELL-32 arrays (see bsr3_kernel) of an int32 CSR with is_bsr3 structure.
 void build_bsr3(pcgx_operator op, long long n, const std::vector<int>& rp32,
                 const std::vector<int>& ci32, const double* va) {
@@ -2036,7 +2123,17 @@ void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, c
   }
   if (n) PCGX_CUDA(cudaMemcpy(op->dvec, dv.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice));
   const int ckern = env_int("PCGX_CSR_KERNEL", 0);  // 0 sell (default), 1 tma tiles, 2 chunked
-  if (ckern == 0 && n > 0 && env_int("PCGX_BSR", 1) != 0 && is_bsr3(n, rp32, ci32)) {
+  std::vector<int> doff;
+  // offset storage moves fewer bytes than int32 CSR while 8 K n + 4 n < 12 nnz + 4 n
+  const bool dia = ckern == 0 && n > 0 && env_int("PCGX_DIA", 1) != 0 && dia_offsets(n, rp32, ci32, doff) &&
+                   (double)doff.size() * (double)n <= 1.5 * (double)nnz;
+  if (dia) {
+    build_dia(op, n, rp32, ci32, va, doff);
+    cudaFree(op->ci);
+    cudaFree(op->va);
+    op->ci = nullptr;
+    op->va = nullptr;
+  } else if (ckern == 0 && n > 0 && env_int("PCGX_BSR", 1) != 0 && is_bsr3(n, rp32, ci32)) {
     build_bsr3(op, n, rp32, ci32, va);
     cudaFree(op->ci);
     cudaFree(op->va);
@@ -2092,6 +2189,8 @@ void free_op(pcgx_operator op) {
   cudaFree(op->bsr_len);
   cudaFree(op->bsr_col);
   cudaFree(op->bsr_val);
+  cudaFree(op->dia_val);
+  cudaFree(op->dia_mask);
   cudaFree(op->send_idx);
   cudaFree(op->sbuf_z);
   cudaFree(op->sbuf_p);
@@ -2401,6 +2500,7 @@ int pcgx_operator_storage(pcgx_operator op) {
   if (!op) return -1;
   if (op->kind == 0) return 0;
   if (op->bsr_ptr) return 2;
+  if (op->dia_val) return 5;
   if (op->sell_ptr) return 1;
   return op->tile_row ? 3 : 4;
 }

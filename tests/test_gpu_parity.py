@@ -562,8 +562,31 @@ def test_bsr3_solve_vs_oracle(P, ctx, oracle):
             assert rel_norm(x, xo) <= 1e-10
 
 
-def test_non_block_matrices_keep_sell(P, ctx):
-    A = P.gen_fe27(9, sigma=1.0, seed=SEED)          # n = 729 = 3 * 243, scalar pattern
-    assert csr(P, ctx, A.row_ptr, A.col_idx, A.values).storage() == "sell32"
-    rp, ci, va = lap3d_csr(6)                          # n = 216, 7-point pattern
-    assert csr(P, ctx, rp, ci, va).storage() == "sell32"
+def test_storage_selection(P, ctx, golden):
+    A = P.gen_fe27(9, sigma=1.0, seed=SEED)          # n = 729 = 3 * 243, 27 offsets: offset storage
+    assert csr(P, ctx, A.row_ptr, A.col_idx, A.values).storage() == "dia"
+    rp, ci, va = lap3d_csr(6)                          # 7 offsets
+    assert csr(P, ctx, rp, ci, va).storage() == "dia"
+    g = golden["csr_apply"]                            # random pattern: SELL-32
+    assert csr(P, ctx, np.array(g["row_ptr"]), np.array(g["col_idx"]),
+               fhs(g["values"])).storage() == "sell32"
+
+
+@pytest.mark.parametrize("nx,sigma", [(8, 1.0), (14, 1.0), (23, 0.5)])
+def test_dia_bitwise_vs_oracle(P, ctx, oracle, nx, sigma, monkeypatch):
+    """27-point FE matrices in offset storage: SpMV and Chebyshev steps bitwise the
+    reference's CSR row sums; the SELL path gives the same bits."""
+    A = P.gen_fe27(nx, sigma=sigma, seed=SEED)
+    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op.storage() == "dia"
+    opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    x = oracle.random_uniform(A.n, 23)
+    assert np.array_equal(op.apply(x), oracle.apply(opo, x))
+    for m in (1, 2, 6):
+        prm = P.cheb_params(0.01, 2.1, m, 1.001)
+        assert np.array_equal(P.apply_chebyshev(prm, op, x),
+                              oracle.apply_chebyshev(opo, oracle.cheb_params(0.01, 2.1, m, 1.001), x))
+    monkeypatch.setenv("PCGX_DIA", "0")
+    op_s = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op_s.storage() == "sell32"
+    assert np.array_equal(op_s.apply(x), op.apply(x))
