@@ -906,8 +906,11 @@ struct Bsr3Geom {
 #endif
 constexpr int kBsrBatch = PCGX_BSR_BATCH;
 
+#ifndef PCGX_BSR_MINB
+#define PCGX_BSR_MINB 4
+#endif
 template <class In, class Epi, bool kRed>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, PCGX_BSR_MINB)
 bsr3_kernel(Bsr3Geom g, In in, Epi epi, Reduce red) {
   in.init();
   const int lane = threadIdx.x & 31;
@@ -1047,6 +1050,43 @@ update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
     }
   }
   if (zmode) block_reduce_finish2(acc, acc2, red);
+  else block_reduce_finish(acc, red);
+}
+
+// update_kernel on 16-byte pairs (n even, 16-byte aligned vectors): the same
+// per-element operations, four 16-byte loads in flight per thread per step.
+template <int kZ>
+__global__ void __launch_bounds__(kVecThreads)
+update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
+               const double2* __restrict__ p, const double2* __restrict__ q, const double* S,
+               int s_rho, int s_pq, Reduce red, double theta, double2* __restrict__ z) {
+  const double alpha = S[s_rho] / S[s_pq];
+  double acc = 0.0, acc2 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 xi = x[i];
+    const double2 pi = __ldg(p + i);
+    double2 ri = r[i];
+    const double2 qi = __ldg(q + i);
+    xi.x = xi.x + alpha * pi.x;
+    xi.y = xi.y + alpha * pi.y;
+    ri.x = ri.x - alpha * qi.x;
+    ri.y = ri.y - alpha * qi.y;
+    x[i] = xi;
+    r[i] = ri;
+    acc = acc + ri.x * ri.x;
+    acc = acc + ri.y * ri.y;
+    if (kZ == 1) {
+      const double2 zi = make_double2(ri.x / theta, ri.y / theta);
+      z[i] = zi;
+      acc2 = acc2 + ri.x * zi.x;
+      acc2 = acc2 + ri.y * zi.y;
+    } else if (kZ == 2) {
+      acc2 = acc2 + ri.x * ri.x;
+      acc2 = acc2 + ri.y * ri.y;
+    }
+  }
+  if (kZ) block_reduce_finish2(acc, acc2, red);
   else block_reduce_finish(acc, red);
 }
 

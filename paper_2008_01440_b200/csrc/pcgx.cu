@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <type_traits>
@@ -35,6 +36,19 @@
 using namespace pcgx;
 
 // ============================================================================ types
+
+// An instantiated CUDA graph of one speculative PCG segment and what one replay
+// launches (kernels and all-reduces are counted per replay).
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
+  int64_t allreduces = 0;
+  ~Graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+std::atomic<uint64_t> g_op_uid{1};
 
 struct pcgx_context_s {
   int device = 0;
@@ -62,6 +76,10 @@ struct pcgx_context_s {
   // Newton-form level vectors L[0..nlev-1] (NewtonWorkspace, polyprec.hpp:69-71)
   std::vector<double*> nl;
   long long nl_n = 0;
+  // instantiated PCG segment graphs, keyed by everything they bake in (operator,
+  // preconditioner coefficients, schedule, workspace generation); reused across solves
+  std::map<std::string, std::unique_ptr<Graph>> gcache;
+  uint64_t ws_gen = 0;  // bumped whenever a workspace buffer is (re)allocated
   // solve-local bookkeeping
   int64_t cur_launches = 0;
   int64_t cur_allreduce = 0;
@@ -71,6 +89,7 @@ struct pcgx_context_s {
 
 struct pcgx_operator_s {
   pcgx_context ctx = nullptr;
+  uint64_t uid = g_op_uid.fetch_add(1);  // never reused (graph-cache key)
   int kind = 0;  // 0 stencil7, 1 csr
   long long n_global = 0, n_local = 0, nnz = 0;
   // stencil
@@ -252,6 +271,8 @@ void ensure_workspace(pcgx_context c, long long n, long long pad = 0) {
   }
   c->ws_n = n;
   c->ws_pad = pad;
+  c->ws_gen++;
+  c->gcache.clear();
 }
 
 int vec_grid(pcgx_context c, long long n) {
@@ -760,6 +781,33 @@ void launch_zr(pcgx_context c, long long n, double* z, const double* r, double t
   count_launch(c);
 }
 
+// x += alpha p ; r -= alpha q (+ z = r / theta) with the r'r (, r'z) reduction:
+// the 16-byte-pair kernel when every vector allows it.
+void launch_update(pcgx_context c, long long n, double* x, double* r, const double* p,
+                   const double* q, int s_rho, int s_pq, int s_rr, int zm, double theta, double* z) {
+  auto al16 = [](const void* v) { return ((uintptr_t)v & 15u) == 0; };
+  const bool vec = (n % 2 == 0) && al16(x) && al16(r) && al16(p) && al16(q) && al16(z) &&
+                   env_int("PCGX_UPD2", 1) != 0;
+  if (!vec) {
+    update_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, r, p, q, c->S, s_rho, s_pq,
+                                                            make_red(c, s_rr), zm, theta, z);
+    return;
+  }
+  const long long n2 = n / 2;
+  const int bps = env_int("PCGX_UPD_BPS", 8);
+  const int grid = (int)std::max(1LL, std::min((n2 + kVecThreads - 1) / kVecThreads, (long long)c->sms * bps));
+  auto d2 = [](const double* v) { return reinterpret_cast<double2*>(const_cast<double*>(v)); };
+  if (zm == 0)
+    update2_kernel<0><<<grid, kVecThreads, 0, c->s>>>(n2, d2(x), d2(r), d2(p), d2(q), c->S, s_rho,
+                                                      s_pq, make_red(c, s_rr), theta, d2(z));
+  else if (zm == 1)
+    update2_kernel<1><<<grid, kVecThreads, 0, c->s>>>(n2, d2(x), d2(r), d2(p), d2(q), c->S, s_rho,
+                                                      s_pq, make_red(c, s_rr), theta, d2(z));
+  else
+    update2_kernel<2><<<grid, kVecThreads, 0, c->s>>>(n2, d2(x), d2(r), d2(p), d2(q), c->S, s_rho,
+                                                      s_pq, make_red(c, s_rr), theta, d2(z));
+}
+
 void launch_dot(pcgx_context c, long long n, const double* a, const double* b, int slot) {
   dot_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, a, b, make_red(c, slot));
   check_launch();
@@ -1018,6 +1066,8 @@ void ensure_newton_ws(pcgx_context c, long long n, int nlev) {
     double* b = nullptr;
     PCGX_CUDA(cudaMalloc(&b, sizeof(double) * (size_t)std::max(n, 1LL)));
     c->nl.push_back(b);
+    c->ws_gen++;
+    c->gcache.clear();
   }
 }
 
@@ -1155,15 +1205,6 @@ void enqueue_prec(pcgx_context c, pcgx_operator op, const Prec& P, const double*
 }
 
 // ---------------------------------------------------------------- PCG
-
-struct Graph {
-  cudaGraphExec_t exec = nullptr;
-  int64_t kernels = 0;
-  int64_t allreduces = 0;
-  ~Graph() {
-    if (exec) cudaGraphExecDestroy(exec);
-  }
-};
 
 template <class F>
 void capture(pcgx_context c, Graph& g, F&& body) {
@@ -1324,25 +1365,6 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   double* Pd[2] = {p, c->p2};  // direction ping-pong: p(it) lives in Pd[it & 1]
   const bool fuse = fuses_dir_update(op) && env_int("PCGX_NO_FUSE_P", 0) == 0;
 
-  // setup: z_0 = P r_0 and rho_0 = r'z -> rz(0) (pcg.cpp:57-64)
-  if (zm == 0) enqueue_prec(c, op, prec, r, z, slot_rz(0));
-  else if (zm == 1) launch_zr(c, n, z, r, P.theta, 1, slot_rz(0));
-  else launch_dot(c, n, r, r, slot_rz(0));
-  allreduce(c, slot_rz(0), 1);
-  alg += cheb_bytes();
-  if (have_prec) {
-    rep->prec_applies++;
-    rep->matvec += m;
-  }
-  rep->ddot++;
-  fetch_scalars(c);
-  {
-    const double rho = c->hS[slot_rz(0)];
-    if (!std::isfinite(rho) || rho <= 0.0)
-      fail(PCGX_ERR_NUMERICAL,
-           "pcg_solve: r'z = " + fmt_double(rho) + " at setup (preconditioner not SPD?)");
-  }
-
   // dir_spmv(it): p(it) = z + beta p(it-1) (p(1) = z), q = A p(it), p'q -> pq(par); the
   // direction update is fused into the SpMV's input (InComb) where the kernels allow it.
   auto enqueue_dir_spmv = [&](int it) {
@@ -1383,7 +1405,54 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     }
     enqueue_dir_spmv(it + 1);
   };
-  Graph gB[2];
+  // setup: z_0 = P r_0 and rho_0 = r'z -> rz(0) (pcg.cpp:57-64)
+  if (zm == 0) enqueue_prec(c, op, prec, r, z, slot_rz(0));
+  else if (zm == 1) launch_zr(c, n, z, r, P.theta, 1, slot_rz(0));
+  else launch_dot(c, n, r, r, slot_rz(0));
+  // the two segment graphs (iteration parity 1, 0): cached across solves; a new
+  // one is captured here, on the host, while the device works on the setup P r
+  Graph* gB[2] = {nullptr, nullptr};
+  if (use_graph) {
+    std::string key;
+    auto add = [&](const void* v, size_t bytes) { key.append((const char*)v, bytes); };
+    const uint64_t ids[2] = {op->uid, c->ws_gen};
+    add(ids, sizeof ids);
+    const int flags[5] = {prec.kind, m, zm, fuse ? 1 : 0, spec_after_update ? 1 : 0};
+    add(flags, sizeof flags);
+    if (prec.kind == 1) {
+      const double t[3] = {P.theta, P.delta, P.sigma};
+      add(t, sizeof t);
+      add(P.rho.data(), sizeof(double) * P.rho.size());
+    } else if (prec.kind == 2) {
+      add(prec.newton.zeta.data(), sizeof(double) * prec.newton.zeta.size());
+    }
+    for (int par = 0; par < 2; ++par) {
+      const std::string k = key + (par ? "1" : "0");
+      auto hit = c->gcache.find(k);
+      if (hit == c->gcache.end()) {
+        if (c->gcache.size() >= 64) c->gcache.clear();
+        auto g = std::make_unique<Graph>();
+        capture(c, *g, [&] { enqueue_B(par ? 1 : 2); });
+        hit = c->gcache.emplace(k, std::move(g)).first;
+      }
+      gB[par] = hit->second.get();
+    }
+  }
+  allreduce(c, slot_rz(0), 1);
+  alg += cheb_bytes();
+  if (have_prec) {
+    rep->prec_applies++;
+    rep->matvec += m;
+  }
+  rep->ddot++;
+  fetch_scalars(c);
+  {
+    const double rho = c->hS[slot_rz(0)];
+    if (!std::isfinite(rho) || rho <= 0.0)
+      fail(PCGX_ERR_NUMERICAL,
+           "pcg_solve: r'z = " + fmt_double(rho) + " at setup (preconditioner not SPD?)");
+  }
+
   const double bytes_B = (zm == 0 ? cheb_bytes() : 0.0) + bytes_dir;
   const double bytes_update = 6 * N8 + (zm == 1 ? N8 : 0.0);
 
@@ -1391,10 +1460,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   alg += bytes_dir;
   for (int it = 1; it <= opts.maxit; ++it) {
     const int par = it & 1;
-    update_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, r, Pd[par], q, c->S,
-                                                            slot_rz(par ^ 1), slot_pq(par),
-                                                            make_red(c, slot_rr(par)), zm,
-                                                            zm == 1 ? P.theta : 1.0, z);
+    launch_update(c, n, x, r, Pd[par], q, slot_rz(par ^ 1), slot_pq(par), slot_rr(par), zm,
+                  zm == 1 ? P.theta : 1.0, z);
     check_launch();
     count_launch(c);
     alg += bytes_update;
@@ -1404,8 +1471,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     if (snap_after_update || !more) snapshot();
     if (more) {
       if (use_graph) {
-        if (!gB[par].exec) capture(c, gB[par], [&] { enqueue_B(it); });
-        replay(c, gB[par]);
+        replay(c, *gB[par]);
       } else {
         enqueue_B(it);
       }
