@@ -24,7 +24,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpcgx.so")
 SOURCES = ["pcgx.cu", "host_math.cpp", "gen.cpp", "mm.cpp"]
-HEADERS = ["common.cuh", "kernels.cuh", "cheb2.cuh", "host_math.hpp"]
+HEADERS = ["common.cuh", "kernels.cuh", "cheb2.cuh", "dir_tma.cuh", "host_math.hpp"]
 
 
 def _nvcc():

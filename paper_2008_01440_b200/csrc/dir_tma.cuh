@@ -1,0 +1,142 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// The PCG direction step on the 7-point stencil, TMA-staged (single rank):
+//   p_new = z + beta p_old   (pcg.cpp:107; first iteration p = z, pcg.cpp:63)
+//   q     = A_scaled p_new   (pcg.cpp:72, linop.cpp:236-258, 271-275)
+//   p_new . q                (pcg.cpp:74, the first reduction point)
+// The register-queue kernel (stencil7v2 with InComb) re-forms z + beta p for every
+// neighbour it loads (three combines and six loads per point); here each plane of
+// z and p_old arrives once as a 68 x 10 TMA box, every element is combined ONCE
+// into a shared p_new plane, and the stencil reads its j-neighbours from there
+// (k-neighbours from a per-lane register queue, i-neighbours by shuffle). Same
+// per-element operations in the same order as the other paths, so p_new and q are
+// bitwise theirs. HBM: read z, p_old; write p_new, q = 32 B per point.
+#pragma once
+
+#include "cheb2.cuh"
+
+namespace pcgx {
+
+constexpr int kDirNS = 6;                 // z / p_old ring slots (4 planes ahead)
+constexpr int kDirNC = 3;                 // p_new planes
+constexpr int kDirThreads = 320;          // one warp per extended row (8 tile rows + 2 halo rows)
+constexpr size_t kDirSmem =
+    sizeof(double) * (size_t)(2 * kDirNS * kC2EStride + kDirNC * kC2BPlane) + 8 * kDirNS + 128;
+
+struct DirParams {
+  int nx, ny, nzl;
+  long long nxy;
+  double d;
+  const double* S;
+  int s_new, s_old, first;
+  double* q;     // A p_new
+  double* pout;  // p_new
+};
+
+// grid: (ceil(nx/64), ceil(ny/8), ceil(nzl/kz)); block 320; dynamic smem kDirSmem.
+__global__ void __launch_bounds__(kDirThreads, 2)
+stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapP,
+                    DirParams p, int k_begin, int k_end, int kz, Reduce red) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sZ = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+  double* sP = sZ + kDirNS * kC2EStride;
+  double* sN = sP + kDirNS * kC2EStride;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sN + kDirNC * kC2BPlane);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i0 = blockIdx.x * kC2TX, j0 = blockIdx.y * kC2TY;
+  const int kb = k_begin + blockIdx.z * kz;
+  const int ke = min(kb + kz, k_end);
+  const bool first = p.first != 0;
+  const double beta = first ? 0.0 : p.S[p.s_new] / p.S[p.s_old];
+  const unsigned bytes = kC2BPlane * 8;
+  auto in_z = [&](int z) { return z >= 0 && z < p.nzl; };
+  // unit u: the z (and p_old) boxes of plane u, slot / barrier (u - (kb-1)) % NS
+  auto issue = [&](int u) {
+    const int q = (u - (kb - 1)) % kDirNS;
+    const bool ld = in_z(u);
+    mbar_expect_tx(&bars[q], ld ? (first ? bytes : 2 * bytes) : 0u);
+    if (ld) {
+      tma_load_3d(sZ + q * kC2EStride, &mapZ, i0 - 2, j0 - 1, u, &bars[q]);
+      if (!first) tma_load_3d(sP + q * kC2EStride, &mapP, i0 - 2, j0 - 1, u, &bars[q]);
+    }
+  };
+  if (tid == 0) {
+    for (int q = 0; q < kDirNS; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int u = kb - 1; u < kb - 1 + kDirNS && u <= ke; ++u) issue(u);
+  }
+  __syncthreads();
+
+  const double d = p.d;
+  const double2 zero2 = make_double2(0.0, 0.0);
+  const int col = 2 * lane + 2;
+  const int gi = i0 + 2 * lane;
+  const bool pair_in = gi < p.nx;
+  const int gj = j0 - 1 + warp;
+  const bool do1 = gj >= 0 && gj < p.ny && pair_in;
+  const bool tile_row = warp >= 1 && warp <= kC2TY;
+  const int off = warp * kC2W + col;
+  const long long goff = (long long)gj * p.nx + gi;
+  auto comb = [&](double zv, double pv) { return first ? zv : zv + beta * pv; };
+
+  double2 pm = zero2, pc = zero2;  // p_new of the warp's row at planes u-2, u-1
+  double acc = 0.0;
+  int slot = 0;
+  unsigned phase = 0;
+  int sc = 0;  // p_new ring slot of plane u
+  for (int u = kb - 1; u <= ke; ++u) {
+    mbar_wait(&bars[slot], phase);
+    const double* Zu = sZ + slot * kC2EStride;
+    const double* Pu = sP + slot * kC2EStride;
+    double2 pn = zero2;
+    if (in_z(u) && do1) {
+      const double2 zv = *reinterpret_cast<const double2*>(Zu + off);
+      if (first) {
+        pn = zv;
+      } else {
+        const double2 pv = *reinterpret_cast<const double2*>(Pu + off);
+        pn = make_double2(comb(zv.x, pv.x), comb(zv.y, pv.y));
+      }
+    }
+    double* Nu = sN + sc * kC2BPlane;
+    *reinterpret_cast<double2*>(Nu + off) = pn;
+    __syncthreads();
+    // the slot of plane u-2 is free (its last readers are behind this barrier)
+    if (tid == 0 && u >= kb + 1 && u - 2 + kDirNS <= ke) issue(u - 2 + kDirNS);
+    const int v = u - 1;
+    if (tile_row && v >= kb) {
+      // p_new of plane v: the warp's own pair (pc), i-neighbours by shuffle, the
+      // lane-0 / lane-31 outer neighbours combined from plane v's boxes (zero-filled
+      // outside the domain), j-neighbours from the shared plane
+      const int sv = slot == 0 ? kDirNS - 1 : slot - 1;
+      const double* Zv = sZ + sv * kC2EStride;
+      const double* Pv = sP + sv * kC2EStride;
+      const double* Nv = sN + (sc == 0 ? kDirNC - 1 : sc - 1) * kC2BPlane;
+      double pw = __shfl_up_sync(0xffffffffu, pc.y, 1);
+      double pe = __shfl_down_sync(0xffffffffu, pc.x, 1);
+      if (lane == 0) pw = comb(Zv[off - 1], first ? 0.0 : Pv[off - 1]);
+      if (lane == 31) pe = comb(Zv[off + 2], first ? 0.0 : Pv[off + 2]);
+      if (do1) {
+        const double2 ps = *reinterpret_cast<const double2*>(Nv + off - kC2W);
+        const double2 pnn = *reinterpret_cast<const double2*>(Nv + off + kC2W);
+        const double y0 = stencil_point(d, pm.x, ps.x, pw, pc.x, pc.y, pnn.x, pn.x);
+        const double y1 = stencil_point(d, pm.y, ps.y, pc.x, pc.y, pe, pnn.y, pn.y);
+        const long long idx = (long long)v * p.nxy + goff;
+        st2(p.q + idx, y0, y1);
+        st2(p.pout + idx, pc.x, pc.y);
+        acc = acc + (pc.x * y0 + pc.y * y1);
+      }
+    }
+    pm = pc;
+    pc = pn;
+    if (++slot == kDirNS) {
+      slot = 0;
+      phase ^= 1u;
+    }
+    sc = (sc + 1 == kDirNC) ? 0 : sc + 1;
+  }
+  block_reduce_finish(acc, red);
+}
+
+}  // namespace pcgx

@@ -29,6 +29,7 @@
 
 #include "cheb2.cuh"
 #include "common.cuh"
+#include "dir_tma.cuh"
 #include "host_math.hpp"
 #include "kernels.cuh"
 #include "pcgx.h"
@@ -896,6 +897,31 @@ void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const doubl
   count_launch(c);
 }
 
+// The direction step p_new = z + beta p_old, q = A p_new, p_new . q -> slot on a
+// single-rank stencil operator (stencil7_dir_kernel, TMA-staged).
+bool dir_tma_ok(pcgx_operator op) {
+  return op->kind == 0 && op->vec2 && op->cheb2 && !op->ghost_lo && !op->ghost_hi && op->zpad == 0 &&
+         env_int("PCGX_DIR_TMA", 1) != 0;
+}
+
+void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const double* pold,
+                    double* pnew, double* q, int s_new, int s_old, int first, int slot) {
+  op->matvecs.fetch_add(1, std::memory_order_relaxed);
+  PCGX_CUDA(cudaFuncSetAttribute(stencil7_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kDirSmem));
+  const CUtensorMap mz = tmaps_for(op, z).e;
+  const CUtensorMap mp = tmaps_for(op, first ? z : pold).e;
+  DirParams prm{(int)op->nx, (int)op->ny, (int)op->nzl, op->nx * op->ny, op->d, c->S, s_new, s_old,
+                first, q, pnew};
+  const int nzl = (int)op->nzl;
+  const int kz = std::max(1, std::min(op->kz2, nzl));
+  dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
+            (unsigned)((nzl + kz - 1) / kz));
+  stencil7_dir_kernel<<<grid, kDirThreads, kDirSmem, c->s>>>(mz, mp, prm, 0, nzl, kz, make_red(c, slot));
+  check_launch();
+  count_launch(c);
+}
+
 // One two-step pass over the local slab. On a z-slab rank the neighbours' two
 // A planes (one B plane) per side are first exchanged into the vectors'
 // padding; the chunks that do not read them run while the planes travel.
@@ -1372,7 +1398,9 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     double* pnew = Pd[par];
     const double* pold = Pd[par ^ 1];
     const int first = (it == 1) ? 1 : 0;
-    if (fuse) {
+    if (fuse && dir_tma_ok(op)) {
+      dir_tma_launch(c, op, zvec, pold, pnew, q, slot_rz(par ^ 1), slot_rz(par), first, slot_pq(par));
+    } else if (fuse) {
       op_launch_in<InComb, EpiStoreP, true>(
           c, op, in_of(op, zvec, pold, c->S, slot_rz(par ^ 1), slot_rz(par), first, true),
           EpiStoreP{q, pnew}, slot_pq(par));

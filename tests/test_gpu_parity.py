@@ -590,3 +590,26 @@ def test_dia_bitwise_vs_oracle(P, ctx, oracle, nx, sigma, monkeypatch):
     op_s = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
     assert op_s.storage() == "sell32"
     assert np.array_equal(op_s.apply(x), op.apply(x))
+
+
+@pytest.mark.parametrize("dims", [(66, 10, 9), (130, 17, 33), (64, 8, 1), (2, 2, 2), (40, 40, 40)])
+@pytest.mark.parametrize("m", [-1, 0, 4])
+def test_dir_tma_matches_register_path(P, ctx, oracle, dims, m, monkeypatch):
+    """stencil7_dir_kernel (TMA-staged p = z + beta p, q = A p, p'q) against the
+    register-queue InComb path and the oracle, on ragged tiles and thin slabs."""
+    nx, ny, nz = dims
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+    opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
+    rhs = oracle.apply(opo, oracle.random_uniform(nx * ny * nz, SEED))
+    prec = None if m < 0 else P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001))
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PCGX_DIR_TMA", flag)
+        out[flag] = P.pcg_solve(stencil(P, ctx, nx, ny, nz), rhs, P.SolveOptions(maxit=3000), prec)
+    (x1, r1), (x0, r0) = out["1"], out["0"]
+    assert r1.iters == r0.iters and rel_norm(x1, x0) <= 1e-12
+    xo, ro = oracle.pcg_solve(opo, None if m < 0 else oracle.cheb_params(a, b, m, 1.001), rhs,
+                              maxit=3000)
+    assert abs(r1.iters - ro["iters"]) <= 1
+    if r1.iters == ro["iters"]:
+        assert rel_norm(x1, xo) <= 1e-10
