@@ -26,7 +26,10 @@
 
 namespace pcgx {
 
-constexpr int kC2TX = 64, kC2TY = 8;                 // output tile (i x j)
+#ifndef PCGX_C2TY
+#define PCGX_C2TY 8
+#endif
+constexpr int kC2TX = 64, kC2TY = PCGX_C2TY;         // output tile (i x j)
 constexpr int kC2W = kC2TX + 4;                      // row width of every smem plane (tile-i t <-> col t+2)
 constexpr int kC2AY = kC2TY + 4;                     // A box rows (2-halo in j)
 constexpr int kC2BY = kC2TY + 2;                     // B, R boxes and the C ring: 1-halo rows
@@ -44,10 +47,10 @@ constexpr int kC2D = PCGX_C2D;                       // prefetch distance (plane
 constexpr int kC2NA = kC2D + 2, kC2NB = kC2D, kC2NR = kC2D + 1, kC2NC = 3;
 constexpr int kC2APlane = kC2W * kC2AY;              // 816 doubles = 51 x 128 B
 constexpr int kC2BPlane = kC2W * kC2BY;              // 680 doubles
-constexpr int kC2EStride = 688;                      // B/R slot stride: 5504 B = 43 x 128 B (TMA dst alignment)
+constexpr int kC2EStride = (kC2W * kC2BY + 15) / 16 * 16;  // B/R slot stride, 128-byte multiple (TMA dst)
 constexpr int kC2CStride = kC2BPlane;                // C ring slot (plain shared stores)
 constexpr int kC2Warps = kC2TY + 2;                  // one warp per extended row in stage 1
-constexpr int kC2Threads = 32 * kC2Warps;            // 320
+constexpr int kC2Threads = 32 * kC2Warps;            // 320 at the default 64 x 8 tile
 constexpr size_t kC2Smem = sizeof(double) * (size_t)(kC2NA * kC2APlane + (kC2NB + kC2NR) * kC2EStride +
                                                      kC2NC * kC2CStride) +
                            16 * (kC2D + 1) + 128;

@@ -19,7 +19,7 @@ namespace pcgx {
 
 constexpr int kDirNS = 6;                 // z / p_old ring slots (4 planes ahead)
 constexpr int kDirNC = 3;                 // p_new planes
-constexpr int kDirThreads = 320;          // one warp per extended row (8 tile rows + 2 halo rows)
+constexpr int kDirThreads = kC2Threads;   // one warp per extended row (tile rows + 2 halo rows)
 constexpr size_t kDirSmem =
     sizeof(double) * (size_t)(2 * kDirNS * kC2EStride + kDirNC * kC2BPlane) + 8 * kDirNS + 128;
 
@@ -29,12 +29,14 @@ struct DirParams {
   double d;
   const double* S;
   int s_new, s_old, first;
+  double* x;     // != nullptr: also the previous iteration's x += alpha p_old (pcg.cpp:82),
+  int s_pq;      //   alpha = S[s_old] / S[s_pq] (deferred from the update kernel)
   double* q;     // A p_new
   double* pout;  // p_new
 };
 
-// grid: (ceil(nx/64), ceil(ny/8), ceil(nzl/kz)); block 320; dynamic smem kDirSmem.
-__global__ void __launch_bounds__(kDirThreads, 2)
+// grid: (ceil(nx/64), ceil(ny/kC2TY), ceil(nzl/kz)); block kDirThreads; dynamic smem kDirSmem.
+__global__ void __launch_bounds__(kDirThreads, PCGX_C2MINB)
 stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapP,
                     DirParams p, int k_begin, int k_end, int kz, Reduce red) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -79,6 +81,8 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   const int off = warp * kC2W + col;
   const long long goff = (long long)gj * p.nx + gi;
   auto comb = [&](double zv, double pv) { return first ? zv : zv + beta * pv; };
+  const bool xupd = p.x != nullptr && !first;
+  const double alpha = xupd ? p.S[p.s_old] / p.S[p.s_pq] : 0.0;
 
   double2 pm = zero2, pc = zero2;  // p_new of the warp's row at planes u-2, u-1
   double acc = 0.0;
@@ -86,6 +90,11 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   unsigned phase = 0;
   int sc = 0;  // p_new ring slot of plane u
   for (int u = kb - 1; u <= ke; ++u) {
+    // the x pair of plane u-1 (deferred update below): issued before the waits of
+    // this iteration so its latency hides behind them
+    double2 xv = zero2;
+    const bool xdo = xupd && tile_row && do1 && u - 1 >= kb;
+    if (xdo) xv = *reinterpret_cast<const double2*>(p.x + (long long)(u - 1) * p.nxy + goff);
     mbar_wait(&bars[slot], phase);
     const double* Zu = sZ + slot * kC2EStride;
     const double* Pu = sP + slot * kC2EStride;
@@ -126,6 +135,12 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
         st2(p.q + idx, y0, y1);
         st2(p.pout + idx, pc.x, pc.y);
         acc = acc + (pc.x * y0 + pc.y * y1);
+        if (xdo) {
+          const double2 po = *reinterpret_cast<const double2*>(Pv + off);
+          xv.x = xv.x + alpha * po.x;
+          xv.y = xv.y + alpha * po.y;
+          st2(p.x + idx, xv.x, xv.y);
+        }
       }
     }
     pm = pc;

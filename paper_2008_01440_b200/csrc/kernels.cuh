@@ -1037,7 +1037,7 @@ update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
   double acc = 0.0, acc2 = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    x[i] = x[i] + alpha * p[i];
+    if (x) x[i] = x[i] + alpha * p[i];  // x == nullptr: deferred to the next direction step
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
     acc = acc + ri * ri;
@@ -1055,7 +1055,7 @@ update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
 
 // update_kernel on 16-byte pairs (n even, 16-byte aligned vectors): the same
 // per-element operations, four 16-byte loads in flight per thread per step.
-template <int kZ>
+template <int kZ, bool kX>
 __global__ void __launch_bounds__(kVecThreads)
 update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
                const double2* __restrict__ p, const double2* __restrict__ q, const double* S,
@@ -1064,15 +1064,17 @@ update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
   double acc = 0.0, acc2 = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
        i += (long long)gridDim.x * blockDim.x) {
-    double2 xi = x[i];
-    const double2 pi = __ldg(p + i);
     double2 ri = r[i];
     const double2 qi = __ldg(q + i);
-    xi.x = xi.x + alpha * pi.x;
-    xi.y = xi.y + alpha * pi.y;
+    if (kX) {  // !kX: x += alpha p is deferred to the next direction step
+      double2 xi = x[i];
+      const double2 pi = __ldg(p + i);
+      xi.x = xi.x + alpha * pi.x;
+      xi.y = xi.y + alpha * pi.y;
+      x[i] = xi;
+    }
     ri.x = ri.x - alpha * qi.x;
     ri.y = ri.y - alpha * qi.y;
-    x[i] = xi;
     r[i] = ri;
     acc = acc + ri.x * ri.x;
     acc = acc + ri.y * ri.y;
@@ -1088,6 +1090,17 @@ update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
   }
   if (kZ) block_reduce_finish2(acc, acc2, red);
   else block_reduce_finish(acc, red);
+}
+
+// x += alpha p, alpha = S[s_rho] / S[s_pq] (pcg.cpp:82): a deferred x update that
+// no later direction step will apply (the iteration limit was reached)
+__global__ void __launch_bounds__(kVecThreads)
+xupd_kernel(long long n, double* __restrict__ x, const double* __restrict__ p, const double* S,
+            int s_rho, int s_pq) {
+  const double alpha = S[s_rho] / S[s_pq];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = x[i] + alpha * p[i];
 }
 
 // p_new = z + beta p_old, beta = rz[cur] / rz[prev] (pcg.cpp:107); first: p = z

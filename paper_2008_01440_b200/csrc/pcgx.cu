@@ -784,11 +784,13 @@ void launch_zr(pcgx_context c, long long n, double* z, const double* r, double t
 
 // x += alpha p ; r -= alpha q (+ z = r / theta) with the r'r (, r'z) reduction:
 // the 16-byte-pair kernel when every vector allows it.
+// x == nullptr: the x update is deferred to the next direction step.
 void launch_update(pcgx_context c, long long n, double* x, double* r, const double* p,
                    const double* q, int s_rho, int s_pq, int s_rr, int zm, double theta, double* z) {
   auto al16 = [](const void* v) { return ((uintptr_t)v & 15u) == 0; };
   const bool vec = (n % 2 == 0) && al16(x) && al16(r) && al16(p) && al16(q) && al16(z) &&
                    env_int("PCGX_UPD2", 1) != 0;
+  const bool dox = x != nullptr;
   if (!vec) {
     update_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, r, p, q, c->S, s_rho, s_pq,
                                                             make_red(c, s_rr), zm, theta, z);
@@ -798,15 +800,13 @@ void launch_update(pcgx_context c, long long n, double* x, double* r, const doub
   const int bps = env_int("PCGX_UPD_BPS", 8);
   const int grid = (int)std::max(1LL, std::min((n2 + kVecThreads - 1) / kVecThreads, (long long)c->sms * bps));
   auto d2 = [](const double* v) { return reinterpret_cast<double2*>(const_cast<double*>(v)); };
-  if (zm == 0)
-    update2_kernel<0><<<grid, kVecThreads, 0, c->s>>>(n2, d2(x), d2(r), d2(p), d2(q), c->S, s_rho,
-                                                      s_pq, make_red(c, s_rr), theta, d2(z));
-  else if (zm == 1)
-    update2_kernel<1><<<grid, kVecThreads, 0, c->s>>>(n2, d2(x), d2(r), d2(p), d2(q), c->S, s_rho,
-                                                      s_pq, make_red(c, s_rr), theta, d2(z));
-  else
-    update2_kernel<2><<<grid, kVecThreads, 0, c->s>>>(n2, d2(x), d2(r), d2(p), d2(q), c->S, s_rho,
-                                                      s_pq, make_red(c, s_rr), theta, d2(z));
+#define PCGX_UPD(ZM, X)                                                                          \
+  update2_kernel<ZM, X><<<grid, kVecThreads, 0, c->s>>>(n2, d2(x), d2(r), d2(p), d2(q), c->S, s_rho, \
+                                                        s_pq, make_red(c, s_rr), theta, d2(z))
+  if (zm == 0) dox ? PCGX_UPD(0, true) : PCGX_UPD(0, false);
+  else if (zm == 1) dox ? PCGX_UPD(1, true) : PCGX_UPD(1, false);
+  else dox ? PCGX_UPD(2, true) : PCGX_UPD(2, false);
+#undef PCGX_UPD
 }
 
 void launch_dot(pcgx_context c, long long n, const double* a, const double* b, int slot) {
@@ -905,14 +905,15 @@ bool dir_tma_ok(pcgx_operator op) {
 }
 
 void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const double* pold,
-                    double* pnew, double* q, int s_new, int s_old, int first, int slot) {
+                    double* pnew, double* q, int s_new, int s_old, int first, int slot,
+                    double* x = nullptr, int s_pq = 0) {
   op->matvecs.fetch_add(1, std::memory_order_relaxed);
   PCGX_CUDA(cudaFuncSetAttribute(stencil7_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kDirSmem));
   const CUtensorMap mz = tmaps_for(op, z).e;
   const CUtensorMap mp = tmaps_for(op, first ? z : pold).e;
   DirParams prm{(int)op->nx, (int)op->ny, (int)op->nzl, op->nx * op->ny, op->d, c->S, s_new, s_old,
-                first, q, pnew};
+                first, x, s_pq, q, pnew};
   const int nzl = (int)op->nzl;
   const int kz = std::max(1, std::min(op->kz2, nzl));
   dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
@@ -1390,6 +1391,9 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   const double* zvec = (zm == 2) ? r : z;
   double* Pd[2] = {p, c->p2};  // direction ping-pong: p(it) lives in Pd[it & 1]
   const bool fuse = fuses_dir_update(op) && env_int("PCGX_NO_FUSE_P", 0) == 0;
+  // single-rank stencil: x += alpha p moves from the update kernel into the next
+  // direction step, which reads p_old anyway (8 B less per unknown and iteration)
+  const bool defer_x = fuse && dir_tma_ok(op) && env_int("PCGX_DEFER_X", 1) != 0;
 
   // dir_spmv(it): p(it) = z + beta p(it-1) (p(1) = z), q = A p(it), p'q -> pq(par); the
   // direction update is fused into the SpMV's input (InComb) where the kernels allow it.
@@ -1399,7 +1403,9 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     const double* pold = Pd[par ^ 1];
     const int first = (it == 1) ? 1 : 0;
     if (fuse && dir_tma_ok(op)) {
-      dir_tma_launch(c, op, zvec, pold, pnew, q, slot_rz(par ^ 1), slot_rz(par), first, slot_pq(par));
+      // the previous iteration's x += alpha p_old rides along (defer_x)
+      dir_tma_launch(c, op, zvec, pold, pnew, q, slot_rz(par ^ 1), slot_rz(par), first, slot_pq(par),
+                     defer_x ? x : nullptr, slot_pq(par ^ 1));
     } else if (fuse) {
       op_launch_in<InComb, EpiStoreP, true>(
           c, op, in_of(op, zvec, pold, c->S, slot_rz(par ^ 1), slot_rz(par), first, true),
@@ -1443,7 +1449,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   if (use_graph) {
     std::string key;
     auto add = [&](const void* v, size_t bytes) { key.append((const char*)v, bytes); };
-    const uint64_t ids[2] = {op->uid, c->ws_gen};
+    const uint64_t ids[3] = {op->uid, c->ws_gen, defer_x ? (uint64_t)(uintptr_t)x : 0};
     add(ids, sizeof ids);
     const int flags[5] = {prec.kind, m, zm, fuse ? 1 : 0, spec_after_update ? 1 : 0};
     add(flags, sizeof flags);
@@ -1481,15 +1487,19 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
            "pcg_solve: r'z = " + fmt_double(rho) + " at setup (preconditioner not SPD?)");
   }
 
-  const double bytes_B = (zm == 0 ? cheb_bytes() : 0.0) + bytes_dir;
-  const double bytes_update = 6 * N8 + (zm == 1 ? N8 : 0.0);
+  const double bytes_B = (zm == 0 ? cheb_bytes() : 0.0) + bytes_dir + (defer_x ? 2 * N8 : 0.0);
+  const double bytes_update = (defer_x ? 3 : 6) * N8 + (zm == 1 ? N8 : 0.0);
+  bool x_pending = false;  // a deferred x update no direction step has applied yet
+  int x_par = 0;
 
   enqueue_dir_spmv(1);
   alg += bytes_dir;
   for (int it = 1; it <= opts.maxit; ++it) {
     const int par = it & 1;
-    launch_update(c, n, x, r, Pd[par], q, slot_rz(par ^ 1), slot_pq(par), slot_rr(par), zm,
-                  zm == 1 ? P.theta : 1.0, z);
+    launch_update(c, n, defer_x ? nullptr : x, r, Pd[par], q, slot_rz(par ^ 1), slot_pq(par),
+                  slot_rr(par), zm, zm == 1 ? P.theta : 1.0, z);
+    x_pending = defer_x;
+    x_par = par;
     check_launch();
     count_launch(c);
     alg += bytes_update;
@@ -1504,6 +1514,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
         enqueue_B(it);
       }
       alg += bytes_B;
+      x_pending = false;  // dir_spmv(it+1) applies it
     }
     PCGX_CUDA(cudaEventSynchronize(c->ev_sync));
     const double* hs = c->hS;
@@ -1540,6 +1551,13 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
       if (!std::isfinite(rz) || rz <= 0.0)
         fail(PCGX_ERR_NUMERICAL, "pcg_solve: r'z = " + fmt_double(rz) + " (preconditioner not SPD?)");
     }
+  }
+  if (x_pending) {  // the iteration limit ended the loop before the next direction step
+    xupd_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, Pd[x_par], c->S, slot_rz(x_par ^ 1),
+                                                          slot_pq(x_par));
+    check_launch();
+    count_launch(c);
+    alg += 3 * N8;
   }
   // true residual (pcg.cpp:112-115)
   op_launch<EpiResid, true>(c, op, x, EpiResid{b, nullptr}, S_EE);
