@@ -1,6 +1,6 @@
 // SPDX-License-Identifier: Apache-2.0
 //
-// The PCG direction step on the 7-point stencil, TMA-staged (single rank):
+// The PCG direction step on the 7-point stencil, TMA-staged:
 //   p_new = z + beta p_old   (pcg.cpp:107; first iteration p = z, pcg.cpp:63)
 //   q     = A_scaled p_new   (pcg.cpp:72, linop.cpp:236-258, 271-275)
 //   p_new . q                (pcg.cpp:74, the first reduction point)
@@ -25,6 +25,10 @@ constexpr size_t kDirSmem =
 
 struct DirParams {
   int nx, ny, nzl;
+  // z-slab ranks: z / p_old planes exist on [a_lo, a_hi) (the slab plus the
+  // neighbours' boundary planes exchanged into the vectors' padding); tensor z of
+  // plane u is u + zoff
+  int a_lo, a_hi, zoff;
   long long nxy;
   double d;
   const double* S;
@@ -52,15 +56,15 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   const bool first = p.first != 0;
   const double beta = first ? 0.0 : p.S[p.s_new] / p.S[p.s_old];
   const unsigned bytes = kC2BPlane * 8;
-  auto in_z = [&](int z) { return z >= 0 && z < p.nzl; };
+  auto in_z = [&](int z) { return z >= p.a_lo && z < p.a_hi; };
   // unit u: the z (and p_old) boxes of plane u, slot / barrier (u - (kb-1)) % NS
   auto issue = [&](int u) {
     const int q = (u - (kb - 1)) % kDirNS;
     const bool ld = in_z(u);
     mbar_expect_tx(&bars[q], ld ? (first ? bytes : 2 * bytes) : 0u);
     if (ld) {
-      tma_load_3d(sZ + q * kC2EStride, &mapZ, i0 - 2, j0 - 1, u, &bars[q]);
-      if (!first) tma_load_3d(sP + q * kC2EStride, &mapP, i0 - 2, j0 - 1, u, &bars[q]);
+      tma_load_3d(sZ + q * kC2EStride, &mapZ, i0 - 2, j0 - 1, u + p.zoff, &bars[q]);
+      if (!first) tma_load_3d(sP + q * kC2EStride, &mapP, i0 - 2, j0 - 1, u + p.zoff, &bars[q]);
     }
   };
   if (tid == 0) {

@@ -898,9 +898,11 @@ void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const doubl
 }
 
 // The direction step p_new = z + beta p_old, q = A p_new, p_new . q -> slot on a
-// single-rank stencil operator (stencil7_dir_kernel, TMA-staged).
+// stencil operator (stencil7_dir_kernel, TMA-staged); on a z-slab rank the
+// neighbours' boundary planes of z and p_old travel into the vectors' padding.
 bool dir_tma_ok(pcgx_operator op) {
-  return op->kind == 0 && op->vec2 && op->cheb2 && !op->ghost_lo && !op->ghost_hi && op->zpad == 0 &&
+  const bool ghosts = op->ghost_lo || op->ghost_hi;
+  return op->kind == 0 && op->vec2 && op->cheb2 && (!ghosts || op->zpad >= 1) &&
          env_int("PCGX_DIR_TMA", 1) != 0;
 }
 
@@ -912,15 +914,48 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
                                  (int)kDirSmem));
   const CUtensorMap mz = tmaps_for(op, z).e;
   const CUtensorMap mp = tmaps_for(op, first ? z : pold).e;
-  DirParams prm{(int)op->nx, (int)op->ny, (int)op->nzl, op->nx * op->ny, op->d, c->S, s_new, s_old,
-                first, x, s_pq, q, pnew};
   const int nzl = (int)op->nzl;
-  const int kz = std::max(1, std::min(op->kz2, nzl));
-  dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
-            (unsigned)((nzl + kz - 1) / kz));
-  stencil7_dir_kernel<<<grid, kDirThreads, kDirSmem, c->s>>>(mz, mp, prm, 0, nzl, kz, make_red(c, slot));
-  check_launch();
-  count_launch(c);
+  const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
+  DirParams prm{(int)op->nx, (int)op->ny, nzl, lo ? -1 : 0, hi ? nzl + 1 : nzl, op->zpad,
+                op->nx * op->ny, op->d, c->S, s_new, s_old, first, x, s_pq, q, pnew};
+  auto launch = [&](int k_begin, int k_end, int kz, bool accumulate) {
+    if (k_end <= k_begin) return;
+    kz = std::max(1, std::min(kz, k_end - k_begin));
+    dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
+              (unsigned)((k_end - k_begin + kz - 1) / kz));
+    stencil7_dir_kernel<<<grid, kDirThreads, kDirSmem, c->s>>>(mz, mp, prm, k_begin, k_end, kz,
+                                                               make_red(c, slot, accumulate));
+    check_launch();
+    count_launch(c);
+  };
+  if (!lo && !hi) {
+    launch(0, nzl, op->kz2, false);
+    return;
+  }
+  // my first / last plane of z (and p_old) -> the neighbours' padding; the planes
+  // that do not read a ghost run while they travel
+  const long long nxy = op->nx * op->ny;
+  CommBase::PlaneX items[2];
+  int ni = 0;
+  items[ni++] = {z, const_cast<double*>(z) - nxy, z + (long long)(nzl - 1) * nxy,
+                 const_cast<double*>(z) + (long long)nzl * nxy, nxy};
+  if (!first)
+    items[ni++] = {pold, const_cast<double*>(pold) - nxy, pold + (long long)(nzl - 1) * nxy,
+                   const_cast<double*>(pold) + (long long)nzl * nxy, nxy};
+  c->cm->xchg(c, op, items, ni);
+  c->cur_halo_bytes += (long long)((lo ? 1 : 0) + (hi ? 1 : 0)) * ni * nxy * 8;
+  const int ib = lo ? std::min(1, nzl) : 0, ie = hi ? std::max(ib, nzl - 1) : nzl;
+  bool wrote = false;
+  if (ie > ib) {
+    launch(ib, ie, op->kz2, false);
+    wrote = true;
+  }
+  c->cm->halo_wait(c);
+  if (ib > 0) {
+    launch(0, ib, 1, wrote);
+    wrote = true;
+  }
+  if (ie < nzl) launch(ie, nzl, 1, wrote);
 }
 
 // One two-step pass over the local slab. On a z-slab rank the neighbours' two
