@@ -332,14 +332,14 @@ def run_gpu(args):
                       "true_rel_res": rep.true_rel_res, "converged": rep.converged,
                       "alg_GBps": round(D.sum(rep.alg_bytes) / t / 1e9, 1),
                       "spmv_equiv_GBps": round(rep.matvec * spmv_bytes / t / 1e9, 1)})
+    # DRAM traffic of one launch of the same kernel from the committed ncu capture
+    # (profiles/ncu_traffic_<config>.json, tools/ncu_to_traffic.py), if it matches
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tp):
         with open(tp) as f:
             td = json.load(f)
-        same_kernel = (td.get("kernel", "").startswith("stencil7_cheb2") ==
-                       (step_bytes == 40.0 * n_loc and kind == "stencil"))
-        if td.get("n") == n_loc and same_kernel:
+        if td.get("n") == n_loc and abs(td.get("algorithmic_bytes", 0) - step_bytes) <= 1e-6 * step_bytes:
             traffic = td.get("dram_bytes_per_launch")
 
     cpu = None
