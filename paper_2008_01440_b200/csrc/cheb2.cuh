@@ -43,6 +43,10 @@ constexpr int kC2AX = kC2W, kC2BX = kC2W;
 #ifndef PCGX_C2MINB
 #define PCGX_C2MINB 2
 #endif
+#ifndef PCGX_C2UNROLL
+#define PCGX_C2UNROLL 4
+#endif
+constexpr int kC2Unroll = PCGX_C2UNROLL;             // plane-loop unroll
 constexpr int kC2D = PCGX_C2D;                       // prefetch distance (planes)
 constexpr int kC2NA = kC2D + 2, kC2NB = kC2D, kC2NR = kC2D + 1, kC2NC = 3;
 constexpr int kC2APlane = kC2W * kC2AY;              // 816 doubles = 51 x 128 B
@@ -216,6 +220,7 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
   double2 cm = zero2, cc = zero2;     // stage-2 C centres of planes v-1, v
   double acc = 0.0;
 
+#pragma unroll kC2Unroll
   for (int u = kb - 1; u <= u_last; ++u) {
     mbar_wait(&bars[bslot], bphase);
     const double* Au = pAu;

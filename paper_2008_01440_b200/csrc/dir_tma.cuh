@@ -19,6 +19,10 @@ namespace pcgx {
 
 constexpr int kDirNS = 6;                 // z / p_old ring slots (4 planes ahead)
 constexpr int kDirNC = 3;                 // p_new planes
+#ifndef PCGX_DIRUNROLL
+#define PCGX_DIRUNROLL 2
+#endif
+constexpr int kDirUnroll = PCGX_DIRUNROLL; // plane-loop unroll
 constexpr int kDirThreads = kC2Threads;   // one warp per extended row (tile rows + 2 halo rows)
 constexpr size_t kDirSmem =
     sizeof(double) * (size_t)(2 * kDirNS * kC2EStride + kDirNC * kC2BPlane) + 8 * kDirNS + 128;
@@ -93,6 +97,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   int slot = 0;
   unsigned phase = 0;
   int sc = 0;  // p_new ring slot of plane u
+#pragma unroll kDirUnroll
   for (int u = kb - 1; u <= ke; ++u) {
     // the x pair of plane u-1 (deferred update below): issued before the waits of
     // this iteration so its latency hides behind them
