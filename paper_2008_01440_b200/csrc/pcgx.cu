@@ -1341,8 +1341,11 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   const int m = prec.degree();
   const long long n = op->n_local;
   ensure_workspace(c, n, ws_pad_of(op));
+  // CUDA graphs on one GPU; multi-rank solves launch directly by default (the
+  // speculative schedule hides the launches either way; PCGX_GRAPH_MULTI=1 captures
+  // the NCCL plane exchanges and all-reduces into the graphs too)
   const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && env_int("PCGX_NO_GRAPH", 0) == 0 &&
-                         (!c->cm || c->cm->graph_capturable());
+                         (!c->cm || (c->cm->graph_capturable() && env_int("PCGX_GRAPH_MULTI", 0) != 0));
   // one GPU: snapshot r'r right after the update and overlap the host check with
   // the speculative P r; multi-GPU: merge [r'r, r'z] into one all-reduce after P r
   // (PCGX_MERGED=1 forces the multi-GPU schedule on one GPU, for tests)

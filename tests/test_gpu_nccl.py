@@ -1,7 +1,8 @@
 # SPDX-License-Identifier: Apache-2.0
 """The NCCL communicator path on one GPU: a 1-rank dist context with
 PCGX_FORCE_NCCL=1 routes every all-reduce through NCCL (loaded at run time from
-the process's libnccl.so.2), inside the per-iteration CUDA graphs, with the
+the process's libnccl.so.2), launched directly (the multi-rank default) or inside
+the per-iteration CUDA graphs (PCGX_GRAPH_MULTI=1), with the
 multi-GPU schedule (PCGX_MERGED=1: merged [r'r, r'z] all-reduce, scalar snapshot
 taken by an external event node inside the graph)."""
 import numpy as np
@@ -14,11 +15,13 @@ pytestmark = pytest.mark.gpu
 SEED = 20240801
 
 
+@pytest.mark.parametrize("graphs", ["0", "1"])
 @pytest.mark.parametrize("m", [-1, 0, 4, 10])
-def test_nccl_one_rank_solve(pcgx, oracle, m, monkeypatch):
+def test_nccl_one_rank_solve(pcgx, oracle, m, graphs, monkeypatch):
     P = pcgx
     monkeypatch.setenv("PCGX_FORCE_NCCL", "1")
     monkeypatch.setenv("PCGX_MERGED", "1")
+    monkeypatch.setenv("PCGX_GRAPH_MULTI", graphs)  # multi-rank default: direct launches
     nid = P.Context.nccl_unique_id()
     with P.Context(0, nranks=1, rank=0, nccl_id=nid, dist=True) as ctx:
         assert ctx.nranks == 1
