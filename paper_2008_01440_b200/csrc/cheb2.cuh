@@ -168,6 +168,7 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
   mbar_wait(&bars[kC2D], 0);
 
   const double d = p.d;
+  const double inv_t = 1.0 / p.theta;  // RN(1/theta): quotients by theta via div_rn
   const double2 zero2 = make_double2(0.0, 0.0);
   const int col = 2 * lane + 2;                    // smem column of the lane's pair
   const int gi = i0 + 2 * lane;                    // global i of the pair's first point
@@ -243,8 +244,8 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
         const double y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
         const double y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
         if (kFirst) {
-          cv.x = p.c1 * ((2.0 * ac.x) - (y0 / p.theta));
-          cv.y = p.c1 * ((2.0 * ac.y) - (y1 / p.theta));
+          cv.x = p.c1 * ((2.0 * ac.x) - div_rn(y0, p.theta, inv_t));
+          cv.y = p.c1 * ((2.0 * ac.y) - div_rn(y1, p.theta, inv_t));
         } else {
           const double2 bb = *reinterpret_cast<const double2*>(Bu + offB1);
           const double2 rr = *reinterpret_cast<const double2*>(Ru + offB1);
@@ -281,7 +282,7 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
         double2 rv, xo;
         if (kFirst) {
           rv = av;  // A == R == r
-          xo = make_double2(av.x / p.theta, av.y / p.theta);  // x_0 = r / theta
+          xo = make_double2(div_rn(av.x, p.theta, inv_t), div_rn(av.y, p.theta, inv_t));  // x_0 = r / theta
         } else {
           rv = *reinterpret_cast<const double2*>(pRm + offC2);  // R[v]
           xo = av;  // x_{k-1}
@@ -300,7 +301,7 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
         const double y = stencil_point(d, in_z(u - 1) ? pAm[offAh] : 0.0, Au[offAh - kC2W],
                                        Au[offAh - 1], xc, Au[offAh + 1], Au[offAh + kC2W],
                                        has_p ? Ap[offAh] : 0.0);
-        if (kFirst) cx = p.c1 * ((2.0 * xc) - (y / p.theta));
+        if (kFirst) cx = p.c1 * ((2.0 * xc) - div_rn(y, p.theta, inv_t));
         else cx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * Bu[offBh])) + p.c2 * (Ru[offBh] - y));
       }
       Cu[offBh] = cx;

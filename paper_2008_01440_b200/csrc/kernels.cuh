@@ -25,6 +25,19 @@
 
 namespace pcgx {
 
+// x / b, correctly rounded, from inv = RN(1/b): Markstein's FMA correction
+// (q0 = RN(x inv), r = x - q0 b exactly, q = RN(q0 + r inv) = RN(x / b) for normal
+// operands away from over/underflow) — the reference's IEEE quotient without the
+// iterative division sequence. Zero, tiny, huge and non-finite x take the IEEE
+// division (a real branch, never taken on the solver's data).
+__device__ __forceinline__ double div_rn(double x, double b, double inv) {
+  const double ax = fabs(x);
+  if (!(ax > 0x1p-960 && ax < 0x1p960)) return x / b;
+  const double q0 = x * inv;
+  const double r = __fma_rn(-q0, b, x);
+  return __fma_rn(r, inv, q0);
+}
+
 // ----------------------------------------------------------------- reduction
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -250,11 +263,12 @@ struct EpiResid {
 struct EpiChebFirst {
   double* __restrict__ xout;
   double theta, c1;
+  double inv;  // RN(1 / theta)
   __device__ __forceinline__ void pf(long long) const {}
   __device__ __forceinline__ void ld(long long, double (&)[2]) const {}
   __device__ __forceinline__ void ld2(long long, double2 (&)[2]) const {}
   __device__ __forceinline__ double f(double y, double xc) const {
-    return c1 * ((2.0 * xc) - (y / theta));
+    return c1 * ((2.0 * xc) - div_rn(y, theta, inv));
   }
   __device__ __forceinline__ double st(long long idx, double y, double xc, const double (&)[2]) const {
     const double xn = f(y, xc);
@@ -280,6 +294,7 @@ struct EpiChebStep {
   double* out;
   double rk, rk1, c2, c3, theta;
   int xold_from_r;
+  double inv;  // RN(1 / theta)
   __device__ __forceinline__ void pf(long long idx) const {
     prefetch_l2(r + idx);
     if (!xold_from_r) prefetch_l2(xold + idx);
@@ -293,7 +308,7 @@ struct EpiChebStep {
     v[1] = xold_from_r ? make_double2(0.0, 0.0) : pcgx::ld2(xold + idx);
   }
   __device__ __forceinline__ double f(double y, double xc, double ri, double xo_in) const {
-    const double xo = xold_from_r ? (ri / theta) : xo_in;
+    const double xo = xold_from_r ? div_rn(ri, theta, inv) : xo_in;
     const double z = c2 * (ri - y);
     return rk * (((c3 * xc) - (rk1 * xo)) + z);
   }
@@ -1034,6 +1049,7 @@ update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
               const double* __restrict__ p, const double* __restrict__ q, const double* S,
               int s_rho, int s_pq, Reduce red, int zmode, double theta, double* __restrict__ z) {
   const double alpha = S[s_rho] / S[s_pq];
+  const double inv = 1.0 / theta;  // RN(1/theta), as on the host
   double acc = 0.0, acc2 = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -1042,7 +1058,7 @@ update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
     r[i] = ri;
     acc = acc + ri * ri;
     if (zmode == 1) {
-      const double zi = ri / theta;
+      const double zi = div_rn(ri, theta, inv);
       z[i] = zi;
       acc2 = acc2 + ri * zi;
     } else if (zmode == 2) {
@@ -1061,6 +1077,7 @@ update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
                const double2* __restrict__ p, const double2* __restrict__ q, const double* S,
                int s_rho, int s_pq, Reduce red, double theta, double2* __restrict__ z) {
   const double alpha = S[s_rho] / S[s_pq];
+  const double inv = 1.0 / theta;  // RN(1/theta), as on the host
   double acc = 0.0, acc2 = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
        i += (long long)gridDim.x * blockDim.x) {
@@ -1079,7 +1096,7 @@ update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
     acc = acc + ri.x * ri.x;
     acc = acc + ri.y * ri.y;
     if (kZ == 1) {
-      const double2 zi = make_double2(ri.x / theta, ri.y / theta);
+      const double2 zi = make_double2(div_rn(ri.x, theta, inv), div_rn(ri.y, theta, inv));
       z[i] = zi;
       acc2 = acc2 + ri.x * zi.x;
       acc2 = acc2 + ri.y * zi.y;
@@ -1119,11 +1136,12 @@ pupdate_kernel(long long n, double* __restrict__ pnew, const double* __restrict_
 __global__ void __launch_bounds__(kVecThreads)
 zr_kernel(long long n, double* __restrict__ z, const double* __restrict__ r, double theta,
           int divide, Reduce red) {
+  const double inv = 1.0 / theta;
   double acc = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const double ri = r[i];
-    const double zi = divide ? ri / theta : ri;
+    const double zi = divide ? div_rn(ri, theta, inv) : ri;
     z[i] = zi;
     acc = acc + ri * zi;
   }

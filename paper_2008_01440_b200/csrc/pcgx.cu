@@ -1033,7 +1033,7 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
   const double c2 = 2.0 / P.delta;
   const double c3 = 2.0 * P.sigma;
   if (P.m == 1) {
-    EpiChebFirst e{out, P.theta, c1};
+    EpiChebFirst e{out, P.theta, c1, 1.0 / P.theta};
     if (rz_slot >= 0) op_launch<EpiChebFirst, true>(c, op, r, e, rz_slot);
     else op_launch<EpiChebFirst, false>(c, op, r, e, -1);
     return;
@@ -1078,20 +1078,21 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
       icur = fe;
     }
     if (k == P.m) {  // odd remainder: x_m = step(x_{m-1}, x_{m-2}) -> out
-      EpiChebStep e{r, bufs[iold], out, P.rho[k], P.rho[k - 1], c2, c3, P.theta, 0};
+      EpiChebStep e{r, bufs[iold], out, P.rho[k], P.rho[k - 1], c2, c3, P.theta, 0, 1.0 / P.theta};
       if (rz_slot >= 0) op_launch<EpiChebStep, true>(c, op, bufs[icur], e, rz_slot);
       else op_launch<EpiChebStep, false>(c, op, bufs[icur], e, -1);
     }
     return;
   }
-  EpiChebFirst e1{c->w1, P.theta, c1};
+  EpiChebFirst e1{c->w1, P.theta, c1, 1.0 / P.theta};
   op_launch<EpiChebFirst, false>(c, op, r, e1, -1);
   double* cur = c->w1;  // x_{k-1}
   double* old = c->w0;  // x_{k-2} (not yet materialised at k == 2)
   for (int k = 2; k <= P.m; ++k) {
     const bool last = (k == P.m);
     double* dst = last ? out : old;
-    EpiChebStep e{r, old, dst, P.rho[k], P.rho[k - 1], c2, c3, P.theta, k == 2 ? 1 : 0};
+    EpiChebStep e{r, old, dst, P.rho[k], P.rho[k - 1], c2, c3, P.theta, k == 2 ? 1 : 0,
+                  1.0 / P.theta};
     if (last && rz_slot >= 0) op_launch<EpiChebStep, true>(c, op, cur, e, rz_slot);
     else op_launch<EpiChebStep, false>(c, op, cur, e, -1);
     old = cur;
@@ -1632,7 +1633,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
       q.outC = c->w2;
       q.outE = c->w3;
     }
-    EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0};
+    EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0,
+                  1.0 / P.theta};
     auto launch = [&] {
       if (two) cheb2_pass<false, false>(c, op, c->w1, c->w0, r, q, -1);
       else op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);
