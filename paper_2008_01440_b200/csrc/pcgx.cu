@@ -1926,9 +1926,6 @@ void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::
     start[(size_t)q] = z0;
   }
   start[(size_t)P] = n;
-  auto owner = [&](long long col) {
-    return (int)(std::upper_bound(start.begin(), start.end(), col) - start.begin()) - 1;
-  };
   const long long r0 = start[(size_t)me], r1 = start[(size_t)me + 1], nloc = r1 - r0;
   if (nloc < 1) fail(PCGX_ERR_INVALID, "csr_create: fewer rows than ranks");
   // ghost columns of my rows, ascending (hence grouped by owner)
