@@ -66,15 +66,28 @@ def command(extra=()):
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if force or _stale():
-        cmd = command()
-        if verbose:
-            print(" ".join(cmd), file=sys.stderr)
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError("libpcgx build failed:\n" + res.stdout + res.stderr)
-        if verbose and res.stderr:
-            print(res.stderr, file=sys.stderr)
+    if not (force or _stale()):
+        return LIB
+    # one builder at a time (torchrun ranks, pytest workers): the others wait on the
+    # lock and then find the library fresh
+    import fcntl
+    with open(os.path.join(PKG, ".build.lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if force or _stale():
+                cmd = command()
+                if verbose:
+                    print(" ".join(cmd), file=sys.stderr)
+                tmp = LIB + f".tmp{os.getpid()}"
+                cmd[cmd.index("-o") + 1] = tmp
+                res = subprocess.run(cmd, capture_output=True, text=True)
+                if res.returncode != 0:
+                    raise RuntimeError("libpcgx build failed:\n" + res.stdout + res.stderr)
+                os.replace(tmp, LIB)  # atomic: a concurrent loader sees the old or the new file
+                if verbose and res.stderr:
+                    print(res.stderr, file=sys.stderr)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
     return LIB
 
 
