@@ -1,6 +1,6 @@
 """One k-degree Chebyshev-PCG solve at NX^3 after a warm-up solve (profiling aid).
 
-    python tools/solve_timeline.py [NX] [K]
+    python tools/solve_timeline.py [NX] [K]      (K < 0: Newton form, nlev = -K)
 Prints the device-timed solve; run under
     ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none
 to get the warm-cache per-launch times of the same solve (the last solve's launches).
@@ -17,7 +17,8 @@ with P.Context(0) as ctx:
     op, _ = P.jacobi_scale(P.StencilOperator(nx), ctx)
     a, b = P.analytic_extremes(3, nx)
     rhs = op.apply(P.random_uniform_vector(nx ** 3, 20240801, ctx=ctx))
-    prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, k, 1.001))
+    prec = (P.NewtonPreconditioner(P.newton_params(a, b, -k, 1.001)) if k < 0 else
+            P.ChebyshevPreconditioner(P.cheb_params(a, b, k, 1.001)))
     x = P.DeviceVector(ctx, nx ** 3)
     for i in range(3):
         l0 = ctx.kernel_launches
