@@ -176,6 +176,13 @@ pcgx_status pcgx_cheb_apply(pcgx_context ctx, pcgx_operator op, const pcgx_cheb*
 pcgx_status pcgx_cheb_apply_device(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* p,
                                    const double* r, double* out);
 
+/* The per-degree-step intermediates of apply_chebyshev (the
+ * parity entry): steps[(j-1)*n .. j*n) = x_j = p_j(A) r for j = 1..m (host
+ * buffers, n = local size). x_j is the degree-j output (the rho prefix does not
+ * depend on m), computed by the device path at every j. */
+pcgx_status pcgx_cheb_apply_steps(pcgx_context ctx, pcgx_operator op, const pcgx_cheb* p,
+                                  const double* r, double* steps);
+
 /* Newton form (polyprec.hpp:22-31): degree 2^nlev - 1, zeta[0..nlev]. */
 typedef struct {
   int nlev;

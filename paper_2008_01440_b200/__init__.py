@@ -14,4 +14,5 @@ from .pcgx import (  # noqa: F401
     pcg_solve, random_uniform_vector, slab_partition, EigOptions, EigResult, power_method,
     dacg_smallest, estimate_bounds, NewtonParams, NewtonPreconditioner, apply_newton,
     newton_params, chi_sequence, ParseError, load_matrix_market, save_matrix_market,
+    apply_chebyshev_steps,
 )

@@ -2716,6 +2716,26 @@ pcgx_status pcgx_cheb_apply(pcgx_context c, pcgx_operator op, const pcgx_cheb* p
   });
 }
 
+pcgx_status pcgx_cheb_apply_steps(pcgx_context c, pcgx_operator op, const pcgx_cheb* p,
+                                  const double* r, double* steps) {
+  return guarded(c, [&] {
+    set_device(c);
+    const long long n = op->n_local;
+    ensure_workspace(c, n, ws_pad_of(op));
+    const Cheb P = cheb_from(p);
+    PCGX_CUDA(cudaMemcpyAsync(c->t0, r, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, c->s));
+    for (int j = 1; j <= P.m; ++j) {
+      Cheb Pj = P;
+      Pj.m = j;
+      Pj.rho.resize((size_t)j + 1);
+      enqueue_cheb(c, op, Pj, c->t0, c->t1, -1);
+      PCGX_CUDA(cudaMemcpyAsync(steps + (size_t)(j - 1) * (size_t)n, c->t1, sizeof(double) * (size_t)n,
+                                cudaMemcpyDeviceToHost, c->s));
+    }
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+  });
+}
+
 pcgx_status pcgx_newton_params(double alpha0, double beta0, int nlev, double scale,
                                double* zeta) {
   std::string msg;

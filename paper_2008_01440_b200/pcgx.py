@@ -138,7 +138,7 @@ SYMBOLS = [
     "pcgx_gen_elast27_fill", "pcgx_newton_params", "pcgx_newton_eval", "pcgx_chi_sequence",
     "pcgx_newton_apply", "pcgx_newton_apply_device", "pcgx_pcg_solve_newton",
     "pcgx_pcg_solve_newton_device", "pcgx_mm_load", "pcgx_mm_load_text", "pcgx_csr_host_free",
-    "pcgx_mm_save", "pcgx_mm_save_text", "pcgx_free_text",
+    "pcgx_mm_save", "pcgx_mm_save_text", "pcgx_free_text", "pcgx_cheb_apply_steps",
 ]
 
 _lib = None
@@ -207,6 +207,7 @@ def lib():
         "pcgx_cheb_eval": (C.c_double, [C.POINTER(_Cheb), C.c_double]),
         "pcgx_cheb_apply": (C.c_int, [ctx, op, C.POINTER(_Cheb), _dp, _dp]),
         "pcgx_cheb_apply_device": (C.c_int, [ctx, op, C.POINTER(_Cheb), C.c_void_p, C.c_void_p]),
+        "pcgx_cheb_apply_steps": (C.c_int, [ctx, op, C.POINTER(_Cheb), _dp, _dp]),
         "pcgx_newton_params": (C.c_int, [C.c_double, C.c_double, C.c_int, C.c_double, _dp]),
         "pcgx_newton_eval": (C.c_double, [C.POINTER(_Newton), C.c_double]),
         "pcgx_chi_sequence": (C.c_int, [C.c_double, C.c_double, C.c_int, _dp]),
@@ -706,6 +707,17 @@ def apply_newton(params: NewtonParams, op: ScaledOperator, r):
         raise InvalidArgument("apply_newton: vector length mismatch")
     out = np.empty(op.local_size())
     _check(lib().pcgx_newton_apply(op.ctx.h, op.h, C.byref(cp), _ptr(r), _ptr(out)), op.ctx.h)
+    return out
+
+
+def apply_chebyshev_steps(params: ChebyshevParams, op: ScaledOperator, r) -> np.ndarray:
+    """Every degree step x_1..x_m of apply_chebyshev (the parity entry): shape (m, n)."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    if r.size != op.local_size():
+        raise InvalidArgument("apply_chebyshev: vector length mismatch")
+    out = np.empty((max(params.m, 0), op.local_size()))
+    cp = params._c()
+    _check(lib().pcgx_cheb_apply_steps(op.ctx.h, op.h, C.byref(cp), _ptr(r), _ptr(out)), op.ctx.h)
     return out
 
 

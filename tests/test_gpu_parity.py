@@ -136,6 +136,26 @@ def test_cheb_apply_per_degree_step_bitwise(P, ctx, golden):
             assert np.array_equal(out, fhs(c["m5_out"]))
 
 
+def test_cheb_apply_steps_entry_bitwise(P, ctx, golden, oracle):
+    """pcgx_cheb_apply_steps: all intermediates x_1..x_m in one call, each bitwise the
+    reference's degree-j output (golden SHA-256) and the oracle's."""
+    for c in golden["apply_chebyshev"]:
+        if "steps" not in c:
+            continue
+        nx = c["nx"]
+        op = stencil(P, ctx, nx)
+        a, b = P.analytic_extremes(3, nx)
+        r = P.random_uniform_vector(nx ** 3, c["r_seed"])
+        mmax = max(st["m"] for st in c["steps"])
+        steps = P.apply_chebyshev_steps(P.cheb_params(a, b, mmax, fh(c["scale"])), op, r)
+        assert steps.shape == (mmax, nx ** 3)
+        for st in c["steps"]:
+            if st["m"] >= 1:
+                assert sha(steps[st["m"] - 1]) == st["sha256"], (nx, st["m"])
+        po = oracle.cheb_params(a, b, 3, fh(c["scale"]))
+        assert np.array_equal(steps[2], oracle.apply_chebyshev(OracleOp("lap3d", nx=nx), po, r))
+
+
 def test_cheb_apply_csr_bitwise(P, ctx, golden):
     g, c = golden["csr_apply"], golden["apply_chebyshev_csr"]
     op = csr(P, ctx, np.array(g["row_ptr"]), np.array(g["col_idx"]), fhs(g["values"]))
