@@ -633,3 +633,20 @@ def test_dir_tma_matches_register_path(P, ctx, oracle, dims, m, monkeypatch):
     assert abs(r1.iters - ro["iters"]) <= 1
     if r1.iters == ro["iters"]:
         assert rel_norm(x1, xo) <= 1e-10
+
+
+@pytest.mark.parametrize("dims", [(33, 17, 9), (7, 5, 3), (65, 9, 12)])
+@pytest.mark.parametrize("m", [0, 3, 8])
+def test_odd_grids_take_the_scalar_paths(P, ctx, oracle, dims, m):
+    """Odd nx (no 16-byte pairs: single-step scalar stencil kernels, InComb
+    direction step, scalar update) and odd n: the same answers as the oracle."""
+    nx, ny, nz = dims
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+    opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
+    rhs = oracle.apply(opo, oracle.random_uniform(nx * ny * nz, SEED))
+    x, rep = P.pcg_solve(stencil(P, ctx, nx, ny, nz), rhs, P.SolveOptions(maxit=5000),
+                         P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001)))
+    xo, ro = oracle.pcg_solve(opo, oracle.cheb_params(a, b, m, 1.001), rhs, maxit=5000)
+    assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
+    if rep.iters == ro["iters"]:
+        assert rel_norm(x, xo) <= 1e-10
