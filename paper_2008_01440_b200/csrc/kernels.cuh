@@ -996,7 +996,20 @@ bsr3_kernel(Bsr3Geom g, In in, Epi epi, Reduce red) {
 // presence mask per row. No column indices: 8 B per stored entry + 4 B per row
 // (vs 12 B per nnz). Terms are taken in ascending offset = ascending column order,
 // only where the mask bit is set, v * (d_c * x_c): bitwise the CSR row sum.
+#ifndef PCGX_DIA_STREAM
+#define PCGX_DIA_STREAM 1
+#endif
 constexpr int kDiaMax = 32;
+// the value stream is read once: keep it out of L1 so the x / d gathers stay there
+__device__ __forceinline__ double ld_stream(const double* p) {
+#if PCGX_DIA_STREAM
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
 
 struct DiaGeom {
   int n, K;
@@ -1027,7 +1040,7 @@ dia_kernel(DiaGeom g, In in, Epi epi, Reduce red) {
     for (int k = 0; k < g.K; ++k) {
       if (msk & (1u << k)) {
         const long long c = i + g.off[k];
-        sum = sum + __ldg(g.val + k * g.ld + i) * (__ldg(g.dvec + c) * in.ldc(c));
+        sum = sum + ld_stream(g.val + k * g.ld + i) * (__ldg(g.dvec + c) * in.ldc(c));
       }
     }
     const double y = sum * dr;
