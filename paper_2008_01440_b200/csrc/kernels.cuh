@@ -38,6 +38,34 @@ __device__ __forceinline__ double div_rn(double x, double b, double inv) {
   return __fma_rn(r, inv, q0);
 }
 
+#ifndef PCGX_DIA_STREAM
+#define PCGX_DIA_STREAM 1
+#endif
+#ifndef PCGX_MAT_STREAM
+#define PCGX_MAT_STREAM 1
+#endif
+// the value stream is read once: keep it out of L1 so the x / d gathers stay there
+__device__ __forceinline__ double ld_stream(const double* p) {
+#if PCGX_DIA_STREAM
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
+// matrix value streams of the SELL / BSR-3 kernels (same policy, separately switchable)
+__device__ __forceinline__ double ld_mat(const double* p) {
+#if PCGX_MAT_STREAM
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 // ----------------------------------------------------------------- reduction
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -879,7 +907,7 @@ sell_kernel(SellGeom g, In in, Epi epi, Reduce red) {
         const bool on = (k + q) < len;
         const long long e = base + (long long)(k + q) * 32;
         const int c = on ? __ldg(g.col + e) : 0;
-        vv[q] = on ? __ldg(g.val + e) : 0.0;
+        vv[q] = on ? ld_mat(g.val + e) : 0.0;
         dv[q] = on ? __ldg(g.dvec + c) : 0.0;  // dvec spans the ghost columns too
         xv[q] = on ? in.ldc(c) : 0.0;
       }
@@ -958,7 +986,7 @@ bsr3_kernel(Bsr3Geom g, In in, Epi epi, Reduce red) {
         const int J = on ? __ldg(g.bcol + slot + lane) : 0;
         const double* vp = g.val + slot * 9 + lane;
 #pragma unroll
-        for (int e = 0; e < 9; ++e) v[q][e] = on ? __ldg(vp + 32 * e) : 0.0;
+        for (int e = 0; e < 9; ++e) v[q][e] = on ? ld_mat(vp + 32 * e) : 0.0;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           const long long cidx = 3LL * J + d;
@@ -996,20 +1024,7 @@ bsr3_kernel(Bsr3Geom g, In in, Epi epi, Reduce red) {
 // presence mask per row. No column indices: 8 B per stored entry + 4 B per row
 // (vs 12 B per nnz). Terms are taken in ascending offset = ascending column order,
 // only where the mask bit is set, v * (d_c * x_c): bitwise the CSR row sum.
-#ifndef PCGX_DIA_STREAM
-#define PCGX_DIA_STREAM 1
-#endif
 constexpr int kDiaMax = 32;
-// the value stream is read once: keep it out of L1 so the x / d gathers stay there
-__device__ __forceinline__ double ld_stream(const double* p) {
-#if PCGX_DIA_STREAM
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-#else
-  return __ldg(p);
-#endif
-}
 
 struct DiaGeom {
   int n, K;
