@@ -55,6 +55,49 @@ __device__ __forceinline__ double ld_stream(const double* p) {
 #endif
 }
 
+// epilogue operand streams (r, x_old, b: read once per point)
+#ifndef PCGX_EPI_STREAM
+#define PCGX_EPI_STREAM 1
+#endif
+__device__ __forceinline__ double ld_epi(const double* p) {
+#if PCGX_EPI_STREAM
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double2 ld_epi2(const double* p) {
+#if PCGX_EPI_STREAM
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#else
+  return __ldg(reinterpret_cast<const double2*>(p));
+#endif
+}
+
+// ... for a stream the same kernel later overwrites in place (coherent path, no .nc)
+__device__ __forceinline__ double ld_epi_rw(const double* p) {
+#if PCGX_EPI_STREAM
+  double v;
+  asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ double2 ld_epi_rw2(const double* p) {
+#if PCGX_EPI_STREAM
+  double2 v;
+  asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#else
+  return *reinterpret_cast<const double2*>(p);
+#endif
+}
+
 // matrix value streams of the SELL / BSR-3 kernels (same policy, separately switchable)
 __device__ __forceinline__ double ld_mat(const double* p) {
 #if PCGX_MAT_STREAM
@@ -269,8 +312,8 @@ struct EpiResid {
   const double* __restrict__ b;
   double* e;  // may be nullptr (true residual: only the norm is needed)
   __device__ __forceinline__ void pf(long long idx) const { prefetch_l2(b + idx); }
-  __device__ __forceinline__ void ld(long long idx, double (&v)[2]) const { v[0] = __ldg(b + idx); }
-  __device__ __forceinline__ void ld2(long long idx, double2 (&v)[2]) const { v[0] = ldg2(b + idx); }
+  __device__ __forceinline__ void ld(long long idx, double (&v)[2]) const { v[0] = ld_epi(b + idx); }
+  __device__ __forceinline__ void ld2(long long idx, double2 (&v)[2]) const { v[0] = ld_epi2(b + idx); }
   __device__ __forceinline__ double st(long long idx, double y, double, const double (&v)[2]) const {
     const double ei = v[0] - y;
     if (e) e[idx] = ei;
@@ -328,12 +371,12 @@ struct EpiChebStep {
     if (!xold_from_r) prefetch_l2(xold + idx);
   }
   __device__ __forceinline__ void ld(long long idx, double (&v)[2]) const {
-    v[0] = __ldg(r + idx);
-    v[1] = xold_from_r ? 0.0 : xold[idx];
+    v[0] = ld_epi(r + idx);
+    v[1] = xold_from_r ? 0.0 : ld_epi_rw(xold + idx);
   }
   __device__ __forceinline__ void ld2(long long idx, double2 (&v)[2]) const {
-    v[0] = ldg2(r + idx);
-    v[1] = xold_from_r ? make_double2(0.0, 0.0) : pcgx::ld2(xold + idx);
+    v[0] = ld_epi2(r + idx);
+    v[1] = xold_from_r ? make_double2(0.0, 0.0) : ld_epi_rw2(xold + idx);
   }
   __device__ __forceinline__ double f(double y, double xc, double ri, double xo_in) const {
     const double xo = xold_from_r ? div_rn(ri, theta, inv) : xo_in;
