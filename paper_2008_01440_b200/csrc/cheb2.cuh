@@ -110,19 +110,30 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 // grid: (ceil(nx/64), ceil(ny/8), ceil(nzl/kz)); block: 320 threads; dynamic smem kC2Smem.
 //
 // Stage 1: warp w owns extended row w (tile row w-1); lane l owns the point
-// pair tile-i (2l, 2l+1). Stage 2: warp w < 8 owns tile row w, lane l the pair
-// (2l, 2l+1); meanwhile warps 8 and 9 compute the two halo columns (tile-i -1
-// and 64) of C for the plane stage 1 just produced (they are first read by
-// stage 2 one iteration later). The k-1 / k+1 neighbours of the pairs live in
-// per-lane register queues, i-1 / i+1 come by shuffle, only j-1 / j+1 and the
-// operands are read from shared memory (16-byte LDS). Ring slots rotate by
-// one per plane and are tracked with incremented indices (no modulo).
-template <bool kFirst, bool kRed>
+// pair tile-i (2l, 2l+1). The k-1 / k+1 neighbours of the pairs live in per-lane
+// register queues, i-1 / i+1 come by shuffle, only j-1 / j+1 and the operands
+// are read from shared memory (16-byte LDS). Ring slots rotate by one per plane
+// and are tracked with incremented indices (no modulo).
+//
+// Stage 2 (kV = 0): warp w < 8 owns tile row w, reading its C centre, the A and
+// R operands from shared memory; warps 8 and 9 compute the two halo columns
+// (tile-i -1 and 64) of C for the plane stage 1 just produced (first read by
+// stage 2 one iteration later).
+// Stage 2 (kV >= 1, "own row"): warp w in 1..8 computes E for the row it produced
+// in stage 1, so the C centre queue (k-1, k, k+1), x_{k-1} and the i-neighbours
+// are its own registers; only C's j +- 1 rows come from shared memory. Warps 0
+// and 9 (the j-halo rows) compute the halo columns.
+// kV = 2 additionally keeps t = d * x instead of x in the stencil queues and in
+// the C ring: each product d * x is formed once per point instead of once per
+// use (7x), so a stencil costs 1-3 DMUL + 7 DADD instead of 9 DMUL + 7 DADD; the
+// IEEE products are the same, hence bitwise the same sums.
+template <bool kFirst, bool kRed, int kV>
 __global__ void __launch_bounds__(kC2Threads, PCGX_C2MINB)
 stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 box)
                       const __grid_constant__ CUtensorMap mapB,  // B (68 x 10 box)
                       const __grid_constant__ CUtensorMap mapR,  // R (68 x 10 box)
                       Cheb2Params p, int k_begin, int k_end, int kz, Reduce red) {
+  constexpr bool kOwn = kV >= 1, kT = kV >= 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 128-byte aligned base, kept as a shared-space pointer (LDS, not generic LD)
   double* sA = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
@@ -181,17 +192,18 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
   const int offB1 = warp * kC2W + col;             // B/R/C offset of the pair
   const bool c_interior = warp >= 1 && warp <= kC2TY;
   double* gC = p.outC + (long long)gj1 * p.nx + gi;  // + u * nxy
-  // stage 2 (tile row `warp` for warps 0..7)
-  const bool stage2 = warp < kC2TY;
-  const int gj2 = j0 + warp;
+  // stage 2: tile row `warp` for warps 0..7 (kV = 0) or own row for warps 1..8
+  const bool stage2 = kOwn ? c_interior : warp < kC2TY;
+  const int gj2 = kOwn ? gj1 : j0 + warp;
   const bool do2 = stage2 && gj2 < p.ny && pair_in;
-  const int offC2 = (warp + 1) * kC2W + col;
-  const int offA2 = (warp + 2) * kC2W + col;
+  const int offC2 = kOwn ? offB1 : (warp + 1) * kC2W + col;
+  const int offA2 = kOwn ? offA1 : (warp + 2) * kC2W + col;
   double* gE = p.outE + (long long)gj2 * p.nx + gi;  // + v * nxy
-  // halo columns (warps 8, 9, lanes 0..9): column tile-i -1 (warp 8) or 64 (warp 9)
-  const bool do_h = warp >= kC2TY && lane < kC2BY;
-  const int hcol = warp == kC2TY ? 1 : kC2TX + 2;
-  const int hgi = warp == kC2TY ? i0 - 1 : i0 + kC2TX;
+  // halo columns (lanes 0..9 of two warps): column tile-i -1 or 64
+  const int hw0 = kOwn ? 0 : kC2TY, hw1 = kOwn ? kC2TY + 1 : kC2TY + 1;
+  const bool do_h = (warp == hw0 || warp == hw1) && lane < kC2BY;
+  const int hcol = warp == hw0 ? 1 : kC2TX + 2;
+  const int hgi = warp == hw0 ? i0 - 1 : i0 + kC2TX;
   const int hgj = j0 - 1 + lane;
   const bool h_in = do_h && hgi >= 0 && hgi < p.nx && hgj >= 0 && hgj < p.ny;
   const int offAh = (lane + 1) * kC2W + hcol, offBh = lane * kC2W + hcol;
@@ -216,9 +228,16 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
   double* gCu = gC + (long long)(kb - 1) * p.nxy;  // this lane's C pair at plane u
   double* gEv = gE + (long long)(kb - 2) * p.nxy;  // this lane's E pair at plane u-1
 
+  auto mul2 = [&](double2 v) { return make_double2(d * v.x, d * v.y); };
+  // stage-1 queue: A (x, or t = d x when kT) of planes u-1, u
   double2 am = in_z(kb - 2) ? *reinterpret_cast<const double2*>(sA + offA1) : zero2;
   double2 ac = in_z(kb - 1) ? *reinterpret_cast<const double2*>(sA + kC2APlane + offA1) : zero2;
-  double2 cm = zero2, cc = zero2;     // stage-2 C centres of planes v-1, v
+  if (kT) {
+    am = mul2(am);
+    ac = mul2(ac);
+  }
+  double2 cm = zero2, cc = zero2;     // stage-2 C (x, or t when kT) of planes v-1, v
+  double2 cx = zero2;                 // kT: C x of plane v (own row)
   double acc = 0.0;
 
 #pragma unroll kC2Unroll
@@ -231,32 +250,44 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
     double* Cu = pCu;
     const bool plane_in = u >= p.c_lo && u < p.c_hi, has_p = in_z(u + 1);
     // ---------------- stage 1: C[u] pairs of the extended tile
+    double2 ap, cv = zero2;
     {
-      const double2 ap = has_p ? *reinterpret_cast<const double2*>(Ap + offA1) : zero2;
+      ap = has_p ? *reinterpret_cast<const double2*>(Ap + offA1) : zero2;
+      if (kT) ap = mul2(ap);
       double aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
       double ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
-      if (lane == 0) aw = Au[offA1 - 1];
-      if (lane == 31) ae = Au[offA1 + 2];
-      double2 cv = zero2;
+      if (lane == 0) aw = kT ? d * Au[offA1 - 1] : Au[offA1 - 1];
+      if (lane == 31) ae = kT ? d * Au[offA1 + 2] : Au[offA1 + 2];
       if (plane_in && do1) {
         const double2 as = *reinterpret_cast<const double2*>(Au + offA1 - kC2W);
         const double2 an = *reinterpret_cast<const double2*>(Au + offA1 + kC2W);
-        const double y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
-        const double y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
+        double y0, y1;
+        double2 xc;
+        if (kT) {
+          xc = *reinterpret_cast<const double2*>(Au + offA1);
+          y0 = stencil_point_t(d, am.x, d * as.x, aw, ac.x, ac.y, d * an.x, ap.x);
+          y1 = stencil_point_t(d, am.y, d * as.y, ac.x, ac.y, ae, d * an.y, ap.y);
+        } else {
+          xc = ac;
+          y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
+          y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
+        }
         if (kFirst) {
-          cv.x = p.c1 * ((2.0 * ac.x) - div_rn(y0, p.theta, inv_t));
-          cv.y = p.c1 * ((2.0 * ac.y) - div_rn(y1, p.theta, inv_t));
+          cv.x = p.c1 * ((2.0 * xc.x) - div_rn(y0, p.theta, inv_t));
+          cv.y = p.c1 * ((2.0 * xc.y) - div_rn(y1, p.theta, inv_t));
         } else {
           const double2 bb = *reinterpret_cast<const double2*>(Bu + offB1);
           const double2 rr = *reinterpret_cast<const double2*>(Ru + offB1);
-          cv.x = p.rk1 * (((p.c3 * ac.x) - (p.rk1m1 * bb.x)) + p.c2 * (rr.x - y0));
-          cv.y = p.rk1 * (((p.c3 * ac.y) - (p.rk1m1 * bb.y)) + p.c2 * (rr.y - y1));
+          cv.x = p.rk1 * (((p.c3 * xc.x) - (p.rk1m1 * bb.x)) + p.c2 * (rr.x - y0));
+          cv.y = p.rk1 * (((p.c3 * xc.y) - (p.rk1m1 * bb.y)) + p.c2 * (rr.y - y1));
         }
         if (c_interior && u >= kb && u < ke) st2(gCu, cv.x, cv.y);
       }
-      *reinterpret_cast<double2*>(Cu + offB1) = cv;
-      am = ac;
-      ac = ap;
+      *reinterpret_cast<double2*>(Cu + offB1) = kT ? mul2(cv) : cv;
+      if (!kOwn) {
+        am = ac;
+        ac = ap;
+      }
     }
     __syncthreads();
     // Refill the ring slots of unit u-1 with unit u-1+D: every warp is past
@@ -264,11 +295,13 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
     // R[u-2]. This is the only block barrier of the iteration: a warp runs on
     // from its stage 2 of u into stage 1 of u+1 without waiting for the others.
     if (tid == 0 && u >= kb && u - 1 + kC2D <= u_last) issue_unit(u - 1 + kC2D);
-    // ---------------- stage 2: E[u-1] on the tile (warps 0..7) | halo columns of C[u] (warps 8, 9)
+    // ---------------- stage 2: E[u-1] on the tile | halo columns of C[u]
     if (stage2) {
       const int v = u - 1;
-      const double2 cp = *reinterpret_cast<const double2*>(Cu + offC2);
       const double* Cv = pCm;
+      double2 cp;  // C (x or t) of plane v+1 = u
+      if (kOwn) cp = kT ? mul2(cv) : cv;
+      else cp = *reinterpret_cast<const double2*>(Cu + offC2);
       double cw = __shfl_up_sync(0xffffffffu, cc.y, 1);
       double ce = __shfl_down_sync(0xffffffffu, cc.x, 1);
       if (lane == 0) cw = Cv[offC2 - 1];
@@ -276,9 +309,19 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
       if (v >= kb && do2) {
         const double2 cs = *reinterpret_cast<const double2*>(Cv + offC2 - kC2W);
         const double2 cn = *reinterpret_cast<const double2*>(Cv + offC2 + kC2W);
-        const double y0 = stencil_point(d, cm.x, cs.x, cw, cc.x, cc.y, cn.x, cp.x);
-        const double y1 = stencil_point(d, cm.y, cs.y, cc.x, cc.y, ce, cn.y, cp.y);
-        const double2 av = *reinterpret_cast<const double2*>(pAm + offA2);  // A[v] = A[u-1]
+        double y0, y1;
+        double2 ccx;
+        if (kT) {
+          y0 = stencil_point_t(d, cm.x, cs.x, cw, cc.x, cc.y, cn.x, cp.x);
+          y1 = stencil_point_t(d, cm.y, cs.y, cc.x, cc.y, ce, cn.y, cp.y);
+          ccx = cx;
+        } else {
+          y0 = stencil_point(d, cm.x, cs.x, cw, cc.x, cc.y, cn.x, cp.x);
+          y1 = stencil_point(d, cm.y, cs.y, cc.x, cc.y, ce, cn.y, cp.y);
+          ccx = cc;
+        }
+        // A[v] = A[u-1]: the stage-1 queue's previous centre (own row, x only)
+        const double2 av = (kOwn && !kT) ? am : *reinterpret_cast<const double2*>(pAm + offA2);
         double2 rv, xo;
         if (kFirst) {
           rv = av;  // A == R == r
@@ -287,24 +330,29 @@ stencil7_cheb2_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 b
           rv = *reinterpret_cast<const double2*>(pRm + offC2);  // R[v]
           xo = av;  // x_{k-1}
         }
-        const double e0 = p.rk2 * (((p.c3 * cc.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
-        const double e1 = p.rk2 * (((p.c3 * cc.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
+        const double e0 = p.rk2 * (((p.c3 * ccx.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
+        const double e1 = p.rk2 * (((p.c3 * ccx.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
         st2(gEv, e0, e1);
         if (kRed) acc = acc + (rv.x * e0 + rv.y * e1);
       }
       cm = cc;
       cc = cp;
+      if (kT) cx = cv;
     } else if (do_h) {
-      double cx = 0.0;
+      double hx = 0.0;
       if (plane_in && h_in) {
         const double xc = Au[offAh];
         const double y = stencil_point(d, in_z(u - 1) ? pAm[offAh] : 0.0, Au[offAh - kC2W],
                                        Au[offAh - 1], xc, Au[offAh + 1], Au[offAh + kC2W],
                                        has_p ? Ap[offAh] : 0.0);
-        if (kFirst) cx = p.c1 * ((2.0 * xc) - div_rn(y, p.theta, inv_t));
-        else cx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * Bu[offBh])) + p.c2 * (Ru[offBh] - y));
+        if (kFirst) hx = p.c1 * ((2.0 * xc) - div_rn(y, p.theta, inv_t));
+        else hx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * Bu[offBh])) + p.c2 * (Ru[offBh] - y));
       }
-      Cu[offBh] = cx;
+      Cu[offBh] = kT ? d * hx : hx;
+    }
+    if (kOwn) {
+      am = ac;
+      ac = ap;
     }
     // rotate the rings and global pointers by one plane
     pAm = pAu;

@@ -1,0 +1,247 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Software-pipelined variant of the two-step Chebyshev pass (cheb2.cuh): the
+// same two fused degree steps per HBM pass, the same tile, TMA boxes and
+// per-point arithmetic (bitwise identical outputs), but iteration t of the plane
+// loop computes stage 1 of plane t AND stage 2 of plane t-2 between the same pair
+// of block barriers. The two stages are independent there (stage 2 of t-2 reads
+// C[t-3..t-1], all complete at the previous barrier), so each lane carries four
+// independent stencil + recurrence dependency chains instead of two: ncu showed
+// the two-step kernel stalled mostly on fixed-latency fp64 dependencies ("wait")
+// and barriers, not on HBM.
+//
+// Stage 2 is computed by the warp that produced the row in stage 1 ("own row":
+// warps 1..8; warps 0 and 9 own the j-halo rows and compute the two i-halo
+// columns of C), so the C centres of planes t-3, t-2, t-1 are registers; only
+// C's j +- 1 rows and the lane-0/31 i-neighbours come from the C ring.
+//
+// Rings (D = prefetch distance in planes, load unit u = A[u+1], B[u], R[u]):
+// A holds planes t-1 .. t+D (D+2 slots; A[t-2] of stage 2 is a register), B
+// t .. t+D-1 (D), R t-2 .. t+D-1 (D+2), C t-2 .. t (3). The refill of unit
+// t-1+D is issued at the top of iteration t: the slots it overwrites (A[t-2],
+// B[t-1], R[t-3]) were last read in iteration t-1, before its closing barrier.
+#pragma once
+
+#include "cheb2.cuh"
+
+namespace pcgx {
+
+// Three CTAs (30 warps) per SM: <= 64 registers and <= 74 KB of rings, hence a
+// prefetch distance of two planes (measured: +7% over two CTAs with D = 4).
+#ifndef PCGX_C2FD
+#define PCGX_C2FD 2
+#endif
+#ifndef PCGX_C2FMINB
+#define PCGX_C2FMINB 3
+#endif
+constexpr int kFD = PCGX_C2FD;
+constexpr int kFNA = kFD + 2, kFNB = kFD, kFNR = kFD + 2, kFNC = 3;
+constexpr size_t kC2FSmem = sizeof(double) * (size_t)(kFNA * kC2APlane + (kFNB + kFNR) * kC2EStride +
+                                                      kFNC * kC2CStride) +
+                            16 * (kFD + 1) + 128;
+
+// z-chunking of a launch: chunk c covers planes [k_begin + start[c], k_begin + start[c+1]).
+// Chunks are dispatched chunk-major (all tiles of chunk 0 first), so the CTAs in
+// flight are neighbouring tiles at similar z and their halo re-reads hit L2;
+// the host shrinks the last chunks so the final wave ends evenly.
+struct ChunkPlan {
+  static constexpr int kMax = 48;
+  int n;
+  int start[kMax + 1];
+};
+
+template <bool kFirst, bool kRed>
+__global__ void __launch_bounds__(kC2Threads, PCGX_C2FMINB)
+stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 box)
+                       const __grid_constant__ CUtensorMap mapB,  // B (68 x 10 box)
+                       const __grid_constant__ CUtensorMap mapR,  // R (68 x 10 box)
+                       Cheb2Params p, int k_begin, int k_end, const __grid_constant__ ChunkPlan plan, Reduce red) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+  double* sB = sA + kFNA * kC2APlane;
+  double* sR = sB + kFNB * kC2EStride;
+  double* sC = sR + kFNR * kC2EStride;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kFNC * kC2CStride);  // kFD unit bars + 1 prologue
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned bytesA = kC2APlane * 8, bytesB = kC2BPlane * 8;
+  const int tiles_x = (p.nx + kC2TX - 1) / kC2TX;
+  const int i0 = (int)(blockIdx.x % tiles_x) * kC2TX, j0 = (int)(blockIdx.x / tiles_x) * kC2TY;
+  const int kb = k_begin + plan.start[blockIdx.y];
+  const int ke = min(k_begin + plan.start[blockIdx.y + 1], k_end);
+  if (tid == 0) {
+    for (int q = 0; q <= kFD; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // slot of plane z: A (z - (kb-2)) % NA, B and R (z - (kb-1)) % N, C (z - (kb-1)) % 3
+  auto in_z = [&](int z) { return z >= p.a_lo && z < p.a_hi; };
+  const int zo = p.zoff;
+  auto issue_unit = [&](int u) {
+    uint64_t* bar = &bars[(u - (kb - 1)) % kFD];
+    const bool la = in_z(u + 1), lbr = !kFirst && in_z(u);
+    mbar_expect_tx(bar, (la ? bytesA : 0u) + (lbr ? 2 * bytesB : 0u));
+    if (la) tma_load_3d(sA + ((u + 1 - (kb - 2)) % kFNA) * kC2APlane, &mapA, i0 - 2, j0 - 2, u + 1 + zo, bar);
+    if (lbr) {
+      tma_load_3d(sB + ((u - (kb - 1)) % kFNB) * kC2EStride, &mapB, i0 - 2, j0 - 1, u + zo, bar);
+      tma_load_3d(sR + ((u - (kb - 1)) % kFNR) * kC2EStride, &mapR, i0 - 2, j0 - 1, u + zo, bar);
+    }
+  };
+  const int u_last = ke;  // stage 1 runs t = kb-1 .. ke, stage 2 v = t-2 = kb .. ke-1
+  if (tid == 0) {
+    uint64_t* pb = &bars[kFD];
+    mbar_expect_tx(pb, (in_z(kb - 2) ? bytesA : 0u) + (in_z(kb - 1) ? bytesA : 0u));
+    if (in_z(kb - 2)) tma_load_3d(sA, &mapA, i0 - 2, j0 - 2, kb - 2 + zo, pb);
+    if (in_z(kb - 1)) tma_load_3d(sA + kC2APlane, &mapA, i0 - 2, j0 - 2, kb - 1 + zo, pb);
+    for (int u = kb - 1; u < kb - 1 + kFD && u <= u_last; ++u) issue_unit(u);
+  }
+  mbar_wait(&bars[kFD], 0);
+
+  const double d = p.d;
+  const double inv_t = 1.0 / p.theta;
+  const double2 zero2 = make_double2(0.0, 0.0);
+  const int col = 2 * lane + 2;
+  const int gi = i0 + 2 * lane;
+  const bool pair_in = gi < p.nx;
+  const int gj = j0 - 1 + warp;                    // this warp's (extended) row
+  const bool do1 = gj >= 0 && gj < p.ny && pair_in;
+  const int offA = (warp + 1) * kC2W + col;        // A-box offset of the pair
+  const int offB = warp * kC2W + col;              // B/R/C offset of the pair
+  const bool interior = warp >= 1 && warp <= kC2TY;  // a tile row: stage 2 here
+  const bool do2 = interior && do1;
+  double* gC = p.outC + (long long)gj * p.nx + gi;
+  double* gE = p.outE + (long long)gj * p.nx + gi;
+  // halo columns: warp 0 -> tile-i -1, warp 9 -> tile-i 64; lanes 0..9 = rows
+  const bool do_h = (warp == 0 || warp == kC2TY + 1) && lane < kC2BY;
+  const int hcol = warp == 0 ? 1 : kC2TX + 2;
+  const int hgi = warp == 0 ? i0 - 1 : i0 + kC2TX;
+  const int hgj = j0 - 1 + lane;
+  const bool h_in = do_h && hgi >= 0 && hgi < p.nx && hgj >= 0 && hgj < p.ny;
+  const int offAh = (lane + 1) * kC2W + hcol, offBh = lane * kC2W + hcol;
+
+  const double* const sAend = sA + kFNA * kC2APlane;
+  const double* const sBend = sB + kFNB * kC2EStride;
+  const double* const sRend = sR + kFNR * kC2EStride;
+  const double* pAm = sA;                           // A[t-1]
+  const double* pAu = sA + kC2APlane;               // A[t]
+  const double* pAp = sA + 2 * kC2APlane;           // A[t+1]
+  const double* pBu = sB;                           // B[t]
+  const double* pRu = sR;                           // R[t]
+  const double* pR2 = sR + (kFNR - 2) * kC2EStride; // R[t-2]
+  const double* pR1 = sR + (kFNR - 1) * kC2EStride; // R[t-1]
+  double* pCu = sC;                                 // C[t]
+  double* pC1 = sC + 2 * kC2CStride;                // C[t-1]
+  double* pC2 = sC + kC2CStride;                    // C[t-2]
+  int bslot = 0;
+  unsigned bphase = 0;
+  double* gCt = gC + (long long)(kb - 1) * p.nxy;   // C pair at plane t
+  double* gEv = gE + (long long)(kb - 3) * p.nxy;   // E pair at plane t-2
+
+  double2 am = in_z(kb - 2) ? *reinterpret_cast<const double2*>(sA + offA) : zero2;
+  double2 ac = in_z(kb - 1) ? *reinterpret_cast<const double2*>(sA + kC2APlane + offA) : zero2;
+  double2 a2 = zero2;                          // A[t-2] (own row)
+  double2 c1 = zero2, c2 = zero2, c3 = zero2;  // C[t-1], C[t-2], C[t-3] (own row)
+  double acc = 0.0;
+
+#pragma unroll kC2Unroll
+  for (int t = kb - 1; t <= ke + 1; ++t) {
+    if (tid == 0 && t >= kb && t - 1 + kFD <= u_last) issue_unit(t - 1 + kFD);
+    const bool s1 = t <= ke;
+    double2 ap = zero2, cv = zero2;
+    if (s1) mbar_wait(&bars[bslot], bphase);
+    // ---------------- stage 1: C[t] on the extended tile row
+    if (s1) {
+      const bool plane_in = t >= p.c_lo && t < p.c_hi, has_p = in_z(t + 1);
+      ap = has_p ? *reinterpret_cast<const double2*>(pAp + offA) : zero2;
+      double aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
+      double ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
+      if (lane == 0) aw = pAu[offA - 1];
+      if (lane == 31) ae = pAu[offA + 2];
+      const double2 as = *reinterpret_cast<const double2*>(pAu + offA - kC2W);
+      const double2 an = *reinterpret_cast<const double2*>(pAu + offA + kC2W);
+      const double y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
+      const double y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
+      double2 c;
+      if (kFirst) {
+        c.x = p.c1 * ((2.0 * ac.x) - div_rn(y0, p.theta, inv_t));
+        c.y = p.c1 * ((2.0 * ac.y) - div_rn(y1, p.theta, inv_t));
+      } else {
+        const double2 bb = *reinterpret_cast<const double2*>(pBu + offB);
+        const double2 rr = *reinterpret_cast<const double2*>(pRu + offB);
+        c.x = p.rk1 * (((p.c3 * ac.x) - (p.rk1m1 * bb.x)) + p.c2 * (rr.x - y0));
+        c.y = p.rk1 * (((p.c3 * ac.y) - (p.rk1m1 * bb.y)) + p.c2 * (rr.y - y1));
+      }
+      const bool live = plane_in && do1;
+      if (live) cv = c;
+      if (live && interior && t >= kb && t < ke) st2(gCt, cv.x, cv.y);
+      *reinterpret_cast<double2*>(pCu + offB) = cv;
+      // i-halo columns of C[t] (read by stage 2 of plane t, two iterations on)
+      if (do_h) {
+        double hx = 0.0;
+        if (plane_in && h_in) {
+          const double xc = pAu[offAh];
+          const double y = stencil_point(d, in_z(t - 1) ? pAm[offAh] : 0.0, pAu[offAh - kC2W],
+                                         pAu[offAh - 1], xc, pAu[offAh + 1], pAu[offAh + kC2W],
+                                         has_p ? pAp[offAh] : 0.0);
+          if (kFirst) hx = p.c1 * ((2.0 * xc) - div_rn(y, p.theta, inv_t));
+          else hx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * pBu[offBh])) + p.c2 * (pRu[offBh] - y));
+        }
+        pCu[offBh] = hx;
+      }
+    }
+    // ---------------- stage 2: E[t-2] on the own tile row (warps 1..8)
+    if (interior && t - 2 >= kb) {
+      double cw = __shfl_up_sync(0xffffffffu, c2.y, 1);
+      double ce = __shfl_down_sync(0xffffffffu, c2.x, 1);
+      if (lane == 0) cw = pC2[offB - 1];
+      if (lane == 31) ce = pC2[offB + 2];
+      const double2 cs = *reinterpret_cast<const double2*>(pC2 + offB - kC2W);
+      const double2 cn = *reinterpret_cast<const double2*>(pC2 + offB + kC2W);
+      const double y0 = stencil_point(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
+      const double y1 = stencil_point(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
+      double2 rv, xo;
+      if (kFirst) {
+        rv = a2;  // A == R == r
+        xo = make_double2(div_rn(a2.x, p.theta, inv_t), div_rn(a2.y, p.theta, inv_t));
+      } else {
+        rv = *reinterpret_cast<const double2*>(pR2 + offB);
+        xo = a2;
+      }
+      const double e0 = p.rk2 * (((p.c3 * c2.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
+      const double e1 = p.rk2 * (((p.c3 * c2.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
+      if (do2) {
+        st2(gEv, e0, e1);
+        if (kRed) acc = acc + (rv.x * e0 + rv.y * e1);
+      }
+    }
+    __syncthreads();
+    // rotate the register queues, rings and global pointers by one plane
+    a2 = am;
+    am = ac;
+    ac = ap;
+    c3 = c2;
+    c2 = c1;
+    c1 = cv;
+    pAm = pAu;
+    pAu = pAp;
+    pAp = (pAp + kC2APlane == sAend) ? sA : pAp + kC2APlane;
+    pBu = (pBu + kC2EStride == sBend) ? sB : pBu + kC2EStride;
+    pR2 = pR1;
+    pR1 = pRu;
+    pRu = (pRu + kC2EStride == sRend) ? sR : pRu + kC2EStride;
+    double* const pc = pC2;
+    pC2 = pC1;
+    pC1 = pCu;
+    pCu = pc;
+    if (++bslot == kFD) {
+      bslot = 0;
+      bphase ^= 1u;
+    }
+    gCt += p.nxy;
+    gEv += p.nxy;
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
+}  // namespace pcgx

@@ -568,6 +568,21 @@ __device__ __forceinline__ double stencil_point(double d, double xm, double xs, 
   return s * d;
 }
 
+// The same sum from pre-scaled neighbours t = d * x (each product formed once per
+// point by the caller): the identical IEEE operations, hence bitwise equal.
+__device__ __forceinline__ double stencil_point_t(double d, double tm, double ts, double tw,
+                                                  double tc, double te, double tn, double tp) {
+  double s = 0.0;
+  s = s + (-tm);
+  s = s + (-ts);
+  s = s + (-tw);
+  s = s + (6.0 * tc);
+  s = s + (-te);
+  s = s + (-tn);
+  s = s + (-tp);
+  return s * d;
+}
+
 // One thread per (i, j) column, marching planes [kb, ke) with the k-1, k, k+1
 // values in registers and the k+2 plane prefetched one iteration ahead; the
 // in-plane neighbours (i +- 1, j +- 1) come through L1 (the block's own plane

@@ -22,12 +22,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <queue>
 #include <memory>
 #include <string>
 #include <type_traits>
 #include <vector>
 
 #include "cheb2.cuh"
+#include "cheb2f.cuh"
 #include "common.cuh"
 #include "dir_tma.cuh"
 #include "host_math.hpp"
@@ -102,6 +104,9 @@ struct pcgx_operator_s {
   bool vec2 = false;  // even nx -> stencil7v2_kernel
   int pfd = 0;        // L2 prefetch distance (planes) of the v2 march
   bool cheb2 = false; // two Chebyshev steps per pass (stencil7_cheb2_kernel, TMA)
+  int cheb2v = 0;     // its stage-2 variant (kV): 0 tile rows, 1 own row, 2 own row + d*x queues, 3 pipelined
+  std::string c2plan;                     // PCGX_C2PLAN: "" auto, "u" uniform kz2, "h1,h2,..." explicit
+  std::map<int, ChunkPlan> c2plans;       // chunk plan per launch span (planes)
   int zpad = 0;       // ghost planes per side in the workspace vectors (z-slab + cheb2: 2)
   int kz2 = 32;       // z-chunk of the two-step kernel
   struct TmaPair { const double* ptr; CUtensorMap a, e; };
@@ -876,12 +881,96 @@ const pcgx_operator_s::TmaPair& tmaps_for(pcgx_operator op, const double* ptr) {
   return op->tmaps.back();
 }
 
-template <bool kFirst, bool kRed>
-void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const double* B,
+// Chunk heights of a two-step launch over `span` planes of `tiles` tiles with
+// `slots` resident CTAs. The block scheduler dispatches chunk-major, greedily;
+// uniform chunks leave a ragged last wave (4.5 waves at 320^3, 3 CTAs/SM). The
+// plan is: uniform chunks of `big` planes, the last (up to three) chunks shrunk
+// so the final wave ends evenly -- chosen by simulating the greedy dispatch (a
+// chunk of h planes costs h + 2.5 plane-times: two halo planes plus the ring
+// ramp). spec "u": uniform kz; "h1,h2,...": explicit heights summing to span.
+ChunkPlan make_chunk_plan(const std::string& spec, int span, int kz, long long tiles, long long slots) {
+  auto pack = [&](const std::vector<int>& hs) {
+    ChunkPlan p{};
+    p.n = 0;
+    p.start[0] = 0;
+    for (int h : hs) {
+      p.start[p.n + 1] = p.start[p.n] + h;
+      ++p.n;
+    }
+    return p;
+  };
+  auto uniform = [&](int h) {
+    std::vector<int> hs;
+    for (int z = 0; z < span; z += h) hs.push_back(std::min(h, span - z));
+    return hs;
+  };
+  std::vector<int> hs;
+  if (spec == "u") {
+    hs = uniform(std::max(kz, (span + ChunkPlan::kMax - 1) / ChunkPlan::kMax));
+  } else if (!spec.empty()) {
+    int sum = 0;
+    for (size_t a = 0; a < spec.size();) {
+      size_t b = spec.find(',', a);
+      if (b == std::string::npos) b = spec.size();
+      hs.push_back(std::max(1, std::atoi(spec.substr(a, b - a).c_str())));
+      sum += hs.back();
+      a = b + 1;
+    }
+    if (sum != span || (int)hs.size() > ChunkPlan::kMax) hs.clear();
+  }
+  if (hs.empty()) {
+    auto makespan = [&](const std::vector<int>& h) {
+      std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+      for (long long s = 0; s < slots; ++s) q.push(0.0);
+      double end = 0.0;
+      for (int c : h)
+        for (long long t = 0; t < tiles; ++t) {
+          const double f = q.top() + c + 2.5;
+          q.pop();
+          q.push(f);
+          end = std::max(end, f);
+        }
+      return end;
+    };
+    double best = 0.0;
+    const int bigs[] = {16, 24, 32, 40, 48, 64, 80, 96};
+    const int tl[] = {0, 4, 8, 12, 16, 20, 24};
+    for (int big : bigs)
+      for (int t1 : tl)
+        for (int t2 : tl)
+          for (int t3 : tl) {
+            if (t2 > t1 || t3 > t2) continue;
+            const int tail = t1 + t2 + t3;
+            if (tail > span) continue;
+            const int rest = span - tail;
+            std::vector<int> c;
+            if (rest % big) c.push_back(rest % big);
+            for (int k = 0; k < rest / big; ++k) c.push_back(big);
+            for (int t : {t1, t2, t3})
+              if (t) c.push_back(t);
+            if (c.empty() || (int)c.size() > ChunkPlan::kMax) continue;
+            const double m = makespan(c);
+            if (hs.empty() || m < best - 1e-9 || (m < best + 1e-9 && c.size() < hs.size())) {
+              best = m;
+              hs = c;
+            }
+          }
+    if (hs.empty()) hs = uniform((span + ChunkPlan::kMax - 1) / ChunkPlan::kMax);
+  }
+  if (env_int("PCGX_C2PLAN_DEBUG", 0)) {
+    std::fprintf(stderr, "[pcgx] two-step chunk plan span=%d tiles=%lld slots=%lld:", span, tiles, slots);
+    for (int h : hs) std::fprintf(stderr, " %d", h);
+    std::fprintf(stderr, "\n");
+  }
+  return pack(hs);
+}
+
+template <bool kFirst, bool kRed, int kV>
+void cheb2_launch_v(pcgx_context c, pcgx_operator op, const double* A, const double* B,
                   const double* R, const Cheb2Params& prm, int slot, int k_begin, int k_end, int kz,
                   bool accumulate) {
   if (k_end <= k_begin) return;
-  PCGX_CUDA(cudaFuncSetAttribute(stencil7_cheb2_kernel<kFirst, kRed>,
+  PCGX_CUDA(cudaFuncSetAttribute(stencil7_cheb2_kernel<kFirst, kRed, kV>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2Smem));
   // copies: a later tmaps_for() may grow the cache and move its elements
   const CUtensorMap ma = tmaps_for(op, A).a;
@@ -891,10 +980,45 @@ void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const doubl
   dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
             (unsigned)((k_end - k_begin + kz - 1) / kz));
   Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
-  stencil7_cheb2_kernel<kFirst, kRed><<<grid, kC2Threads, kC2Smem, c->s>>>(ma, mb, mr, prm, k_begin,
-                                                                           k_end, kz, red);
+  stencil7_cheb2_kernel<kFirst, kRed, kV><<<grid, kC2Threads, kC2Smem, c->s>>>(ma, mb, mr, prm, k_begin,
+                                                                               k_end, kz, red);
   check_launch();
   count_launch(c);
+}
+
+template <bool kFirst, bool kRed>
+void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const double* B,
+                  const double* R, const Cheb2Params& prm, int slot, int k_begin, int k_end, int kz,
+                  bool accumulate) {
+  if (op->cheb2v == 3) {
+    if (k_end <= k_begin) return;
+    auto kern = stencil7_cheb2f_kernel<kFirst, kRed>;
+    PCGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2FSmem));
+    const CUtensorMap ma = tmaps_for(op, A).a;
+    const CUtensorMap mb = tmaps_for(op, B ? B : A).e;
+    const CUtensorMap mr = tmaps_for(op, R).e;
+    const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kC2TY - 1) / kC2TY);
+    const int span = k_end - k_begin;
+    auto it = op->c2plans.find(span);
+    if (it == op->c2plans.end()) {
+      int occ = 0;
+      PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kC2Threads, kC2FSmem));
+      it = op->c2plans.emplace(span, make_chunk_plan(op->c2plan, span, op->kz2, tiles,
+                                                     (long long)std::max(occ, 1) * c->sms)).first;
+    }
+    const ChunkPlan& plan = it->second;
+    Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
+    kern<<<dim3((unsigned)tiles, (unsigned)plan.n), kC2Threads, kC2FSmem, c->s>>>(ma, mb, mr, prm, k_begin,
+                                                                                  k_end, plan, red);
+    check_launch();
+    count_launch(c);
+    return;
+  }
+  switch (op->cheb2v) {
+    case 0: cheb2_launch_v<kFirst, kRed, 0>(c, op, A, B, R, prm, slot, k_begin, k_end, kz, accumulate); break;
+    case 1: cheb2_launch_v<kFirst, kRed, 1>(c, op, A, B, R, prm, slot, k_begin, k_end, kz, accumulate); break;
+    default: cheb2_launch_v<kFirst, kRed, 2>(c, op, A, B, R, prm, slot, k_begin, k_end, kz, accumulate); break;
+  }
 }
 
 // The direction step p_new = z + beta p_old, q = A p_new, p_new . q -> slot on a
@@ -2584,6 +2708,8 @@ pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t
     op->pfd = env_int("PCGX_PFD", 2);
     op->cheb2 = op->vec2 && env_int("PCGX_CHEB2", 1) != 0;
     op->kz2 = env_int("PCGX_KZ2", 32);
+    op->cheb2v = env_int("PCGX_CHEB2V", 3);
+    if (const char* e = std::getenv("PCGX_C2PLAN")) op->c2plan = e;
     try {
       init_stencil_ghosts(c, op);
       if (c->nranks > 1 && op->nzl < 2) op->cheb2 = false;  // 2-plane halos need >= 2 planes
