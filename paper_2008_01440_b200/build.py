@@ -24,7 +24,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpcgx.so")
 SOURCES = ["pcgx.cu", "host_math.cpp", "gen.cpp", "mm.cpp"]
-HEADERS = ["common.cuh", "kernels.cuh", "cheb2.cuh", "dir_tma.cuh", "host_math.hpp"]
+HEADERS = sorted(f for f in os.listdir(os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc"))
+                 if f.endswith((".cuh", ".hpp", ".h")))
 
 
 def _nvcc():

@@ -26,18 +26,43 @@
 
 namespace pcgx {
 
-// Three CTAs (30 warps) per SM: <= 64 registers and <= 74 KB of rings, hence a
-// prefetch distance of two planes (measured: +7% over two CTAs with D = 4).
+// Tile 64 x kFTY, kFTY + 2 warps. Default: 64 x 20 (22 warps, ONE CTA per SM,
+// 80 registers), rings four planes deep (206 KB), R of stage 2 in registers.
+// Measured at 320^3 against the alternatives (tools/kbench_cheb2.py, one box):
+// 64 x 8 with 3 CTAs/SM and D = 2: +5%; 64 x 12, 2 CTAs/SM, D = 3: +1%;
+// 64 x 20 with D = 3: +4%; 64 x 16, D = 5: +6%; 64 x 24, D = 3: +4%. Fewer
+// redundant stage-1 rows (22 per 20 output rows) and a deep prefetch both pay.
+#ifndef PCGX_C2FTY
+#define PCGX_C2FTY 20
+#endif
 #ifndef PCGX_C2FD
-#define PCGX_C2FD 2
+#define PCGX_C2FD 4
 #endif
 #ifndef PCGX_C2FMINB
-#define PCGX_C2FMINB 3
+#define PCGX_C2FMINB 1
 #endif
+// R of stage 2 (plane t-2) from a register queue instead of the R ring
+#ifndef PCGX_C2FRREG
+#define PCGX_C2FRREG 1
+#endif
+// register cap with one CTA per SM: 22 warps put 6 on one SM sub-partition (16K
+// registers each), so 64 x 20 tiles allow 80
+#ifndef PCGX_C2FMAXREG
+#define PCGX_C2FMAXREG 80
+#endif
+constexpr int kFTY = PCGX_C2FTY;
+constexpr int kFW = kC2W;                            // 68: tile-i t <-> smem column t+2
+constexpr int kFAY = kFTY + 4, kFBY = kFTY + 2;      // A box rows (2-halo), B/R/C rows (1-halo)
+constexpr int kFAPlane = (kFW * kFAY + 15) / 16 * 16;  // A slot stride (128-byte TMA destinations)
+constexpr int kFBPlane = kFW * kFBY;
+constexpr int kFEStride = (kFBPlane + 15) / 16 * 16;  // TMA destinations: 128-byte multiples
+constexpr int kFCStride = kFBPlane;
+constexpr int kFWarps = kFTY + 2, kFThreads = 32 * kFWarps;
+constexpr bool kFRReg = PCGX_C2FRREG != 0;
 constexpr int kFD = PCGX_C2FD;
-constexpr int kFNA = kFD + 2, kFNB = kFD, kFNR = kFD + 2, kFNC = 3;
-constexpr size_t kC2FSmem = sizeof(double) * (size_t)(kFNA * kC2APlane + (kFNB + kFNR) * kC2EStride +
-                                                      kFNC * kC2CStride) +
+constexpr int kFNA = kFD + 2, kFNB = kFD, kFNR = kFD + (kFRReg ? 0 : 2), kFNC = 3;
+constexpr size_t kC2FSmem = sizeof(double) * (size_t)(kFNA * kFAPlane + (kFNB + kFNR) * kFEStride +
+                                                      kFNC * kFCStride) +
                             16 * (kFD + 1) + 128;
 
 // z-chunking of a launch: chunk c covers planes [k_begin + start[c], k_begin + start[c+1]).
@@ -50,23 +75,27 @@ struct ChunkPlan {
   int start[kMax + 1];
 };
 
-template <bool kFirst, bool kRed>
-__global__ void __launch_bounds__(kC2Threads, PCGX_C2FMINB)
-stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 box)
+template <bool kFirst, bool kRed, bool kT>
+#if PCGX_C2FMINB == 1
+__global__ void __maxnreg__(PCGX_C2FMAXREG)
+#else
+__global__ void __launch_bounds__(kFThreads, PCGX_C2FMINB)
+#endif
+stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kFTY+4) box)
                        const __grid_constant__ CUtensorMap mapB,  // B (68 x 10 box)
                        const __grid_constant__ CUtensorMap mapR,  // R (68 x 10 box)
                        Cheb2Params p, int k_begin, int k_end, const __grid_constant__ ChunkPlan plan, Reduce red) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sA = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
-  double* sB = sA + kFNA * kC2APlane;
-  double* sR = sB + kFNB * kC2EStride;
-  double* sC = sR + kFNR * kC2EStride;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kFNC * kC2CStride);  // kFD unit bars + 1 prologue
+  double* sB = sA + kFNA * kFAPlane;
+  double* sR = sB + kFNB * kFEStride;
+  double* sC = sR + kFNR * kFEStride;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kFNC * kFCStride);  // kFD unit bars + 1 prologue
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned bytesA = kC2APlane * 8, bytesB = kC2BPlane * 8;
+  const unsigned bytesA = kFW * kFAY * 8, bytesB = kFBPlane * 8;  // box bytes (slots may be padded)
   const int tiles_x = (p.nx + kC2TX - 1) / kC2TX;
-  const int i0 = (int)(blockIdx.x % tiles_x) * kC2TX, j0 = (int)(blockIdx.x / tiles_x) * kC2TY;
+  const int i0 = (int)(blockIdx.x % tiles_x) * kC2TX, j0 = (int)(blockIdx.x / tiles_x) * kFTY;
   const int kb = k_begin + plan.start[blockIdx.y];
   const int ke = min(k_begin + plan.start[blockIdx.y + 1], k_end);
   if (tid == 0) {
@@ -82,10 +111,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 
     uint64_t* bar = &bars[(u - (kb - 1)) % kFD];
     const bool la = in_z(u + 1), lbr = !kFirst && in_z(u);
     mbar_expect_tx(bar, (la ? bytesA : 0u) + (lbr ? 2 * bytesB : 0u));
-    if (la) tma_load_3d(sA + ((u + 1 - (kb - 2)) % kFNA) * kC2APlane, &mapA, i0 - 2, j0 - 2, u + 1 + zo, bar);
+    if (la) tma_load_3d(sA + ((u + 1 - (kb - 2)) % kFNA) * kFAPlane, &mapA, i0 - 2, j0 - 2, u + 1 + zo, bar);
     if (lbr) {
-      tma_load_3d(sB + ((u - (kb - 1)) % kFNB) * kC2EStride, &mapB, i0 - 2, j0 - 1, u + zo, bar);
-      tma_load_3d(sR + ((u - (kb - 1)) % kFNR) * kC2EStride, &mapR, i0 - 2, j0 - 1, u + zo, bar);
+      tma_load_3d(sB + ((u - (kb - 1)) % kFNB) * kFEStride, &mapB, i0 - 2, j0 - 1, u + zo, bar);
+      tma_load_3d(sR + ((u - (kb - 1)) % kFNR) * kFEStride, &mapR, i0 - 2, j0 - 1, u + zo, bar);
     }
   };
   const int u_last = ke;  // stage 1 runs t = kb-1 .. ke, stage 2 v = t-2 = kb .. ke-1
@@ -93,7 +122,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 
     uint64_t* pb = &bars[kFD];
     mbar_expect_tx(pb, (in_z(kb - 2) ? bytesA : 0u) + (in_z(kb - 1) ? bytesA : 0u));
     if (in_z(kb - 2)) tma_load_3d(sA, &mapA, i0 - 2, j0 - 2, kb - 2 + zo, pb);
-    if (in_z(kb - 1)) tma_load_3d(sA + kC2APlane, &mapA, i0 - 2, j0 - 2, kb - 1 + zo, pb);
+    if (in_z(kb - 1)) tma_load_3d(sA + kFAPlane, &mapA, i0 - 2, j0 - 2, kb - 1 + zo, pb);
     for (int u = kb - 1; u < kb - 1 + kFD && u <= u_last; ++u) issue_unit(u);
   }
   mbar_wait(&bars[kFD], 0);
@@ -106,88 +135,112 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 
   const bool pair_in = gi < p.nx;
   const int gj = j0 - 1 + warp;                    // this warp's (extended) row
   const bool do1 = gj >= 0 && gj < p.ny && pair_in;
-  const int offA = (warp + 1) * kC2W + col;        // A-box offset of the pair
-  const int offB = warp * kC2W + col;              // B/R/C offset of the pair
-  const bool interior = warp >= 1 && warp <= kC2TY;  // a tile row: stage 2 here
+  const int offA = (warp + 1) * kFW + col;        // A-box offset of the pair
+  const int offB = warp * kFW + col;              // B/R/C offset of the pair
+  const bool interior = warp >= 1 && warp <= kFTY;  // a tile row: stage 2 here
   const bool do2 = interior && do1;
   double* gC = p.outC + (long long)gj * p.nx + gi;
   double* gE = p.outE + (long long)gj * p.nx + gi;
   // halo columns: warp 0 -> tile-i -1, warp 9 -> tile-i 64; lanes 0..9 = rows
-  const bool do_h = (warp == 0 || warp == kC2TY + 1) && lane < kC2BY;
+  const bool do_h = (warp == 0 || warp == kFTY + 1) && lane < kFBY;
   const int hcol = warp == 0 ? 1 : kC2TX + 2;
   const int hgi = warp == 0 ? i0 - 1 : i0 + kC2TX;
   const int hgj = j0 - 1 + lane;
   const bool h_in = do_h && hgi >= 0 && hgi < p.nx && hgj >= 0 && hgj < p.ny;
-  const int offAh = (lane + 1) * kC2W + hcol, offBh = lane * kC2W + hcol;
+  const int offAh = (lane + 1) * kFW + hcol, offBh = lane * kFW + hcol;
 
-  const double* const sAend = sA + kFNA * kC2APlane;
-  const double* const sBend = sB + kFNB * kC2EStride;
-  const double* const sRend = sR + kFNR * kC2EStride;
+  const double* const sAend = sA + kFNA * kFAPlane;
+  const double* const sBend = sB + kFNB * kFEStride;
+  const double* const sRend = sR + kFNR * kFEStride;
   const double* pAm = sA;                           // A[t-1]
-  const double* pAu = sA + kC2APlane;               // A[t]
-  const double* pAp = sA + 2 * kC2APlane;           // A[t+1]
+  const double* pAu = sA + kFAPlane;               // A[t]
+  const double* pAp = sA + 2 * kFAPlane;           // A[t+1]
   const double* pBu = sB;                           // B[t]
   const double* pRu = sR;                           // R[t]
-  const double* pR2 = sR + (kFNR - 2) * kC2EStride; // R[t-2]
-  const double* pR1 = sR + (kFNR - 1) * kC2EStride; // R[t-1]
+  const double* pR2 = sR + ((kFNR - 2 + kFNR) % kFNR) * kFEStride;  // R[t-2] (ring variant)
+  const double* pR1 = sR + (kFNR - 1) * kFEStride;                  // R[t-1]
+  double2 r1 = zero2, r2 = zero2;                  // R[t-1], R[t-2] (register variant, own row)
   double* pCu = sC;                                 // C[t]
-  double* pC1 = sC + 2 * kC2CStride;                // C[t-1]
-  double* pC2 = sC + kC2CStride;                    // C[t-2]
+  double* pC1 = sC + 2 * kFCStride;                // C[t-1]
+  double* pC2 = sC + kFCStride;                    // C[t-2]
   int bslot = 0;
   unsigned bphase = 0;
   double* gCt = gC + (long long)(kb - 1) * p.nxy;   // C pair at plane t
   double* gEv = gE + (long long)(kb - 3) * p.nxy;   // E pair at plane t-2
 
+  // kT: the stencil queues hold t = d * x (each product formed once per point);
+  // the recurrences' centre values travel in separate x queues
+  auto mul2 = [&](double2 v) { return make_double2(d * v.x, d * v.y); };
   double2 am = in_z(kb - 2) ? *reinterpret_cast<const double2*>(sA + offA) : zero2;
-  double2 ac = in_z(kb - 1) ? *reinterpret_cast<const double2*>(sA + kC2APlane + offA) : zero2;
-  double2 a2 = zero2;                          // A[t-2] (own row)
-  double2 c1 = zero2, c2 = zero2, c3 = zero2;  // C[t-1], C[t-2], C[t-3] (own row)
+  double2 ac = in_z(kb - 1) ? *reinterpret_cast<const double2*>(sA + kFAPlane + offA) : zero2;
+  double2 x1 = ac;                             // kT: A[t-1] x (own row)
+  if (kT) {
+    am = mul2(am);
+    ac = mul2(ac);
+  }
+  double2 a2 = zero2;                          // A[t-2] x (own row)
+  double2 c1 = zero2, c2 = zero2, c3 = zero2;  // C[t-1], C[t-2], C[t-3] (own row; t when kT)
+  double2 cx1 = zero2, cx2 = zero2;            // kT: C[t-1], C[t-2] x
   double acc = 0.0;
 
 #pragma unroll kC2Unroll
   for (int t = kb - 1; t <= ke + 1; ++t) {
     if (tid == 0 && t >= kb && t - 1 + kFD <= u_last) issue_unit(t - 1 + kFD);
     const bool s1 = t <= ke;
-    double2 ap = zero2, cv = zero2;
+    double2 ap = zero2, cv = zero2, rt = zero2;
+    double2 ct = zero2, xt = zero2;  // kT: C[t] as t = d x; A[t] x
     if (s1) mbar_wait(&bars[bslot], bphase);
     // ---------------- stage 1: C[t] on the extended tile row
     if (s1) {
       const bool plane_in = t >= p.c_lo && t < p.c_hi, has_p = in_z(t + 1);
       ap = has_p ? *reinterpret_cast<const double2*>(pAp + offA) : zero2;
+      if (kT) ap = mul2(ap);
       double aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
       double ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
-      if (lane == 0) aw = pAu[offA - 1];
-      if (lane == 31) ae = pAu[offA + 2];
-      const double2 as = *reinterpret_cast<const double2*>(pAu + offA - kC2W);
-      const double2 an = *reinterpret_cast<const double2*>(pAu + offA + kC2W);
-      const double y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
-      const double y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
+      if (lane == 0) aw = kT ? d * pAu[offA - 1] : pAu[offA - 1];
+      if (lane == 31) ae = kT ? d * pAu[offA + 2] : pAu[offA + 2];
+      const double2 as = *reinterpret_cast<const double2*>(pAu + offA - kFW);
+      const double2 an = *reinterpret_cast<const double2*>(pAu + offA + kFW);
+      double y0, y1;
+      double2 xc;  // A[t] x at the pair
+      if (kT) {
+        xc = *reinterpret_cast<const double2*>(pAu + offA);
+        y0 = stencil_point_t(d, am.x, d * as.x, aw, ac.x, ac.y, d * an.x, ap.x);
+        y1 = stencil_point_t(d, am.y, d * as.y, ac.x, ac.y, ae, d * an.y, ap.y);
+      } else {
+        xc = ac;
+        y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
+        y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
+      }
+      if (kT) xt = xc;
       double2 c;
       if (kFirst) {
-        c.x = p.c1 * ((2.0 * ac.x) - div_rn(y0, p.theta, inv_t));
-        c.y = p.c1 * ((2.0 * ac.y) - div_rn(y1, p.theta, inv_t));
+        c.x = p.c1 * ((2.0 * xc.x) - div_rn(y0, p.theta, inv_t));
+        c.y = p.c1 * ((2.0 * xc.y) - div_rn(y1, p.theta, inv_t));
       } else {
         const double2 bb = *reinterpret_cast<const double2*>(pBu + offB);
         const double2 rr = *reinterpret_cast<const double2*>(pRu + offB);
-        c.x = p.rk1 * (((p.c3 * ac.x) - (p.rk1m1 * bb.x)) + p.c2 * (rr.x - y0));
-        c.y = p.rk1 * (((p.c3 * ac.y) - (p.rk1m1 * bb.y)) + p.c2 * (rr.y - y1));
+        rt = rr;
+        c.x = p.rk1 * (((p.c3 * xc.x) - (p.rk1m1 * bb.x)) + p.c2 * (rr.x - y0));
+        c.y = p.rk1 * (((p.c3 * xc.y) - (p.rk1m1 * bb.y)) + p.c2 * (rr.y - y1));
       }
       const bool live = plane_in && do1;
       if (live) cv = c;
       if (live && interior && t >= kb && t < ke) st2(gCt, cv.x, cv.y);
-      *reinterpret_cast<double2*>(pCu + offB) = cv;
+      if (kT) ct = mul2(cv);
+      *reinterpret_cast<double2*>(pCu + offB) = kT ? ct : cv;
       // i-halo columns of C[t] (read by stage 2 of plane t, two iterations on)
       if (do_h) {
         double hx = 0.0;
         if (plane_in && h_in) {
           const double xc = pAu[offAh];
-          const double y = stencil_point(d, in_z(t - 1) ? pAm[offAh] : 0.0, pAu[offAh - kC2W],
-                                         pAu[offAh - 1], xc, pAu[offAh + 1], pAu[offAh + kC2W],
+          const double y = stencil_point(d, in_z(t - 1) ? pAm[offAh] : 0.0, pAu[offAh - kFW],
+                                         pAu[offAh - 1], xc, pAu[offAh + 1], pAu[offAh + kFW],
                                          has_p ? pAp[offAh] : 0.0);
           if (kFirst) hx = p.c1 * ((2.0 * xc) - div_rn(y, p.theta, inv_t));
           else hx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * pBu[offBh])) + p.c2 * (pRu[offBh] - y));
         }
-        pCu[offBh] = hx;
+        pCu[offBh] = kT ? d * hx : hx;
       }
     }
     // ---------------- stage 2: E[t-2] on the own tile row (warps 1..8)
@@ -196,20 +249,29 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 
       double ce = __shfl_down_sync(0xffffffffu, c2.x, 1);
       if (lane == 0) cw = pC2[offB - 1];
       if (lane == 31) ce = pC2[offB + 2];
-      const double2 cs = *reinterpret_cast<const double2*>(pC2 + offB - kC2W);
-      const double2 cn = *reinterpret_cast<const double2*>(pC2 + offB + kC2W);
-      const double y0 = stencil_point(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
-      const double y1 = stencil_point(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
+      const double2 cs = *reinterpret_cast<const double2*>(pC2 + offB - kFW);
+      const double2 cn = *reinterpret_cast<const double2*>(pC2 + offB + kFW);
+      double y0, y1;
+      double2 cc;  // C[t-2] x at the pair
+      if (kT) {
+        y0 = stencil_point_t(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
+        y1 = stencil_point_t(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
+        cc = cx2;
+      } else {
+        y0 = stencil_point(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
+        y1 = stencil_point(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
+        cc = c2;
+      }
       double2 rv, xo;
       if (kFirst) {
         rv = a2;  // A == R == r
         xo = make_double2(div_rn(a2.x, p.theta, inv_t), div_rn(a2.y, p.theta, inv_t));
       } else {
-        rv = *reinterpret_cast<const double2*>(pR2 + offB);
+        rv = kFRReg ? r2 : *reinterpret_cast<const double2*>(pR2 + offB);
         xo = a2;
       }
-      const double e0 = p.rk2 * (((p.c3 * c2.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
-      const double e1 = p.rk2 * (((p.c3 * c2.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
+      const double e0 = p.rk2 * (((p.c3 * cc.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
+      const double e1 = p.rk2 * (((p.c3 * cc.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
       if (do2) {
         st2(gEv, e0, e1);
         if (kRed) acc = acc + (rv.x * e0 + rv.y * e1);
@@ -217,19 +279,28 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x 12 
     }
     __syncthreads();
     // rotate the register queues, rings and global pointers by one plane
-    a2 = am;
+    if (kT) {
+      a2 = x1;
+      x1 = xt;
+    } else {
+      a2 = am;
+    }
     am = ac;
     ac = ap;
     c3 = c2;
     c2 = c1;
-    c1 = cv;
+    c1 = kT ? ct : cv;
+    cx2 = cx1;
+    cx1 = cv;
+    r2 = r1;
+    r1 = rt;
     pAm = pAu;
     pAu = pAp;
-    pAp = (pAp + kC2APlane == sAend) ? sA : pAp + kC2APlane;
-    pBu = (pBu + kC2EStride == sBend) ? sB : pBu + kC2EStride;
+    pAp = (pAp + kFAPlane == sAend) ? sA : pAp + kFAPlane;
+    pBu = (pBu + kFEStride == sBend) ? sB : pBu + kFEStride;
     pR2 = pR1;
     pR1 = pRu;
-    pRu = (pRu + kC2EStride == sRend) ? sR : pRu + kC2EStride;
+    pRu = (pRu + kFEStride == sRend) ? sR : pRu + kFEStride;
     double* const pc = pC2;
     pC2 = pC1;
     pC1 = pCu;

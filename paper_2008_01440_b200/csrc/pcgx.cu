@@ -109,8 +109,9 @@ struct pcgx_operator_s {
   std::map<int, ChunkPlan> c2plans;       // chunk plan per launch span (planes)
   int zpad = 0;       // ghost planes per side in the workspace vectors (z-slab + cheb2: 2)
   int kz2 = 32;       // z-chunk of the two-step kernel
-  struct TmaPair { const double* ptr; CUtensorMap a, e; };
-  std::vector<TmaPair> tmaps;  // per-buffer tensor maps (A box 68x12, B/R box 68x10)
+  struct TmaPair { const double* ptr; CUtensorMap a, e, fa, fe; };
+  std::vector<TmaPair> tmaps;  // per-buffer tensor maps (A box 68x12, B/R box 68x10; f: the
+                               // pipelined two-step kernel's 68 x (kFTY+4), 68 x (kFTY+2))
   // csr
   int* tile_row = nullptr;  // csr2 tiles (ntiles + 1), nullptr -> csr_kernel
   // SELL-32 layout (sell_kernel, the default CSR path)
@@ -874,10 +875,14 @@ CUtensorMap make_map(pcgx_operator op, const double* ptr, int bx, int by) {
   return m;
 }
 
-const pcgx_operator_s::TmaPair& tmaps_for(pcgx_operator op, const double* ptr) {
+using TmaPair = pcgx_operator_s::TmaPair;
+const TmaPair& tmaps_for(pcgx_operator op, const double* ptr) {
   for (auto& t : op->tmaps)
     if (t.ptr == ptr) return t;
-  op->tmaps.push_back({ptr, make_map(op, ptr, kC2AX, kC2AY), make_map(op, ptr, kC2BX, kC2BY)});
+  TmaPair t{ptr, make_map(op, ptr, kC2AX, kC2AY), make_map(op, ptr, kC2BX, kC2BY), {}, {}};
+  t.fa = kFAY == kC2AY ? t.a : make_map(op, ptr, kFW, kFAY);
+  t.fe = kFBY == kC2BY ? t.e : make_map(op, ptr, kFW, kFBY);
+  op->tmaps.push_back(t);
   return op->tmaps.back();
 }
 
@@ -990,25 +995,26 @@ template <bool kFirst, bool kRed>
 void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const double* B,
                   const double* R, const Cheb2Params& prm, int slot, int k_begin, int k_end, int kz,
                   bool accumulate) {
-  if (op->cheb2v == 3) {
+  if (op->cheb2v >= 3) {
     if (k_end <= k_begin) return;
-    auto kern = stencil7_cheb2f_kernel<kFirst, kRed>;
+    auto kern = op->cheb2v == 4 ? stencil7_cheb2f_kernel<kFirst, kRed, true>
+                                : stencil7_cheb2f_kernel<kFirst, kRed, false>;
     PCGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2FSmem));
-    const CUtensorMap ma = tmaps_for(op, A).a;
-    const CUtensorMap mb = tmaps_for(op, B ? B : A).e;
-    const CUtensorMap mr = tmaps_for(op, R).e;
-    const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kC2TY - 1) / kC2TY);
+    const CUtensorMap ma = tmaps_for(op, A).fa;
+    const CUtensorMap mb = tmaps_for(op, B ? B : A).fe;
+    const CUtensorMap mr = tmaps_for(op, R).fe;
+    const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kFTY - 1) / kFTY);
     const int span = k_end - k_begin;
     auto it = op->c2plans.find(span);
     if (it == op->c2plans.end()) {
       int occ = 0;
-      PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kC2Threads, kC2FSmem));
+      PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFThreads, kC2FSmem));
       it = op->c2plans.emplace(span, make_chunk_plan(op->c2plan, span, op->kz2, tiles,
                                                      (long long)std::max(occ, 1) * c->sms)).first;
     }
     const ChunkPlan& plan = it->second;
     Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
-    kern<<<dim3((unsigned)tiles, (unsigned)plan.n), kC2Threads, kC2FSmem, c->s>>>(ma, mb, mr, prm, k_begin,
+    kern<<<dim3((unsigned)tiles, (unsigned)plan.n), kFThreads, kC2FSmem, c->s>>>(ma, mb, mr, prm, k_begin,
                                                                                   k_end, plan, red);
     check_launch();
     count_launch(c);

@@ -88,6 +88,13 @@ def same(nx, m, reps, rounds, variants):
         r = P.random_uniform_vector(n, 1, ctx=ctx)
         out = P.DeviceVector(ctx, n)
         res = {v: [] for v in variants}
+        clk = {v: [] for v in variants}
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            hdl = pynvml.nvmlDeviceGetHandleByIndex(0)
+        except Exception:
+            hdl = None
         for op in ops:
             for _ in range(3):
                 pcgx._check(L.pcgx_cheb_apply_device(ctx.h, op.h, C.byref(cp), r.ptr, out.ptr), ctx.h)
@@ -95,13 +102,16 @@ def same(nx, m, reps, rounds, variants):
             for v, op in zip(variants, ops):
                 ctx.synchronize()
                 ctx.timer_start()
-                for _ in range(reps):
+                for i in range(reps):
                     pcgx._check(L.pcgx_cheb_apply_device(ctx.h, op.h, C.byref(cp), r.ptr, out.ptr), ctx.h)
+                    if hdl is not None and i == reps // 2:
+                        clk[v].append(pynvml.nvmlDeviceGetClockInfo(hdl, pynvml.NVML_CLOCK_SM))
                 res[v].append(ctx.timer_stop() / reps / (m // 2))
         for v in variants:
             t = sorted(res[v])
             print(json.dumps({"variant": v, "pass_ms_min": round(t[0], 5), "pass_ms_med": round(t[len(t) // 2], 5),
                               "pass_GBps_med": round(40 * n / t[len(t) // 2] / 1e6, 1),
+                              "sm_mhz": sorted(clk[v])[len(clk[v]) // 2] if clk[v] else None,
                               "all": [round(x, 4) for x in res[v]]}), flush=True)
 
 
