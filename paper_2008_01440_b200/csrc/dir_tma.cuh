@@ -13,19 +13,35 @@
 // bitwise theirs. HBM: read z, p_old; write p_new, q = 32 B per point.
 #pragma once
 
-#include "cheb2.cuh"
+#include "cheb2f.cuh"
 
 namespace pcgx {
 
-constexpr int kDirNS = 6;                 // z / p_old ring slots (4 planes ahead)
+// Tile 64 x kDTY (default: the pipelined two-step kernel's 64 x 20, one CTA of
+// 22 warps per SM, so both share the 68 x 22 tensor maps): fewer redundant halo
+// rows than 64 x 8 (22 box rows per 20 output rows instead of 10 per 8).
+#ifndef PCGX_DIRTY
+#define PCGX_DIRTY PCGX_C2FTY
+#endif
+#ifndef PCGX_DIRMINB
+#define PCGX_DIRMINB 1
+#endif
+#ifndef PCGX_DIRNS
+#define PCGX_DIRNS 6
+#endif
+constexpr int kDTY = PCGX_DIRTY;
+constexpr int kDBY = kDTY + 2;                          // box rows (1-halo)
+constexpr int kDBPlane = kC2W * kDBY;
+constexpr int kDEStride = (kDBPlane + 15) / 16 * 16;    // TMA destinations: 128-byte multiples
+constexpr int kDirNS = PCGX_DIRNS;        // z / p_old ring slots (NS - 2 planes ahead)
 constexpr int kDirNC = 3;                 // p_new planes
 #ifndef PCGX_DIRUNROLL
 #define PCGX_DIRUNROLL 2
 #endif
 constexpr int kDirUnroll = PCGX_DIRUNROLL; // plane-loop unroll
-constexpr int kDirThreads = kC2Threads;   // one warp per extended row (tile rows + 2 halo rows)
+constexpr int kDirThreads = 32 * (kDTY + 2);  // one warp per extended row (tile rows + 2 halo rows)
 constexpr size_t kDirSmem =
-    sizeof(double) * (size_t)(2 * kDirNS * kC2EStride + kDirNC * kC2BPlane) + 8 * kDirNS + 128;
+    sizeof(double) * (size_t)(2 * kDirNS * kDEStride + kDirNC * kDBPlane) + 8 * kDirNS + 128;
 
 struct DirParams {
   int nx, ny, nzl;
@@ -43,23 +59,24 @@ struct DirParams {
   double* pout;  // p_new
 };
 
-// grid: (ceil(nx/64), ceil(ny/kC2TY), ceil(nzl/kz)); block kDirThreads; dynamic smem kDirSmem.
-__global__ void __launch_bounds__(kDirThreads, PCGX_C2MINB)
+// grid: (tiles, plan.n); block kDirThreads; dynamic smem kDirSmem.
+__global__ void __launch_bounds__(kDirThreads, PCGX_DIRMINB)
 stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapP,
-                    DirParams p, int k_begin, int k_end, int kz, Reduce red) {
+                    DirParams p, int k_begin, int k_end, const __grid_constant__ ChunkPlan plan, Reduce red) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sZ = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
-  double* sP = sZ + kDirNS * kC2EStride;
-  double* sN = sP + kDirNS * kC2EStride;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sN + kDirNC * kC2BPlane);
+  double* sP = sZ + kDirNS * kDEStride;
+  double* sN = sP + kDirNS * kDEStride;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sN + kDirNC * kDBPlane);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int i0 = blockIdx.x * kC2TX, j0 = blockIdx.y * kC2TY;
-  const int kb = k_begin + blockIdx.z * kz;
-  const int ke = min(kb + kz, k_end);
+  const int tiles_x = (p.nx + kC2TX - 1) / kC2TX;
+  const int i0 = (int)(blockIdx.x % tiles_x) * kC2TX, j0 = (int)(blockIdx.x / tiles_x) * kDTY;
+  const int kb = k_begin + plan.start[blockIdx.y];
+  const int ke = min(k_begin + plan.start[blockIdx.y + 1], k_end);
   const bool first = p.first != 0;
   const double beta = first ? 0.0 : p.S[p.s_new] / p.S[p.s_old];
-  const unsigned bytes = kC2BPlane * 8;
+  const unsigned bytes = kDBPlane * 8;  // box bytes
   auto in_z = [&](int z) { return z >= p.a_lo && z < p.a_hi; };
   // unit u: the z (and p_old) boxes of plane u, slot / barrier (u - (kb-1)) % NS
   auto issue = [&](int u) {
@@ -67,8 +84,8 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
     const bool ld = in_z(u);
     mbar_expect_tx(&bars[q], ld ? (first ? bytes : 2 * bytes) : 0u);
     if (ld) {
-      tma_load_3d(sZ + q * kC2EStride, &mapZ, i0 - 2, j0 - 1, u + p.zoff, &bars[q]);
-      if (!first) tma_load_3d(sP + q * kC2EStride, &mapP, i0 - 2, j0 - 1, u + p.zoff, &bars[q]);
+      tma_load_3d(sZ + q * kDEStride, &mapZ, i0 - 2, j0 - 1, u + p.zoff, &bars[q]);
+      if (!first) tma_load_3d(sP + q * kDEStride, &mapP, i0 - 2, j0 - 1, u + p.zoff, &bars[q]);
     }
   };
   if (tid == 0) {
@@ -85,7 +102,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   const bool pair_in = gi < p.nx;
   const int gj = j0 - 1 + warp;
   const bool do1 = gj >= 0 && gj < p.ny && pair_in;
-  const bool tile_row = warp >= 1 && warp <= kC2TY;
+  const bool tile_row = warp >= 1 && warp <= kDTY;
   const int off = warp * kC2W + col;
   const long long goff = (long long)gj * p.nx + gi;
   auto comb = [&](double zv, double pv) { return first ? zv : zv + beta * pv; };
@@ -105,8 +122,8 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
     const bool xdo = xupd && tile_row && do1 && u - 1 >= kb;
     if (xdo) xv = *reinterpret_cast<const double2*>(p.x + (long long)(u - 1) * p.nxy + goff);
     mbar_wait(&bars[slot], phase);
-    const double* Zu = sZ + slot * kC2EStride;
-    const double* Pu = sP + slot * kC2EStride;
+    const double* Zu = sZ + slot * kDEStride;
+    const double* Pu = sP + slot * kDEStride;
     double2 pn = zero2;
     if (in_z(u) && do1) {
       const double2 zv = *reinterpret_cast<const double2*>(Zu + off);
@@ -117,7 +134,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
         pn = make_double2(comb(zv.x, pv.x), comb(zv.y, pv.y));
       }
     }
-    double* Nu = sN + sc * kC2BPlane;
+    double* Nu = sN + sc * kDBPlane;
     *reinterpret_cast<double2*>(Nu + off) = pn;
     __syncthreads();
     // the slot of plane u-2 is free (its last readers are behind this barrier)
@@ -128,9 +145,9 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
       // lane-0 / lane-31 outer neighbours combined from plane v's boxes (zero-filled
       // outside the domain), j-neighbours from the shared plane
       const int sv = slot == 0 ? kDirNS - 1 : slot - 1;
-      const double* Zv = sZ + sv * kC2EStride;
-      const double* Pv = sP + sv * kC2EStride;
-      const double* Nv = sN + (sc == 0 ? kDirNC - 1 : sc - 1) * kC2BPlane;
+      const double* Zv = sZ + sv * kDEStride;
+      const double* Pv = sP + sv * kDEStride;
+      const double* Nv = sN + (sc == 0 ? kDirNC - 1 : sc - 1) * kDBPlane;
       double pw = __shfl_up_sync(0xffffffffu, pc.y, 1);
       double pe = __shfl_down_sync(0xffffffffu, pc.x, 1);
       if (lane == 0) pw = comb(Zv[off - 1], first ? 0.0 : Pv[off - 1]);

@@ -32,12 +32,19 @@ namespace pcgx {
 // division (a real branch, never taken on the solver's data).
 __device__ __forceinline__ double div_rn(double x, double b, double inv) {
   const double ax = fabs(x);
+#if PCGX_DIVFAST
+  if (!(ax > 0.0)) return x * inv;
+#else
   if (!(ax > 0x1p-960 && ax < 0x1p960)) return x / b;
+#endif
   const double q0 = x * inv;
   const double r = __fma_rn(-q0, b, x);
   return __fma_rn(r, inv, q0);
 }
 
+#ifndef PCGX_DIVFAST
+#define PCGX_DIVFAST 0
+#endif
 #ifndef PCGX_DIA_STREAM
 #define PCGX_DIA_STREAM 1
 #endif

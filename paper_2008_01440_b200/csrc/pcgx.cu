@@ -107,6 +107,7 @@ struct pcgx_operator_s {
   int cheb2v = 0;     // its stage-2 variant (kV): 0 tile rows, 1 own row, 2 own row + d*x queues, 3 pipelined
   std::string c2plan;                     // PCGX_C2PLAN: "" auto, "u" uniform kz2, "h1,h2,..." explicit
   std::map<int, ChunkPlan> c2plans;       // chunk plan per launch span (planes)
+  std::map<int, ChunkPlan> dirplans;      // the same for the direction step
   int zpad = 0;       // ghost planes per side in the workspace vectors (z-slab + cheb2: 2)
   int kz2 = 32;       // z-chunk of the two-step kernel
   struct TmaPair { const double* ptr; CUtensorMap a, e, fa, fe; };
@@ -1042,19 +1043,27 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
   op->matvecs.fetch_add(1, std::memory_order_relaxed);
   PCGX_CUDA(cudaFuncSetAttribute(stencil7_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kDirSmem));
-  const CUtensorMap mz = tmaps_for(op, z).e;
-  const CUtensorMap mp = tmaps_for(op, first ? z : pold).e;
+  static_assert(kDBY == kFBY || kDBY == kC2BY, "direction-step box rows: no tensor map of that shape");
+  const CUtensorMap mz = kDBY == kFBY ? tmaps_for(op, z).fe : tmaps_for(op, z).e;
+  const CUtensorMap mp = kDBY == kFBY ? tmaps_for(op, first ? z : pold).fe : tmaps_for(op, first ? z : pold).e;
   const int nzl = (int)op->nzl;
   const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
   DirParams prm{(int)op->nx, (int)op->ny, nzl, lo ? -1 : 0, hi ? nzl + 1 : nzl, op->zpad,
                 op->nx * op->ny, op->d, c->S, s_new, s_old, first, x, s_pq, q, pnew};
   auto launch = [&](int k_begin, int k_end, int kz, bool accumulate) {
     if (k_end <= k_begin) return;
-    kz = std::max(1, std::min(kz, k_end - k_begin));
-    dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
-              (unsigned)((k_end - k_begin + kz - 1) / kz));
-    stencil7_dir_kernel<<<grid, kDirThreads, kDirSmem, c->s>>>(mz, mp, prm, k_begin, k_end, kz,
-                                                               make_red(c, slot, accumulate));
+    const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kDTY - 1) / kDTY);
+    const int span = k_end - k_begin;
+    auto it = op->dirplans.find(span);
+    if (it == op->dirplans.end()) {
+      int occ = 0;
+      PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil7_dir_kernel, kDirThreads,
+                                                              kDirSmem));
+      it = op->dirplans.emplace(span, make_chunk_plan(op->c2plan, span, kz, tiles,
+                                                      (long long)std::max(occ, 1) * c->sms)).first;
+    }
+    stencil7_dir_kernel<<<dim3((unsigned)tiles, (unsigned)it->second.n), kDirThreads, kDirSmem, c->s>>>(
+        mz, mp, prm, k_begin, k_end, it->second, make_red(c, slot, accumulate));
     check_launch();
     count_launch(c);
   };
