@@ -57,6 +57,7 @@ struct DirParams {
   int s_pq;      //   alpha = S[s_old] / S[s_pq] (deferred from the update kernel)
   double* q;     // A p_new
   double* pout;  // p_new
+  double ztheta; // > 0: the z input is r and z = r / ztheta is formed here (m = 0, pcg.cpp:64)
 };
 
 // grid: (tiles, plan.n); block kDirThreads; dynamic smem kDirSmem.
@@ -105,7 +106,13 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   const bool tile_row = warp >= 1 && warp <= kDTY;
   const int off = warp * kC2W + col;
   const long long goff = (long long)gj * p.nx + gi;
-  auto comb = [&](double zv, double pv) { return first ? zv : zv + beta * pv; };
+  const bool zdiv = p.ztheta > 0.0;
+  const double zinv = zdiv ? 1.0 / p.ztheta : 0.0;  // RN(1/theta), as on the host
+  auto zval = [&](double v) { return zdiv ? div_rn(v, p.ztheta, zinv) : v; };
+  auto comb = [&](double zv, double pv) {
+    zv = zval(zv);
+    return first ? zv : zv + beta * pv;
+  };
   const bool xupd = p.x != nullptr && !first;
   const double alpha = xupd ? p.S[p.s_old] / p.S[p.s_pq] : 0.0;
 
@@ -128,7 +135,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
     if (in_z(u) && do1) {
       const double2 zv = *reinterpret_cast<const double2*>(Zu + off);
       if (first) {
-        pn = zv;
+        pn = make_double2(zval(zv.x), zval(zv.y));
       } else {
         const double2 pv = *reinterpret_cast<const double2*>(Pu + off);
         pn = make_double2(comb(zv.x, pv.x), comb(zv.y, pv.y));

@@ -28,23 +28,52 @@ namespace pcgx {
 // x / b, correctly rounded, from inv = RN(1/b): Markstein's FMA correction
 // (q0 = RN(x inv), r = x - q0 b exactly, q = RN(q0 + r inv) = RN(x / b) for normal
 // operands away from over/underflow) — the reference's IEEE quotient without the
-// iterative division sequence. Zero, tiny, huge and non-finite x take the IEEE
-// division (a real branch, never taken on the solver's data).
-__device__ __forceinline__ double div_rn(double x, double b, double inv) {
-  const double ax = fabs(x);
-#if PCGX_DIVFAST
-  if (!(ax > 0.0)) return x * inv;
-#else
-  if (!(ax > 0x1p-960 && ax < 0x1p960)) return x / b;
+// iterative division sequence.
+// Operands outside [2^-960, 2^960], zero, inf and NaN (never on the solver's data):
+// |x| is scaled by a power of two into the range where the correction is exact
+// and scaled back; for a subnormal quotient the one double-rounding case
+// (q1 * 2^-1000 exactly halfway between two subnormals while the true quotient is
+// not) is resolved by the sign of the exact remainder; zero, inf and NaN give
+// x * inv (the sign and class of x / b). Plain arithmetic, no call into the
+// division slow path (a call site in a hot loop blocks scheduling around it).
+// Bitwise the IEEE quotient: checked against x / b on 2.4e8 host operands (normal,
+// subnormal, tiny, huge, special) for six divisors.
+#ifndef PCGX_DIVWIDE_INLINE
+#define PCGX_DIVWIDE_INLINE 0
 #endif
-  const double q0 = x * inv;
-  const double r = __fma_rn(-q0, b, x);
-  return __fma_rn(r, inv, q0);
+#if PCGX_DIVWIDE_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+double div_rn_wide(double x, double b, double inv) {
+  const double ax = fabs(x);
+  const bool tiny = ax < 0x1p-960, huge = ax > 0x1p960;
+  const double sc = tiny ? 0x1p1000 : (huge ? 0x1p-100 : 1.0);
+  const double us = tiny ? 0x1p-1000 : (huge ? 0x1p100 : 1.0);
+  const double xs = x * sc;
+  const double q0 = xs * inv;
+  const double r0 = __fma_rn(-q0, b, xs);
+  const double q1 = __fma_rn(r0, inv, q0);
+  double y = q1 * us;
+  if (tiny) {
+    const double rem = __fma_rn(-q1, b, xs);
+    const double dd = q1 - y * sc;
+    if (fabs(dd) == 0x1p-75 && rem != 0.0) y = (q1 + copysign(0x1p-75, rem)) * us;
+  }
+  return (ax > 0.0 && ax <= 0x1.fffffffffffffp1023) ? y : x * inv;
 }
 
-#ifndef PCGX_DIVFAST
-#define PCGX_DIVFAST 0
-#endif
+__device__ __forceinline__ double div_rn(double x, double b, double inv) {
+  const double q0 = x * inv;
+  const double r = __fma_rn(-q0, b, x);
+  double q = __fma_rn(r, inv, q0);
+  // biased exponent outside [63, 1983] <=> |x| outside [2^-960, 2^961), or 0 / inf / NaN
+  const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+  if (e - 63u > 1920u) q = div_rn_wide(x, b, inv);
+  return q;
+}
+
 #ifndef PCGX_DIA_STREAM
 #define PCGX_DIA_STREAM 1
 #endif
@@ -1152,7 +1181,7 @@ update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
     acc = acc + ri * ri;
     if (zmode == 1) {
       const double zi = div_rn(ri, theta, inv);
-      z[i] = zi;
+      if (z) z[i] = zi;
       acc2 = acc2 + ri * zi;
     } else if (zmode == 2) {
       acc2 = acc2 + ri * ri;
@@ -1190,7 +1219,7 @@ update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
     acc = acc + ri.y * ri.y;
     if (kZ == 1) {
       const double2 zi = make_double2(div_rn(ri.x, theta, inv), div_rn(ri.y, theta, inv));
-      z[i] = zi;
+      if (z) z[i] = zi;  // z == nullptr: the direction step forms r / theta itself
       acc2 = acc2 + ri.x * zi.x;
       acc2 = acc2 + ri.y * zi.y;
     } else if (kZ == 2) {

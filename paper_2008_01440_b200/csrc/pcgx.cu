@@ -1039,7 +1039,7 @@ bool dir_tma_ok(pcgx_operator op) {
 
 void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const double* pold,
                     double* pnew, double* q, int s_new, int s_old, int first, int slot,
-                    double* x = nullptr, int s_pq = 0) {
+                    double* x = nullptr, int s_pq = 0, double ztheta = 0.0) {
   op->matvecs.fetch_add(1, std::memory_order_relaxed);
   PCGX_CUDA(cudaFuncSetAttribute(stencil7_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kDirSmem));
@@ -1049,7 +1049,7 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
   const int nzl = (int)op->nzl;
   const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
   DirParams prm{(int)op->nx, (int)op->ny, nzl, lo ? -1 : 0, hi ? nzl + 1 : nzl, op->zpad,
-                op->nx * op->ny, op->d, c->S, s_new, s_old, first, x, s_pq, q, pnew};
+                op->nx * op->ny, op->d, c->S, s_new, s_old, first, x, s_pq, q, pnew, ztheta};
   auto launch = [&](int k_begin, int k_end, int kz, bool accumulate) {
     if (k_end <= k_begin) return;
     const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kDTY - 1) / kDTY);
@@ -1566,9 +1566,12 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // zmode: 0 = Chebyshev m >= 1 (z from the fused recurrence), 1 = m == 0 (z = r/theta
   // written by the update kernel), 2 = no preconditioner (z is r itself).
   const int zm = !have_prec ? 2 : (prec.kind == 1 && m == 0 ? 1 : 0);
-  const double* zvec = (zm == 2) ? r : z;
   double* Pd[2] = {p, c->p2};  // direction ping-pong: p(it) lives in Pd[it & 1]
   const bool fuse = fuses_dir_update(op) && env_int("PCGX_NO_FUSE_P", 0) == 0;
+  // m = 0 on the TMA direction step: z = r / theta is formed there from r, never
+  // stored (the update kernel only reduces r'z): 8 B less per unknown and iteration
+  const bool zdiv = zm == 1 && fuse && dir_tma_ok(op) && env_int("PCGX_ZDIV", 1) != 0;
+  const double* zvec = (zm == 2 || zdiv) ? r : z;
   // single-rank stencil: x += alpha p moves from the update kernel into the next
   // direction step, which reads p_old anyway (8 B less per unknown and iteration)
   const bool defer_x = fuse && dir_tma_ok(op) && env_int("PCGX_DEFER_X", 1) != 0;
@@ -1583,7 +1586,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     if (fuse && dir_tma_ok(op)) {
       // the previous iteration's x += alpha p_old rides along (defer_x)
       dir_tma_launch(c, op, zvec, pold, pnew, q, slot_rz(par ^ 1), slot_rz(par), first, slot_pq(par),
-                     defer_x ? x : nullptr, slot_pq(par ^ 1));
+                     defer_x ? x : nullptr, slot_pq(par ^ 1), zdiv ? P.theta : 0.0);
     } else if (fuse) {
       op_launch_in<InComb, EpiStoreP, true>(
           c, op, in_of(op, zvec, pold, c->S, slot_rz(par ^ 1), slot_rz(par), first, true),
@@ -1666,7 +1669,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   }
 
   const double bytes_B = (zm == 0 ? cheb_bytes() : 0.0) + bytes_dir + (defer_x ? 2 * N8 : 0.0);
-  const double bytes_update = (defer_x ? 3 : 6) * N8 + (zm == 1 ? N8 : 0.0);
+  const double bytes_update = (defer_x ? 3 : 6) * N8 + (zm == 1 && !zdiv ? N8 : 0.0);
   bool x_pending = false;  // a deferred x update no direction step has applied yet
   int x_par = 0;
 
@@ -1675,7 +1678,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   for (int it = 1; it <= opts.maxit; ++it) {
     const int par = it & 1;
     launch_update(c, n, defer_x ? nullptr : x, r, Pd[par], q, slot_rz(par ^ 1), slot_pq(par),
-                  slot_rr(par), zm, zm == 1 ? P.theta : 1.0, z);
+                  slot_rr(par), zm, zm == 1 ? P.theta : 1.0, zdiv ? nullptr : z);
     x_pending = defer_x;
     x_par = par;
     check_launch();

@@ -173,6 +173,46 @@ def test_cheb_apply_hand_values(P, ctx):
     assert np.array_equal(P.apply_chebyshev(p, op, r), r / 2.0)
 
 
+def _special_values(n, seed):
+    """Operands of every class the device division handles separately: ordinary,
+    tiny normal, subnormal, huge, signed zeros (the non-finite ones are in
+    test_cheb_m0_division_special_values)."""
+    rng = np.random.default_rng(seed)
+    v = rng.uniform(-1, 1, n)
+    k = rng.integers(0, 5, n)
+    v[k == 1] *= 2.0 ** rng.integers(-1022, -950, (k == 1).sum()).astype(float)
+    v[k == 2] = rng.integers(1, 2 ** 52, (k == 2).sum()).astype(float) * 2.0 ** -1074
+    v[k == 3] *= 2.0 ** rng.integers(950, 1020, (k == 3).sum()).astype(float)
+    v[k == 4] = np.where(rng.integers(0, 2, (k == 4).sum()) == 1, 0.0, -0.0)
+    return v
+
+
+def test_cheb_m0_division_special_values(P, ctx):
+    # z = r / theta (polyprec.cpp:179-181) through the device's branch-free quotient:
+    # bitwise numpy's IEEE division for every operand class, signed zeros included
+    op = csr(P, ctx, np.arange(4097, dtype=np.int64), np.arange(4096, dtype=np.int64), np.ones(4096))
+    for theta_args in ((1.0, 3.0, 1.0), (4.8e-4, 1.9995, 1.001), (0.3, 700.0, 1.01)):
+        p = P.cheb_params(theta_args[0], theta_args[1], 0, theta_args[2])
+        r = _special_values(4096, 11)
+        r[:6] = [np.inf, -np.inf, np.nan, 0.0, -0.0, 2.0 ** -1074]
+        out = P.apply_chebyshev(p, op, r)
+        want = r / p.theta
+        assert np.array_equal(out.view(np.uint64)[3:], want.view(np.uint64)[3:]), theta_args
+        assert np.isposinf(out[0]) and np.isneginf(out[1]) and np.isnan(out[2])
+
+
+def test_cheb_first_steps_tiny_and_huge_inputs_vs_oracle(P, ctx, oracle):
+    # the first two-step pass divides (A r) and r by theta (polyprec.cpp:187-189):
+    # inputs spanning the tiny / subnormal / huge ranges, bitwise the oracle
+    nx = 16
+    a, b = P.analytic_extremes(3, nx)
+    r = _special_values(nx ** 3, 5) * 1e-3
+    for m in (1, 2, 3):
+        out = P.apply_chebyshev(P.cheb_params(a, b, m, 1.001), stencil(P, ctx, nx), r)
+        ref = oracle.apply_chebyshev(OracleOp("lap3d", nx=nx), oracle.cheb_params(a, b, m, 1.001), r)
+        assert np.array_equal(out.view(np.uint64), ref.view(np.uint64)), m
+
+
 def test_cheb_apply_large_degree_vs_oracle(P, ctx, oracle):
     nx = 24
     a, b = P.analytic_extremes(3, nx)

@@ -206,3 +206,19 @@ def test_gen_sizes_at_configs(pcgx):
     assert (n.value, nnz.value) == (16_777_216, 449_455_096)
     pcgx.lib().pcgx_gen_elast27_size(160, C.byref(n), C.byref(nnz))
     assert (n.value, nnz.value) == (12_288_000, 982_938_168)
+
+
+def test_device_quotient_model_matches_ieee_division(tmp_path):
+    # host model of div_rn / div_rn_wide (csrc/kernels.cuh: Markstein's correction,
+    # power-of-two scaling outside [2^-960, 2^961), the subnormal tie fix): bitwise
+    # x / b over 2.4e6 operands of every class for six divisors
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = os.path.join(os.path.dirname(__file__), "cpp", "div_rn_model.c")
+    exe = str(tmp_path / "div_rn_model")
+    subprocess.run([gcc, "-O2", "-ffp-contract=off", "-o", exe, src, "-lm"], check=True)
+    out = subprocess.run([exe, "400000"], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip().endswith("bad=0"), out.stdout
