@@ -352,7 +352,7 @@ def run_gpu(args):
                else f"working set {ws_bytes / 1e6:.0f} MB fits L2 (126 MB): L2-bound, not an HBM roofline claim")
     storage = op.storage()
     kdesc = {
-        "stencil": ("stencil7_cheb2_kernel (TMA, two fused SpMV + Chebyshev steps per pass, 40 B/unknown)"
+        "stencil": ("stencil7_cheb2f_kernel (TMA, two fused SpMV + Chebyshev steps per pass, software-pipelined, 64x20 tiles, 40 B/unknown)"
                     if step_bytes == 40.0 * n_loc else
                     "stencil7v2_kernel<EpiChebStep> (fused SpMV + Chebyshev step, 32 B/unknown)"),
         "sell32": "sell_kernel<EpiChebStep> (SELL-32 int32 CSR SpMV + Chebyshev step, 12 nnz + 4(n+1) + 40 n bytes)",

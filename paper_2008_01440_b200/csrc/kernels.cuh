@@ -81,8 +81,12 @@ __device__ __forceinline__ double div_rn(double x, double b, double inv) {
 #define PCGX_MAT_STREAM 1
 #endif
 // the value stream is read once: keep it out of L1 so the x / d gathers stay there
+// (when the matrix exceeds L2: an L2-resident one, cfg1's 56 MB, streams 20% slower
+// through the non-allocating path, so the operator picks the plain path there)
+template <bool kStream = true>
 __device__ __forceinline__ double ld_stream(const double* p) {
 #if PCGX_DIA_STREAM
+  if (!kStream) return __ldg(p);
   double v;
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
@@ -1132,7 +1136,7 @@ struct DiaGeom {
 #ifndef PCGX_DIA_MINB
 #define PCGX_DIA_MINB 8
 #endif
-template <class In, class Epi, bool kRed>
+template <class In, class Epi, bool kRed, bool kStream>
 __global__ void __launch_bounds__(256, PCGX_DIA_MINB)
 dia_kernel(DiaGeom g, In in, Epi epi, Reduce red) {
   in.init();
@@ -1149,7 +1153,7 @@ dia_kernel(DiaGeom g, In in, Epi epi, Reduce red) {
     for (int k = 0; k < g.K; ++k) {
       if (msk & (1u << k)) {
         const long long c = i + g.off[k];
-        sum = sum + ld_stream(g.val + k * g.ld + i) * (__ldg(g.dvec + c) * in.ldc(c));
+        sum = sum + ld_stream<kStream>(g.val + k * g.ld + i) * (__ldg(g.dvec + c) * in.ldc(c));
       }
     }
     const double y = sum * dr;

@@ -655,16 +655,18 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
     g.dvec = op->dvec;
     // one full wave of resident blocks, grid-stride over the rows (a partial second
     // wave would leave SMs idle at the tail)
+    const bool stream = (double)op->dia_k * (double)op->dia_ld * 8.0 > 64e6;  // values exceed ~half of L2
+    auto kern = stream ? dia_kernel<In, Epi, kRed, true> : dia_kernel<In, Epi, kRed, false>;
     static int occ = 0;
     if (!occ) {
-      PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dia_kernel<In, Epi, kRed>, 256, 0));
+      PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dia_kernel<In, Epi, kRed, true>, 256, 0));
       occ = std::max(occ, 1);
     }
     const long long want = (op->n_local + 255) / 256;
     const int bps = env_int("PCGX_DIA_BPS", 0);
     const int grid = (int)std::max(1LL, std::min(want, (long long)c->sms * (bps > 0 ? bps : occ)));
     Reduce red = kRed ? make_red(c, slot) : Reduce{};
-    dia_kernel<In, Epi, kRed><<<grid, 256, 0, c->s>>>(g, in, epi, red);
+    kern<<<grid, 256, 0, c->s>>>(g, in, epi, red);
     check_launch();
     count_launch(c);
     return;
