@@ -108,7 +108,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   const long long goff = (long long)gj * p.nx + gi;
   const bool zdiv = p.ztheta > 0.0;
   const double zinv = zdiv ? 1.0 / p.ztheta : 0.0;  // RN(1/theta), as on the host
-  auto zval = [&](double v) { return zdiv ? div_rn(v, p.ztheta, zinv) : v; };
+  auto zval = [&](double v) { return zdiv ? div_rn_z(v, p.ztheta, zinv) : v; };
   auto comb = [&](double zv, double pv) {
     zv = zval(zv);
     return first ? zv : zv + beta * pv;

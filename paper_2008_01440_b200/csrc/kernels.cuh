@@ -73,6 +73,18 @@ __device__ __forceinline__ double div_rn(double x, double b, double inv) {
   if (e - 63u > 1920u) q = div_rn_wide(x, b, inv);
   return q;
 }
+// The same quotient where zeros are frequent (zero-filled Dirichlet halo values in
+// the direction step): +-0 / b = +-0 by a select instead of the out-of-line path,
+// which a warp would otherwise take for every boundary lane (and the block barrier
+// would wait for it).
+__device__ __forceinline__ double div_rn_z(double x, double b, double inv) {
+  const double q0 = x * inv;
+  const double r = __fma_rn(-q0, b, x);
+  double q = __fma_rn(r, inv, q0);
+  const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+  if (e - 63u > 1920u && x != 0.0) q = div_rn_wide(x, b, inv);
+  return x == 0.0 ? x : q;
+}
 
 #ifndef PCGX_DIA_STREAM
 #define PCGX_DIA_STREAM 1

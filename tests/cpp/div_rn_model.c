@@ -25,11 +25,17 @@ static double wide(double x, double b, double inv) {
     if (fabs(dd) == 0x1p-75 && rem != 0.0) y = (q1 + copysign(0x1p-75, rem)) * us; }
   return (ax > 0.0 && ax <= 0x1.fffffffffffffp1023) ? y : x * inv;
 }
-static double div_rn(double x, double b, double inv) {
+static double div_rn_plain(double x, double b, double inv) {
   const double q0 = x * inv; const double r = fma(-q0, b, x); double q = fma(r, inv, q0);
   uint64_t u = ubits(x); unsigned e = (unsigned)((u >> 52) & 0x7ff);
   if (e - 63u > 1920u) q = wide(x, b, inv);
   return q;
+}
+static double div_rn(double x, double b, double inv) {  /* div_rn_z */
+  const double q0 = x * inv; const double r = fma(-q0, b, x); double q = fma(r, inv, q0);
+  uint64_t u = ubits(x); unsigned e = (unsigned)((u >> 52) & 0x7ff);
+  if (e - 63u > 1920u && x != 0.0) q = wide(x, b, inv);
+  return x == 0.0 ? x : q;
 }
 int main(int argc, char** argv){
   long bad=0, n=0;
@@ -45,7 +51,8 @@ int main(int argc, char** argv){
       else if(mode==3) x=bits((u & 0x800FFFFFFFFFFFFFULL) | ((uint64_t)(2046-(rnd()%90))<<52));
       else if(mode==4) x=bits((u & 0x800FFFFFFFFFFFFFULL) | ((uint64_t)(1980+(rnd()%6))<<52)); // around 2^960
       else x=((double)(int64_t)u)*0x1p-63;
-      double a=x/b, c=div_rn(x,b,inv); n++;
+      double a=x/b, c=div_rn(x,b,inv), c2=div_rn_plain(x,b,inv); n++;
+      if (ubits(a)!=ubits(c2) && !(isnan(a)&&isnan(c2))) { if(bad<10) printf("plain x=%a b=%a ieee=%a got=%a\n",x,b,a,c2); bad++; }
       if (ubits(a)!=ubits(c) && !(isnan(a)&&isnan(c))) { if(bad<10) printf("x=%a b=%a ieee=%a got=%a\n",x,b,a,c); bad++; }
     }
   }
