@@ -75,6 +75,12 @@ struct Cheb2Params {
   double c2, c3;            // 2/delta, 2 sigma
   double* outC;             // x_k   (interior tile points)
   double* outE;             // x_{k+1}
+  // fused PCG update (pipelined kernel, kFirst): A = r_old and the Q map hold
+  // r(it-1) and q(it); r = r_old - alpha q (pcg.cpp:83), alpha = S[s_rho] / S[s_pq],
+  // is formed in shared memory, written to rout and reduced as r'r
+  const double* S;
+  int s_rho, s_pq;
+  double* rout;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

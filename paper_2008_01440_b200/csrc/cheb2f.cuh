@@ -75,22 +75,27 @@ struct ChunkPlan {
   int start[kMax + 1];
 };
 
-template <bool kFirst, bool kRed, bool kT>
+template <bool kFirst, bool kRed, bool kT, bool kUpd = false>
 #if PCGX_C2FMINB == 1
 __global__ void __maxnreg__(PCGX_C2FMAXREG)
 #else
 __global__ void __launch_bounds__(kFThreads, PCGX_C2FMINB)
 #endif
 stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kFTY+4) box)
-                       const __grid_constant__ CUtensorMap mapB,  // B (68 x 10 box)
-                       const __grid_constant__ CUtensorMap mapR,  // R (68 x 10 box)
-                       Cheb2Params p, int k_begin, int k_end, const __grid_constant__ ChunkPlan plan, Reduce red) {
+                       const __grid_constant__ CUtensorMap mapB,  // B (68 x (kFTY+2) box); kUpd: Q (A's box)
+                       const __grid_constant__ CUtensorMap mapR,  // R (68 x (kFTY+2) box)
+                       Cheb2Params p, int k_begin, int k_end, const __grid_constant__ ChunkPlan plan, Reduce red,
+                       Reduce red_rr) {
+  static_assert(!kUpd || (kFirst && !kRed), "the PCG update is fused into a non-reducing first pass only");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sA = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   double* sB = sA + kFNA * kFAPlane;
   double* sR = sB + kFNB * kFEStride;
   double* sC = sR + kFNR * kFEStride;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kFNC * kFCStride);  // kFD unit bars + 1 prologue
+  // kUpd: the q ring (A's slots and box) lives where the first pass has no B / R
+  static_assert(kFNA * kFAPlane <= (kFNB + kFNR) * kFEStride, "q ring does not fit the B / R rings");
+  double* sQ = sB;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned bytesA = kFW * kFAY * 8, bytesB = kFBPlane * 8;  // box bytes (slots may be padded)
@@ -110,8 +115,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   auto issue_unit = [&](int u) {
     uint64_t* bar = &bars[(u - (kb - 1)) % kFD];
     const bool la = in_z(u + 1), lbr = !kFirst && in_z(u);
-    mbar_expect_tx(bar, (la ? bytesA : 0u) + (lbr ? 2 * bytesB : 0u));
+    mbar_expect_tx(bar, (la ? (kUpd ? 2 : 1) * bytesA : 0u) + (lbr ? 2 * bytesB : 0u));
     if (la) tma_load_3d(sA + ((u + 1 - (kb - 2)) % kFNA) * kFAPlane, &mapA, i0 - 2, j0 - 2, u + 1 + zo, bar);
+    if (kUpd && la)
+      tma_load_3d(sQ + ((u + 1 - (kb - 2)) % kFNA) * kFAPlane, &mapB, i0 - 2, j0 - 2, u + 1 + zo, bar);
     if (lbr) {
       tma_load_3d(sB + ((u - (kb - 1)) % kFNB) * kFEStride, &mapB, i0 - 2, j0 - 1, u + zo, bar);
       tma_load_3d(sR + ((u - (kb - 1)) % kFNR) * kFEStride, &mapR, i0 - 2, j0 - 1, u + zo, bar);
@@ -120,12 +127,33 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   const int u_last = ke;  // stage 1 runs t = kb-1 .. ke, stage 2 v = t-2 = kb .. ke-1
   if (tid == 0) {
     uint64_t* pb = &bars[kFD];
-    mbar_expect_tx(pb, (in_z(kb - 2) ? bytesA : 0u) + (in_z(kb - 1) ? bytesA : 0u));
+    const unsigned ba = (kUpd ? 2 : 1) * bytesA;
+    mbar_expect_tx(pb, (in_z(kb - 2) ? ba : 0u) + (in_z(kb - 1) ? ba : 0u));
     if (in_z(kb - 2)) tma_load_3d(sA, &mapA, i0 - 2, j0 - 2, kb - 2 + zo, pb);
     if (in_z(kb - 1)) tma_load_3d(sA + kFAPlane, &mapA, i0 - 2, j0 - 2, kb - 1 + zo, pb);
+    if (kUpd && in_z(kb - 2)) tma_load_3d(sQ, &mapB, i0 - 2, j0 - 2, kb - 2 + zo, pb);
+    if (kUpd && in_z(kb - 1)) tma_load_3d(sQ + kFAPlane, &mapB, i0 - 2, j0 - 2, kb - 1 + zo, pb);
     for (int u = kb - 1; u < kb - 1 + kFD && u <= u_last; ++u) issue_unit(u);
   }
   mbar_wait(&bars[kFD], 0);
+
+  // kUpd: every A value (r(it-1)) is read together with q(it) at the same offset of
+  // the q ring and combined on the fly into r(it) = r(it-1) - alpha q(it), the update
+  // kernel's element operation (pcg.cpp:83); the own row's new plane goes to rout
+  // and into r'r (each interior point once, when its plane enters the queue).
+  double acc_rr = 0.0;
+  const double alpha = kUpd ? p.S[p.s_rho] / p.S[p.s_pq] : 0.0;
+  const double* const sA0 = sA;
+  auto rq = [&](const double* a, int off) {  // r(it) at offset off of A slot a
+    const double v = a[off];
+    return kUpd ? v - alpha * sQ[(a - sA0) + off] : v;
+  };
+  auto rq2 = [&](const double* a, int off) {
+    const double2 v = *reinterpret_cast<const double2*>(a + off);
+    if (!kUpd) return v;
+    const double2 w = *reinterpret_cast<const double2*>(sQ + (a - sA0) + off);
+    return make_double2(v.x - alpha * w.x, v.y - alpha * w.y);
+  };
 
   const double d = p.d;
   const double inv_t = 1.0 / p.theta;
@@ -171,8 +199,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   // kT: the stencil queues hold t = d * x (each product formed once per point);
   // the recurrences' centre values travel in separate x queues
   auto mul2 = [&](double2 v) { return make_double2(d * v.x, d * v.y); };
-  double2 am = in_z(kb - 2) ? *reinterpret_cast<const double2*>(sA + offA) : zero2;
-  double2 ac = in_z(kb - 1) ? *reinterpret_cast<const double2*>(sA + kFAPlane + offA) : zero2;
+  double2 am = in_z(kb - 2) ? rq2(sA, offA) : zero2;
+  double2 ac = in_z(kb - 1) ? rq2(sA + kFAPlane, offA) : zero2;
   double2 x1 = ac;                             // kT: A[t-1] x (own row)
   if (kT) {
     am = mul2(am);
@@ -193,14 +221,19 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     // ---------------- stage 1: C[t] on the extended tile row
     if (s1) {
       const bool plane_in = t >= p.c_lo && t < p.c_hi, has_p = in_z(t + 1);
-      ap = has_p ? *reinterpret_cast<const double2*>(pAp + offA) : zero2;
+      ap = has_p ? rq2(pAp, offA) : zero2;
+      if (kUpd && has_p && interior && do1 && t + 1 >= kb && t + 1 < ke && t + 1 >= p.c_lo && t + 1 < p.c_hi) {
+        st2(p.rout + (long long)(t + 1) * p.nxy + (long long)gj * p.nx + gi, ap.x, ap.y);
+        acc_rr = acc_rr + ap.x * ap.x;
+        acc_rr = acc_rr + ap.y * ap.y;
+      }
       if (kT) ap = mul2(ap);
       double aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
       double ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
-      if (lane == 0) aw = kT ? d * pAu[offA - 1] : pAu[offA - 1];
-      if (lane == 31) ae = kT ? d * pAu[offA + 2] : pAu[offA + 2];
-      const double2 as = *reinterpret_cast<const double2*>(pAu + offA - kFW);
-      const double2 an = *reinterpret_cast<const double2*>(pAu + offA + kFW);
+      if (lane == 0) aw = kT ? d * pAu[offA - 1] : rq(pAu, offA - 1);
+      if (lane == 31) ae = kT ? d * pAu[offA + 2] : rq(pAu, offA + 2);
+      const double2 as = rq2(pAu, offA - kFW);
+      const double2 an = rq2(pAu, offA + kFW);
       double y0, y1;
       double2 xc;  // A[t] x at the pair
       if (kT) {
@@ -233,10 +266,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (do_h) {
         double hx = 0.0;
         if (plane_in && h_in) {
-          const double xc = pAu[offAh];
-          const double y = stencil_point(d, in_z(t - 1) ? pAm[offAh] : 0.0, pAu[offAh - kFW],
-                                         pAu[offAh - 1], xc, pAu[offAh + 1], pAu[offAh + kFW],
-                                         has_p ? pAp[offAh] : 0.0);
+          const double xc = rq(pAu, offAh);
+          const double y = stencil_point(d, in_z(t - 1) ? rq(pAm, offAh) : 0.0, rq(pAu, offAh - kFW),
+                                         rq(pAu, offAh - 1), xc, rq(pAu, offAh + 1), rq(pAu, offAh + kFW),
+                                         has_p ? rq(pAp, offAh) : 0.0);
           if (kFirst) hx = p.c1 * ((2.0 * xc) - div_rn(y, p.theta, inv_t));
           else hx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * pBu[offBh])) + p.c2 * (pRu[offBh] - y));
         }
@@ -277,7 +310,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         if (kRed) acc = acc + (rv.x * e0 + rv.y * e1);
       }
     }
-    __syncthreads();
+      __syncthreads();
     // rotate the register queues, rings and global pointers by one plane
     if (kT) {
       a2 = x1;
@@ -313,6 +346,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     gEv += p.nxy;
   }
   if (kRed) block_reduce_finish(acc, red);
+  if (kUpd) block_reduce_finish(acc_rr, red_rr);
 }
 
 }  // namespace pcgx

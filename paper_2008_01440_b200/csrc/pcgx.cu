@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <queue>
 #include <memory>
@@ -73,7 +74,8 @@ struct pcgx_context_s {
   // workspace (device), sized for the largest operator used
   long long ws_n = 0, ws_pad = 0;
   double *r = nullptr, *z = nullptr, *p = nullptr, *p2 = nullptr, *q = nullptr, *w0 = nullptr,
-         *w1 = nullptr, *w2 = nullptr, *w3 = nullptr, *t0 = nullptr, *t1 = nullptr;
+         *w1 = nullptr, *w2 = nullptr, *w3 = nullptr, *t0 = nullptr, *t1 = nullptr,
+         *r2 = nullptr;  // r ping-pong partner when the update is fused into P r
   double* flush = nullptr;
   size_t flush_bytes = 0;
   // Newton-form level vectors L[0..nlev-1] (NewtonWorkspace, polyprec.hpp:69-71)
@@ -264,7 +266,8 @@ long long ws_pad_of(pcgx_operator op) { return op->zpad * op->nx * op->ny; }
 // two ghost planes per side that the two-step kernel reads through TMA).
 void ensure_workspace(pcgx_context c, long long n, long long pad = 0) {
   if (c->ws_n >= n && c->ws_pad == pad) return;
-  double** bufs[] = {&c->r, &c->z, &c->p, &c->p2, &c->q, &c->w0, &c->w1, &c->w2, &c->w3, &c->t0, &c->t1};
+  double** bufs[] = {&c->r, &c->z, &c->p, &c->p2, &c->q, &c->w0, &c->w1, &c->w2, &c->w3, &c->t0, &c->t1,
+                     &c->r2};
   for (double** b : bufs) {
     if (*b) cudaFree(*b - c->ws_pad);
     *b = nullptr;
@@ -1018,7 +1021,7 @@ void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const doubl
     const ChunkPlan& plan = it->second;
     Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
     kern<<<dim3((unsigned)tiles, (unsigned)plan.n), kFThreads, kC2FSmem, c->s>>>(ma, mb, mr, prm, k_begin,
-                                                                                  k_end, plan, red);
+                                                                                  k_end, plan, red, Reduce{});
     check_launch();
     count_launch(c);
     return;
@@ -1141,6 +1144,53 @@ void cheb2_pass(pcgx_context c, pcgx_operator op, const double* A, const double*
   if (ie < nzl) cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, ie, nzl, 2, wrote);
 }
 
+// The PCG update r(it) = r(it-1) - alpha q(it) and r'r fused into the first
+// two-step pass of P r(it) (pipelined kernel, single rank): the pass reads r(it-1)
+// and q(it) through TMA, forms r(it) in shared memory (bitwise the update kernel's
+// element operations), writes it to rnew and reduces r'r into s_rr. Saves the
+// update launch and 8 B per unknown and iteration.
+struct CgUpd {
+  const double* rold;
+  const double* q;
+  double* rnew;
+  int s_rho, s_pq, s_rr;
+};
+
+bool cheb_upd_ok(pcgx_context c, pcgx_operator op, int m) {
+  return m >= 3 && op->kind == 0 && op->cheb2 && op->cheb2v >= 3 && !c->cm && op->zpad == 0 &&
+         env_int("PCGX_FUSE_UPD", 1) != 0;
+}
+
+void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Params prm) {
+  op->matvecs.fetch_add(2, std::memory_order_relaxed);
+  const int nzl = (int)op->nzl;
+  prm.zoff = op->zpad;
+  prm.a_lo = 0;
+  prm.a_hi = nzl;
+  prm.c_lo = 0;
+  prm.c_hi = nzl;
+  prm.S = c->S;
+  prm.s_rho = u.s_rho;
+  prm.s_pq = u.s_pq;
+  prm.rout = u.rnew;
+  auto kern = stencil7_cheb2f_kernel<true, false, false, true>;
+  PCGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2FSmem));
+  const CUtensorMap ma = tmaps_for(op, u.rold).fa;
+  const CUtensorMap mq = tmaps_for(op, u.q).fa;
+  const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kFTY - 1) / kFTY);
+  auto it = op->c2plans.find(nzl);
+  if (it == op->c2plans.end()) {
+    int occ = 0;
+    PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFThreads, kC2FSmem));
+    it = op->c2plans.emplace(nzl, make_chunk_plan(op->c2plan, nzl, op->kz2, tiles,
+                                                  (long long)std::max(occ, 1) * c->sms)).first;
+  }
+  kern<<<dim3((unsigned)tiles, (unsigned)it->second.n), kFThreads, kC2FSmem, c->s>>>(
+      ma, mq, ma, prm, 0, nzl, it->second, Reduce{}, make_red(c, u.s_rr));
+  check_launch();
+  count_launch(c);
+}
+
 // ---------------------------------------------------------------- Chebyshev apply
 
 struct Cheb {
@@ -1164,7 +1214,8 @@ Cheb cheb_from(const pcgx_cheb* p) {
 // out = p_m(A) r (polyprec.cpp:169-198); rz_slot >= 0 also reduces r . out there.
 // Uses c->w0, c->w1 as the recurrence workspace. out must not alias r, w0, w1.
 void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double* r, double* out,
-                  int rz_slot) {
+                  int rz_slot, const CgUpd* upd = nullptr, const std::function<void()>& after_first = {}) {
+  // upd: r is r(it) = upd->rnew, produced by the first pass itself (cheb_upd_ok)
   const long long n = op->n_local;
   if (P.m == 0) {  // out = r / theta
     launch_zr(c, n, out, r, P.theta, 1, rz_slot >= 0 ? rz_slot : S_DOT2);
@@ -1197,8 +1248,10 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
     q.rk2m1 = P.rho[1];
     q.outC = bufs[0];
     q.outE = last12 ? out : bufs[1];
-    if (last12 && rz_slot >= 0) cheb2_pass<true, true>(c, op, r, nullptr, r, q, rz_slot);
+    if (upd) cheb2f_upd_launch(c, op, *upd, q);
+    else if (last12 && rz_slot >= 0) cheb2_pass<true, true>(c, op, r, nullptr, r, q, rz_slot);
     else cheb2_pass<true, false>(c, op, r, nullptr, r, q, -1);
+    if (after_first) after_first();
     if (last12) return;
     int iold = 0, icur = 1;  // x_{k-2}, x_{k-1} buffer indices
     int k = 3;
@@ -1577,6 +1630,11 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // single-rank stencil: x += alpha p moves from the update kernel into the next
   // direction step, which reads p_old anyway (8 B less per unknown and iteration)
   const bool defer_x = fuse && dir_tma_ok(op) && env_int("PCGX_DEFER_X", 1) != 0;
+  // one GPU, Chebyshev m >= 3 on the stencil: the update r -= alpha q, r'r rides in
+  // the first two-step pass of P r (cheb2f_upd_launch); r(it) lives in Rb[it & 1]
+  const bool fuse_upd = zm == 0 && prec.kind == 1 && spec_after_update && defer_x &&
+                        cheb_upd_ok(c, op, m);
+  double* Rb[2] = {r, fuse_upd ? c->r2 : r};
 
   // dir_spmv(it): p(it) = z + beta p(it-1) (p(1) = z), q = A p(it), p'q -> pq(par); the
   // direction update is fused into the SpMV's input (InComb) where the kernels allow it.
@@ -1613,7 +1671,12 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // B(it): [prec(it) -> z, r'z ; multi-GPU: all-reduce (r'r, r'z) + snapshot] ; dir_spmv(it+1)
   auto enqueue_B = [&](int it) {
     const int par = it & 1;
-    if (zm == 0) {
+    if (fuse_upd) {
+      // r(it) = r(it-1) - alpha(it) q(it) inside P r(it)'s first pass; the scalar
+      // snapshot (r'r(it), p'q(it)) is taken right after that pass
+      const CgUpd u{Rb[par ^ 1], q, Rb[par], slot_rz(par ^ 1), slot_pq(par), slot_rr(par)};
+      enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u, [&] { snapshot(); });
+    } else if (zm == 0) {
       enqueue_prec(c, op, prec, r, z, slot_rz(par));
       if (!spec_after_update) {
         allreduce(c, slot_rr(par), 2);
@@ -1634,7 +1697,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     auto add = [&](const void* v, size_t bytes) { key.append((const char*)v, bytes); };
     const uint64_t ids[3] = {op->uid, c->ws_gen, defer_x ? (uint64_t)(uintptr_t)x : 0};
     add(ids, sizeof ids);
-    const int flags[5] = {prec.kind, m, zm, fuse ? 1 : 0, spec_after_update ? 1 : 0};
+    const int flags[6] = {prec.kind, m, zm, fuse ? 1 : 0, spec_after_update ? 1 : 0, fuse_upd ? 1 : 0};
     add(flags, sizeof flags);
     if (prec.kind == 1) {
       const double t[3] = {P.theta, P.delta, P.sigma};
@@ -1670,7 +1733,9 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
            "pcg_solve: r'z = " + fmt_double(rho) + " at setup (preconditioner not SPD?)");
   }
 
-  const double bytes_B = (zm == 0 ? cheb_bytes() : 0.0) + bytes_dir + (defer_x ? 2 * N8 : 0.0);
+  // fused: the first pass also reads q and writes r (+16 B), the update (24 B) is gone
+  const double bytes_B = (zm == 0 ? cheb_bytes() : 0.0) + bytes_dir + (defer_x ? 2 * N8 : 0.0) +
+                         (fuse_upd ? 2 * N8 : 0.0);
   const double bytes_update = (defer_x ? 3 : 6) * N8 + (zm == 1 && !zdiv ? N8 : 0.0);
   bool x_pending = false;  // a deferred x update no direction step has applied yet
   int x_par = 0;
@@ -1679,17 +1744,20 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   alg += bytes_dir;
   for (int it = 1; it <= opts.maxit; ++it) {
     const int par = it & 1;
-    launch_update(c, n, defer_x ? nullptr : x, r, Pd[par], q, slot_rz(par ^ 1), slot_pq(par),
-                  slot_rr(par), zm, zm == 1 ? P.theta : 1.0, zdiv ? nullptr : z);
+    const bool more = it < opts.maxit;
+    const bool upd_in_B = fuse_upd && more;  // else a standalone update (in place)
+    if (!upd_in_B) {
+      launch_update(c, n, defer_x ? nullptr : x, Rb[par ^ 1], Pd[par], q, slot_rz(par ^ 1), slot_pq(par),
+                    slot_rr(par), zm, zm == 1 ? P.theta : 1.0, zdiv ? nullptr : z);
+      check_launch();
+      count_launch(c);
+      alg += bytes_update;
+    }
     x_pending = defer_x;
     x_par = par;
-    check_launch();
-    count_launch(c);
-    alg += bytes_update;
     rep->matvec++;  // q = A p of this iteration
-    const bool more = it < opts.maxit;
     if (!spec_after_update && (zm > 0 || !more)) allreduce(c, slot_rr(par), zm > 0 ? 2 : 1);
-    if (snap_after_update || !more) snapshot();
+    if ((snap_after_update && !upd_in_B) || !more) snapshot();
     if (more) {
       if (use_graph) {
         replay(c, *gB[par]);
@@ -2599,7 +2667,7 @@ void pcgx_context_destroy(pcgx_context c) {
   cudaStreamSynchronize(c->s);
   if (c->comm) nccl().CommDestroy(c->comm);
   delete c->cm;
-  double* ws[] = {c->r, c->z, c->p, c->p2, c->q, c->w0, c->w1, c->w2, c->w3, c->t0, c->t1};
+  double* ws[] = {c->r, c->z, c->p, c->p2, c->q, c->w0, c->w1, c->w2, c->w3, c->t0, c->t1, c->r2};
   for (double* b : ws)
     if (b) cudaFree(b - c->ws_pad);
   double* bufs[] = {c->flush, c->S, c->partials};

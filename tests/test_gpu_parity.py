@@ -493,6 +493,52 @@ def test_pcg_schedules_agree(P, ctx, oracle, env, m, monkeypatch):
         assert rel_norm(x, xo) <= 1e-10
 
 
+@pytest.mark.parametrize("dims,m", [((24, 24, 24), 3), ((24, 24, 24), 4), ((20, 30, 26), 5),
+                                    ((32, 32, 32), 20), ((66, 44, 28), 7)])
+def test_pcg_fused_update_bitwise_vs_separate(P, ctx, oracle, dims, m, monkeypatch):
+    """The update fused into the first two-step pass of P r (r(it) ping-ponged
+    between two buffers) performs the update kernel's element operations: the same
+    iterations, scalar products, matvecs and a bitwise identical solution; only the
+    r'r reduction tree differs (rel_res within 1e-13)."""
+    nx, ny, nz = dims
+    op = stencil(P, ctx, nx, ny, nz)
+    a, b = P.analytic_extremes(3, max(dims))
+    xt = P.random_uniform_vector(nx * ny * nz, SEED)
+    rhs = op.apply(xt)
+    prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001))
+    runs = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("PCGX_FUSE_UPD", fused)
+        runs[fused] = P.pcg_solve(op, rhs, None, prec)
+        # a second solve replays the cached graphs of the same schedule
+        x2, r2 = P.pcg_solve(op, rhs, None, prec)
+        assert np.array_equal(x2, runs[fused][0]) and r2.iters == runs[fused][1].iters
+    (x1, r1), (x0, r0) = runs["1"], runs["0"]
+    assert r1.converged and r1.iters == r0.iters and r1.ddot == r0.ddot and r1.matvec == r0.matvec
+    assert np.array_equal(x1, x0)
+    assert abs(r1.rel_res - r0.rel_res) <= 1e-13 * r0.rel_res
+    assert r1.kernel_launches < r0.kernel_launches
+    if dims == (24, 24, 24):
+        po = oracle.cheb_params(a, b, m, 1.001)
+        xo, ro = oracle.pcg_solve(OracleOp("lap3d", nx=nx), po, rhs)
+        assert abs(r1.iters - ro["iters"]) <= 1 and rel_norm(x1, xo) <= 1e-10
+
+
+def test_pcg_fused_update_iteration_limit(P, ctx, monkeypatch):
+    # maxit stops the loop on an iteration whose update runs standalone (in place)
+    nx = 24
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    rhs = op.apply(P.random_uniform_vector(nx ** 3, SEED))
+    prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, 6, 1.001))
+    out = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("PCGX_FUSE_UPD", fused)
+        out[fused] = P.pcg_solve(op, rhs, P.SolveOptions(maxit=3), prec)
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert out["1"][1].iters == out["0"][1].iters == 3 and not out["1"][1].converged
+
+
 def test_pcg_csr_fallback_kernels(P, ctx, oracle, golden, monkeypatch):
     """csr2 (TMA tiles) and the chunked CSR kernel: not fused with the direction update."""
     c = _golden_case(golden, "csr300_m7")
