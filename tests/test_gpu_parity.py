@@ -433,13 +433,23 @@ def test_cfg2_320_k20_known_answer(P, ctx):
 
 # ------------------------------------------------------------------ two-step (temporal blocking) kernel
 
-@pytest.mark.parametrize("dims", [(24, 24, 24), (66, 10, 9), (64, 8, 1), (130, 17, 33), (2, 2, 2)])
-@pytest.mark.parametrize("kz2", ["1", "5", "32"])
-def test_cheb2_bitwise_vs_oracle(P, ctx, oracle, dims, kz2, monkeypatch):
-    """stencil7_cheb2_kernel (two degree steps per pass, TMA tiles with zero-filled
-    halos) must reproduce every per-step value of the reference recurrence."""
+@pytest.mark.parametrize("dims", [(24, 24, 24), (66, 10, 9), (64, 8, 1), (130, 17, 33), (2, 2, 2),
+                                  (130, 47, 41), (64, 61, 7)])
+@pytest.mark.parametrize("plan", [("3", "", "32"), ("3", "u", "1"), ("3", "u", "5"), ("3", "3,2,1,1", "7"),
+                                  ("0", "", "5"), ("0", "", "32")])
+def test_cheb2_bitwise_vs_oracle(P, ctx, oracle, dims, plan, monkeypatch):
+    """The two-step kernels (pipelined stencil7_cheb2f_kernel: automatic chunk plan,
+    uniform chunks of kz planes, an explicit plan; round-1 stencil7_cheb2_kernel:
+    uniform chunks) must reproduce every per-step value of the reference recurrence
+    (partial tiles in i and j, single planes, chunks of one plane)."""
+    variant, spec, kz2 = plan
+    if spec == "3,2,1,1" and dims[2] != 7:
+        spec = ""  # an explicit plan only applies to a launch of exactly that span
+    monkeypatch.setenv("PCGX_CHEB2V", variant)
+    monkeypatch.setenv("PCGX_C2PLAN", spec)
     monkeypatch.setenv("PCGX_KZ2", kz2)
     monkeypatch.setenv("PCGX_CHEB2", "1")
+    kz2 = plan
     nx, ny, nz = dims
     op = stencil(P, ctx, nx, ny, nz)
     opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
