@@ -77,6 +77,7 @@ struct Reduce {
   unsigned* counter = nullptr;
   double* result = nullptr;
   int accumulate = 0;
+  double* mirror = nullptr;  // != nullptr: the result also goes to this host-mapped slot
 };
 
 // Geometry of one (slab of a) 7-point stencil operator.

@@ -205,7 +205,9 @@ __device__ __forceinline__ void block_reduce_finish(double v, const Reduce& red)
     s = lane < nwarps ? ws[lane] : 0.0;
     s = warp_sum(s);
     if (lane == 0) {
-      *red.result = red.accumulate ? (*red.result + s) : s;
+      const double res = red.accumulate ? (*red.result + s) : s;
+      *red.result = res;
+      if (red.mirror) *red.mirror = res;
       *red.counter = 0u;
       __threadfence();
     }
@@ -261,6 +263,10 @@ __device__ __forceinline__ void block_reduce_finish2(double v0, double v1, const
     if (lane == 0) {
       red.result[0] = s0;
       red.result[1] = s1;
+      if (red.mirror) {
+        red.mirror[0] = s0;
+        red.mirror[1] = s1;
+      }
       *red.counter = 0u;
       __threadfence();
     }
@@ -315,6 +321,8 @@ __device__ __forceinline__ void block_reduce_finishN(const double (&vin)[N], con
     if (lane == 0) {
 #pragma unroll
       for (int k = 0; k < N; ++k) red.result[k] = v[k];
+      if (red.mirror)
+        for (int k = 0; k < N; ++k) red.mirror[k] = v[k];
       *red.counter = 0u;
       __threadfence();
     }

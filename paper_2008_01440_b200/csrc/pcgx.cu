@@ -63,7 +63,8 @@ struct pcgx_context_s {
   ncclComm_t comm = nullptr;
   struct CommBase* cm = nullptr;  // nullptr on a single-GPU context
   double* S = nullptr;        // device scalars
-  double* hS = nullptr;       // pinned mirror
+  double* hS = nullptr;       // pinned mirror (host-mapped)
+  double* dS_map = nullptr;   // hS as seen from the device: single-rank reductions store there too
   double* partials = nullptr;
   unsigned* counter = nullptr;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_sync = nullptr, ev_fork = nullptr,
@@ -247,6 +248,9 @@ Reduce make_red(pcgx_context c, int slot, bool accumulate = false) {
   r.counter = c->counter;
   r.result = c->S + slot;
   r.accumulate = accumulate ? 1 : 0;
+  // one rank: the reducing block also stores the scalar into the host-mapped slot
+  // array, so a solve's per-iteration snapshot is an event, not a D2H copy
+  r.mirror = (!c->cm && c->dS_map) ? c->dS_map + slot : nullptr;
   return r;
 }
 
@@ -1661,8 +1665,12 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     allreduce(c, slot_pq(par), 1);
   };
   const double bytes_dir = fuse ? spmv_alg_bytes(op) + 2 * N8 : spmv_alg_bytes(op) + 3 * N8;
+  // one rank: every scalar the host checks reached hS from its reducing kernel
+  // (Reduce::mirror); several ranks: the all-reduced slots are copied
+  const bool snap_copy = c->cm != nullptr || env_int("PCGX_SNAP_MEMCPY", 0) != 0;
   auto snapshot = [&]() {  // External: when captured, the graph records ev_sync on every replay
-    PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
+    if (snap_copy)
+      PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
     if (c->capturing) PCGX_CUDA(cudaEventRecordWithFlags(c->ev_sync, c->s, cudaEventRecordExternal));
     else PCGX_CUDA(cudaEventRecord(c->ev_sync, c->s));
   };
@@ -1697,7 +1705,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     auto add = [&](const void* v, size_t bytes) { key.append((const char*)v, bytes); };
     const uint64_t ids[3] = {op->uid, c->ws_gen, defer_x ? (uint64_t)(uintptr_t)x : 0};
     add(ids, sizeof ids);
-    const int flags[6] = {prec.kind, m, zm, fuse ? 1 : 0, spec_after_update ? 1 : 0, fuse_upd ? 1 : 0};
+    const int flags[7] = {prec.kind, m,        zm, fuse ? 1 : 0, spec_after_update ? 1 : 0, fuse_upd ? 1 : 0,
+                          snap_copy ? 1 : 0};
     add(flags, sizeof flags);
     if (prec.kind == 1) {
       const double t[3] = {P.theta, P.delta, P.sigma};
@@ -2567,7 +2576,8 @@ void ctx_init(pcgx_context c) {
   PCGX_CUDA(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
   PCGX_CUDA(cudaMalloc(&c->S, sizeof(double) * kSlots));
   PCGX_CUDA(cudaMemset(c->S, 0, sizeof(double) * kSlots));
-  PCGX_CUDA(cudaMallocHost(&c->hS, sizeof(double) * kSlots));
+  PCGX_CUDA(cudaHostAlloc(&c->hS, sizeof(double) * kSlots, cudaHostAllocMapped));
+  PCGX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dS_map), c->hS, 0));
   PCGX_CUDA(cudaMalloc(&c->partials, sizeof(double) * kMaxBlocks));
   PCGX_CUDA(cudaMalloc(&c->counter, sizeof(unsigned) * 4));
   PCGX_CUDA(cudaMemset(c->counter, 0, sizeof(unsigned) * 4));
