@@ -1183,6 +1183,132 @@ dia_kernel(DiaGeom g, In in, Epi epi, Reduce red) {
   if (kRed) block_reduce_finish(acc, red);
 }
 
+// ----------------------------------------------------------------- offset storage on a grid
+// The offset storage of a matrix on a cubic nx^3 grid whose column offsets are
+// exactly a structured pattern (the 27-point box, cfg3; the 7-point star, cfg1)
+// and whose couplings never wrap across a grid face (checked at upload). Slot s
+// of the storage is then the grid neighbour (dz, dy, dx) of DiaPat<P>, in the
+// same ascending-offset order. Instead of gathering d_c and x_c per slot through
+// L1 (dia_kernel: 54 dependent gathers per row, latency-bound), a CTA owns a
+// 32 x 8 column tile, marches its z-chunk and stages t = d * x of a 34 x 10 patch
+// per plane in a 4-plane shared ring (the product ScaledOperator forms,
+// linop.cpp:272); a row's terms are its value stream times ring reads, added in
+// slot order, absent slots skipped — the row sums are bitwise dia_kernel's.
+template <int P>
+struct DiaPat;
+template <>
+struct DiaPat<27> {
+  static constexpr int K = 27;
+  __host__ __device__ static constexpr int dz(int s) { return s / 9 - 1; }
+  __host__ __device__ static constexpr int dy(int s) { return (s / 3) % 3 - 1; }
+  __host__ __device__ static constexpr int dx(int s) { return s % 3 - 1; }
+};
+template <>
+struct DiaPat<7> {  // k-1, j-1, i-1, centre, i+1, j+1, k+1
+  static constexpr int K = 7;
+  __host__ __device__ static constexpr int dz(int s) { return s == 0 ? -1 : (s == 6 ? 1 : 0); }
+  __host__ __device__ static constexpr int dy(int s) { return s == 1 ? -1 : (s == 5 ? 1 : 0); }
+  __host__ __device__ static constexpr int dx(int s) { return s == 2 ? -1 : (s == 4 ? 1 : 0); }
+};
+
+#ifndef PCGX_D3X
+#define PCGX_D3X 32
+#endif
+#ifndef PCGX_D3Y
+#define PCGX_D3Y 8
+#endif
+constexpr int kD3X = PCGX_D3X, kD3Y = PCGX_D3Y, kD3PX = kD3X + 2, kD3PY = kD3Y + 2;
+constexpr int kD3Plane = kD3PX * kD3PY, kD3Threads = kD3X * kD3Y;
+static_assert(kD3Plane <= 2 * kD3Threads, "two staged patch elements per thread");
+
+struct Dia3Geom {
+  int nx, kz;  // grid edge, planes per z-chunk
+  long long ld;
+  const double* val;
+  const unsigned* mask;
+  const double* dvec;
+};
+
+#ifndef PCGX_DIA3_MINB
+#define PCGX_DIA3_MINB 3
+#endif
+template <int P, class In, class Epi, bool kRed, bool kStream>
+__global__ void __launch_bounds__(kD3Threads, PCGX_DIA3_MINB)
+dia3_kernel(Dia3Geom g, In in, Epi epi, Reduce red) {
+  __shared__ double sT[4][kD3Plane];
+  using Pat = DiaPat<P>;
+  in.init();
+  const int nx = g.nx;
+  const long long nxy = (long long)nx * nx;
+  const int tiles_x = (nx + kD3X - 1) / kD3X;
+  const int i0 = (int)(blockIdx.x % tiles_x) * kD3X, j0 = (int)(blockIdx.x / tiles_x) * kD3Y;
+  const int kb = blockIdx.y * g.kz, ke = min(kb + g.kz, nx);
+  const int tid = threadIdx.x, tx = tid % kD3X, ty = tid / kD3X;
+  const int i = i0 + tx, j = j0 + ty;
+  const bool own = i < nx && j < nx;
+  // the two patch elements this thread stages
+  const int e1 = tid + kD3Threads;
+  const int pi0 = i0 - 1 + tid % kD3PX, pj0 = j0 - 1 + tid / kD3PX;
+  const int pi1 = i0 - 1 + e1 % kD3PX, pj1 = j0 - 1 + e1 / kD3PX;
+  const bool in0 = pi0 >= 0 && pi0 < nx && pj0 >= 0 && pj0 < nx;
+  const bool in1 = e1 < kD3Plane && pi1 >= 0 && pi1 < nx && pj1 >= 0 && pj1 < nx;
+  const long long c0 = (long long)pj0 * nx + pi0, c1 = (long long)pj1 * nx + pi1;
+  auto stage = [&](int k, double& t0, double& t1) {
+    const bool kin = k >= 0 && k < nx;
+    const long long kb0 = (long long)k * nxy;
+    t0 = (kin && in0) ? __ldg(g.dvec + kb0 + c0) * in.ldc(kb0 + c0) : 0.0;
+    t1 = (kin && in1) ? __ldg(g.dvec + kb0 + c1) * in.ldc(kb0 + c1) : 0.0;
+  };
+  auto put = [&](int k, double t0, double t1) {
+    double* s = sT[(k + 4) & 3];
+    s[tid] = t0;
+    if (e1 < kD3Plane) s[e1] = t1;
+  };
+  {
+    double a0, a1, b0, b1, c0v, c1v;
+    stage(kb - 1, a0, a1);
+    stage(kb, b0, b1);
+    stage(kb + 1, c0v, c1v);
+    put(kb - 1, a0, a1);
+    put(kb, b0, b1);
+    put(kb + 1, c0v, c1v);
+  }
+  __syncthreads();
+  const int own_off = (ty + 1) * kD3PX + tx + 1;
+  double acc = 0.0;
+  for (int k = kb; k < ke; ++k) {
+    double n0, n1;
+    stage(k + 2, n0, n1);  // plane k+2, stored after this plane's rows
+    if (own) {
+      const long long row = (long long)k * nxy + (long long)j * nx + i;
+      double ev[2];
+      epi.ld(row, ev);
+      const double xr = in.ld1(row);
+      const double dr = __ldg(g.dvec + row);
+      const unsigned msk = __ldg(g.mask + row);
+      double v[Pat::K];
+#pragma unroll
+      for (int s = 0; s < Pat::K; ++s)
+        v[s] = ((msk >> s) & 1u) ? ld_stream<kStream>(g.val + s * g.ld + row) : 0.0;
+      const double* pm = sT[(k + 3) & 3] + own_off;
+      const double* p0 = sT[k & 3] + own_off;
+      const double* pp = sT[(k + 1) & 3] + own_off;
+      double sum = 0.0;
+#pragma unroll
+      for (int s = 0; s < Pat::K; ++s) {
+        const double* pl = Pat::dz(s) < 0 ? pm : (Pat::dz(s) == 0 ? p0 : pp);
+        if ((msk >> s) & 1u) sum = sum + v[s] * pl[Pat::dy(s) * kD3PX + Pat::dx(s)];
+      }
+      const double y = sum * dr;
+      const double cc = epi.st(row, y, xr, ev);
+      if (kRed) acc = acc + cc;
+    }
+    put(k + 2, n0, n1);
+    __syncthreads();
+  }
+  if (kRed) block_reduce_finish(acc, red);
+}
+
 // ----------------------------------------------------------------- vector kernels
 // Grid-stride over a fixed grid (deterministic element -> thread map).
 

@@ -140,6 +140,7 @@ struct pcgx_operator_s {
   int dia_k = 0;
   int dia_off[32] = {0};
   long long dia_ld = 0;
+  int dia3_pat = 0, dia3_nx = 0;  // structured pattern (27 / 7) on an nx^3 grid (dia3_kernel)
   // CSR block rows on a multi-rank context: this rank owns rows [row0, row0 + n_local);
   // columns >= n_local index the ghost array (values of other ranks' rows)
   long long row0 = 0, nghost = 0, nsend = 0;
@@ -640,6 +641,15 @@ int halo_vecs(const InComb& in, const double** xs) {
   return in.first ? 1 : 2;
 }
 
+// Offset storage applied by grid tiles (dia3_kernel): the 27-point box by default
+// (cfg3: 0.99 -> 0.83 ms per Chebyshev step at 256^3); the 7-point star only on
+// request (PCGX_DIA3=2) — at cfg1's L2-resident 100^3 the row-thread kernel is 2x
+// faster, its seven gathers hit L2.
+bool dia3_on(pcgx_operator op) {
+  const int e = env_int("PCGX_DIA3", 1);
+  return (op->dia3_pat == 27 && e >= 1) || (op->dia3_pat == 7 && e >= 2);
+}
+
 // Whether the operator's kernels accept the fused direction-update input.
 bool fuses_dir_update(pcgx_operator op) {
   return op->kind == 0 || op->sell_ptr != nullptr || op->bsr_ptr != nullptr ||
@@ -663,6 +673,26 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
     // one full wave of resident blocks, grid-stride over the rows (a partial second
     // wave would leave SMs idle at the tail)
     const bool stream = (double)op->dia_k * (double)op->dia_ld * 8.0 > 64e6;  // values exceed ~half of L2
+    if (dia3_on(op)) {
+      Dia3Geom g3{op->dia3_nx, 0, op->dia_ld, op->dia_val, op->dia_mask, op->dvec};
+      const int tiles = ((g3.nx + kD3X - 1) / kD3X) * ((g3.nx + kD3Y - 1) / kD3Y);
+      // z-chunks: about 8 waves of 3 resident CTAs per SM, at least 8 planes each
+      const int want = std::max(1, (c->sms * 3 * 8 + tiles - 1) / tiles);
+      g3.kz = std::max(env_int("PCGX_DIA3_KZ", 0) > 0 ? env_int("PCGX_DIA3_KZ", 0) : (g3.nx + want - 1) / want,
+                       std::min(8, g3.nx));
+      const dim3 grid3(tiles, (g3.nx + g3.kz - 1) / g3.kz);
+      Reduce red = kRed ? make_red(c, slot) : Reduce{};
+      if (op->dia3_pat == 27) {
+        auto k3 = stream ? dia3_kernel<27, In, Epi, kRed, true> : dia3_kernel<27, In, Epi, kRed, false>;
+        k3<<<grid3, kD3Threads, 0, c->s>>>(g3, in, epi, red);
+      } else {
+        auto k3 = stream ? dia3_kernel<7, In, Epi, kRed, true> : dia3_kernel<7, In, Epi, kRed, false>;
+        k3<<<grid3, kD3Threads, 0, c->s>>>(g3, in, epi, red);
+      }
+      check_launch();
+      count_launch(c);
+      return;
+    }
     auto kern = stream ? dia_kernel<In, Epi, kRed, true> : dia_kernel<In, Epi, kRed, false>;
     static int occ = 0;
     if (!occ) {
@@ -2366,6 +2396,44 @@ bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>
   return !off.empty();
 }
 
+// dia3_kernel applies when the matrix lives on a cubic nx^3 grid in the
+// reference's index order, its column offsets are exactly DiaPat<P>'s (slot s =
+// grid neighbour s) and no coupling wraps across a grid face.
+template <int P>
+bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vector<int>& ci,
+                const std::vector<int>& off) {
+  using Pat = DiaPat<P>;
+  if ((int)off.size() != Pat::K) return false;
+  const long long nxy = (long long)nx * nx;
+  for (int s = 0; s < Pat::K; ++s)
+    if ((long long)off[(size_t)s] != Pat::dz(s) * nxy + Pat::dy(s) * (long long)nx + Pat::dx(s)) return false;
+  int ok = 1;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+  for (long long r = 0; r < n; ++r) {
+    const int a = (int)(r % nx), b = (int)((r / nx) % nx), c = (int)(r / nxy);
+    for (int k = rp[(size_t)r]; k < rp[(size_t)r + 1]; ++k) {
+      const long long o = (long long)ci[(size_t)k] - r;
+      int s = 0;
+      while (s < Pat::K && off[(size_t)s] != o) ++s;
+      const int aa = a + Pat::dx(s), bb = b + Pat::dy(s), cc = c + Pat::dz(s);
+      if (aa < 0 || aa >= nx || bb < 0 || bb >= nx || cc < 0 || cc >= nx) ok = 0;
+    }
+  }
+  return ok != 0;
+}
+
+void dia3_detect(pcgx_operator op, long long n, const std::vector<int>& rp, const std::vector<int>& ci,
+                 const std::vector<int>& off) {
+  op->dia3_pat = 0;
+  int nx = (int)std::llround(std::cbrt((double)n));
+  while ((long long)nx * nx * nx > n) --nx;
+  while ((long long)(nx + 1) * (nx + 1) * (nx + 1) <= n) ++nx;
+  if (nx < 3 || (long long)nx * nx * nx != n) return;
+  if (dia3_match<27>(n, nx, rp, ci, off)) op->dia3_pat = 27;
+  else if (dia3_match<7>(n, nx, rp, ci, off)) op->dia3_pat = 7;
+  op->dia3_nx = nx;
+}
+
 // Offset-storage arrays (see dia_kernel).
 void build_dia(pcgx_operator op, long long n, const std::vector<int>& rp32,
                const std::vector<int>& ci32, const double* va, const std::vector<int>& off) {
@@ -2385,6 +2453,7 @@ void build_dia(pcgx_operator op, long long n, const std::vector<int>& rp32,
   }
   op->dia_k = K;
   op->dia_ld = ld;
+  dia3_detect(op, n, rp32, ci32, off);
   for (int k = 0; k < K; ++k) op->dia_off[k] = off[(size_t)k];
   PCGX_CUDA(cudaMalloc(&op->dia_val, sizeof(double) * val.size()));
   PCGX_CUDA(cudaMalloc(&op->dia_mask, sizeof(unsigned) * mask.size()));
@@ -2873,7 +2942,7 @@ int pcgx_operator_storage(pcgx_operator op) {
   if (!op) return -1;
   if (op->kind == 0) return 0;
   if (op->bsr_ptr) return 2;
-  if (op->dia_val) return 5;
+  if (op->dia_val) return dia3_on(op) ? 6 : 5;
   if (op->sell_ptr) return 1;
   return op->tile_row ? 3 : 4;
 }

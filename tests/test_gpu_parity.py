@@ -680,8 +680,8 @@ def test_bsr3_solve_vs_oracle(P, ctx, oracle):
 
 def test_storage_selection(P, ctx, golden):
     A = P.gen_fe27(9, sigma=1.0, seed=SEED)          # n = 729 = 3 * 243, 27 offsets: offset storage
-    assert csr(P, ctx, A.row_ptr, A.col_idx, A.values).storage() == "dia"
-    rp, ci, va = lap3d_csr(6)                          # 7 offsets
+    assert csr(P, ctx, A.row_ptr, A.col_idx, A.values).storage() == "dia_grid"
+    rp, ci, va = lap3d_csr(6)                          # 7 offsets: grid tiles only on request
     assert csr(P, ctx, rp, ci, va).storage() == "dia"
     g = golden["csr_apply"]                            # random pattern: SELL-32
     assert csr(P, ctx, np.array(g["row_ptr"]), np.array(g["col_idx"]),
@@ -693,19 +693,85 @@ def test_dia_bitwise_vs_oracle(P, ctx, oracle, nx, sigma, monkeypatch):
     """27-point FE matrices in offset storage: SpMV and Chebyshev steps bitwise the
     reference's CSR row sums; the SELL path gives the same bits."""
     A = P.gen_fe27(nx, sigma=sigma, seed=SEED)
-    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
-    assert op.storage() == "dia"
     opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
     x = oracle.random_uniform(A.n, 23)
-    assert np.array_equal(op.apply(x), oracle.apply(opo, x))
-    for m in (1, 2, 6):
-        prm = P.cheb_params(0.01, 2.1, m, 1.001)
-        assert np.array_equal(P.apply_chebyshev(prm, op, x),
-                              oracle.apply_chebyshev(opo, oracle.cheb_params(0.01, 2.1, m, 1.001), x))
+    for grid, want in (("1", "dia_grid"), ("0", "dia")):  # dia3_kernel, then dia_kernel
+        monkeypatch.setenv("PCGX_DIA3", grid)
+        op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+        assert op.storage() == want
+        assert np.array_equal(op.apply(x), oracle.apply(opo, x))
+        for m in (1, 2, 6):
+            prm = P.cheb_params(0.01, 2.1, m, 1.001)
+            assert np.array_equal(P.apply_chebyshev(prm, op, x),
+                                  oracle.apply_chebyshev(opo, oracle.cheb_params(0.01, 2.1, m, 1.001), x))
     monkeypatch.setenv("PCGX_DIA", "0")
     op_s = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
     assert op_s.storage() == "sell32"
     assert np.array_equal(op_s.apply(x), op.apply(x))
+
+
+@pytest.mark.parametrize("gen,nx", [("fe27", 33), ("fe27", 41), ("lap", 3), ("lap", 37), ("lap", 70)])
+@pytest.mark.parametrize("m", [-1, 0, 5])
+def test_dia_grid_solve_matches_oracle(P, ctx, oracle, gen, nx, m, monkeypatch):
+    """Offset storage on grid tiles (dia3_kernel: ragged 32 x 8 tiles, partial
+    z-chunks, 27-point box and 7-point star): bitwise SpMV, every PCG fusion (direction
+    update input, residual, Chebyshev steps) through a whole solve against the oracle,
+    and the same iterations as the row-thread kernel."""
+    if gen == "fe27":
+        A = P.gen_fe27(nx, sigma=1.0, seed=SEED)
+        rp, ci, va = A.row_ptr, A.col_idx, A.values
+    else:
+        rp, ci, va = lap3d_csr(nx)
+    n = len(rp) - 1
+    opo = OracleOp("csr", row_ptr=rp, col_idx=ci, values=va)
+    x = oracle.random_uniform(n, 5)
+    rhs = oracle.apply(opo, oracle.random_uniform(n, SEED))
+    lo, hi = (0.002, 2.2) if gen == "fe27" else P.analytic_extremes(3, nx)
+    prec = None if m < 0 else P.ChebyshevPreconditioner(P.cheb_params(lo, hi, m, 1.001))
+    monkeypatch.setenv("PCGX_DIA3_KZ", "5")  # several z-chunks with a partial last one
+    out = {}
+    for grid, want in (("2", "dia_grid"), ("0", "dia")):
+        monkeypatch.setenv("PCGX_DIA3", grid)
+        op = csr(P, ctx, rp, ci, va)
+        assert op.storage() == want
+        assert np.array_equal(op.apply(x), oracle.apply(opo, x))
+        out[grid] = P.pcg_solve(op, rhs, P.SolveOptions(maxit=4000), prec)
+    (x1, r1), (x0, r0) = out["2"], out["0"]
+    assert abs(r1.iters - r0.iters) <= 1  # reductions in another (fixed) block order
+    if r1.iters == r0.iters:
+        assert rel_norm(x1, x0) <= 1e-12
+    xo, ro = oracle.pcg_solve(opo, None if m < 0 else oracle.cheb_params(lo, hi, m, 1.001), rhs, maxit=4000)
+    assert r1.converged and abs(r1.iters - ro["iters"]) <= 1
+    if r1.iters == ro["iters"]:
+        assert rel_norm(x1, xo) <= 1e-10
+
+
+def test_dia_grid_rejects_wrapping_couplings(P, ctx, oracle):
+    """A 7-point pattern plus couplings that wrap across the i faces keeps the same
+    column offsets but is not a grid stencil: it stays on the row-thread kernel,
+    bitwise the oracle."""
+    nx = 6
+    rp, ci, va = lap3d_csr(nx)
+    n = nx ** 3
+    rows = [[] for _ in range(n)]
+    for r in range(n):
+        for k in range(rp[r], rp[r + 1]):
+            rows[r].append((int(ci[k]), float(va[k])))
+    for r in range(nx - 1, n - 1, nx):  # (nx-1, j, k) <-> (0, j+1, k): column offset +-1
+        rows[r].append((r + 1, -0.25))
+        rows[r + 1].append((r, -0.25))
+    rp2 = np.zeros(n + 1, dtype=np.int64)
+    ci2, va2 = [], []
+    for r in range(n):
+        rows[r].sort()
+        ci2 += [c for c, _ in rows[r]]
+        va2 += [v for _, v in rows[r]]
+        rp2[r + 1] = len(ci2)
+    ci2, va2 = np.array(ci2, dtype=np.int64), np.array(va2)
+    op = csr(P, ctx, rp2, ci2, va2)
+    assert op.storage() == "dia"
+    x = oracle.random_uniform(n, 3)
+    assert np.array_equal(op.apply(x), oracle.apply(OracleOp("csr", row_ptr=rp2, col_idx=ci2, values=va2), x))
 
 
 @pytest.mark.parametrize("dims", [(66, 10, 9), (130, 17, 33), (64, 8, 1), (2, 2, 2), (40, 40, 40)])
