@@ -32,6 +32,7 @@
 #include "cheb2.cuh"
 #include "cheb2f.cuh"
 #include "common.cuh"
+#include "dia3t.cuh"
 #include "dir_tma.cuh"
 #include "host_math.hpp"
 #include "kernels.cuh"
@@ -141,6 +142,8 @@ struct pcgx_operator_s {
   int dia_off[32] = {0};
   long long dia_ld = 0;
   int dia3_pat = 0, dia3_nx = 0;  // structured pattern (27 / 7) on an nx^3 grid (dia3_kernel)
+  struct GMap { const void* ptr; int kind; CUtensorMap m; };
+  std::vector<GMap> gmaps;        // dia3t_kernel tensor maps per buffer
   // CSR block rows on a multi-rank context: this rank owns rows [row0, row0 + n_local);
   // columns >= n_local index the ghost array (values of other ranks' rows)
   long long row0 = 0, nghost = 0, nsend = 0;
@@ -650,6 +653,9 @@ bool dia3_on(pcgx_operator op) {
   return (op->dia3_pat == 27 && e >= 1) || (op->dia3_pat == 7 && e >= 2);
 }
 
+template <bool kRed>
+bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot);
+
 // Whether the operator's kernels accept the fused direction-update input.
 bool fuses_dir_update(pcgx_operator op) {
   return op->kind == 0 || op->sell_ptr != nullptr || op->bsr_ptr != nullptr ||
@@ -673,6 +679,9 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
     // one full wave of resident blocks, grid-stride over the rows (a partial second
     // wave would leave SMs idle at the tail)
     const bool stream = (double)op->dia_k * (double)op->dia_ld * 8.0 > 64e6;  // values exceed ~half of L2
+    if constexpr (std::is_same<In, InVec>::value && std::is_same<Epi, EpiChebStep>::value) {
+      if (dia3t_launch<kRed>(c, op, in, epi, slot)) return;
+    }
     if (dia3_on(op)) {
       Dia3Geom g3{op->dia3_nx, 0, op->dia_ld, op->dia_val, op->dia_mask, op->dvec};
       const int tiles = ((g3.nx + kD3X - 1) / kD3X) * ((g3.nx + kD3Y - 1) / kD3Y);
@@ -925,6 +934,61 @@ const TmaPair& tmaps_for(pcgx_operator op, const double* ptr) {
   op->tmaps.push_back(t);
   return op->tmaps.back();
 }
+
+// dia3t_kernel (regular Chebyshev steps on 27-point grid-tile offset storage,
+// every operand by TMA): tensor maps per buffer, cached on the operator.
+// kind 0: fp64 (32, 8, 1) tiles; 1: fp64 (36, 10, 1) patches; 2: u32 mask tiles;
+// 3: the 4D value array (nx, nx, nx, 27), box (32, 8, 1, 27).
+const CUtensorMap& dia3t_map(pcgx_operator op, const void* ptr, int kind) {
+  for (auto& g : op->gmaps)
+    if (g.ptr == ptr && g.kind == kind) return g.m;
+  const cuuint64_t nx = (cuuint64_t)op->dia3_nx;
+  const cuuint64_t es = kind == 2 ? 4 : 8;
+  const cuuint64_t dims[4] = {nx, nx, nx, (cuuint64_t)kT3K};
+  const cuuint64_t strides[3] = {nx * es, nx * nx * es, (cuuint64_t)op->dia_ld * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)(kind == 1 ? kT3PX : kD3X), (cuuint32_t)(kind == 1 ? kT3PY : kD3Y), 1,
+                             (cuuint32_t)kT3K};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = encode_tiled()(&m, kind == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                                    kind == 3 ? 4 : 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(PCGX_ERR_CUDA, "cuTensorMapEncodeTiled (dia3t) failed: " + std::to_string((int)r));
+  op->gmaps.push_back({ptr, kind, m});
+  return op->gmaps.back().m;
+}
+
+template <bool kRed>
+bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot) {
+  const int nx = op->dia3_nx;
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+  if (!dia3_on(op) || op->dia3_pat != 27 || env_int("PCGX_DIA3T", 1) == 0 || nx % 4 != 0 || nx < kT3PX ||
+      in.gx || !al16(in.x) || !al16(epi.r) || !al16(epi.out) || (!epi.xold_from_r && !al16(epi.xold)) ||
+      epi.out == in.x || epi.out == epi.r)
+    return false;
+  Dia3tMaps maps;
+  maps.val = dia3t_map(op, op->dia_val, 3);
+  maps.mask = dia3t_map(op, op->dia_mask, 2);
+  maps.r = dia3t_map(op, epi.r, 0);
+  maps.xo = epi.xold_from_r ? maps.r : dia3t_map(op, epi.xold, 0);
+  maps.x = dia3t_map(op, in.x, 1);
+  maps.d = dia3t_map(op, op->dvec, 1);
+  const int kz = std::max(1, env_int("PCGX_DIA3T_KZ", 32));  // 8: -3%, 16: -1.5% at 256^3
+  const int tiles = ((nx + kD3X - 1) / kD3X) * ((nx + kD3Y - 1) / kD3Y);
+  const dim3 grid(tiles, (nx + kz - 1) / kz);
+  static bool attr = false;
+  if (!attr) {
+    PCGX_CUDA(cudaFuncSetAttribute(dia3t_kernel<kRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDia3tSmem));
+    attr = true;
+  }
+  Reduce red = kRed ? make_red(c, slot) : Reduce{};
+  dia3t_kernel<kRed><<<grid, kD3Threads, kDia3tSmem, c->s>>>(maps, nx, kz, epi, red);
+  check_launch();
+  count_launch(c);
+  return true;
+}
+
 
 // Chunk heights of a two-step launch over `span` planes of `tiles` tiles with
 // `slots` resident CTAs. The block scheduler dispatches chunk-major, greedily;

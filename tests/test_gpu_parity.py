@@ -688,15 +688,17 @@ def test_storage_selection(P, ctx, golden):
                fhs(g["values"])).storage() == "sell32"
 
 
-@pytest.mark.parametrize("nx,sigma", [(8, 1.0), (14, 1.0), (23, 0.5)])
+@pytest.mark.parametrize("nx,sigma", [(8, 1.0), (14, 1.0), (23, 0.5), (40, 1.0), (44, 0.7)])
 def test_dia_bitwise_vs_oracle(P, ctx, oracle, nx, sigma, monkeypatch):
     """27-point FE matrices in offset storage: SpMV and Chebyshev steps bitwise the
     reference's CSR row sums; the SELL path gives the same bits."""
     A = P.gen_fe27(nx, sigma=sigma, seed=SEED)
     opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
     x = oracle.random_uniform(A.n, 23)
-    for grid, want in (("1", "dia_grid"), ("0", "dia")):  # dia3_kernel, then dia_kernel
+    # dia3t_kernel (TMA operand ring; regular steps, nx % 4 == 0 and >= 36), dia3_kernel, dia_kernel
+    for grid, tma, want in (("1", "1", "dia_grid"), ("1", "0", "dia_grid"), ("0", "0", "dia")):
         monkeypatch.setenv("PCGX_DIA3", grid)
+        monkeypatch.setenv("PCGX_DIA3T", tma)
         op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
         assert op.storage() == want
         assert np.array_equal(op.apply(x), oracle.apply(opo, x))
@@ -710,7 +712,7 @@ def test_dia_bitwise_vs_oracle(P, ctx, oracle, nx, sigma, monkeypatch):
     assert np.array_equal(op_s.apply(x), op.apply(x))
 
 
-@pytest.mark.parametrize("gen,nx", [("fe27", 33), ("fe27", 41), ("lap", 3), ("lap", 37), ("lap", 70)])
+@pytest.mark.parametrize("gen,nx", [("fe27", 33), ("fe27", 40), ("fe27", 41), ("lap", 3), ("lap", 37), ("lap", 70)])
 @pytest.mark.parametrize("m", [-1, 0, 5])
 def test_dia_grid_solve_matches_oracle(P, ctx, oracle, gen, nx, m, monkeypatch):
     """Offset storage on grid tiles (dia3_kernel: ragged 32 x 8 tiles, partial
@@ -729,6 +731,7 @@ def test_dia_grid_solve_matches_oracle(P, ctx, oracle, gen, nx, m, monkeypatch):
     lo, hi = (0.002, 2.2) if gen == "fe27" else P.analytic_extremes(3, nx)
     prec = None if m < 0 else P.ChebyshevPreconditioner(P.cheb_params(lo, hi, m, 1.001))
     monkeypatch.setenv("PCGX_DIA3_KZ", "5")  # several z-chunks with a partial last one
+    monkeypatch.setenv("PCGX_DIA3T_KZ", "7")
     out = {}
     for grid, want in (("2", "dia_grid"), ("0", "dia")):
         monkeypatch.setenv("PCGX_DIA3", grid)
