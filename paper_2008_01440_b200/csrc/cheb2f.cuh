@@ -47,6 +47,12 @@ namespace pcgx {
 #endif
 // register cap with one CTA per SM: 22 warps put 6 on one SM sub-partition (16K
 // registers each), so 64 x 20 tiles allow 80
+// lane 0 / 31 i-neighbours: one LDS for every lane (lane 0: the west of its pair,
+// the others: broadcast of lane 31's east) merged by selects, instead of two
+// divergent per-lane loads
+#ifndef PCGX_C2FEDGE
+#define PCGX_C2FEDGE 1
+#endif
 #ifndef PCGX_C2FMAXREG
 #define PCGX_C2FMAXREG 80
 #endif
@@ -165,6 +171,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   const bool do1 = gj >= 0 && gj < p.ny && pair_in;
   const int offA = (warp + 1) * kFW + col;        // A-box offset of the pair
   const int offB = warp * kFW + col;              // B/R/C offset of the pair
+  const int eoff = lane == 0 ? -1 : 64 - 2 * lane;  // lane 0: west of its pair; else lane 31's east
   const bool interior = warp >= 1 && warp <= kFTY;  // a tile row: stage 2 here
   const bool do2 = interior && do1;
   double* gC = p.outC + (long long)gj * p.nx + gi;
@@ -230,8 +237,16 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (kT) ap = mul2(ap);
       double aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
       double ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
+#if PCGX_C2FEDGE
+      {
+        const double edge = kT ? d * pAu[offA + eoff] : rq(pAu, offA + eoff);
+        aw = lane == 0 ? edge : aw;
+        ae = lane == 31 ? edge : ae;
+      }
+#else
       if (lane == 0) aw = kT ? d * pAu[offA - 1] : rq(pAu, offA - 1);
       if (lane == 31) ae = kT ? d * pAu[offA + 2] : rq(pAu, offA + 2);
+#endif
       const double2 as = rq2(pAu, offA - kFW);
       const double2 an = rq2(pAu, offA + kFW);
       double y0, y1;
@@ -280,8 +295,16 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     if (interior && t - 2 >= kb) {
       double cw = __shfl_up_sync(0xffffffffu, c2.y, 1);
       double ce = __shfl_down_sync(0xffffffffu, c2.x, 1);
+#if PCGX_C2FEDGE
+      {
+        const double edge = pC2[offB + eoff];
+        cw = lane == 0 ? edge : cw;
+        ce = lane == 31 ? edge : ce;
+      }
+#else
       if (lane == 0) cw = pC2[offB - 1];
       if (lane == 31) ce = pC2[offB + 2];
+#endif
       const double2 cs = *reinterpret_cast<const double2*>(pC2 + offB - kFW);
       const double2 cn = *reinterpret_cast<const double2*>(pC2 + offB + kFW);
       double y0, y1;
