@@ -431,6 +431,61 @@ def test_cfg2_320_k20_known_answer(P, ctx):
     assert rel_norm(xh, xth) == pytest.approx(1.513e-6, rel=1e-3)
 
 
+@pytest.mark.slow
+def test_cfg3_256_full_size(P, ctx, monkeypatch):
+    """Config 3 at its full size (256^3, 449,455,096 nnz): the grid-tile offset
+    storage (dia3t / dia3 kernels) gives bitwise the SELL-32 CSR row sums for the
+    SpMV and the row-thread offset kernel's bits for every Chebyshev step (the
+    reference's CSR order in all three); the k = 40 solve converges (43 iterations
+    in the round-1 bench) with a true residual at the tolerance."""
+    A = P.gen_fe27(256, sigma=1.0, seed=SEED)
+    assert A.nnz() == 449455096
+    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op.storage() == "dia_grid"
+    x = P.random_uniform_vector(A.n, 23, ctx=ctx)
+    y = op.apply(x).numpy()
+    lo, hi = P.lanczos_bounds(op, 20, 30, SEED)
+    prm = P.cheb_params(lo, hi, 6, 1.001)
+    z = P.apply_chebyshev(prm, op, x.numpy())
+    monkeypatch.setenv("PCGX_DIA3", "0")
+    op_r = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op_r.storage() == "dia"
+    assert np.array_equal(P.apply_chebyshev(prm, op_r, x.numpy()), z)
+    op_r.close()
+    monkeypatch.setenv("PCGX_DIA", "0")
+    op_s = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op_s.storage() == "sell32"
+    assert np.array_equal(op_s.apply(x).numpy(), y)
+    op_s.close()
+    monkeypatch.delenv("PCGX_DIA")
+    monkeypatch.delenv("PCGX_DIA3")
+    xt = P.random_uniform_vector(A.n, SEED, ctx=ctx)
+    rhs = op.apply(xt)
+    xs, rep = P.pcg_solve(op, rhs, None, P.ChebyshevPreconditioner(P.cheb_params(lo, hi, 40, 1.001)))
+    assert rep.converged and 40 <= rep.iters <= 46
+    assert rep.rel_res <= 1e-8 and rep.true_rel_res <= 1.01e-8
+
+
+@pytest.mark.slow
+def test_cfg4_160_full_size(P, ctx, monkeypatch):
+    """Config 4 at its full size (160^3 x 3 dof, 982,938,168 nnz): BSR-3 gives the
+    SELL-32 CSR row sums bitwise (SpMV and a Chebyshev apply)."""
+    A = P.gen_elast27(160, 1.0, 0.5, 0.1, seed=SEED)
+    assert A.nnz() == 982938168
+    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op.storage() == "bsr3"
+    x = P.random_uniform_vector(A.n, 29, ctx=ctx)
+    y = op.apply(x).numpy()
+    prm = P.cheb_params(0.001, 2.5, 5, 1.001)
+    z = P.apply_chebyshev(prm, op, x.numpy())
+    op.close()
+    monkeypatch.setenv("PCGX_BSR", "0")
+    op_s = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    assert op_s.storage() == "sell32"
+    assert np.array_equal(op_s.apply(x).numpy(), y)
+    assert np.array_equal(P.apply_chebyshev(prm, op_s, x.numpy()), z)
+
+
 # ------------------------------------------------------------------ two-step (temporal blocking) kernel
 
 @pytest.mark.parametrize("dims", [(24, 24, 24), (66, 10, 9), (64, 8, 1), (130, 17, 33), (2, 2, 2),
