@@ -105,6 +105,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   const bool do1 = gj >= 0 && gj < p.ny && pair_in;
   const bool tile_row = warp >= 1 && warp <= kDTY;
   const int off = warp * kC2W + col;
+  const int eoff = lane == 0 ? -1 : 64 - 2 * lane;  // lane 0: west of its pair; else lane 31's east
   const long long goff = (long long)gj * p.nx + gi;
   const bool zdiv = p.ztheta > 0.0;
   const double zinv = zdiv ? 1.0 / p.ztheta : 0.0;  // RN(1/theta), as on the host
@@ -157,8 +158,18 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
       const double* Nv = sN + (sc == 0 ? kDirNC - 1 : sc - 1) * kDBPlane;
       double pw = __shfl_up_sync(0xffffffffu, pc.y, 1);
       double pe = __shfl_down_sync(0xffffffffu, pc.x, 1);
+#if PCGX_C2FEDGE
+      {
+        // one combine for the warp (lane 0: its west, the others: broadcast of lane
+        // 31's east) instead of two divergent ones
+        const double e = comb(Zv[off + eoff], first ? 0.0 : Pv[off + eoff]);
+        pw = lane == 0 ? e : pw;
+        pe = lane == 31 ? e : pe;
+      }
+#else
       if (lane == 0) pw = comb(Zv[off - 1], first ? 0.0 : Pv[off - 1]);
       if (lane == 31) pe = comb(Zv[off + 2], first ? 0.0 : Pv[off + 2]);
+#endif
       if (do1) {
         const double2 ps = *reinterpret_cast<const double2*>(Nv + off - kC2W);
         const double2 pnn = *reinterpret_cast<const double2*>(Nv + off + kC2W);
