@@ -53,6 +53,11 @@ namespace pcgx {
 #ifndef PCGX_C2FEDGE
 #define PCGX_C2FEDGE 1
 #endif
+// i-neighbours of every lane straight from shared memory (two 8-byte LDS per
+// stage) instead of shuffles + the edge select (plain A, not kT / kUpd)
+#ifndef PCGX_C2FNBR
+#define PCGX_C2FNBR 1
+#endif
 #ifndef PCGX_C2FMAXREG
 #define PCGX_C2FMAXREG 80
 #endif
@@ -235,8 +240,13 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         acc_rr = acc_rr + ap.y * ap.y;
       }
       if (kT) ap = mul2(ap);
-      double aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
-      double ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
+      double aw, ae;
+      if (PCGX_C2FNBR && !kT && !kUpd) {
+        aw = pAu[offA - 1];
+        ae = pAu[offA + 2];
+      } else {
+      aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
+      ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
 #if PCGX_C2FEDGE
       {
         const double edge = kT ? d * pAu[offA + eoff] : rq(pAu, offA + eoff);
@@ -247,6 +257,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (lane == 0) aw = kT ? d * pAu[offA - 1] : rq(pAu, offA - 1);
       if (lane == 31) ae = kT ? d * pAu[offA + 2] : rq(pAu, offA + 2);
 #endif
+      }
       const double2 as = rq2(pAu, offA - kFW);
       const double2 an = rq2(pAu, offA + kFW);
       double y0, y1;
@@ -293,8 +304,13 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     }
     // ---------------- stage 2: E[t-2] on the own tile row (warps 1..8)
     if (interior && t - 2 >= kb) {
-      double cw = __shfl_up_sync(0xffffffffu, c2.y, 1);
-      double ce = __shfl_down_sync(0xffffffffu, c2.x, 1);
+      double cw, ce;
+      if (PCGX_C2FNBR) {
+        cw = pC2[offB - 1];
+        ce = pC2[offB + 2];
+      } else {
+      cw = __shfl_up_sync(0xffffffffu, c2.y, 1);
+      ce = __shfl_down_sync(0xffffffffu, c2.x, 1);
 #if PCGX_C2FEDGE
       {
         const double edge = pC2[offB + eoff];
@@ -305,6 +321,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (lane == 0) cw = pC2[offB - 1];
       if (lane == 31) ce = pC2[offB + 2];
 #endif
+      }
       const double2 cs = *reinterpret_cast<const double2*>(pC2 + offB - kFW);
       const double2 cn = *reinterpret_cast<const double2*>(pC2 + offB + kFW);
       double y0, y1;
