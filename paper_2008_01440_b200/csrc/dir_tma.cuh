@@ -26,8 +26,13 @@ namespace pcgx {
 #ifndef PCGX_DIRMINB
 #define PCGX_DIRMINB 1
 #endif
+// x tiles of the deferred x += alpha p_old by TMA in the z / p_old units (instead
+// of a register load one plane ahead)
+#ifndef PCGX_DIRXTMA
+#define PCGX_DIRXTMA 1
+#endif
 #ifndef PCGX_DIRNS
-#define PCGX_DIRNS 6
+#define PCGX_DIRNS (PCGX_DIRXTMA ? 5 : 6)
 #endif
 constexpr int kDTY = PCGX_DIRTY;
 constexpr int kDBY = kDTY + 2;                          // box rows (1-halo)
@@ -40,8 +45,11 @@ constexpr int kDirNC = 3;                 // p_new planes
 #endif
 constexpr int kDirUnroll = PCGX_DIRUNROLL; // plane-loop unroll
 constexpr int kDirThreads = 32 * (kDTY + 2);  // one warp per extended row (tile rows + 2 halo rows)
+constexpr bool kDirXTma = PCGX_DIRXTMA != 0;
+constexpr int kDXStride = kC2TX * kDTY;  // x tile (64 x kDTY), a 128-byte multiple
 constexpr size_t kDirSmem =
-    sizeof(double) * (size_t)(2 * kDirNS * kDEStride + kDirNC * kDBPlane) + 8 * kDirNS + 128;
+    sizeof(double) * (size_t)(2 * kDirNS * kDEStride + kDirNC * kDBPlane + (kDirXTma ? kDirNS * kDXStride : 0)) +
+    8 * kDirNS + 128;
 
 struct DirParams {
   int nx, ny, nzl;
@@ -63,11 +71,13 @@ struct DirParams {
 // grid: (tiles, plan.n); block kDirThreads; dynamic smem kDirSmem.
 __global__ void __launch_bounds__(kDirThreads, PCGX_DIRMINB)
 stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_constant__ CUtensorMap mapP,
-                    DirParams p, int k_begin, int k_end, const __grid_constant__ ChunkPlan plan, Reduce red) {
+                    const __grid_constant__ CUtensorMap mapX, DirParams p, int k_begin, int k_end,
+                    const __grid_constant__ ChunkPlan plan, Reduce red) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sZ = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   double* sP = sZ + kDirNS * kDEStride;
-  double* sN = sP + kDirNS * kDEStride;
+  double* sX = sP + kDirNS * kDEStride;  // kDirXTma: x tiles, one per unit (128-byte aligned)
+  double* sN = sX + (kDirXTma ? kDirNS * kDXStride : 0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sN + kDirNC * kDBPlane);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -79,15 +89,18 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   const double beta = first ? 0.0 : p.S[p.s_new] / p.S[p.s_old];
   const unsigned bytes = kDBPlane * 8;  // box bytes
   auto in_z = [&](int z) { return z >= p.a_lo && z < p.a_hi; };
+  const bool xupd = p.x != nullptr && !first;
   // unit u: the z (and p_old) boxes of plane u, slot / barrier (u - (kb-1)) % NS
   auto issue = [&](int u) {
     const int q = (u - (kb - 1)) % kDirNS;
     const bool ld = in_z(u);
-    mbar_expect_tx(&bars[q], ld ? (first ? bytes : 2 * bytes) : 0u);
+    const bool lx = kDirXTma && xupd && u >= kb && u < ke;
+    mbar_expect_tx(&bars[q], (ld ? (first ? bytes : 2 * bytes) : 0u) + (lx ? kDXStride * 8u : 0u));
     if (ld) {
       tma_load_3d(sZ + q * kDEStride, &mapZ, i0 - 2, j0 - 1, u + p.zoff, &bars[q]);
       if (!first) tma_load_3d(sP + q * kDEStride, &mapP, i0 - 2, j0 - 1, u + p.zoff, &bars[q]);
     }
+    if (lx) tma_load_3d(sX + q * kDXStride, &mapX, i0, j0, u, &bars[q]);
   };
   if (tid == 0) {
     for (int q = 0; q < kDirNS; ++q) mbar_init(&bars[q], 1);
@@ -114,7 +127,6 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
     zv = zval(zv);
     return first ? zv : zv + beta * pv;
   };
-  const bool xupd = p.x != nullptr && !first;
   const double alpha = xupd ? p.S[p.s_old] / p.S[p.s_pq] : 0.0;
 
   double2 pm = zero2, pc = zero2;  // p_new of the warp's row at planes u-2, u-1
@@ -128,7 +140,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
     // this iteration so its latency hides behind them
     double2 xv = zero2;
     const bool xdo = xupd && tile_row && do1 && u - 1 >= kb;
-    if (xdo) xv = *reinterpret_cast<const double2*>(p.x + (long long)(u - 1) * p.nxy + goff);
+    if (!kDirXTma && xdo) xv = *reinterpret_cast<const double2*>(p.x + (long long)(u - 1) * p.nxy + goff);
     mbar_wait(&bars[slot], phase);
     const double* Zu = sZ + slot * kDEStride;
     const double* Pu = sP + slot * kDEStride;
@@ -180,6 +192,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
         st2(p.pout + idx, pc.x, pc.y);
         acc = acc + (pc.x * y0 + pc.y * y1);
         if (xdo) {
+          if (kDirXTma) xv = *reinterpret_cast<const double2*>(sX + sv * kDXStride + (warp - 1) * kC2TX + 2 * lane);
           const double2 po = *reinterpret_cast<const double2*>(Pv + off);
           xv.x = xv.x + alpha * po.x;
           xv.y = xv.y + alpha * po.y;

@@ -924,6 +924,23 @@ CUtensorMap make_map(pcgx_operator op, const double* ptr, int bx, int by) {
   return m;
 }
 
+// The direction step's x tiles: a map over the rank's unpadded x, box 64 x kDTY.
+const CUtensorMap& xtile_map(pcgx_operator op, const double* x) {
+  for (auto& g : op->gmaps)
+    if (g.ptr == x && g.kind == 10) return g.m;
+  const cuuint64_t dims[3] = {(cuuint64_t)op->nx, (cuuint64_t)op->ny, (cuuint64_t)op->nzl};
+  const cuuint64_t strides[2] = {(cuuint64_t)op->nx * 8, (cuuint64_t)(op->nx * op->ny) * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)kC2TX, (cuuint32_t)kDTY, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(PCGX_ERR_CUDA, "cuTensorMapEncodeTiled (x tiles) failed: " + std::to_string((int)r));
+  op->gmaps.push_back({x, 10, m});
+  return op->gmaps.back().m;
+}
+
 using TmaPair = pcgx_operator_s::TmaPair;
 const TmaPair& tmaps_for(pcgx_operator op, const double* ptr) {
   for (auto& t : op->tmaps)
@@ -1148,6 +1165,7 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
                                  (int)kDirSmem));
   static_assert(kDBY == kFBY || kDBY == kC2BY, "direction-step box rows: no tensor map of that shape");
   const CUtensorMap mz = kDBY == kFBY ? tmaps_for(op, z).fe : tmaps_for(op, z).e;
+  const CUtensorMap mx = (kDirXTma && x && !first) ? xtile_map(op, x) : mz;  // unused unless x is updated
   const CUtensorMap mp = kDBY == kFBY ? tmaps_for(op, first ? z : pold).fe : tmaps_for(op, first ? z : pold).e;
   const int nzl = (int)op->nzl;
   const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
@@ -1166,7 +1184,7 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
                                                       (long long)std::max(occ, 1) * c->sms)).first;
     }
     stencil7_dir_kernel<<<dim3((unsigned)tiles, (unsigned)it->second.n), kDirThreads, kDirSmem, c->s>>>(
-        mz, mp, prm, k_begin, k_end, it->second, make_red(c, slot, accumulate));
+        mz, mp, mx, prm, k_begin, k_end, it->second, make_red(c, slot, accumulate));
     check_launch();
     count_launch(c);
   };
