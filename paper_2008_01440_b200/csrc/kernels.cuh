@@ -1343,6 +1343,9 @@ update_kernel(long long n, double* __restrict__ x, double* __restrict__ r,
 
 // update_kernel on 16-byte pairs (n even, 16-byte aligned vectors): the same
 // per-element operations, four 16-byte loads in flight per thread per step.
+#ifndef PCGX_UPD_U2
+#define PCGX_UPD_U2 1  // k = 0 solve -3% at 320^3
+#endif
 template <int kZ, bool kX>
 __global__ void __launch_bounds__(kVecThreads)
 update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
@@ -1351,6 +1354,49 @@ update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
   const double alpha = S[s_rho] / S[s_pq];
   const double inv = 1.0 / theta;  // RN(1/theta), as on the host
   double acc = 0.0, acc2 = 0.0;
+#if PCGX_UPD_U2
+  // two elements per thread and step, both pairs' loads issued before either store
+  const long long G = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += 2 * G) {
+    const long long j = i + G;
+    const bool hj = j < n2;
+    double2 ri = r[i], rj = make_double2(0.0, 0.0);
+    const double2 qi = __ldg(q + i);
+    double2 qj = make_double2(0.0, 0.0);
+    if (hj) {
+      rj = r[j];
+      qj = __ldg(q + j);
+    }
+    auto one = [&](long long k, double2 rv, const double2 qv) {
+      if (kX) {
+        double2 xi = x[k];
+        const double2 pi = __ldg(p + k);
+        xi.x = xi.x + alpha * pi.x;
+        xi.y = xi.y + alpha * pi.y;
+        x[k] = xi;
+      }
+      rv.x = rv.x - alpha * qv.x;
+      rv.y = rv.y - alpha * qv.y;
+      r[k] = rv;
+      acc = acc + rv.x * rv.x;
+      acc = acc + rv.y * rv.y;
+      if (kZ == 1) {
+        const double2 zi = make_double2(div_rn(rv.x, theta, inv), div_rn(rv.y, theta, inv));
+        if (z) z[k] = zi;
+        acc2 = acc2 + rv.x * zi.x;
+        acc2 = acc2 + rv.y * zi.y;
+      } else if (kZ == 2) {
+        acc2 = acc2 + rv.x * rv.x;
+        acc2 = acc2 + rv.y * rv.y;
+      }
+    };
+    one(i, ri, qi);
+    if (hj) one(j, rj, qj);
+  }
+  if (kZ) block_reduce_finish2(acc, acc2, red);
+  else block_reduce_finish(acc, red);
+  return;
+#endif
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
        i += (long long)gridDim.x * blockDim.x) {
     double2 ri = r[i];

@@ -1,6 +1,7 @@
 # SPDX-License-Identifier: Apache-2.0
 """A/B of whole solves (device wall_time of pcg_solve) between library builds,
-interleaved over rounds: python tools/solve_ab.py NX M ROUNDS LIB1 LIB2 ...
+interleaved over rounds: python tools/solve_ab.py NX M ROUNDS VARIANT ...
+VARIANT = LIB[+NAME=VALUE...] (library path, then environment settings).
 Each (round, lib) runs in a subprocess: build the operator, one warm-up solve,
 then three timed solves; prints the median."""
 import json
@@ -35,7 +36,9 @@ if __name__ == "__main__":
     res = {l: [] for l in libs}
     for r in range(rounds):
         for l in libs:
-            env = dict(os.environ, PCGX_LIB=l)
+            parts = l.split("+")
+            env = dict(os.environ, PCGX_LIB=parts[0])
+            env.update(kv.split("=", 1) for kv in parts[1:])
             out = subprocess.run([sys.executable, __file__, "--child", str(nx), str(m)], env=env,
                                  capture_output=True, text=True).stdout.strip().splitlines()[-1]
             res[l].append(json.loads(out)["t"])
