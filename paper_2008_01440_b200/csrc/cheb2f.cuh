@@ -53,6 +53,12 @@ namespace pcgx {
 #ifndef PCGX_C2FEDGE
 #define PCGX_C2FEDGE 1
 #endif
+// kUpd: r(it) = r(it-1) - alpha q(it) formed ONCE per element, in place in the A
+// slot, when the plane arrives (own pairs by their warps, the box's outer rows and
+// columns by the two halo warps); every later read is a plain load
+#ifndef PCGX_C2FUPDIP
+#define PCGX_C2FUPDIP 1
+#endif
 // i-neighbours of every lane straight from shared memory (two 8-byte LDS per
 // stage) instead of shuffles + the edge select (plain A, not kT / kUpd)
 #ifndef PCGX_C2FNBR
@@ -165,6 +171,23 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     const double2 w = *reinterpret_cast<const double2*>(sQ + (a - sA0) + off);
     return make_double2(v.x - alpha * w.x, v.y - alpha * w.y);
   };
+  constexpr bool kIP = kUpd && PCGX_C2FUPDIP;
+  // reads of planes already combined in place
+  auto rqx = [&](const double* a, int off) { return kIP ? a[off] : rq(a, off); };
+  auto rqx2 = [&](const double* a, int off) {
+    return kIP ? *reinterpret_cast<const double2*>(a + off) : rq2(a, off);
+  };
+  // kIP: element e of an A slot combined in place
+  auto combine_slot = [&](double* a, int e) {
+    a[e] = a[e] - alpha * sQ[(a - sA0) + e];
+  };
+  if (kIP) {  // the prologue planes kb-2, kb-1, whole boxes
+    for (int e = tid; e < kFW * kFAY; e += kFThreads) {
+      if (in_z(kb - 2)) combine_slot(sA, e);
+      if (in_z(kb - 1)) combine_slot(sA + kFAPlane, e);
+    }
+    __syncthreads();
+  }
 
   const double d = p.d;
   const double inv_t = 1.0 / p.theta;
@@ -211,8 +234,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   // kT: the stencil queues hold t = d * x (each product formed once per point);
   // the recurrences' centre values travel in separate x queues
   auto mul2 = [&](double2 v) { return make_double2(d * v.x, d * v.y); };
-  double2 am = in_z(kb - 2) ? rq2(sA, offA) : zero2;
-  double2 ac = in_z(kb - 1) ? rq2(sA + kFAPlane, offA) : zero2;
+  double2 am = in_z(kb - 2) ? rqx2(sA, offA) : zero2;
+  double2 ac = in_z(kb - 1) ? rqx2(sA + kFAPlane, offA) : zero2;
   double2 x1 = ac;                             // kT: A[t-1] x (own row)
   if (kT) {
     am = mul2(am);
@@ -234,6 +257,21 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     if (s1) {
       const bool plane_in = t >= p.c_lo && t < p.c_hi, has_p = in_z(t + 1);
       ap = has_p ? rq2(pAp, offA) : zero2;
+      if (kIP && has_p) {
+        // the own pair of plane t+1 in place; the halo warps take the box's outer
+        // rows (0, kFAY-1) and columns (0, 1 / kFW-2, kFW-1) of that plane
+        *reinterpret_cast<double2*>(const_cast<double*>(pAp) + offA) = ap;
+        if (warp == 0 || warp == kFTY + 1) {
+          constexpr int kOut = kFW + 2 * kFBY;  // outer row + two columns of rows 1..kFBY
+          for (int e = lane; e < kOut; e += 32) {
+            int off;
+            if (e < kFW) off = (warp == 0 ? 0 : kFAY - 1) * kFW + e;
+            else off = (1 + (e - kFW) / 2) * kFW + (warp == 0 ? 0 : kFW - 2) + (e - kFW) % 2;
+            combine_slot(const_cast<double*>(pAp), off);
+          }
+          __syncwarp();
+        }
+      }
       if (kUpd && has_p && interior && do1 && t + 1 >= kb && t + 1 < ke && t + 1 >= p.c_lo && t + 1 < p.c_hi) {
         st2(p.rout + (long long)(t + 1) * p.nxy + (long long)gj * p.nx + gi, ap.x, ap.y);
         acc_rr = acc_rr + ap.x * ap.x;
@@ -241,7 +279,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       }
       if (kT) ap = mul2(ap);
       double aw, ae;
-      if (PCGX_C2FNBR && !kT && !kUpd) {
+      if (PCGX_C2FNBR && !kT && (!kUpd || kIP)) {
         aw = pAu[offA - 1];
         ae = pAu[offA + 2];
       } else {
@@ -258,8 +296,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (lane == 31) ae = kT ? d * pAu[offA + 2] : rq(pAu, offA + 2);
 #endif
       }
-      const double2 as = rq2(pAu, offA - kFW);
-      const double2 an = rq2(pAu, offA + kFW);
+      const double2 as = rqx2(pAu, offA - kFW);
+      const double2 an = rqx2(pAu, offA + kFW);
       double y0, y1;
       double2 xc;  // A[t] x at the pair
       if (kT) {
@@ -292,10 +330,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (do_h) {
         double hx = 0.0;
         if (plane_in && h_in) {
-          const double xc = rq(pAu, offAh);
-          const double y = stencil_point(d, in_z(t - 1) ? rq(pAm, offAh) : 0.0, rq(pAu, offAh - kFW),
-                                         rq(pAu, offAh - 1), xc, rq(pAu, offAh + 1), rq(pAu, offAh + kFW),
-                                         has_p ? rq(pAp, offAh) : 0.0);
+          const double xc = rqx(pAu, offAh);
+          const double y = stencil_point(d, in_z(t - 1) ? rqx(pAm, offAh) : 0.0, rqx(pAu, offAh - kFW),
+                                         rqx(pAu, offAh - 1), xc, rqx(pAu, offAh + 1), rqx(pAu, offAh + kFW),
+                                         has_p ? rqx(pAp, offAh) : 0.0);
           if (kFirst) hx = p.c1 * ((2.0 * xc) - div_rn(y, p.theta, inv_t));
           else hx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * pBu[offBh])) + p.c2 * (pRu[offBh] - y));
         }
