@@ -54,7 +54,8 @@ typedef enum {
   PCGX_ERR_NCCL = 4,        /* communicator failure */
   PCGX_ERR_OVERFLOW = 5,    /* index does not fit the int32 device CSR */
   PCGX_ERR_UNSUPPORTED = 6, /* valid reference input this build does not accelerate */
-  PCGX_ERR_PARSE = 7        /* polycg::ParseError (MatrixMarket input), message has file:line */
+  PCGX_ERR_PARSE = 7,       /* polycg::ParseError (MatrixMarket input), message has file:line */
+  PCGX_ERR_CALLBACK = 8     /* the on_iterate callback asked to stop (it holds the reason) */
 } pcgx_status;
 
 typedef struct pcgx_context_s* pcgx_context;
@@ -212,11 +213,21 @@ pcgx_status pcgx_newton_apply_device(pcgx_context ctx, pcgx_operator op, const p
 #define PCGX_FLAG_TIME_KERNELS 1u /* time every Chebyshev-step launch with CUDA events */
 #define PCGX_FLAG_NO_GRAPH 2u     /* launch kernels one by one instead of CUDA graphs */
 
+/* SolveOptions::on_iterate (pcg.hpp:62-63, called at pcg.cpp:88): after every
+ * iteration with (iteration, current x). x is a HOST copy of the rank's x (n
+ * values), valid during the call. Return 0 to continue; nonzero aborts the solve
+ * with PCGX_ERR_CALLBACK (the caller rethrows what its callback caught). */
+typedef int (*pcgx_iterate_fn)(int64_t iter, const double* x, int64_t n, void* user);
+
 typedef struct {
   double tol;         /* SolveOptions::tol (default 1e-8) */
   int maxit;          /* SolveOptions::maxit (default 20000) */
   const double* x0;   /* initial guess (same memory space as b), NULL = zero */
   uint32_t flags;
+  pcgx_iterate_fn on_iterate; /* NULL = none; otherwise x is kept current every
+                                 iteration (no deferred x / fused update) and
+                                 copied to the host for the call */
+  void* on_iterate_user;
 } pcgx_solve_opts;
 
 typedef struct {

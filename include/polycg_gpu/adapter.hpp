@@ -22,6 +22,8 @@
 #ifndef POLYCG_GPU_ADAPTER_HPP
 #define POLYCG_GPU_ADAPTER_HPP
 
+#include <algorithm>
+#include <exception>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -102,8 +104,6 @@ inline std::pair<Vector, SolveReport> pcg_solve(const Session& s, const DeviceOp
   const Index n = op.size();
   if (b.size() != n) throw std::invalid_argument("pcg_solve: rhs length mismatch");
   if (opts.x0 && opts.x0->size() != n) throw std::invalid_argument("pcg_solve: x0 length mismatch");
-  if (opts.on_iterate)
-    throw std::invalid_argument("gpu::pcg_solve: on_iterate is not supported on the device path");
   pcgx_cheb cheb{};
   const pcgx_cheb* cp = nullptr;
   pcgx_newton newton{};
@@ -131,10 +131,34 @@ inline std::pair<Vector, SolveReport> pcg_solve(const Session& s, const DeviceOp
   o.tol = opts.tol;
   o.maxit = opts.maxit;
   o.x0 = opts.x0 ? opts.x0->data() : nullptr;
+  // on_iterate(it, x) (pcg.cpp:88): the library hands a host copy of x; an
+  // exception the callback throws is held here and rethrown after the C call
+  struct Iterate {
+    const SolveOptions* opts;
+    Vector xv;
+    std::exception_ptr err;
+  } it_state{&opts, Vector(), nullptr};
+  if (opts.on_iterate) {
+    o.on_iterate = [](int64_t it, const double* xh, int64_t nx, void* user) -> int {
+      auto* st = static_cast<Iterate*>(user);
+      try {
+        st->xv.resize(static_cast<Index>(nx));
+        std::copy(xh, xh + nx, st->xv.data());
+        st->opts->on_iterate(static_cast<int>(it), st->xv);
+        return 0;
+      } catch (...) {
+        st->err = std::current_exception();
+        return 1;
+      }
+    };
+    o.on_iterate_user = &it_state;
+  }
   pcgx_report r{};
   Vector x(n);
-  if (np) check(pcgx_pcg_solve_newton(s.get(), dop.get(), np, b.data(), x.data(), &o, &r), s.get());
-  else check(pcgx_pcg_solve(s.get(), dop.get(), cp, b.data(), x.data(), &o, &r), s.get());
+  const pcgx_status st = np ? pcgx_pcg_solve_newton(s.get(), dop.get(), np, b.data(), x.data(), &o, &r)
+                            : pcgx_pcg_solve(s.get(), dop.get(), cp, b.data(), x.data(), &o, &r);
+  if (it_state.err) std::rethrow_exception(it_state.err);
+  check(st, s.get());
   SolveReport rep;
   rep.iters = static_cast<int>(r.iters);
   rep.ddot = static_cast<std::uint64_t>(r.ddot);

@@ -65,6 +65,7 @@ struct pcgx_context_s {
   struct CommBase* cm = nullptr;  // nullptr on a single-GPU context
   double* S = nullptr;        // device scalars
   double* hS = nullptr;       // pinned mirror (host-mapped)
+  std::vector<double> hx;     // host copy of x for SolveOptions::on_iterate
   double* dS_map = nullptr;   // hS as seen from the device: single-rank reductions store there too
   double* partials = nullptr;
   unsigned* counter = nullptr;
@@ -1745,7 +1746,9 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   const double* zvec = (zm == 2 || zdiv) ? r : z;
   // single-rank stencil: x += alpha p moves from the update kernel into the next
   // direction step, which reads p_old anyway (8 B less per unknown and iteration)
-  const bool defer_x = fuse && dir_tma_ok(op) && env_int("PCGX_DEFER_X", 1) != 0;
+  // (not with on_iterate: x must be current at every iteration's callback)
+  const bool cb = opts.on_iterate != nullptr;
+  const bool defer_x = fuse && dir_tma_ok(op) && env_int("PCGX_DEFER_X", 1) != 0 && !cb;
   // one GPU, Chebyshev m >= 3 on the stencil: the update r -= alpha q, r'r rides in
   // the first two-step pass of P r (cheb2f_upd_launch); r(it) lives in Rb[it & 1]
   const bool fuse_upd = zm == 0 && prec.kind == 1 && spec_after_update && defer_x &&
@@ -1907,6 +1910,13 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     if (!std::isfinite(rnorm)) fail(PCGX_ERR_NUMERICAL, "pcg_solve: residual norm is not finite");
     rep->iters = it;
     rep->rel_res = rnorm / bnorm;
+    if (cb) {  // opts.on_iterate(it, x) (pcg.cpp:88): x(it) was final before the snapshot
+      c->hx.resize((size_t)n);
+      PCGX_CUDA(cudaMemcpyAsync(c->hx.data(), x, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
+      PCGX_CUDA(cudaStreamSynchronize(c->s));
+      if (opts.on_iterate(it, c->hx.data(), n, opts.on_iterate_user) != 0)
+        fail(PCGX_ERR_CALLBACK, "pcg_solve: on_iterate stopped the solve at iteration " + std::to_string(it));
+    }
     if (rep->rel_res <= opts.tol) {
       rep->converged = 1;
       if (more) rep->wasted_matvec = (zm == 0 ? m : 0) + 1;  // speculative P r and A p
@@ -3235,6 +3245,8 @@ void pcgx_solve_opts_default(pcgx_solve_opts* o) {
   o->maxit = 20000;
   o->x0 = nullptr;
   o->flags = 0;
+  o->on_iterate = nullptr;
+  o->on_iterate_user = nullptr;
 }
 
 namespace {

@@ -83,8 +83,13 @@ class ParseError(PcgxError):
     status = 7
 
 
+class CallbackStop(PcgxError):
+    """SolveOptions.on_iterate stopped the solve (its exception is chained)."""
+    status = 8
+
+
 _ERRS = {1: InvalidArgument, 2: NumericalError, 3: CudaError, 4: NcclError, 5: OverflowError_,
-         6: Unsupported, 7: ParseError}
+         6: Unsupported, 7: ParseError, 8: CallbackStop}
 
 
 class _CsrHost(C.Structure):
@@ -101,8 +106,12 @@ class _Newton(C.Structure):
     _fields_ = [("nlev", C.c_int), ("zeta", _dp)]
 
 
+_ITERATE_FN = C.CFUNCTYPE(C.c_int, C.c_int64, _dp, C.c_int64, C.c_void_p)
+
+
 class _Opts(C.Structure):
-    _fields_ = [("tol", C.c_double), ("maxit", C.c_int), ("x0", _vp), ("flags", C.c_uint32)]
+    _fields_ = [("tol", C.c_double), ("maxit", C.c_int), ("x0", _vp), ("flags", C.c_uint32),
+                ("on_iterate", _ITERATE_FN), ("on_iterate_user", C.c_void_p)]
 
 
 class _Report(C.Structure):
@@ -725,11 +734,14 @@ def apply_chebyshev_steps(params: ChebyshevParams, op: ScaledOperator, r) -> np.
 
 @dataclass
 class SolveOptions:
-    """SolveOptions (pcg.hpp:57-64). on_iterate is not supported on the device path."""
+    """SolveOptions (pcg.hpp:57-64). on_iterate(it, x) is called after every
+    iteration (pcg.cpp:88) with a host numpy copy of the current x (the rank's part
+    on a multi-rank context); an exception it raises stops the solve and propagates."""
     tol: float = 1e-8
     maxit: int = 20000
     x0: object = None
     flags: int = 0
+    on_iterate: object = None
 
 
 @dataclass
@@ -773,6 +785,16 @@ def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
     o = _Opts()
     L.pcgx_solve_opts_default(C.byref(o))
     o.tol, o.maxit, o.flags = opts.tol, opts.maxit, opts.flags
+    caught = []
+    if opts.on_iterate is not None:
+        def _tramp(it, xp, n, _user):
+            try:
+                opts.on_iterate(int(it), np.ctypeslib.as_array(xp, shape=(n,)).copy())
+                return 0
+            except BaseException as e:  # noqa: BLE001 - rethrown after the C call
+                caught.append(e)
+                return 1
+        o.on_iterate = _ITERATE_FN(_tramp)
     rep = _Report()
     newton = isinstance(prec, NewtonPreconditioner)
     cp = C.byref(prec.params()._c()) if prec is not None else None
@@ -782,7 +804,10 @@ def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
         x = x_out or DeviceVector(op.ctx, op.local_size())
         if opts.x0 is not None:
             o.x0 = opts.x0.ptr
-        _check(f_dev(op.ctx.h, op.h, cp, b.ptr, x.ptr, C.byref(o), C.byref(rep)), op.ctx.h)
+        st = f_dev(op.ctx.h, op.h, cp, b.ptr, x.ptr, C.byref(o), C.byref(rep))
+        if caught:
+            raise caught[0]
+        _check(st, op.ctx.h)
         return x, SolveReport._from(rep)
     b = np.ascontiguousarray(b, dtype=np.float64)
     if b.size != op.local_size():
@@ -794,8 +819,10 @@ def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
         if x0.size != b.size:
             raise InvalidArgument("pcg_solve: x0 length mismatch")
         o.x0 = x0.ctypes.data
-    _check(f_host(op.ctx.h, op.h, cp, _ptr(b), x.ctypes.data_as(_dp), C.byref(o), C.byref(rep)),
-           op.ctx.h)
+    st = f_host(op.ctx.h, op.h, cp, _ptr(b), x.ctypes.data_as(_dp), C.byref(o), C.byref(rep))
+    if caught:
+        raise caught[0]
+    _check(st, op.ctx.h)
     return x, SolveReport._from(rep)
 
 

@@ -9,10 +9,14 @@
 // polycg::pcg_solve (CPU reference) and polycg::gpu::pcg_solve (B200), and the
 // program prints one JSON line per case with both reports and the solution
 // difference; exit code 0 iff every case meets the parity bar.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <memory>
+#include <stdexcept>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "polycg/eigenest.hpp"
 #include "polycg/linop.hpp"
@@ -94,6 +98,54 @@ int main() {
     std::printf("{\"case\": \"stencil40_newton3\", \"ok\": %s, \"iters\": [%d, %d], "
                 "\"x_rel_diff\": %.3e, \"newton4_bitwise\": %s}\n",
                 ok ? "true" : "false", r_ref.iters, r_gpu.iters, rel, bitwise ? "true" : "false");
+    bad += ok ? 0 : 1;
+  }
+  // SolveOptions::on_iterate (pcg.hpp:62-63, pcg.cpp:88): the same (iteration, x)
+  // sequence as the reference; an exception thrown by the callback propagates
+  {
+    const StencilOperator st24(StencilKind::lap3d, 24);
+    auto [scaled, d] = jacobi_scale(st24);
+    const auto [a0, b0] = analytic_extremes(StencilKind::lap3d, 24, true);
+    const Vector b = scaled.apply(random_uniform_vector(scaled.size(), 20240801));
+    ChebyshevPreconditioner p_cpu(cheb_params(a0, b0, 6, 1.001));
+    ChebyshevPreconditioner p_gpu(cheb_params(a0, b0, 6, 1.001));
+    std::vector<std::pair<int, Vector>> seq_cpu, seq_gpu;
+    SolveOptions o_cpu, o_gpu;
+    o_cpu.on_iterate = [&](int it, const Vector& x) { seq_cpu.emplace_back(it, x); };
+    o_gpu.on_iterate = [&](int it, const Vector& x) { seq_gpu.emplace_back(it, x); };
+    auto [x_ref, r_ref] = pcg_solve(scaled, b, o_cpu, &p_cpu);
+    polycg::gpu::DeviceOperator dop(sess, scaled);
+    auto [x_gpu, r_gpu] = polycg::gpu::pcg_solve(sess, dop, scaled, b, o_gpu, &p_gpu);
+    bool ok = seq_cpu.size() == seq_gpu.size() && (int)seq_gpu.size() == r_gpu.iters;
+    double worst = 0.0;
+    for (size_t k = 0; ok && k < seq_cpu.size(); ++k) {
+      ok = seq_cpu[k].first == seq_gpu[k].first;
+      double dn = 0.0, xn = 0.0;
+      for (Index i = 0; i < seq_cpu[k].second.size(); ++i) {
+        const double e = seq_gpu[k].second[i] - seq_cpu[k].second[i];
+        dn += e * e;
+        xn += seq_cpu[k].second[i] * seq_cpu[k].second[i];
+      }
+      worst = std::max(worst, std::sqrt(dn / xn));
+    }
+    bool last_is_x = !seq_gpu.empty();
+    for (Index i = 0; last_is_x && i < x_gpu.size(); ++i) last_is_x = seq_gpu.back().second[i] == x_gpu[i];
+    ok = ok && worst <= 1e-10 && last_is_x;
+    bool thrown = false;
+    SolveOptions o_stop;
+    o_stop.on_iterate = [](int it, const Vector&) {
+      if (it == 3) throw std::runtime_error("stop at 3");
+    };
+    try {
+      polycg::gpu::pcg_solve(sess, dop, scaled, b, o_stop, &p_gpu);
+    } catch (const std::runtime_error& e) {
+      thrown = std::string(e.what()) == "stop at 3";
+    }
+    auto [x_again, r_again] = polycg::gpu::pcg_solve(sess, dop, scaled, b, {}, &p_gpu);
+    ok = ok && thrown && r_again.converged && r_again.iters == r_gpu.iters;
+    std::printf("{\"case\": \"on_iterate_stencil24_m6\", \"ok\": %s, \"calls\": [%zu, %zu], "
+                "\"worst_x_rel_diff\": %.3e, \"exception_propagated\": %s}\n",
+                ok ? "true" : "false", seq_cpu.size(), seq_gpu.size(), worst, thrown ? "true" : "false");
     bad += ok ? 0 : 1;
   }
   // error path: an unknown preconditioner type is rejected like a bad argument

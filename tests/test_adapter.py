@@ -27,7 +27,8 @@ def test_adapter_matches_reference_pcg_solve():
     res = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     lines = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
     assert res.returncode == 0, res.stdout + res.stderr
-    assert {l["case"] for l in lines} >= {"stencil40_m10", "csr30_m20", "stencil40_newton3", "reject_custom_prec"}
+    assert {l["case"] for l in lines} >= {"stencil40_m10", "csr30_m20", "stencil40_newton3", "on_iterate_stencil24_m6",
+                                         "reject_custom_prec"}
     for l in lines:
         assert l["ok"], l
         if "iters" in l:

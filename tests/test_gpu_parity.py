@@ -870,3 +870,46 @@ def test_odd_grids_take_the_scalar_paths(P, ctx, oracle, dims, m):
     assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
     if rep.iters == ro["iters"]:
         assert rel_norm(x, xo) <= 1e-10
+
+
+# ------------------------------------------------------------------ SolveOptions::on_iterate
+
+@pytest.mark.parametrize("m", [-1, 0, 4, 9])
+def test_on_iterate_sequence(P, ctx, m):
+    """on_iterate(it, x) after every iteration (pcg.cpp:88): called iters times in
+    order, the last x is the returned x bitwise, x(j) matches a solve stopped at
+    maxit = j, the solution matches the default (deferred-x, fused-update) schedule;
+    host and device entries alike."""
+    nx = 22
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    rhs = op.apply(P.random_uniform_vector(nx ** 3, SEED))
+    prec = None if m < 0 else P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001))
+    seen = []
+    x, rep = P.pcg_solve(op, rhs, P.SolveOptions(on_iterate=lambda it, xi: seen.append((it, xi))), prec)
+    assert rep.converged and [s[0] for s in seen] == list(range(1, rep.iters + 1))
+    assert np.array_equal(seen[-1][1], x)
+    x_def, rep_def = P.pcg_solve(op, rhs, None, prec)
+    assert abs(rep.iters - rep_def.iters) <= 1 and rel_norm(x, x_def) <= 1e-10
+    j = max(1, rep.iters // 2)
+    xj, rj = P.pcg_solve(op, rhs, P.SolveOptions(maxit=j), prec)
+    assert rj.iters == j and rel_norm(seen[j - 1][1], xj) <= 1e-10
+    seen_d = []
+    xd, rd = P.pcg_solve(op, P.DeviceVector.from_numpy(ctx, rhs),
+                         P.SolveOptions(on_iterate=lambda it, xi: seen_d.append(it)), prec)
+    assert seen_d == list(range(1, rd.iters + 1)) and np.array_equal(xd.numpy(), x)
+
+
+def test_on_iterate_exception_stops_the_solve(P, ctx):
+    op = stencil(P, ctx, 16)
+    a, b = P.analytic_extremes(3, 16)
+    rhs = op.apply(P.random_uniform_vector(16 ** 3, SEED))
+    prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, 6, 1.001))
+
+    def stop(it, x):
+        if it == 2:
+            raise KeyError("stop")
+    with pytest.raises(KeyError):
+        P.pcg_solve(op, rhs, P.SolveOptions(on_iterate=stop), prec)
+    x, rep = P.pcg_solve(op, rhs, None, prec)  # the context is usable afterwards
+    assert rep.converged
