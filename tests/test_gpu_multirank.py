@@ -26,7 +26,10 @@ def run_ranks(P, fn):
 
 
 @pytest.mark.parametrize("nranks,dims,m", [(2, (24, 24, 24), 10), (3, (20, 16, 26), 5),
-                                           (4, (32, 32, 30), 20), (4, (30, 30, 4), 3)])
+                                           (4, (32, 32, 30), 20), (4, (30, 30, 4), 3),
+                                           # the 8-GPU layouts: even slabs, uneven slabs, m = 0
+                                           (8, (64, 40, 48), 20), (8, (66, 20, 17), 7),
+                                           (8, (32, 32, 40), 0)])
 def test_slab_solve_matches_single_domain(pcgx, oracle, nranks, dims, m):
     P = pcgx
     nx, ny, nz = dims
