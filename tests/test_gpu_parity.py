@@ -913,3 +913,23 @@ def test_on_iterate_exception_stops_the_solve(P, ctx):
         P.pcg_solve(op, rhs, P.SolveOptions(on_iterate=stop), prec)
     x, rep = P.pcg_solve(op, rhs, None, prec)  # the context is usable afterwards
     assert rep.converged
+
+
+def test_assembled_laplacian_as_stencil_opt_in(P, ctx, oracle, monkeypatch):
+    """PCGX_CSR_STENCIL=1: an assembled lap3d CsrMatrix (exact pattern, 6 / -1,
+    1/sqrt(6) Jacobi) is served by the matrix-free kernels, bitwise the CSR path;
+    any other matrix (a perturbed value) keeps a CSR storage."""
+    nx = 18
+    rp, ci, va = lap3d_csr(nx)
+    x = oracle.random_uniform(nx ** 3, 8)
+    op_c = csr(P, ctx, rp, ci, va)
+    assert op_c.storage() == "dia"
+    monkeypatch.setenv("PCGX_CSR_STENCIL", "1")
+    op_s = csr(P, ctx, rp, ci, va)
+    assert op_s.storage() == "stencil" and op_s.nnz() == len(ci)
+    assert np.array_equal(op_s.apply(x), op_c.apply(x))
+    prm = P.cheb_params(*P.analytic_extremes(3, nx), 9, 1.001)
+    assert np.array_equal(P.apply_chebyshev(prm, op_s, x), P.apply_chebyshev(prm, op_c, x))
+    va2 = va.copy()
+    va2[np.flatnonzero(va == 6.0)[5]] = 6.5
+    assert csr(P, ctx, rp, ci, va2).storage() == "dia"
