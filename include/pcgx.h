@@ -145,7 +145,9 @@ int64_t pcgx_operator_nnz(pcgx_operator op);         /* CSR nnz, or the assemble
  * 2 BSR-3 (aligned 3x3 blocks, detected), 3 CSR row tiles (TMA), 4 chunked CSR,
  * 5 offset (diagonal) storage (at most 32 distinct column offsets, detected),
  * 6 offset storage on a cubic grid whose offsets are the 27-point box or the
- *   7-point star (detected; applied by grid tiles with t = d x staged on chip). */
+ *   7-point star (detected; applied by grid tiles with t = d x staged on chip),
+ * 7 BSR-3 whose nodes form a cubic grid with the 27-point block box: the BSR-3
+ *   arrays plus a grid copy the regular Chebyshev steps stream by TMA. */
 int pcgx_operator_storage(pcgx_operator op);
 /* Number of matvecs applied so far (LinearOperator::matvec_count, linop.hpp:37). */
 uint64_t pcgx_operator_matvec_count(pcgx_operator op);

@@ -32,6 +32,7 @@
 #include "cheb2.cuh"
 #include "cheb2f.cuh"
 #include "common.cuh"
+#include "bsr3t.cuh"
 #include "dia3t.cuh"
 #include "dir_tma.cuh"
 #include "host_math.hpp"
@@ -136,6 +137,12 @@ struct pcgx_operator_s {
   int bsr_slices = 0;
   long long bsr_blocks = 0;     // stored (unpadded) blocks = nnz / 9
   long long bsr_padded = 0;     // blocks incl. slice padding
+  // BSR-3 on a cubic node grid with the 27-point block box (bsr3t_kernel): grid copy
+  // of the values gval[(s * 9 + e) * ldn + node] and a 27-bit presence mask per node
+  double* b3g_val = nullptr;
+  unsigned* b3g_mask = nullptr;
+  long long b3g_ld = 0;
+  int b3g_nx = 0;
   // offset (diagonal) storage (dia_kernel): K fixed column offsets, values by offset
   double* dia_val = nullptr;
   unsigned* dia_mask = nullptr;
@@ -656,6 +663,8 @@ bool dia3_on(pcgx_operator op) {
 
 template <bool kRed>
 bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot);
+template <bool kRed>
+bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot);
 
 // Whether the operator's kernels accept the fused direction-update input.
 bool fuses_dir_update(pcgx_operator op) {
@@ -719,6 +728,9 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
     return;
   }
   if (op->kind == 1 && op->bsr_ptr) {
+    if constexpr (std::is_same<In, InVec>::value && std::is_same<Epi, EpiChebStep>::value) {
+      if (bsr3t_launch<kRed>(c, op, in, epi, slot)) return;
+    }
     Bsr3Geom g{(int)(op->n_local / 3), 0, op->bsr_slices, op->bsr_ptr, op->bsr_len, op->bsr_col,
                op->bsr_val, op->dvec};
     const int wpb = 8;
@@ -1002,6 +1014,72 @@ bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiCh
   }
   Reduce red = kRed ? make_red(c, slot) : Reduce{};
   dia3t_kernel<kRed><<<grid, kD3Threads, kDia3tSmem, c->s>>>(maps, nx, kz, epi, red);
+  check_launch();
+  count_launch(c);
+  return true;
+}
+
+// bsr3t_kernel tensor maps (cached per buffer): kind 20 value array (4D), 21 masks,
+// 22 (3 nx, nx, nx) fp64 tiles of 96 x 4, 23 patches of 108 x 6.
+const CUtensorMap& bsr3t_map(pcgx_operator op, const void* ptr, int kind) {
+  for (auto& g : op->gmaps)
+    if (g.ptr == ptr && g.kind == kind) return g.m;
+  const cuuint64_t nx = (cuuint64_t)op->b3g_nx;
+  CUtensorMap m;
+  CUresult r;
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (kind == 20) {
+    const cuuint64_t dims[4] = {nx, nx, nx, 243};
+    const cuuint64_t strides[3] = {nx * 8, nx * nx * 8, (cuuint64_t)op->b3g_ld * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)kB3X, (cuuint32_t)kB3Y, 1, 27};
+    r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (kind == 21) {
+    const cuuint64_t dims[3] = {nx, nx, nx};
+    const cuuint64_t strides[2] = {nx * 4, nx * nx * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)kB3X, (cuuint32_t)kB3Y, 1};
+    r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[3] = {3 * nx, nx, nx};
+    const cuuint64_t strides[2] = {3 * nx * 8, 3 * nx * nx * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)(kind == 22 ? 3 * kB3X : kB3PX), (cuuint32_t)(kind == 22 ? kB3Y : kB3PY),
+                               1};
+    r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) fail(PCGX_ERR_CUDA, "cuTensorMapEncodeTiled (bsr3t) failed: " + std::to_string((int)r));
+  op->gmaps.push_back({ptr, kind, m});
+  return op->gmaps.back().m;
+}
+
+template <bool kRed>
+bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot) {
+  const int nx = op->b3g_nx;
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+  if (!op->b3g_val || env_int("PCGX_BSR3T", 1) == 0 || in.gx || !al16(in.x) || !al16(epi.r) || !al16(epi.out) ||
+      (!epi.xold_from_r && !al16(epi.xold)) || epi.out == in.x || epi.out == epi.r)
+    return false;
+  Bsr3tMaps maps;
+  maps.val = bsr3t_map(op, op->b3g_val, 20);
+  maps.mask = bsr3t_map(op, op->b3g_mask, 21);
+  maps.r = bsr3t_map(op, epi.r, 22);
+  maps.xo = epi.xold_from_r ? maps.r : bsr3t_map(op, epi.xold, 22);
+  maps.x = bsr3t_map(op, in.x, 23);
+  maps.d = bsr3t_map(op, op->dvec, 23);
+  const int kz = std::max(1, env_int("PCGX_BSR3T_KZ", 32));
+  const int tiles = ((nx + kB3X - 1) / kB3X) * ((nx + kB3Y - 1) / kB3Y);
+  const dim3 grid(tiles, (nx + kz - 1) / kz);
+  static bool attr = false;
+  if (!attr) {
+    PCGX_CUDA(cudaFuncSetAttribute(bsr3t_kernel<kRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsr3tSmem));
+    attr = true;
+  }
+  Reduce red = kRed ? make_red(c, slot) : Reduce{};
+  bsr3t_kernel<kRed><<<grid, kB3Threads, kBsr3tSmem, c->s>>>(maps, nx, kz, epi, red);
   check_launch();
   count_launch(c);
   return true;
@@ -1620,6 +1698,10 @@ std::string fmt_double(double v) { return std::to_string(v); }
 // BSR-3 8 nnz + 4 per block + 4 per block row; stencil none.
 double matrix_bytes(pcgx_operator op) {
   if (op->kind == 0) return 0.0;
+  // the grid copy the regular steps stream (bsr3t_kernel): every slot of every node
+  // (absent blocks as zeros) + the masks; the other launches' SELL arrays are ~4% larger
+  if (op->b3g_val && env_int("PCGX_BSR3T", 1) != 0)
+    return 8.0 * 243.0 * (double)(op->n_local / 3) + 4.0 * (double)(op->n_local / 3);
   if (op->bsr_ptr)
     return 8.0 * (double)op->nnz + 4.0 * (double)op->bsr_blocks + 4.0 * (double)(op->n_local / 3 + 1);
   if (op->dia_val) return 8.0 * (double)op->dia_k * (double)op->n_local + 4.0 * (double)op->n_local;
@@ -2553,6 +2635,62 @@ void build_dia(pcgx_operator op, long long n, const std::vector<int>& rp32,
   PCGX_CUDA(cudaMemcpy(op->dia_mask, mask.data(), sizeof(unsigned) * mask.size(), cudaMemcpyHostToDevice));
 }
 
+// The bsr3t_kernel's grid copy of a BSR-3 matrix whose nodes form a cubic nx^3
+// grid (nx % 4 == 0, nx >= 36: TMA strides and boxes) and whose blocks lie in the
+// 27-point box without wrapping across a face; built slot by slot (one 9 ldn
+// host buffer at a time) so the host never holds a second full copy.
+void bsr3_grid_build(pcgx_operator op, long long n, const std::vector<int>& rp32,
+                     const std::vector<int>& ci32, const double* va) {
+  if (env_int("PCGX_BSR3T", 1) == 0) return;
+  const long long nb = n / 3;
+  long long nx = (long long)std::llround(std::cbrt((double)nb));
+  while (nx * nx * nx > nb) --nx;
+  while ((nx + 1) * (nx + 1) * (nx + 1) <= nb) ++nx;
+  if (nx * nx * nx != nb || nx % 4 != 0 || nx < kB3PX / 3) return;
+  const long long nxy = nx * nx;
+  std::vector<signed char> pos((size_t)nb * 27, (signed char)-1);  // block index of slot s
+  int ok = 1;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+  for (long long b = 0; b < nb; ++b) {
+    const int a = (int)(b % nx), bb = (int)((b / nx) % nx), cc = (int)(b / nxy);
+    const int len = (rp32[(size_t)(3 * b + 1)] - rp32[(size_t)(3 * b)]) / 3;
+    for (int k = 0; k < len && ok; ++k) {
+      const long long o = (long long)(ci32[(size_t)rp32[(size_t)(3 * b)] + 3 * k] / 3) - b;
+      int s = -1;
+      for (int q = 0; q < 27; ++q)
+        if (o == (q / 9 - 1) * nxy + ((q / 3) % 3 - 1) * nx + (q % 3 - 1)) s = q;
+      if (s < 0) { ok = 0; break; }
+      const int x2 = a + s % 3 - 1, y2 = bb + (s / 3) % 3 - 1, z2 = cc + s / 9 - 1;
+      if (x2 < 0 || x2 >= nx || y2 < 0 || y2 >= nx || z2 < 0 || z2 >= nx) { ok = 0; break; }
+      pos[(size_t)(b * 27 + s)] = (signed char)k;
+    }
+  }
+  if (!ok) return;
+  const long long ldn = (nb + 31) / 32 * 32;
+  std::vector<unsigned> mask((size_t)nb, 0u);
+#pragma omp parallel for schedule(static)
+  for (long long b = 0; b < nb; ++b)
+    for (int s = 0; s < 27; ++s)
+      if (pos[(size_t)(b * 27 + s)] >= 0) mask[(size_t)b] |= 1u << s;
+  PCGX_CUDA(cudaMalloc(&op->b3g_val, sizeof(double) * (size_t)(243 * ldn)));
+  PCGX_CUDA(cudaMalloc(&op->b3g_mask, sizeof(unsigned) * (size_t)nb));
+  PCGX_CUDA(cudaMemcpy(op->b3g_mask, mask.data(), sizeof(unsigned) * (size_t)nb, cudaMemcpyHostToDevice));
+  std::vector<double> buf((size_t)(9 * ldn));
+  for (int s = 0; s < 27; ++s) {
+#pragma omp parallel for schedule(static)
+    for (long long b = 0; b < ldn; ++b) {
+      const int k = b < nb ? pos[(size_t)(b * 27 + s)] : -1;
+      for (int c = 0; c < 3; ++c)
+        for (int d = 0; d < 3; ++d)
+          buf[(size_t)((3 * c + d) * ldn + b)] = k >= 0 ? va[(size_t)rp32[(size_t)(3 * b + c)] + 3 * k + d] : 0.0;
+    }
+    PCGX_CUDA(cudaMemcpy(op->b3g_val + (size_t)(9 * s * ldn), buf.data(), sizeof(double) * buf.size(),
+                         cudaMemcpyHostToDevice));
+  }
+  op->b3g_ld = ldn;
+  op->b3g_nx = (int)nx;
+}
+
 // BSR-3 / SELL-32 arrays (see bsr3_kernel) of an int32 CSR with is_bsr3 structure.
 void build_bsr3(pcgx_operator op, long long n, const std::vector<int>& rp32,
                 const std::vector<int>& ci32, const double* va) {
@@ -2595,6 +2733,7 @@ void build_bsr3(pcgx_operator op, long long n, const std::vector<int>& rp32,
   PCGX_CUDA(cudaMemcpy(op->bsr_len, bl.data(), sizeof(int) * bl.size(), cudaMemcpyHostToDevice));
   PCGX_CUDA(cudaMemcpy(op->bsr_col, bcol.data(), sizeof(int) * bcol.size(), cudaMemcpyHostToDevice));
   PCGX_CUDA(cudaMemcpy(op->bsr_val, bval.data(), sizeof(double) * bval.size(), cudaMemcpyHostToDevice));
+  bsr3_grid_build(op, n, rp32, ci32, va);
 }
 
 template <class IdxT>
@@ -2720,6 +2859,8 @@ void free_op(pcgx_operator op) {
   cudaFree(op->bsr_len);
   cudaFree(op->bsr_col);
   cudaFree(op->bsr_val);
+  cudaFree(op->b3g_val);
+  cudaFree(op->b3g_mask);
   cudaFree(op->dia_val);
   cudaFree(op->dia_mask);
   cudaFree(op->send_idx);
@@ -3084,7 +3225,7 @@ int64_t pcgx_operator_nnz(pcgx_operator op) { return op ? op->nnz : -1; }
 int pcgx_operator_storage(pcgx_operator op) {
   if (!op) return -1;
   if (op->kind == 0) return 0;
-  if (op->bsr_ptr) return 2;
+  if (op->bsr_ptr) return op->b3g_val && env_int("PCGX_BSR3T", 1) != 0 ? 7 : 2;
   if (op->dia_val) return dia3_on(op) ? 6 : 5;
   if (op->sell_ptr) return 1;
   return op->tile_row ? 3 : 4;

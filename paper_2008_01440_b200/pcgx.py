@@ -522,7 +522,7 @@ class ScaledOperator:
         """First global row owned by this rank (slab / block rows)."""
         return lib().pcgx_operator_row0(self.h)
 
-    STORAGE = {0: "stencil", 1: "sell32", 2: "bsr3", 3: "csr_tiles", 4: "csr_chunked", 5: "dia", 6: "dia_grid"}
+    STORAGE = {0: "stencil", 1: "sell32", 2: "bsr3", 3: "csr_tiles", 4: "csr_chunked", 5: "dia", 6: "dia_grid", 7: "bsr3_grid"}
 
     def storage(self) -> str:
         """Device storage of the operator (pcgx_operator_storage)."""

@@ -468,12 +468,13 @@ def test_cfg3_256_full_size(P, ctx, monkeypatch):
 
 @pytest.mark.slow
 def test_cfg4_160_full_size(P, ctx, monkeypatch):
-    """Config 4 at its full size (160^3 x 3 dof, 982,938,168 nnz): BSR-3 gives the
-    SELL-32 CSR row sums bitwise (SpMV and a Chebyshev apply)."""
+    """Config 4 at its full size (160^3 x 3 dof, 982,938,168 nnz): BSR-3 (with the
+    grid copy its regular steps stream) gives the SELL-32 CSR row sums bitwise (SpMV
+    and a Chebyshev apply)."""
     A = P.gen_elast27(160, 1.0, 0.5, 0.1, seed=SEED)
     assert A.nnz() == 982938168
     op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
-    assert op.storage() == "bsr3"
+    assert op.storage() == "bsr3_grid"
     x = P.random_uniform_vector(A.n, 29, ctx=ctx)
     y = op.apply(x).numpy()
     prm = P.cheb_params(0.001, 2.5, 5, 1.001)
@@ -731,6 +732,38 @@ def test_bsr3_solve_vs_oracle(P, ctx, oracle):
         assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
         if rep.iters == ro["iters"]:
             assert rel_norm(x, xo) <= 1e-10
+
+
+@pytest.mark.parametrize("nx,kz", [(36, "32"), (40, "7"), (44, "5")])
+def test_bsr3_grid_tma_step_bitwise(P, ctx, oracle, nx, kz, monkeypatch):
+    """bsr3t_kernel (regular Chebyshev steps of BSR-3 on the node grid, every operand
+    by TMA; ragged 32 x 4 tiles, partial z-chunks) against the oracle and the
+    SELL-32 BSR-3 kernel bitwise, and a whole solve."""
+    monkeypatch.setenv("PCGX_BSR3T_KZ", kz)
+    A = P.gen_elast27(nx, 1.0, 0.5, 0.1, seed=SEED)
+    opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    x = oracle.random_uniform(A.n, 19)
+    outs = {}
+    for t in ("1", "0"):
+        monkeypatch.setenv("PCGX_BSR3T", t)
+        op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+        assert op.storage() == ("bsr3_grid" if t == "1" else "bsr3")
+        for m in (2, 3, 6):
+            prm = P.cheb_params(0.01, 2.9, m, 1.001)
+            outs[(t, m)] = P.apply_chebyshev(prm, op, x)
+        op.close()
+    for m in (2, 3, 6):
+        ref = oracle.apply_chebyshev(opo, oracle.cheb_params(0.01, 2.9, m, 1.001), x)
+        assert np.array_equal(outs[("1", m)], ref) and np.array_equal(outs[("0", m)], ref), m
+    monkeypatch.setenv("PCGX_BSR3T", "1")
+    op = csr(P, ctx, A.row_ptr, A.col_idx, A.values)
+    lo, hi = P.lanczos_bounds(op, 20, 30, SEED)
+    rhs = op.apply(P.random_uniform_vector(A.n, SEED))
+    xs, rep = P.pcg_solve(op, rhs, P.SolveOptions(maxit=5000), P.ChebyshevPreconditioner(P.cheb_params(lo, hi, 12, 1.001)))
+    xo, ro = oracle.pcg_solve(opo, oracle.cheb_params(lo, hi, 12, 1.001), rhs, maxit=5000)
+    assert rep.converged and abs(rep.iters - ro["iters"]) <= 1
+    if rep.iters == ro["iters"]:
+        assert rel_norm(xs, xo) <= 1e-10
 
 
 def test_storage_selection(P, ctx, golden):

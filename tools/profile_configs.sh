@@ -7,7 +7,7 @@ for cfg in "$@"; do
   case $cfg in
     cfg1) kern=dia_kernel; skip=40 ;;
     cfg3) kern=dia3t_kernel; skip=40 ;;
-    cfg4) kern=bsr3_kernel; skip=40 ;;
+    cfg4) kern=bsr3t_kernel; skip=40 ;;
     *) kern="cheb2f_kernel<\\(bool\\)0, \\(bool\\)0, \\(bool\\)0, \\(bool\\)0>"; skip=100 ;;
   esac
   extra=""
