@@ -58,9 +58,12 @@ struct Dia3tMaps {
   CUtensorMap x, d;  // 3D fp64, box (36, 10, 1)
 };
 
-template <bool kRed>
+// Epi: EpiChebStep (regular step: r and x_old tiles by TMA) or EpiChebFirst (step 1,
+// polyprec.cpp:187-189: x_1 = c1 ((2 r) - (A r) / theta), the input IS r, no tiles)
+template <bool kRed, class Epi>
 __global__ void __launch_bounds__(kD3Threads, 1)
-dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, EpiChebStep epi, Reduce red) {
+dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, Epi epi, Reduce red) {
+  constexpr bool kFirst = std::is_same<Epi, EpiChebFirst>::value;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* st0 = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   double* tr = st0 + kT3D * kT3Stage;  // t ring, 4 planes
@@ -72,9 +75,11 @@ dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, EpiChebStep
   const int i = i0 + tx, j = j0 + ty;
   const bool own = i < nx && j < nx;
   const long long nxy = (long long)nx * nx;
-  const bool need_xo = !epi.xold_from_r;
+  bool need_xo = false;
+  if constexpr (!kFirst) need_xo = !epi.xold_from_r;
   const unsigned bytes_tile = kT3Tile * 8, bytes_patch = kT3Patch * 8;
-  const unsigned bytes_vals = (unsigned)(kT3K * kT3Tile * 8) + bytes_tile / 2 + bytes_tile * (need_xo ? 2 : 1);
+  const unsigned bytes_vals =
+      (unsigned)(kT3K * kT3Tile * 8) + bytes_tile / 2 + (kFirst ? 0u : bytes_tile * (need_xo ? 2 : 1));
   const int u0 = kb - 2;  // first unit
 
   // unit u: values, masks, r, x_old of plane u (kb <= u < ke) and the x, d
@@ -88,7 +93,7 @@ dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, EpiChebStep
     if (vals) {
       tma_load_4d(s + kT3OffV, &maps.val, i0, j0, u, 0, bar);
       tma_load_3d(s + kT3OffM, &maps.mask, i0, j0, u, bar);
-      tma_load_3d(s + kT3OffR, &maps.r, i0, j0, u, bar);
+      if (!kFirst) tma_load_3d(s + kT3OffR, &maps.r, i0, j0, u, bar);
       if (need_xo) tma_load_3d(s + kT3OffO, &maps.xo, i0, j0, u, bar);
     }
     if (pat) {
@@ -149,11 +154,18 @@ dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, EpiChebStep
         if ((msk >> q) & 1u) sum = sum + s[kT3OffV + q * kT3Tile + tid] * pl[Pat::dy(q) * kT3PX + Pat::dx(q)];
       }
       const double y = sum * dr;
-      const double ri = s[kT3OffR + tid];
-      const double xo = need_xo ? s[kT3OffO + tid] : 0.0;
-      const double xnew = epi.f(y, xr, ri, xo);
-      epi.out[(long long)k * nxy + (long long)j * nx + i] = xnew;
-      if (kRed) acc = acc + ri * xnew;
+      const long long row = (long long)k * nxy + (long long)j * nx + i;
+      if constexpr (kFirst) {
+        const double xnew = epi.f(y, xr);
+        epi.xout[row] = xnew;
+        if (kRed) acc = acc + xr * xnew;  // EpiChebFirst: r . x_1 (m == 1)
+      } else {
+        const double ri = s[kT3OffR + tid];
+        const double xo = need_xo ? s[kT3OffO + tid] : 0.0;
+        const double xnew = epi.f(y, xr, ri, xo);
+        epi.out[row] = xnew;
+        if (kRed) acc = acc + ri * xnew;
+      }
     }
     xr = xn_;
     dr = dn_;

@@ -664,6 +664,8 @@ bool dia3_on(pcgx_operator op) {
 template <bool kRed>
 bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot);
 template <bool kRed>
+bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebFirst& epi, int slot);
+template <bool kRed>
 bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot);
 
 // Whether the operator's kernels accept the fused direction-update input.
@@ -689,7 +691,8 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
     // one full wave of resident blocks, grid-stride over the rows (a partial second
     // wave would leave SMs idle at the tail)
     const bool stream = (double)op->dia_k * (double)op->dia_ld * 8.0 > 64e6;  // values exceed ~half of L2
-    if constexpr (std::is_same<In, InVec>::value && std::is_same<Epi, EpiChebStep>::value) {
+    if constexpr (std::is_same<In, InVec>::value &&
+                  (std::is_same<Epi, EpiChebStep>::value || std::is_same<Epi, EpiChebFirst>::value)) {
       if (dia3t_launch<kRed>(c, op, in, epi, slot)) return;
     }
     if (dia3_on(op)) {
@@ -989,19 +992,30 @@ const CUtensorMap& dia3t_map(pcgx_operator op, const void* ptr, int kind) {
   return op->gmaps.back().m;
 }
 
-template <bool kRed>
-bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot) {
+template <bool kRed, class Epi>
+bool dia3t_launch_any(pcgx_context c, pcgx_operator op, const InVec& in, const Epi& epi, int slot) {
+  constexpr bool kFirst = std::is_same<Epi, EpiChebFirst>::value;
+  const double* eout;
+  const double* er = nullptr;
+  const double* exo = nullptr;
+  if constexpr (kFirst) {
+    eout = epi.xout;
+  } else {
+    eout = epi.out;
+    er = epi.r;
+    if (!epi.xold_from_r) exo = epi.xold;
+  }
   const int nx = op->dia3_nx;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
   if (!dia3_on(op) || op->dia3_pat != 27 || env_int("PCGX_DIA3T", 1) == 0 || nx % 4 != 0 || nx < kT3PX ||
-      in.gx || !al16(in.x) || !al16(epi.r) || !al16(epi.out) || (!epi.xold_from_r && !al16(epi.xold)) ||
-      epi.out == in.x || epi.out == epi.r)
+      in.gx || !al16(in.x) || (er && !al16(er)) || !al16(eout) || (exo && !al16(exo)) || eout == in.x ||
+      (er && eout == er))
     return false;
   Dia3tMaps maps;
   maps.val = dia3t_map(op, op->dia_val, 3);
   maps.mask = dia3t_map(op, op->dia_mask, 2);
-  maps.r = dia3t_map(op, epi.r, 0);
-  maps.xo = epi.xold_from_r ? maps.r : dia3t_map(op, epi.xold, 0);
+  maps.r = er ? dia3t_map(op, er, 0) : maps.mask;  // unused for the first step
+  maps.xo = exo ? dia3t_map(op, exo, 0) : maps.r;
   maps.x = dia3t_map(op, in.x, 1);
   maps.d = dia3t_map(op, op->dvec, 1);
   const int kz = std::max(1, env_int("PCGX_DIA3T_KZ", 32));  // 8: -3%, 16: -1.5% at 256^3
@@ -1009,14 +1023,22 @@ bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiCh
   const dim3 grid(tiles, (nx + kz - 1) / kz);
   static bool attr = false;
   if (!attr) {
-    PCGX_CUDA(cudaFuncSetAttribute(dia3t_kernel<kRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDia3tSmem));
+    PCGX_CUDA(cudaFuncSetAttribute(dia3t_kernel<kRed, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDia3tSmem));
     attr = true;
   }
   Reduce red = kRed ? make_red(c, slot) : Reduce{};
-  dia3t_kernel<kRed><<<grid, kD3Threads, kDia3tSmem, c->s>>>(maps, nx, kz, epi, red);
+  dia3t_kernel<kRed, Epi><<<grid, kD3Threads, kDia3tSmem, c->s>>>(maps, nx, kz, epi, red);
   check_launch();
   count_launch(c);
   return true;
+}
+template <bool kRed>
+bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot) {
+  return dia3t_launch_any<kRed>(c, op, in, epi, slot);
+}
+template <bool kRed>
+bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebFirst& epi, int slot) {
+  return env_int("PCGX_DIA3T_FIRST", 1) != 0 && dia3t_launch_any<kRed>(c, op, in, epi, slot);
 }
 
 // bsr3t_kernel tensor maps (cached per buffer): kind 20 value array (4D), 21 masks,
