@@ -44,7 +44,8 @@ constexpr int kT3OffR = kT3OffM + kT3Tile / 2;
 constexpr int kT3OffO = kT3OffR + kT3Tile;
 constexpr int kT3OffX = kT3OffO + kT3Tile;
 constexpr int kT3OffD = kT3OffX + (kT3Patch + 15) / 16 * 16;
-constexpr int kT3Stage = kT3OffD + (kT3Patch + 15) / 16 * 16;
+constexpr int kT3OffP = kT3OffD + (kT3Patch + 15) / 16 * 16;  // direction step: p_old patch
+constexpr int kT3Stage = kT3OffP + (kT3Patch + 15) / 16 * 16;
 constexpr int kT3TRing = 4;
 constexpr size_t kDia3tSmem =
     sizeof(double) * ((size_t)kT3D * kT3Stage + (size_t)kT3TRing * kT3Patch) + 16 * kT3D + 128;
@@ -56,14 +57,22 @@ struct Dia3tMaps {
   CUtensorMap mask;  // 3D (nx, nx, nx) u32, box (32, 8, 1)
   CUtensorMap r, xo; // 3D fp64, box (32, 8, 1)
   CUtensorMap x, d;  // 3D fp64, box (36, 10, 1)
+  CUtensorMap p;     // direction step: p_old patches (36, 10, 1)
 };
 
-// Epi: EpiChebStep (regular step: r and x_old tiles by TMA) or EpiChebFirst (step 1,
+// Epi: EpiChebStep (regular step: r and x_old tiles by TMA), EpiChebFirst (step 1,
 // polyprec.cpp:187-189: x_1 = c1 ((2 r) - (A r) / theta), the input IS r, no tiles)
-template <bool kRed, class Epi>
+// or EpiStoreP with In = InComb (the PCG direction step, pcg.cpp:63,72-74,107: the
+// patches of z and p_old combine into p = z + beta p_old before t = d p; q = A p,
+// p written at the own points, p . q reduced)
+template <bool kRed, class Epi, class In = InVec>
 __global__ void __launch_bounds__(kD3Threads, 1)
-dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, Epi epi, Reduce red) {
+dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, Epi epi, Reduce red, In in) {
   constexpr bool kFirst = std::is_same<Epi, EpiChebFirst>::value;
+  constexpr bool kDir = std::is_same<Epi, EpiStoreP>::value;
+  in.init();
+  bool first_dir = false;
+  if constexpr (kDir) first_dir = in.first != 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* st0 = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   double* tr = st0 + kT3D * kT3Stage;  // t ring, 4 planes
@@ -76,10 +85,11 @@ dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, Epi epi, Re
   const bool own = i < nx && j < nx;
   const long long nxy = (long long)nx * nx;
   bool need_xo = false;
-  if constexpr (!kFirst) need_xo = !epi.xold_from_r;
+  if constexpr (!kFirst && !kDir) need_xo = !epi.xold_from_r;
   const unsigned bytes_tile = kT3Tile * 8, bytes_patch = kT3Patch * 8;
   const unsigned bytes_vals =
-      (unsigned)(kT3K * kT3Tile * 8) + bytes_tile / 2 + (kFirst ? 0u : bytes_tile * (need_xo ? 2 : 1));
+      (unsigned)(kT3K * kT3Tile * 8) + bytes_tile / 2 + (kFirst || kDir ? 0u : bytes_tile * (need_xo ? 2 : 1));
+  const unsigned npatch = (kDir && !first_dir) ? 3u : 2u;
   const int u0 = kb - 2;  // first unit
 
   // unit u: values, masks, r, x_old of plane u (kb <= u < ke) and the x, d
@@ -89,16 +99,17 @@ dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, Epi epi, Re
     double* s = st0 + sidx * kT3Stage;
     uint64_t* bar = &bars[sidx];
     const bool vals = u >= kb && u < ke, pat = u + 1 >= 0 && u + 1 < nx;
-    mbar_expect_tx(bar, (vals ? bytes_vals : 0u) + (pat ? 2 * bytes_patch : 0u));
+    mbar_expect_tx(bar, (vals ? bytes_vals : 0u) + (pat ? npatch * bytes_patch : 0u));
     if (vals) {
       tma_load_4d(s + kT3OffV, &maps.val, i0, j0, u, 0, bar);
       tma_load_3d(s + kT3OffM, &maps.mask, i0, j0, u, bar);
-      if (!kFirst) tma_load_3d(s + kT3OffR, &maps.r, i0, j0, u, bar);
+      if (!kFirst && !kDir) tma_load_3d(s + kT3OffR, &maps.r, i0, j0, u, bar);
       if (need_xo) tma_load_3d(s + kT3OffO, &maps.xo, i0, j0, u, bar);
     }
     if (pat) {
       tma_load_3d(s + kT3OffX, &maps.x, i0 - 2, j0 - 1, u + 1, bar);
       tma_load_3d(s + kT3OffD, &maps.d, i0 - 2, j0 - 1, u + 1, bar);
+      if (kDir && !first_dir) tma_load_3d(s + kT3OffP, &maps.p, i0 - 2, j0 - 1, u + 1, bar);
     }
   };
   auto wait_unit = [&](int u) {
@@ -112,8 +123,14 @@ dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, Epi epi, Re
     const double* s = st0 + ((u - u0) % kT3D) * kT3Stage;
     double* tp = tr + ((u + 1 + kT3TRing) & 3) * kT3Patch;
     const bool pat = u + 1 >= 0 && u + 1 < nx;
-    for (int e = tid; e < kT3Patch; e += kD3Threads) tp[e] = pat ? s[kT3OffD + e] * s[kT3OffX + e] : 0.0;
-    xo_ = pat ? s[kT3OffX + own_p] : 0.0;
+    if constexpr (kDir) {  // p = z + beta p_old, combined once per element (InComb::f)
+      for (int e = tid; e < kT3Patch; e += kD3Threads)
+        tp[e] = pat ? s[kT3OffD + e] * in.f(s[kT3OffX + e], first_dir ? 0.0 : s[kT3OffP + e]) : 0.0;
+      xo_ = pat ? in.f(s[kT3OffX + own_p], first_dir ? 0.0 : s[kT3OffP + own_p]) : 0.0;
+    } else {
+      for (int e = tid; e < kT3Patch; e += kD3Threads) tp[e] = pat ? s[kT3OffD + e] * s[kT3OffX + e] : 0.0;
+      xo_ = pat ? s[kT3OffX + own_p] : 0.0;
+    }
     do_ = pat ? s[kT3OffD + own_p] : 0.0;
   };
 
@@ -155,7 +172,11 @@ dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, Epi epi, Re
       }
       const double y = sum * dr;
       const long long row = (long long)k * nxy + (long long)j * nx + i;
-      if constexpr (kFirst) {
+      if constexpr (kDir) {
+        epi.q[row] = y;
+        epi.pout[row] = xr;
+        if (kRed) acc = acc + xr * y;  // EpiStoreP: p . q
+      } else if constexpr (kFirst) {
         const double xnew = epi.f(y, xr);
         epi.xout[row] = xnew;
         if (kRed) acc = acc + xr * xnew;  // EpiChebFirst: r . x_1 (m == 1)

@@ -666,6 +666,8 @@ bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiCh
 template <bool kRed>
 bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebFirst& epi, int slot);
 template <bool kRed>
+bool dia3t_launch(pcgx_context c, pcgx_operator op, const InComb& in, const EpiStoreP& epi, int slot);
+template <bool kRed>
 bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot);
 
 // Whether the operator's kernels accept the fused direction-update input.
@@ -691,8 +693,9 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
     // one full wave of resident blocks, grid-stride over the rows (a partial second
     // wave would leave SMs idle at the tail)
     const bool stream = (double)op->dia_k * (double)op->dia_ld * 8.0 > 64e6;  // values exceed ~half of L2
-    if constexpr (std::is_same<In, InVec>::value &&
-                  (std::is_same<Epi, EpiChebStep>::value || std::is_same<Epi, EpiChebFirst>::value)) {
+    if constexpr ((std::is_same<In, InVec>::value &&
+                   (std::is_same<Epi, EpiChebStep>::value || std::is_same<Epi, EpiChebFirst>::value)) ||
+                  (std::is_same<In, InComb>::value && std::is_same<Epi, EpiStoreP>::value)) {
       if (dia3t_launch<kRed>(c, op, in, epi, slot)) return;
     }
     if (dia3_on(op)) {
@@ -992,42 +995,62 @@ const CUtensorMap& dia3t_map(pcgx_operator op, const void* ptr, int kind) {
   return op->gmaps.back().m;
 }
 
-template <bool kRed, class Epi>
-bool dia3t_launch_any(pcgx_context c, pcgx_operator op, const InVec& in, const Epi& epi, int slot) {
+template <bool kRed, class Epi, class In>
+bool dia3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi, int slot) {
   constexpr bool kFirst = std::is_same<Epi, EpiChebFirst>::value;
+  constexpr bool kDir = std::is_same<Epi, EpiStoreP>::value;
   const double* eout;
+  const double* eout2 = nullptr;
   const double* er = nullptr;
   const double* exo = nullptr;
-  if constexpr (kFirst) {
-    eout = epi.xout;
+  const double* ex;
+  const double* ep = nullptr;
+  bool ghosts;
+  if constexpr (kDir) {
+    eout = epi.q;
+    eout2 = epi.pout;
+    ex = in.z;
+    if (!in.first) ep = in.p;
+    ghosts = in.gz || in.gp || in.zlo || in.zhi;
   } else {
-    eout = epi.out;
-    er = epi.r;
-    if (!epi.xold_from_r) exo = epi.xold;
+    ex = in.x;
+    ghosts = in.gx != nullptr;
+    if constexpr (kFirst) {
+      eout = epi.xout;
+    } else {
+      eout = epi.out;
+      er = epi.r;
+      if (!epi.xold_from_r) exo = epi.xold;
+    }
   }
   const int nx = op->dia3_nx;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+  auto clash = [&](const double* o) { return o && (o == ex || o == ep || o == er); };
   if (!dia3_on(op) || op->dia3_pat != 27 || env_int("PCGX_DIA3T", 1) == 0 || nx % 4 != 0 || nx < kT3PX ||
-      in.gx || !al16(in.x) || (er && !al16(er)) || !al16(eout) || (exo && !al16(exo)) || eout == in.x ||
-      (er && eout == er))
+      ghosts || !al16(ex) || (ep && !al16(ep)) || (er && !al16(er)) || !al16(eout) || (eout2 && !al16(eout2)) ||
+      (exo && !al16(exo)) || clash(eout) || clash(eout2))
     return false;
+  if (kDir && env_int("PCGX_DIA3T_DIR", 1) == 0) return false;
+  if (kFirst && env_int("PCGX_DIA3T_FIRST", 1) == 0) return false;
   Dia3tMaps maps;
   maps.val = dia3t_map(op, op->dia_val, 3);
   maps.mask = dia3t_map(op, op->dia_mask, 2);
-  maps.r = er ? dia3t_map(op, er, 0) : maps.mask;  // unused for the first step
+  maps.r = er ? dia3t_map(op, er, 0) : maps.mask;  // unused for the first / direction step
   maps.xo = exo ? dia3t_map(op, exo, 0) : maps.r;
-  maps.x = dia3t_map(op, in.x, 1);
+  maps.x = dia3t_map(op, ex, 1);
   maps.d = dia3t_map(op, op->dvec, 1);
+  maps.p = ep ? dia3t_map(op, ep, 1) : maps.x;
   const int kz = std::max(1, env_int("PCGX_DIA3T_KZ", 32));  // 8: -3%, 16: -1.5% at 256^3
   const int tiles = ((nx + kD3X - 1) / kD3X) * ((nx + kD3Y - 1) / kD3Y);
   const dim3 grid(tiles, (nx + kz - 1) / kz);
   static bool attr = false;
   if (!attr) {
-    PCGX_CUDA(cudaFuncSetAttribute(dia3t_kernel<kRed, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDia3tSmem));
+    PCGX_CUDA(cudaFuncSetAttribute(dia3t_kernel<kRed, Epi, In>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kDia3tSmem));
     attr = true;
   }
   Reduce red = kRed ? make_red(c, slot) : Reduce{};
-  dia3t_kernel<kRed, Epi><<<grid, kD3Threads, kDia3tSmem, c->s>>>(maps, nx, kz, epi, red);
+  dia3t_kernel<kRed, Epi, In><<<grid, kD3Threads, kDia3tSmem, c->s>>>(maps, nx, kz, epi, red, in);
   check_launch();
   count_launch(c);
   return true;
@@ -1038,7 +1061,11 @@ bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiCh
 }
 template <bool kRed>
 bool dia3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebFirst& epi, int slot) {
-  return env_int("PCGX_DIA3T_FIRST", 1) != 0 && dia3t_launch_any<kRed>(c, op, in, epi, slot);
+  return dia3t_launch_any<kRed>(c, op, in, epi, slot);
+}
+template <bool kRed>
+bool dia3t_launch(pcgx_context c, pcgx_operator op, const InComb& in, const EpiStoreP& epi, int slot) {
+  return dia3t_launch_any<kRed>(c, op, in, epi, slot);
 }
 
 // bsr3t_kernel tensor maps (cached per buffer): kind 20 value array (4D), 21 masks,
