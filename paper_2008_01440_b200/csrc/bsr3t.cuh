@@ -34,8 +34,10 @@ constexpr int kB3OffO = kB3OffR + 3 * kB3Tile;
 constexpr int kB3OffX = kB3OffO + 3 * kB3Tile;
 constexpr int kB3PatchS = (kB3Patch + 15) / 16 * 16;
 constexpr int kB3OffD = kB3OffX + kB3PatchS;
-constexpr int kB3Aux = kB3OffD + kB3PatchS;
-static_assert(kB3OffX % 16 == 0 && kB3OffD % 16 == 0 && kB3Aux % 16 == 0, "128-byte TMA destinations");
+constexpr int kB3OffP = kB3OffD + kB3PatchS;  // direction step: p_old patch
+constexpr int kB3Aux = kB3OffP + kB3PatchS;
+static_assert(kB3OffX % 16 == 0 && kB3OffD % 16 == 0 && kB3OffP % 16 == 0 && kB3Aux % 16 == 0,
+              "128-byte TMA destinations");
 constexpr size_t kBsr3tSmem =
     sizeof(double) * ((size_t)kB3NV * kB3VBox + (size_t)kB3NA * kB3Aux + (size_t)kB3TR * kB3Patch) +
     8 * (kB3NV + kB3NA) + 128;
@@ -45,11 +47,18 @@ struct Bsr3tMaps {
   CUtensorMap mask;  // 3D (nx, nx, nx) u32, box (32, 4, 1)
   CUtensorMap r, xo; // 3D (3 nx, nx, nx) fp64, box (96, 4, 1)
   CUtensorMap x, d;  // 3D (3 nx, nx, nx) fp64, box (108, 6, 1)
+  CUtensorMap p;     // direction step: p_old patches
 };
 
-template <bool kRed>
+// Epi as in dia3t_kernel: EpiChebStep, EpiChebFirst, or EpiStoreP with In = InComb.
+template <bool kRed, class Epi, class In = InVec>
 __global__ void __launch_bounds__(kB3Threads, 1)
-bsr3t_kernel(const __grid_constant__ Bsr3tMaps maps, int nx, int kz, EpiChebStep epi, Reduce red) {
+bsr3t_kernel(const __grid_constant__ Bsr3tMaps maps, int nx, int kz, Epi epi, Reduce red, In in) {
+  constexpr bool kFirst = std::is_same<Epi, EpiChebFirst>::value;
+  constexpr bool kDir = std::is_same<Epi, EpiStoreP>::value;
+  in.init();
+  bool first_dir = false;
+  if constexpr (kDir) first_dir = in.first != 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sV = reinterpret_cast<double*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   double* sA = sV + kB3NV * kB3VBox;
@@ -63,9 +72,11 @@ bsr3t_kernel(const __grid_constant__ Bsr3tMaps maps, int nx, int kz, EpiChebStep
   const int i = i0 + tx, j = j0 + ty;
   const bool own = i < nx && j < nx;
   const long long nxy = (long long)nx * nx;
-  const bool need_xo = !epi.xold_from_r;
+  bool need_xo = false;
+  if constexpr (!kFirst && !kDir) need_xo = !epi.xold_from_r;
   const unsigned bytes_patch = kB3Patch * 8;
-  const unsigned bytes_aux = kB3Tile * 4 + 3 * kB3Tile * 8 * (need_xo ? 2 : 1);
+  const unsigned bytes_aux = kB3Tile * 4 + (kFirst || kDir ? 0u : 3 * kB3Tile * 8 * (need_xo ? 2 : 1));
+  const unsigned npatch = (kDir && !first_dir) ? 3u : 2u;
   const int u0 = kb - 2;  // first aux unit: patch of plane kb-1
   const int nvu = (ke - kb) * 9;
 
@@ -74,15 +85,16 @@ bsr3t_kernel(const __grid_constant__ Bsr3tMaps maps, int nx, int kz, EpiChebStep
     const int q = (u - u0) % kB3NA;
     double* s = sA + q * kB3Aux;
     const bool vals = u >= kb && u < ke, pat = u + 1 >= 0 && u + 1 < nx;
-    mbar_expect_tx(&barA[q], (vals ? bytes_aux : 0u) + (pat ? 2 * bytes_patch : 0u));
+    mbar_expect_tx(&barA[q], (vals ? bytes_aux : 0u) + (pat ? npatch * bytes_patch : 0u));
     if (vals) {
       tma_load_3d(s + kB3OffM, &maps.mask, i0, j0, u, &barA[q]);
-      tma_load_3d(s + kB3OffR, &maps.r, 3 * i0, j0, u, &barA[q]);
+      if (!kFirst && !kDir) tma_load_3d(s + kB3OffR, &maps.r, 3 * i0, j0, u, &barA[q]);
       if (need_xo) tma_load_3d(s + kB3OffO, &maps.xo, 3 * i0, j0, u, &barA[q]);
     }
     if (pat) {
       tma_load_3d(s + kB3OffX, &maps.x, 3 * (i0 - 2), j0 - 1, u + 1, &barA[q]);
       tma_load_3d(s + kB3OffD, &maps.d, 3 * (i0 - 2), j0 - 1, u + 1, &barA[q]);
+      if (kDir && !first_dir) tma_load_3d(s + kB3OffP, &maps.p, 3 * (i0 - 2), j0 - 1, u + 1, &barA[q]);
     }
   };
   // value unit v: plane kb + v / 9, slot group g = v % 9 (slots 3g .. 3g+2)
@@ -103,10 +115,17 @@ bsr3t_kernel(const __grid_constant__ Bsr3tMaps maps, int nx, int kz, EpiChebStep
     const double* s = sA + ((u - u0) % kB3NA) * kB3Aux;
     double* tp = tr + ((u + 1 + kB3TR) & 3) * kB3Patch;
     const bool pat = u + 1 >= 0 && u + 1 < nx;
-    for (int e = tid; e < kB3Patch; e += kB3Threads) tp[e] = pat ? s[kB3OffD + e] * s[kB3OffX + e] : 0.0;
+    if constexpr (kDir) {  // p = z + beta p_old, combined once per element (InComb::f)
+      for (int e = tid; e < kB3Patch; e += kB3Threads)
+        tp[e] = pat ? s[kB3OffD + e] * in.f(s[kB3OffX + e], first_dir ? 0.0 : s[kB3OffP + e]) : 0.0;
+    } else {
+      for (int e = tid; e < kB3Patch; e += kB3Threads) tp[e] = pat ? s[kB3OffD + e] * s[kB3OffX + e] : 0.0;
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      xo_[c] = pat ? s[kB3OffX + own_p + c] : 0.0;
+      double xv = pat ? s[kB3OffX + own_p + c] : 0.0;
+      if constexpr (kDir) xv = pat ? in.f(xv, first_dir ? 0.0 : s[kB3OffP + own_p + c]) : 0.0;
+      xo_[c] = xv;
       do_[c] = pat ? s[kB3OffD + own_p + c] : 0.0;
     }
   };
@@ -173,11 +192,21 @@ bsr3t_kernel(const __grid_constant__ Bsr3tMaps maps, int nx, int kz, EpiChebStep
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double y = sum[c] * dr[c];
-        const double ri = sa[kB3OffR + 3 * tid + c];
-        const double xo = need_xo ? sa[kB3OffO + 3 * tid + c] : 0.0;
-        const double xnew = epi.f(y, xr[c], ri, xo);
-        epi.out[row + c] = xnew;
-        if (kRed) acc = acc + ri * xnew;
+        if constexpr (kDir) {
+          epi.q[row + c] = y;
+          epi.pout[row + c] = xr[c];
+          if (kRed) acc = acc + xr[c] * y;
+        } else if constexpr (kFirst) {
+          const double xnew = epi.f(y, xr[c]);
+          epi.xout[row + c] = xnew;
+          if (kRed) acc = acc + xr[c] * xnew;
+        } else {
+          const double ri = sa[kB3OffR + 3 * tid + c];
+          const double xo = need_xo ? sa[kB3OffO + 3 * tid + c] : 0.0;
+          const double xnew = epi.f(y, xr[c], ri, xo);
+          epi.out[row + c] = xnew;
+          if (kRed) acc = acc + ri * xnew;
+        }
       }
     }
 #pragma unroll

@@ -669,6 +669,10 @@ template <bool kRed>
 bool dia3t_launch(pcgx_context c, pcgx_operator op, const InComb& in, const EpiStoreP& epi, int slot);
 template <bool kRed>
 bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot);
+template <bool kRed>
+bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebFirst& epi, int slot);
+template <bool kRed>
+bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InComb& in, const EpiStoreP& epi, int slot);
 
 // Whether the operator's kernels accept the fused direction-update input.
 bool fuses_dir_update(pcgx_operator op) {
@@ -734,7 +738,9 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
     return;
   }
   if (op->kind == 1 && op->bsr_ptr) {
-    if constexpr (std::is_same<In, InVec>::value && std::is_same<Epi, EpiChebStep>::value) {
+    if constexpr ((std::is_same<In, InVec>::value &&
+                   (std::is_same<Epi, EpiChebStep>::value || std::is_same<Epi, EpiChebFirst>::value)) ||
+                  (std::is_same<In, InComb>::value && std::is_same<Epi, EpiStoreP>::value)) {
       if (bsr3t_launch<kRed>(c, op, in, epi, slot)) return;
     }
     Bsr3Geom g{(int)(op->n_local / 3), 0, op->bsr_slices, op->bsr_ptr, op->bsr_len, op->bsr_col,
@@ -1105,33 +1111,71 @@ const CUtensorMap& bsr3t_map(pcgx_operator op, const void* ptr, int kind) {
   return op->gmaps.back().m;
 }
 
-template <bool kRed>
-bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot) {
+template <bool kRed, class Epi, class In>
+bool bsr3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi, int slot) {
+  constexpr bool kFirst = std::is_same<Epi, EpiChebFirst>::value;
+  constexpr bool kDir = std::is_same<Epi, EpiStoreP>::value;
+  const double *eout, *eout2 = nullptr, *er = nullptr, *exo = nullptr, *ex, *ep = nullptr;
+  bool ghosts;
+  if constexpr (kDir) {
+    eout = epi.q;
+    eout2 = epi.pout;
+    ex = in.z;
+    if (!in.first) ep = in.p;
+    ghosts = in.gz || in.gp || in.zlo || in.zhi;
+  } else {
+    ex = in.x;
+    ghosts = in.gx != nullptr;
+    if constexpr (kFirst) {
+      eout = epi.xout;
+    } else {
+      eout = epi.out;
+      er = epi.r;
+      if (!epi.xold_from_r) exo = epi.xold;
+    }
+  }
   const int nx = op->b3g_nx;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
-  if (!op->b3g_val || env_int("PCGX_BSR3T", 1) == 0 || in.gx || !al16(in.x) || !al16(epi.r) || !al16(epi.out) ||
-      (!epi.xold_from_r && !al16(epi.xold)) || epi.out == in.x || epi.out == epi.r)
+  auto clash = [&](const double* o) { return o && (o == ex || o == ep || o == er); };
+  if (!op->b3g_val || env_int("PCGX_BSR3T", 1) == 0 || ghosts || !al16(ex) || (ep && !al16(ep)) ||
+      (er && !al16(er)) || !al16(eout) || (eout2 && !al16(eout2)) || (exo && !al16(exo)) || clash(eout) ||
+      clash(eout2))
     return false;
+  if ((kDir || kFirst) && env_int("PCGX_BSR3T_MODES", 1) == 0) return false;
   Bsr3tMaps maps;
   maps.val = bsr3t_map(op, op->b3g_val, 20);
   maps.mask = bsr3t_map(op, op->b3g_mask, 21);
-  maps.r = bsr3t_map(op, epi.r, 22);
-  maps.xo = epi.xold_from_r ? maps.r : bsr3t_map(op, epi.xold, 22);
-  maps.x = bsr3t_map(op, in.x, 23);
+  maps.r = er ? bsr3t_map(op, er, 22) : maps.mask;  // unused for the first / direction step
+  maps.xo = exo ? bsr3t_map(op, exo, 22) : maps.r;
+  maps.x = bsr3t_map(op, ex, 23);
   maps.d = bsr3t_map(op, op->dvec, 23);
+  maps.p = ep ? bsr3t_map(op, ep, 23) : maps.x;
   const int kz = std::max(1, env_int("PCGX_BSR3T_KZ", 32));
   const int tiles = ((nx + kB3X - 1) / kB3X) * ((nx + kB3Y - 1) / kB3Y);
   const dim3 grid(tiles, (nx + kz - 1) / kz);
   static bool attr = false;
   if (!attr) {
-    PCGX_CUDA(cudaFuncSetAttribute(bsr3t_kernel<kRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsr3tSmem));
+    PCGX_CUDA(cudaFuncSetAttribute(bsr3t_kernel<kRed, Epi, In>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kBsr3tSmem));
     attr = true;
   }
   Reduce red = kRed ? make_red(c, slot) : Reduce{};
-  bsr3t_kernel<kRed><<<grid, kB3Threads, kBsr3tSmem, c->s>>>(maps, nx, kz, epi, red);
+  bsr3t_kernel<kRed, Epi, In><<<grid, kB3Threads, kBsr3tSmem, c->s>>>(maps, nx, kz, epi, red, in);
   check_launch();
   count_launch(c);
   return true;
+}
+template <bool kRed>
+bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebStep& epi, int slot) {
+  return bsr3t_launch_any<kRed>(c, op, in, epi, slot);
+}
+template <bool kRed>
+bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InVec& in, const EpiChebFirst& epi, int slot) {
+  return bsr3t_launch_any<kRed>(c, op, in, epi, slot);
+}
+template <bool kRed>
+bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InComb& in, const EpiStoreP& epi, int slot) {
+  return bsr3t_launch_any<kRed>(c, op, in, epi, slot);
 }
 
 
