@@ -6,8 +6,8 @@ mkdir -p gpurun_out
 for cfg in "$@"; do
   case $cfg in
     cfg1) kern=dia_kernel; skip=40 ;;
-    cfg3) kern=dia3t_kernel; skip=40 ;;
-    cfg4) kern=bsr3t_kernel; skip=40 ;;
+    cfg3) kern="dia3t_kernel<\\(bool\\)0, pcgx::EpiChebStep"; skip=40 ;;
+    cfg4) kern="bsr3t_kernel<\\(bool\\)0, pcgx::EpiChebStep"; skip=40 ;;
     *) kern="cheb2f_kernel<\\(bool\\)0, \\(bool\\)0, \\(bool\\)0, \\(bool\\)0>"; skip=100 ;;
   esac
   extra=""
