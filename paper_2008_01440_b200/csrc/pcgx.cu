@@ -1049,11 +1049,12 @@ bool dia3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
   const int kz = std::max(1, env_int("PCGX_DIA3T_KZ", 32));  // 8: -3%, 16: -1.5% at 256^3
   const int tiles = ((nx + kD3X - 1) / kD3X) * ((nx + kD3Y - 1) / kD3Y);
   const dim3 grid(tiles, (nx + kz - 1) / kz);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};  // per device: the attribute is set per device
+  const uint64_t bit = 1ull << (c->device & 63);
+  if (!(attr.load() & bit)) {
     PCGX_CUDA(cudaFuncSetAttribute(dia3t_kernel<kRed, Epi, In>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)kDia3tSmem));
-    attr = true;
+    attr.fetch_or(bit);
   }
   Reduce red = kRed ? make_red(c, slot) : Reduce{};
   dia3t_kernel<kRed, Epi, In><<<grid, kD3Threads, kDia3tSmem, c->s>>>(maps, nx, kz, epi, red, in);
@@ -1153,11 +1154,12 @@ bool bsr3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
   const int kz = std::max(1, env_int("PCGX_BSR3T_KZ", 32));
   const int tiles = ((nx + kB3X - 1) / kB3X) * ((nx + kB3Y - 1) / kB3Y);
   const dim3 grid(tiles, (nx + kz - 1) / kz);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};  // per device: the attribute is set per device
+  const uint64_t bit = 1ull << (c->device & 63);
+  if (!(attr.load() & bit)) {
     PCGX_CUDA(cudaFuncSetAttribute(bsr3t_kernel<kRed, Epi, In>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)kBsr3tSmem));
-    attr = true;
+    attr.fetch_or(bit);
   }
   Reduce red = kRed ? make_red(c, slot) : Reduce{};
   bsr3t_kernel<kRed, Epi, In><<<grid, kB3Threads, kBsr3tSmem, c->s>>>(maps, nx, kz, epi, red, in);
