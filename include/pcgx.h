@@ -252,6 +252,7 @@ typedef struct {
   double step_ms;            /* total device ms of timed Chebyshev-step launches */
   int64_t step_launches;     /* number of timed Chebyshev-step launches */
   double step_bytes;         /* algorithmic bytes per Chebyshev-step launch */
+  int64_t step_steps;        /* Chebyshev degree steps per timed launch (1, 2 or 3) */
 } pcgx_report;
 
 void pcgx_solve_opts_default(pcgx_solve_opts* o);

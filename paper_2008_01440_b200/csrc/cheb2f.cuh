@@ -325,7 +325,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       }
       const bool live = plane_in && do1;
       if (live) cv = c;
-      if (live && interior && t >= kb && t < ke) st2(gCt, cv.x, cv.y);
+      if (p.outC && live && interior && t >= kb && t < ke) st2(gCt, cv.x, cv.y);  // outC null: last pass
       if (kT) ct = mul2(cv);
       *reinterpret_cast<double2*>(pCu + offB) = kT ? ct : cv;
       // i-halo columns of C[t] (read by stage 2 of plane t, two iterations on)

@@ -63,6 +63,7 @@ enum Slot : int {
   S_EE = 7,                     // true residual e'e
   S_DOT = 8, S_DOT2 = 9,        // scratch reductions (Lanczos, tests)
   S_E0 = 10, S_E1 = 11, S_E2 = 12,  // eigen-estimator reductions (2-3 values at once)
+  S_BNORM = 13, S_TOL = 14,     // ||b|| and tol of the running solve (device convergence test)
   kSlots = 16
 };
 __host__ __device__ inline int slot_pq(int par) { return par ? S_PQ1 : S_PQ0; }

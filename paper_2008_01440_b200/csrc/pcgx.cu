@@ -31,6 +31,7 @@
 
 #include "cheb2.cuh"
 #include "cheb2f.cuh"
+#include "cheb3.cuh"
 #include "common.cuh"
 #include "bsr3t.cuh"
 #include "dia3t.cuh"
@@ -49,6 +50,7 @@ struct Graph {
   cudaGraphExec_t exec = nullptr;
   int64_t kernels = 0;
   int64_t allreduces = 0;
+  int64_t body_kernels = 0;  // kernels inside the conditional (IF) node, if any
   ~Graph() {
     if (exec) cudaGraphExecDestroy(exec);
   }
@@ -94,6 +96,12 @@ struct pcgx_context_s {
   int64_t cur_allreduce = 0;
   int64_t cur_halo_bytes = 0;
   bool capturing = false;
+  // conditional-graph capture (device-side convergence): the root graph, its IF
+  // handle, and the launch count when the IF body's capture began
+  cudaGraph_t cond_root = nullptr;
+  cudaGraphConditionalHandle cond_h = 0;
+  bool cond_split = false;
+  int64_t cond_mark = 0;
 };
 
 struct pcgx_operator_s {
@@ -114,6 +122,8 @@ struct pcgx_operator_s {
   std::string c2plan;                     // PCGX_C2PLAN: "" auto, "u" uniform kz2, "h1,h2,..." explicit
   std::map<int, ChunkPlan> c2plans;       // chunk plan per launch span (planes)
   std::map<int, ChunkPlan> dirplans;      // the same for the direction step
+  bool cheb3 = false;                     // three Chebyshev steps per pass (stencil7_cheb3_kernel)
+  std::map<int, ChunkPlan> c3plans;       // chunk plans of the three-step pass
   int zpad = 0;       // ghost planes per side in the workspace vectors (z-slab + cheb2: 2)
   int kz2 = 32;       // z-chunk of the two-step kernel
   struct TmaPair { const double* ptr; CUtensorMap a, e, fa, fe; };
@@ -253,6 +263,15 @@ pcgx_status guarded(pcgx_context ctx, F&& f) {
 }
 
 void set_device(pcgx_context c) { PCGX_CUDA(cudaSetDevice(c->device)); }
+
+// A reducing launch writes one partial per block (two for block_reduce_finish2)
+// into c->partials (kMaxBlocks doubles): fail loudly instead of writing past it.
+void check_red_grid(unsigned long long nblocks, int per_block = 1) {
+  if (nblocks * (unsigned long long)per_block > (unsigned long long)kMaxBlocks)
+    fail(PCGX_ERR_UNSUPPORTED, "reduction over " + std::to_string(nblocks) +
+                                   " blocks exceeds the partials buffer (" + std::to_string(kMaxBlocks) + ")");
+}
+unsigned long long nblocks_of(const dim3& g) { return (unsigned long long)g.x * g.y * g.z; }
 
 Reduce make_red(pcgx_context c, int slot, bool accumulate = false) {
   Reduce r;
@@ -591,11 +610,16 @@ template <class In, class Epi, bool kRed>
 void stencil_launch(pcgx_context c, pcgx_operator op, const StencilGeom& g, const In& in,
                     const Epi& epi, int k_begin, int k_end, int slot, bool accumulate) {
   if (k_end <= k_begin) return;
-  const int kz = std::max(1, std::min(op->kz, k_end - k_begin));
+  const unsigned gy = (unsigned)((g.ny + kStencilBY - 1) / kStencilBY);
+  const unsigned gx = (unsigned)(op->vec2 ? (g.nx + 63) / 64 : (g.nx + kStencilBX - 1) / kStencilBX);
+  // planes per block: op->kz, raised so a reducing grid fits the partials buffer
+  const long long span = k_end - k_begin;
+  const long long kz_min = kRed ? (span * gx * gy + kMaxBlocks - 1) / kMaxBlocks : 1;
+  const int kz = (int)std::max(1LL, std::min((long long)span, std::max((long long)op->kz, kz_min)));
   dim3 block(kStencilBX, kStencilBY, 1);
   Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
-  const unsigned gy = (unsigned)((g.ny + kStencilBY - 1) / kStencilBY);
-  const unsigned gz = (unsigned)((k_end - k_begin + kz - 1) / kz);
+  const unsigned gz = (unsigned)((span + kz - 1) / kz);
+  if (kRed) check_red_grid((unsigned long long)gx * gy * gz);
   if (op->vec2) {  // even nx: two points per lane, 16-byte loads
     dim3 grid((unsigned)((g.nx + 63) / 64), gy, gz);
     stencil7v2_kernel<In, Epi, kRed><<<grid, block, 0, c->s>>>(g, in, epi, k_begin, k_end, kz, red,
@@ -710,6 +734,7 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
       g3.kz = std::max(env_int("PCGX_DIA3_KZ", 0) > 0 ? env_int("PCGX_DIA3_KZ", 0) : (g3.nx + want - 1) / want,
                        std::min(8, g3.nx));
       const dim3 grid3(tiles, (g3.nx + g3.kz - 1) / g3.kz);
+      if (kRed) check_red_grid(nblocks_of(grid3));
       Reduce red = kRed ? make_red(c, slot) : Reduce{};
       if (op->dia3_pat == 27) {
         auto k3 = stream ? dia3_kernel<27, In, Epi, kRed, true> : dia3_kernel<27, In, Epi, kRed, false>;
@@ -723,10 +748,14 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
       return;
     }
     auto kern = stream ? dia_kernel<In, Epi, kRed, true> : dia_kernel<In, Epi, kRed, false>;
-    static int occ = 0;
+    // occupancy of this instantiation, queried once (atomic: local-group ranks drive
+    // the library from several host threads)
+    static std::atomic<int> occ_cache{0};
+    int occ = occ_cache.load(std::memory_order_relaxed);
     if (!occ) {
       PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dia_kernel<In, Epi, kRed, true>, 256, 0));
       occ = std::max(occ, 1);
+      occ_cache.store(occ, std::memory_order_relaxed);
     }
     const long long want = (op->n_local + 255) / 256;
     const int bps = env_int("PCGX_DIA_BPS", 0);
@@ -1056,6 +1085,7 @@ bool dia3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
                                    (int)kDia3tSmem));
     attr.fetch_or(bit);
   }
+  if (kRed) check_red_grid(nblocks_of(grid));
   Reduce red = kRed ? make_red(c, slot) : Reduce{};
   dia3t_kernel<kRed, Epi, In><<<grid, kD3Threads, kDia3tSmem, c->s>>>(maps, nx, kz, epi, red, in);
   check_launch();
@@ -1161,6 +1191,7 @@ bool bsr3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
                                    (int)kBsr3tSmem));
     attr.fetch_or(bit);
   }
+  if (kRed) check_red_grid(nblocks_of(grid));
   Reduce red = kRed ? make_red(c, slot) : Reduce{};
   bsr3t_kernel<kRed, Epi, In><<<grid, kB3Threads, kBsr3tSmem, c->s>>>(maps, nx, kz, epi, red, in);
   check_launch();
@@ -1188,7 +1219,8 @@ bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InComb& in, const EpiS
 // so the final wave ends evenly -- chosen by simulating the greedy dispatch (a
 // chunk of h planes costs h + 2.5 plane-times: two halo planes plus the ring
 // ramp). spec "u": uniform kz; "h1,h2,...": explicit heights summing to span.
-ChunkPlan make_chunk_plan(const std::string& spec, int span, int kz, long long tiles, long long slots) {
+ChunkPlan make_chunk_plan(const std::string& spec, int span, int kz, long long tiles, long long slots,
+                          double ovh = 2.5) {
   auto pack = [&](const std::vector<int>& hs) {
     ChunkPlan p{};
     p.n = 0;
@@ -1225,7 +1257,7 @@ ChunkPlan make_chunk_plan(const std::string& spec, int span, int kz, long long t
       double end = 0.0;
       for (int c : h)
         for (long long t = 0; t < tiles; ++t) {
-          const double f = q.top() + c + 2.5;
+          const double f = q.top() + c + ovh;
           q.pop();
           q.push(f);
           end = std::max(end, f);
@@ -1257,6 +1289,11 @@ ChunkPlan make_chunk_plan(const std::string& spec, int span, int kz, long long t
           }
     if (hs.empty()) hs = uniform((span + ChunkPlan::kMax - 1) / ChunkPlan::kMax);
   }
+  // a reducing launch of `tiles` x chunks blocks must fit the partials buffer
+  if ((long long)hs.size() * tiles > kMaxBlocks && tiles <= kMaxBlocks) {
+    const long long maxn = std::max(1LL, (long long)kMaxBlocks / tiles);
+    hs = uniform((int)((span + maxn - 1) / maxn));
+  }
   if (env_int("PCGX_C2PLAN_DEBUG", 0)) {
     std::fprintf(stderr, "[pcgx] two-step chunk plan span=%d tiles=%lld slots=%lld:", span, tiles, slots);
     for (int h : hs) std::fprintf(stderr, " %d", h);
@@ -1279,6 +1316,7 @@ void cheb2_launch_v(pcgx_context c, pcgx_operator op, const double* A, const dou
   kz = std::max(1, std::min(kz, k_end - k_begin));
   dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
             (unsigned)((k_end - k_begin + kz - 1) / kz));
+  if (kRed) check_red_grid(nblocks_of(grid));
   Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
   stencil7_cheb2_kernel<kFirst, kRed, kV><<<grid, kC2Threads, kC2Smem, c->s>>>(ma, mb, mr, prm, k_begin,
                                                                                k_end, kz, red);
@@ -1308,6 +1346,7 @@ void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const doubl
                                                      (long long)std::max(occ, 1) * c->sms)).first;
     }
     const ChunkPlan& plan = it->second;
+    if (kRed) check_red_grid((unsigned long long)tiles * plan.n);
     Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
     kern<<<dim3((unsigned)tiles, (unsigned)plan.n), kFThreads, kC2FSmem, c->s>>>(ma, mb, mr, prm, k_begin,
                                                                                   k_end, plan, red, Reduce{});
@@ -1357,6 +1396,7 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
       it = op->dirplans.emplace(span, make_chunk_plan(op->c2plan, span, kz, tiles,
                                                       (long long)std::max(occ, 1) * c->sms)).first;
     }
+    check_red_grid((unsigned long long)tiles * it->second.n);
     stencil7_dir_kernel<<<dim3((unsigned)tiles, (unsigned)it->second.n), kDirThreads, kDirSmem, c->s>>>(
         mz, mp, mx, prm, k_begin, k_end, it->second, make_red(c, slot, accumulate));
     check_launch();
@@ -1475,8 +1515,61 @@ void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Pa
     it = op->c2plans.emplace(nzl, make_chunk_plan(op->c2plan, nzl, op->kz2, tiles,
                                                   (long long)std::max(occ, 1) * c->sms)).first;
   }
+  check_red_grid((unsigned long long)tiles * it->second.n);
   kern<<<dim3((unsigned)tiles, (unsigned)it->second.n), kFThreads, kC2FSmem, c->s>>>(
       ma, mq, ma, prm, 0, nzl, it->second, Reduce{}, make_red(c, u.s_rr));
+  check_launch();
+  count_launch(c);
+}
+
+// Tensor maps of the three-step pass, cached per buffer: kind 20 the A box
+// (72 x (k3TY+6)), kind 21 the B / R boxes (68 x (k3TY+4)).
+CUtensorMap cheb3_map(pcgx_operator op, const double* ptr, int kind) {
+  for (auto& g : op->gmaps)
+    if (g.ptr == ptr && g.kind == kind) return g.m;
+  const CUtensorMap m = kind == 20 ? make_map(op, ptr, k3AW, k3AR) : make_map(op, ptr, k3W, k3R);
+  op->gmaps.push_back({ptr, kind, m});
+  return m;
+}
+
+bool cheb3_ok(pcgx_context c, pcgx_operator op) {
+  return op->kind == 0 && op->cheb3 && op->zpad == 0 && c->nranks == 1;
+}
+
+// One three-step pass (stencil7_cheb3_kernel) over the slab: reads A = x_{k-1},
+// B = x_{k-2}, R = r; writes x_{k+1} (prm.outE, unless nullptr) and x_{k+2} (prm.outF).
+template <bool kRed>
+void cheb3_pass(pcgx_context c, pcgx_operator op, const double* A, const double* B, const double* R,
+                Cheb3Params prm, int slot) {
+  op->matvecs.fetch_add(3, std::memory_order_relaxed);
+  const int nzl = (int)op->nzl;
+  prm.nx = (int)op->nx;
+  prm.ny = (int)op->ny;
+  prm.nzl = nzl;
+  prm.nxy = op->nx * op->ny;
+  prm.d = op->d;
+  prm.zoff = 0;
+  prm.a_lo = 0;
+  prm.a_hi = nzl;
+  prm.c_lo = 0;
+  prm.c_hi = nzl;
+  auto kern = stencil7_cheb3_kernel<kRed>;
+  PCGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3Smem));
+  const CUtensorMap ma = cheb3_map(op, A, 20);
+  const CUtensorMap mb = cheb3_map(op, B, 21);
+  const CUtensorMap mr = cheb3_map(op, R, 21);
+  const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + k3TY - 1) / k3TY);
+  auto it = op->c3plans.find(nzl);
+  if (it == op->c3plans.end()) {
+    int occ = 0;
+    PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, k3Threads, k3Smem));
+    it = op->c3plans.emplace(nzl, make_chunk_plan(op->c2plan, nzl, op->kz2, tiles,
+                                                  (long long)std::max(occ, 1) * c->sms, 4.5)).first;
+  }
+  if (kRed) check_red_grid((unsigned long long)tiles * it->second.n);
+  Reduce red = kRed ? make_red(c, slot, false) : Reduce{};
+  kern<<<dim3((unsigned)tiles, (unsigned)it->second.n), k3Threads, k3Smem, c->s>>>(ma, mb, mr, prm, 0, nzl,
+                                                                                   it->second, red);
   check_launch();
   count_launch(c);
 }
@@ -1536,7 +1629,7 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
     const bool last12 = (P.m == 2);
     q.rk2 = P.rho[2];
     q.rk2m1 = P.rho[1];
-    q.outC = bufs[0];
+    q.outC = (last12 && op->cheb2v >= 3) ? nullptr : bufs[0];  // x_1 is dead after a last pass
     q.outE = last12 ? out : bufs[1];
     if (upd) cheb2f_upd_launch(c, op, *upd, q);
     else if (last12 && rz_slot >= 0) cheb2_pass<true, true>(c, op, r, nullptr, r, q, rz_slot);
@@ -1544,17 +1637,68 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
     if (after_first) after_first();
     if (last12) return;
     int iold = 0, icur = 1;  // x_{k-2}, x_{k-1} buffer indices
+    auto free_pair = [&](int& fa, int& fb) {
+      fa = fb = -1;
+      for (int b = 0; b < 4; ++b)
+        if (b != iold && b != icur) (fa < 0 ? fa : fb) = b;
+    };
     int k = 3;
+    if (cheb3_ok(c, op)) {
+      // three steps per pass (cheb3.cuh); the m - 2 remaining steps split into
+      // three-step passes and at most two two-step passes (never a single step
+      // unless m == 3)
+      const int rest = P.m - 2;
+      int n3 = rest / 3, n2 = 0;
+      if (rest % 3 == 2) n2 = 1;
+      if (rest % 3 == 1 && n3 >= 1) {
+        n3 -= 1;
+        n2 = 2;
+      }
+      for (int pass = 0; pass < n3; ++pass, k += 3) {
+        const bool last = (k + 2 == P.m);
+        int fe, ff;
+        free_pair(fe, ff);
+        Cheb3Params q3{};
+        q3.c2 = c2;
+        q3.c3 = c3;
+        q3.rk1 = P.rho[k];
+        q3.rk1m1 = P.rho[k - 1];
+        q3.rk2 = P.rho[k + 1];
+        q3.rk2m1 = P.rho[k];
+        q3.rk3 = P.rho[k + 2];
+        q3.rk3m1 = P.rho[k + 1];
+        q3.outE = last ? nullptr : bufs[fe];
+        q3.outF = last ? out : bufs[ff];
+        if (last && rz_slot >= 0) cheb3_pass<true>(c, op, bufs[icur], bufs[iold], r, q3, rz_slot);
+        else cheb3_pass<false>(c, op, bufs[icur], bufs[iold], r, q3, -1);
+        iold = fe;
+        icur = ff;
+      }
+      for (int pass = 0; pass < n2; ++pass, k += 2) {
+        const bool last = (k + 1 == P.m);
+        int fc, fe;
+        free_pair(fc, fe);
+        q.rk1 = P.rho[k];
+        q.rk1m1 = P.rho[k - 1];
+        q.rk2 = P.rho[k + 1];
+        q.rk2m1 = P.rho[k];
+        q.outC = last ? nullptr : bufs[fc];
+        q.outE = last ? out : bufs[fe];
+        if (last && rz_slot >= 0) cheb2_pass<false, true>(c, op, bufs[icur], bufs[iold], r, q, rz_slot);
+        else cheb2_pass<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1);
+        iold = fc;
+        icur = fe;
+      }
+    }
     for (; k + 1 <= P.m; k += 2) {
       const bool last = (k + 1 == P.m);
-      int fc = -1, fe = -1;
-      for (int b = 0; b < 4; ++b)
-        if (b != iold && b != icur) (fc < 0 ? fc : fe) = b;
+      int fc, fe;
+      free_pair(fc, fe);
       q.rk1 = P.rho[k];
       q.rk1m1 = P.rho[k - 1];
       q.rk2 = P.rho[k + 1];
       q.rk2m1 = P.rho[k];
-      q.outC = bufs[fc];
+      q.outC = last && op->cheb2v >= 3 ? nullptr : bufs[fc];
       q.outE = last ? out : bufs[fe];
       if (last && rz_slot >= 0) cheb2_pass<false, true>(c, op, bufs[icur], bufs[iold], r, q, rz_slot);
       else cheb2_pass<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1);
@@ -1780,6 +1924,87 @@ void capture(pcgx_context c, Graph& g, F&& body) {
   c->cur_allreduce = before_ar;
 }
 
+// Capture of a PCG segment whose tail runs only while the solve has not
+// converged: body() enqueues the head, calls cond_split(c) once (after the kernel
+// that writes the convergence flag), then the tail. The head is captured into the
+// root graph, the tail into the body graph of an IF node that follows it, so at
+// convergence the device skips the tail (the speculative P r and A p of the
+// reference's stopping iteration, pcg.cpp:89-95) instead of computing and
+// discarding it.
+template <class F>
+void capture_cond(pcgx_context c, Graph& g, F&& body) {
+  const int64_t before = c->cur_launches;
+  const int64_t before_ar = c->cur_allreduce;
+  cudaGraph_t root = nullptr;
+  PCGX_CUDA(cudaGraphCreate(&root, 0));
+  c->cond_root = root;
+  c->cond_split = false;
+  c->cond_mark = 0;
+  try {
+    PCGX_CUDA(cudaGraphConditionalHandleCreate(&c->cond_h, root, 1u, cudaGraphCondAssignDefault));
+    PCGX_CUDA(cudaStreamBeginCaptureToGraph(c->s, root, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
+    body();
+    c->capturing = false;
+    cudaGraph_t tmp = nullptr;
+    PCGX_CUDA(cudaStreamEndCapture(c->s, &tmp));
+    if (!c->cond_split) fail(PCGX_ERR_CUDA, "capture_cond: the segment never split");
+    PCGX_CUDA(cudaGraphInstantiate(&g.exec, root, 0));
+  } catch (...) {
+    c->capturing = false;
+    cudaStreamCaptureStatus st;
+    if (cudaStreamIsCapturing(c->s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+      cudaGraph_t tmp = nullptr;
+      cudaStreamEndCapture(c->s, &tmp);
+    }
+    cudaGetLastError();
+    cudaGraphDestroy(root);
+    c->cond_root = nullptr;
+    throw;
+  }
+  cudaGraphDestroy(root);
+  c->cond_root = nullptr;
+  g.kernels = c->cur_launches - before;
+  g.body_kernels = c->cur_launches - c->cond_mark;
+  c->cur_launches = before;
+  c->launches -= g.kernels;
+  g.allreduces = c->cur_allreduce - before_ar;
+  c->cur_allreduce = before_ar;
+}
+
+__global__ void cond_kernel(cudaGraphConditionalHandle h, const double* S, int slot_rr, int slot_bnorm,
+                            int slot_tol) {
+  // the host's test, same operations: rel_res = sqrt(r'r) / ||b||; stop iff <= tol
+  const double rel = sqrt(S[slot_rr]) / S[slot_bnorm];
+  cudaGraphSetConditional(h, rel <= S[slot_tol] ? 0u : 1u);
+}
+
+// Inside capture_cond's body: the convergence flag from S[slot_rr], then the IF
+// node; everything enqueued after this runs only if the solve goes on.
+void cond_split(pcgx_context c, int slot_rr) {
+  cond_kernel<<<1, 1, 0, c->s>>>(c->cond_h, c->S, slot_rr, S_BNORM, S_TOL);
+  check_launch();
+  count_launch(c);
+  cudaStreamCaptureStatus st;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  PCGX_CUDA(cudaStreamGetCaptureInfo(c->s, &st, nullptr, nullptr, &deps, &nd));
+  std::vector<cudaGraphNode_t> dv(deps, deps + nd);
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = c->cond_h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  PCGX_CUDA(cudaGraphAddNode(&node, c->cond_root, dv.data(), dv.size(), &cp));
+  cudaGraph_t tmp = nullptr;
+  PCGX_CUDA(cudaStreamEndCapture(c->s, &tmp));
+  PCGX_CUDA(cudaStreamBeginCaptureToGraph(c->s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+  c->cond_split = true;
+  c->cond_mark = c->cur_launches;
+}
+
 void replay(pcgx_context c, Graph& g) {
   PCGX_CUDA(cudaGraphLaunch(g.exec, c->s));
   c->cur_launches += g.kernels;
@@ -1839,6 +2064,10 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // the speculative P r; multi-GPU: merge [r'r, r'z] into one all-reduce after P r
   // (PCGX_MERGED=1 forces the multi-GPU schedule on one GPU, for tests)
   const bool spec_after_update = !c->cm && env_int("PCGX_MERGED", 0) == 0;
+  // one GPU with graphs: the speculative tail of each segment (P r and A p of the
+  // next iteration) sits in a conditional IF node that a device-side convergence
+  // test closes, so nothing is computed and discarded at convergence
+  const bool use_cond = use_graph && spec_after_update && env_int("PCGX_COND_GRAPH", 1) != 0;
 
   std::memset(rep, 0, sizeof *rep);
   c->cur_launches = 0;
@@ -1881,6 +2110,11 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   alg += N8;
   const double bnorm = std::sqrt(c->hS[S_BB]);
   rep->ddot++;
+  if (use_cond) {  // ||b|| and tol for the device convergence test (cond_kernel)
+    const double bt[2] = {bnorm, opts.tol};
+    static_assert(S_TOL == S_BNORM + 1, "adjacent slots");
+    PCGX_CUDA(cudaMemcpyAsync(c->S + S_BNORM, bt, sizeof bt, cudaMemcpyHostToDevice, c->s));
+  }
   if (bnorm == 0.0) {
     launch_fill(c, n, x, 0.0);
     rep->converged = 1;
@@ -1973,9 +2207,16 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     const int par = it & 1;
     if (fuse_upd) {
       // r(it) = r(it-1) - alpha(it) q(it) inside P r(it)'s first pass; the scalar
-      // snapshot (r'r(it), p'q(it)) is taken right after that pass
+      // snapshot (r'r(it), p'q(it)) is taken right after that pass (and, with the
+      // conditional graph, the convergence test: the rest runs only if not converged)
       const CgUpd u{Rb[par ^ 1], q, Rb[par], slot_rz(par ^ 1), slot_pq(par), slot_rr(par)};
-      enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u, [&] { snapshot(); });
+      enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u, [&] {
+        snapshot();
+        if (use_cond) cond_split(c, slot_rr(par));
+      });
+    } else if (use_cond) {
+      cond_split(c, slot_rr(par));  // r'r(it) came from the update kernel before this segment
+      if (zm == 0) enqueue_prec(c, op, prec, r, z, slot_rz(par));
     } else if (zm == 0) {
       enqueue_prec(c, op, prec, r, z, slot_rz(par));
       if (!spec_after_update) {
@@ -1997,8 +2238,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     auto add = [&](const void* v, size_t bytes) { key.append((const char*)v, bytes); };
     const uint64_t ids[3] = {op->uid, c->ws_gen, defer_x ? (uint64_t)(uintptr_t)x : 0};
     add(ids, sizeof ids);
-    const int flags[7] = {prec.kind, m,        zm, fuse ? 1 : 0, spec_after_update ? 1 : 0, fuse_upd ? 1 : 0,
-                          snap_copy ? 1 : 0};
+    const int flags[8] = {prec.kind, m,        zm, fuse ? 1 : 0, spec_after_update ? 1 : 0, fuse_upd ? 1 : 0,
+                          snap_copy ? 1 : 0, use_cond ? 1 : 0};
     add(flags, sizeof flags);
     if (prec.kind == 1) {
       const double t[3] = {P.theta, P.delta, P.sigma};
@@ -2013,7 +2254,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
       if (hit == c->gcache.end()) {
         if (c->gcache.size() >= 64) c->gcache.clear();
         auto g = std::make_unique<Graph>();
-        capture(c, *g, [&] { enqueue_B(par ? 1 : 2); });
+        if (use_cond) capture_cond(c, *g, [&] { enqueue_B(par ? 1 : 2); });
+        else capture(c, *g, [&] { enqueue_B(par ? 1 : 2); });
         hit = c->gcache.emplace(k, std::move(g)).first;
       }
       gB[par] = hit->second.get();
@@ -2096,7 +2338,18 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     }
     if (rep->rel_res <= opts.tol) {
       rep->converged = 1;
-      if (more) rep->wasted_matvec = (zm == 0 ? m : 0) + 1;  // speculative P r and A p
+      if (more && use_cond) {
+        // the device skipped the segment's tail (IF node): only a fused first pass
+        // of P r ran; the direction step that would apply x += alpha p did not
+        rep->wasted_matvec = fuse_upd ? 2 : 0;
+        c->cur_launches -= gB[par]->body_kernels;
+        c->launches -= gB[par]->body_kernels;
+        alg -= bytes_B - (fuse_upd ? 5 * N8 : 0.0);
+        x_pending = defer_x;
+        x_par = par;
+      } else if (more) {
+        rep->wasted_matvec = (zm == 0 ? m : 0) + 1;  // speculative P r and A p
+      }
       break;
     }
     if (!more) break;
@@ -2155,8 +2408,21 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     }
     EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0,
                   1.0 / P.theta};
+    const bool three = two && cheb3_ok(c, op) && m >= 5;
+    Cheb3Params q3{};
+    q3.c2 = 2.0 / P.delta;
+    q3.c3 = 2.0 * P.sigma;
+    q3.rk1 = P.rho[3];
+    q3.rk1m1 = P.rho[2];
+    q3.rk2 = P.rho[4];
+    q3.rk2m1 = P.rho[3];
+    q3.rk3 = P.rho[5];
+    q3.rk3m1 = P.rho[4];
+    q3.outE = c->w2;
+    q3.outF = c->w3;
     auto launch = [&] {
-      if (two) cheb2_pass<false, false>(c, op, c->w1, c->w0, r, q, -1);
+      if (three) cheb3_pass<false>(c, op, c->w1, c->w0, r, q3, -1);
+      else if (two) cheb2_pass<false, false>(c, op, c->w1, c->w0, r, q, -1);
       else op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);
     };
     const uint64_t mv0 = op->matvecs.load();
@@ -2171,6 +2437,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     rep->step_ms = ms;
     rep->step_launches = reps;
     rep->step_bytes = two ? 40.0 * (double)op->n_local : cheb_step_bytes(op);
+    rep->step_steps = three ? 3 : (two ? 2 : 1);
   }
 }
 
@@ -3011,6 +3278,7 @@ void stencil_setup(pcgx_context c, pcgx_operator op, int64_t nx, int64_t ny, int
       init_stencil_ghosts(c, op);
       if (c->nranks > 1 && op->nzl < 2) op->cheb2 = false;  // 2-plane halos need >= 2 planes
       op->zpad = (op->cheb2 && c->nranks > 1) ? 2 : 0;
+      op->cheb3 = op->cheb2 && op->cheb2v >= 3 && c->nranks == 1 && env_int("PCGX_CHEB3", 1) != 0;
     } catch (...) {
       free_op(op);
       throw;
@@ -3132,6 +3400,32 @@ pcgx_status pcgx_context_create_dist(int device, int nranks, int rank, const voi
 pcgx_status pcgx_local_group_create(int nranks, const int* devices, pcgx_context* out) {
   return guarded(nullptr, [&] {
     if (nranks < 1 || !out) fail(PCGX_ERR_INVALID, "local_group_create: bad nranks");
+    int ndev = 0;
+    PCGX_CUDA(cudaGetDeviceCount(&ndev));
+    if (devices)
+      for (int r = 0; r < nranks; ++r)
+        if (devices[r] < 0 || devices[r] >= ndev)
+          fail(PCGX_ERR_INVALID, "local_group_create: device " + std::to_string(devices[r]) + " of rank " +
+                                     std::to_string(r) + " does not exist (" + std::to_string(ndev) +
+                                     " devices)");
+    // the group's scalar contributions live on rank 0's device and every rank's
+    // group_sum_kernel reads them: ranks on other devices need peer access to it
+    // (and halo copies between devices use it too)
+    if (devices)
+      for (int r = 0; r < nranks; ++r)
+        for (int q = 0; q < nranks; ++q) {
+          if (devices[r] == devices[q]) continue;
+          int can = 0;
+          PCGX_CUDA(cudaDeviceCanAccessPeer(&can, devices[r], devices[q]));
+          if (!can)
+            fail(PCGX_ERR_UNSUPPORTED, "local_group_create: device " + std::to_string(devices[r]) +
+                                           " cannot access device " + std::to_string(devices[q]) +
+                                           " (peer access)");
+          PCGX_CUDA(cudaSetDevice(devices[r]));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else PCGX_CUDA(e);
+        }
     auto grp = std::make_shared<LocalGroup>(nranks);
     std::vector<std::unique_ptr<pcgx_context_s>> made;
     for (int r = 0; r < nranks; ++r) {

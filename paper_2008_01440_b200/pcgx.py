@@ -122,7 +122,8 @@ class _Report(C.Structure):
                 ("wasted_matvec", C.c_int64), ("allreduces", C.c_int64),
                 ("halo_bytes", C.c_int64), ("alg_bytes", C.c_double),
                 ("spmv_equiv_bytes", C.c_double), ("step_ms", C.c_double),
-                ("step_launches", C.c_int64), ("step_bytes", C.c_double)]
+                ("step_launches", C.c_int64), ("step_bytes", C.c_double),
+                ("step_steps", C.c_int64)]
 
 
 FLAG_TIME_KERNELS = 1
@@ -764,6 +765,7 @@ class SolveReport:
     step_ms: float = 0.0
     step_launches: int = 0
     step_bytes: float = 0.0
+    step_steps: int = 0
 
     @classmethod
     def _from(cls, r: _Report):
@@ -801,6 +803,9 @@ def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
     f_dev = L.pcgx_pcg_solve_newton_device if newton else L.pcgx_pcg_solve_device
     f_host = L.pcgx_pcg_solve_newton if newton else L.pcgx_pcg_solve
     if isinstance(b, DeviceVector):
+        if x_out is not None and (not isinstance(x_out, DeviceVector) or x_out.n != op.local_size()):
+            raise InvalidArgument("pcg_solve: x_out must be a DeviceVector of "
+                                  f"{op.local_size()} elements for a device rhs")
         x = x_out or DeviceVector(op.ctx, op.local_size())
         if opts.x0 is not None:
             o.x0 = opts.x0.ptr
@@ -812,7 +817,14 @@ def pcg_solve(op: ScaledOperator, b, opts: SolveOptions | None = None,
     b = np.ascontiguousarray(b, dtype=np.float64)
     if b.size != op.local_size():
         raise InvalidArgument("pcg_solve: rhs length mismatch")
-    x = np.empty(op.local_size()) if x_out is None else x_out
+    if x_out is None:
+        x = np.empty(op.local_size())
+    else:
+        x = x_out
+        if (not isinstance(x, np.ndarray) or x.dtype != np.float64 or not x.flags.c_contiguous
+                or not x.flags.writeable or x.size != op.local_size()):
+            raise InvalidArgument("pcg_solve: x_out must be a writeable C-contiguous float64 array of "
+                                  f"{op.local_size()} elements")
     x0 = None
     if opts.x0 is not None:
         x0 = np.ascontiguousarray(opts.x0, dtype=np.float64)

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -62,6 +63,105 @@ static int run_case(const char* tag, const LinearOperator& inner, Index nx, int 
       (unsigned long long)r_gpu.matvec, r_ref.rel_res, r_gpu.rel_res, rel,
       bitwise ? "true" : "false", r_ref.wall_time, r_gpu.wall_time);
   return ok ? 0 : 1;
+}
+
+static bool same_bits(const Vector& a, const Vector& b) {
+  if (a.size() != b.size()) return false;
+  for (Index i = 0; i < a.size(); ++i)
+    if (std::memcmp(a.data() + i, b.data() + i, sizeof(double)) != 0) return false;
+  return true;
+}
+
+static bool same_report(const SolveReport& a, const SolveReport& b) {
+  return a.iters == b.iters && a.ddot == b.ddot && a.matvec == b.matvec &&
+         a.prec_applies == b.prec_applies && a.rel_res == b.rel_res &&
+         a.true_rel_res == b.true_rel_res && a.converged == b.converged;
+}
+
+// The reference's own extension points (linop.hpp:21-47, pcg.hpp:20-25): the
+// reference's pcg_solve / power_method / dacg_smallest run unchanged with the
+// device operator and the device preconditioners plugged in. The device SpMV and
+// Chebyshev / Newton applies are bitwise the reference's and the reductions are
+// the reference's own (host), so x, every counter and every residual must be
+// bit-identical to the all-CPU run.
+static int plugin_cases(polycg::gpu::Session& sess) {
+  int bad = 0;
+  auto run = [&](const char* tag, const LinearOperator& inner, Index nx, int m, bool newton) {
+    auto [scaled, d] = jacobi_scale(inner);
+    const auto [a0, b0] = analytic_extremes(StencilKind::lap3d, nx, true);
+    const Vector b = scaled.apply(random_uniform_vector(scaled.size(), 20240801));
+    std::unique_ptr<Preconditioner> p_cpu, p_gpu, p_gpu2;
+    if (newton) {
+      p_cpu = std::make_unique<NewtonPreconditioner>(newton_params(a0, b0, m, 1.001));
+      p_gpu = std::make_unique<polycg::gpu::NewtonPreconditioner>(sess, newton_params(a0, b0, m, 1.001));
+      p_gpu2 = std::make_unique<polycg::gpu::NewtonPreconditioner>(sess, newton_params(a0, b0, m, 1.001));
+    } else {
+      p_cpu = std::make_unique<ChebyshevPreconditioner>(cheb_params(a0, b0, m, 1.001));
+      p_gpu = std::make_unique<polycg::gpu::ChebyshevPreconditioner>(sess, cheb_params(a0, b0, m, 1.001));
+      p_gpu2 = std::make_unique<polycg::gpu::ChebyshevPreconditioner>(sess, cheb_params(a0, b0, m, 1.001));
+    }
+    auto [x_ref, r_ref] = polycg::pcg_solve(scaled, b, {}, p_cpu.get());
+    // (1) device operator + device preconditioner under the reference's pcg_solve
+    polycg::gpu::DeviceLinearOperator dlo(sess, scaled);
+    auto [x_dev, r_dev] = polycg::pcg_solve(dlo, b, {}, p_gpu.get());
+    // (2) the device preconditioner with the host operator (cached upload)
+    const int up0 = sess.uploads();
+    auto [x_mix, r_mix] = polycg::pcg_solve(scaled, b, {}, p_gpu2.get());
+    auto [x_mix2, r_mix2] = polycg::pcg_solve(scaled, b, {}, p_gpu2.get());
+    const int reup = sess.uploads() - up0;
+    const bool ok = same_bits(x_ref, x_dev) && same_report(r_ref, r_dev) && same_bits(x_ref, x_mix) &&
+                    same_report(r_ref, r_mix) && same_bits(x_ref, x_mix2) && reup == 0 &&
+                    dlo.matvec_count() == static_cast<std::uint64_t>(r_ref.iters + 1);
+    std::printf("{\"case\": \"%s\", \"ok\": %s, \"iters\": [%d, %d], \"matvec\": [%llu, %llu], "
+                "\"x_bitwise\": [%s, %s], \"report_equal\": [%s, %s], \"reuploads\": %d, "
+                "\"dlo_matvec_count\": %llu}\n",
+                tag, ok ? "true" : "false", r_ref.iters, r_dev.iters, (unsigned long long)r_ref.matvec,
+                (unsigned long long)r_dev.matvec, same_bits(x_ref, x_dev) ? "true" : "false",
+                same_bits(x_ref, x_mix) ? "true" : "false", same_report(r_ref, r_dev) ? "true" : "false",
+                same_report(r_ref, r_mix) ? "true" : "false", reup,
+                (unsigned long long)dlo.matvec_count());
+    return ok ? 0 : 1;
+  };
+  const StencilOperator st32(StencilKind::lap3d, 32);
+  bad += run("plugin_ref_pcg_stencil32_cheb10", st32, 32, 10, false);
+  const CsrMatrix cs24 = assemble_laplacian(StencilKind::lap3d, 24);
+  bad += run("plugin_ref_pcg_csr24_cheb7", cs24, 24, 7, false);
+  bad += run("plugin_ref_pcg_stencil32_newton3", st32, 32, 3, true);
+  // power_method / dacg_smallest (eigenest.cpp:48-167) on the device operator
+  {
+    auto [scaled, d] = jacobi_scale(st32);
+    polycg::gpu::DeviceLinearOperator dlo(sess, scaled);
+    const EigResult pc = polycg::power_method(scaled), pg = polycg::power_method(dlo);
+    EigOptions dopt;
+    dopt.tol = 1e-2;
+    dopt.maxit = 5000;
+    const EigResult dc = polycg::dacg_smallest(scaled, dopt), dg = polycg::dacg_smallest(dlo, dopt);
+    const bool ok = pc.value == pg.value && pc.iters == pg.iters && pc.matvecs == pg.matvecs &&
+                    dc.value == dg.value && dc.iters == dg.iters && dc.matvecs == dg.matvecs &&
+                    pc.trace == pg.trace && dc.trace == dg.trace;
+    std::printf("{\"case\": \"plugin_ref_power_dacg_stencil32\", \"ok\": %s, \"power\": [%.17g, %.17g], "
+                "\"dacg\": [%.17g, %.17g], \"iters\": [%d, %d, %d, %d]}\n",
+                ok ? "true" : "false", pc.value, pg.value, dc.value, dg.value, pc.iters, pg.iters, dc.iters,
+                dg.iters);
+    bad += ok ? 0 : 1;
+  }
+  // the one-shot drop-in pcg_solve caches its session and operator upload
+  {
+    auto [scaled, d] = jacobi_scale(st32);
+    const auto [a0, b0] = analytic_extremes(StencilKind::lap3d, 32, true);
+    const Vector b = scaled.apply(random_uniform_vector(scaled.size(), 20240801));
+    ChebyshevPreconditioner p(cheb_params(a0, b0, 10, 1.001));
+    auto& ds = polycg::gpu::default_session(0);
+    const int u0 = ds.uploads();
+    auto [x1, r1] = polycg::gpu::pcg_solve(scaled, b, {}, &p);
+    auto [x2, r2] = polycg::gpu::pcg_solve(scaled, b, {}, &p);
+    const int ups = ds.uploads() - u0;
+    const bool ok = ups == 1 && same_bits(x1, x2) && r1.iters == r2.iters;
+    std::printf("{\"case\": \"oneshot_upload_cached\", \"ok\": %s, \"uploads\": %d}\n",
+                ok ? "true" : "false", ups);
+    bad += ok ? 0 : 1;
+  }
+  return bad;
 }
 
 int main() {
@@ -160,5 +260,6 @@ int main() {
   } catch (const std::invalid_argument&) {
     std::printf("{\"case\": \"reject_custom_prec\", \"ok\": true}\n");
   }
+  bad += plugin_cases(sess);
   return bad == 0 ? 0 : 1;
 }

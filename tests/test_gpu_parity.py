@@ -517,6 +517,50 @@ def test_cheb2_bitwise_vs_oracle(P, ctx, oracle, dims, plan, monkeypatch):
         assert np.array_equal(out, ref), (dims, kz2, m)
 
 
+@pytest.mark.parametrize("dims", [(24, 24, 24), (66, 10, 9), (64, 16, 1), (130, 17, 33), (2, 2, 2),
+                                  (130, 47, 41), (64, 61, 7), (128, 33, 70), (192, 20, 3)])
+@pytest.mark.parametrize("plan", [("", "32"), ("u", "1"), ("u", "5"), ("u", "2")])
+def test_cheb3_bitwise_vs_oracle(P, ctx, oracle, dims, plan, monkeypatch):
+    """The three-step pass (stencil7_cheb3_kernel: stage 1 on a 2-deep halo, stage 2
+    on a 1-deep one, the i-halo columns on the j-halo warps, z-chunks of any height)
+    reproduces every per-step value of the reference recurrence: degrees that split
+    into (2-step first pass) + 3-step passes + up to two 2-step passes, partial tiles
+    in i and j, single planes, chunks of one plane."""
+    spec, kz2 = plan
+    monkeypatch.setenv("PCGX_C2PLAN", spec)
+    monkeypatch.setenv("PCGX_KZ2", kz2)
+    nx, ny, nz = dims
+    op = stencil(P, ctx, nx, ny, nz)
+    opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+    r = oracle.random_uniform(nx * ny * nz, 13)
+    for m in (5, 6, 7, 9, 11, 14, 20):
+        out = P.apply_chebyshev(P.cheb_params(a, b, m, 1.001), op, r)
+        ref = oracle.apply_chebyshev(opo, oracle.cheb_params(a, b, m, 1.001), r)
+        assert np.array_equal(out, ref), (dims, plan, m)
+
+
+@pytest.mark.parametrize("m", [5, 7, 20, 40])
+def test_cheb3_pcg_matches_two_step_path(P, ctx, oracle, m, monkeypatch):
+    """PCG with three-step passes against the two-step schedule and the oracle:
+    per-step values are bitwise equal, only the r'z reduction of the last pass is
+    taken over another launch shape."""
+    nx = 48
+    a, b = P.analytic_extremes(3, nx)
+    op3 = stencil(P, ctx, nx)
+    rhs = op3.apply(P.random_uniform_vector(nx ** 3, SEED))
+    prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001))
+    x3, r3 = P.pcg_solve(op3, rhs, None, prec)
+    monkeypatch.setenv("PCGX_CHEB3", "0")
+    op2 = stencil(P, ctx, nx)
+    x2, r2 = P.pcg_solve(op2, rhs, None, prec)
+    xo, ro = oracle.pcg_solve(OracleOp("lap3d", nx=nx), oracle.cheb_params(a, b, m, 1.001), rhs)
+    assert r3.iters == r2.iters == ro["iters"]
+    assert r3.ddot == ro["ddot"] and r3.matvec == ro["matvec"]
+    assert rel_norm(x3, xo) <= 1e-12 and rel_norm(x2, xo) <= 1e-12
+    assert r3.kernel_launches < r2.kernel_launches
+
+
 def test_cheb2_matches_single_step_path(P, ctx, monkeypatch):
     monkeypatch.setenv("PCGX_CHEB2", "1")
     nx = 40
