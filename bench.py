@@ -128,7 +128,9 @@ class Dist:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             if backend is None:
                 backend = "cpu:gloo,cuda:nccl" if torch.cuda.is_available() else "gloo"
-            if torch.cuda.is_available():
+            if os.environ.get("PCGX_BENCH_COMM") == "host":
+                backend = "gloo"  # all ranks may share one GPU: plumbing on the CPU only
+            elif torch.cuda.is_available():
                 torch.cuda.set_device(local)
             if not dist.is_initialized():
                 dist.init_process_group(backend=backend, rank=rank, world_size=ws)
@@ -244,12 +246,22 @@ def run_gpu(args):
     D = Dist(ws, rank, local)
     # PCGX_BENCH_DIST=1: take the multi-GPU code path even at world size 1 (a
     # 1-rank NCCL communicator; with PCGX_FORCE_NCCL=1 its all-reduces go through NCCL)
-    if ws > 1 or os.environ.get("PCGX_BENCH_DIST") == "1":
+    comm = "nccl"
+    if ws > 1 and os.environ.get("PCGX_BENCH_COMM") == "host":
+        # every rank on GPU 0, halos and all-reduces through host shared memory
+        # (pcgx_context_create_host): the multi-process path where there is one GPU
+        import uuid
+        name = D.bcast_bytes(f"pcgx_bench_{uuid.uuid4().hex[:12]}".encode() if rank == 0 else None)
+        ctx = P.Context(0, nranks=ws, rank=rank, host_comm=name.decode())
+        comm = "host shared memory (all ranks on GPU 0)"
+    elif ws > 1 or os.environ.get("PCGX_BENCH_DIST") == "1":
         nid = D.bcast_bytes(P.Context.nccl_unique_id() if rank == 0 else None)
         ctx = P.Context(local, nranks=ws, rank=rank, nccl_id=nid, dist=True)
     else:
         ctx = P.Context(0)
-    kind, (nx, ny, nz), degrees, desc = workload(args.config, ws)
+    config = args.config or ("cfg2" if ws == 1 else "cfg5w")
+    args.config = config
+    kind, (nx, ny, nz), degrees, desc = workload(config, ws)
     if args.degrees:
         degrees = [int(v) for v in args.degrees.split(",")]
     t_setup = time.perf_counter()
@@ -328,7 +340,8 @@ def run_gpu(args):
     per_k = []
     for k, rep, t in reps:
         per_k.append({"k": k, "iters": rep.iters, "ddot": rep.ddot, "matvec": rep.matvec,
-                      "time_to_1e8_s": round(t, 6), "rel_res": rep.rel_res,
+                      "time_to_1e8_s": round(t, 6), "ms_per_iter": round(t * 1e3 / max(rep.iters, 1), 4),
+                      "rel_res": rep.rel_res,
                       "true_rel_res": rep.true_rel_res, "converged": rep.converged,
                       "alg_GBps": round(D.sum(rep.alg_bytes) / t / 1e9, 1),
                       "spmv_equiv_GBps": round(rep.matvec * spmv_bytes / t / 1e9, 1)})
@@ -352,7 +365,9 @@ def run_gpu(args):
                else f"working set {ws_bytes / 1e6:.0f} MB fits L2 (126 MB): L2-bound, not an HBM roofline claim")
     storage = op.storage()
     kdesc = {
-        "stencil": ("stencil7_cheb2f_kernel (TMA, two fused SpMV + Chebyshev steps per pass, software-pipelined, 64x20 tiles, 40 B/unknown)"
+        "stencil": ("stencil7_cheb3_kernel (TMA, three fused SpMV + Chebyshev steps per pass, 64x12 tiles, 40 B/unknown)"
+                    if rprof.step_steps == 3 else
+                    "stencil7_cheb2f_kernel (TMA, two fused SpMV + Chebyshev steps per pass, software-pipelined, 64x20 tiles, 40 B/unknown)"
                     if step_bytes == 40.0 * n_loc else
                     "stencil7v2_kernel<EpiChebStep> (fused SpMV + Chebyshev step, 32 B/unknown)"),
         "sell32": "sell_kernel<EpiChebStep> (SELL-32 int32 CSR SpMV + Chebyshev step, 12 nnz + 4(n+1) + 40 n bytes)",
@@ -373,6 +388,7 @@ def run_gpu(args):
                    "n_global": n_glob, "degrees": degrees, "theta_scale": SCALE, "tol": TOL,
                    "bounds": bounds, "alpha": alpha, "beta": beta,
                    "parallelism": (f"z-slab x{ws}" if kind == "stencil" else f"block rows x{ws}"),
+                   "comm": comm if ws > 1 else None,
                    "setup_s": round(t_setup, 2),
                    "spmv_equiv_bytes": spmv_bytes,
                    "storage": op.storage(),
@@ -558,8 +574,10 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="pcgx", choices=["pcgx", "reference"])
-    ap.add_argument("--config", default="cfg2",
-                    choices=["cfg2", "cfg5s", "cfg5w", "cfg1", "cfg3", "cfg4"])
+    ap.add_argument("--config", default=None,
+                    choices=["cfg2", "cfg5s", "cfg5w", "cfg1", "cfg3", "cfg4"],
+                    help="default: cfg2 (BASELINE configs[1]) at one GPU, the north-star weak-scaling "
+                         "config cfg5w (512 x 512 x 512N, k=40) at N > 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--degrees", default=None, help="override the degree list (profiling)")
     args = ap.parse_args()

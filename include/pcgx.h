@@ -81,6 +81,14 @@ pcgx_status pcgx_context_create_dist(int device, int nranks, int rank, const voi
  * (every rank calls the same sequence, as with NCCL). Used to exercise the
  * multi-rank slab path on a single GPU. */
 pcgx_status pcgx_local_group_create(int nranks, const int* devices, pcgx_context* out);
+/* One rank of an nranks-process job on ONE host whose ranks exchange through a
+ * POSIX shared-memory segment `name` (host-staged, synchronous; all ranks pass the
+ * same name, rank 0 creates it). Ranks may share a GPU: no kernel or stream waits
+ * on another rank. mailbox_bytes (0 = 64 MiB) bounds one message per rank. For
+ * running the multi-process slab / block-row algorithm where NCCL cannot (several
+ * ranks on one device); scalars are summed in rank order. */
+pcgx_status pcgx_context_create_host(int device, int nranks, int rank, const char* name,
+                                     size_t mailbox_bytes, pcgx_context* out);
 void pcgx_context_destroy(pcgx_context ctx);
 int pcgx_context_rank(pcgx_context ctx);
 int pcgx_context_nranks(pcgx_context ctx);

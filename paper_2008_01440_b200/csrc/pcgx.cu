@@ -11,6 +11,11 @@
 // all-reduces (8 B and 16 B) per PCG iteration.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <pthread.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -451,6 +456,188 @@ struct LocalComm : CommBase {
                    double* const* gbuf) override;
   bool graph_capturable() const override { return false; }
 };
+
+// ---------------------------------------------------------------- host-staged comm
+// HostComm: P ranks in P processes on one host (any devices, also all on ONE GPU)
+// exchanging through a POSIX shared-memory segment: every plane / segment / scalar
+// is copied device -> shared memory -> device by the host, synchronously, with a
+// process-shared barrier between the write and read phases. No kernel and no
+// stream ever waits on another rank, so ranks that share a GPU cannot deadlock
+// it. It exists to run the multi-process slab / block-row algorithm (the same
+// CommBase calls NCCL serves) where there is one GPU: bitwise the LocalGroup
+// results (scalars are summed in rank order, like group_sum_kernel).
+struct ShmHeader {
+  std::atomic<uint64_t> magic;
+  pthread_barrier_t bar;
+  int nranks;
+  size_t cap;
+};
+constexpr uint64_t kShmMagic = 0x70636778686f7374ull;  // "pcgxhost"
+constexpr size_t kShmHdr = 4096;
+
+struct HostComm : CommBase {
+  int rank = 0, nranks = 1;
+  std::string name;
+  unsigned char* base = nullptr;
+  size_t total = 0, cap = 0;
+  ShmHeader* hdr() const { return reinterpret_cast<ShmHeader*>(base); }
+  double* box(int r) const { return reinterpret_cast<double*>(base + kShmHdr + (size_t)r * cap); }
+  void barrier() const {
+    const int e = pthread_barrier_wait(&hdr()->bar);
+    if (e != 0 && e != PTHREAD_BARRIER_SERIAL_THREAD) fail(PCGX_ERR_NCCL, "host comm: barrier failed");
+  }
+  void need(size_t bytes) const {
+    if (bytes > cap)
+      fail(PCGX_ERR_UNSUPPORTED, "host comm: message of " + std::to_string(bytes) + " bytes exceeds the " +
+                                     std::to_string(cap) + "-byte mailbox");
+  }
+  ~HostComm() override {
+    if (!base) return;
+    try {
+      barrier();
+    } catch (...) {
+    }
+    munmap(base, total);
+    if (rank == 0) shm_unlink(name.c_str());
+  }
+  void allreduce(pcgx_context c, int slot, int count) override {
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+    PCGX_CUDA(cudaMemcpy(box(rank), c->S + slot, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    barrier();
+    double sum[kSlots];
+    for (int i = 0; i < count; ++i) {
+      double v = 0.0;
+      for (int q = 0; q < nranks; ++q) v += box(q)[i];
+      sum[i] = v;
+    }
+    barrier();
+    PCGX_CUDA(cudaMemcpy(c->S + slot, sum, sizeof(double) * count, cudaMemcpyHostToDevice));
+  }
+  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override {
+    (void)op;
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+    size_t off = 0;
+    for (int i = 0; i < n; ++i) off += 2 * (size_t)items[i].count;
+    need(sizeof(double) * off);
+    off = 0;
+    for (int i = 0; i < n; ++i) {  // my outbox: [lo part | hi part] per item
+      const size_t b = sizeof(double) * (size_t)items[i].count;
+      if (rank > 0) PCGX_CUDA(cudaMemcpy(box(rank) + off, items[i].send_lo, b, cudaMemcpyDeviceToHost));
+      if (rank < nranks - 1)
+        PCGX_CUDA(cudaMemcpy(box(rank) + off + items[i].count, items[i].send_hi, b, cudaMemcpyDeviceToHost));
+      off += 2 * (size_t)items[i].count;
+    }
+    barrier();
+    off = 0;
+    for (int i = 0; i < n; ++i) {  // rank-1's top -> my recv_lo, rank+1's bottom -> my recv_hi
+      const size_t b = sizeof(double) * (size_t)items[i].count;
+      if (rank > 0 && items[i].recv_lo)
+        PCGX_CUDA(cudaMemcpy(items[i].recv_lo, box(rank - 1) + off + items[i].count, b, cudaMemcpyHostToDevice));
+      if (rank < nranks - 1 && items[i].recv_hi)
+        PCGX_CUDA(cudaMemcpy(items[i].recv_hi, box(rank + 1) + off, b, cudaMemcpyHostToDevice));
+      off += 2 * (size_t)items[i].count;
+    }
+    barrier();
+  }
+  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override {
+    const long long nxy = op->nx * op->ny, nzl = op->nzl;
+    PlaneX items[2];
+    for (int v = 0; v < nv && v < 2; ++v)
+      items[v] = {xs[v], v ? op->ghost_lo2 : op->ghost_lo, xs[v] + (nzl - 1) * nxy,
+                  v ? op->ghost_hi2 : op->ghost_hi, nxy};
+    xchg(c, op, items, std::min(nv, 2));
+  }
+  void halo_wait(pcgx_context c) override { (void)c; }  // the exchange completed synchronously
+  void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
+                   double* const* gbuf) override {
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
+    const int P = nranks;
+    // my outbox: a directory (offset, count) per destination rank, then the data
+    int64_t* dir = reinterpret_cast<int64_t*>(box(rank));
+    for (int q = 0; q < 2 * P; ++q) dir[q] = 0;
+    size_t off = 2 * (size_t)P;  // in doubles (int64 and double are both 8 bytes)
+    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
+      const int q = op->nb_rank[i];
+      dir[q] = (int64_t)off;
+      dir[P + q] = op->send_cnt[i];
+      need(sizeof(double) * (off + (size_t)nv * op->send_cnt[i]));
+      for (int v = 0; v < nv; ++v) {
+        if (op->send_cnt[i])
+          PCGX_CUDA(cudaMemcpy(box(rank) + off, sbuf[v] + op->send_off[i], sizeof(double) * op->send_cnt[i],
+                               cudaMemcpyDeviceToHost));
+        off += (size_t)op->send_cnt[i];
+      }
+    }
+    barrier();
+    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
+      const int q = op->nb_rank[i];
+      const int64_t* qd = reinterpret_cast<const int64_t*>(box(q));
+      const int64_t qoff = qd[rank], qcnt = qd[P + rank];
+      if (qcnt != op->recv_cnt[i]) fail(PCGX_ERR_NCCL, "host comm: block-row segment size mismatch");
+      for (int v = 0; v < nv; ++v)
+        if (qcnt)
+          PCGX_CUDA(cudaMemcpy(gbuf[v] + op->recv_off[i], box(q) + qoff + (size_t)v * qcnt,
+                               sizeof(double) * qcnt, cudaMemcpyHostToDevice));
+    }
+    barrier();
+  }
+  bool graph_capturable() const override { return false; }
+};
+
+HostComm* host_comm_open(int nranks, int rank, const std::string& name, size_t cap) {
+  auto hc = std::make_unique<HostComm>();
+  hc->rank = rank;
+  hc->nranks = nranks;
+  hc->name = name;
+  hc->cap = (cap + 4095) / 4096 * 4096;
+  hc->total = kShmHdr + (size_t)nranks * hc->cap;
+  int fd = -1;
+  if (rank == 0) {
+    shm_unlink(name.c_str());  // a stale segment of a crashed job
+    fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) fail(PCGX_ERR_NCCL, "host comm: shm_open(" + name + ") failed");
+    if (ftruncate(fd, (off_t)hc->total) != 0) {
+      close(fd);
+      fail(PCGX_ERR_NCCL, "host comm: ftruncate failed");
+    }
+  } else {
+    for (int tries = 0; fd < 0; ++tries) {  // rank 0 creates it; up to 120 s
+      fd = shm_open(name.c_str(), O_RDWR, 0600);
+      struct stat st;
+      if (fd >= 0 && (fstat(fd, &st) != 0 || (size_t)st.st_size < hc->total)) {
+        close(fd);
+        fd = -1;
+      }
+      if (fd < 0) {
+        if (tries > 120000) fail(PCGX_ERR_NCCL, "host comm: segment " + name + " never appeared");
+        usleep(1000);
+      }
+    }
+  }
+  void* m = mmap(nullptr, hc->total, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (m == MAP_FAILED) fail(PCGX_ERR_NCCL, "host comm: mmap failed");
+  hc->base = static_cast<unsigned char*>(m);
+  ShmHeader* h = hc->hdr();
+  if (rank == 0) {
+    pthread_barrierattr_t a;
+    pthread_barrierattr_init(&a);
+    pthread_barrierattr_setpshared(&a, PTHREAD_PROCESS_SHARED);
+    pthread_barrier_init(&h->bar, &a, (unsigned)nranks);
+    pthread_barrierattr_destroy(&a);
+    h->nranks = nranks;
+    h->cap = hc->cap;
+    h->magic.store(kShmMagic, std::memory_order_release);
+  } else {
+    for (int tries = 0; h->magic.load(std::memory_order_acquire) != kShmMagic; ++tries) {
+      if (tries > 120000) fail(PCGX_ERR_NCCL, "host comm: segment " + name + " never initialised");
+      usleep(1000);
+    }
+    if (h->nranks != nranks || h->cap != hc->cap) fail(PCGX_ERR_INVALID, "host comm: ranks disagree on the job shape");
+  }
+  hc->barrier();  // everyone attached
+  return hc.release();
+}
 
 void allreduce(pcgx_context c, int slot, int count) {
   if (!c->cm) return;
@@ -3278,7 +3465,7 @@ void stencil_setup(pcgx_context c, pcgx_operator op, int64_t nx, int64_t ny, int
       init_stencil_ghosts(c, op);
       if (c->nranks > 1 && op->nzl < 2) op->cheb2 = false;  // 2-plane halos need >= 2 planes
       op->zpad = (op->cheb2 && c->nranks > 1) ? 2 : 0;
-      op->cheb3 = op->cheb2 && op->cheb2v >= 3 && c->nranks == 1 && env_int("PCGX_CHEB3", 1) != 0;
+      op->cheb3 = op->cheb2 && op->cheb2v >= 3 && c->nranks == 1 && env_int("PCGX_CHEB3", 0) != 0;
     } catch (...) {
       free_op(op);
       throw;
@@ -3393,6 +3580,23 @@ pcgx_status pcgx_context_create_dist(int device, int nranks, int rank, const voi
       PCGX_NCCL(nccl().CommInitRank(&c->comm, nranks, id, rank));
       c->cm = new NcclComm();
     }
+    *out = c.release();
+  });
+}
+
+pcgx_status pcgx_context_create_host(int device, int nranks, int rank, const char* name, size_t mailbox_bytes,
+                                     pcgx_context* out) {
+  return guarded(nullptr, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks || !name || !out)
+      fail(PCGX_ERR_INVALID, "context_create_host: bad rank/nranks/name");
+    auto c = std::make_unique<pcgx_context_s>();
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    ctx_init(c.get());
+    if (nranks > 1)
+      c->cm = host_comm_open(nranks, rank, name[0] == '/' ? std::string(name) : "/" + std::string(name),
+                             mailbox_bytes ? mailbox_bytes : ((size_t)64 << 20));
     *out = c.release();
   });
 }

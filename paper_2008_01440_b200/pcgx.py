@@ -132,7 +132,8 @@ FLAG_NO_GRAPH = 2
 # Exported symbols of include/pcgx.h (tests check the .so exports all of them).
 SYMBOLS = [
     "pcgx_abi_version", "pcgx_last_error", "pcgx_context_create", "pcgx_nccl_unique_id",
-    "pcgx_context_create_dist", "pcgx_local_group_create", "pcgx_context_destroy", "pcgx_context_rank",
+    "pcgx_context_create_dist", "pcgx_local_group_create", "pcgx_context_create_host",
+    "pcgx_context_destroy", "pcgx_context_rank",
     "pcgx_context_nranks", "pcgx_synchronize", "pcgx_kernel_launches", "pcgx_device_alloc",
     "pcgx_device_free", "pcgx_memcpy_h2d", "pcgx_memcpy_d2h", "pcgx_memcpy_d2d",
     "pcgx_host_alloc", "pcgx_host_free", "pcgx_timer_start", "pcgx_timer_stop",
@@ -182,6 +183,8 @@ def lib():
         "pcgx_context_create_dist": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p,
                                                C.POINTER(ctx)]),
         "pcgx_local_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(ctx)]),
+        "pcgx_context_create_host": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t,
+                                               C.POINTER(ctx)]),
         "pcgx_context_destroy": (None, [ctx]),
         "pcgx_context_rank": (C.c_int, [ctx]),
         "pcgx_context_nranks": (C.c_int, [ctx]),
@@ -284,11 +287,17 @@ class Context:
     one call at a time."""
 
     def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, nccl_id=None,
-                 dist: bool = False, _handle=None):
+                 dist: bool = False, host_comm: str | None = None, mailbox_bytes: int = 0,
+                 _handle=None):
         L = lib()
         h = C.c_void_p()
         if _handle is not None:
             h = _handle
+        elif host_comm is not None:
+            # one rank of a multi-process job on one host, exchanging through the
+            # shared-memory segment `host_comm` (pcgx_context_create_host)
+            _check(L.pcgx_context_create_host(device, nranks, rank, host_comm.encode(), mailbox_bytes,
+                                              C.byref(h)))
         elif nranks == 1 and not dist:
             _check(L.pcgx_context_create(device, C.byref(h)))
         else:

@@ -1,0 +1,53 @@
+# SPDX-License-Identifier: Apache-2.0
+"""One rank of a multi-PROCESS job on one GPU (tests/test_gpu_multiproc.py):
+pcgx_context_create_host -- halo planes, block-row segments and scalars through a
+shared-memory segment, no kernel waiting on another rank. Writes its slab /
+block of b = A x_true, P_m(A) r, the solution and the report to OUT/rank<r>.npz.
+
+    python tests/mp_worker.py NAME NRANKS RANK OUT KIND NX NY NZ M
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+SEED = 20240801
+
+
+def main():
+    name, nranks, rank, out, kind = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
+    nx, ny, nz, m = (int(v) for v in sys.argv[6:10])
+    from paper_2008_01440_b200 import pcgx as P
+    ctx = P.Context(0, nranks=nranks, rank=rank, host_comm=name)
+    if kind == "stencil":
+        op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
+        a, b = P.analytic_extremes_box(nx, ny, nz)
+        n = nx * ny * nz
+    else:
+        A = P.gen_fe27(nx, 1.0, SEED)
+        op, _ = P.jacobi_scale(A, ctx)
+        a, b = 0.01, 2.5
+        n = A.n
+    lo, nl = op.row0(), op.local_size()
+    xt = P.random_uniform_vector(nl, SEED, offset=lo)
+    bl = op.apply(xt)
+    r_full = P.random_uniform_vector(n, 77)
+    prm = P.cheb_params(a, b, m, 1.001)
+    zl = P.apply_chebyshev(prm, op, r_full[lo:lo + nl])
+    x, rep = P.pcg_solve(op, bl, P.SolveOptions(), P.ChebyshevPreconditioner(prm))
+    np.savez(os.path.join(out, f"rank{rank}.npz"), lo=lo, b=bl, z=zl, x=x,
+             rep=json.dumps({"iters": rep.iters, "ddot": rep.ddot, "matvec": rep.matvec,
+                             "converged": bool(rep.converged), "allreduces": rep.allreduces,
+                             "halo_bytes": rep.halo_bytes, "rel_res": rep.rel_res,
+                             "true_rel_res": rep.true_rel_res}),
+             storage=op.storage())
+    op.close()
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,113 @@
+# SPDX-License-Identifier: Apache-2.0
+"""The multi-rank algorithm across PROCESSES on one GPU: P Python processes, one
+pcgx context each (pcgx_context_create_host: halo planes, block-row segments and
+scalars through a POSIX shared-memory segment, host-staged -- no kernel or stream
+waits on another rank, so ranks sharing one GPU cannot deadlock it). This is the
+process layout of a torchrun job; only the transport differs from NCCL.
+
+SpMV and every Chebyshev step are elementwise exact across slabs / row blocks,
+so b and P_m(A) r must be BITWISE the single-domain oracle's; the solve matches
+within the PCG parity bar (its reductions are per-rank trees summed in rank order)."""
+import json
+import os
+import subprocess
+import sys
+import uuid
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleOp
+from tests._util import rel_norm
+
+pytestmark = pytest.mark.gpu
+SEED = 20240801
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def run_job(nranks, kind, dims, m, tmp_path):
+    name = f"pcgx_test_{uuid.uuid4().hex[:12]}"
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), name, str(nranks), str(r),
+                               str(tmp_path), kind, *map(str, dims), str(m)],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for r in range(nranks)]
+    outs = []
+    for p in procs:
+        try:
+            o, _ = p.communicate(timeout=600)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise
+        outs.append((p.returncode, o))
+    for rc, o in outs:
+        assert rc == 0, o
+    res = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(nranks)]
+    return res
+
+
+@pytest.mark.parametrize("nranks,dims,m", [(2, (24, 24, 24), 10), (3, (20, 16, 26), 5), (2, (64, 40, 33), 20)])
+def test_multiprocess_slabs_match_single_domain(pcgx, oracle, nranks, dims, m, tmp_path):
+    P = pcgx
+    nx, ny, nz = dims
+    res = run_job(nranks, "stencil", dims, m, tmp_path)
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+    opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
+    xt = oracle.random_uniform(nx * ny * nz, SEED)
+    b_full = oracle.apply(opo, xt)
+    prm = oracle.cheb_params(a, b, m, 1.001)
+    z_full = oracle.apply_chebyshev(opo, prm, oracle.random_uniform(nx * ny * nz, 77))
+    x_full, rep_o = oracle.pcg_solve(opo, prm, b_full)
+    assert np.array_equal(np.concatenate([r["b"] for r in res]), b_full)
+    assert np.array_equal(np.concatenate([r["z"] for r in res]), z_full)
+    reps = [json.loads(str(r["rep"])) for r in res]
+    assert all(r["iters"] == reps[0]["iters"] for r in reps)
+    assert reps[0]["converged"] and abs(reps[0]["iters"] - rep_o["iters"]) <= 1
+    assert reps[0]["ddot"] == rep_o["ddot"] and reps[0]["matvec"] == rep_o["matvec"]
+    if reps[0]["iters"] == rep_o["iters"]:
+        assert rel_norm(np.concatenate([r["x"] for r in res]), x_full) <= 1e-10
+    assert all(r["halo_bytes"] > 0 for r in reps)
+
+
+def test_multiprocess_slabs_match_local_group(pcgx, tmp_path):
+    """Processes + shared memory and threads + stream-ordered copies run the same
+    algorithm with scalars summed in rank order: the solutions are bit-identical."""
+    P = pcgx
+    nx, ny, nz, m = 24, 20, 30, 8
+    res = run_job(3, "stencil", (nx, ny, nz), m, tmp_path)
+    ctxs = P.Context.local_group(3)
+    from concurrent.futures import ThreadPoolExecutor
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+
+    def rank(r, ctx):
+        op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
+        xt = P.random_uniform_vector(op.local_size(), SEED, offset=op.row0())
+        x, rep = P.pcg_solve(op, op.apply(xt), P.SolveOptions(),
+                             P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001)))
+        return x, rep
+
+    with ThreadPoolExecutor(3) as ex:
+        outs = [f.result(timeout=600) for f in [ex.submit(rank, r, c) for r, c in enumerate(ctxs)]]
+    assert np.array_equal(np.concatenate([o[0] for o in outs]), np.concatenate([r["x"] for r in res]))
+    assert outs[0][1].iters == json.loads(str(res[0]["rep"]))["iters"]
+    for c in ctxs:
+        c.close()
+
+
+def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, tmp_path):
+    """CSR block rows (the paper's distributed SpMV) across 2
+    processes: per-neighbour packed halos through the shared segment."""
+    P = pcgx
+    nx, m = 14, 6
+    res = run_job(2, "fe27", (nx, nx, nx), m, tmp_path)
+    A = P.gen_fe27(nx, 1.0, SEED)
+    opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
+    xt = oracle.random_uniform(A.n, SEED)
+    b_full = oracle.apply(opo, xt)
+    prm = oracle.cheb_params(0.01, 2.5, m, 1.001)
+    z_full = oracle.apply_chebyshev(opo, prm, oracle.random_uniform(A.n, 77))
+    assert np.array_equal(np.concatenate([r["b"] for r in res]), b_full)
+    assert np.array_equal(np.concatenate([r["z"] for r in res]), z_full)
+    x_full, rep_o = oracle.pcg_solve(opo, prm, b_full)
+    rep = json.loads(str(res[0]["rep"]))
+    assert rep["converged"] and abs(rep["iters"] - rep_o["iters"]) <= 1

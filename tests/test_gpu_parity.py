@@ -365,7 +365,29 @@ def test_no_graph_path_identical(P, ctx):
     x1, r1 = P.pcg_solve(op, rhs, P.SolveOptions(), prec)
     x2, r2 = P.pcg_solve(op, rhs, P.SolveOptions(flags=P.FLAG_NO_GRAPH), prec)
     assert np.array_equal(x1, x2) and r1.iters == r2.iters
-    assert r1.kernel_launches == r2.kernel_launches
+    # graphs: the tail of each segment sits in a conditional node a device-side
+    # convergence test closes (one tiny kernel per segment), so the stopping
+    # iteration does not compute and discard P r and A p as the direct launches do
+    assert r1.wasted_matvec == 2 and r2.wasted_matvec == 10 + 1
+    assert r2.kernel_launches - 6 < r1.kernel_launches <= r2.kernel_launches + r1.iters
+
+
+def test_device_convergence_skips_the_speculative_tail(P, ctx, oracle):
+    """The conditional-graph schedule on every preconditioner shape: the same x as
+    the speculative direct schedule, bitwise, and only the fused first pass of the
+    stopping iteration's P r (2 SpMVs) or nothing is computed beyond the reference."""
+    nx = 24
+    op = stencil(P, ctx, nx)
+    a, b = P.analytic_extremes(3, nx)
+    rhs = op.apply(P.random_uniform_vector(nx ** 3, SEED))
+    for m in (0, 1, 2, 3, 6, 13):
+        prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001))
+        x1, r1 = P.pcg_solve(op, rhs, P.SolveOptions(), prec)
+        x2, r2 = P.pcg_solve(op, rhs, P.SolveOptions(flags=P.FLAG_NO_GRAPH), prec)
+        assert np.array_equal(x1, x2) and (r1.iters, r1.matvec, r1.ddot) == (r2.iters, r2.matvec, r2.ddot)
+        assert r1.wasted_matvec == (2 if m >= 3 else 0), m
+        xo, ro = oracle.pcg_solve(OracleOp("lap3d", nx=nx), oracle.cheb_params(a, b, m, 1.001), rhs)
+        assert r1.iters == ro["iters"] and rel_norm(x1, xo) <= 1e-10
 
 
 def test_determinism_run_to_run(P, ctx):
@@ -529,6 +551,7 @@ def test_cheb3_bitwise_vs_oracle(P, ctx, oracle, dims, plan, monkeypatch):
     spec, kz2 = plan
     monkeypatch.setenv("PCGX_C2PLAN", spec)
     monkeypatch.setenv("PCGX_KZ2", kz2)
+    monkeypatch.setenv("PCGX_CHEB3", "1")
     nx, ny, nz = dims
     op = stencil(P, ctx, nx, ny, nz)
     opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
@@ -547,6 +570,7 @@ def test_cheb3_pcg_matches_two_step_path(P, ctx, oracle, m, monkeypatch):
     taken over another launch shape."""
     nx = 48
     a, b = P.analytic_extremes(3, nx)
+    monkeypatch.setenv("PCGX_CHEB3", "1")
     op3 = stencil(P, ctx, nx)
     rhs = op3.apply(P.random_uniform_vector(nx ** 3, SEED))
     prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001))
