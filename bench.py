@@ -375,7 +375,6 @@ def run_gpu(args):
         "bsr3_grid": "bsr3t_kernel (3x3 blocks on 32x4 node tiles, nine 4D value boxes + masks / r / x_old / x, d patches per plane by TMA, t = d x in shared memory, SpMV + Chebyshev step, 8*243 n/3 + 4 n/3 + 40 n bytes)",
         "dia": "dia_kernel<EpiChebStep> (offset storage SpMV + Chebyshev step, 8 K n + 4 n + 40 n bytes)",
         "dia_grid": "dia3t_kernel (offset storage on 32x8 grid tiles, values / masks / r / x_old / x, d patches by TMA through a 3-stage ring, t = d x in shared memory, SpMV + Chebyshev step, 8 K n + 4 n + 40 n bytes)",
-        "csr_tiles": "csr2_kernel<EpiChebStep> (TMA row tiles, 12 nnz + 4(n+1) + 40 n bytes)",
         "csr_chunked": "csr_kernel<EpiChebStep> (chunked CSR, 12 nnz + 4(n+1) + 40 n bytes)",
     }[storage]
 

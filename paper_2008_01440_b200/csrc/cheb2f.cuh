@@ -60,7 +60,7 @@ namespace pcgx {
 #define PCGX_C2FUPDIP 1
 #endif
 // i-neighbours of every lane straight from shared memory (two 8-byte LDS per
-// stage) instead of shuffles + the edge select (plain A, not kT / kUpd)
+// stage) instead of shuffles + the edge select (plain A, not the kUpd combine)
 #ifndef PCGX_C2FNBR
 #define PCGX_C2FNBR 1
 #endif
@@ -92,7 +92,7 @@ struct ChunkPlan {
   int start[kMax + 1];
 };
 
-template <bool kFirst, bool kRed, bool kT, bool kUpd = false>
+template <bool kFirst, bool kRed, bool kUpd = false>
 #if PCGX_C2FMINB == 1
 __global__ void __maxnreg__(PCGX_C2FMAXREG)
 #else
@@ -231,19 +231,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   double* gCt = gC + (long long)(kb - 1) * p.nxy;   // C pair at plane t
   double* gEv = gE + (long long)(kb - 3) * p.nxy;   // E pair at plane t-2
 
-  // kT: the stencil queues hold t = d * x (each product formed once per point);
-  // the recurrences' centre values travel in separate x queues
-  auto mul2 = [&](double2 v) { return make_double2(d * v.x, d * v.y); };
   double2 am = in_z(kb - 2) ? rqx2(sA, offA) : zero2;
   double2 ac = in_z(kb - 1) ? rqx2(sA + kFAPlane, offA) : zero2;
-  double2 x1 = ac;                             // kT: A[t-1] x (own row)
-  if (kT) {
-    am = mul2(am);
-    ac = mul2(ac);
-  }
   double2 a2 = zero2;                          // A[t-2] x (own row)
-  double2 c1 = zero2, c2 = zero2, c3 = zero2;  // C[t-1], C[t-2], C[t-3] (own row; t when kT)
-  double2 cx1 = zero2, cx2 = zero2;            // kT: C[t-1], C[t-2] x
+  double2 c1 = zero2, c2 = zero2, c3 = zero2;  // C[t-1], C[t-2], C[t-3] (own row)
   double acc = 0.0;
 
 #pragma unroll kC2Unroll
@@ -251,7 +242,6 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     if (tid == 0 && t >= kb && t - 1 + kFD <= u_last) issue_unit(t - 1 + kFD);
     const bool s1 = t <= ke;
     double2 ap = zero2, cv = zero2, rt = zero2;
-    double2 ct = zero2, xt = zero2;  // kT: C[t] as t = d x; A[t] x
     if (s1) mbar_wait(&bars[bslot], bphase);
     // ---------------- stage 1: C[t] on the extended tile row
     if (s1) {
@@ -279,9 +269,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         acc_rr = acc_rr + ap.x * ap.x;
         acc_rr = acc_rr + ap.y * ap.y;
       }
-      if (kT) ap = mul2(ap);
       double aw, ae;
-      if (PCGX_C2FNBR && !kT && (!kUpd || kIP)) {
+      if (PCGX_C2FNBR && (!kUpd || kIP)) {
         aw = pAu[offA - 1];
         ae = pAu[offA + 2];
       } else {
@@ -289,29 +278,20 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
 #if PCGX_C2FEDGE
       {
-        const double edge = kT ? d * pAu[offA + eoff] : rq(pAu, offA + eoff);
+        const double edge = rq(pAu, offA + eoff);
         aw = lane == 0 ? edge : aw;
         ae = lane == 31 ? edge : ae;
       }
 #else
-      if (lane == 0) aw = kT ? d * pAu[offA - 1] : rq(pAu, offA - 1);
-      if (lane == 31) ae = kT ? d * pAu[offA + 2] : rq(pAu, offA + 2);
+      if (lane == 0) aw = rq(pAu, offA - 1);
+      if (lane == 31) ae = rq(pAu, offA + 2);
 #endif
       }
       const double2 as = rqx2(pAu, offA - kFW);
       const double2 an = rqx2(pAu, offA + kFW);
-      double y0, y1;
-      double2 xc;  // A[t] x at the pair
-      if (kT) {
-        xc = *reinterpret_cast<const double2*>(pAu + offA);
-        y0 = stencil_point_t(d, am.x, d * as.x, aw, ac.x, ac.y, d * an.x, ap.x);
-        y1 = stencil_point_t(d, am.y, d * as.y, ac.x, ac.y, ae, d * an.y, ap.y);
-      } else {
-        xc = ac;
-        y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
-        y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
-      }
-      if (kT) xt = xc;
+      const double2 xc = ac;  // A[t] at the pair
+      const double y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
+      const double y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
       double2 c;
       if (kFirst) {
         c.x = p.c1 * ((2.0 * xc.x) - div_rn(y0, p.theta, inv_t));
@@ -326,8 +306,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       const bool live = plane_in && do1;
       if (live) cv = c;
       if (p.outC && live && interior && t >= kb && t < ke) st2(gCt, cv.x, cv.y);  // outC null: last pass
-      if (kT) ct = mul2(cv);
-      *reinterpret_cast<double2*>(pCu + offB) = kT ? ct : cv;
+      *reinterpret_cast<double2*>(pCu + offB) = cv;
       // i-halo columns of C[t] (read by stage 2 of plane t, two iterations on)
       if (do_h) {
         double hx = 0.0;
@@ -339,7 +318,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
           if (kFirst) hx = p.c1 * ((2.0 * xc) - div_rn(y, p.theta, inv_t));
           else hx = p.rk1 * (((p.c3 * xc) - (p.rk1m1 * pBu[offBh])) + p.c2 * (pRu[offBh] - y));
         }
-        pCu[offBh] = kT ? d * hx : hx;
+        pCu[offBh] = hx;
       }
     }
     // ---------------- stage 2: E[t-2] on the own tile row (warps 1..8)
@@ -364,17 +343,9 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       }
       const double2 cs = *reinterpret_cast<const double2*>(pC2 + offB - kFW);
       const double2 cn = *reinterpret_cast<const double2*>(pC2 + offB + kFW);
-      double y0, y1;
-      double2 cc;  // C[t-2] x at the pair
-      if (kT) {
-        y0 = stencil_point_t(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
-        y1 = stencil_point_t(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
-        cc = cx2;
-      } else {
-        y0 = stencil_point(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
-        y1 = stencil_point(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
-        cc = c2;
-      }
+      const double y0 = stencil_point(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
+      const double y1 = stencil_point(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
+      const double2 cc = c2;  // C[t-2] at the pair
       double2 rv, xo;
       if (kFirst) {
         rv = a2;  // A == R == r
@@ -392,19 +363,12 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     }
       __syncthreads();
     // rotate the register queues, rings and global pointers by one plane
-    if (kT) {
-      a2 = x1;
-      x1 = xt;
-    } else {
-      a2 = am;
-    }
+    a2 = am;
     am = ac;
     ac = ap;
     c3 = c2;
     c2 = c1;
-    c1 = kT ? ct : cv;
-    cx2 = cx1;
-    cx1 = cv;
+    c1 = cv;
     r2 = r1;
     r1 = rt;
     pAm = pAu;

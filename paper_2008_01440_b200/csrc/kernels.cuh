@@ -839,134 +839,6 @@ csr_kernel(CsrGeom g, const double* __restrict__ x, Epi epi, Reduce red) {
 
 // ----------------------------------------------------------------- CSR, TMA-pipelined
 
-// Tiles of <= kCsr2Rows consecutive rows whose nnz fit kCsr2Nnz (host-built
-// table). A persistent CTA double-buffers tiles: one elected thread bulk-copies
-// (cp.async.bulk, TMA) the next tile's values and column indices into shared
-// memory while the CTA works on the current one; each row-thread then sums
-// va[k] * (d[c] * x[c]) over its row sequentially in column order
-// (linop.cpp:183-185 -> bitwise rows), with the gathers issued in batches, and
-// runs the epilogue.
-constexpr int kCsr2Rows = 128;
-constexpr int kCsr2Nnz = 3072;                 // nnz budget per tile
-constexpr int kCsr2Buf = kCsr2Nnz + 8;         // + alignment slack (copies start at k & ~3)
-constexpr int kCsr2Batch = 8;
-constexpr size_t kCsr2Smem = 2 * ((size_t)kCsr2Buf * 8 + (size_t)kCsr2Buf * 4) + 2 * 8 + 128;
-
-struct Csr2Geom {
-  int n;
-  int ntiles;
-  const int* tile_row;   // ntiles + 1
-  const int* row_ptr;
-  const int* col_idx;    // padded by >= 8 entries
-  const double* values;  // padded by >= 8 entries
-  const double* dvec;
-};
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_init2(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(b)))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx2(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(b))),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait2(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n.reg .pred P1;\nW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra W_%=;\n}\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(b))),
-      "r"(parity)
-      : "memory");
-}
-
-template <class Epi, bool kRed>
-__global__ void __launch_bounds__(kCsr2Rows, 2)
-csr2_kernel(Csr2Geom g, const double* __restrict__ x, Epi epi, Reduce red) {
-  extern __shared__ __align__(128) unsigned char smem2[];
-  unsigned char* base = smem2 + ((128u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem2)) & 127u)) & 127u);
-  // stage st: values at base + st * kCsr2Buf * 8, column indices after both value stages
-  auto sva = [&](int st) { return reinterpret_cast<double*>(base + (size_t)st * kCsr2Buf * 8); };
-  auto sci = [&](int st) {
-    return reinterpret_cast<int*>(base + 2 * (size_t)kCsr2Buf * 8 + (size_t)st * kCsr2Buf * 4);
-  };
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 2 * (size_t)kCsr2Buf * 12);
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    mbar_init2(&bar[0]);
-    mbar_init2(&bar[1]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int t, int st) {
-    const int r0 = __ldg(g.tile_row + t), r1 = __ldg(g.tile_row + t + 1);
-    const int k0 = __ldg(g.row_ptr + r0) & ~3, k1 = __ldg(g.row_ptr + r1);
-    const int len = (k1 - k0 + 3) & ~3;  // multiple of 4 entries: 16-byte multiple for both arrays
-    mbar_arrive_tx2(&bar[st], (unsigned)len * 12u);
-    bulk_g2s(sva(st), g.values + k0, (unsigned)len * 8u, &bar[st]);
-    bulk_g2s(sci(st), g.col_idx + k0, (unsigned)len * 4u, &bar[st]);
-  };
-  double acc = 0.0;
-  int it = 0;
-  if (tid == 0 && (int)blockIdx.x < g.ntiles) issue(blockIdx.x, 0);
-  for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++it) {
-    const int st = it & 1;
-    if (tid == 0 && t + (int)gridDim.x < g.ntiles) issue(t + gridDim.x, st ^ 1);
-    const int r0 = __ldg(g.tile_row + t), r1 = __ldg(g.tile_row + t + 1);
-    const int nz0 = __ldg(g.row_ptr + r0), nz1 = __ldg(g.row_ptr + r1);
-    const int kb = nz0 & ~3;
-    const int row = r0 + tid;
-    // the row's own operands first (independent of the tile data)
-    double ev[2] = {0.0, 0.0};
-    double xr = 0.0, dr = 0.0;
-    int mb = 0, me = 0;
-    if (row < r1) {
-      epi.ld(row, ev);
-      xr = __ldg(x + row);
-      dr = __ldg(g.dvec + row);
-      mb = __ldg(g.row_ptr + row);
-      me = __ldg(g.row_ptr + row + 1);
-    }
-    mbar_wait2(&bar[st], (unsigned)(it >> 1) & 1u);
-    const double* va = sva(st) - kb;  // index by global k
-    const int* ci = sci(st) - kb;
-    // each row-thread walks its own row in column order: column indices and
-    // values from shared memory, the x / d gathers in batches (coalesced across
-    // the warp for stencil-structured rows), the sum strictly sequential
-    if (row < r1) {
-      double sum = 0.0;
-      for (int k = mb; k < me; k += kCsr2Batch) {
-        double dxv[kCsr2Batch], xv[kCsr2Batch], vv[kCsr2Batch];
-#pragma unroll
-        for (int q = 0; q < kCsr2Batch; ++q) {
-          const int kk = k + q;
-          const int c = kk < me ? ci[kk] : 0;
-          vv[q] = kk < me ? va[kk] : 0.0;
-          dxv[q] = __ldg(g.dvec + c);
-          xv[q] = __ldg(x + c);
-        }
-#pragma unroll
-        for (int q = 0; q < kCsr2Batch; ++q)
-          if (k + q < me) sum = sum + vv[q] * (dxv[q] * xv[q]);
-      }
-      const double y = sum * dr;
-      const double cst = epi.st(row, y, xr, ev);
-      if (kRed) acc = acc + cst;
-    }
-    __syncthreads();  // stage st free for reuse
-  }
-  if (kRed) block_reduce_finish(acc, red);
-}
-
 
 // ----------------------------------------------------------------- SELL-32 (sliced ELLPACK)
 

@@ -51,6 +51,70 @@ using namespace pcgx;
 
 // An instantiated CUDA graph of one speculative PCG segment and what one replay
 // launches (kernels and all-reduces are counted per replay).
+inline int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// Library switches: A/B and test knobs whose defaults are the production path.
+// Read from the environment ONCE, when an operator (or a context) is created, into
+// this snapshot; kernels, launches and solves read the snapshot, never the
+// environment. Names: PCGX_<FIELD> in upper case (see from_env).
+struct Tuning {
+  // operator storage / kernel choice (CSR detection, grid-tile and TMA kernels)
+  int dia = 1, dia3 = 1, dia3_kz = 0, dia_bps = 0, bsr = 1, bsr_bps = 16, sell_bps = 8;
+  int dia3t = 1, dia3t_dir = 1, dia3t_first = 1, dia3t_kz = 32;
+  int bsr3t = 1, bsr3t_modes = 1, bsr3t_kz = 32;
+  int csr_stencil = 0;
+  // stencil kernels
+  int kz = 0, kz2 = 32, pfd = 2, cheb2 = 1, cheb3 = 0, dir_tma = 1;
+  std::string c2plan;  // "" automatic chunk plan, "u" uniform kz2, "h1,h2,..." explicit
+  // PCG schedule
+  int fuse_upd = 1, no_graph = 0, graph_multi = 0, merged = 0, cond_graph = 1, no_fuse_p = 0, zdiv = 1,
+      defer_x = 1, snap_memcpy = 0, step_reps = 20;
+  // vector kernels
+  int upd2 = 1, upd_bps = 8;
+  static Tuning from_env() {
+    Tuning t;
+    auto g = [](const char* n, int& v) { v = env_int(n, v); };
+    g("PCGX_DIA", t.dia);
+    g("PCGX_DIA3", t.dia3);
+    g("PCGX_DIA3_KZ", t.dia3_kz);
+    g("PCGX_DIA_BPS", t.dia_bps);
+    g("PCGX_BSR", t.bsr);
+    g("PCGX_BSR_BPS", t.bsr_bps);
+    g("PCGX_SELL_BPS", t.sell_bps);
+    g("PCGX_DIA3T", t.dia3t);
+    g("PCGX_DIA3T_DIR", t.dia3t_dir);
+    g("PCGX_DIA3T_FIRST", t.dia3t_first);
+    g("PCGX_DIA3T_KZ", t.dia3t_kz);
+    g("PCGX_BSR3T", t.bsr3t);
+    g("PCGX_BSR3T_MODES", t.bsr3t_modes);
+    g("PCGX_BSR3T_KZ", t.bsr3t_kz);
+    g("PCGX_CSR_STENCIL", t.csr_stencil);
+    g("PCGX_KZ", t.kz);
+    g("PCGX_KZ2", t.kz2);
+    g("PCGX_PFD", t.pfd);
+    g("PCGX_CHEB2", t.cheb2);
+    g("PCGX_CHEB3", t.cheb3);
+    g("PCGX_DIR_TMA", t.dir_tma);
+    if (const char* e = std::getenv("PCGX_C2PLAN")) t.c2plan = e;
+    g("PCGX_FUSE_UPD", t.fuse_upd);
+    g("PCGX_NO_GRAPH", t.no_graph);
+    g("PCGX_GRAPH_MULTI", t.graph_multi);
+    g("PCGX_MERGED", t.merged);
+    g("PCGX_COND_GRAPH", t.cond_graph);
+    g("PCGX_NO_FUSE_P", t.no_fuse_p);
+    g("PCGX_ZDIV", t.zdiv);
+    g("PCGX_DEFER_X", t.defer_x);
+    g("PCGX_SNAP_MEMCPY", t.snap_memcpy);
+    g("PCGX_STEP_REPS", t.step_reps);
+    g("PCGX_UPD2", t.upd2);
+    g("PCGX_UPD_BPS", t.upd_bps);
+    return t;
+  }
+};
+
 struct Graph {
   cudaGraphExec_t exec = nullptr;
   int64_t kernels = 0;
@@ -65,6 +129,7 @@ std::atomic<uint64_t> g_op_uid{1};
 
 struct pcgx_context_s {
   int device = 0;
+  Tuning tune;  // environment snapshot at creation (vector-kernel knobs)
   int rank = 0, nranks = 1;
   int sms = 148;
   cudaStream_t s = nullptr;   // compute
@@ -111,6 +176,7 @@ struct pcgx_context_s {
 
 struct pcgx_operator_s {
   pcgx_context ctx = nullptr;
+  Tuning tune;  // environment snapshot at creation: every switch its launches and solves read
   uint64_t uid = g_op_uid.fetch_add(1);  // never reused (graph-cache key)
   int kind = 0;  // 0 stencil7, 1 csr
   long long n_global = 0, n_local = 0, nnz = 0;
@@ -122,8 +188,7 @@ struct pcgx_operator_s {
   int kz = 16;
   bool vec2 = false;  // even nx -> stencil7v2_kernel
   int pfd = 0;        // L2 prefetch distance (planes) of the v2 march
-  bool cheb2 = false; // two Chebyshev steps per pass (stencil7_cheb2_kernel, TMA)
-  int cheb2v = 0;     // its stage-2 variant (kV): 0 tile rows, 1 own row, 2 own row + d*x queues, 3 pipelined
+  bool cheb2 = false; // two Chebyshev steps per pass (stencil7_cheb2f_kernel, TMA)
   std::string c2plan;                     // PCGX_C2PLAN: "" auto, "u" uniform kz2, "h1,h2,..." explicit
   std::map<int, ChunkPlan> c2plans;       // chunk plan per launch span (planes)
   std::map<int, ChunkPlan> dirplans;      // the same for the direction step
@@ -131,11 +196,10 @@ struct pcgx_operator_s {
   std::map<int, ChunkPlan> c3plans;       // chunk plans of the three-step pass
   int zpad = 0;       // ghost planes per side in the workspace vectors (z-slab + cheb2: 2)
   int kz2 = 32;       // z-chunk of the two-step kernel
-  struct TmaPair { const double* ptr; CUtensorMap a, e, fa, fe; };
-  std::vector<TmaPair> tmaps;  // per-buffer tensor maps (A box 68x12, B/R box 68x10; f: the
-                               // pipelined two-step kernel's 68 x (kFTY+4), 68 x (kFTY+2))
+  struct TmaPair { const double* ptr; CUtensorMap fa, fe; };
+  std::vector<TmaPair> tmaps;  // per-buffer tensor maps: the two-step kernel's A box 68 x (kFTY+4)
+                               // and B / R / direction-step box 68 x (kFTY+2)
   // csr
-  int* tile_row = nullptr;  // csr2 tiles (ntiles + 1), nullptr -> csr_kernel
   // SELL-32 layout (sell_kernel, the default CSR path)
   long long* sell_ptr = nullptr;
   int* sell_len = nullptr;
@@ -175,7 +239,6 @@ struct pcgx_operator_s {
   std::vector<int> nb_rank;                // neighbours with traffic
   std::vector<long long> send_off, send_cnt, recv_off, recv_cnt;
   int sl_b0 = 0, sl_b1 = 0;                // slices [sl_b0, sl_b1) read no ghost column
-  int ntiles = 0;
   int *rp = nullptr, *ci = nullptr;
   double *va = nullptr, *dvec = nullptr;
   std::atomic<uint64_t> matvecs{0};
@@ -235,11 +298,6 @@ const Nccl& nccl() {
   }();
   if (!n.ok) fail(PCGX_ERR_NCCL, n.why);
   return n;
-}
-
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
 }
 
 #define PCGX_NCCL(call)                                                                   \
@@ -317,7 +375,9 @@ void ensure_workspace(pcgx_context c, long long n, long long pad = 0) {
     double* raw = nullptr;
     const size_t tot = (size_t)std::max(n, 1LL) + 2 * (size_t)pad;
     PCGX_CUDA(cudaMalloc(&raw, sizeof(double) * tot));
-    if (pad) PCGX_CUDA(cudaMemset(raw, 0, sizeof(double) * tot));
+    // zeroed on the compute stream: a legacy-stream memset is unordered with the
+    // (non-blocking) compute stream and could land after the first kernels
+    if (pad) PCGX_CUDA(cudaMemsetAsync(raw, 0, sizeof(double) * tot, c->s));
     *b = raw + pad;
   }
   c->ws_n = n;
@@ -511,7 +571,8 @@ struct HostComm : CommBase {
       sum[i] = v;
     }
     barrier();
-    PCGX_CUDA(cudaMemcpy(c->S + slot, sum, sizeof(double) * count, cudaMemcpyHostToDevice));
+    PCGX_CUDA(cudaMemcpyAsync(c->S + slot, sum, sizeof(double) * count, cudaMemcpyHostToDevice, c->s));
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
   }
   void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override {
     (void)op;
@@ -532,11 +593,13 @@ struct HostComm : CommBase {
     for (int i = 0; i < n; ++i) {  // rank-1's top -> my recv_lo, rank+1's bottom -> my recv_hi
       const size_t b = sizeof(double) * (size_t)items[i].count;
       if (rank > 0 && items[i].recv_lo)
-        PCGX_CUDA(cudaMemcpy(items[i].recv_lo, box(rank - 1) + off + items[i].count, b, cudaMemcpyHostToDevice));
+        PCGX_CUDA(cudaMemcpyAsync(items[i].recv_lo, box(rank - 1) + off + items[i].count, b,
+                                  cudaMemcpyHostToDevice, c->s));
       if (rank < nranks - 1 && items[i].recv_hi)
-        PCGX_CUDA(cudaMemcpy(items[i].recv_hi, box(rank + 1) + off, b, cudaMemcpyHostToDevice));
+        PCGX_CUDA(cudaMemcpyAsync(items[i].recv_hi, box(rank + 1) + off, b, cudaMemcpyHostToDevice, c->s));
       off += 2 * (size_t)items[i].count;
     }
+    PCGX_CUDA(cudaStreamSynchronize(c->s));  // the peers may refill their outboxes after the barrier
     barrier();
   }
   void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override {
@@ -576,9 +639,10 @@ struct HostComm : CommBase {
       if (qcnt != op->recv_cnt[i]) fail(PCGX_ERR_NCCL, "host comm: block-row segment size mismatch");
       for (int v = 0; v < nv; ++v)
         if (qcnt)
-          PCGX_CUDA(cudaMemcpy(gbuf[v] + op->recv_off[i], box(q) + qoff + (size_t)v * qcnt,
-                               sizeof(double) * qcnt, cudaMemcpyHostToDevice));
+          PCGX_CUDA(cudaMemcpyAsync(gbuf[v] + op->recv_off[i], box(q) + qoff + (size_t)v * qcnt,
+                                    sizeof(double) * qcnt, cudaMemcpyHostToDevice, c->s));
     }
+    PCGX_CUDA(cudaStreamSynchronize(c->s));
     barrier();
   }
   bool graph_capturable() const override { return false; }
@@ -868,7 +932,7 @@ int halo_vecs(const InComb& in, const double** xs) {
 // request (PCGX_DIA3=2) — at cfg1's L2-resident 100^3 the row-thread kernel is 2x
 // faster, its seven gathers hit L2.
 bool dia3_on(pcgx_operator op) {
-  const int e = env_int("PCGX_DIA3", 1);
+  const int e = op->tune.dia3;
   return (op->dia3_pat == 27 && e >= 1) || (op->dia3_pat == 7 && e >= 2);
 }
 
@@ -918,7 +982,7 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
       const int tiles = ((g3.nx + kD3X - 1) / kD3X) * ((g3.nx + kD3Y - 1) / kD3Y);
       // z-chunks: about 8 waves of 3 resident CTAs per SM, at least 8 planes each
       const int want = std::max(1, (c->sms * 3 * 8 + tiles - 1) / tiles);
-      g3.kz = std::max(env_int("PCGX_DIA3_KZ", 0) > 0 ? env_int("PCGX_DIA3_KZ", 0) : (g3.nx + want - 1) / want,
+      g3.kz = std::max(op->tune.dia3_kz > 0 ? op->tune.dia3_kz : (g3.nx + want - 1) / want,
                        std::min(8, g3.nx));
       const dim3 grid3(tiles, (g3.nx + g3.kz - 1) / g3.kz);
       if (kRed) check_red_grid(nblocks_of(grid3));
@@ -945,7 +1009,7 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
       occ_cache.store(occ, std::memory_order_relaxed);
     }
     const long long want = (op->n_local + 255) / 256;
-    const int bps = env_int("PCGX_DIA_BPS", 0);
+    const int bps = op->tune.dia_bps;
     const int grid = (int)std::max(1LL, std::min(want, (long long)c->sms * (bps > 0 ? bps : occ)));
     Reduce red = kRed ? make_red(c, slot) : Reduce{};
     kern<<<grid, 256, 0, c->s>>>(g, in, epi, red);
@@ -963,7 +1027,7 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
                op->bsr_val, op->dvec};
     const int wpb = 8;
     const int want = (op->bsr_slices + wpb - 1) / wpb;
-    const int grid = std::max(1, std::min(want, c->sms * env_int("PCGX_BSR_BPS", 16)));
+    const int grid = std::max(1, std::min(want, c->sms * op->tune.bsr_bps));
     Reduce red = kRed ? make_red(c, slot) : Reduce{};
     bsr3_kernel<In, Epi, kRed><<<grid, 32 * wpb, 0, c->s>>>(g, in, epi, red);
     check_launch();
@@ -977,7 +1041,7 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
                  op->sell_val, op->dvec};
       const int wpb = 8;
       const int want = (s1 - s0 + wpb - 1) / wpb;
-      const int grid = std::max(1, std::min(want, c->sms * env_int("PCGX_SELL_BPS", 8)));
+      const int grid = std::max(1, std::min(want, c->sms * op->tune.sell_bps));
       Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
       sell_kernel<In, Epi, kRed><<<grid, 32 * wpb, 0, c->s>>>(g, in, epi, red);
       check_launch();
@@ -1010,21 +1074,10 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
     return;
   }
   if constexpr (std::is_same_v<In, InVec>) {
-    if (op->kind == 1 && op->tile_row) {
-      Csr2Geom g{(int)op->n_local, op->ntiles, op->tile_row, op->rp, op->ci, op->va, op->dvec};
-      PCGX_CUDA(cudaFuncSetAttribute(csr2_kernel<Epi, kRed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kCsr2Smem));
-      const int grid = std::max(1, std::min(op->ntiles, c->sms * env_int("PCGX_CSR2_BPS", 2)));
-      Reduce red = kRed ? make_red(c, slot) : Reduce{};
-      csr2_kernel<Epi, kRed><<<grid, kCsr2Rows, kCsr2Smem, c->s>>>(g, in.x, epi, red);
-      check_launch();
-      count_launch(c);
-      return;
-    }
     if (op->kind == 1) {
       CsrGeom g{(int)op->n_local, op->rp, op->ci, op->va, op->dvec};
       const int nrb = (int)((op->n_local + kCsrRows - 1) / kCsrRows);
-      const int grid = std::max(1, std::min(nrb, c->sms * env_int("PCGX_CSR_BPS", 12)));
+      const int grid = std::max(1, std::min(nrb, c->sms * 12));
       Reduce red = kRed ? make_red(c, slot) : Reduce{};
       csr_kernel<Epi, kRed><<<grid, kCsrRows, 0, c->s>>>(g, in.x, epi, red);
       check_launch();
@@ -1085,7 +1138,7 @@ void launch_update(pcgx_context c, long long n, double* x, double* r, const doub
                    const double* q, int s_rho, int s_pq, int s_rr, int zm, double theta, double* z) {
   auto al16 = [](const void* v) { return ((uintptr_t)v & 15u) == 0; };
   const bool vec = (n % 2 == 0) && al16(x) && al16(r) && al16(p) && al16(q) && al16(z) &&
-                   env_int("PCGX_UPD2", 1) != 0;
+                   c->tune.upd2 != 0;
   const bool dox = x != nullptr;
   if (!vec) {
     update_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, r, p, q, c->S, s_rho, s_pq,
@@ -1093,7 +1146,7 @@ void launch_update(pcgx_context c, long long n, double* x, double* r, const doub
     return;
   }
   const long long n2 = n / 2;
-  const int bps = env_int("PCGX_UPD_BPS", 8);
+  const int bps = c->tune.upd_bps;
   const int grid = (int)std::max(1LL, std::min((n2 + kVecThreads - 1) / kVecThreads, (long long)c->sms * bps));
   auto d2 = [](const double* v) { return reinterpret_cast<double2*>(const_cast<double*>(v)); };
 #define PCGX_UPD(ZM, X)                                                                          \
@@ -1186,9 +1239,7 @@ using TmaPair = pcgx_operator_s::TmaPair;
 const TmaPair& tmaps_for(pcgx_operator op, const double* ptr) {
   for (auto& t : op->tmaps)
     if (t.ptr == ptr) return t;
-  TmaPair t{ptr, make_map(op, ptr, kC2AX, kC2AY), make_map(op, ptr, kC2BX, kC2BY), {}, {}};
-  t.fa = kFAY == kC2AY ? t.a : make_map(op, ptr, kFW, kFAY);
-  t.fe = kFBY == kC2BY ? t.e : make_map(op, ptr, kFW, kFBY);
+  TmaPair t{ptr, make_map(op, ptr, kFW, kFAY), make_map(op, ptr, kFW, kFBY)};
   op->tmaps.push_back(t);
   return op->tmaps.back();
 }
@@ -1248,12 +1299,12 @@ bool dia3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
   const int nx = op->dia3_nx;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
   auto clash = [&](const double* o) { return o && (o == ex || o == ep || o == er); };
-  if (!dia3_on(op) || op->dia3_pat != 27 || env_int("PCGX_DIA3T", 1) == 0 || nx % 4 != 0 || nx < kT3PX ||
+  if (!dia3_on(op) || op->dia3_pat != 27 || op->tune.dia3t == 0 || nx % 4 != 0 || nx < kT3PX ||
       ghosts || !al16(ex) || (ep && !al16(ep)) || (er && !al16(er)) || !al16(eout) || (eout2 && !al16(eout2)) ||
       (exo && !al16(exo)) || clash(eout) || clash(eout2))
     return false;
-  if (kDir && env_int("PCGX_DIA3T_DIR", 1) == 0) return false;
-  if (kFirst && env_int("PCGX_DIA3T_FIRST", 1) == 0) return false;
+  if (kDir && op->tune.dia3t_dir == 0) return false;
+  if (kFirst && op->tune.dia3t_first == 0) return false;
   Dia3tMaps maps;
   maps.val = dia3t_map(op, op->dia_val, 3);
   maps.mask = dia3t_map(op, op->dia_mask, 2);
@@ -1262,7 +1313,7 @@ bool dia3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
   maps.x = dia3t_map(op, ex, 1);
   maps.d = dia3t_map(op, op->dvec, 1);
   maps.p = ep ? dia3t_map(op, ep, 1) : maps.x;
-  const int kz = std::max(1, env_int("PCGX_DIA3T_KZ", 32));  // 8: -3%, 16: -1.5% at 256^3
+  const int kz = std::max(1, op->tune.dia3t_kz);  // 8: -3%, 16: -1.5% at 256^3
   const int tiles = ((nx + kD3X - 1) / kD3X) * ((nx + kD3Y - 1) / kD3Y);
   const dim3 grid(tiles, (nx + kz - 1) / kz);
   static std::atomic<uint64_t> attr{0};  // per device: the attribute is set per device
@@ -1355,11 +1406,11 @@ bool bsr3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
   const int nx = op->b3g_nx;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
   auto clash = [&](const double* o) { return o && (o == ex || o == ep || o == er); };
-  if (!op->b3g_val || env_int("PCGX_BSR3T", 1) == 0 || ghosts || !al16(ex) || (ep && !al16(ep)) ||
+  if (!op->b3g_val || op->tune.bsr3t == 0 || ghosts || !al16(ex) || (ep && !al16(ep)) ||
       (er && !al16(er)) || !al16(eout) || (eout2 && !al16(eout2)) || (exo && !al16(exo)) || clash(eout) ||
       clash(eout2))
     return false;
-  if ((kDir || kFirst) && env_int("PCGX_BSR3T_MODES", 1) == 0) return false;
+  if ((kDir || kFirst) && op->tune.bsr3t_modes == 0) return false;
   Bsr3tMaps maps;
   maps.val = bsr3t_map(op, op->b3g_val, 20);
   maps.mask = bsr3t_map(op, op->b3g_mask, 21);
@@ -1368,7 +1419,7 @@ bool bsr3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
   maps.x = bsr3t_map(op, ex, 23);
   maps.d = bsr3t_map(op, op->dvec, 23);
   maps.p = ep ? bsr3t_map(op, ep, 23) : maps.x;
-  const int kz = std::max(1, env_int("PCGX_BSR3T_KZ", 32));
+  const int kz = std::max(1, op->tune.bsr3t_kz);
   const int tiles = ((nx + kB3X - 1) / kB3X) * ((nx + kB3Y - 1) / kB3Y);
   const dim3 grid(tiles, (nx + kz - 1) / kz);
   static std::atomic<uint64_t> attr{0};  // per device: the attribute is set per device
@@ -1481,44 +1532,17 @@ ChunkPlan make_chunk_plan(const std::string& spec, int span, int kz, long long t
     const long long maxn = std::max(1LL, (long long)kMaxBlocks / tiles);
     hs = uniform((int)((span + maxn - 1) / maxn));
   }
-  if (env_int("PCGX_C2PLAN_DEBUG", 0)) {
-    std::fprintf(stderr, "[pcgx] two-step chunk plan span=%d tiles=%lld slots=%lld:", span, tiles, slots);
-    for (int h : hs) std::fprintf(stderr, " %d", h);
-    std::fprintf(stderr, "\n");
-  }
   return pack(hs);
-}
-
-template <bool kFirst, bool kRed, int kV>
-void cheb2_launch_v(pcgx_context c, pcgx_operator op, const double* A, const double* B,
-                  const double* R, const Cheb2Params& prm, int slot, int k_begin, int k_end, int kz,
-                  bool accumulate) {
-  if (k_end <= k_begin) return;
-  PCGX_CUDA(cudaFuncSetAttribute(stencil7_cheb2_kernel<kFirst, kRed, kV>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2Smem));
-  // copies: a later tmaps_for() may grow the cache and move its elements
-  const CUtensorMap ma = tmaps_for(op, A).a;
-  const CUtensorMap mb = tmaps_for(op, B ? B : A).e;
-  const CUtensorMap mr = tmaps_for(op, R).e;
-  kz = std::max(1, std::min(kz, k_end - k_begin));
-  dim3 grid((unsigned)((op->nx + kC2TX - 1) / kC2TX), (unsigned)((op->ny + kC2TY - 1) / kC2TY),
-            (unsigned)((k_end - k_begin + kz - 1) / kz));
-  if (kRed) check_red_grid(nblocks_of(grid));
-  Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
-  stencil7_cheb2_kernel<kFirst, kRed, kV><<<grid, kC2Threads, kC2Smem, c->s>>>(ma, mb, mr, prm, k_begin,
-                                                                               k_end, kz, red);
-  check_launch();
-  count_launch(c);
 }
 
 template <bool kFirst, bool kRed>
 void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const double* B,
                   const double* R, const Cheb2Params& prm, int slot, int k_begin, int k_end, int kz,
                   bool accumulate) {
-  if (op->cheb2v >= 3) {
+  (void)kz;
+  {
     if (k_end <= k_begin) return;
-    auto kern = op->cheb2v == 4 ? stencil7_cheb2f_kernel<kFirst, kRed, true>
-                                : stencil7_cheb2f_kernel<kFirst, kRed, false>;
+    auto kern = stencil7_cheb2f_kernel<kFirst, kRed>;
     PCGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2FSmem));
     const CUtensorMap ma = tmaps_for(op, A).fa;
     const CUtensorMap mb = tmaps_for(op, B ? B : A).fe;
@@ -1539,12 +1563,6 @@ void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const doubl
                                                                                   k_end, plan, red, Reduce{});
     check_launch();
     count_launch(c);
-    return;
-  }
-  switch (op->cheb2v) {
-    case 0: cheb2_launch_v<kFirst, kRed, 0>(c, op, A, B, R, prm, slot, k_begin, k_end, kz, accumulate); break;
-    case 1: cheb2_launch_v<kFirst, kRed, 1>(c, op, A, B, R, prm, slot, k_begin, k_end, kz, accumulate); break;
-    default: cheb2_launch_v<kFirst, kRed, 2>(c, op, A, B, R, prm, slot, k_begin, k_end, kz, accumulate); break;
   }
 }
 
@@ -1554,7 +1572,7 @@ void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const doubl
 bool dir_tma_ok(pcgx_operator op) {
   const bool ghosts = op->ghost_lo || op->ghost_hi;
   return op->kind == 0 && op->vec2 && op->cheb2 && (!ghosts || op->zpad >= 1) &&
-         env_int("PCGX_DIR_TMA", 1) != 0;
+         op->tune.dir_tma != 0;
 }
 
 void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const double* pold,
@@ -1563,10 +1581,10 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
   op->matvecs.fetch_add(1, std::memory_order_relaxed);
   PCGX_CUDA(cudaFuncSetAttribute(stencil7_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kDirSmem));
-  static_assert(kDBY == kFBY || kDBY == kC2BY, "direction-step box rows: no tensor map of that shape");
-  const CUtensorMap mz = kDBY == kFBY ? tmaps_for(op, z).fe : tmaps_for(op, z).e;
+  static_assert(kDBY == kFBY, "direction-step box rows: no tensor map of that shape");
+  const CUtensorMap mz = tmaps_for(op, z).fe;
   const CUtensorMap mx = (kDirXTma && x && !first) ? xtile_map(op, x) : mz;  // unused unless x is updated
-  const CUtensorMap mp = kDBY == kFBY ? tmaps_for(op, first ? z : pold).fe : tmaps_for(op, first ? z : pold).e;
+  const CUtensorMap mp = tmaps_for(op, first ? z : pold).fe;
   const int nzl = (int)op->nzl;
   const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
   DirParams prm{(int)op->nx, (int)op->ny, nzl, lo ? -1 : 0, hi ? nzl + 1 : nzl, op->zpad,
@@ -1674,8 +1692,8 @@ struct CgUpd {
 };
 
 bool cheb_upd_ok(pcgx_context c, pcgx_operator op, int m) {
-  return m >= 3 && op->kind == 0 && op->cheb2 && op->cheb2v >= 3 && !c->cm && op->zpad == 0 &&
-         env_int("PCGX_FUSE_UPD", 1) != 0;
+  return m >= 3 && op->kind == 0 && op->cheb2 && !c->cm && op->zpad == 0 &&
+         op->tune.fuse_upd != 0;
 }
 
 void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Params prm) {
@@ -1690,7 +1708,7 @@ void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Pa
   prm.s_rho = u.s_rho;
   prm.s_pq = u.s_pq;
   prm.rout = u.rnew;
-  auto kern = stencil7_cheb2f_kernel<true, false, false, true>;
+  auto kern = stencil7_cheb2f_kernel<true, false, true>;
   PCGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC2FSmem));
   const CUtensorMap ma = tmaps_for(op, u.rold).fa;
   const CUtensorMap mq = tmaps_for(op, u.q).fa;
@@ -1816,7 +1834,7 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
     const bool last12 = (P.m == 2);
     q.rk2 = P.rho[2];
     q.rk2m1 = P.rho[1];
-    q.outC = (last12 && op->cheb2v >= 3) ? nullptr : bufs[0];  // x_1 is dead after a last pass
+    q.outC = last12 ? nullptr : bufs[0];  // x_1 is dead after a last pass
     q.outE = last12 ? out : bufs[1];
     if (upd) cheb2f_upd_launch(c, op, *upd, q);
     else if (last12 && rz_slot >= 0) cheb2_pass<true, true>(c, op, r, nullptr, r, q, rz_slot);
@@ -1885,7 +1903,7 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
       q.rk1m1 = P.rho[k - 1];
       q.rk2 = P.rho[k + 1];
       q.rk2m1 = P.rho[k];
-      q.outC = last && op->cheb2v >= 3 ? nullptr : bufs[fc];
+      q.outC = last ? nullptr : bufs[fc];
       q.outE = last ? out : bufs[fe];
       if (last && rz_slot >= 0) cheb2_pass<false, true>(c, op, bufs[icur], bufs[iold], r, q, rz_slot);
       else cheb2_pass<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1);
@@ -2207,7 +2225,7 @@ double matrix_bytes(pcgx_operator op) {
   if (op->kind == 0) return 0.0;
   // the grid copy the regular steps stream (bsr3t_kernel): every slot of every node
   // (absent blocks as zeros) + the masks; the other launches' SELL arrays are ~4% larger
-  if (op->b3g_val && env_int("PCGX_BSR3T", 1) != 0)
+  if (op->b3g_val && op->tune.bsr3t != 0)
     return 8.0 * 243.0 * (double)(op->n_local / 3) + 4.0 * (double)(op->n_local / 3);
   if (op->bsr_ptr)
     return 8.0 * (double)op->nnz + 4.0 * (double)op->bsr_blocks + 4.0 * (double)(op->n_local / 3 + 1);
@@ -2245,16 +2263,16 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // CUDA graphs on one GPU; multi-rank solves launch directly by default (the
   // speculative schedule hides the launches either way; PCGX_GRAPH_MULTI=1 captures
   // the NCCL plane exchanges and all-reduces into the graphs too)
-  const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && env_int("PCGX_NO_GRAPH", 0) == 0 &&
-                         (!c->cm || (c->cm->graph_capturable() && env_int("PCGX_GRAPH_MULTI", 0) != 0));
+  const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && op->tune.no_graph == 0 &&
+                         (!c->cm || (c->cm->graph_capturable() && op->tune.graph_multi != 0));
   // one GPU: snapshot r'r right after the update and overlap the host check with
   // the speculative P r; multi-GPU: merge [r'r, r'z] into one all-reduce after P r
   // (PCGX_MERGED=1 forces the multi-GPU schedule on one GPU, for tests)
-  const bool spec_after_update = !c->cm && env_int("PCGX_MERGED", 0) == 0;
+  const bool spec_after_update = !c->cm && op->tune.merged == 0;
   // one GPU with graphs: the speculative tail of each segment (P r and A p of the
   // next iteration) sits in a conditional IF node that a device-side convergence
   // test closes, so nothing is computed and discarded at convergence
-  const bool use_cond = use_graph && spec_after_update && env_int("PCGX_COND_GRAPH", 1) != 0;
+  const bool use_cond = use_graph && spec_after_update && op->tune.cond_graph != 0;
 
   std::memset(rep, 0, sizeof *rep);
   c->cur_launches = 0;
@@ -2337,16 +2355,16 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // written by the update kernel), 2 = no preconditioner (z is r itself).
   const int zm = !have_prec ? 2 : (prec.kind == 1 && m == 0 ? 1 : 0);
   double* Pd[2] = {p, c->p2};  // direction ping-pong: p(it) lives in Pd[it & 1]
-  const bool fuse = fuses_dir_update(op) && env_int("PCGX_NO_FUSE_P", 0) == 0;
+  const bool fuse = fuses_dir_update(op) && op->tune.no_fuse_p == 0;
   // m = 0 on the TMA direction step: z = r / theta is formed there from r, never
   // stored (the update kernel only reduces r'z): 8 B less per unknown and iteration
-  const bool zdiv = zm == 1 && fuse && dir_tma_ok(op) && env_int("PCGX_ZDIV", 1) != 0;
+  const bool zdiv = zm == 1 && fuse && dir_tma_ok(op) && op->tune.zdiv != 0;
   const double* zvec = (zm == 2 || zdiv) ? r : z;
   // single-rank stencil: x += alpha p moves from the update kernel into the next
   // direction step, which reads p_old anyway (8 B less per unknown and iteration)
   // (not with on_iterate: x must be current at every iteration's callback)
   const bool cb = opts.on_iterate != nullptr;
-  const bool defer_x = fuse && dir_tma_ok(op) && env_int("PCGX_DEFER_X", 1) != 0 && !cb;
+  const bool defer_x = fuse && dir_tma_ok(op) && op->tune.defer_x != 0 && !cb;
   // one GPU, Chebyshev m >= 3 on the stencil: the update r -= alpha q, r'r rides in
   // the first two-step pass of P r (cheb2f_upd_launch); r(it) lives in Rb[it & 1]
   const bool fuse_upd = zm == 0 && prec.kind == 1 && spec_after_update && defer_x &&
@@ -2380,7 +2398,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   const double bytes_dir = fuse ? spmv_alg_bytes(op) + 2 * N8 : spmv_alg_bytes(op) + 3 * N8;
   // one rank: every scalar the host checks reached hS from its reducing kernel
   // (Reduce::mirror); several ranks: the all-reduced slots are copied
-  const bool snap_copy = c->cm != nullptr || env_int("PCGX_SNAP_MEMCPY", 0) != 0;
+  const bool snap_copy = c->cm != nullptr || op->tune.snap_memcpy != 0;
   auto snapshot = [&]() {  // External: when captured, the graph records ev_sync on every replay
     if (snap_copy)
       PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
@@ -2574,7 +2592,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // this solve's operator and buffers: the two-step pass (stencil, cheb2) or the
   // fused single middle step.
   if ((opts.flags & PCGX_FLAG_TIME_KERNELS) && prec.kind == 1 && m >= 4) {
-    const int reps = std::max(3, env_int("PCGX_STEP_REPS", 20));
+    const int reps = std::max(3, op->tune.step_reps);
     const bool two = (op->kind == 0 && op->cheb2);
     Cheb2Params q{};
     if (two) {
@@ -2872,8 +2890,7 @@ void init_stencil_ghosts(pcgx_context c, pcgx_operator op) {
 }
 
 int default_kz(pcgx_context c, long long nx, long long ny, long long nzl) {
-  const int env = env_int("PCGX_KZ", 0);
-  if (env > 0) return env;
+  (void)0;
   (void)c;
   (void)nx;
   (void)ny;
@@ -3190,7 +3207,7 @@ void build_dia(pcgx_operator op, long long n, const std::vector<int>& rp32,
 // host buffer at a time) so the host never holds a second full copy.
 void bsr3_grid_build(pcgx_operator op, long long n, const std::vector<int>& rp32,
                      const std::vector<int>& ci32, const double* va) {
-  if (env_int("PCGX_BSR3T", 1) == 0) return;
+  if (op->tune.bsr3t == 0) return;
   const long long nb = n / 3;
   long long nx = (long long)std::llround(std::cbrt((double)nb));
   while (nx * nx * nx > nb) --nx;
@@ -3341,10 +3358,9 @@ void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, c
     PCGX_CUDA(cudaMemcpy(op->va, va, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice));
   }
   if (n) PCGX_CUDA(cudaMemcpy(op->dvec, dv.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice));
-  const int ckern = env_int("PCGX_CSR_KERNEL", 0);  // 0 sell (default), 1 tma tiles, 2 chunked
   std::vector<int> doff;
   // offset storage moves fewer bytes than int32 CSR while 8 K n + 4 n < 12 nnz + 4 n
-  const bool dia = ckern == 0 && n > 0 && env_int("PCGX_DIA", 1) != 0 && dia_offsets(n, rp32, ci32, doff) &&
+  const bool dia = n > 0 && op->tune.dia != 0 && dia_offsets(n, rp32, ci32, doff) &&
                    (double)doff.size() * (double)n <= 1.5 * (double)nnz;
   if (dia) {
     build_dia(op, n, rp32, ci32, va, doff);
@@ -3352,40 +3368,19 @@ void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, c
     cudaFree(op->va);
     op->ci = nullptr;
     op->va = nullptr;
-  } else if (ckern == 0 && n > 0 && env_int("PCGX_BSR", 1) != 0 && is_bsr3(n, rp32, ci32)) {
+  } else if (n > 0 && op->tune.bsr != 0 && is_bsr3(n, rp32, ci32)) {
     build_bsr3(op, n, rp32, ci32, va);
     cudaFree(op->ci);
     cudaFree(op->va);
     op->ci = nullptr;
     op->va = nullptr;
-  } else if (ckern == 0 && n > 0) {
+  } else if (n > 0) {
     build_sell(op, n, rp32, ci32, va);
     // the SELL copy replaces the CSR value/index arrays on the device
     cudaFree(op->ci);
     cudaFree(op->va);
     op->ci = nullptr;
     op->va = nullptr;
-  }
-  // csr2 tiles: greedy, <= kCsr2Rows rows and <= kCsr2Nnz nnz (+3 alignment) each
-  if (ckern == 1 && n > 0) {
-    std::vector<int> tiles{0};
-    bool ok = true;
-    long long r = 0;
-    while (r < n) {
-      const long long start = r;
-      const long long k0 = (long long)rp32[(size_t)start] & ~3LL;
-      while (r < n && r - start < kCsr2Rows && (long long)rp32[(size_t)r + 1] - k0 <= kCsr2Nnz) ++r;
-      if (r == start) {  // one row longer than the tile budget: keep the chunked kernel
-        ok = false;
-        break;
-      }
-      tiles.push_back((int)r);
-    }
-    if (ok) {
-      op->ntiles = (int)tiles.size() - 1;
-      PCGX_CUDA(cudaMalloc(&op->tile_row, sizeof(int) * tiles.size()));
-      PCGX_CUDA(cudaMemcpy(op->tile_row, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice));
-    }
   }
 }
 
@@ -3399,7 +3394,6 @@ void free_op(pcgx_operator op) {
   cudaFree(op->ci);
   cudaFree(op->va);
   cudaFree(op->dvec);
-  cudaFree(op->tile_row);
   cudaFree(op->sell_ptr);
   cudaFree(op->sell_len);
   cudaFree(op->sell_col);
@@ -3421,6 +3415,7 @@ void free_op(pcgx_operator op) {
 }
 
 void ctx_init(pcgx_context c) {
+  c->tune = Tuning::from_env();
   PCGX_CUDA(cudaSetDevice(c->device));
   PCGX_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
   PCGX_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
@@ -3437,6 +3432,8 @@ void ctx_init(pcgx_context c) {
   PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming));
   PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  // the legacy-stream memsets above are unordered with the non-blocking streams
+  PCGX_CUDA(cudaDeviceSynchronize());
 }
 
 // The matrix-free 7-point operator's fields (frees op on failure).
@@ -3455,17 +3452,16 @@ void stencil_setup(pcgx_context c, pcgx_operator op, int64_t nx, int64_t ny, int
     op->nnz = 7 * op->n_global - 2 * (ny * nz + nx * nz + nx * ny);
     op->d = inv_sqrt_diag > 0.0 ? inv_sqrt_diag : 1.0 / std::sqrt(6.0);
     op->kz = default_kz(c, nx, ny, op->nzl);
-    op->vec2 = (nx % 2 == 0) && env_int("PCGX_STENCIL_SCALAR", 0) == 0;
-    op->pfd = env_int("PCGX_PFD", 2);
-    op->cheb2 = op->vec2 && env_int("PCGX_CHEB2", 1) != 0;
-    op->kz2 = env_int("PCGX_KZ2", 32);
-    op->cheb2v = env_int("PCGX_CHEB2V", 3);
-    if (const char* e = std::getenv("PCGX_C2PLAN")) op->c2plan = e;
+    op->vec2 = (nx % 2 == 0);
+    op->pfd = op->tune.pfd;
+    op->cheb2 = op->vec2 && op->tune.cheb2 != 0;
+    op->kz2 = op->tune.kz2;
+    op->c2plan = op->tune.c2plan;
     try {
       init_stencil_ghosts(c, op);
       if (c->nranks > 1 && op->nzl < 2) op->cheb2 = false;  // 2-plane halos need >= 2 planes
       op->zpad = (op->cheb2 && c->nranks > 1) ? 2 : 0;
-      op->cheb3 = op->cheb2 && op->cheb2v >= 3 && c->nranks == 1 && env_int("PCGX_CHEB3", 0) != 0;
+      op->cheb3 = op->cheb2 && c->nranks == 1 && op->tune.cheb3 != 0;
     } catch (...) {
       free_op(op);
       throw;
@@ -3513,7 +3509,7 @@ template <class I>
 void csr_create_any(pcgx_context c, pcgx_operator op, int64_t n, const I* rp, const I* ci, const double* va,
                     const double* isd) {
   int64_t nx = 0;
-  if (c->nranks == 1 && rp && ci && va && env_int("PCGX_CSR_STENCIL", 0) != 0 &&
+  if (c->nranks == 1 && rp && ci && va && op->tune.csr_stencil != 0 &&
       csr_is_lap3d(n, rp, ci, va, isd, &nx)) {
     stencil_setup(c, op, nx, nx, nx, 1.0 / std::sqrt(6.0));
     op->nnz = (int64_t)rp[n];
@@ -3771,7 +3767,9 @@ pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t
     if (nz < c->nranks) fail(PCGX_ERR_INVALID, "stencil7_create: fewer planes than ranks");
     auto op = new pcgx_operator_s();
     op->ctx = c;
+    op->tune = Tuning::from_env();
     stencil_setup(c, op, nx, ny, nz, inv_sqrt_diag);
+    PCGX_CUDA(cudaDeviceSynchronize());  // legacy-stream uploads / memsets before any compute-stream work
     *out = op;
   });
 }
@@ -3783,7 +3781,9 @@ pcgx_status pcgx_csr_create(pcgx_context c, int64_t n, const int64_t* row_ptr,
     set_device(c);
     auto op = new pcgx_operator_s();
     op->ctx = c;
+    op->tune = Tuning::from_env();
     csr_create_any(c, op, n, row_ptr, col_idx, values, inv_sqrt_diag);
+    PCGX_CUDA(cudaDeviceSynchronize());  // legacy-stream uploads / memsets before any compute-stream work
     *out = op;
   });
 }
@@ -3795,7 +3795,9 @@ pcgx_status pcgx_csr_create_i32(pcgx_context c, int64_t n, const int32_t* row_pt
     set_device(c);
     auto op = new pcgx_operator_s();
     op->ctx = c;
+    op->tune = Tuning::from_env();
     csr_create_any(c, op, n, row_ptr, col_idx, values, inv_sqrt_diag);
+    PCGX_CUDA(cudaDeviceSynchronize());  // legacy-stream uploads / memsets before any compute-stream work
     *out = op;
   });
 }
@@ -3818,10 +3820,10 @@ int64_t pcgx_operator_nnz(pcgx_operator op) { return op ? op->nnz : -1; }
 int pcgx_operator_storage(pcgx_operator op) {
   if (!op) return -1;
   if (op->kind == 0) return 0;
-  if (op->bsr_ptr) return op->b3g_val && env_int("PCGX_BSR3T", 1) != 0 ? 7 : 2;
+  if (op->bsr_ptr) return op->b3g_val && op->tune.bsr3t != 0 ? 7 : 2;
   if (op->dia_val) return dia3_on(op) ? 6 : 5;
   if (op->sell_ptr) return 1;
-  return op->tile_row ? 3 : 4;
+  return 4;  // the chunked CSR kernel: only an empty (n = 0) matrix has no other storage
 }
 uint64_t pcgx_operator_matvec_count(pcgx_operator op) { return op ? op->matvecs.load() : 0; }
 

@@ -513,17 +513,15 @@ def test_cfg4_160_full_size(P, ctx, monkeypatch):
 
 @pytest.mark.parametrize("dims", [(24, 24, 24), (66, 10, 9), (64, 8, 1), (130, 17, 33), (2, 2, 2),
                                   (130, 47, 41), (64, 61, 7)])
-@pytest.mark.parametrize("plan", [("3", "", "32"), ("3", "u", "1"), ("3", "u", "5"), ("3", "3,2,1,1", "7"),
-                                  ("0", "", "5"), ("0", "", "32")])
+@pytest.mark.parametrize("plan", [("", "32"), ("u", "1"), ("u", "5"), ("3,2,1,1", "7")])
 def test_cheb2_bitwise_vs_oracle(P, ctx, oracle, dims, plan, monkeypatch):
-    """The two-step kernels (pipelined stencil7_cheb2f_kernel: automatic chunk plan,
-    uniform chunks of kz planes, an explicit plan; round-1 stencil7_cheb2_kernel:
-    uniform chunks) must reproduce every per-step value of the reference recurrence
-    (partial tiles in i and j, single planes, chunks of one plane)."""
-    variant, spec, kz2 = plan
+    """The two-step kernel (pipelined stencil7_cheb2f_kernel: automatic chunk plan,
+    uniform chunks of kz planes, an explicit plan) must reproduce every per-step
+    value of the reference recurrence (partial tiles in i and j, single planes,
+    chunks of one plane)."""
+    spec, kz2 = plan
     if spec == "3,2,1,1" and dims[2] != 7:
         spec = ""  # an explicit plan only applies to a launch of exactly that span
-    monkeypatch.setenv("PCGX_CHEB2V", variant)
     monkeypatch.setenv("PCGX_C2PLAN", spec)
     monkeypatch.setenv("PCGX_KZ2", kz2)
     monkeypatch.setenv("PCGX_CHEB2", "1")
@@ -671,17 +669,6 @@ def test_pcg_fused_update_iteration_limit(P, ctx, monkeypatch):
         out[fused] = P.pcg_solve(op, rhs, P.SolveOptions(maxit=3), prec)
     assert np.array_equal(out["1"][0], out["0"][0])
     assert out["1"][1].iters == out["0"][1].iters == 3 and not out["1"][1].converged
-
-
-def test_pcg_csr_fallback_kernels(P, ctx, oracle, golden, monkeypatch):
-    """csr2 (TMA tiles) and the chunked CSR kernel: not fused with the direction update."""
-    c = _golden_case(golden, "csr300_m7")
-    g = golden["csr_apply"]
-    rp, ci, va = np.array(g["row_ptr"]), np.array(g["col_idx"]), fhs(g["values"])
-    for kern in ("1", "2"):
-        monkeypatch.setenv("PCGX_CSR_KERNEL", kern)
-        _check_solve(P, oracle, c, csr(P, ctx, rp, ci, va),
-                     OracleOp("csr", row_ptr=rp, col_idx=ci, values=va), len(rp) - 1)
 
 
 @pytest.mark.parametrize("k,iters,ddot,matvec,rel_res,err", [

@@ -53,7 +53,7 @@ def main():
             env = {}
             for kv in v.split(","):
                 k, val = kv.split("=")
-                env[{"kz": "PCGX_KZ", "scalar": "PCGX_STENCIL_SCALAR", "pfd": "PCGX_PFD"}.get(k, k)] = val
+                env[{"kz": "PCGX_KZ", "pfd": "PCGX_PFD"}.get(k, k)] = val
             print(json.dumps(run(ctx, nx, env)), flush=True)
 
 

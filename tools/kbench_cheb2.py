@@ -6,7 +6,7 @@ are interleaved over several rounds so thermal / power-cap drift hits all of
 them alike; the SM clock is sampled (NVML) while each variant runs.
 
     python tools/kbench_cheb2.py [--rounds 3] [--nx 320] VARIANT ...
-    VARIANT = "PCGX_CHEB2V=3" | "lib=tools/bin/libpcgx_d3.so+PCGX_CHEB2V=3" (settings joined by +)
+    VARIANT = "PCGX_CHEB3=1" | "lib=tools/bin/libpcgx_d3.so+PCGX_KZ2=16" (settings joined by +)
 
 --same: env-only variants as operators of ONE context, alternated on the same
 device buffers (run-to-run allocation effects cancel).

@@ -3,7 +3,7 @@
 samples NVML power, SM / memory clocks and throttle reasons meanwhile, to tell a
 power-capped kernel from a bandwidth- or latency-bound one.
 
-    python tools/power_probe.py [copy|step|cheb2|cheb2v0] [seconds]
+    python tools/power_probe.py [copy|step|cheb2|cheb3] [seconds]
 """
 import ctypes as C
 import json
@@ -26,8 +26,8 @@ def main():
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(0)
     nx = 320
-    if what == "cheb2v0":
-        os.environ["PCGX_CHEB2V"] = "0"
+    if what == "cheb3":
+        os.environ["PCGX_CHEB3"] = "1"
     with P.Context(0) as ctx:
         op, _ = P.jacobi_scale(P.StencilOperator(nx), ctx)
         n = op.local_size()
@@ -42,7 +42,7 @@ def main():
             nbytes = 2 * src.numel() * 8
             sync = torch.cuda.synchronize
         else:
-            m = 40 if what.startswith("cheb2") else 1
+            m = 40 if what.startswith("cheb") else 1
             cp = P.cheb_params(a, b, m, 1.001)._c()
             if what == "step":  # single fused step kernel: m = 1 apply = one first step
                 cp = P.cheb_params(a, b, 1, 1.001)._c()
