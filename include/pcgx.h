@@ -138,6 +138,18 @@ void pcgx_slab_partition(int64_t nz, int nranks, int rank, int64_t* z0, int64_t*
 pcgx_status pcgx_csr_create(pcgx_context ctx, int64_t n, const int64_t* row_ptr,
                             const int64_t* col_idx, const double* values,
                             const double* inv_sqrt_diag, pcgx_operator* out);
+/* Block-row CsrMatrix from THIS rank's rows only (no rank holds the full matrix;
+ * the paper's distributed layout): rows [row0, row0 + n_local)
+ * of a symmetric n x n matrix, row0 / n_local = pcgx_slab_partition(n, nranks,
+ * rank); row_ptr has n_local+1 entries (any base), col_idx global, ascending per
+ * row. The symmetric pattern gives every rank its send / receive lists without
+ * communication; the ghost columns' Jacobi values (inv_sqrt_diag: this rank's
+ * n_local entries, or NULL = computed from the local diagonal) are exchanged once.
+ * Bitwise the same operator as pcgx_csr_create with the full matrix. A single-rank
+ * context takes the whole matrix (row0 = 0, n_local = n). */
+pcgx_status pcgx_csr_create_local(pcgx_context ctx, int64_t n, int64_t row0, int64_t n_local,
+                                  const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                                  const double* inv_sqrt_diag, pcgx_operator* out);
 /* Same, from int32 host arrays (the builder's generators produce these). */
 pcgx_status pcgx_csr_create_i32(pcgx_context ctx, int64_t n, const int32_t* row_ptr,
                                 const int32_t* col_idx, const double* values,

@@ -2988,6 +2988,143 @@ void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::
   build_sell(op, nloc, lrp, lci, va + k0);
 }
 
+// Block-row CSR from THIS rank's rows only (the paper's distributed matrix,
+// PAPER.md:683-685): rows [row0, row0 + nloc) of a symmetric n x n matrix with
+// global column indices, the balanced row partition pcgx_slab_partition gives.
+// No rank holds the full matrix. The halo lists need no communication because the
+// pattern is symmetric (a_ic != 0 <=> a_ci != 0): rank q needs my x_c exactly when
+// my row c has a column in q's rows, and I receive my ghost columns from their
+// owners -- both sides list them in ascending column order. The Jacobi values of
+// the ghost columns (other ranks' diagonals) travel once through the operator's own
+// block-row exchange. Values are uploaded as given: bitwise the rows the full-matrix
+// path uploads, so every SpMV / Chebyshev step equals the single-domain result.
+template <class I>
+void csr_upload_local(pcgx_context c, pcgx_operator op, long long n, long long r0, long long nloc, const I* rp,
+                      const I* ci, const double* va, const double* isd) {
+  const int P = c->nranks, me = c->rank;
+  std::vector<long long> start(P + 1);
+  for (int q = 0; q < P; ++q) {
+    int64_t z0, nl;
+    pcgx_slab_partition(n, P, q, &z0, &nl);
+    start[(size_t)q] = z0;
+  }
+  start[(size_t)P] = n;
+  if (r0 != start[(size_t)me] || r0 + nloc != start[(size_t)me + 1])
+    fail(PCGX_ERR_INVALID, "csr_create_local: rank " + std::to_string(me) + " must own rows [" +
+                               std::to_string(start[(size_t)me]) + ", " + std::to_string(start[(size_t)me + 1]) +
+                               ") (pcgx_slab_partition)");
+  if (nloc < 1) fail(PCGX_ERR_INVALID, "csr_create: fewer rows than ranks");
+  if (!rp || !ci || !va) fail(PCGX_ERR_INVALID, "CsrMatrix: null array");
+  const long long base = (long long)rp[0], nnz = (long long)rp[nloc] - base;
+  if (nnz >= (1LL << 31) || n >= (1LL << 31))
+    fail(PCGX_ERR_OVERFLOW, "csr_create: nnz " + std::to_string(nnz) + " does not fit the int32 device CSR");
+  const long long r1 = r0 + nloc;
+  std::vector<int> ghosts;
+  std::vector<double> dv((size_t)nloc);
+  long long bad = -1;
+  for (long long i = 0; i < nloc; ++i) {
+    if (rp[i + 1] < rp[i]) fail(PCGX_ERR_INVALID, "CsrMatrix: row_ptr not nondecreasing");
+    double diag = 0.0;
+    for (long long k = (long long)rp[i] - base; k < (long long)rp[i + 1] - base; ++k) {
+      const long long col = (long long)ci[k];
+      if (col < 0 || col >= n)
+        fail(PCGX_ERR_INVALID, "CsrMatrix: column index out of range in row " + std::to_string(r0 + i));
+      if (k > (long long)rp[i] - base && col <= (long long)ci[k - 1])
+        fail(PCGX_ERR_INVALID, "CsrMatrix: columns not strictly increasing in row " + std::to_string(r0 + i));
+      if (col == r0 + i) diag = va[k];
+      if (col < r0 || col >= r1) ghosts.push_back((int)col);
+    }
+    if (isd) dv[(size_t)i] = isd[i];
+    else if (!(diag > 0.0)) {
+      if (bad < 0) bad = r0 + i;
+    } else {
+      dv[(size_t)i] = 1.0 / std::sqrt(diag);  // jacobi_scale (linop.cpp:340-351)
+    }
+  }
+  // every rank learns whether any rank's diagonal is nonpositive (no rank may be
+  // left waiting in the exchange below)
+  {
+    const double flag = bad >= 0 ? 1.0 : 0.0;
+    PCGX_CUDA(cudaMemcpy(c->S + S_DOT, &flag, sizeof flag, cudaMemcpyHostToDevice));
+    allreduce(c, S_DOT, 1);
+    double any = 0.0;
+    PCGX_CUDA(cudaMemcpy(&any, c->S + S_DOT, sizeof any, cudaMemcpyDeviceToHost));
+    if (bad >= 0) fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry at index " + std::to_string(bad));
+    if (any > 0.0) fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry on another rank");
+  }
+  std::sort(ghosts.begin(), ghosts.end());
+  ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+  std::vector<int> lrp((size_t)nloc + 1), lci((size_t)nnz);
+  for (long long i = 0; i <= nloc; ++i) lrp[(size_t)i] = (int)((long long)rp[i] - base);
+  for (long long k = 0; k < nnz; ++k) {
+    const long long col = (long long)ci[k];
+    lci[(size_t)k] = (col >= r0 && col < r1)
+                         ? (int)(col - r0)
+                         : (int)(nloc + (std::lower_bound(ghosts.begin(), ghosts.end(), (int)col) - ghosts.begin()));
+  }
+  op->nb_rank.clear();
+  op->send_off.clear();
+  op->send_cnt.clear();
+  op->recv_off.clear();
+  op->recv_cnt.clear();
+  std::vector<int> send_idx;
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    const long long lo = std::lower_bound(ghosts.begin(), ghosts.end(), (int)start[(size_t)q]) - ghosts.begin();
+    const long long hi = std::lower_bound(ghosts.begin(), ghosts.end(), (int)start[(size_t)q + 1]) - ghosts.begin();
+    std::vector<int> need;  // my rows with a column in q's rows (= the rows of mine q's rows reference)
+    for (long long i = 0; i < nloc; ++i)
+      for (long long k = lrp[(size_t)i]; k < lrp[(size_t)i + 1]; ++k) {
+        const long long col = (long long)ci[k];
+        if (col >= start[(size_t)q] && col < start[(size_t)q + 1]) {
+          need.push_back((int)i);
+          break;
+        }
+      }
+    if (hi == lo && need.empty()) continue;
+    op->nb_rank.push_back(q);
+    op->recv_off.push_back(lo);
+    op->recv_cnt.push_back(hi - lo);
+    op->send_off.push_back((long long)send_idx.size());
+    op->send_cnt.push_back((long long)need.size());
+    for (int r : need) send_idx.push_back(r);
+  }
+  op->kind = 1;
+  op->n_global = n;
+  op->nnz = nnz;  // this rank's rows
+  op->row0 = r0;
+  op->n_local = nloc;
+  op->nghost = (long long)ghosts.size();
+  op->nsend = (long long)send_idx.size();
+  PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * (size_t)(nloc + std::max(op->nghost, 1LL))));
+  PCGX_CUDA(cudaMemcpy(op->dvec, dv.data(), sizeof(double) * (size_t)nloc, cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMalloc(&op->rp, sizeof(int) * lrp.size()));
+  PCGX_CUDA(cudaMemcpy(op->rp, lrp.data(), sizeof(int) * lrp.size(), cudaMemcpyHostToDevice));
+  const size_t ng = (size_t)std::max(op->nghost, 1LL), nsd = (size_t)std::max(op->nsend, 1LL);
+  PCGX_CUDA(cudaMalloc(&op->send_idx, sizeof(int) * nsd));
+  if (op->nsend)
+    PCGX_CUDA(cudaMemcpy(op->send_idx, send_idx.data(), sizeof(int) * send_idx.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMalloc(&op->sbuf_z, sizeof(double) * nsd));
+  PCGX_CUDA(cudaMalloc(&op->sbuf_p, sizeof(double) * nsd));
+  PCGX_CUDA(cudaMalloc(&op->ghost_z, sizeof(double) * ng));
+  PCGX_CUDA(cudaMalloc(&op->ghost_p, sizeof(double) * ng));
+  PCGX_CUDA(cudaDeviceSynchronize());  // legacy-stream uploads before the compute stream
+  // the ghost columns' Jacobi values from their owners, through the block-row exchange
+  if (op->nsend)
+    pack_kernel<<<vec_grid(c, op->nsend), kVecThreads, 0, c->s>>>(op->nsend, op->send_idx, op->dvec,
+                                                                   op->sbuf_z);
+  check_launch();
+  const double* sb[1] = {op->sbuf_z};
+  double* gb[1] = {op->ghost_z};
+  c->cm->sparse_xchg(c, op, 1, sb, gb);
+  c->cm->halo_wait(c);
+  if (op->nghost)
+    PCGX_CUDA(cudaMemcpyAsync(op->dvec + nloc, op->ghost_z, sizeof(double) * (size_t)op->nghost,
+                              cudaMemcpyDeviceToDevice, c->s));
+  PCGX_CUDA(cudaStreamSynchronize(c->s));
+  build_sell(op, nloc, lrp, lci, va);
+}
+
 // SELL-32 arrays of an int32 CSR (n rows, local column space) -> op (see sell_kernel).
 void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
                 const std::vector<int>& ci32, const double* va) {
@@ -3784,6 +3921,32 @@ pcgx_status pcgx_csr_create(pcgx_context c, int64_t n, const int64_t* row_ptr,
     op->tune = Tuning::from_env();
     csr_create_any(c, op, n, row_ptr, col_idx, values, inv_sqrt_diag);
     PCGX_CUDA(cudaDeviceSynchronize());  // legacy-stream uploads / memsets before any compute-stream work
+    *out = op;
+  });
+}
+
+pcgx_status pcgx_csr_create_local(pcgx_context c, int64_t n, int64_t row0, int64_t n_local,
+                                  const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                                  const double* inv_sqrt_diag, pcgx_operator* out) {
+  return guarded(c, [&] {
+    set_device(c);
+    if (!c->cm && c->nranks == 1 && (row0 != 0 || n_local != n))
+      fail(PCGX_ERR_INVALID, "csr_create_local: a single rank owns all rows");
+    auto op = new pcgx_operator_s();
+    op->ctx = c;
+    op->tune = Tuning::from_env();
+    try {
+      if (c->nranks == 1) {
+        if (row_ptr && row_ptr[0] != 0) fail(PCGX_ERR_INVALID, "csr_create_local: row_ptr must start at 0");
+        csr_upload(c, op, n, row_ptr, col_idx, values, inv_sqrt_diag);
+      } else {
+        csr_upload_local(c, op, n, row0, n_local, row_ptr, col_idx, values, inv_sqrt_diag);
+      }
+    } catch (...) {
+      free_op(op);
+      throw;
+    }
+    PCGX_CUDA(cudaDeviceSynchronize());
     *out = op;
   });
 }

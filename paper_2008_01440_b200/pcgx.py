@@ -138,6 +138,7 @@ SYMBOLS = [
     "pcgx_device_free", "pcgx_memcpy_h2d", "pcgx_memcpy_d2h", "pcgx_memcpy_d2d",
     "pcgx_host_alloc", "pcgx_host_free", "pcgx_timer_start", "pcgx_timer_stop",
     "pcgx_flush_l2", "pcgx_stencil7_create", "pcgx_slab_partition", "pcgx_csr_create", "pcgx_csr_create_i32",
+    "pcgx_csr_create_local",
     "pcgx_operator_destroy", "pcgx_operator_size", "pcgx_operator_local_size",
     "pcgx_operator_z0", "pcgx_operator_row0", "pcgx_operator_nnz", "pcgx_operator_storage", "pcgx_operator_matvec_count",
     "pcgx_operator_apply", "pcgx_operator_apply_device", "pcgx_cheb_params", "pcgx_cheb_eval",
@@ -205,6 +206,8 @@ def lib():
         "pcgx_csr_create": (C.c_int, [ctx, C.c_int64, _i64p, _i64p, _dp, _dp, C.POINTER(op)]),
         "pcgx_csr_create_i32": (C.c_int, [ctx, C.c_int64, _i32p, _i32p, _dp, _dp,
                                           C.POINTER(op)]),
+        "pcgx_csr_create_local": (C.c_int, [ctx, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, _dp, _dp,
+                                            C.POINTER(op)]),
         "pcgx_slab_partition": (None, [C.c_int64, C.c_int, C.c_int, _i64p, _i64p]),
         "pcgx_operator_destroy": (None, [op]),
         "pcgx_operator_size": (C.c_int64, [op]),
@@ -592,6 +595,22 @@ def jacobi_scale(op, ctx: Context):
                                      None, C.byref(h)), ctx.h)
         return ScaledOperator(ctx, h, op), None
     raise InvalidArgument("jacobi_scale: unsupported operator type")
+
+
+def csr_block_rows(ctx: Context, n, row_ptr, col_idx, values, row0=None):
+    """Jacobi-scaled block-row CsrMatrix from this rank's rows only
+    (pcgx_csr_create_local): row_ptr (n_local + 1, any base) / col_idx (global) /
+    values of rows [row0, row0 + n_local), the pcgx_slab_partition block."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+    va = np.ascontiguousarray(values, dtype=np.float64)
+    nl = len(rp) - 1
+    if row0 is None:
+        row0, _ = slab_partition(n, ctx.nranks, ctx.rank)
+    h = C.c_void_p()
+    _check(lib().pcgx_csr_create_local(ctx.h, n, row0, nl, _ptr(rp, _i64p), _ptr(ci, _i64p), _ptr(va), None,
+                                       C.byref(h)), ctx.h)
+    return ScaledOperator(ctx, h, None)
 
 
 # ============================================================================ polynomial

@@ -27,11 +27,19 @@ def main():
         op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
         a, b = P.analytic_extremes_box(nx, ny, nz)
         n = nx * ny * nz
-    else:
+    elif kind == "fe27":
         A = P.gen_fe27(nx, 1.0, SEED)
         op, _ = P.jacobi_scale(A, ctx)
         a, b = 0.01, 2.5
         n = A.n
+    else:  # "fe27_local": this rank's block of rows only (pcgx_csr_create_local)
+        A = P.gen_fe27(nx, 1.0, SEED)
+        n = A.n
+        r0, nl = P.slab_partition(n, nranks, rank)
+        lo, hi = int(A.row_ptr[r0]), int(A.row_ptr[r0 + nl])
+        op = P.csr_block_rows(ctx, n, A.row_ptr[r0:r0 + nl + 1], A.col_idx[lo:hi], A.values[lo:hi])
+        del A
+        a, b = 0.01, 2.5
     lo, nl = op.row0(), op.local_size()
     xt = P.random_uniform_vector(nl, SEED, offset=lo)
     bl = op.apply(xt)

@@ -94,12 +94,16 @@ def test_multiprocess_slabs_match_local_group(pcgx, tmp_path):
         c.close()
 
 
-def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, tmp_path):
-    """CSR block rows (the paper's distributed SpMV) across 2
-    processes: per-neighbour packed halos through the shared segment."""
+@pytest.mark.parametrize("kind,nranks", [("fe27", 2), ("fe27_local", 2), ("fe27_local", 3)])
+def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks, tmp_path):
+    """CSR block rows (the paper's distributed SpMV) across
+    processes: per-neighbour packed halos through the shared segment; every rank
+    given the full matrix ("fe27") or only its own rows ("fe27_local",
+    pcgx_csr_create_local: lists from the symmetric pattern, ghost Jacobi values
+    exchanged once)."""
     P = pcgx
     nx, m = 14, 6
-    res = run_job(2, "fe27", (nx, nx, nx), m, tmp_path)
+    res = run_job(nranks, kind, (nx, nx, nx), m, tmp_path)
     A = P.gen_fe27(nx, 1.0, SEED)
     opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
     xt = oracle.random_uniform(A.n, SEED)

@@ -640,10 +640,11 @@ def test_pcg_fused_update_bitwise_vs_separate(P, ctx, oracle, dims, m, monkeypat
     prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001))
     runs = {}
     for fused in ("1", "0"):
-        monkeypatch.setenv("PCGX_FUSE_UPD", fused)
-        runs[fused] = P.pcg_solve(op, rhs, None, prec)
+        monkeypatch.setenv("PCGX_FUSE_UPD", fused)  # read when the operator is created
+        opf = stencil(P, ctx, nx, ny, nz)
+        runs[fused] = P.pcg_solve(opf, rhs, None, prec)
         # a second solve replays the cached graphs of the same schedule
-        x2, r2 = P.pcg_solve(op, rhs, None, prec)
+        x2, r2 = P.pcg_solve(opf, rhs, None, prec)
         assert np.array_equal(x2, runs[fused][0]) and r2.iters == runs[fused][1].iters
     (x1, r1), (x0, r0) = runs["1"], runs["0"]
     assert r1.converged and r1.iters == r0.iters and r1.ddot == r0.ddot and r1.matvec == r0.matvec
@@ -665,8 +666,8 @@ def test_pcg_fused_update_iteration_limit(P, ctx, monkeypatch):
     prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, 6, 1.001))
     out = {}
     for fused in ("1", "0"):
-        monkeypatch.setenv("PCGX_FUSE_UPD", fused)
-        out[fused] = P.pcg_solve(op, rhs, P.SolveOptions(maxit=3), prec)
+        monkeypatch.setenv("PCGX_FUSE_UPD", fused)  # read when the operator is created
+        out[fused] = P.pcg_solve(stencil(P, ctx, nx), rhs, P.SolveOptions(maxit=3), prec)
     assert np.array_equal(out["1"][0], out["0"][0])
     assert out["1"][1].iters == out["0"][1].iters == 3 and not out["1"][1].converged
 
