@@ -211,6 +211,12 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   const int hgj = j0 - 1 + lane;
   const bool h_in = do_h && hgi >= 0 && hgi < p.nx && hgj >= 0 && hgj < p.ny;
   const int offAh = (lane + 1) * kFW + hcol, offBh = lane * kFW + hcol;
+  // every shared offset this thread reads / writes lies inside its slot
+  PCGX_DCHECK(offA - kFW - 1 >= 0 && offA + kFW + 2 < kFW * kFAY);
+  PCGX_DCHECK(offB - kFW - 1 >= 0 || warp == 0);
+  PCGX_DCHECK(offB + 2 <= kFBPlane && (warp == kFTY + 1 || offB + kFW + 2 <= kFBPlane));
+  PCGX_DCHECK(!do_h || (offAh - kFW - 1 >= 0 && offAh + kFW + 1 < kFW * kFAY && offBh < kFBPlane));
+  const long long g_lo = -(long long)p.zoff * p.nxy, g_hi = (long long)(p.nzl + p.zoff) * p.nxy;
 
   const double* const sAend = sA + kFNA * kFAPlane;
   const double* const sBend = sB + kFNB * kFEStride;
@@ -265,6 +271,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         }
       }
       if (kUpd && has_p && interior && do1 && t + 1 >= kb && t + 1 < ke && t + 1 >= p.c_lo && t + 1 < p.c_hi) {
+        PCGX_DCHECK((long long)(t + 1) * p.nxy + (long long)gj * p.nx + gi + 2 <= g_hi);
         st2(p.rout + (long long)(t + 1) * p.nxy + (long long)gj * p.nx + gi, ap.x, ap.y);
         acc_rr = acc_rr + ap.x * ap.x;
         acc_rr = acc_rr + ap.y * ap.y;
@@ -294,8 +301,9 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       const double y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
       double2 c;
       if (kFirst) {
-        c.x = p.c1 * ((2.0 * xc.x) - div_rn(y0, p.theta, inv_t));
-        c.y = p.c1 * ((2.0 * xc.y) - div_rn(y1, p.theta, inv_t));
+        const double2 yq = div2_rn(y0, y1, p.theta, inv_t);
+        c.x = p.c1 * ((2.0 * xc.x) - yq.x);
+        c.y = p.c1 * ((2.0 * xc.y) - yq.y);
       } else {
         const double2 bb = *reinterpret_cast<const double2*>(pBu + offB);
         const double2 rr = *reinterpret_cast<const double2*>(pRu + offB);
@@ -305,7 +313,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       }
       const bool live = plane_in && do1;
       if (live) cv = c;
-      if (p.outC && live && interior && t >= kb && t < ke) st2(gCt, cv.x, cv.y);  // outC null: last pass
+      if (p.outC && live && interior && t >= kb && t < ke) {  // outC null: last pass
+        PCGX_DCHECK(gCt - p.outC >= g_lo && gCt - p.outC + 2 <= g_hi);
+        st2(gCt, cv.x, cv.y);
+      }
       *reinterpret_cast<double2*>(pCu + offB) = cv;
       // i-halo columns of C[t] (read by stage 2 of plane t, two iterations on)
       if (do_h) {
@@ -349,7 +360,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       double2 rv, xo;
       if (kFirst) {
         rv = a2;  // A == R == r
-        xo = make_double2(div_rn(a2.x, p.theta, inv_t), div_rn(a2.y, p.theta, inv_t));
+        xo = div2_rn(a2.x, a2.y, p.theta, inv_t);
       } else {
         rv = kFRReg ? r2 : *reinterpret_cast<const double2*>(pR2 + offB);
         xo = a2;
@@ -357,6 +368,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       const double e0 = p.rk2 * (((p.c3 * cc.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
       const double e1 = p.rk2 * (((p.c3 * cc.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
       if (do2) {
+        PCGX_DCHECK(gEv - p.outE >= g_lo && gEv - p.outE + 2 <= g_hi);
         st2(gEv, e0, e1);
         if (kRed) acc = acc + (rv.x * e0 + rv.y * e1);
       }

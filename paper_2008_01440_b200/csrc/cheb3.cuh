@@ -159,6 +159,9 @@ stencil7_cheb3_kernel(const __grid_constant__ CUtensorMap mapA,  // A, box 72 x 
   const int h2gi = warp == 1 ? i0 - 1 : i0 + kC2TX, h2gj = j0 - 1 + lane;
   const bool h2_in = h2gi >= 0 && h2gi < p.nx && h2gj >= 0 && h2gj < p.ny;
 
+  PCGX_DCHECK(offA - k3AW - 1 >= 0 && offA + k3AW + 2 <= k3AW * k3AR);
+  PCGX_DCHECK(offB - k3W - 1 >= -k3W && offB + k3W + 2 <= k3Plane + k3W);  // +-1 row: rings / guard
+  const long long g_hi = (long long)p.nzl * p.nxy;
   const double* const sAend = sA + k3NA * k3APlane;
   const double* const sBend = sB + k3NB * k3Plane;
   const double* const sRend = sR + k3NR * k3Plane;
@@ -324,7 +327,10 @@ stencil7_cheb3_kernel(const __grid_constant__ CUtensorMap mapA,  // A, box 72 x 
       if constexpr (kCls >= 2) {
         if (s2) {
           st2s(pE0 + offB, ev);
-          if (kCls == 3 && gE && own_in && t - 2 >= kb && t - 2 < ke) st2(gE, ev.x, ev.y);
+          if (kCls == 3 && gE && own_in && t - 2 >= kb && t - 2 < ke) {
+            PCGX_DCHECK(gE - p.outE >= 0 && gE - p.outE + 2 <= g_hi);
+            st2(gE, ev.x, ev.y);
+          }
         }
       }
       if constexpr (kCls == 2) {
@@ -332,6 +338,7 @@ stencil7_cheb3_kernel(const __grid_constant__ CUtensorMap mapA,  // A, box 72 x 
       }
       if constexpr (kCls == 3) {
         if (s3 && own_in) {
+          PCGX_DCHECK(gF - p.outF >= 0 && gF - p.outF + 2 <= g_hi);
           st2(gF, f0, f1);
           if (kRed) acc = acc + (r4.x * f0 + r4.y * f1);
         }

@@ -19,6 +19,28 @@
 
 #include "pcgx.h"
 
+// Checked build (-DPCGX_CHECKED; tools/build_variant.py checked -DPCGX_CHECKED):
+// device-side bounds checks on the hand-written TMA / shared-memory kernels --
+// every shared-memory ring offset a thread uses, every global store index -- that
+// trap on a violation. compute-sanitizer is not available on the GPU pool, so
+// this is the memory-safety check the sanitizer run would have been
+// (tools/sanitize_run.py drives it on ragged small grids). Compiled out by default.
+#ifdef PCGX_CHECKED
+#include <cstdio>
+#define PCGX_DCHECK(cond)                                                                   \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("pcgx check failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                            \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define PCGX_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace pcgx {
 
 // ------------------------------------------------------------------ errors
@@ -79,6 +101,11 @@ struct Reduce {
   double* result = nullptr;
   int accumulate = 0;
   double* mirror = nullptr;  // != nullptr: the result also goes to this host-mapped slot
+  // != nullptr (a launch inside a conditional PCG segment): the result is r'r and
+  // the reducing block also sets the segment's IF condition -- "not converged",
+  // sqrt(r'r) / cond_bt[0] > cond_bt[1] (||b||, tol), the host's own test
+  const double* cond_bt = nullptr;
+  unsigned long long cond = 0;  // cudaGraphConditionalHandle
 };
 
 // Geometry of one (slab of a) 7-point stencil operator.

@@ -173,6 +173,7 @@ dia3t_kernel(const __grid_constant__ Dia3tMaps maps, int nx, int kz, Epi epi, Re
       const double y = sum * dr;
       const long long row = (long long)k * nxy + (long long)j * nx + i;
       if constexpr (kDir) {
+        PCGX_DCHECK(row >= 0);
         epi.q[row] = y;
         epi.pout[row] = xr;
         if (kRed) acc = acc + xr * y;  // EpiStoreP: p . q

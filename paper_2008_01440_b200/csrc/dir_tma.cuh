@@ -188,6 +188,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
         const double y0 = stencil_point(d, pm.x, ps.x, pw, pc.x, pc.y, pnn.x, pn.x);
         const double y1 = stencil_point(d, pm.y, ps.y, pc.x, pc.y, pe, pnn.y, pn.y);
         const long long idx = (long long)v * p.nxy + goff;
+        PCGX_DCHECK(idx >= -(long long)p.zoff * p.nxy && idx + 2 <= (long long)(p.nzl + p.zoff) * p.nxy);
         st2(p.q + idx, y0, y1);
         st2(p.pout + idx, pc.x, pc.y);
         acc = acc + (pc.x * y0 + pc.y * y1);

@@ -73,6 +73,23 @@ __device__ __forceinline__ double div_rn(double x, double b, double inv) {
   if (e - 63u > 1920u) q = div_rn_wide(x, b, inv);
   return q;
 }
+// Two quotients by the same divisor with ONE range branch (the first two-step
+// pass divides four values per lane and plane): the fast path for both, the
+// out-of-line path only for an operand outside [2^-960, 2^961) -- bitwise div_rn.
+__device__ __forceinline__ double2 div2_rn(double x0, double x1, double b, double inv) {
+  const double p0 = x0 * inv, p1 = x1 * inv;
+  const double r0 = __fma_rn(-p0, b, x0), r1 = __fma_rn(-p1, b, x1);
+  double q0 = __fma_rn(r0, inv, p0), q1 = __fma_rn(r1, inv, p1);
+  const unsigned e0 = ((unsigned)__double2hiint(x0) >> 20) & 0x7ffu;
+  const unsigned e1 = ((unsigned)__double2hiint(x1) >> 20) & 0x7ffu;
+  const bool w0 = e0 - 63u > 1920u, w1 = e1 - 63u > 1920u;
+  if (w0 | w1) {
+    if (w0) q0 = div_rn_wide(x0, b, inv);
+    if (w1) q1 = div_rn_wide(x1, b, inv);
+  }
+  return make_double2(q0, q1);
+}
+
 // The same quotient where zeros are frequent (zero-filled Dirichlet halo values in
 // the direction step): +-0 / b = +-0 by a select instead of the out-of-line path,
 // which a warp would otherwise take for every boundary lane (and the block barrier
@@ -208,6 +225,7 @@ __device__ __forceinline__ void block_reduce_finish(double v, const Reduce& red)
       const double res = red.accumulate ? (*red.result + s) : s;
       *red.result = res;
       if (red.mirror) *red.mirror = res;
+      if (red.cond_bt) cudaGraphSetConditional(red.cond, sqrt(res) / red.cond_bt[0] <= red.cond_bt[1] ? 0u : 1u);
       *red.counter = 0u;
       __threadfence();
     }

@@ -70,7 +70,7 @@ struct Tuning {
   int kz = 0, kz2 = 32, pfd = 2, cheb2 = 1, cheb3 = 0, dir_tma = 1;
   std::string c2plan;  // "" automatic chunk plan, "u" uniform kz2, "h1,h2,..." explicit
   // PCG schedule
-  int fuse_upd = 1, no_graph = 0, graph_multi = 0, merged = 0, cond_graph = 1, no_fuse_p = 0, zdiv = 1,
+  int fuse_upd = 1, no_graph = 0, graph_multi = 0, merged = 0, cond_graph = 10, no_fuse_p = 0, zdiv = 1,
       defer_x = 1, snap_memcpy = 0, step_reps = 20;
   // vector kernels
   int upd2 = 1, upd_bps = 8;
@@ -1721,8 +1721,13 @@ void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Pa
                                                   (long long)std::max(occ, 1) * c->sms)).first;
   }
   check_red_grid((unsigned long long)tiles * it->second.n);
+  Reduce rr = make_red(c, u.s_rr);
+  if (c->cond_root && !c->cond_split) {  // the head of a conditional segment: r'r closes it
+    rr.cond_bt = c->S + S_BNORM;
+    rr.cond = c->cond_h;
+  }
   kern<<<dim3((unsigned)tiles, (unsigned)it->second.n), kFThreads, kC2FSmem, c->s>>>(
-      ma, mq, ma, prm, 0, nzl, it->second, Reduce{}, make_red(c, u.s_rr));
+      ma, mq, ma, prm, 0, nzl, it->second, Reduce{}, rr);
   check_launch();
   count_launch(c);
 }
@@ -2186,10 +2191,14 @@ __global__ void cond_kernel(cudaGraphConditionalHandle h, const double* S, int s
 
 // Inside capture_cond's body: the convergence flag from S[slot_rr], then the IF
 // node; everything enqueued after this runs only if the solve goes on.
-void cond_split(pcgx_context c, int slot_rr) {
-  cond_kernel<<<1, 1, 0, c->s>>>(c->cond_h, c->S, slot_rr, S_BNORM, S_TOL);
-  check_launch();
-  count_launch(c);
+// with_kernel = false: the reducing block of the preceding launch already set the
+// condition (Reduce::cond_bt, the fused first pass's r'r)
+void cond_split(pcgx_context c, int slot_rr, bool with_kernel = true) {
+  if (with_kernel) {
+    cond_kernel<<<1, 1, 0, c->s>>>(c->cond_h, c->S, slot_rr, S_BNORM, S_TOL);
+    check_launch();
+    count_launch(c);
+  }
   cudaStreamCaptureStatus st;
   const cudaGraphNode_t* deps = nullptr;
   size_t nd = 0;
@@ -2272,7 +2281,10 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // one GPU with graphs: the speculative tail of each segment (P r and A p of the
   // next iteration) sits in a conditional IF node that a device-side convergence
   // test closes, so nothing is computed and discarded at convergence
-  const bool use_cond = use_graph && spec_after_update && op->tune.cond_graph != 0;
+  // (degree >= tune.cond_graph, default 10: below it the IF node's per-iteration
+  // cost outweighs the one skipped tail per solve; m = 0 / plain CG never)
+  const bool use_cond = use_graph && spec_after_update && op->tune.cond_graph > 0 && prec.kind != 0 &&
+                        m >= op->tune.cond_graph;
 
   std::memset(rep, 0, sizeof *rep);
   c->cur_launches = 0;
@@ -2417,7 +2429,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
       const CgUpd u{Rb[par ^ 1], q, Rb[par], slot_rz(par ^ 1), slot_pq(par), slot_rr(par)};
       enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u, [&] {
         snapshot();
-        if (use_cond) cond_split(c, slot_rr(par));
+        if (use_cond) cond_split(c, slot_rr(par), false);  // the first pass set the condition
       });
     } else if (use_cond) {
       cond_split(c, slot_rr(par));  // r'r(it) came from the update kernel before this segment

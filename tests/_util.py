@@ -46,3 +46,18 @@ def csr_to_dense(rp, ci, va, n):
     for i in range(n):
         A[i, ci[rp[i]:rp[i + 1]]] = va[rp[i]:rp[i + 1]]
     return A
+
+
+def lap2d_csr(nx):
+    """assemble_laplacian(lap2d, nx) (proj/src/linop.cpp:299-331) as int64 CSR:
+    diagonal 4, off-diagonal -1, the 5-point star in ascending columns."""
+    n = nx * nx
+    rp, ci, va = [0], [], []
+    for r in range(n):
+        i, j = r % nx, r // nx
+        for off, ok in ((-nx, j > 0), (-1, i > 0), (0, True), (1, i < nx - 1), (nx, j < nx - 1)):
+            if ok:
+                ci.append(r + off)
+                va.append(4.0 if off == 0 else -1.0)
+        rp.append(len(ci))
+    return np.array(rp, dtype=np.int64), np.array(ci, dtype=np.int64), np.array(va)

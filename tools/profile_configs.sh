@@ -8,7 +8,7 @@ for cfg in "$@"; do
     cfg1) kern=dia_kernel; skip=40 ;;
     cfg3) kern="dia3t_kernel<\\(bool\\)0, pcgx::EpiChebStep"; skip=40 ;;
     cfg4) kern="bsr3t_kernel<\\(bool\\)0, pcgx::EpiChebStep"; skip=40 ;;
-    *) kern="cheb2f_kernel<\\(bool\\)0, \\(bool\\)0, \\(bool\\)0, \\(bool\\)0>"; skip=100 ;;
+    *) kern="cheb2f_kernel<\\(bool\\)0, \\(bool\\)0, \\(bool\\)0>"; skip=100 ;;
   esac
   extra=""
   [ "$cfg" != "cfg2" ] && extra="--no-cpu-baseline"
