@@ -10,6 +10,7 @@
 // per neighbour per SpMV overlapped with the interior planes, and two NCCL
 // all-reduces (8 B and 16 B) per PCG iteration.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 #include <fcntl.h>
 #include <pthread.h>
@@ -113,6 +114,16 @@ struct Tuning {
     g("PCGX_UPD_BPS", t.upd_bps);
     return t;
   }
+};
+
+// NVTX ranges around the library's phases (header-only NVTX v3: free unless a
+// profiler is attached) -- solve, setup, iterations, exit residual, applies,
+// operator uploads -- so nsys / ncu timelines show where a solve's time goes.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 struct Graph {
@@ -2258,6 +2269,7 @@ double cheb_step_bytes(pcgx_operator op) {
 
 void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const double* b,
                       double* x, const pcgx_solve_opts* o, pcgx_report* rep) {
+  NvtxRange nvtx_solve("pcgx::pcg_solve");
   if (op->ctx != c) fail(PCGX_ERR_INVALID, "pcg_solve: operator belongs to another context");
   pcgx_solve_opts opts;
   pcgx_solve_opts_default(&opts);
@@ -2321,6 +2333,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   };
 
   // ||b|| (pcg.cpp:32)
+  auto nvtx_setup = std::make_unique<NvtxRange>("pcgx::pcg_solve setup");
   launch_dot(c, n, b, b, S_BB);
   allreduce(c, S_BB, 1);
   fetch_scalars(c);
@@ -2502,6 +2515,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
 
   enqueue_dir_spmv(1);
   alg += bytes_dir;
+  nvtx_setup.reset();
+  auto nvtx_iter = std::make_unique<NvtxRange>("pcgx::pcg_solve iterations");
   for (int it = 1; it <= opts.maxit; ++it) {
     const int par = it & 1;
     const bool more = it < opts.maxit;
@@ -2589,6 +2604,8 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     alg += 3 * N8;
   }
   // true residual (pcg.cpp:112-115)
+  nvtx_iter.reset();
+  NvtxRange nvtx_exit("pcgx::pcg_solve true residual");
   op_launch<EpiResid, true>(c, op, x, EpiResid{b, nullptr}, S_EE);
   allreduce(c, S_EE, 1);
   fetch_scalars(c);
@@ -3909,6 +3926,7 @@ void pcgx_slab_partition(int64_t nz, int nranks, int rank, int64_t* z0, int64_t*
 pcgx_status pcgx_stencil7_create(pcgx_context c, int64_t nx, int64_t ny, int64_t nz,
                                  double inv_sqrt_diag, pcgx_operator* out) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::operator_create");
     set_device(c);
     if (nx < 1 || ny < 1 || nz < 1) fail(PCGX_ERR_INVALID, "StencilOperator: nx must be >= 1");
     if (nx > (1 << 30) || ny > (1 << 30) || nx * ny > (1LL << 31))
@@ -3927,6 +3945,7 @@ pcgx_status pcgx_csr_create(pcgx_context c, int64_t n, const int64_t* row_ptr,
                             const int64_t* col_idx, const double* values,
                             const double* inv_sqrt_diag, pcgx_operator* out) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::operator_create");
     set_device(c);
     auto op = new pcgx_operator_s();
     op->ctx = c;
@@ -3941,6 +3960,7 @@ pcgx_status pcgx_csr_create_local(pcgx_context c, int64_t n, int64_t row0, int64
                                   const int64_t* row_ptr, const int64_t* col_idx, const double* values,
                                   const double* inv_sqrt_diag, pcgx_operator* out) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::operator_create");
     set_device(c);
     if (!c->cm && c->nranks == 1 && (row0 != 0 || n_local != n))
       fail(PCGX_ERR_INVALID, "csr_create_local: a single rank owns all rows");
@@ -3967,6 +3987,7 @@ pcgx_status pcgx_csr_create_i32(pcgx_context c, int64_t n, const int32_t* row_pt
                                 const int32_t* col_idx, const double* values,
                                 const double* inv_sqrt_diag, pcgx_operator* out) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::operator_create");
     set_device(c);
     auto op = new pcgx_operator_s();
     op->ctx = c;
@@ -4005,6 +4026,7 @@ uint64_t pcgx_operator_matvec_count(pcgx_operator op) { return op ? op->matvecs.
 pcgx_status pcgx_operator_apply_device(pcgx_context c, pcgx_operator op, const double* x,
                                        double* y) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::operator_apply");
     set_device(c);
     op_launch<EpiStore, false>(c, op, x, EpiStore{y}, -1);
   });
@@ -4012,6 +4034,7 @@ pcgx_status pcgx_operator_apply_device(pcgx_context c, pcgx_operator op, const d
 
 pcgx_status pcgx_operator_apply(pcgx_context c, pcgx_operator op, const double* x, double* y) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::operator_apply");
     set_device(c);
     const long long n = op->n_local;
     ensure_workspace(c, n, ws_pad_of(op));
@@ -4037,6 +4060,7 @@ double pcgx_cheb_eval(const pcgx_cheb* p, double lambda) {
 pcgx_status pcgx_cheb_apply_device(pcgx_context c, pcgx_operator op, const pcgx_cheb* p,
                                    const double* r, double* out) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::cheb_apply");
     set_device(c);
     if (r == out) fail(PCGX_ERR_INVALID, "apply_chebyshev: out must not alias r");
     ensure_workspace(c, op->n_local, ws_pad_of(op));
@@ -4052,6 +4076,7 @@ pcgx_status pcgx_cheb_apply_device(pcgx_context c, pcgx_operator op, const pcgx_
 pcgx_status pcgx_cheb_apply(pcgx_context c, pcgx_operator op, const pcgx_cheb* p, const double* r,
                             double* out) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::cheb_apply");
     set_device(c);
     const long long n = op->n_local;
     ensure_workspace(c, n, ws_pad_of(op));
@@ -4105,6 +4130,7 @@ pcgx_status pcgx_chi_sequence(double alpha, double beta, int nlev, double* chi) 
 pcgx_status pcgx_newton_apply_device(pcgx_context c, pcgx_operator op, const pcgx_newton* p,
                                      const double* r, double* out) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::newton_apply");
     set_device(c);
     if (r == out) fail(PCGX_ERR_INVALID, "apply_newton: out must not alias r");
     Newton N = newton_from(p);
@@ -4115,6 +4141,7 @@ pcgx_status pcgx_newton_apply_device(pcgx_context c, pcgx_operator op, const pcg
 pcgx_status pcgx_newton_apply(pcgx_context c, pcgx_operator op, const pcgx_newton* p,
                               const double* r, double* out) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::newton_apply");
     set_device(c);
     const long long n = op->n_local;
     ensure_workspace(c, n, ws_pad_of(op));
@@ -4307,6 +4334,7 @@ void pcgx_analytic_extremes_box(int64_t nx, int64_t ny, int64_t nz, double* lo, 
 pcgx_status pcgx_power_method(pcgx_context c, pcgx_operator op, double tol, int maxit,
                               uint64_t seed, double* out4) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::power_method");
     set_device(c);
     power_method_device(c, op, tol, maxit, seed, out4);
   });
@@ -4315,6 +4343,7 @@ pcgx_status pcgx_power_method(pcgx_context c, pcgx_operator op, double tol, int 
 pcgx_status pcgx_dacg_smallest(pcgx_context c, pcgx_operator op, double tol, int maxit,
                                uint64_t seed, double* out4) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::dacg");
     set_device(c);
     dacg_device(c, op, tol, maxit, seed, out4);
   });
@@ -4323,6 +4352,7 @@ pcgx_status pcgx_dacg_smallest(pcgx_context c, pcgx_operator op, double tol, int
 pcgx_status pcgx_lanczos_bounds(pcgx_context c, pcgx_operator op, int steps_hi, int steps,
                                 uint64_t seed, double* lo, double* hi) {
   return guarded(c, [&] {
+    NvtxRange nvtx_r("pcgx::lanczos");
     set_device(c);
     lanczos_device(c, op, steps_hi, steps, seed, lo, hi);
   });
