@@ -52,6 +52,36 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+CHECKED_LIB = os.path.join(PKG, "libpcgx_checked.so")
+
+
+def _stale_lib(lib: str) -> bool:
+    if not os.path.exists(lib):
+        return True
+    t = os.path.getmtime(lib)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(ROOT, "include", "pcgx.h"))
+    deps.append(__file__)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def build_checked(force: bool = False) -> str:
+    """The checked build (-DPCGX_CHECKED: device-side bounds asserts in the TMA /
+    shared-memory kernels, common.cuh PCGX_DCHECK) as libpcgx_checked.so beside
+    the production library. compute-sanitizer is not available on the GPU pool;
+    tests/test_gpu_checked.py runs a ragged small-grid workload on this build."""
+    if not (force or _stale_lib(CHECKED_LIB)):
+        return CHECKED_LIB
+    cmd = command(["-DPCGX_CHECKED"])
+    tmp = CHECKED_LIB + f".tmp{os.getpid()}"
+    cmd[cmd.index("-o") + 1] = tmp
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("libpcgx_checked build failed:\n" + res.stdout + res.stderr)
+    os.replace(tmp, CHECKED_LIB)
+    return CHECKED_LIB
+
+
 def command(extra=()):
     return [
         _nvcc(), "-ccbin", _host_cxx(), "-O3", "-std=c++17",
@@ -94,3 +124,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))

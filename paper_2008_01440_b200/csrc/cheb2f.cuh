@@ -26,6 +26,26 @@
 
 namespace pcgx {
 
+// Power / ceiling experiment only (tools/build_variant.py nomath -DPCGX_C2F_NOMATH=1;
+// NOT bitwise, never the product): the stencil sums replaced by an integer XOR of
+// the same seven operands, so the pass keeps every TMA box, shared load and store
+// but drops ~15 of its ~22 fp64 operations per point-step.
+#ifndef PCGX_C2F_NOMATH
+#define PCGX_C2F_NOMATH 0
+#endif
+__device__ __forceinline__ double c2f_stencil(double d, double a, double b, double c, double e, double f,
+                                              double g, double h) {
+#if PCGX_C2F_NOMATH
+  (void)d;
+  const long long x = __double_as_longlong(a) ^ __double_as_longlong(b) ^ __double_as_longlong(c) ^
+                      __double_as_longlong(e) ^ __double_as_longlong(f) ^ __double_as_longlong(g) ^
+                      __double_as_longlong(h);
+  return __longlong_as_double(x & 0x3fffffffffffffffll);
+#else
+  return stencil_point(d, a, b, c, e, f, g, h);
+#endif
+}
+
 // Tile 64 x kFTY, kFTY + 2 warps. Default: 64 x 20 (22 warps, ONE CTA per SM,
 // 80 registers), rings four planes deep (206 KB), R of stage 2 in registers.
 // Measured at 320^3 against the alternatives (tools/kbench_cheb2.py, one box):
@@ -182,6 +202,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     a[e] = a[e] - alpha * sQ[(a - sA0) + e];
   };
   if (kIP) {  // the prologue planes kb-2, kb-1, whole boxes
+    // (combining each plane's whole box one iteration ahead, by all threads
+    // uniformly, instead of the own pairs + border split below: 291 -> 312 us)
     for (int e = tid; e < kFW * kFAY; e += kFThreads) {
       if (in_z(kb - 2)) combine_slot(sA, e);
       if (in_z(kb - 1)) combine_slot(sA + kFAPlane, e);
@@ -297,8 +319,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       const double2 as = rqx2(pAu, offA - kFW);
       const double2 an = rqx2(pAu, offA + kFW);
       const double2 xc = ac;  // A[t] at the pair
-      const double y0 = stencil_point(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
-      const double y1 = stencil_point(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
+      const double y0 = c2f_stencil(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
+      const double y1 = c2f_stencil(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
       double2 c;
       if (kFirst) {
         const double2 yq = div2_rn(y0, y1, p.theta, inv_t);
@@ -354,8 +376,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       }
       const double2 cs = *reinterpret_cast<const double2*>(pC2 + offB - kFW);
       const double2 cn = *reinterpret_cast<const double2*>(pC2 + offB + kFW);
-      const double y0 = stencil_point(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
-      const double y1 = stencil_point(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
+      const double y0 = c2f_stencil(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
+      const double y1 = c2f_stencil(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
       const double2 cc = c2;  // C[t-2] at the pair
       double2 rv, xo;
       if (kFirst) {
