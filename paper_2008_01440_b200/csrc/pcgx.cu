@@ -20,6 +20,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <condition_variable>
 #include <mutex>
@@ -539,10 +540,14 @@ struct LocalComm : CommBase {
 // results (scalars are summed in rank order, like group_sum_kernel).
 struct ShmHeader {
   std::atomic<uint64_t> magic;
-  pthread_barrier_t bar;
+  std::atomic<int> count;  // barrier arrivals of the current generation
+  std::atomic<int> gen;    // barrier generation
+  std::atomic<int> abort;  // a rank gave up (timeout): the others fail instead of waiting
   int nranks;
   size_t cap;
 };
+static_assert(std::atomic<int>::is_always_lock_free && std::atomic<uint64_t>::is_always_lock_free,
+              "host comm: atomics in shared memory must be address-free (lock-free)");
 constexpr uint64_t kShmMagic = 0x70636778686f7374ull;  // "pcgxhost"
 constexpr size_t kShmHdr = 4096;
 
@@ -553,9 +558,32 @@ struct HostComm : CommBase {
   size_t total = 0, cap = 0;
   ShmHeader* hdr() const { return reinterpret_cast<ShmHeader*>(base); }
   double* box(int r) const { return reinterpret_cast<double*>(base + kShmHdr + (size_t)r * cap); }
+  // Counter barrier on lock-free atomics in the shared segment (release / acquire
+  // orders each rank's outbox writes before the peers' reads). A rank that waits
+  // longer than PCGX_HOSTCOMM_TIMEOUT seconds (default 600) marks the job aborted
+  // and fails; every waiting rank then fails too instead of hanging.
   void barrier() const {
-    const int e = pthread_barrier_wait(&hdr()->bar);
-    if (e != 0 && e != PTHREAD_BARRIER_SERIAL_THREAD) fail(PCGX_ERR_NCCL, "host comm: barrier failed");
+    ShmHeader* h = hdr();
+    if (h->abort.load(std::memory_order_acquire)) fail(PCGX_ERR_NCCL, "host comm: a peer rank gave up");
+    const int g = h->gen.load(std::memory_order_acquire);
+    if (h->count.fetch_add(1, std::memory_order_acq_rel) + 1 == nranks) {
+      h->count.store(0, std::memory_order_relaxed);
+      h->gen.store(g + 1, std::memory_order_release);
+      return;
+    }
+    const double limit = (double)std::max(1, env_int("PCGX_HOSTCOMM_TIMEOUT", 600));
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long spins = 0; h->gen.load(std::memory_order_acquire) == g; ++spins) {
+      if (h->abort.load(std::memory_order_acquire)) fail(PCGX_ERR_NCCL, "host comm: a peer rank gave up");
+      if (spins > 2000) {
+        usleep(20);
+        if ((spins & 1023) == 0 &&
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+          h->abort.store(1, std::memory_order_release);
+          fail(PCGX_ERR_NCCL, "host comm: barrier timed out (a peer rank is gone)");
+        }
+      }
+    }
   }
   void need(size_t bytes) const {
     if (bytes > cap)
@@ -695,11 +723,9 @@ HostComm* host_comm_open(int nranks, int rank, const std::string& name, size_t c
   hc->base = static_cast<unsigned char*>(m);
   ShmHeader* h = hc->hdr();
   if (rank == 0) {
-    pthread_barrierattr_t a;
-    pthread_barrierattr_init(&a);
-    pthread_barrierattr_setpshared(&a, PTHREAD_PROCESS_SHARED);
-    pthread_barrier_init(&h->bar, &a, (unsigned)nranks);
-    pthread_barrierattr_destroy(&a);
+    h->count.store(0, std::memory_order_relaxed);
+    h->gen.store(0, std::memory_order_relaxed);
+    h->abort.store(0, std::memory_order_relaxed);
     h->nranks = nranks;
     h->cap = hc->cap;
     h->magic.store(kShmMagic, std::memory_order_release);
