@@ -3144,6 +3144,31 @@ void csr_upload_local(pcgx_context c, pcgx_operator op, long long n, long long r
     op->send_cnt.push_back((long long)need.size());
     for (int r : need) send_idx.push_back(r);
   }
+  // The lists are consistent only if the pattern is symmetric across ranks: check
+  // it before any point-to-point exchange (a mismatch would hang NCCL). Every rank
+  // contributes its row of the P x P "receive from" and "send to" count matrices;
+  // after the all-reduce recv[a][b] must equal send[b][a] everywhere.
+  {
+    std::vector<double> cnt(2 * (size_t)P * P, 0.0);
+    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
+      cnt[(size_t)me * P + op->nb_rank[i]] = (double)op->recv_cnt[i];
+      cnt[(size_t)P * P + (size_t)me * P + op->nb_rank[i]] = (double)op->send_cnt[i];
+    }
+    const int chunk = S_E2 - S_DOT + 1;  // scratch slots S_DOT .. S_E2
+    for (size_t b0 = 0; b0 < cnt.size(); b0 += (size_t)chunk) {
+      const int k = (int)std::min<size_t>((size_t)chunk, cnt.size() - b0);
+      PCGX_CUDA(cudaMemcpy(c->S + S_DOT, cnt.data() + b0, sizeof(double) * k, cudaMemcpyHostToDevice));
+      allreduce(c, S_DOT, k);
+      PCGX_CUDA(cudaMemcpy(cnt.data() + b0, c->S + S_DOT, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+    for (int a = 0; a < P; ++a)
+      for (int q = 0; q < P; ++q)
+        if (cnt[(size_t)a * P + q] != cnt[(size_t)P * P + (size_t)q * P + a])
+          fail(PCGX_ERR_INVALID, "CsrMatrix: block rows are not symmetric: rank " + std::to_string(a) +
+                                     " needs " + std::to_string((long long)cnt[(size_t)a * P + q]) +
+                                     " values of rank " + std::to_string(q) + ", which would send " +
+                                     std::to_string((long long)cnt[(size_t)P * P + (size_t)q * P + a]));
+  }
   op->kind = 1;
   op->n_global = n;
   op->nnz = nnz;  // this rank's rows

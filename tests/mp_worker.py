@@ -32,12 +32,27 @@ def main():
         op, _ = P.jacobi_scale(A, ctx)
         a, b = 0.01, 2.5
         n = A.n
-    else:  # "fe27_local": this rank's block of rows only (pcgx_csr_create_local)
+    else:  # "fe27_local[_asym]": this rank's block of rows only (pcgx_csr_create_local)
         A = P.gen_fe27(nx, 1.0, SEED)
         n = A.n
         r0, nl = P.slab_partition(n, nranks, rank)
         lo, hi = int(A.row_ptr[r0]), int(A.row_ptr[r0 + nl])
-        op = P.csr_block_rows(ctx, n, A.row_ptr[r0:r0 + nl + 1], A.col_idx[lo:hi], A.values[lo:hi])
+        rp, ci, va = A.row_ptr[r0:r0 + nl + 1].astype(np.int64), A.col_idx[lo:hi], A.values[lo:hi]
+        if kind.endswith("_asym") and rank == 0:
+            # drop every coupling of rank 0's rows to rank 1's first row: rank 0 no
+            # longer needs that value, rank 1 (whose row still couples back) sends it
+            c = r0 + nl
+            keep = ci != c
+            ck = np.concatenate([[0], np.cumsum(keep)])
+            rp = ck[rp - rp[0]].astype(np.int64)
+            ci, va = ci[keep], va[keep]
+        try:
+            op = P.csr_block_rows(ctx, n, rp, ci, va)
+        except P.InvalidArgument as e:
+            with open(os.path.join(out, f"rank{rank}.err"), "w") as f:
+                f.write(str(e))
+            ctx.close()
+            return
         del A
         a, b = 0.01, 2.5
     lo, nl = op.row0(), op.local_size()

@@ -115,3 +115,19 @@ def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks,
     x_full, rep_o = oracle.pcg_solve(opo, prm, b_full)
     rep = json.loads(str(res[0]["rep"]))
     assert rep["converged"] and abs(rep["iters"] - rep_o["iters"]) <= 1
+
+
+def test_multiprocess_local_rows_reject_asymmetric_pattern(pcgx, tmp_path):
+    """pcgx_csr_create_local derives its halo lists from the symmetric pattern; a
+    pattern that is not symmetric across ranks is caught on EVERY rank before any
+    point-to-point exchange (InvalidArgument naming the ranks), instead of a hang."""
+    name = f"pcgx_test_{uuid.uuid4().hex[:12]}"
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), name, "2", str(r),
+                               str(tmp_path), "fe27_local_asym", "12", "12", "12", "4"],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    for p in procs:
+        out, _ = p.communicate(timeout=600)
+        assert p.returncode == 0, out
+    for r in range(2):
+        msg = open(os.path.join(tmp_path, f"rank{r}.err")).read()
+        assert "block rows are not symmetric" in msg, msg
