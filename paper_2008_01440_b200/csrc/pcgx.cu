@@ -1060,6 +1060,21 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
                   (std::is_same<In, InComb>::value && std::is_same<Epi, EpiStoreP>::value)) {
       if (bsr3t_launch<kRed>(c, op, in, epi, slot)) return;
     }
+    if (!op->nb_rank.empty()) {  // block-row rank: the ghost columns first (no overlap)
+      const double* src[2];
+      const int nv = halo_vecs(in, src);
+      const double* sb[2] = {op->sbuf_z, op->sbuf_p};
+      double* gb[2] = {op->ghost_z, op->ghost_p};
+      for (int v = 0; v < nv && op->nsend; ++v) {
+        pack_kernel<<<vec_grid(c, op->nsend), kVecThreads, 0, c->s>>>(op->nsend, op->send_idx, src[v],
+                                                                       const_cast<double*>(sb[v]));
+        check_launch();
+        count_launch(c);
+      }
+      c->cm->sparse_xchg(c, op, nv, sb, gb);
+      c->cur_halo_bytes += (long long)nv * op->nsend * 8;
+      c->cm->halo_wait(c);
+    }
     Bsr3Geom g{(int)(op->n_local / 3), 0, op->bsr_slices, op->bsr_ptr, op->bsr_len, op->bsr_col,
                op->bsr_val, op->dvec};
     const int wpb = 8;
@@ -2955,6 +2970,9 @@ int default_kz(pcgx_context c, long long nx, long long ny, long long nzl) {
 
 void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
                 const std::vector<int>& ci32, const double* va);
+void build_bsr3(pcgx_operator op, long long n, const std::vector<int>& rp32,
+                const std::vector<int>& ci32, const double* va);
+bool is_bsr3(long long n, const std::vector<int>& rp, const std::vector<int>& ci);
 
 // CSR block rows (the paper's MPI block-row SpMV): this rank
 // keeps rows [row0, row0 + nloc) with columns remapped to the local space:
@@ -2965,10 +2983,20 @@ void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
 void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::vector<int>& rp32,
                       const std::vector<int>& ci32, const double* va, const std::vector<double>& dv) {
   const int P = c->nranks, me = c->rank;
+  // a matrix of aligned 3 x 3 blocks keeps BSR-3 on every rank: rows split in whole
+  // block rows (the balanced partition of the n/3 block rows), the local columns
+  // remapped to [local | ghost] stay aligned triples, and bsr3_kernel reads the
+  // ghost columns through the same exchange as SELL
+  const bool bsr = op->tune.bsr != 0 && n % 3 == 0 && n >= 3LL * P && is_bsr3(n, rp32, ci32);
   std::vector<long long> start(P + 1);
   for (int q = 0; q < P; ++q) {
     int64_t z0, nl;
-    pcgx_slab_partition(n, P, q, &z0, &nl);
+    if (bsr) {
+      pcgx_slab_partition(n / 3, P, q, &z0, &nl);
+      z0 *= 3;
+    } else {
+      pcgx_slab_partition(n, P, q, &z0, &nl);
+    }
     start[(size_t)q] = z0;
   }
   start[(size_t)P] = n;
@@ -3040,7 +3068,8 @@ void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::
   PCGX_CUDA(cudaMalloc(&op->sbuf_p, sizeof(double) * nsd));
   PCGX_CUDA(cudaMalloc(&op->ghost_z, sizeof(double) * ng));
   PCGX_CUDA(cudaMalloc(&op->ghost_p, sizeof(double) * ng));
-  build_sell(op, nloc, lrp, lci, va + k0);
+  if (bsr && is_bsr3(nloc, lrp, lci)) build_bsr3(op, nloc, lrp, lci, va + k0);
+  else build_sell(op, nloc, lrp, lci, va + k0);
 }
 
 // Block-row CSR from THIS rank's rows only (the paper's distributed matrix,

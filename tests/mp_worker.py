@@ -27,10 +27,10 @@ def main():
         op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
         a, b = P.analytic_extremes_box(nx, ny, nz)
         n = nx * ny * nz
-    elif kind == "fe27":
-        A = P.gen_fe27(nx, 1.0, SEED)
+    elif kind in ("fe27", "elast27"):
+        A = P.gen_fe27(nx, 1.0, SEED) if kind == "fe27" else P.gen_elast27(nx, 1.0, 0.5, 0.1, SEED)
         op, _ = P.jacobi_scale(A, ctx)
-        a, b = 0.01, 2.5
+        a, b = (0.01, 2.5) if kind == "fe27" else (0.005, 3.2)
         n = A.n
     else:  # "fe27_local[_asym]": this rank's block of rows only (pcgx_csr_create_local)
         A = P.gen_fe27(nx, 1.0, SEED)

@@ -94,7 +94,8 @@ def test_multiprocess_slabs_match_local_group(pcgx, tmp_path):
         c.close()
 
 
-@pytest.mark.parametrize("kind,nranks", [("fe27", 2), ("fe27_local", 2), ("fe27_local", 3)])
+@pytest.mark.parametrize("kind,nranks", [("fe27", 2), ("fe27_local", 2), ("fe27_local", 3), ("elast27", 2),
+                                         ("elast27", 3)])
 def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks, tmp_path):
     """CSR block rows (the paper's distributed SpMV) across
     processes: per-neighbour packed halos through the shared segment; every rank
@@ -102,13 +103,15 @@ def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks,
     pcgx_csr_create_local: lists from the symmetric pattern, ghost Jacobi values
     exchanged once)."""
     P = pcgx
-    nx, m = 14, 6
+    nx, m = (14, 6) if kind.startswith("fe27") else (8, 6)
     res = run_job(nranks, kind, (nx, nx, nx), m, tmp_path)
-    A = P.gen_fe27(nx, 1.0, SEED)
+    if kind == "elast27":
+        assert all(str(r["storage"]) == "bsr3" for r in res)
+    A = P.gen_fe27(nx, 1.0, SEED) if kind.startswith("fe27") else P.gen_elast27(nx, 1.0, 0.5, 0.1, SEED)
     opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
     xt = oracle.random_uniform(A.n, SEED)
     b_full = oracle.apply(opo, xt)
-    prm = oracle.cheb_params(0.01, 2.5, m, 1.001)
+    prm = oracle.cheb_params(*((0.01, 2.5) if kind.startswith("fe27") else (0.005, 3.2)), m, 1.001)
     z_full = oracle.apply_chebyshev(opo, prm, oracle.random_uniform(A.n, 77))
     assert np.array_equal(np.concatenate([r["b"] for r in res]), b_full)
     assert np.array_equal(np.concatenate([r["z"] for r in res]), z_full)

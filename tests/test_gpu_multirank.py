@@ -98,8 +98,9 @@ def test_slab_lanczos_matches_single_domain(pcgx):
 
 @pytest.mark.parametrize("nranks,gen,m", [(2, "fe27", 6), (3, "elast27", 4), (4, "lap", 5)])
 def test_csr_block_rows_match_single_domain(pcgx, oracle, nranks, gen, m):
-    """Multi-rank CSR (block rows + per-neighbour halo, SELL kernel): SpMV and P_m(A) r
-    bitwise equal to the single-domain oracle, the solve within the PCG bar."""
+    """Multi-rank CSR (block rows + per-neighbour halo; SELL-32, or BSR-3 for the 3 x 3
+    block matrix): SpMV and P_m(A) r bitwise equal to the single-domain oracle, the
+    solve within the PCG bar."""
     P = pcgx
     if gen == "fe27":
         A = P.gen_fe27(10, 1.0, SEED)
@@ -124,7 +125,11 @@ def test_csr_block_rows_match_single_domain(pcgx, oracle, nranks, gen, m):
         op, _ = P.jacobi_scale(A, ctx)
         lo = op.row0()
         hi = lo + op.local_size()
-        assert (lo, op.local_size()) == P.slab_partition(n, nranks, r)
+        if gen == "elast27":  # 3 x 3 blocks: whole block rows per rank, BSR-3 kept
+            z0, nb = P.slab_partition(n // 3, nranks, r)
+            assert (lo, op.local_size()) == (3 * z0, 3 * nb) and op.storage() == "bsr3"
+        else:
+            assert (lo, op.local_size()) == P.slab_partition(n, nranks, r)
         bl = op.apply(P.random_uniform_vector(op.local_size(), SEED, offset=lo))
         zl = P.apply_chebyshev(P.cheb_params(a, b, m, 1.001), op, r_full[lo:hi])
         x, rep = P.pcg_solve(op, bl, P.SolveOptions(),
