@@ -1112,11 +1112,17 @@ constexpr int kD3Plane = kD3PX * kD3PY, kD3Threads = kD3X * kD3Y;
 static_assert(kD3Plane <= 2 * kD3Threads, "two staged patch elements per thread");
 
 struct Dia3Geom {
-  int nx, kz;  // grid edge, planes per z-chunk
+  int nx, kz;  // grid edge (i, j), planes per z-chunk
   long long ld;
   const double* val;
   const unsigned* mask;
   const double* dvec;
+  // z-slab of a multi-rank operator: nzl local planes, this launch covers planes
+  // [kb0, ke0); dlo / dhi = the Jacobi values of the neighbours' boundary planes
+  // (nullptr: Dirichlet side), their x planes come through In's glo / ghi
+  int nzl = 0, kb0 = 0, ke0 = 0;
+  const double* dlo = nullptr;
+  const double* dhi = nullptr;
 };
 
 #ifndef PCGX_DIA3_MINB
@@ -1132,7 +1138,8 @@ dia3_kernel(Dia3Geom g, In in, Epi epi, Reduce red) {
   const long long nxy = (long long)nx * nx;
   const int tiles_x = (nx + kD3X - 1) / kD3X;
   const int i0 = (int)(blockIdx.x % tiles_x) * kD3X, j0 = (int)(blockIdx.x / tiles_x) * kD3Y;
-  const int kb = blockIdx.y * g.kz, ke = min(kb + g.kz, nx);
+  const int kb = g.kb0 + blockIdx.y * g.kz, ke = min(kb + g.kz, g.ke0);
+  const int nzl = g.nzl;
   const int tid = threadIdx.x, tx = tid % kD3X, ty = tid / kD3X;
   const int i = i0 + tx, j = j0 + ty;
   const bool own = i < nx && j < nx;
@@ -1144,10 +1151,20 @@ dia3_kernel(Dia3Geom g, In in, Epi epi, Reduce red) {
   const bool in1 = e1 < kD3Plane && pi1 >= 0 && pi1 < nx && pj1 >= 0 && pj1 < nx;
   const long long c0 = (long long)pj0 * nx + pi0, c1 = (long long)pj1 * nx + pi1;
   auto stage = [&](int k, double& t0, double& t1) {
-    const bool kin = k >= 0 && k < nx;
+    const bool kin = k >= 0 && k < nzl;
     const long long kb0 = (long long)k * nxy;
-    t0 = (kin && in0) ? __ldg(g.dvec + kb0 + c0) * in.ldc(kb0 + c0) : 0.0;
-    t1 = (kin && in1) ? __ldg(g.dvec + kb0 + c1) * in.ldc(kb0 + c1) : 0.0;
+    if (kin) {
+      t0 = in0 ? __ldg(g.dvec + kb0 + c0) * in.ldc(kb0 + c0) : 0.0;
+      t1 = in1 ? __ldg(g.dvec + kb0 + c1) * in.ldc(kb0 + c1) : 0.0;
+    } else if (k == -1 && g.dlo) {  // the lower neighbour's last plane
+      t0 = in0 ? __ldg(g.dlo + c0) * in.glo1(c0) : 0.0;
+      t1 = in1 ? __ldg(g.dlo + c1) * in.glo1(c1) : 0.0;
+    } else if (k == nzl && g.dhi) {  // the upper neighbour's first plane
+      t0 = in0 ? __ldg(g.dhi + c0) * in.ghi1(c0) : 0.0;
+      t1 = in1 ? __ldg(g.dhi + c1) * in.ghi1(c1) : 0.0;
+    } else {
+      t0 = t1 = 0.0;
+    }
   };
   auto put = [&](int k, double t0, double t1) {
     double* s = sT[(k + 4) & 3];

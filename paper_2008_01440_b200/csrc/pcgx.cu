@@ -241,6 +241,8 @@ struct pcgx_operator_s {
   int dia_off[32] = {0};
   long long dia_ld = 0;
   int dia3_pat = 0, dia3_nx = 0;  // structured pattern (27 / 7) on an nx^3 grid (dia3_kernel)
+  int dia3_nzl = 0;                // z-slab rank: local planes of the grid (0: the whole grid)
+  double *dia3_dlo = nullptr, *dia3_dhi = nullptr;  // Jacobi values of the neighbours' boundary planes
   struct GMap { const void* ptr; int kind; CUtensorMap m; };
   std::vector<GMap> gmaps;        // dia3t_kernel tensor maps per buffer
   // CSR block rows on a multi-rank context: this rank owns rows [row0, row0 + n_local);
@@ -1015,24 +1017,55 @@ void op_launch_in(pcgx_context c, pcgx_operator op, const In& in, const Epi& epi
       if (dia3t_launch<kRed>(c, op, in, epi, slot)) return;
     }
     if (dia3_on(op)) {
-      Dia3Geom g3{op->dia3_nx, 0, op->dia_ld, op->dia_val, op->dia_mask, op->dvec};
-      const int tiles = ((g3.nx + kD3X - 1) / kD3X) * ((g3.nx + kD3Y - 1) / kD3Y);
-      // z-chunks: about 8 waves of 3 resident CTAs per SM, at least 8 planes each
-      const int want = std::max(1, (c->sms * 3 * 8 + tiles - 1) / tiles);
-      g3.kz = std::max(op->tune.dia3_kz > 0 ? op->tune.dia3_kz : (g3.nx + want - 1) / want,
-                       std::min(8, g3.nx));
-      const dim3 grid3(tiles, (g3.nx + g3.kz - 1) / g3.kz);
-      if (kRed) check_red_grid(nblocks_of(grid3));
-      Reduce red = kRed ? make_red(c, slot) : Reduce{};
-      if (op->dia3_pat == 27) {
-        auto k3 = stream ? dia3_kernel<27, In, Epi, kRed, true> : dia3_kernel<27, In, Epi, kRed, false>;
-        k3<<<grid3, kD3Threads, 0, c->s>>>(g3, in, epi, red);
-      } else {
-        auto k3 = stream ? dia3_kernel<7, In, Epi, kRed, true> : dia3_kernel<7, In, Epi, kRed, false>;
-        k3<<<grid3, kD3Threads, 0, c->s>>>(g3, in, epi, red);
+      const int nzl = op->dia3_nzl > 0 ? op->dia3_nzl : op->dia3_nx;
+      auto launch3 = [&](int k0, int k1, bool accumulate) {
+        if (k1 <= k0) return;
+        Dia3Geom g3{op->dia3_nx, 0, op->dia_ld, op->dia_val, op->dia_mask, op->dvec};
+        g3.nzl = nzl;
+        g3.kb0 = k0;
+        g3.ke0 = k1;
+        g3.dlo = op->dia3_dlo;
+        g3.dhi = op->dia3_dhi;
+        const int tiles = ((g3.nx + kD3X - 1) / kD3X) * ((g3.nx + kD3Y - 1) / kD3Y);
+        // z-chunks: about 8 waves of 3 resident CTAs per SM, at least 8 planes each
+        const int want = std::max(1, (c->sms * 3 * 8 + tiles - 1) / tiles);
+        g3.kz = std::max(op->tune.dia3_kz > 0 ? op->tune.dia3_kz : (nzl + want - 1) / want, std::min(8, nzl));
+        const dim3 grid3(tiles, (k1 - k0 + g3.kz - 1) / g3.kz);
+        if (kRed) check_red_grid(nblocks_of(grid3));
+        Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
+        if (op->dia3_pat == 27) {
+          auto k3 = stream ? dia3_kernel<27, In, Epi, kRed, true> : dia3_kernel<27, In, Epi, kRed, false>;
+          k3<<<grid3, kD3Threads, 0, c->s>>>(g3, in, epi, red);
+        } else {
+          auto k3 = stream ? dia3_kernel<7, In, Epi, kRed, true> : dia3_kernel<7, In, Epi, kRed, false>;
+          k3<<<grid3, kD3Threads, 0, c->s>>>(g3, in, epi, red);
+        }
+        check_launch();
+        count_launch(c);
+      };
+      const bool lo_nb = op->ghost_lo != nullptr, hi_nb = op->ghost_hi != nullptr;
+      if (!lo_nb && !hi_nb) {
+        launch3(0, nzl, false);
+        return;
       }
-      check_launch();
-      count_launch(c);
+      // z-slab rank of a grid-tile offset storage: my boundary planes to the
+      // neighbours' ghost planes; the planes that read no ghost run meanwhile
+      const double* xs[2];
+      const int nv = halo_vecs(in, xs);
+      c->cm->halo_begin(c, op, xs, nv);
+      c->cur_halo_bytes += (long long)nv * ((lo_nb ? 1 : 0) + (hi_nb ? 1 : 0)) * op->nx * op->ny * 8;
+      const int ib = lo_nb ? 1 : 0, ie = hi_nb ? nzl - 1 : nzl;
+      bool wrote = false;
+      if (ie > ib) {
+        launch3(ib, ie, false);
+        wrote = true;
+      }
+      c->cm->halo_wait(c);
+      if (lo_nb) {
+        launch3(0, std::min(1, nzl), wrote);
+        wrote = true;
+      }
+      if (hi_nb && nzl - 1 >= ib) launch3(nzl - 1, nzl, wrote);
       return;
     }
     auto kern = stream ? dia_kernel<In, Epi, kRed, true> : dia_kernel<In, Epi, kRed, false>;
@@ -1352,6 +1385,7 @@ bool dia3t_launch_any(pcgx_context c, pcgx_operator op, const In& in, const Epi&
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
   auto clash = [&](const double* o) { return o && (o == ex || o == ep || o == er); };
   if (!dia3_on(op) || op->dia3_pat != 27 || op->tune.dia3t == 0 || nx % 4 != 0 || nx < kT3PX ||
+      op->dia3_nzl > 0 ||  // a z-slab rank: the grid-tile kernel with ghost planes (dia3_kernel)
       ghosts || !al16(ex) || (ep && !al16(ep)) || (er && !al16(er)) || !al16(eout) || (eout2 && !al16(eout2)) ||
       (exo && !al16(exo)) || clash(eout) || clash(eout2))
     return false;
@@ -2973,6 +3007,10 @@ void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
 void build_bsr3(pcgx_operator op, long long n, const std::vector<int>& rp32,
                 const std::vector<int>& ci32, const double* va);
 bool is_bsr3(long long n, const std::vector<int>& rp, const std::vector<int>& ci);
+bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>& ci, std::vector<int>& off);
+template <int P>
+bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vector<int>& ci,
+                const std::vector<int>& off);
 
 // CSR block rows (the paper's MPI block-row SpMV): this rank
 // keeps rows [row0, row0 + nloc) with columns remapped to the local space:
@@ -2980,6 +3018,66 @@ bool is_bsr3(long long n, const std::vector<int>& rp, const std::vector<int>& ci
 // of ghost columns). Entries keep their order (the reference's summation order).
 // Each rank holds the full matrix on the host, so the send lists (the rows of
 // mine other ranks' rows reference) are computed without communication.
+// Offset storage of one plane-aligned z-slab of a 27-point-box matrix on an nx^3
+// grid (multi-rank cfg3): the rank owns node planes [z0, z0 + nzl) (pcgx_slab_partition
+// of the nx planes), its rows' values by offset as build_dia lays them out, the
+// Jacobi values of its rows and of the neighbours' boundary planes (from the full
+// matrix: no exchange), and x-ghost planes the stencil slab machinery fills before
+// each SpMV (dia3_kernel reads them as planes -1 and nzl).
+void dia_slab_upload(pcgx_context c, pcgx_operator op, long long n, int nx, const std::vector<int>& rp32,
+                     const std::vector<int>& ci32, const double* va, const std::vector<double>& dv,
+                     const std::vector<int>& off) {
+  const int P = c->nranks, me = c->rank;
+  int64_t z0 = 0, nzl = 0;
+  pcgx_slab_partition(nx, P, me, &z0, &nzl);
+  const long long nxy = (long long)nx * nx, r0 = z0 * nxy, nloc = nzl * nxy;
+  const int K = (int)off.size();
+  const long long ld = (nloc + 31) / 32 * 32;
+  std::vector<double> val((size_t)(ld * K), 0.0);
+  std::vector<unsigned> mask((size_t)nloc, 0u);
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < nloc; ++i) {
+    const long long g = r0 + i;
+    int q = 0;
+    for (int k = rp32[(size_t)g]; k < rp32[(size_t)g + 1]; ++k) {
+      const int o = (int)((long long)ci32[(size_t)k] - g);
+      while (off[(size_t)q] != o) ++q;  // both ascending
+      val[(size_t)(q * ld + i)] = va[k];
+      mask[(size_t)i] |= 1u << q;
+    }
+  }
+  op->kind = 1;
+  op->n_global = n;
+  op->nnz = (long long)rp32[(size_t)(r0 + nloc)] - rp32[(size_t)r0];
+  op->row0 = r0;
+  op->n_local = nloc;
+  op->dia_k = K;
+  op->dia_ld = ld;
+  for (int k = 0; k < K; ++k) op->dia_off[k] = off[(size_t)k];
+  op->dia3_pat = 27;
+  op->dia3_nx = nx;
+  op->dia3_nzl = (int)nzl;
+  op->nx = op->ny = nx;
+  op->nz = nx;
+  op->z0 = z0;
+  op->nzl = nzl;
+  PCGX_CUDA(cudaMalloc(&op->dia_val, sizeof(double) * val.size()));
+  PCGX_CUDA(cudaMalloc(&op->dia_mask, sizeof(unsigned) * std::max<size_t>(mask.size(), 1)));
+  PCGX_CUDA(cudaMemcpy(op->dia_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMemcpy(op->dia_mask, mask.data(), sizeof(unsigned) * mask.size(), cudaMemcpyHostToDevice));
+  PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * (size_t)std::max(nloc, 1LL)));
+  PCGX_CUDA(cudaMemcpy(op->dvec, dv.data() + r0, sizeof(double) * (size_t)nloc, cudaMemcpyHostToDevice));
+  if (me > 0) {
+    PCGX_CUDA(cudaMalloc(&op->dia3_dlo, sizeof(double) * (size_t)nxy));
+    PCGX_CUDA(cudaMemcpy(op->dia3_dlo, dv.data() + r0 - nxy, sizeof(double) * (size_t)nxy, cudaMemcpyHostToDevice));
+  }
+  if (me < P - 1) {
+    PCGX_CUDA(cudaMalloc(&op->dia3_dhi, sizeof(double) * (size_t)nxy));
+    PCGX_CUDA(cudaMemcpy(op->dia3_dhi, dv.data() + r0 + nloc, sizeof(double) * (size_t)nxy, cudaMemcpyHostToDevice));
+  }
+  init_stencil_ghosts(c, op);  // x / p ghost planes (nx * nx) for the plane exchange
+}
+
 void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::vector<int>& rp32,
                       const std::vector<int>& ci32, const double* va, const std::vector<double>& dv) {
   const int P = c->nranks, me = c->rank;
@@ -2988,6 +3086,20 @@ void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::
   // remapped to [local | ghost] stay aligned triples, and bsr3_kernel reads the
   // ghost columns through the same exchange as SELL
   const bool bsr = op->tune.bsr != 0 && n % 3 == 0 && n >= 3LL * P && is_bsr3(n, rp32, ci32);
+  // offset storage on a cubic grid with the 27-point box (cfg3): plane-aligned
+  // z-slabs and the grid-tile kernel with the neighbours' boundary planes as ghosts
+  if (!bsr && op->tune.dia != 0 && op->tune.dia3 != 0) {
+    std::vector<int> doff;
+    const long long nnz_all = rp32[(size_t)n];
+    int nx = (int)std::llround(std::cbrt((double)n));
+    while ((long long)nx * nx * nx > n) --nx;
+    while ((long long)(nx + 1) * (nx + 1) * (nx + 1) <= n) ++nx;
+    if ((long long)nx * nx * nx == n && nx >= 3 && nx >= P && dia_offsets(n, rp32, ci32, doff) &&
+        (double)doff.size() * (double)n <= 1.5 * (double)nnz_all && dia3_match<27>(n, nx, rp32, ci32, doff)) {
+      dia_slab_upload(c, op, n, nx, rp32, ci32, va, dv, doff);
+      return;
+    }
+  }
   std::vector<long long> start(P + 1);
   for (int q = 0; q < P; ++q) {
     int64_t z0, nl;
@@ -3652,6 +3764,8 @@ void free_op(pcgx_operator op) {
   cudaFree(op->b3g_mask);
   cudaFree(op->dia_val);
   cudaFree(op->dia_mask);
+  cudaFree(op->dia3_dlo);
+  cudaFree(op->dia3_dhi);
   cudaFree(op->send_idx);
   cudaFree(op->sbuf_z);
   cudaFree(op->sbuf_p);

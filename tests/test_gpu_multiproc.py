@@ -107,6 +107,8 @@ def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks,
     res = run_job(nranks, kind, (nx, nx, nx), m, tmp_path)
     if kind == "elast27":
         assert all(str(r["storage"]) == "bsr3" for r in res)
+    if kind == "fe27":
+        assert all(str(r["storage"]) == "dia_grid" for r in res)
     A = P.gen_fe27(nx, 1.0, SEED) if kind.startswith("fe27") else P.gen_elast27(nx, 1.0, 0.5, 0.1, SEED)
     opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
     xt = oracle.random_uniform(A.n, SEED)

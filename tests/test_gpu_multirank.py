@@ -128,6 +128,9 @@ def test_csr_block_rows_match_single_domain(pcgx, oracle, nranks, gen, m):
         if gen == "elast27":  # 3 x 3 blocks: whole block rows per rank, BSR-3 kept
             z0, nb = P.slab_partition(n // 3, nranks, r)
             assert (lo, op.local_size()) == (3 * z0, 3 * nb) and op.storage() == "bsr3"
+        elif gen == "fe27":  # 27-point box on the 10^3 grid: node-plane slabs, grid-tile offset storage
+            z0, nzl = P.slab_partition(10, nranks, r)
+            assert (lo, op.local_size()) == (100 * z0, 100 * nzl) and op.storage() == "dia_grid"
         else:
             assert (lo, op.local_size()) == P.slab_partition(n, nranks, r)
         bl = op.apply(P.random_uniform_vector(op.local_size(), SEED, offset=lo))
