@@ -3012,12 +3012,6 @@ template <int P>
 bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vector<int>& ci,
                 const std::vector<int>& off);
 
-// CSR block rows (the paper's MPI block-row SpMV, PAPER.md:683-685): this rank
-// keeps rows [row0, row0 + nloc) with columns remapped to the local space:
-// owned columns -> [0, nloc), others -> nloc + (position in the ascending list
-// of ghost columns). Entries keep their order (the reference's summation order).
-// Each rank holds the full matrix on the host, so the send lists (the rows of
-// mine other ranks' rows reference) are computed without communication.
 // Offset storage of one plane-aligned z-slab of a 27-point-box matrix on an nx^3
 // grid (multi-rank cfg3): the rank owns node planes [z0, z0 + nzl) (pcgx_slab_partition
 // of the nx planes), its rows' values by offset as build_dia lays them out, the
@@ -3078,6 +3072,12 @@ void dia_slab_upload(pcgx_context c, pcgx_operator op, long long n, int nx, cons
   init_stencil_ghosts(c, op);  // x / p ghost planes (nx * nx) for the plane exchange
 }
 
+// CSR block rows (the paper's MPI block-row SpMV, PAPER.md:683-685): this rank
+// keeps rows [row0, row0 + nloc) with columns remapped to the local space:
+// owned columns -> [0, nloc), others -> nloc + (position in the ascending list
+// of ghost columns). Entries keep their order (the reference's summation order).
+// Each rank holds the full matrix on the host, so the send lists (the rows of
+// mine other ranks' rows reference) are computed without communication.
 void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::vector<int>& rp32,
                       const std::vector<int>& ci32, const double* va, const std::vector<double>& dv) {
   const int P = c->nranks, me = c->rank;
