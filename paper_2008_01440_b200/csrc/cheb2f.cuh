@@ -238,7 +238,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   PCGX_DCHECK(offB - kFW - 1 >= 0 || warp == 0);
   PCGX_DCHECK(offB + 2 <= kFBPlane && (warp == kFTY + 1 || offB + kFW + 2 <= kFBPlane));
   PCGX_DCHECK(!do_h || (offAh - kFW - 1 >= 0 && offAh + kFW + 1 < kFW * kFAY && offBh < kFBPlane));
-  const long long g_lo = -(long long)p.zoff * p.nxy, g_hi = (long long)(p.nzl + p.zoff) * p.nxy;
+  [[maybe_unused]] const long long g_lo = -(long long)p.zoff * p.nxy;  // PCGX_DCHECK bounds
+  [[maybe_unused]] const long long g_hi = (long long)(p.nzl + p.zoff) * p.nxy;
 
   const double* const sAend = sA + kFNA * kFAPlane;
   const double* const sBend = sB + kFNB * kFEStride;

@@ -161,7 +161,7 @@ stencil7_cheb3_kernel(const __grid_constant__ CUtensorMap mapA,  // A, box 72 x 
 
   PCGX_DCHECK(offA - k3AW - 1 >= 0 && offA + k3AW + 2 <= k3AW * k3AR);
   PCGX_DCHECK(offB - k3W - 1 >= -k3W && offB + k3W + 2 <= k3Plane + k3W);  // +-1 row: rings / guard
-  const long long g_hi = (long long)p.nzl * p.nxy;
+  [[maybe_unused]] const long long g_hi = (long long)p.nzl * p.nxy;  // PCGX_DCHECK bound
   const double* const sAend = sA + k3NA * k3APlane;
   const double* const sBend = sB + k3NB * k3Plane;
   const double* const sRend = sR + k3NR * k3Plane;

@@ -1300,10 +1300,7 @@ update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
     one(i, ri, qi);
     if (hj) one(j, rj, qj);
   }
-  if (kZ) block_reduce_finish2(acc, acc2, red);
-  else block_reduce_finish(acc, red);
-  return;
-#endif
+#else
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
        i += (long long)gridDim.x * blockDim.x) {
     double2 ri = r[i];
@@ -1330,6 +1327,7 @@ update2_kernel(long long n2, double2* __restrict__ x, double2* __restrict__ r,
       acc2 = acc2 + ri.y * ri.y;
     }
   }
+#endif
   if (kZ) block_reduce_finish2(acc, acc2, red);
   else block_reduce_finish(acc, red);
 }
