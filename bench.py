@@ -128,7 +128,7 @@ class Dist:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             if backend is None:
                 backend = "cpu:gloo,cuda:nccl" if torch.cuda.is_available() else "gloo"
-            if os.environ.get("PCGX_BENCH_COMM") == "host":
+            if os.environ.get("PCGX_BENCH_COMM") in ("host", "ipc_local"):
                 backend = "gloo"  # all ranks may share one GPU: plumbing on the CPU only
             elif torch.cuda.is_available():
                 torch.cuda.set_device(local)
@@ -247,13 +247,21 @@ def run_gpu(args):
     # PCGX_BENCH_DIST=1: take the multi-GPU code path even at world size 1 (a
     # 1-rank NCCL communicator; with PCGX_FORCE_NCCL=1 its all-reduces go through NCCL)
     comm = "nccl"
-    if ws > 1 and os.environ.get("PCGX_BENCH_COMM") == "host":
-        # every rank on GPU 0, halos and all-reduces through host shared memory
-        # (pcgx_context_create_host): the multi-process path where there is one GPU
+    if ws > 1 and os.environ.get("PCGX_BENCH_COMM") in ("host", "ipc", "ipc_local"):
+        # host: every rank on GPU 0, halos and all-reduces through host shared memory
+        # (pcgx_context_create_host), the multi-process path where there is one GPU;
+        # ipc: CUDA-IPC device mailboxes (pcgx_context_create_ipc), one GPU per rank
+        # (peer-to-peer over NVLink) -- ipc_local puts every rank on GPU 0
         import uuid
+        mode = os.environ["PCGX_BENCH_COMM"]
         name = D.bcast_bytes(f"pcgx_bench_{uuid.uuid4().hex[:12]}".encode() if rank == 0 else None)
-        ctx = P.Context(0, nranks=ws, rank=rank, host_comm=name.decode())
-        comm = "host shared memory (all ranks on GPU 0)"
+        if mode == "host":
+            ctx = P.Context(0, nranks=ws, rank=rank, host_comm=name.decode())
+            comm = "host shared memory (all ranks on GPU 0)"
+        else:
+            dev = local if mode == "ipc" else 0
+            ctx = P.Context(dev, nranks=ws, rank=rank, ipc_comm=name.decode())
+            comm = "CUDA-IPC device mailboxes" + (" (all ranks on GPU 0)" if mode == "ipc_local" else "")
     elif ws > 1 or os.environ.get("PCGX_BENCH_DIST") == "1":
         nid = D.bcast_bytes(P.Context.nccl_unique_id() if rank == 0 else None)
         ctx = P.Context(local, nranks=ws, rank=rank, nccl_id=nid, dist=True)

@@ -89,6 +89,17 @@ pcgx_status pcgx_local_group_create(int nranks, const int* devices, pcgx_context
  * ranks on one device); scalars are summed in rank order. */
 pcgx_status pcgx_context_create_host(int device, int nranks, int rank, const char* name,
                                      size_t mailbox_bytes, pcgx_context* out);
+/* One rank of an nranks-process job on ONE node whose ranks exchange through
+ * DEVICE memory: each rank exports a device mailbox and its events by CUDA IPC;
+ * halo planes, block-row segments and scalars are copied stream-ordered into the
+ * sender's mailbox and pulled by the receivers' streams (peer-to-peer over NVLink
+ * between GPUs), ordered by IPC events; the host only meets the peers at one
+ * shared-memory barrier (segment `name`) per exchange. Ranks may be on different
+ * GPUs (peer access required) or share one: no kernel waits on another rank.
+ * mailbox_bytes (0 = 64 MiB) bounds one message per rank; scalars are summed in
+ * rank order (bitwise pcgx_context_create_host / pcgx_local_group_create). */
+pcgx_status pcgx_context_create_ipc(int device, int nranks, int rank, const char* name,
+                                    size_t mailbox_bytes, pcgx_context* out);
 void pcgx_context_destroy(pcgx_context ctx);
 int pcgx_context_rank(pcgx_context ctx);
 int pcgx_context_nranks(pcgx_context ctx);

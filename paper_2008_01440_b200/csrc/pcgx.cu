@@ -20,6 +20,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <atomic>
 #include <condition_variable>
@@ -742,10 +743,258 @@ HostComm* host_comm_open(int nranks, int rank, const std::string& name, size_t c
   return hc.release();
 }
 
+// ---------------------------------------------------------------- peer-memory comm
+// IpcComm: P ranks in P processes on one node (one GPU each over NVLink / NVSwitch,
+// or sharing a GPU) exchanging through DEVICE memory: each rank exports a device
+// mailbox (two parity areas) and four events by CUDA IPC; every exchange is
+// stream-ordered -- the sender's stream copies its planes / segments / scalars
+// into its own mailbox and records `ready`, the receivers' streams wait on that
+// event and pull straight from the peer's mailbox into their ghost buffers (a
+// peer-to-peer copy over NVLink between GPUs), then record `done`. The host only
+// meets the peers at one shared-memory barrier per exchange (so each wait is
+// issued after the record it waits for); no host-side stream synchronisation, no
+// host staging, and the halo copies overlap the interior kernels like NCCL's.
+// No kernel ever waits on another rank (only streams wait on recorded events),
+// so ranks that share a GPU cannot deadlock it. Parity areas: an exchange reuses
+// the area of two exchanges ago only after every peer's `done` of that exchange
+// (the barrier in between orders the host calls). Scalars are summed in rank
+// order by peer_sum_kernel (bitwise the LocalGroup / HostComm sums).
+__global__ void peer_sum_kernel(const double* const* boxes, long long area_off, int nranks, int slot, int count,
+                                double* S) {
+  const int i = threadIdx.x;
+  if (i < count) {
+    double s = 0.0;
+    for (int q = 0; q < nranks; ++q) s += boxes[q][area_off + i];
+    S[slot + i] = s;
+  }
+}
+
+struct IpcExport {
+  cudaIpcMemHandle_t box;
+  cudaIpcEventHandle_t ready[2], done[2];
+  int device;
+  long long cap;
+};
+
+struct IpcComm : CommBase {
+  std::unique_ptr<HostComm> hc;  // barrier + setup exchange + block-row directories
+  int rank = 0, nranks = 1, device = 0;
+  long long capd = 0;                    // doubles per parity area (kSlots scalars + data)
+  double* box = nullptr;                 // my mailbox: 2 parity areas
+  std::vector<double*> peer;             // every rank's mailbox as mapped here (peer[rank] = box)
+  const double** d_peer = nullptr;       // the same table on the device (peer_sum_kernel)
+  cudaEvent_t ready[2] = {}, done[2] = {};
+  std::vector<std::array<cudaEvent_t, 2>> pready, pdone;  // the peers' events, opened here
+  uint64_t seq = 0;
+
+  double* area(int q, int par) const { return peer[(size_t)q] + (size_t)par * capd; }
+  // host-side block-row directory of rank q for parity par (offset, count per rank)
+  int64_t* dir(int q, int par) const { return reinterpret_cast<int64_t*>(hc->box(q)) + (size_t)par * 2 * nranks; }
+  void need(long long doubles) const {
+    if (doubles > capd - kSlots)
+      fail(PCGX_ERR_UNSUPPORTED, "ipc comm: message of " + std::to_string(8 * doubles) + " bytes exceeds the " +
+                                     std::to_string(8 * (capd - kSlots)) + "-byte mailbox");
+  }
+  // Start exchange `seq` on stream st: the parity area is free once every peer has
+  // finished reading it (their `done` of two exchanges ago).
+  int begin(cudaStream_t st) {
+    const int par = (int)(seq++ & 1);
+    for (int q = 0; q < nranks; ++q)
+      if (q != rank) PCGX_CUDA(cudaStreamWaitEvent(st, pdone[(size_t)q][par], 0));
+    return par;
+  }
+  void publish(cudaStream_t st, int par) {
+    PCGX_CUDA(cudaEventRecord(ready[par], st));
+    hc->barrier();  // every rank's `ready` recorded before anyone waits on it
+  }
+  void finish(pcgx_context c, cudaStream_t st, int par, bool join) {
+    PCGX_CUDA(cudaEventRecord(done[par], st));
+    if (join) PCGX_CUDA(cudaEventRecord(c->ev_join, st));
+  }
+  void copy(double* dst, const double* src, long long count, cudaStream_t st) {
+    if (count > 0) PCGX_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * (size_t)count, cudaMemcpyDefault, st));
+  }
+
+  ~IpcComm() override {
+    if (!hc) return;
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();  // my streams no longer touch the peers' mailboxes
+    try {
+      hc->barrier();
+    } catch (...) {
+    }
+    for (int q = 0; q < nranks; ++q) {
+      if (q == rank) continue;
+      if (peer[(size_t)q]) cudaIpcCloseMemHandle(peer[(size_t)q]);
+      for (int par = 0; par < 2; ++par) {
+        if (pready[(size_t)q][par]) cudaEventDestroy(pready[(size_t)q][par]);
+        if (pdone[(size_t)q][par]) cudaEventDestroy(pdone[(size_t)q][par]);
+      }
+    }
+    try {
+      hc->barrier();  // nobody maps my mailbox any more
+    } catch (...) {
+    }
+    for (int par = 0; par < 2; ++par) {
+      if (ready[par]) cudaEventDestroy(ready[par]);
+      if (done[par]) cudaEventDestroy(done[par]);
+    }
+    if (d_peer) cudaFree(d_peer);
+    if (box) cudaFree(box);
+  }
+
+  void allreduce(pcgx_context c, int slot, int count) override {
+    cudaStream_t st = c->s;
+    const int par = begin(st);
+    copy(area(rank, par), c->S + slot, count, st);
+    publish(st, par);
+    for (int q = 0; q < nranks; ++q)
+      if (q != rank) PCGX_CUDA(cudaStreamWaitEvent(st, pready[(size_t)q][par], 0));
+    peer_sum_kernel<<<1, 32, 0, st>>>(d_peer, (long long)par * capd, nranks, slot, count, c->S);
+    check_launch();
+    finish(c, st, par, false);
+  }
+  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override {
+    (void)op;
+    long long tot = 0;
+    for (int i = 0; i < n; ++i) tot += 2 * items[i].count;
+    need(tot);
+    PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+    PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+    cudaStream_t st = c->cs;
+    const int par = begin(st);
+    double* mine = area(rank, par) + kSlots;
+    long long off = 0;
+    for (int i = 0; i < n; ++i) {  // my area: [bottom planes | top planes] per item
+      if (rank > 0) copy(mine + off, items[i].send_lo, items[i].count, st);
+      if (rank < nranks - 1) copy(mine + off + items[i].count, items[i].send_hi, items[i].count, st);
+      off += 2 * items[i].count;
+    }
+    publish(st, par);
+    if (rank > 0) PCGX_CUDA(cudaStreamWaitEvent(st, pready[(size_t)rank - 1][par], 0));
+    if (rank < nranks - 1) PCGX_CUDA(cudaStreamWaitEvent(st, pready[(size_t)rank + 1][par], 0));
+    off = 0;
+    for (int i = 0; i < n; ++i) {  // rank-1's top -> my recv_lo, rank+1's bottom -> my recv_hi
+      if (rank > 0 && items[i].recv_lo)
+        copy(items[i].recv_lo, area(rank - 1, par) + kSlots + off + items[i].count, items[i].count, st);
+      if (rank < nranks - 1 && items[i].recv_hi)
+        copy(items[i].recv_hi, area(rank + 1, par) + kSlots + off, items[i].count, st);
+      off += 2 * items[i].count;
+    }
+    finish(c, st, par, true);
+  }
+  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override {
+    const long long nxy = op->nx * op->ny, nzl = op->nzl;
+    PlaneX items[2];
+    for (int v = 0; v < nv && v < 2; ++v)
+      items[v] = {xs[v], v ? op->ghost_lo2 : op->ghost_lo, xs[v] + (nzl - 1) * nxy,
+                  v ? op->ghost_hi2 : op->ghost_hi, nxy};
+    xchg(c, op, items, std::min(nv, 2));
+  }
+  void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
+  void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
+                   double* const* gbuf) override {
+    const int P = nranks;
+    PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+    PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+    cudaStream_t st = c->cs;
+    const int par = begin(st);
+    int64_t* d = dir(rank, par);  // host directory: where my segment for rank q starts, its length
+    for (int q = 0; q < 2 * P; ++q) d[q] = 0;
+    double* mine = area(rank, par) + kSlots;
+    long long off = 0;
+    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
+      const int q = op->nb_rank[i];
+      d[q] = off;
+      d[P + q] = op->send_cnt[i];
+      need(off + (long long)nv * op->send_cnt[i]);
+      for (int v = 0; v < nv; ++v) {
+        copy(mine + off, sbuf[v] + op->send_off[i], op->send_cnt[i], st);
+        off += op->send_cnt[i];
+      }
+    }
+    publish(st, par);
+    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
+      const int q = op->nb_rank[i];
+      const int64_t* qd = dir(q, par);
+      const int64_t qoff = qd[rank], qcnt = qd[P + rank];
+      if (qcnt != op->recv_cnt[i]) fail(PCGX_ERR_NCCL, "ipc comm: block-row segment size mismatch");
+      if (!qcnt) continue;
+      PCGX_CUDA(cudaStreamWaitEvent(st, pready[(size_t)q][par], 0));
+      for (int v = 0; v < nv; ++v)
+        copy(gbuf[v] + op->recv_off[i], area(q, par) + kSlots + qoff + (long long)v * qcnt, qcnt, st);
+    }
+    finish(c, st, par, true);
+  }
+  bool graph_capturable() const override { return false; }
+};
+
+IpcComm* ipc_comm_open(pcgx_context c, const std::string& name, size_t mailbox_bytes) {
+  auto ic = std::make_unique<IpcComm>();
+  const int P = c->nranks;
+  ic->rank = c->rank;
+  ic->nranks = P;
+  ic->device = c->device;
+  // the shared-memory segment holds the setup exports and two block-row directories
+  const size_t hbox = std::max(sizeof(IpcExport), (size_t)4 * P * sizeof(int64_t));
+  ic->hc.reset(host_comm_open(P, c->rank, name, hbox));
+  ic->capd = (long long)((mailbox_bytes + 127) / 128 * 16) + kSlots;  // 128-byte aligned areas
+  PCGX_CUDA(cudaMalloc(&ic->box, sizeof(double) * 2 * (size_t)ic->capd));
+  IpcExport ex{};
+  PCGX_CUDA(cudaIpcGetMemHandle(&ex.box, ic->box));
+  for (int par = 0; par < 2; ++par) {
+    PCGX_CUDA(cudaEventCreateWithFlags(&ic->ready[par], cudaEventDisableTiming | cudaEventInterprocess));
+    PCGX_CUDA(cudaEventCreateWithFlags(&ic->done[par], cudaEventDisableTiming | cudaEventInterprocess));
+    PCGX_CUDA(cudaIpcGetEventHandle(&ex.ready[par], ic->ready[par]));
+    PCGX_CUDA(cudaIpcGetEventHandle(&ex.done[par], ic->done[par]));
+  }
+  ex.device = c->device;
+  ex.cap = ic->capd;
+  std::memcpy(ic->hc->box(c->rank), &ex, sizeof ex);
+  ic->hc->barrier();
+  ic->peer.assign((size_t)P, nullptr);
+  ic->pready.assign((size_t)P, {nullptr, nullptr});
+  ic->pdone.assign((size_t)P, {nullptr, nullptr});
+  ic->peer[(size_t)c->rank] = ic->box;
+  for (int q = 0; q < P; ++q) {
+    if (q == c->rank) continue;
+    IpcExport qe;
+    std::memcpy(&qe, ic->hc->box(q), sizeof qe);
+    if (qe.cap != ic->capd) fail(PCGX_ERR_INVALID, "ipc comm: ranks disagree on the mailbox size");
+    if (qe.device != c->device) {
+      int can = 0;
+      PCGX_CUDA(cudaDeviceCanAccessPeer(&can, c->device, qe.device));
+      if (!can)
+        fail(PCGX_ERR_UNSUPPORTED, "ipc comm: device " + std::to_string(c->device) + " cannot access device " +
+                                       std::to_string(qe.device) + " (peer access)");
+    }
+    void* m = nullptr;
+    PCGX_CUDA(cudaIpcOpenMemHandle(&m, qe.box, cudaIpcMemLazyEnablePeerAccess));
+    ic->peer[(size_t)q] = static_cast<double*>(m);
+    for (int par = 0; par < 2; ++par) {
+      PCGX_CUDA(cudaIpcOpenEventHandle(&ic->pready[(size_t)q][par], qe.ready[par]));
+      PCGX_CUDA(cudaIpcOpenEventHandle(&ic->pdone[(size_t)q][par], qe.done[par]));
+    }
+  }
+  PCGX_CUDA(cudaMalloc(&ic->d_peer, sizeof(double*) * (size_t)P));
+  PCGX_CUDA(cudaMemcpy(ic->d_peer, ic->peer.data(), sizeof(double*) * (size_t)P, cudaMemcpyHostToDevice));
+  ic->hc->barrier();  // every rank has read the exports: the segment's boxes become directories
+  return ic.release();
+}
+
 void allreduce(pcgx_context c, int slot, int count) {
   if (!c->cm) return;
   c->cm->allreduce(c, slot, count);
   c->cur_allreduce++;
+}
+
+// Sum k <= 5 host doubles over the ranks through the scratch slots S_DOT..S_E2 (setup
+// checks), stream-ordered on c->s: the comms' all-reduces are asynchronous there.
+void allreduce_host(pcgx_context c, const double* in, double* out, int k) {
+  PCGX_CUDA(cudaMemcpyAsync(c->S + S_DOT, in, sizeof(double) * k, cudaMemcpyHostToDevice, c->s));
+  allreduce(c, S_DOT, k);
+  PCGX_CUDA(cudaMemcpyAsync(out, c->S + S_DOT, sizeof(double) * k, cudaMemcpyDeviceToHost, c->s));
+  PCGX_CUDA(cudaStreamSynchronize(c->s));
 }
 
 // ---------------------------------------------------------------- operator launch
@@ -3241,10 +3490,8 @@ void csr_upload_local(pcgx_context c, pcgx_operator op, long long n, long long r
   // left waiting in the exchange below)
   {
     const double flag = bad >= 0 ? 1.0 : 0.0;
-    PCGX_CUDA(cudaMemcpy(c->S + S_DOT, &flag, sizeof flag, cudaMemcpyHostToDevice));
-    allreduce(c, S_DOT, 1);
     double any = 0.0;
-    PCGX_CUDA(cudaMemcpy(&any, c->S + S_DOT, sizeof any, cudaMemcpyDeviceToHost));
+    allreduce_host(c, &flag, &any, 1);
     if (bad >= 0) fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry at index " + std::to_string(bad));
     if (any > 0.0) fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry on another rank");
   }
@@ -3298,9 +3545,7 @@ void csr_upload_local(pcgx_context c, pcgx_operator op, long long n, long long r
     const int chunk = S_E2 - S_DOT + 1;  // scratch slots S_DOT .. S_E2
     for (size_t b0 = 0; b0 < cnt.size(); b0 += (size_t)chunk) {
       const int k = (int)std::min<size_t>((size_t)chunk, cnt.size() - b0);
-      PCGX_CUDA(cudaMemcpy(c->S + S_DOT, cnt.data() + b0, sizeof(double) * k, cudaMemcpyHostToDevice));
-      allreduce(c, S_DOT, k);
-      PCGX_CUDA(cudaMemcpy(cnt.data() + b0, c->S + S_DOT, sizeof(double) * k, cudaMemcpyDeviceToHost));
+      allreduce_host(c, cnt.data() + b0, cnt.data() + b0, k);
     }
     for (int a = 0; a < P; ++a)
       for (int q = 0; q < P; ++q)
@@ -3953,6 +4198,23 @@ pcgx_status pcgx_context_create_host(int device, int nranks, int rank, const cha
     if (nranks > 1)
       c->cm = host_comm_open(nranks, rank, name[0] == '/' ? std::string(name) : "/" + std::string(name),
                              mailbox_bytes ? mailbox_bytes : ((size_t)64 << 20));
+    *out = c.release();
+  });
+}
+
+pcgx_status pcgx_context_create_ipc(int device, int nranks, int rank, const char* name, size_t mailbox_bytes,
+                                    pcgx_context* out) {
+  return guarded(nullptr, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks || !name || !out)
+      fail(PCGX_ERR_INVALID, "context_create_ipc: bad rank/nranks/name");
+    auto c = std::make_unique<pcgx_context_s>();
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    ctx_init(c.get());
+    if (nranks > 1)
+      c->cm = ipc_comm_open(c.get(), name[0] == '/' ? std::string(name) : "/" + std::string(name),
+                            mailbox_bytes ? mailbox_bytes : ((size_t)64 << 20));
     *out = c.release();
   });
 }

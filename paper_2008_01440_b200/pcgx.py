@@ -133,6 +133,7 @@ FLAG_NO_GRAPH = 2
 SYMBOLS = [
     "pcgx_abi_version", "pcgx_last_error", "pcgx_context_create", "pcgx_nccl_unique_id",
     "pcgx_context_create_dist", "pcgx_local_group_create", "pcgx_context_create_host",
+    "pcgx_context_create_ipc",
     "pcgx_context_destroy", "pcgx_context_rank",
     "pcgx_context_nranks", "pcgx_synchronize", "pcgx_kernel_launches", "pcgx_device_alloc",
     "pcgx_device_free", "pcgx_memcpy_h2d", "pcgx_memcpy_d2h", "pcgx_memcpy_d2d",
@@ -186,6 +187,8 @@ def lib():
         "pcgx_local_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(ctx)]),
         "pcgx_context_create_host": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t,
                                                C.POINTER(ctx)]),
+        "pcgx_context_create_ipc": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t,
+                                              C.POINTER(ctx)]),
         "pcgx_context_destroy": (None, [ctx]),
         "pcgx_context_rank": (C.c_int, [ctx]),
         "pcgx_context_nranks": (C.c_int, [ctx]),
@@ -290,7 +293,8 @@ class Context:
     one call at a time."""
 
     def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, nccl_id=None,
-                 dist: bool = False, host_comm: str | None = None, mailbox_bytes: int = 0,
+                 dist: bool = False, host_comm: str | None = None, ipc_comm: str | None = None,
+                 mailbox_bytes: int = 0,
                  _handle=None):
         L = lib()
         h = C.c_void_p()
@@ -301,6 +305,11 @@ class Context:
             # shared-memory segment `host_comm` (pcgx_context_create_host)
             _check(L.pcgx_context_create_host(device, nranks, rank, host_comm.encode(), mailbox_bytes,
                                               C.byref(h)))
+        elif ipc_comm is not None:
+            # one rank of a multi-process job on one node exchanging through CUDA-IPC
+            # device mailboxes, handshake segment `ipc_comm` (pcgx_context_create_ipc)
+            _check(L.pcgx_context_create_ipc(device, nranks, rank, ipc_comm.encode(), mailbox_bytes,
+                                             C.byref(h)))
         elif nranks == 1 and not dist:
             _check(L.pcgx_context_create(device, C.byref(h)))
         else:

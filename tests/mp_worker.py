@@ -1,7 +1,8 @@
 # SPDX-License-Identifier: Apache-2.0
 """One rank of a multi-PROCESS job on one GPU (tests/test_gpu_multiproc.py):
 pcgx_context_create_host -- halo planes, block-row segments and scalars through a
-shared-memory segment, no kernel waiting on another rank. Writes its slab /
+shared-memory segment -- or, with PCGX_MP_COMM=ipc, pcgx_context_create_ipc
+(CUDA-IPC device mailboxes ordered by IPC events); no kernel waits on another rank. Writes its slab /
 block of b = A x_true, P_m(A) r, the solution and the report to OUT/rank<r>.npz.
 
     python tests/mp_worker.py NAME NRANKS RANK OUT KIND NX NY NZ M
@@ -22,7 +23,10 @@ def main():
     name, nranks, rank, out, kind = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
     nx, ny, nz, m = (int(v) for v in sys.argv[6:10])
     from paper_2008_01440_b200 import pcgx as P
-    ctx = P.Context(0, nranks=nranks, rank=rank, host_comm=name)
+    if os.environ.get("PCGX_MP_COMM", "host") == "ipc":  # CUDA-IPC device mailboxes
+        ctx = P.Context(0, nranks=nranks, rank=rank, ipc_comm=name)
+    else:  # host shared memory
+        ctx = P.Context(0, nranks=nranks, rank=rank, host_comm=name)
     if kind == "stencil":
         op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
         a, b = P.analytic_extremes_box(nx, ny, nz)

@@ -1,8 +1,10 @@
 # SPDX-License-Identifier: Apache-2.0
 """The multi-rank algorithm across PROCESSES on one GPU: P Python processes, one
 pcgx context each (pcgx_context_create_host: halo planes, block-row segments and
-scalars through a POSIX shared-memory segment, host-staged -- no kernel or stream
-waits on another rank, so ranks sharing one GPU cannot deadlock it). This is the
+scalars through a POSIX shared-memory segment, host-staged; or
+pcgx_context_create_ipc: CUDA-IPC device mailboxes, stream-ordered by IPC events
+-- in neither does a kernel wait on another rank, so ranks sharing one GPU cannot
+deadlock it). This is the
 process layout of a torchrun job; only the transport differs from NCCL.
 
 SpMV and every Chebyshev step are elementwise exact across slabs / row blocks,
@@ -25,11 +27,12 @@ SEED = 20240801
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def run_job(nranks, kind, dims, m, tmp_path):
+def run_job(nranks, kind, dims, m, tmp_path, comm="host"):
     name = f"pcgx_test_{uuid.uuid4().hex[:12]}"
+    env = dict(os.environ, PCGX_MP_COMM=comm)
     procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), name, str(nranks), str(r),
                                str(tmp_path), kind, *map(str, dims), str(m)],
-                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, env=env)
              for r in range(nranks)]
     outs = []
     for p in procs:
@@ -46,11 +49,12 @@ def run_job(nranks, kind, dims, m, tmp_path):
     return res
 
 
+@pytest.mark.parametrize("comm", ["host", "ipc"])
 @pytest.mark.parametrize("nranks,dims,m", [(2, (24, 24, 24), 10), (3, (20, 16, 26), 5), (2, (64, 40, 33), 20)])
-def test_multiprocess_slabs_match_single_domain(pcgx, oracle, nranks, dims, m, tmp_path):
+def test_multiprocess_slabs_match_single_domain(pcgx, oracle, nranks, dims, m, comm, tmp_path):
     P = pcgx
     nx, ny, nz = dims
-    res = run_job(nranks, "stencil", dims, m, tmp_path)
+    res = run_job(nranks, "stencil", dims, m, tmp_path, comm)
     a, b = P.analytic_extremes_box(nx, ny, nz)
     opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
     xt = oracle.random_uniform(nx * ny * nz, SEED)
@@ -69,12 +73,14 @@ def test_multiprocess_slabs_match_single_domain(pcgx, oracle, nranks, dims, m, t
     assert all(r["halo_bytes"] > 0 for r in reps)
 
 
-def test_multiprocess_slabs_match_local_group(pcgx, tmp_path):
-    """Processes + shared memory and threads + stream-ordered copies run the same
-    algorithm with scalars summed in rank order: the solutions are bit-identical."""
+@pytest.mark.parametrize("comm", ["host", "ipc"])
+def test_multiprocess_slabs_match_local_group(pcgx, comm, tmp_path):
+    """Processes + shared memory (or CUDA-IPC device mailboxes) and threads +
+    stream-ordered copies run the same algorithm with scalars summed in rank order:
+    the solutions are bit-identical."""
     P = pcgx
     nx, ny, nz, m = 24, 20, 30, 8
-    res = run_job(3, "stencil", (nx, ny, nz), m, tmp_path)
+    res = run_job(3, "stencil", (nx, ny, nz), m, tmp_path, comm)
     ctxs = P.Context.local_group(3)
     from concurrent.futures import ThreadPoolExecutor
     a, b = P.analytic_extremes_box(nx, ny, nz)
@@ -94,9 +100,11 @@ def test_multiprocess_slabs_match_local_group(pcgx, tmp_path):
         c.close()
 
 
-@pytest.mark.parametrize("kind,nranks", [("fe27", 2), ("fe27_local", 2), ("fe27_local", 3), ("elast27", 2),
-                                         ("elast27", 3)])
-def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks, tmp_path):
+@pytest.mark.parametrize("kind,nranks,comm", [("fe27", 2, "host"), ("fe27_local", 2, "host"),
+                                              ("fe27_local", 3, "host"), ("elast27", 2, "host"),
+                                              ("elast27", 3, "host"), ("fe27", 3, "ipc"),
+                                              ("fe27_local", 3, "ipc"), ("elast27", 2, "ipc")])
+def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks, comm, tmp_path):
     """CSR block rows (the paper's distributed SpMV) across
     processes: per-neighbour packed halos through the shared segment; every rank
     given the full matrix ("fe27") or only its own rows ("fe27_local",
@@ -104,7 +112,7 @@ def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks,
     exchanged once)."""
     P = pcgx
     nx, m = (14, 6) if kind.startswith("fe27") else (8, 6)
-    res = run_job(nranks, kind, (nx, nx, nx), m, tmp_path)
+    res = run_job(nranks, kind, (nx, nx, nx), m, tmp_path, comm)
     if kind == "elast27":
         assert all(str(r["storage"]) == "bsr3" for r in res)
     if kind == "fe27":
