@@ -300,6 +300,7 @@ def run_gpu(args):
     D.barrier()
     l0 = ctx.kernel_launches
     times, mvs, reps = [], [], None
+    per_k_times = {}  # k -> time-to-1e-8 of every timed step (best / median, like the reference's --repeat)
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             D.barrier()
@@ -307,6 +308,8 @@ def run_gpu(args):
             t, mv, reps = sweep()
             times.append(t)
             mvs.append(mv)
+            for k, _, tk in reps:
+                per_k_times.setdefault(k, []).append(tk)
     launches = ctx.kernel_launches - l0
     clocks = clk.summary()
     t_step = float(np.mean(times))
@@ -349,6 +352,7 @@ def run_gpu(args):
     for k, rep, t in reps:
         per_k.append({"k": k, "iters": rep.iters, "ddot": rep.ddot, "matvec": rep.matvec,
                       "time_to_1e8_s": round(t, 6), "ms_per_iter": round(t * 1e3 / max(rep.iters, 1), 4),
+                      "best_s": round(min(per_k_times[k]), 6), "median_s": round(float(np.median(per_k_times[k])), 6),
                       "rel_res": rep.rel_res,
                       "true_rel_res": rep.true_rel_res, "converged": rep.converged,
                       "alg_GBps": round(D.sum(rep.alg_bytes) / t / 1e9, 1),
