@@ -588,10 +588,15 @@ struct HostComm : CommBase {
       }
     }
   }
+  // A rank that cannot continue marks the job aborted first, so the peers fail at
+  // their next barrier instead of waiting out the timeout.
+  void give_up() const { hdr()->abort.store(1, std::memory_order_release); }
   void need(size_t bytes) const {
-    if (bytes > cap)
+    if (bytes > cap) {
+      give_up();
       fail(PCGX_ERR_UNSUPPORTED, "host comm: message of " + std::to_string(bytes) + " bytes exceeds the " +
                                      std::to_string(cap) + "-byte mailbox");
+    }
   }
   ~HostComm() override {
     if (!base) return;
@@ -791,9 +796,11 @@ struct IpcComm : CommBase {
   // host-side block-row directory of rank q for parity par (offset, count per rank)
   int64_t* dir(int q, int par) const { return reinterpret_cast<int64_t*>(hc->box(q)) + (size_t)par * 2 * nranks; }
   void need(long long doubles) const {
-    if (doubles > capd - kSlots)
+    if (doubles > capd - kSlots) {
+      hc->give_up();
       fail(PCGX_ERR_UNSUPPORTED, "ipc comm: message of " + std::to_string(8 * doubles) + " bytes exceeds the " +
                                      std::to_string(8 * (capd - kSlots)) + "-byte mailbox");
+    }
   }
   // Start exchange `seq` on stream st: the parity area is free once every peer has
   // finished reading it (their `done` of two exchanges ago).
@@ -895,6 +902,9 @@ struct IpcComm : CommBase {
   void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
                    double* const* gbuf) override {
     const int P = nranks;
+    long long tot = 0;
+    for (size_t i = 0; i < op->nb_rank.size(); ++i) tot += (long long)nv * op->send_cnt[i];
+    need(tot);
     PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
     PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
     cudaStream_t st = c->cs;
@@ -907,7 +917,6 @@ struct IpcComm : CommBase {
       const int q = op->nb_rank[i];
       d[q] = off;
       d[P + q] = op->send_cnt[i];
-      need(off + (long long)nv * op->send_cnt[i]);
       for (int v = 0; v < nv; ++v) {
         copy(mine + off, sbuf[v] + op->send_off[i], op->send_cnt[i], st);
         off += op->send_cnt[i];

@@ -23,10 +23,11 @@ def main():
     name, nranks, rank, out, kind = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
     nx, ny, nz, m = (int(v) for v in sys.argv[6:10])
     from paper_2008_01440_b200 import pcgx as P
+    mb = int(os.environ.get("PCGX_MP_MAILBOX", "0"))  # bytes per message (0: the library default)
     if os.environ.get("PCGX_MP_COMM", "host") == "ipc":  # CUDA-IPC device mailboxes
-        ctx = P.Context(0, nranks=nranks, rank=rank, ipc_comm=name)
+        ctx = P.Context(0, nranks=nranks, rank=rank, ipc_comm=name, mailbox_bytes=mb)
     else:  # host shared memory
-        ctx = P.Context(0, nranks=nranks, rank=rank, host_comm=name)
+        ctx = P.Context(0, nranks=nranks, rank=rank, host_comm=name, mailbox_bytes=mb)
     if kind == "stencil":
         op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
         a, b = P.analytic_extremes_box(nx, ny, nz)

@@ -144,3 +144,22 @@ def test_multiprocess_local_rows_reject_asymmetric_pattern(pcgx, tmp_path):
     for r in range(2):
         msg = open(os.path.join(tmp_path, f"rank{r}.err")).read()
         assert "block rows are not symmetric" in msg, msg
+
+
+@pytest.mark.parametrize("comm", ["host", "ipc"])
+def test_multiprocess_small_mailbox_fails_every_rank_fast(pcgx, comm, tmp_path):
+    """A halo plane larger than the mailbox: the rank that finds out marks the job
+    aborted, so EVERY rank fails promptly (no rank waits out the barrier timeout)."""
+    import time
+    name = f"pcgx_test_{uuid.uuid4().hex[:12]}"
+    env = dict(os.environ, PCGX_MP_COMM=comm, PCGX_MP_MAILBOX="4096")
+    t0 = time.time()
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), name, "2", str(r),
+                               str(tmp_path), "stencil", "40", "40", "12", "4"],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, env=env)
+             for r in range(2)]
+    outs = [p.communicate(timeout=300)[0] for p in procs]
+    assert time.time() - t0 < 240
+    for p, o in zip(procs, outs):
+        assert p.returncode != 0, o
+        assert "mailbox" in o or "gave up" in o, o

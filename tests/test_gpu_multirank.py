@@ -96,14 +96,16 @@ def test_slab_lanczos_matches_single_domain(pcgx):
     single.close()
 
 
-@pytest.mark.parametrize("nranks,gen,m", [(2, "fe27", 6), (3, "elast27", 4), (4, "lap", 5)])
+@pytest.mark.parametrize("nranks,gen,m", [(2, "fe27", 6), (3, "elast27", 4), (4, "lap", 5), (4, "fe27_3", 4),
+                                          (3, "fe27_odd", 5)])
 def test_csr_block_rows_match_single_domain(pcgx, oracle, nranks, gen, m):
     """Multi-rank CSR (block rows + per-neighbour halo; SELL-32, or BSR-3 for the 3 x 3
     block matrix): SpMV and P_m(A) r bitwise equal to the single-domain oracle, the
     solve within the PCG bar."""
     P = pcgx
-    if gen == "fe27":
-        A = P.gen_fe27(10, 1.0, SEED)
+    nxg = {"fe27": 10, "fe27_3": 3, "fe27_odd": 7}.get(gen)
+    if nxg:  # fe27_3: fewer node planes than ranks -> row blocks (SELL); fe27_odd: ragged slabs
+        A = P.gen_fe27(nxg, 1.0, SEED)
     elif gen == "elast27":
         A = P.gen_elast27(6, 1.0, 0.5, 0.1, SEED)
     else:
@@ -128,9 +130,9 @@ def test_csr_block_rows_match_single_domain(pcgx, oracle, nranks, gen, m):
         if gen == "elast27":  # 3 x 3 blocks: whole block rows per rank, BSR-3 kept
             z0, nb = P.slab_partition(n // 3, nranks, r)
             assert (lo, op.local_size()) == (3 * z0, 3 * nb) and op.storage() == "bsr3"
-        elif gen == "fe27":  # 27-point box on the 10^3 grid: node-plane slabs, grid-tile offset storage
-            z0, nzl = P.slab_partition(10, nranks, r)
-            assert (lo, op.local_size()) == (100 * z0, 100 * nzl) and op.storage() == "dia_grid"
+        elif gen in ("fe27", "fe27_odd"):  # 27-point box on an nx^3 grid: node-plane slabs, grid-tile offsets
+            z0, nzl = P.slab_partition(nxg, nranks, r)
+            assert (lo, op.local_size()) == (nxg * nxg * z0, nxg * nxg * nzl) and op.storage() == "dia_grid"
         else:
             assert (lo, op.local_size()) == P.slab_partition(n, nranks, r)
         bl = op.apply(P.random_uniform_vector(op.local_size(), SEED, offset=lo))
@@ -147,7 +149,11 @@ def test_csr_block_rows_match_single_domain(pcgx, oracle, nranks, gen, m):
     assert all(r.iters == reps[0].iters for r in reps) and reps[0].converged
     assert abs(reps[0].iters - rep_o["iters"]) <= 1
     if reps[0].iters == rep_o["iters"]:
-        assert rel_norm(np.concatenate([o[2] for o in outs]), x_full) <= 1e-10
+        # 27 unknowns (fe27_3): a handful of iterations on a tiny system, where the
+        # per-rank reduction order moves x by ~5e-10 relative; the elementwise work
+        # above is still bitwise
+        tol = 1e-8 if n < 100 else 1e-10
+        assert rel_norm(np.concatenate([o[2] for o in outs]), x_full) <= tol
     assert all(r.halo_bytes > 0 for r in reps)
     olo, _, al, be = oracle.lanczos(opo, 15, SEED)
     _, ohi = oracle.tridiag_extremes(al[:10], be[:10])
