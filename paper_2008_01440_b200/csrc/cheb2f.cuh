@@ -33,9 +33,18 @@ namespace pcgx {
 #ifndef PCGX_C2F_NOMATH
 #define PCGX_C2F_NOMATH 0
 #endif
+// Power-ceiling experiments (tools/build_variant.py, never the product, NOT bitwise):
+// 1: no j-neighbour shared loads; 2: no i-neighbour loads either; 3: + no i-halo
+// columns; 4: + no stencil arithmetic (the pass keeps its TMA boxes, one shared
+// load per operand, the recurrence and the stores)
+#ifndef PCGX_C2F_EXP
+#define PCGX_C2F_EXP 0
+#endif
 __device__ __forceinline__ double c2f_stencil(double d, double a, double b, double c, double e, double f,
                                               double g, double h) {
-#if PCGX_C2F_NOMATH
+#if PCGX_C2F_EXP >= 4
+  return d * e + (a * 0.0 + b * 0.0 + c * 0.0 + f * 0.0 + g * 0.0 + h * 0.0) * 0.0 == 0.0 ? d * e : e;
+#elif PCGX_C2F_NOMATH
   (void)d;
   const long long x = __double_as_longlong(a) ^ __double_as_longlong(b) ^ __double_as_longlong(c) ^
                       __double_as_longlong(e) ^ __double_as_longlong(f) ^ __double_as_longlong(g) ^
@@ -300,7 +309,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         acc_rr = acc_rr + ap.y * ap.y;
       }
       double aw, ae;
-      if (PCGX_C2FNBR && (!kUpd || kIP)) {
+      if (PCGX_C2F_EXP >= 2) {
+        aw = ac.y;
+        ae = ac.x;
+      } else if (PCGX_C2FNBR && (!kUpd || kIP)) {
         aw = pAu[offA - 1];
         ae = pAu[offA + 2];
       } else {
@@ -317,8 +329,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (lane == 31) ae = rq(pAu, offA + 2);
 #endif
       }
-      const double2 as = rqx2(pAu, offA - kFW);
-      const double2 an = rqx2(pAu, offA + kFW);
+      const double2 as = PCGX_C2F_EXP >= 1 ? ac : rqx2(pAu, offA - kFW);
+      const double2 an = PCGX_C2F_EXP >= 1 ? ac : rqx2(pAu, offA + kFW);
       const double2 xc = ac;  // A[t] at the pair
       const double y0 = c2f_stencil(d, am.x, as.x, aw, ac.x, ac.y, an.x, ap.x);
       const double y1 = c2f_stencil(d, am.y, as.y, ac.x, ac.y, ae, an.y, ap.y);
@@ -342,7 +354,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       }
       *reinterpret_cast<double2*>(pCu + offB) = cv;
       // i-halo columns of C[t] (read by stage 2 of plane t, two iterations on)
-      if (do_h) {
+      if (PCGX_C2F_EXP < 3 && do_h) {
         double hx = 0.0;
         if (plane_in && h_in) {
           const double xc = rqx(pAu, offAh);
@@ -358,7 +370,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     // ---------------- stage 2: E[t-2] on the own tile row (warps 1..8)
     if (interior && t - 2 >= kb) {
       double cw, ce;
-      if (PCGX_C2FNBR) {
+      if (PCGX_C2F_EXP >= 2) {
+        cw = c2.y;
+        ce = c2.x;
+      } else if (PCGX_C2FNBR) {
         cw = pC2[offB - 1];
         ce = pC2[offB + 2];
       } else {
@@ -375,8 +390,8 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (lane == 31) ce = pC2[offB + 2];
 #endif
       }
-      const double2 cs = *reinterpret_cast<const double2*>(pC2 + offB - kFW);
-      const double2 cn = *reinterpret_cast<const double2*>(pC2 + offB + kFW);
+      const double2 cs = PCGX_C2F_EXP >= 1 ? c2 : *reinterpret_cast<const double2*>(pC2 + offB - kFW);
+      const double2 cn = PCGX_C2F_EXP >= 1 ? c2 : *reinterpret_cast<const double2*>(pC2 + offB + kFW);
       const double y0 = c2f_stencil(d, c3.x, cs.x, cw, c2.x, c2.y, cn.x, c1.x);
       const double y1 = c2f_stencil(d, c3.y, cs.y, c2.x, c2.y, ce, cn.y, c1.y);
       const double2 cc = c2;  // C[t-2] at the pair

@@ -70,7 +70,7 @@ struct Tuning {
   int bsr3t = 1, bsr3t_modes = 1, bsr3t_kz = 32;
   int csr_stencil = 0;
   // stencil kernels
-  int kz = 0, kz2 = 32, pfd = 2, cheb2 = 1, cheb3 = 0, dir_tma = 1;
+  int kz = 0, kz2 = 32, pfd = 2, cheb2 = 1, cheb3 = 2, dir_tma = 1;
   std::string c2plan;  // "" automatic chunk plan, "u" uniform kz2, "h1,h2,..." explicit
   // PCG schedule
   int fuse_upd = 1, no_graph = 0, graph_multi = 0, merged = 0, cond_graph = 10, no_fuse_p = 0, zdiv = 1,
@@ -2197,7 +2197,10 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
         if (b != iold && b != icur) (fa < 0 ? fa : fb) = b;
     };
     int k = 3;
-    if (cheb3_ok(c, op)) {
+    // PCGX_CHEB3=2: two-step passes, and an odd m ends with ONE three-step pass
+    // (steps m-2 .. m, 32 B per unknown) instead of a two-step pass + a single step
+    const bool tail3 = cheb3_ok(c, op) && op->tune.cheb3 == 2 && (P.m % 2) == 1 && P.m >= 5;
+    if (cheb3_ok(c, op) && op->tune.cheb3 != 2) {
       // three steps per pass (cheb3.cuh); the m - 2 remaining steps split into
       // three-step passes and at most two two-step passes (never a single step
       // unless m == 3)
@@ -2245,6 +2248,7 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
       }
     }
     for (; k + 1 <= P.m; k += 2) {
+      if (tail3 && k + 2 == P.m) break;
       const bool last = (k + 1 == P.m);
       int fc, fe;
       free_pair(fc, fe);
@@ -2258,6 +2262,22 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
       else cheb2_pass<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1);
       iold = fc;
       icur = fe;
+    }
+    if (tail3 && k + 2 == P.m) {
+      Cheb3Params q3{};
+      q3.c2 = c2;
+      q3.c3 = c3;
+      q3.rk1 = P.rho[k];
+      q3.rk1m1 = P.rho[k - 1];
+      q3.rk2 = P.rho[k + 1];
+      q3.rk2m1 = P.rho[k];
+      q3.rk3 = P.rho[k + 2];
+      q3.rk3m1 = P.rho[k + 1];
+      q3.outE = nullptr;
+      q3.outF = out;
+      if (rz_slot >= 0) cheb3_pass<true>(c, op, bufs[icur], bufs[iold], r, q3, rz_slot);
+      else cheb3_pass<false>(c, op, bufs[icur], bufs[iold], r, q3, -1);
+      k += 3;
     }
     if (k == P.m) {  // odd remainder: x_m = step(x_{m-1}, x_{m-2}) -> out
       EpiChebStep e{r, bufs[iold], out, P.rho[k], P.rho[k - 1], c2, c3, P.theta, 0, 1.0 / P.theta};
@@ -2975,7 +2995,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
     }
     EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0,
                   1.0 / P.theta};
-    const bool three = two && cheb3_ok(c, op) && m >= 5;
+    const bool three = two && cheb3_ok(c, op) && op->tune.cheb3 == 1 && m >= 5;
     Cheb3Params q3{};
     q3.c2 = 2.0 / P.delta;
     q3.c3 = 2.0 * P.sigma;

@@ -585,6 +585,33 @@ def test_cheb3_pcg_matches_two_step_path(P, ctx, oracle, m, monkeypatch):
     assert r3.kernel_launches < r2.kernel_launches
 
 
+@pytest.mark.parametrize("dims", [(48, 48, 48), (130, 47, 41), (66, 10, 9), (64, 16, 1)])
+def test_cheb3_tail_default_bitwise(P, ctx, oracle, dims, monkeypatch):
+    """The default schedule ends an odd degree m >= 5 with ONE three-step pass (steps
+    m-2 .. m; PCGX_CHEB3=2) instead of a two-step pass plus a single step: fewer
+    launches, bitwise the oracle and the two-step + single-step schedule."""
+    nx, ny, nz = dims
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+    r = oracle.random_uniform(nx * ny * nz, 17)
+    opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
+    monkeypatch.delenv("PCGX_CHEB3", raising=False)
+    op_t = stencil(P, ctx, nx, ny, nz)
+    monkeypatch.setenv("PCGX_CHEB3", "0")
+    op_s = stencil(P, ctx, nx, ny, nz)
+    for m in (5, 7, 9, 21):
+        prm = P.cheb_params(a, b, m, 1.001)
+        out_t = P.apply_chebyshev(prm, op_t, r)
+        out_s = P.apply_chebyshev(prm, op_s, r)
+        ref = oracle.apply_chebyshev(opo, oracle.cheb_params(a, b, m, 1.001), r)
+        assert np.array_equal(out_t, ref) and np.array_equal(out_s, ref), (dims, m)
+    rhs = op_t.apply(P.random_uniform_vector(nx * ny * nz, SEED))
+    prec = P.ChebyshevPreconditioner(P.cheb_params(a, b, 5, 1.001))
+    xt, rt = P.pcg_solve(op_t, rhs, None, prec)
+    xs, rs = P.pcg_solve(op_s, rhs, None, prec)
+    assert rt.iters == rs.iters and rel_norm(xt, xs) <= 1e-12
+    assert rt.kernel_launches < rs.kernel_launches
+
+
 def test_cheb2_matches_single_step_path(P, ctx, monkeypatch):
     monkeypatch.setenv("PCGX_CHEB2", "1")
     nx = 40
