@@ -152,8 +152,12 @@ pcgx_status pcgx_csr_create(pcgx_context ctx, int64_t n, const int64_t* row_ptr,
 /* Block-row CsrMatrix from THIS rank's rows only (no rank holds the full matrix;
  * the paper's distributed layout): rows [row0, row0 + n_local)
  * of a symmetric n x n matrix, row0 / n_local = pcgx_slab_partition(n, nranks,
- * rank); row_ptr has n_local+1 entries (any base), col_idx global, ascending per
- * row. The symmetric pattern gives every rank its send / receive lists without
+ * rank) -- or, on every rank alike, the partitions pcgx_csr_create cuts a full
+ * matrix by to keep its fast storages: whole 3 x 3 block rows (3 x
+ * pcgx_slab_partition(n / 3, ...): BSR-3) or whole node planes of an nx^3 grid
+ * (nx^2 x pcgx_slab_partition(nx, ...): the offset storage on z-slabs, for the
+ * 27-point box). row_ptr has n_local+1 entries (any base), col_idx global,
+ * ascending per row. The symmetric pattern gives every rank its send / receive lists without
  * communication; the ghost columns' Jacobi values (inv_sqrt_diag: this rank's
  * n_local entries, or NULL = computed from the local diagonal) are exchanged once.
  * Bitwise the same operator as pcgx_csr_create with the full matrix. A single-rank

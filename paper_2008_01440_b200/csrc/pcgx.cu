@@ -3285,10 +3285,11 @@ void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
 void build_bsr3(pcgx_operator op, long long n, const std::vector<int>& rp32,
                 const std::vector<int>& ci32, const double* va);
 bool is_bsr3(long long n, const std::vector<int>& rp, const std::vector<int>& ci);
-bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>& ci, std::vector<int>& off);
+bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>& ci, std::vector<int>& off,
+                 long long row_base = 0);
 template <int P>
 bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vector<int>& ci,
-                const std::vector<int>& off);
+                const std::vector<int>& off, long long row_base = 0);
 
 // Offset storage of one plane-aligned z-slab of a 27-point-box matrix on an nx^3
 // grid (multi-rank cfg3): the rank owns node planes [z0, z0 + nzl) (pcgx_slab_partition
@@ -3296,13 +3297,16 @@ bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vect
 // Jacobi values of its rows and of the neighbours' boundary planes (from the full
 // matrix: no exchange), and x-ghost planes the stencil slab machinery fills before
 // each SpMV (dia3_kernel reads them as planes -1 and nzl).
+// local: rp32 / va / dv hold this rank's rows only (rp32 from 0, ci32 global); the
+// neighbours' boundary-plane Jacobi values then come through the plane exchange.
 void dia_slab_upload(pcgx_context c, pcgx_operator op, long long n, int nx, const std::vector<int>& rp32,
                      const std::vector<int>& ci32, const double* va, const std::vector<double>& dv,
-                     const std::vector<int>& off) {
+                     const std::vector<int>& off, bool local = false) {
   const int P = c->nranks, me = c->rank;
   int64_t z0 = 0, nzl = 0;
   pcgx_slab_partition(nx, P, me, &z0, &nzl);
   const long long nxy = (long long)nx * nx, r0 = z0 * nxy, nloc = nzl * nxy;
+  const long long rb = local ? r0 : 0;  // rp32 / dv index of global row g: g - rb
   const int K = (int)off.size();
   const long long ld = (nloc + 31) / 32 * 32;
   std::vector<double> val((size_t)(ld * K), 0.0);
@@ -3311,7 +3315,7 @@ void dia_slab_upload(pcgx_context c, pcgx_operator op, long long n, int nx, cons
   for (long long i = 0; i < nloc; ++i) {
     const long long g = r0 + i;
     int q = 0;
-    for (int k = rp32[(size_t)g]; k < rp32[(size_t)g + 1]; ++k) {
+    for (int k = rp32[(size_t)(g - rb)]; k < rp32[(size_t)(g - rb) + 1]; ++k) {
       const int o = (int)((long long)ci32[(size_t)k] - g);
       while (off[(size_t)q] != o) ++q;  // both ascending
       val[(size_t)(q * ld + i)] = va[k];
@@ -3320,7 +3324,7 @@ void dia_slab_upload(pcgx_context c, pcgx_operator op, long long n, int nx, cons
   }
   op->kind = 1;
   op->n_global = n;
-  op->nnz = (long long)rp32[(size_t)(r0 + nloc)] - rp32[(size_t)r0];
+  op->nnz = (long long)rp32[(size_t)(r0 - rb + nloc)] - rp32[(size_t)(r0 - rb)];
   op->row0 = r0;
   op->n_local = nloc;
   op->dia_k = K;
@@ -3338,16 +3342,27 @@ void dia_slab_upload(pcgx_context c, pcgx_operator op, long long n, int nx, cons
   PCGX_CUDA(cudaMemcpy(op->dia_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
   PCGX_CUDA(cudaMemcpy(op->dia_mask, mask.data(), sizeof(unsigned) * mask.size(), cudaMemcpyHostToDevice));
   PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * (size_t)std::max(nloc, 1LL)));
-  PCGX_CUDA(cudaMemcpy(op->dvec, dv.data() + r0, sizeof(double) * (size_t)nloc, cudaMemcpyHostToDevice));
-  if (me > 0) {
-    PCGX_CUDA(cudaMalloc(&op->dia3_dlo, sizeof(double) * (size_t)nxy));
-    PCGX_CUDA(cudaMemcpy(op->dia3_dlo, dv.data() + r0 - nxy, sizeof(double) * (size_t)nxy, cudaMemcpyHostToDevice));
-  }
-  if (me < P - 1) {
-    PCGX_CUDA(cudaMalloc(&op->dia3_dhi, sizeof(double) * (size_t)nxy));
-    PCGX_CUDA(cudaMemcpy(op->dia3_dhi, dv.data() + r0 + nloc, sizeof(double) * (size_t)nxy, cudaMemcpyHostToDevice));
-  }
+  PCGX_CUDA(cudaMemcpy(op->dvec, dv.data() + (r0 - rb), sizeof(double) * (size_t)nloc, cudaMemcpyHostToDevice));
+  if (me > 0) PCGX_CUDA(cudaMalloc(&op->dia3_dlo, sizeof(double) * (size_t)nxy));
+  if (me < P - 1) PCGX_CUDA(cudaMalloc(&op->dia3_dhi, sizeof(double) * (size_t)nxy));
   init_stencil_ghosts(c, op);  // x / p ghost planes (nx * nx) for the plane exchange
+  if (!local) {
+    if (me > 0)
+      PCGX_CUDA(cudaMemcpy(op->dia3_dlo, dv.data() + r0 - nxy, sizeof(double) * (size_t)nxy, cudaMemcpyHostToDevice));
+    if (me < P - 1)
+      PCGX_CUDA(cudaMemcpy(op->dia3_dhi, dv.data() + r0 + nloc, sizeof(double) * (size_t)nxy, cudaMemcpyHostToDevice));
+    return;
+  }
+  // the neighbours' boundary planes of d, once, through the operator's own plane exchange
+  PCGX_CUDA(cudaDeviceSynchronize());  // legacy-stream uploads before the compute / comm streams
+  const double* xs[1] = {op->dvec};
+  c->cm->halo_begin(c, op, xs, 1);
+  c->cm->halo_wait(c);
+  if (me > 0)
+    PCGX_CUDA(cudaMemcpyAsync(op->dia3_dlo, op->ghost_lo, sizeof(double) * (size_t)nxy, cudaMemcpyDeviceToDevice, c->s));
+  if (me < P - 1)
+    PCGX_CUDA(cudaMemcpyAsync(op->dia3_dhi, op->ghost_hi, sizeof(double) * (size_t)nxy, cudaMemcpyDeviceToDevice, c->s));
+  PCGX_CUDA(cudaStreamSynchronize(c->s));
 }
 
 // CSR block rows (the paper's MPI block-row SpMV): this rank
@@ -3476,19 +3491,80 @@ template <class I>
 void csr_upload_local(pcgx_context c, pcgx_operator op, long long n, long long r0, long long nloc, const I* rp,
                       const I* ci, const double* va, const double* isd) {
   const int P = c->nranks, me = c->rank;
-  std::vector<long long> start(P + 1);
-  for (int q = 0; q < P; ++q) {
-    int64_t z0, nl;
-    pcgx_slab_partition(n, P, q, &z0, &nl);
-    start[(size_t)q] = z0;
-  }
-  start[(size_t)P] = n;
-  if (r0 != start[(size_t)me] || r0 + nloc != start[(size_t)me + 1])
-    fail(PCGX_ERR_INVALID, "csr_create_local: rank " + std::to_string(me) + " must own rows [" +
-                               std::to_string(start[(size_t)me]) + ", " + std::to_string(start[(size_t)me + 1]) +
-                               ") (pcgx_slab_partition)");
-  if (nloc < 1) fail(PCGX_ERR_INVALID, "csr_create: fewer rows than ranks");
   if (!rp || !ci || !va) fail(PCGX_ERR_INVALID, "CsrMatrix: null array");
+  // The rows may follow one of three balanced partitions (the ones pcgx_csr_create
+  // cuts a full matrix by): plain rows; whole 3 x 3 block rows (n % 3 == 0: keeps
+  // BSR-3); whole node planes of an nx^3 grid (keeps the offset storage on z-slabs).
+  // Every rank reports which ones its [row0, row0 + n_local) matches and the job
+  // takes the first that all ranks match -- rows, block rows, planes.
+  int nxg = (int)std::llround(std::cbrt((double)n));
+  while ((long long)nxg * nxg * nxg > n) --nxg;
+  while ((long long)(nxg + 1) * (nxg + 1) * (nxg + 1) <= n) ++nxg;
+  const bool cube = (long long)nxg * nxg * nxg == n && nxg >= 3 && nxg >= P;
+  auto part_start = [&](int kind, int q) -> long long {  // first row of rank q (q == P: n)
+    if (q == P) return n;
+    int64_t z0, nl;
+    if (kind == 1) {
+      pcgx_slab_partition(n / 3, P, q, &z0, &nl);
+      return 3 * z0;
+    }
+    if (kind == 2) {
+      pcgx_slab_partition(nxg, P, q, &z0, &nl);
+      return z0 * (long long)nxg * nxg;
+    }
+    pcgx_slab_partition(n, P, q, &z0, &nl);
+    return z0;
+  };
+  auto matches = [&](int kind) {
+    if (kind == 1 && (n % 3 != 0 || n < 3LL * P)) return false;
+    if (kind == 2 && !cube) return false;
+    return r0 == part_start(kind, me) && r0 + nloc == part_start(kind, me + 1);
+  };
+  // local int32 arrays (rp from 0, global columns) for the pattern checks of the
+  // plane partition; validated below like every other path
+  int kind = -1;
+  bool slab = false;
+  std::vector<int> doff;
+  {
+    double f[4] = {matches(0) ? 1.0 : 0.0, matches(1) ? 1.0 : 0.0, matches(2) ? 1.0 : 0.0, 0.0};
+    std::vector<int> grp, gci;
+    if (f[2] > 0.0 && op->tune.dia != 0 && op->tune.dia3 != 0 && nloc >= 1 && n < (1LL << 31) &&
+        (long long)rp[nloc] - (long long)rp[0] < (1LL << 31)) {
+      const long long base0 = (long long)rp[0], nz = (long long)rp[nloc] - base0;
+      grp.resize((size_t)nloc + 1);
+      gci.resize((size_t)nz);
+      bool sane = true;
+      for (long long i = 0; i <= nloc; ++i) {
+        grp[(size_t)i] = (int)((long long)rp[i] - base0);
+        if (i && grp[(size_t)i] < grp[(size_t)i - 1]) sane = false;
+      }
+      for (long long k = 0; k < nz && sane; ++k) {
+        gci[(size_t)k] = (int)ci[k];
+        if ((long long)ci[k] < 0 || (long long)ci[k] >= n) sane = false;
+      }
+      if (sane && dia_offsets(nloc, grp, gci, doff, r0) && dia3_match<27>(nloc, nxg, grp, gci, doff, r0)) f[3] = 1.0;
+    }
+    double g[4];
+    allreduce_host(c, f, g, 4);
+    if (g[2] == (double)P && g[3] == (double)P) {
+      kind = 2;
+      slab = true;
+    } else if (g[0] == (double)P) {
+      kind = 0;
+    } else if (g[1] == (double)P) {
+      kind = 1;
+    } else if (g[2] == (double)P) {
+      kind = 2;
+    } else {
+      fail(PCGX_ERR_INVALID, "csr_create_local: rank " + std::to_string(me) + " must own rows [" +
+                                 std::to_string(part_start(0, me)) + ", " + std::to_string(part_start(0, me + 1)) +
+                                 ") (pcgx_slab_partition of the rows; or, on every rank, of the 3 x 3 block rows "
+                                 "or of the node planes of a cubic grid)");
+    }
+  }
+  std::vector<long long> start(P + 1);
+  for (int q = 0; q <= P; ++q) start[(size_t)q] = part_start(kind, q);
+  if (nloc < 1) fail(PCGX_ERR_INVALID, "csr_create: fewer rows than ranks");
   const long long base = (long long)rp[0], nnz = (long long)rp[nloc] - base;
   if (nnz >= (1LL << 31) || n >= (1LL << 31))
     fail(PCGX_ERR_OVERFLOW, "csr_create: nnz " + std::to_string(nnz) + " does not fit the int32 device CSR");
@@ -3523,6 +3599,15 @@ void csr_upload_local(pcgx_context c, pcgx_operator op, long long n, long long r
     allreduce_host(c, &flag, &any, 1);
     if (bad >= 0) fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry at index " + std::to_string(bad));
     if (any > 0.0) fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry on another rank");
+  }
+  if (slab) {
+    // 27-point box on plane-aligned slabs: the offset storage, ghost planes through
+    // the stencil's plane exchange (as pcgx_csr_create keeps it for a full matrix)
+    std::vector<int> grp((size_t)nloc + 1), gci((size_t)nnz);
+    for (long long i = 0; i <= nloc; ++i) grp[(size_t)i] = (int)((long long)rp[i] - base);
+    for (long long k = 0; k < nnz; ++k) gci[(size_t)k] = (int)ci[k];
+    dia_slab_upload(c, op, n, nxg, grp, gci, va, dv, doff, true);
+    return;
   }
   std::sort(ghosts.begin(), ghosts.end());
   ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
@@ -3617,7 +3702,10 @@ void csr_upload_local(pcgx_context c, pcgx_operator op, long long n, long long r
     PCGX_CUDA(cudaMemcpyAsync(op->dvec + nloc, op->ghost_z, sizeof(double) * (size_t)op->nghost,
                               cudaMemcpyDeviceToDevice, c->s));
   PCGX_CUDA(cudaStreamSynchronize(c->s));
-  build_sell(op, nloc, lrp, lci, va);
+  // whole 3 x 3 block rows with block-aligned ghost columns keep BSR-3 (a per-rank
+  // choice: the exchange lists do not depend on the storage)
+  if (op->tune.bsr != 0 && r0 % 3 == 0 && is_bsr3(nloc, lrp, lci)) build_bsr3(op, nloc, lrp, lci, va);
+  else build_sell(op, nloc, lrp, lci, va);
 }
 
 // SELL-32 arrays of an int32 CSR (n rows, local column space) -> op (see sell_kernel).
@@ -3741,8 +3829,9 @@ bool is_bsr3(long long n, const std::vector<int>& rp, const std::vector<int>& ci
 }
 
 // The sorted set of column offsets (col - row) if it has at most kDiaMax members.
+// (rows [row_base, row_base + n) of a larger matrix: rp is local, ci global)
 bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>& ci,
-                 std::vector<int>& off) {
+                 std::vector<int>& off, long long row_base) {
   off.clear();
   // rows mostly repeat their neighbour's offset pattern: only new patterns are merged
   int pa = 0, pb = 0;  // previous row's entries [pa, pb) and its row index
@@ -3754,7 +3843,7 @@ bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>
       same = (long long)ci[(size_t)(a + k)] - i == (long long)ci[(size_t)(pa + k)] - prow;
     if (!same)
       for (int k = a; k < b; ++k) {
-        const long long o = (long long)ci[(size_t)k] - i;
+        const long long o = (long long)ci[(size_t)k] - (i + row_base);
         if (std::find(off.begin(), off.end(), (int)o) == off.end()) {
           if ((int)off.size() == kDiaMax) return false;
           off.push_back((int)o);
@@ -3773,7 +3862,7 @@ bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>
 // grid neighbour s) and no coupling wraps across a grid face.
 template <int P>
 bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vector<int>& ci,
-                const std::vector<int>& off) {
+                const std::vector<int>& off, long long row_base) {
   using Pat = DiaPat<P>;
   if ((int)off.size() != Pat::K) return false;
   const long long nxy = (long long)nx * nx;
@@ -3781,9 +3870,10 @@ bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vect
     if ((long long)off[(size_t)s] != Pat::dz(s) * nxy + Pat::dy(s) * (long long)nx + Pat::dx(s)) return false;
   int ok = 1;
 #pragma omp parallel for schedule(static) reduction(&& : ok)
-  for (long long r = 0; r < n; ++r) {
+  for (long long rl = 0; rl < n; ++rl) {
+    const long long r = rl + row_base;
     const int a = (int)(r % nx), b = (int)((r / nx) % nx), c = (int)(r / nxy);
-    for (int k = rp[(size_t)r]; k < rp[(size_t)r + 1]; ++k) {
+    for (int k = rp[(size_t)rl]; k < rp[(size_t)rl + 1]; ++k) {
       const long long o = (long long)ci[(size_t)k] - r;
       int s = 0;
       while (s < Pat::K && off[(size_t)s] != o) ++s;

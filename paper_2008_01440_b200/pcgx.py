@@ -609,7 +609,9 @@ def jacobi_scale(op, ctx: Context):
 def csr_block_rows(ctx: Context, n, row_ptr, col_idx, values, row0=None):
     """Jacobi-scaled block-row CsrMatrix from this rank's rows only
     (pcgx_csr_create_local): row_ptr (n_local + 1, any base) / col_idx (global) /
-    values of rows [row0, row0 + n_local), the pcgx_slab_partition block."""
+    values of rows [row0, row0 + n_local): the pcgx_slab_partition block of the rows
+    (row0 None), or on every rank whole 3 x 3 block rows / whole node planes of a
+    cubic grid (the partitions that keep BSR-3 / the offset storage)."""
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
     ci = np.ascontiguousarray(col_idx, dtype=np.int64)
     va = np.ascontiguousarray(values, dtype=np.float64)

@@ -37,10 +37,22 @@ def main():
         op, _ = P.jacobi_scale(A, ctx)
         a, b = (0.01, 2.5) if kind == "fe27" else (0.005, 3.2)
         n = A.n
-    else:  # "fe27_local[_asym]": this rank's block of rows only (pcgx_csr_create_local)
-        A = P.gen_fe27(nx, 1.0, SEED)
+    else:
+        # this rank's block of rows only (pcgx_csr_create_local): "fe27_local[_asym]" the
+        # balanced rows, "fe27_planes" whole node planes (keeps the offset storage),
+        # "elast27_local" whole 3 x 3 block rows (keeps BSR-3)
+        if kind == "elast27_local":
+            A = P.gen_elast27(nx, 1.0, 0.5, 0.1, SEED)
+            b0, nb = P.slab_partition(A.n // 3, nranks, rank)
+            r0, nl = 3 * b0, 3 * nb
+        else:
+            A = P.gen_fe27(nx, 1.0, SEED)
+            if kind == "fe27_planes":
+                z0, nzl = P.slab_partition(nx, nranks, rank)
+                r0, nl = z0 * nx * nx, nzl * nx * nx
+            else:
+                r0, nl = P.slab_partition(A.n, nranks, rank)
         n = A.n
-        r0, nl = P.slab_partition(n, nranks, rank)
         lo, hi = int(A.row_ptr[r0]), int(A.row_ptr[r0 + nl])
         rp, ci, va = A.row_ptr[r0:r0 + nl + 1].astype(np.int64), A.col_idx[lo:hi], A.values[lo:hi]
         if kind.endswith("_asym") and rank == 0:
@@ -52,14 +64,14 @@ def main():
             rp = ck[rp - rp[0]].astype(np.int64)
             ci, va = ci[keep], va[keep]
         try:
-            op = P.csr_block_rows(ctx, n, rp, ci, va)
+            op = P.csr_block_rows(ctx, n, rp, ci, va, row0=r0)
         except P.InvalidArgument as e:
             with open(os.path.join(out, f"rank{rank}.err"), "w") as f:
                 f.write(str(e))
             ctx.close()
             return
         del A
-        a, b = 0.01, 2.5
+        a, b = (0.005, 3.2) if kind == "elast27_local" else (0.01, 2.5)
     lo, nl = op.row0(), op.local_size()
     xt = P.random_uniform_vector(nl, SEED, offset=lo)
     bl = op.apply(xt)

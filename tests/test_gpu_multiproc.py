@@ -103,20 +103,26 @@ def test_multiprocess_slabs_match_local_group(pcgx, comm, tmp_path):
 @pytest.mark.parametrize("kind,nranks,comm", [("fe27", 2, "host"), ("fe27_local", 2, "host"),
                                               ("fe27_local", 3, "host"), ("elast27", 2, "host"),
                                               ("elast27", 3, "host"), ("fe27", 3, "ipc"),
-                                              ("fe27_local", 3, "ipc"), ("elast27", 2, "ipc")])
+                                              ("fe27_local", 3, "ipc"), ("elast27", 2, "ipc"),
+                                              ("fe27_planes", 3, "host"), ("fe27_planes", 2, "ipc"),
+                                              ("elast27_local", 2, "host"), ("elast27_local", 3, "ipc")])
 def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks, comm, tmp_path):
     """CSR block rows (the paper's distributed SpMV) across
     processes: per-neighbour packed halos through the shared segment; every rank
     given the full matrix ("fe27") or only its own rows ("fe27_local",
     pcgx_csr_create_local: lists from the symmetric pattern, ghost Jacobi values
-    exchanged once)."""
+    exchanged once). Local rows cut at whole node planes ("fe27_planes") keep the
+    offset storage, at whole 3 x 3 block rows ("elast27_local") BSR-3 -- partitions
+    that differ from the balanced rows at these sizes."""
     P = pcgx
-    nx, m = (14, 6) if kind.startswith("fe27") else (8, 6)
+    nx, m = (14, 6) if kind.startswith("fe27") else ((7, 6) if kind == "elast27_local" else (8, 6))
     res = run_job(nranks, kind, (nx, nx, nx), m, tmp_path, comm)
-    if kind == "elast27":
+    if kind.startswith("elast27"):
         assert all(str(r["storage"]) == "bsr3" for r in res)
-    if kind == "fe27":
+    if kind in ("fe27", "fe27_planes"):
         assert all(str(r["storage"]) == "dia_grid" for r in res)
+    if kind == "fe27_local":  # 14 planes: two ranks' balanced rows ARE whole planes, three ranks' are not
+        assert all(str(r["storage"]) == ("dia_grid" if nranks == 2 else "sell32") for r in res)
     A = P.gen_fe27(nx, 1.0, SEED) if kind.startswith("fe27") else P.gen_elast27(nx, 1.0, 0.5, 0.1, SEED)
     opo = OracleOp("csr", row_ptr=A.row_ptr, col_idx=A.col_idx, values=A.values)
     xt = oracle.random_uniform(A.n, SEED)
@@ -133,10 +139,13 @@ def test_multiprocess_block_rows_match_single_domain(pcgx, oracle, kind, nranks,
 def test_multiprocess_local_rows_reject_asymmetric_pattern(pcgx, tmp_path):
     """pcgx_csr_create_local derives its halo lists from the symmetric pattern; a
     pattern that is not symmetric across ranks is caught on EVERY rank before any
-    point-to-point exchange (InvalidArgument naming the ranks), instead of a hang."""
+    point-to-point exchange (InvalidArgument naming the ranks), instead of a hang.
+    (13 planes: the balanced rows are not whole planes, so the rows go through the
+    packed per-neighbour exchange; plane-aligned rows take the plane exchange, whose
+    messages do not depend on the pattern.)"""
     name = f"pcgx_test_{uuid.uuid4().hex[:12]}"
     procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), name, "2", str(r),
-                               str(tmp_path), "fe27_local_asym", "12", "12", "12", "4"],
+                               str(tmp_path), "fe27_local_asym", "13", "13", "13", "4"],
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
     for p in procs:
         out, _ = p.communicate(timeout=600)

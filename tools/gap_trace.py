@@ -46,7 +46,7 @@ def main():
     gaps.sort(reverse=True)
     kinds = {}
     for s, t, name, cat in iv:
-        key = name.split("<")[0].split("(")[0][:40] if cat == "kernel" else cat
+        key = name.split("(")[0].replace("void ", "").replace("pcgx::", "")[:48] if cat == "kernel" else cat
         kinds.setdefault(key, [0, 0.0])
         kinds[key][0] += 1
         kinds[key][1] += t - s

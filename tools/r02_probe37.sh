@@ -1,0 +1,21 @@
+#!/bin/bash
+# producer warps for the box border only: the pass under ncu, parity tests, solves A/B
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+NEW=paper_2008_01440_b200/libpcgx.so; OLD=tools/bin/libpcgx_noprod.so
+for L in $OLD $NEW; do
+PCGX_LIB=$L PCGX_NO_GRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:stencil7_cheb2f_kernel -c 60 --csv \
+    python tools/solve_once.py 320 20 4 2>/dev/null | python -c "
+import csv,sys
+rows=[r for r in csv.reader(sys.stdin) if len(r)>10]; hdr=rows[0]; v={}
+for r in rows[1:]:
+    d=dict(zip(hdr,r)); v.setdefault(d['Kernel Name'][:34],[]).append(float(d['Metric Value']))
+for k in v:
+    if '1, 0, 1' in k: print('$L', k, len(v[k]), round(sorted(v[k])[len(v[k])//2]/1e3,1))" | tee -a gpurun_out/p37_ncu.log
+done
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_checked.py -x -q > gpurun_out/p37_tests.log 2>&1; echo "rc=$?" >> gpurun_out/p37_tests.log
+tail -3 gpurun_out/p37_tests.log
+for m in 5 20; do
+  timeout 600 python tools/solve_ab.py 320 $m 3 $OLD $NEW > gpurun_out/p37_ab_k$m.log 2>&1
+  echo "k=$m"; cat gpurun_out/p37_ab_k$m.log
+done
