@@ -36,7 +36,9 @@ namespace pcgx {
 // Power-ceiling experiments (tools/build_variant.py, never the product, NOT bitwise):
 // 1: no j-neighbour shared loads; 2: no i-neighbour loads either; 3: + no i-halo
 // columns; 4: + no stencil arithmetic (the pass keeps its TMA boxes, one shared
-// load per operand, the recurrence and the stores)
+// load per operand, the recurrence and the stores); 5: + the recurrence replaced by
+// three additions; 6: + no C ring stores; 7: + no shared loads at all (TMA boxes in,
+// constant stores out)
 #ifndef PCGX_C2F_EXP
 #define PCGX_C2F_EXP 0
 #endif
@@ -284,7 +286,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     // ---------------- stage 1: C[t] on the extended tile row
     if (s1) {
       const bool plane_in = t >= p.c_lo && t < p.c_hi, has_p = in_z(t + 1);
-      ap = has_p ? rq2(pAp, offA) : zero2;
+      ap = has_p && PCGX_C2F_EXP < 7 ? rq2(pAp, offA) : zero2;
       if (kIP && has_p) {
         // the own pair of plane t+1 in place; the halo warps take the two outer
         // columns on their side of rows 1..kFBY (their halo-column stencil reads them
@@ -340,11 +342,16 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         c.x = p.c1 * ((2.0 * xc.x) - yq.x);
         c.y = p.c1 * ((2.0 * xc.y) - yq.y);
       } else {
-        const double2 bb = *reinterpret_cast<const double2*>(pBu + offB);
-        const double2 rr = *reinterpret_cast<const double2*>(pRu + offB);
+        const double2 bb = PCGX_C2F_EXP >= 7 ? zero2 : *reinterpret_cast<const double2*>(pBu + offB);
+        const double2 rr = PCGX_C2F_EXP >= 7 ? zero2 : *reinterpret_cast<const double2*>(pRu + offB);
         rt = rr;
+        if (PCGX_C2F_EXP >= 5) {
+          c.x = (xc.x + bb.x) + (rr.x + y0);
+          c.y = (xc.y + bb.y) + (rr.y + y1);
+        } else {
         c.x = p.rk1 * (((p.c3 * xc.x) - (p.rk1m1 * bb.x)) + p.c2 * (rr.x - y0));
         c.y = p.rk1 * (((p.c3 * xc.y) - (p.rk1m1 * bb.y)) + p.c2 * (rr.y - y1));
+        }
       }
       const bool live = plane_in && do1;
       if (live) cv = c;
@@ -352,7 +359,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         PCGX_DCHECK(gCt - p.outC >= g_lo && gCt - p.outC + 2 <= g_hi);
         st2(gCt, cv.x, cv.y);
       }
-      *reinterpret_cast<double2*>(pCu + offB) = cv;
+      if (PCGX_C2F_EXP < 6) *reinterpret_cast<double2*>(pCu + offB) = cv;
       // i-halo columns of C[t] (read by stage 2 of plane t, two iterations on)
       if (PCGX_C2F_EXP < 3 && do_h) {
         double hx = 0.0;
@@ -403,8 +410,10 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         rv = kFRReg ? r2 : *reinterpret_cast<const double2*>(pR2 + offB);
         xo = a2;
       }
-      const double e0 = p.rk2 * (((p.c3 * cc.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
-      const double e1 = p.rk2 * (((p.c3 * cc.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
+      const double e0 = PCGX_C2F_EXP >= 5 ? (cc.x + xo.x) + (rv.x + y0)
+                                          : p.rk2 * (((p.c3 * cc.x) - (p.rk2m1 * xo.x)) + p.c2 * (rv.x - y0));
+      const double e1 = PCGX_C2F_EXP >= 5 ? (cc.y + xo.y) + (rv.y + y1)
+                                          : p.rk2 * (((p.c3 * cc.y) - (p.rk2m1 * xo.y)) + p.c2 * (rv.y - y1));
       if (do2) {
         PCGX_DCHECK(gEv - p.outE >= g_lo && gEv - p.outE + 2 <= g_hi);
         st2(gEv, e0, e1);
