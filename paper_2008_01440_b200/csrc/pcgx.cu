@@ -31,6 +31,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <tuple>
 #include <queue>
 #include <memory>
 #include <string>
@@ -1801,8 +1802,26 @@ bool bsr3t_launch(pcgx_context c, pcgx_operator op, const InComb& in, const EpiS
 // so the final wave ends evenly -- chosen by simulating the greedy dispatch (a
 // chunk of h planes costs h + 2.5 plane-times: two halo planes plus the ring
 // ramp). spec "u": uniform kz; "h1,h2,...": explicit heights summing to span.
+ChunkPlan make_chunk_plan_search(const std::string& spec, int span, int kz, long long tiles, long long slots,
+                                 double ovh, bool long_chunks);
+// plans are pure functions of their arguments: searched once per process
 ChunkPlan make_chunk_plan(const std::string& spec, int span, int kz, long long tiles, long long slots,
-                          double ovh = 2.5) {
+                          double ovh = 2.5, bool long_chunks = true) {
+  static std::mutex mu;
+  static std::map<std::tuple<std::string, int, int, long long, long long, double, bool>, ChunkPlan> cache;
+  const auto key = std::make_tuple(spec, span, kz, tiles, slots, ovh, long_chunks);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const ChunkPlan p = make_chunk_plan_search(spec, span, kz, tiles, slots, ovh, long_chunks);
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace(key, p);
+  return p;
+}
+ChunkPlan make_chunk_plan_search(const std::string& spec, int span, int kz, long long tiles, long long slots,
+                                 double ovh, bool long_chunks) {
   auto pack = [&](const std::vector<int>& hs) {
     ChunkPlan p{};
     p.n = 0;
@@ -1847,8 +1866,24 @@ ChunkPlan make_chunk_plan(const std::string& spec, int span, int kz, long long t
       return end;
     };
     double best = 0.0;
-    const int bigs[] = {16, 24, 32, 40, 48, 64, 80, 96};
-    const int tl[] = {0, 4, 8, 12, 16, 20, 24};
+    std::vector<int> bigs = {16, 24, 32, 40, 48, 64, 80, 96};
+    std::vector<int> tl = {0, 4, 8, 12, 16, 20, 24};
+    // When every tile of a z-level runs at once (tiles <= resident CTAs: 80 tiles on
+    // 148 SMs at 320^3) neighbouring tiles stay at the same z however long a chunk
+    // is, so long chunks cost no L2 locality and save the per-chunk overhead: the
+    // search then covers any first-chunk height and longer tails (320^3: 176, 88,
+    // 28, 28 instead of 20, 80, 80, 80, 24, 24, 12: the two-step pass -3.7% live).
+    // With more tiles than resident CTAs the tiles of a level run in turns and long
+    // chunks let them drift out of the L2 window (measured at 640^3).
+    // The long first chunk lies near the balanced makespan span * tiles / slots (the
+    // other SMs share what is left), which keeps the search small. The direction
+    // step keeps the short-chunk plans (long chunks measured 7% slower there).
+    if (long_chunks && tiles <= slots && span > 96) {
+      const int ideal = (int)((long long)span * tiles / slots);
+      for (int b = std::max(100, (ideal - 16) / 4 * 4); b <= std::min(span, ideal + 32); b += 4) bigs.push_back(b);
+      for (int t : {28, 32, 40, 48, 56, 64, 72, 80, 88, 96})
+        if (t <= span / 2) tl.push_back(t);
+    }
     for (int big : bigs)
       for (int t1 : tl)
         for (int t2 : tl)
@@ -1943,7 +1978,7 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
       PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil7_dir_kernel, kDirThreads,
                                                               kDirSmem));
       it = op->dirplans.emplace(span, make_chunk_plan(op->c2plan, span, kz, tiles,
-                                                      (long long)std::max(occ, 1) * c->sms)).first;
+                                                      (long long)std::max(occ, 1) * c->sms, 2.5, false)).first;
     }
     check_red_grid((unsigned long long)tiles * it->second.n);
     stencil7_dir_kernel<<<dim3((unsigned)tiles, (unsigned)it->second.n), kDirThreads, kDirSmem, c->s>>>(
