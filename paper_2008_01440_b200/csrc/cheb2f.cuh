@@ -72,29 +72,14 @@ __device__ __forceinline__ double c2f_stencil(double d, double a, double b, doub
 #ifndef PCGX_C2FMINB
 #define PCGX_C2FMINB 1
 #endif
-// R of stage 2 (plane t-2) from a register queue instead of the R ring
-#ifndef PCGX_C2FRREG
-#define PCGX_C2FRREG 1
-#endif
 // register cap with one CTA per SM: 22 warps put 6 on one SM sub-partition (16K
 // registers each), so 64 x 20 tiles allow 80
-// lane 0 / 31 i-neighbours: one LDS for every lane (lane 0: the west of its pair,
-// the others: broadcast of lane 31's east) merged by selects, instead of two
-// divergent per-lane loads
-#ifndef PCGX_C2FEDGE
-#define PCGX_C2FEDGE 1
-#endif
 // kUpd: r(it) = r(it-1) - alpha q(it) formed ONCE per element, in place in the A
 // slot, when the plane arrives (own pairs by their warps, the box's outer rows and
 // columns by the two halo warps); every later read is a plain load
-#ifndef PCGX_C2FUPDIP
-#define PCGX_C2FUPDIP 1
-#endif
-// i-neighbours of every lane straight from shared memory (two 8-byte LDS per
-// stage) instead of shuffles + the edge select (plain A, not the kUpd combine)
-#ifndef PCGX_C2FNBR
-#define PCGX_C2FNBR 1
-#endif
+// (i-neighbours of every lane come straight from shared memory, two 8-byte LDS per
+// stage; R of stage 2 travels in a register queue. The shuffle / edge-select and
+// R-ring alternatives measured slower or equal in round 1 and were removed.)
 #ifndef PCGX_C2FMAXREG
 #define PCGX_C2FMAXREG 80
 #endif
@@ -106,9 +91,8 @@ constexpr int kFBPlane = kFW * kFBY;
 constexpr int kFEStride = (kFBPlane + 15) / 16 * 16;  // TMA destinations: 128-byte multiples
 constexpr int kFCStride = kFBPlane;
 constexpr int kFWarps = kFTY + 2, kFThreads = 32 * kFWarps;
-constexpr bool kFRReg = PCGX_C2FRREG != 0;
 constexpr int kFD = PCGX_C2FD;
-constexpr int kFNA = kFD + 2, kFNB = kFD, kFNR = kFD + (kFRReg ? 0 : 2), kFNC = 3;
+constexpr int kFNA = kFD + 2, kFNB = kFD, kFNR = kFD, kFNC = 3;
 constexpr size_t kC2FSmem = sizeof(double) * (size_t)(kFNA * kFAPlane + (kFNB + kFNR) * kFEStride +
                                                       kFNC * kFCStride) +
                             16 * (kFD + 1) + 128;
@@ -192,22 +176,16 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   double acc_rr = 0.0;
   const double alpha = kUpd ? p.S[p.s_rho] / p.S[p.s_pq] : 0.0;
   const double* const sA0 = sA;
-  auto rq = [&](const double* a, int off) {  // r(it) at offset off of A slot a
-    const double v = a[off];
-    return kUpd ? v - alpha * sQ[(a - sA0) + off] : v;
-  };
   auto rq2 = [&](const double* a, int off) {
     const double2 v = *reinterpret_cast<const double2*>(a + off);
     if (!kUpd) return v;
     const double2 w = *reinterpret_cast<const double2*>(sQ + (a - sA0) + off);
     return make_double2(v.x - alpha * w.x, v.y - alpha * w.y);
   };
-  constexpr bool kIP = kUpd && PCGX_C2FUPDIP;
-  // reads of planes already combined in place
-  auto rqx = [&](const double* a, int off) { return kIP ? a[off] : rq(a, off); };
-  auto rqx2 = [&](const double* a, int off) {
-    return kIP ? *reinterpret_cast<const double2*>(a + off) : rq2(a, off);
-  };
+  constexpr bool kIP = kUpd;
+  // reads of planes already combined in place (kUpd) or plain (otherwise)
+  auto rqx = [&](const double* a, int off) { return a[off]; };
+  auto rqx2 = [&](const double* a, int off) { return *reinterpret_cast<const double2*>(a + off); };
   // kIP: element e of an A slot combined in place
   auto combine_slot = [&](double* a, int e) {
     a[e] = a[e] - alpha * sQ[(a - sA0) + e];
@@ -232,7 +210,6 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   const bool do1 = gj >= 0 && gj < p.ny && pair_in;
   const int offA = (warp + 1) * kFW + col;        // A-box offset of the pair
   const int offB = warp * kFW + col;              // B/R/C offset of the pair
-  const int eoff = lane == 0 ? -1 : 64 - 2 * lane;  // lane 0: west of its pair; else lane 31's east
   const bool interior = warp >= 1 && warp <= kFTY;  // a tile row: stage 2 here
   const bool do2 = interior && do1;
   double* gC = p.outC + (long long)gj * p.nx + gi;
@@ -260,9 +237,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   const double* pAp = sA + 2 * kFAPlane;           // A[t+1]
   const double* pBu = sB;                           // B[t]
   const double* pRu = sR;                           // R[t]
-  const double* pR2 = sR + ((kFNR - 2 + kFNR) % kFNR) * kFEStride;  // R[t-2] (ring variant)
-  const double* pR1 = sR + (kFNR - 1) * kFEStride;                  // R[t-1]
-  double2 r1 = zero2, r2 = zero2;                  // R[t-1], R[t-2] (register variant, own row)
+  double2 r1 = zero2, r2 = zero2;                  // R[t-1], R[t-2] (own row)
   double* pCu = sC;                                 // C[t]
   double* pC1 = sC + 2 * kFCStride;                // C[t-1]
   double* pC2 = sC + kFCStride;                    // C[t-2]
@@ -314,22 +289,9 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (PCGX_C2F_EXP >= 2) {
         aw = ac.y;
         ae = ac.x;
-      } else if (PCGX_C2FNBR && (!kUpd || kIP)) {
+      } else {
         aw = pAu[offA - 1];
         ae = pAu[offA + 2];
-      } else {
-      aw = __shfl_up_sync(0xffffffffu, ac.y, 1);
-      ae = __shfl_down_sync(0xffffffffu, ac.x, 1);
-#if PCGX_C2FEDGE
-      {
-        const double edge = rq(pAu, offA + eoff);
-        aw = lane == 0 ? edge : aw;
-        ae = lane == 31 ? edge : ae;
-      }
-#else
-      if (lane == 0) aw = rq(pAu, offA - 1);
-      if (lane == 31) ae = rq(pAu, offA + 2);
-#endif
       }
       const double2 as = PCGX_C2F_EXP >= 1 ? ac : rqx2(pAu, offA - kFW);
       const double2 an = PCGX_C2F_EXP >= 1 ? ac : rqx2(pAu, offA + kFW);
@@ -380,22 +342,9 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
       if (PCGX_C2F_EXP >= 2) {
         cw = c2.y;
         ce = c2.x;
-      } else if (PCGX_C2FNBR) {
+      } else {
         cw = pC2[offB - 1];
         ce = pC2[offB + 2];
-      } else {
-      cw = __shfl_up_sync(0xffffffffu, c2.y, 1);
-      ce = __shfl_down_sync(0xffffffffu, c2.x, 1);
-#if PCGX_C2FEDGE
-      {
-        const double edge = pC2[offB + eoff];
-        cw = lane == 0 ? edge : cw;
-        ce = lane == 31 ? edge : ce;
-      }
-#else
-      if (lane == 0) cw = pC2[offB - 1];
-      if (lane == 31) ce = pC2[offB + 2];
-#endif
       }
       const double2 cs = PCGX_C2F_EXP >= 1 ? c2 : *reinterpret_cast<const double2*>(pC2 + offB - kFW);
       const double2 cn = PCGX_C2F_EXP >= 1 ? c2 : *reinterpret_cast<const double2*>(pC2 + offB + kFW);
@@ -407,7 +356,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
         rv = a2;  // A == R == r
         xo = div2_rn(a2.x, a2.y, p.theta, inv_t);
       } else {
-        rv = kFRReg ? r2 : *reinterpret_cast<const double2*>(pR2 + offB);
+        rv = r2;
         xo = a2;
       }
       const double e0 = PCGX_C2F_EXP >= 5 ? (cc.x + xo.x) + (rv.x + y0)
@@ -434,8 +383,6 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
     pAu = pAp;
     pAp = (pAp + kFAPlane == sAend) ? sA : pAp + kFAPlane;
     pBu = (pBu + kFEStride == sBend) ? sB : pBu + kFEStride;
-    pR2 = pR1;
-    pR1 = pRu;
     pRu = (pRu + kFEStride == sRend) ? sR : pRu + kFEStride;
     double* const pc = pC2;
     pC2 = pC1;

@@ -26,13 +26,10 @@ namespace pcgx {
 #ifndef PCGX_DIRMINB
 #define PCGX_DIRMINB 1
 #endif
-// x tiles of the deferred x += alpha p_old by TMA in the z / p_old units (instead
-// of a register load one plane ahead)
-#ifndef PCGX_DIRXTMA
-#define PCGX_DIRXTMA 1
-#endif
+// (the x tiles of the deferred x += alpha p_old arrive by TMA in the z / p_old units;
+// a register load one plane ahead left warps waiting at the plane barrier: removed)
 #ifndef PCGX_DIRNS
-#define PCGX_DIRNS (PCGX_DIRXTMA ? 5 : 6)
+#define PCGX_DIRNS 5
 #endif
 constexpr int kDTY = PCGX_DIRTY;
 constexpr int kDBY = kDTY + 2;                          // box rows (1-halo)
@@ -45,7 +42,7 @@ constexpr int kDirNC = 3;                 // p_new planes
 #endif
 constexpr int kDirUnroll = PCGX_DIRUNROLL; // plane-loop unroll
 constexpr int kDirThreads = 32 * (kDTY + 2);  // one warp per extended row (tile rows + 2 halo rows)
-constexpr bool kDirXTma = PCGX_DIRXTMA != 0;
+constexpr bool kDirXTma = true;
 constexpr int kDXStride = kC2TX * kDTY;  // x tile (64 x kDTY), a 128-byte multiple
 constexpr size_t kDirSmem =
     sizeof(double) * (size_t)(2 * kDirNS * kDEStride + kDirNC * kDBPlane + (kDirXTma ? kDirNS * kDXStride : 0)) +
@@ -140,7 +137,6 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
     // this iteration so its latency hides behind them
     double2 xv = zero2;
     const bool xdo = xupd && tile_row && do1 && u - 1 >= kb;
-    if (!kDirXTma && xdo) xv = *reinterpret_cast<const double2*>(p.x + (long long)(u - 1) * p.nxy + goff);
     mbar_wait(&bars[slot], phase);
     const double* Zu = sZ + slot * kDEStride;
     const double* Pu = sP + slot * kDEStride;
@@ -170,7 +166,6 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
       const double* Nv = sN + (sc == 0 ? kDirNC - 1 : sc - 1) * kDBPlane;
       double pw = __shfl_up_sync(0xffffffffu, pc.y, 1);
       double pe = __shfl_down_sync(0xffffffffu, pc.x, 1);
-#if PCGX_C2FEDGE
       {
         // one combine for the warp (lane 0: its west, the others: broadcast of lane
         // 31's east) instead of two divergent ones
@@ -178,10 +173,6 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
         pw = lane == 0 ? e : pw;
         pe = lane == 31 ? e : pe;
       }
-#else
-      if (lane == 0) pw = comb(Zv[off - 1], first ? 0.0 : Pv[off - 1]);
-      if (lane == 31) pe = comb(Zv[off + 2], first ? 0.0 : Pv[off + 2]);
-#endif
       if (do1) {
         const double2 ps = *reinterpret_cast<const double2*>(Nv + off - kC2W);
         const double2 pnn = *reinterpret_cast<const double2*>(Nv + off + kC2W);
@@ -193,7 +184,7 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
         st2(p.pout + idx, pc.x, pc.y);
         acc = acc + (pc.x * y0 + pc.y * y1);
         if (xdo) {
-          if (kDirXTma) xv = *reinterpret_cast<const double2*>(sX + sv * kDXStride + (warp - 1) * kC2TX + 2 * lane);
+          xv = *reinterpret_cast<const double2*>(sX + sv * kDXStride + (warp - 1) * kC2TX + 2 * lane);
           const double2 po = *reinterpret_cast<const double2*>(Pv + off);
           xv.x = xv.x + alpha * po.x;
           xv.y = xv.y + alpha * po.y;
