@@ -1852,20 +1852,24 @@ ChunkPlan make_chunk_plan_search(const std::string& spec, int span, int kz, long
     if (sum != span || (int)hs.size() > ChunkPlan::kMax) hs.clear();
   }
   if (hs.empty()) {
-    auto makespan = [&](const std::vector<int>& h) {
-      std::priority_queue<double, std::vector<double>, std::greater<double>> q;
-      for (long long s = 0; s < slots; ++s) q.push(0.0);
+    double best = 0.0;
+    std::vector<double> heap;
+    // greedy in-order dispatch onto `slots` resident CTAs; gives up (returns a value
+    // above `limit`) as soon as a chunk finishes after the best makespan so far
+    auto makespan = [&](const std::vector<int>& h, double limit) {
+      heap.assign((size_t)slots, 0.0);  // all-equal values: already a heap
       double end = 0.0;
       for (int c : h)
         for (long long t = 0; t < tiles; ++t) {
-          const double f = q.top() + c + ovh;
-          q.pop();
-          q.push(f);
+          std::pop_heap(heap.begin(), heap.end(), std::greater<double>());
+          const double f = heap.back() + c + ovh;
+          heap.back() = f;
+          std::push_heap(heap.begin(), heap.end(), std::greater<double>());
           end = std::max(end, f);
+          if (end > limit) return end;
         }
       return end;
     };
-    double best = 0.0;
     std::vector<int> bigs = {16, 24, 32, 40, 48, 64, 80, 96};
     std::vector<int> tl = {0, 4, 8, 12, 16, 20, 24};
     // When every tile of a z-level runs at once (tiles <= resident CTAs: 80 tiles on
@@ -1898,7 +1902,7 @@ ChunkPlan make_chunk_plan_search(const std::string& spec, int span, int kz, long
             for (int t : {t1, t2, t3})
               if (t) c.push_back(t);
             if (c.empty() || (int)c.size() > ChunkPlan::kMax) continue;
-            const double m = makespan(c);
+            const double m = makespan(c, hs.empty() ? 1e300 : best + 1e-9);
             if (hs.empty() || m < best - 1e-9 || (m < best + 1e-9 && c.size() < hs.size())) {
               best = m;
               hs = c;
