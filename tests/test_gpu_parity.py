@@ -539,6 +539,34 @@ def test_cheb2_bitwise_vs_oracle(P, ctx, oracle, dims, plan, monkeypatch):
         assert np.array_equal(out, ref), (dims, kz2, m)
 
 
+@pytest.mark.parametrize("dims", [(64, 20, 130), (66, 44, 101), (20, 130, 201), (130, 41, 97)])
+def test_cheb_long_chunk_plans_bitwise_vs_oracle(P, ctx, oracle, dims):
+    """Spans above 96 planes with every tile of a z-level resident: the planner admits
+    a long first chunk (320^3 runs 176, 88, 28, 28). Two-step passes, the fused
+    first pass of a PCG solve, the three-step tail of odd degrees and the direction
+    step (short-chunk plans) on such spans: P_m(A) r bitwise the oracle, the solve
+    within the parity bar."""
+    nx, ny, nz = dims
+    op = stencil(P, ctx, nx, ny, nz)
+    opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+    r = oracle.random_uniform(nx * ny * nz, 19)
+    for m in (4, 7, 12):
+        out = P.apply_chebyshev(P.cheb_params(a, b, m, 1.001), op, r)
+        ref = oracle.apply_chebyshev(opo, oracle.cheb_params(a, b, m, 1.001), r)
+        assert np.array_equal(out, ref), (dims, m)
+    xt = oracle.random_uniform(nx * ny * nz, SEED)
+    rhs = op.apply(xt)
+    assert np.array_equal(rhs, oracle.apply(opo, xt))
+    for m in (0, 5, 12):
+        prm = P.cheb_params(a, b, m, 1.001)
+        x, rep = P.pcg_solve(op, rhs, None, P.ChebyshevPreconditioner(prm))
+        xo, ro = oracle.pcg_solve(opo, oracle.cheb_params(a, b, m, 1.001), rhs)
+        assert rep.converged and rep.iters == ro["iters"], (dims, m, rep.iters, ro["iters"])
+        assert (rep.ddot, rep.matvec) == (ro["ddot"], ro["matvec"])
+        assert rel_norm(x, xo) <= 1e-10, (dims, m)
+
+
 @pytest.mark.parametrize("dims", [(24, 24, 24), (66, 10, 9), (64, 16, 1), (130, 17, 33), (2, 2, 2),
                                   (130, 47, 41), (64, 61, 7), (128, 33, 70), (192, 20, 3)])
 @pytest.mark.parametrize("plan", [("", "32"), ("u", "1"), ("u", "5"), ("u", "2")])
