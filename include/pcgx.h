@@ -136,6 +136,12 @@ pcgx_status pcgx_stencil7_create(pcgx_context ctx, int64_t nx, int64_t ny, int64
 /* The z-slab partition every rank uses (host-only): rank r of P owns planes
  * [z0, z0 + nz_local), balanced, the first nz % P ranks one plane more. */
 void pcgx_slab_partition(int64_t nz, int nranks, int rank, int64_t* z0, int64_t* nz_local);
+/* The z-chunk plan of the temporally blocked stencil passes (inspection / tests; host
+ * only, no device needed): the heights of the chunks a launch over `span` planes is
+ * cut into for `tiles` column tiles on `slots` resident CTAs, in dispatch order.
+ * long_chunks != 0: the Chebyshev passes' search (a long first chunk when tiles <=
+ * slots); 0: the direction step's. heights must hold 48 entries; returns the count. */
+int pcgx_chunk_plan(int span, int64_t tiles, int64_t slots, int long_chunks, int* heights);
 
 /* CsrMatrix (symmetric, both triangles, int64 host arrays as in the reference)
  * Jacobi-scaled. Narrowed to int32 on upload (PCGX_ERR_OVERFLOW if nnz >= 2^31).

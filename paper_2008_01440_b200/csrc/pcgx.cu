@@ -4456,6 +4456,17 @@ int pcgx_context_rank(pcgx_context c) { return c ? c->rank : -1; }
 int pcgx_context_nranks(pcgx_context c) { return c ? c->nranks : -1; }
 int64_t pcgx_kernel_launches(pcgx_context c) { return c ? c->launches : 0; }
 
+int pcgx_chunk_plan(int span, int64_t tiles, int64_t slots, int long_chunks, int* heights) {
+  if (span < 1 || tiles < 1 || slots < 1 || !heights) return 0;
+  try {
+    const ChunkPlan p = make_chunk_plan("", span, 32, tiles, slots, 2.5, long_chunks != 0);
+    for (int i = 0; i < p.n; ++i) heights[i] = p.start[i + 1] - p.start[i];
+    return p.n;
+  } catch (...) {
+    return 0;
+  }
+}
+
 pcgx_status pcgx_synchronize(pcgx_context c) {
   return guarded(c, [&] {
     set_device(c);

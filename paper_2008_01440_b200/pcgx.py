@@ -138,7 +138,8 @@ SYMBOLS = [
     "pcgx_context_nranks", "pcgx_synchronize", "pcgx_kernel_launches", "pcgx_device_alloc",
     "pcgx_device_free", "pcgx_memcpy_h2d", "pcgx_memcpy_d2h", "pcgx_memcpy_d2d",
     "pcgx_host_alloc", "pcgx_host_free", "pcgx_timer_start", "pcgx_timer_stop",
-    "pcgx_flush_l2", "pcgx_stencil7_create", "pcgx_slab_partition", "pcgx_csr_create", "pcgx_csr_create_i32",
+    "pcgx_flush_l2", "pcgx_stencil7_create", "pcgx_slab_partition", "pcgx_chunk_plan", "pcgx_csr_create",
+    "pcgx_csr_create_i32",
     "pcgx_csr_create_local",
     "pcgx_operator_destroy", "pcgx_operator_size", "pcgx_operator_local_size",
     "pcgx_operator_z0", "pcgx_operator_row0", "pcgx_operator_nnz", "pcgx_operator_storage", "pcgx_operator_matvec_count",
@@ -212,6 +213,7 @@ def lib():
         "pcgx_csr_create_local": (C.c_int, [ctx, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, _dp, _dp,
                                             C.POINTER(op)]),
         "pcgx_slab_partition": (None, [C.c_int64, C.c_int, C.c_int, _i64p, _i64p]),
+        "pcgx_chunk_plan": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_int)]),
         "pcgx_operator_destroy": (None, [op]),
         "pcgx_operator_size": (C.c_int64, [op]),
         "pcgx_operator_local_size": (C.c_int64, [op]),
@@ -946,6 +948,13 @@ def slab_partition(nz, nranks, rank):
     z0, nl = C.c_int64(), C.c_int64()
     lib().pcgx_slab_partition(nz, nranks, rank, C.byref(z0), C.byref(nl))
     return z0.value, nl.value
+
+
+def chunk_plan(span, tiles, slots=148, long_chunks=True):
+    """Chunk heights of a temporally blocked pass over `span` planes (pcgx_chunk_plan)."""
+    h = (C.c_int * 48)()
+    n = lib().pcgx_chunk_plan(span, tiles, slots, 1 if long_chunks else 0, h)
+    return [h[i] for i in range(n)]
 
 
 def analytic_extremes(dim, nx, scaled=True):

@@ -222,3 +222,20 @@ def test_device_quotient_model_matches_ieee_division(tmp_path):
     subprocess.run([gcc, "-O2", "-ffp-contract=off", "-o", exe, src, "-lm"], check=True)
     out = subprocess.run([exe, "400000"], capture_output=True, text=True)
     assert out.returncode == 0 and out.stdout.strip().endswith("bad=0"), out.stdout
+
+
+def test_chunk_plans(pcgx):
+    """The z-chunk planner of the temporally blocked passes (host code): plans cover
+    the span exactly, respect the chunk limit, and admit a long first chunk exactly
+    when every tile of a z-level is resident (tiles <= resident CTAs)."""
+    P = pcgx
+    for span, tiles, slots in ((320, 80, 148), (512, 208, 148), (640, 320, 148), (1, 1, 148), (7, 3, 148),
+                               (97, 10, 148), (200, 148, 148), (4096, 208, 148), (33, 1000, 296)):
+        for lc in (True, False):
+            h = P.chunk_plan(span, tiles, slots, lc)
+            assert 1 <= len(h) <= 48 and sum(h) == span and min(h) >= 1, (span, tiles, h)
+    # 320^3: 80 tiles of 64 x 20 on 148 SMs -- one long chunk, the other SMs share the rest
+    assert P.chunk_plan(320, 80, 148, True) == [176, 88, 28, 28]
+    assert max(P.chunk_plan(320, 80, 148, False)) <= 96      # the direction step keeps short chunks
+    assert max(P.chunk_plan(512, 208, 148, True)) <= 96      # more tiles than resident CTAs: short chunks
+    assert max(P.chunk_plan(640, 320, 148, True)) <= 96
