@@ -100,6 +100,14 @@ pcgx_status pcgx_context_create_host(int device, int nranks, int rank, const cha
  * rank order (bitwise pcgx_context_create_host / pcgx_local_group_create). */
 pcgx_status pcgx_context_create_ipc(int device, int nranks, int rank, const char* name,
                                     size_t mailbox_bytes, pcgx_context* out);
+/* MEASUREMENT ONLY: one process standing in for rank `rank` of an nranks-rank z-slab
+ * job on a single GPU. Operators own that rank's slab and run the whole slab code
+ * path (ghost planes, exchange on the comm stream, interior / boundary launches,
+ * all-reduce points), but the neighbours' planes are the rank's own opposite boundary
+ * planes copied on the device and an all-reduce keeps the local value: the slab with
+ * periodic ghosts in z. Times the slab path's own overhead without a link
+ * (tools/slab_overhead.py); matrix-free stencil operators only. */
+pcgx_status pcgx_context_create_loopback(int device, int nranks, int rank, pcgx_context* out);
 void pcgx_context_destroy(pcgx_context ctx);
 int pcgx_context_rank(pcgx_context ctx);
 int pcgx_context_nranks(pcgx_context ctx);

@@ -457,6 +457,50 @@ struct NcclComm : CommBase {
   bool graph_capturable() const override { return true; }
 };
 
+// LoopbackComm (measurement only): ONE process standing in for a rank of a P-rank
+// z-slab job on a single GPU. It owns its slab of the global grid and runs the whole
+// slab code path -- ghost planes, the exchange forked onto the comm stream, interior
+// launches meanwhile, boundary launches after the join, per-iteration all-reduce
+// points -- but its neighbours' planes are its OWN opposite boundary planes, copied
+// device-to-device with the real exchange's sizes, and an all-reduce keeps the local
+// value. What it solves is the slab with periodic ghosts in z (still SPD: Dirichlet in
+// x and y), so a PCG solve converges and its per-iteration time is that of a rank with
+// two neighbours minus the link: the slab path's own overhead, measurable on one GPU
+// (tools/slab_overhead.py). Not a product communicator.
+struct LoopbackComm : CommBase {
+  void allreduce(pcgx_context, int, int) override {}
+  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override {
+    const long long nxy = op->nx * op->ny, nzl = op->nzl;
+    const size_t pb = sizeof(double) * (size_t)nxy;
+    PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+    PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+    for (int v = 0; v < nv; ++v) {
+      double* glo = v ? op->ghost_lo2 : op->ghost_lo;
+      double* ghi = v ? op->ghost_hi2 : op->ghost_hi;
+      if (glo) PCGX_CUDA(cudaMemcpyAsync(glo, xs[v] + (nzl - 1) * nxy, pb, cudaMemcpyDeviceToDevice, c->cs));
+      if (ghi) PCGX_CUDA(cudaMemcpyAsync(ghi, xs[v], pb, cudaMemcpyDeviceToDevice, c->cs));
+    }
+    PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+  }
+  void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
+  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override {
+    const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
+    PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
+    PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
+    for (int i = 0; i < n; ++i) {
+      const PlaneX& it = items[i];
+      const size_t bytes = sizeof(double) * (size_t)it.count;
+      if (lo) PCGX_CUDA(cudaMemcpyAsync(it.recv_lo, it.send_hi, bytes, cudaMemcpyDeviceToDevice, c->cs));
+      if (hi) PCGX_CUDA(cudaMemcpyAsync(it.recv_hi, it.send_lo, bytes, cudaMemcpyDeviceToDevice, c->cs));
+    }
+    PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
+  }
+  void sparse_xchg(pcgx_context, pcgx_operator, int, const double* const*, double* const*) override {
+    fail(PCGX_ERR_UNSUPPORTED, "loopback context: matrix-free stencil operators only");
+  }
+  bool graph_capturable() const override { return false; }
+};
+
 class HostBarrier {
  public:
   explicit HostBarrier(int n) : n_(n) {}
@@ -4356,6 +4400,20 @@ pcgx_status pcgx_context_create_host(int device, int nranks, int rank, const cha
     if (nranks > 1)
       c->cm = host_comm_open(nranks, rank, name[0] == '/' ? std::string(name) : "/" + std::string(name),
                              mailbox_bytes ? mailbox_bytes : ((size_t)64 << 20));
+    *out = c.release();
+  });
+}
+
+pcgx_status pcgx_context_create_loopback(int device, int nranks, int rank, pcgx_context* out) {
+  return guarded(nullptr, [&] {
+    if (nranks < 2 || rank < 0 || rank >= nranks || !out)
+      fail(PCGX_ERR_INVALID, "context_create_loopback: bad rank/nranks");
+    auto c = std::make_unique<pcgx_context_s>();
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    ctx_init(c.get());
+    c->cm = new LoopbackComm();
     *out = c.release();
   });
 }

@@ -136,6 +136,7 @@ SYMBOLS = [
     "pcgx_context_create_ipc",
     "pcgx_context_destroy", "pcgx_context_rank",
     "pcgx_context_nranks", "pcgx_synchronize", "pcgx_kernel_launches", "pcgx_device_alloc",
+    "pcgx_context_create_loopback",
     "pcgx_device_free", "pcgx_memcpy_h2d", "pcgx_memcpy_d2h", "pcgx_memcpy_d2d",
     "pcgx_host_alloc", "pcgx_host_free", "pcgx_timer_start", "pcgx_timer_stop",
     "pcgx_flush_l2", "pcgx_stencil7_create", "pcgx_slab_partition", "pcgx_chunk_plan", "pcgx_csr_create",
@@ -188,6 +189,7 @@ def lib():
         "pcgx_local_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(ctx)]),
         "pcgx_context_create_host": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t,
                                                C.POINTER(ctx)]),
+        "pcgx_context_create_loopback": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(ctx)]),
         "pcgx_context_create_ipc": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t,
                                               C.POINTER(ctx)]),
         "pcgx_context_destroy": (None, [ctx]),
@@ -296,12 +298,15 @@ class Context:
 
     def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, nccl_id=None,
                  dist: bool = False, host_comm: str | None = None, ipc_comm: str | None = None,
-                 mailbox_bytes: int = 0,
+                 mailbox_bytes: int = 0, loopback: bool = False,
                  _handle=None):
         L = lib()
         h = C.c_void_p()
         if _handle is not None:
             h = _handle
+        elif loopback:
+            # measurement only: a rank of a z-slab job whose neighbours are itself
+            _check(L.pcgx_context_create_loopback(device, nranks, rank, C.byref(h)))
         elif host_comm is not None:
             # one rank of a multi-process job on one host, exchanging through the
             # shared-memory segment `host_comm` (pcgx_context_create_host)

@@ -161,3 +161,36 @@ def test_csr_block_rows_match_single_domain(pcgx, oracle, nranks, gen, m):
         assert o[4][0] == pytest.approx(olo, rel=1e-8) and o[4][1] == pytest.approx(ohi, rel=1e-8)
     for c in ctxs:
         c.close()
+
+
+def test_loopback_rank_runs_the_slab_path(pcgx, monkeypatch):
+    """pcgx_context_create_loopback (measurement only, tools/slab_overhead.py): a rank of
+    a z-slab job whose neighbours are its own opposite planes. The slab it owns with
+    periodic ghosts in z is a consistent SPD problem: the scaled SpMV matches a numpy
+    periodic stencil, the two-step passes (two ghost planes per side) match the
+    single-step path bitwise, and a PCG solve recovers x_true."""
+    P = pcgx
+    nx, ny, nzl, m = 66, 24, 20, 6
+    with P.Context(0, nranks=3, rank=1, loopback=True) as ctx:
+        assert (ctx.rank, ctx.nranks) == (1, 3)
+        op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, 3 * nzl), ctx)
+        assert op.local_size() == nx * ny * nzl and op.row0() == nx * ny * nzl
+        xt = P.random_uniform_vector(op.local_size(), SEED, offset=op.row0())
+        y = op.apply(xt)
+        X = xt.reshape(nzl, ny, nx)
+        Y = 6.0 * X - np.roll(X, 1, 0) - np.roll(X, -1, 0)
+        Y[:, 1:, :] -= X[:, :-1, :]
+        Y[:, :-1, :] -= X[:, 1:, :]
+        Y[:, :, 1:] -= X[:, :, :-1]
+        Y[:, :, :-1] -= X[:, :, 1:]
+        assert np.allclose(y.reshape(nzl, ny, nx), Y / 6.0, rtol=0, atol=1e-14)
+        a, b = P.analytic_extremes_box(nx, ny, 3 * nzl)
+        prm = P.cheb_params(a, b, m, 1.001)
+        r = P.random_uniform_vector(op.local_size(), 7)
+        z2 = P.apply_chebyshev(prm, op, r)
+        monkeypatch.setenv("PCGX_CHEB2", "0")
+        op1, _ = P.jacobi_scale(P.StencilOperator(nx, ny, 3 * nzl), ctx)
+        assert np.array_equal(z2, P.apply_chebyshev(prm, op1, r))
+        x, rep = P.pcg_solve(op, y, P.SolveOptions(tol=1e-10), P.ChebyshevPreconditioner(prm))
+        assert rep.converged and rep.halo_bytes > 0
+        assert rel_norm(x, xt) <= 1e-7
