@@ -105,6 +105,9 @@ struct ChunkPlan {
   static constexpr int kMax = 48;
   int n;
   int start[kMax + 1];
+  // chunks whose bit is set are not computed (their CTAs exit at once): a slab rank's
+  // two boundary strips as ONE non-reducing launch with the interior chunk masked
+  unsigned long long skip;
 };
 
 template <bool kFirst, bool kRed, bool kUpd = false>
@@ -135,6 +138,7 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   const int i0 = (int)(blockIdx.x % tiles_x) * kC2TX, j0 = (int)(blockIdx.x / tiles_x) * kFTY;
   const int kb = k_begin + plan.start[blockIdx.y];
   const int ke = min(k_begin + plan.start[blockIdx.y + 1], k_end);
+  if (!kRed && !kUpd && ((plan.skip >> blockIdx.y) & 1ull)) return;  // block-uniform
   if (tid == 0) {
     for (int q = 0; q <= kFD; ++q) mbar_init(&bars[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

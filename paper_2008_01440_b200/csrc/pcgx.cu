@@ -1965,7 +1965,7 @@ ChunkPlan make_chunk_plan_search(const std::string& spec, int span, int kz, long
 template <bool kFirst, bool kRed>
 void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const double* B,
                   const double* R, const Cheb2Params& prm, int slot, int k_begin, int k_end, int kz,
-                  bool accumulate) {
+                  bool accumulate, const ChunkPlan* forced = nullptr) {
   (void)kz;
   {
     if (k_end <= k_begin) return;
@@ -1983,7 +1983,7 @@ void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const doubl
       it = op->c2plans.emplace(span, make_chunk_plan(op->c2plan, span, op->kz2, tiles,
                                                      (long long)std::max(occ, 1) * c->sms)).first;
     }
-    const ChunkPlan& plan = it->second;
+    const ChunkPlan& plan = forced ? *forced : it->second;
     if (kRed) check_red_grid((unsigned long long)tiles * plan.n);
     Reduce red = kRed ? make_red(c, slot, accumulate) : Reduce{};
     kern<<<dim3((unsigned)tiles, (unsigned)plan.n), kFThreads, kC2FSmem, c->s>>>(ma, mb, mr, prm, k_begin,
@@ -2099,6 +2099,19 @@ void cheb2_pass(pcgx_context c, pcgx_operator op, const double* A, const double*
     wrote = true;
   }
   c->cm->halo_wait(c);
+  if (!kRed && ib > 0 && ie < nzl && ie > ib) {
+    // both boundary strips in ONE launch (chunks [0, ib), [ib, ie) masked, [ie, nzl)):
+    // they run side by side instead of one after the other
+    ChunkPlan bp{};
+    bp.n = 3;
+    bp.start[0] = 0;
+    bp.start[1] = ib;
+    bp.start[2] = ie;
+    bp.start[3] = nzl;
+    bp.skip = 2ull;
+    cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, 0, nzl, 2, false, &bp);
+    return;
+  }
   if (ib > 0) {
     cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, 0, ib, 2, wrote);
     wrote = true;
