@@ -71,7 +71,7 @@ struct Tuning {
   int bsr3t = 1, bsr3t_modes = 1, bsr3t_kz = 32;
   int csr_stencil = 0;
   // stencil kernels
-  int kz = 0, kz2 = 32, pfd = 2, cheb2 = 1, cheb3 = 2, dir_tma = 1;
+  int kz = 0, kz2 = 32, pfd = 2, cheb2 = 1, cheb3 = 2, dir_tma = 1, fuse_upd_slab = 1;
   std::string c2plan;  // "" automatic chunk plan, "u" uniform kz2, "h1,h2,..." explicit
   // PCG schedule
   int fuse_upd = 1, no_graph = 0, graph_multi = 0, merged = 0, cond_graph = 10, no_fuse_p = 0, zdiv = 1,
@@ -101,6 +101,7 @@ struct Tuning {
     g("PCGX_PFD", t.pfd);
     g("PCGX_CHEB2", t.cheb2);
     g("PCGX_CHEB3", t.cheb3);
+    g("PCGX_FUSE_UPD_SLAB", t.fuse_upd_slab);
     g("PCGX_DIR_TMA", t.dir_tma);
     if (const char* e = std::getenv("PCGX_C2PLAN")) t.c2plan = e;
     g("PCGX_FUSE_UPD", t.fuse_upd);
@@ -2069,7 +2070,7 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
 // padding; the chunks that do not read them run while the planes travel.
 template <bool kFirst, bool kRed>
 void cheb2_pass(pcgx_context c, pcgx_operator op, const double* A, const double* B,
-                const double* R, Cheb2Params prm, int slot) {
+                const double* R, Cheb2Params prm, int slot, bool xchg_r = false) {
   op->matvecs.fetch_add(2, std::memory_order_relaxed);
   const int nzl = (int)op->nzl;
   const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
@@ -2083,15 +2084,21 @@ void cheb2_pass(pcgx_context c, pcgx_operator op, const double* A, const double*
     return;
   }
   const long long nxy = op->nx * op->ny;
-  CommBase::PlaneX items[2];
+  CommBase::PlaneX items[3];
   int ni = 0;
   items[ni++] = {A, const_cast<double*>(A) - 2 * nxy, A + (long long)(nzl - 2) * nxy,
                  const_cast<double*>(A) + (long long)nzl * nxy, 2 * nxy};
   if (!kFirst)
     items[ni++] = {B, const_cast<double*>(B) - nxy, B + (long long)(nzl - 1) * nxy,
                    const_cast<double*>(B) + (long long)nzl * nxy, nxy};
+  // r(it) came out of a fused first pass, which writes own planes only: its boundary
+  // plane travels with this pass's operands (the passes read one ghost plane of r)
+  if (xchg_r)
+    items[ni++] = {R, const_cast<double*>(R) - nxy, R + (long long)(nzl - 1) * nxy,
+                   const_cast<double*>(R) + (long long)nzl * nxy, nxy};
   c->cm->xchg(c, op, items, ni);
-  c->cur_halo_bytes += (long long)((lo ? 1 : 0) + (hi ? 1 : 0)) * (2 + (kFirst ? 0 : 1)) * nxy * 8;
+  c->cur_halo_bytes +=
+      (long long)((lo ? 1 : 0) + (hi ? 1 : 0)) * (2 + (kFirst ? 0 : 1) + (xchg_r ? 1 : 0)) * nxy * 8;
   const int ib = lo ? std::min(2, nzl) : 0, ie = hi ? std::max(ib, nzl - 2) : nzl;
   bool wrote = false;
   if (ie > ib) {
@@ -2132,18 +2139,21 @@ struct CgUpd {
 };
 
 bool cheb_upd_ok(pcgx_context c, pcgx_operator op, int m) {
-  return m >= 3 && op->kind == 0 && op->cheb2 && !c->cm && op->zpad == 0 &&
-         op->tune.fuse_upd != 0;
+  if (!(m >= 3 && op->kind == 0 && op->cheb2 && op->tune.fuse_upd != 0)) return false;
+  if (!c->cm) return op->zpad == 0;
+  // z-slab rank: r(it-1) and q(it) travel as two ghost planes per side (round 2)
+  return op->zpad >= 2 && op->nzl >= 4 && op->tune.fuse_upd_slab != 0;
 }
 
 void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Params prm) {
   op->matvecs.fetch_add(2, std::memory_order_relaxed);
   const int nzl = (int)op->nzl;
+  const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
   prm.zoff = op->zpad;
-  prm.a_lo = 0;
-  prm.a_hi = nzl;
-  prm.c_lo = 0;
-  prm.c_hi = nzl;
+  prm.a_lo = lo ? -2 : 0;
+  prm.a_hi = hi ? nzl + 2 : nzl;
+  prm.c_lo = lo ? -1 : 0;
+  prm.c_hi = hi ? nzl + 1 : nzl;
   prm.S = c->S;
   prm.s_rho = u.s_rho;
   prm.s_pq = u.s_pq;
@@ -2153,23 +2163,54 @@ void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Pa
   const CUtensorMap ma = tmaps_for(op, u.rold).fa;
   const CUtensorMap mq = tmaps_for(op, u.q).fa;
   const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kFTY - 1) / kFTY);
-  auto it = op->c2plans.find(nzl);
-  if (it == op->c2plans.end()) {
-    int occ = 0;
-    PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFThreads, kC2FSmem));
-    it = op->c2plans.emplace(nzl, make_chunk_plan(op->c2plan, nzl, op->kz2, tiles,
-                                                  (long long)std::max(occ, 1) * c->sms)).first;
+  auto launch = [&](int k_begin, int k_end, bool accumulate) {
+    if (k_end <= k_begin) return;
+    const int span = k_end - k_begin;
+    auto it = op->c2plans.find(span);
+    if (it == op->c2plans.end()) {
+      int occ = 0;
+      PCGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFThreads, kC2FSmem));
+      it = op->c2plans.emplace(span, make_chunk_plan(op->c2plan, span, op->kz2, tiles,
+                                                     (long long)std::max(occ, 1) * c->sms)).first;
+    }
+    check_red_grid((unsigned long long)tiles * it->second.n);
+    Reduce rr = make_red(c, u.s_rr, accumulate);
+    if (c->cond_root && !c->cond_split) {  // the head of a conditional segment: r'r closes it
+      rr.cond_bt = c->S + S_BNORM;
+      rr.cond = c->cond_h;
+    }
+    kern<<<dim3((unsigned)tiles, (unsigned)it->second.n), kFThreads, kC2FSmem, c->s>>>(
+        ma, mq, ma, prm, k_begin, k_end, it->second, Reduce{}, rr);
+    check_launch();
+    count_launch(c);
+  };
+  if (!lo && !hi) {
+    launch(0, nzl, false);
+    return;
   }
-  check_red_grid((unsigned long long)tiles * it->second.n);
-  Reduce rr = make_red(c, u.s_rr);
-  if (c->cond_root && !c->cond_split) {  // the head of a conditional segment: r'r closes it
-    rr.cond_bt = c->S + S_BNORM;
-    rr.cond = c->cond_h;
+  // z-slab rank: my two boundary planes of r(it-1) and of q(it) -> the neighbours'
+  // padding; the chunks that read no ghost plane run while they travel, the boundary
+  // strips after the join (their r'r contributions accumulate in that order)
+  const long long nxy = op->nx * op->ny;
+  double* ro = const_cast<double*>(u.rold);
+  double* qo = const_cast<double*>(u.q);
+  CommBase::PlaneX items[2] = {
+      {ro, ro - 2 * nxy, ro + (long long)(nzl - 2) * nxy, ro + (long long)nzl * nxy, 2 * nxy},
+      {qo, qo - 2 * nxy, qo + (long long)(nzl - 2) * nxy, qo + (long long)nzl * nxy, 2 * nxy}};
+  c->cm->xchg(c, op, items, 2);
+  c->cur_halo_bytes += (long long)((lo ? 1 : 0) + (hi ? 1 : 0)) * 4 * nxy * 8;
+  const int ib = lo ? std::min(2, nzl) : 0, ie = hi ? std::max(ib, nzl - 2) : nzl;
+  bool wrote = false;
+  if (ie > ib) {
+    launch(ib, ie, false);
+    wrote = true;
   }
-  kern<<<dim3((unsigned)tiles, (unsigned)it->second.n), kFThreads, kC2FSmem, c->s>>>(
-      ma, mq, ma, prm, 0, nzl, it->second, Reduce{}, rr);
-  check_launch();
-  count_launch(c);
+  c->cm->halo_wait(c);
+  if (ib > 0) {
+    launch(0, ib, wrote);
+    wrote = true;
+  }
+  if (ie < nzl) launch(ie, nzl, wrote);
 }
 
 // Tensor maps of the three-step pass, cached per buffer: kind 20 the A box
@@ -2343,6 +2384,8 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
         icur = fe;
       }
     }
+    // slab rank after a fused first pass: r(it)'s ghost planes ride in the next pass's exchange
+    bool xr = upd != nullptr && c->cm != nullptr;
     for (; k + 1 <= P.m; k += 2) {
       if (tail3 && k + 2 == P.m) break;
       const bool last = (k + 1 == P.m);
@@ -2354,8 +2397,9 @@ void enqueue_cheb(pcgx_context c, pcgx_operator op, const Cheb& P, const double*
       q.rk2m1 = P.rho[k];
       q.outC = last ? nullptr : bufs[fc];
       q.outE = last ? out : bufs[fe];
-      if (last && rz_slot >= 0) cheb2_pass<false, true>(c, op, bufs[icur], bufs[iold], r, q, rz_slot);
-      else cheb2_pass<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1);
+      if (last && rz_slot >= 0) cheb2_pass<false, true>(c, op, bufs[icur], bufs[iold], r, q, rz_slot, xr);
+      else cheb2_pass<false, false>(c, op, bufs[icur], bufs[iold], r, q, -1, xr);
+      xr = false;
       iold = fc;
       icur = fe;
     }
@@ -2841,7 +2885,7 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   const bool defer_x = fuse && dir_tma_ok(op) && op->tune.defer_x != 0 && !cb;
   // one GPU, Chebyshev m >= 3 on the stencil: the update r -= alpha q, r'r rides in
   // the first two-step pass of P r (cheb2f_upd_launch); r(it) lives in Rb[it & 1]
-  const bool fuse_upd = zm == 0 && prec.kind == 1 && spec_after_update && defer_x &&
+  const bool fuse_upd = zm == 0 && prec.kind == 1 && (spec_after_update || c->cm != nullptr) && defer_x &&
                         cheb_upd_ok(c, op, m);
   double* Rb[2] = {r, fuse_upd ? c->r2 : r};
 
@@ -2889,10 +2933,18 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
       // snapshot (r'r(it), p'q(it)) is taken right after that pass (and, with the
       // conditional graph, the convergence test: the rest runs only if not converged)
       const CgUpd u{Rb[par ^ 1], q, Rb[par], slot_rz(par ^ 1), slot_pq(par), slot_rr(par)};
-      enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u, [&] {
+      if (spec_after_update) {
+        enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u, [&] {
+          snapshot();
+          if (use_cond) cond_split(c, slot_rr(par), false);  // the first pass set the condition
+        });
+      } else {
+        // several ranks: the pass reduced this rank's share of r'r; [r'r, r'z] are
+        // all-reduced together after P r, as without the fusion
+        enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u);
+        allreduce(c, slot_rr(par), 2);
         snapshot();
-        if (use_cond) cond_split(c, slot_rr(par), false);  // the first pass set the condition
-      });
+      }
     } else if (use_cond) {
       cond_split(c, slot_rr(par));  // r'r(it) came from the update kernel before this segment
       if (zm == 0) enqueue_prec(c, op, prec, r, z, slot_rz(par));
