@@ -105,8 +105,8 @@ struct ChunkPlan {
   static constexpr int kMax = 48;
   int n;
   int start[kMax + 1];
-  // chunks whose bit is set are not computed (their CTAs exit at once): a slab rank's
-  // two boundary strips as ONE non-reducing launch with the interior chunk masked
+  // chunks whose bit is set are not computed (their CTAs only join the reductions): a
+  // slab rank's two boundary strips as ONE launch with the interior chunk masked
   unsigned long long skip;
 };
 
@@ -138,7 +138,11 @@ stencil7_cheb2f_kernel(const __grid_constant__ CUtensorMap mapA,  // A (68 x (kF
   const int i0 = (int)(blockIdx.x % tiles_x) * kC2TX, j0 = (int)(blockIdx.x / tiles_x) * kFTY;
   const int kb = k_begin + plan.start[blockIdx.y];
   const int ke = min(k_begin + plan.start[blockIdx.y + 1], k_end);
-  if (!kRed && !kUpd && ((plan.skip >> blockIdx.y) & 1ull)) return;  // block-uniform
+  if ((plan.skip >> blockIdx.y) & 1ull) {  // block-uniform; a masked chunk still joins the reductions
+    if (kRed) block_reduce_finish(0.0, red);
+    if (kUpd) block_reduce_finish(0.0, red_rr);
+    return;
+  }
   if (tid == 0) {
     for (int q = 0; q <= kFD; ++q) mbar_init(&bars[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

@@ -82,6 +82,10 @@ stencil7_dir_kernel(const __grid_constant__ CUtensorMap mapZ, const __grid_const
   const int i0 = (int)(blockIdx.x % tiles_x) * kC2TX, j0 = (int)(blockIdx.x / tiles_x) * kDTY;
   const int kb = k_begin + plan.start[blockIdx.y];
   const int ke = min(k_begin + plan.start[blockIdx.y + 1], k_end);
+  if ((plan.skip >> blockIdx.y) & 1ull) {  // a masked chunk (ChunkPlan::skip) only joins the reduction
+    block_reduce_finish(0.0, red);
+    return;
+  }
   const bool first = p.first != 0;
   const double beta = first ? 0.0 : p.S[p.s_new] / p.S[p.s_old];
   const unsigned bytes = kDBPlane * 8;  // box bytes

@@ -1963,6 +1963,18 @@ ChunkPlan make_chunk_plan_search(const std::string& spec, int span, int kz, long
   return pack(hs);
 }
 
+// [0, ib) and [ie, nzl) as chunks 0 and 2 of one launch, the interior chunk masked
+ChunkPlan strips_plan(int ib, int ie, int nzl) {
+  ChunkPlan bp{};
+  bp.n = 3;
+  bp.start[0] = 0;
+  bp.start[1] = ib;
+  bp.start[2] = ie;
+  bp.start[3] = nzl;
+  bp.skip = 2ull;
+  return bp;
+}
+
 template <bool kFirst, bool kRed>
 void cheb2_launch(pcgx_context c, pcgx_operator op, const double* A, const double* B,
                   const double* R, const Cheb2Params& prm, int slot, int k_begin, int k_end, int kz,
@@ -2017,7 +2029,7 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
   const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
   DirParams prm{(int)op->nx, (int)op->ny, nzl, lo ? -1 : 0, hi ? nzl + 1 : nzl, op->zpad,
                 op->nx * op->ny, op->d, c->S, s_new, s_old, first, x, s_pq, q, pnew, ztheta};
-  auto launch = [&](int k_begin, int k_end, int kz, bool accumulate) {
+  auto launch = [&](int k_begin, int k_end, int kz, bool accumulate, const ChunkPlan* forced = nullptr) {
     if (k_end <= k_begin) return;
     const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kDTY - 1) / kDTY);
     const int span = k_end - k_begin;
@@ -2029,9 +2041,10 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
       it = op->dirplans.emplace(span, make_chunk_plan(op->c2plan, span, kz, tiles,
                                                       (long long)std::max(occ, 1) * c->sms, 2.5, false)).first;
     }
-    check_red_grid((unsigned long long)tiles * it->second.n);
-    stencil7_dir_kernel<<<dim3((unsigned)tiles, (unsigned)it->second.n), kDirThreads, kDirSmem, c->s>>>(
-        mz, mp, mx, prm, k_begin, k_end, it->second, make_red(c, slot, accumulate));
+    const ChunkPlan& plan = forced ? *forced : it->second;
+    check_red_grid((unsigned long long)tiles * plan.n);
+    stencil7_dir_kernel<<<dim3((unsigned)tiles, (unsigned)plan.n), kDirThreads, kDirSmem, c->s>>>(
+        mz, mp, mx, prm, k_begin, k_end, plan, make_red(c, slot, accumulate));
     check_launch();
     count_launch(c);
   };
@@ -2058,6 +2071,11 @@ void dir_tma_launch(pcgx_context c, pcgx_operator op, const double* z, const dou
     wrote = true;
   }
   c->cm->halo_wait(c);
+  if (ib > 0 && ie < nzl && ie > ib) {
+    const ChunkPlan bp = strips_plan(ib, ie, nzl);
+    launch(0, nzl, 1, wrote, &bp);
+    return;
+  }
   if (ib > 0) {
     launch(0, ib, 1, wrote);
     wrote = true;
@@ -2106,17 +2124,12 @@ void cheb2_pass(pcgx_context c, pcgx_operator op, const double* A, const double*
     wrote = true;
   }
   c->cm->halo_wait(c);
-  if (!kRed && ib > 0 && ie < nzl && ie > ib) {
+  if (ib > 0 && ie < nzl && ie > ib) {
     // both boundary strips in ONE launch (chunks [0, ib), [ib, ie) masked, [ie, nzl)):
-    // they run side by side instead of one after the other
-    ChunkPlan bp{};
-    bp.n = 3;
-    bp.start[0] = 0;
-    bp.start[1] = ib;
-    bp.start[2] = ie;
-    bp.start[3] = nzl;
-    bp.skip = 2ull;
-    cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, 0, nzl, 2, false, &bp);
+    // they run side by side instead of one after the other; a reducing pass adds
+    // their shares to the interior's (the masked CTAs contribute zeros)
+    const ChunkPlan bp = strips_plan(ib, ie, nzl);
+    cheb2_launch<kFirst, kRed>(c, op, A, B, R, prm, slot, 0, nzl, 2, wrote, &bp);
     return;
   }
   if (ib > 0) {
@@ -2163,7 +2176,7 @@ void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Pa
   const CUtensorMap ma = tmaps_for(op, u.rold).fa;
   const CUtensorMap mq = tmaps_for(op, u.q).fa;
   const long long tiles = ((op->nx + kC2TX - 1) / kC2TX) * ((op->ny + kFTY - 1) / kFTY);
-  auto launch = [&](int k_begin, int k_end, bool accumulate) {
+  auto launch = [&](int k_begin, int k_end, bool accumulate, const ChunkPlan* forced = nullptr) {
     if (k_end <= k_begin) return;
     const int span = k_end - k_begin;
     auto it = op->c2plans.find(span);
@@ -2173,14 +2186,15 @@ void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Pa
       it = op->c2plans.emplace(span, make_chunk_plan(op->c2plan, span, op->kz2, tiles,
                                                      (long long)std::max(occ, 1) * c->sms)).first;
     }
-    check_red_grid((unsigned long long)tiles * it->second.n);
+    const ChunkPlan& plan = forced ? *forced : it->second;
+    check_red_grid((unsigned long long)tiles * plan.n);
     Reduce rr = make_red(c, u.s_rr, accumulate);
     if (c->cond_root && !c->cond_split) {  // the head of a conditional segment: r'r closes it
       rr.cond_bt = c->S + S_BNORM;
       rr.cond = c->cond_h;
     }
-    kern<<<dim3((unsigned)tiles, (unsigned)it->second.n), kFThreads, kC2FSmem, c->s>>>(
-        ma, mq, ma, prm, k_begin, k_end, it->second, Reduce{}, rr);
+    kern<<<dim3((unsigned)tiles, (unsigned)plan.n), kFThreads, kC2FSmem, c->s>>>(
+        ma, mq, ma, prm, k_begin, k_end, plan, Reduce{}, rr);
     check_launch();
     count_launch(c);
   };
@@ -2206,6 +2220,11 @@ void cheb2f_upd_launch(pcgx_context c, pcgx_operator op, const CgUpd& u, Cheb2Pa
     wrote = true;
   }
   c->cm->halo_wait(c);
+  if (ib > 0 && ie < nzl && ie > ib) {
+    const ChunkPlan bp = strips_plan(ib, ie, nzl);
+    launch(0, nzl, wrote, &bp);
+    return;
+  }
   if (ib > 0) {
     launch(0, ib, wrote);
     wrote = true;
