@@ -408,650 +408,7 @@ int vec_grid(pcgx_context c, long long n) {
   return (int)std::max(1LL, std::min(want, (long long)c->sms * 8));
 }
 
-// ---------------------------------------------------------------- communication
-//
-// CommBase is the only place ranks meet. NcclComm: one process per GPU, NCCL
-// over NVLink/NVSwitch (the production path). LocalGroup: P ranks as P
-// contexts in ONE process (one host thread each, any devices), exchanging halo
-// planes with stream-ordered cudaMemcpyAsync and reducing scalars in rank
-// order; no kernel ever waits on another kernel (dependencies are CUDA events
-// plus a host barrier), so the multi-rank slab logic can be exercised on a
-// single GPU. Both are collective: every rank calls them at the same point.
-
-}  // namespace
-struct CommBase {
-  virtual ~CommBase() = default;
-  virtual void allreduce(pcgx_context c, int slot, int count) = 0;
-  // Start exchanging the first/last owned plane of each of the nv vectors into
-  // the neighbours' ghost set v (v = 0: ghost_lo/hi, v = 1: ghost_lo2/hi2).
-  virtual void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) = 0;
-  // Make c->s wait until this rank's ghost planes hold the neighbours' planes.
-  virtual void halo_wait(pcgx_context c) = 0;
-  // Generic plane exchange (two-step kernel): for each item my bottom `count`
-  // elements go to rank-1's recv_hi and my top ones to rank+1's recv_lo; I
-  // receive into my recv_lo / recv_hi. Completes like halo_begin (halo_wait).
-  struct PlaneX {
-    const double* send_lo;
-    double* recv_lo;
-    const double* send_hi;
-    double* recv_hi;
-    long long count;
-  };
-  virtual void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) = 0;
-  // CSR block rows: send nv packed buffers' per-neighbour segments, receive the
-  // neighbours' segments into the ghost arrays (op->nb_rank / send_* / recv_*).
-  virtual void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
-                           double* const* gbuf) = 0;
-  virtual bool graph_capturable() const = 0;
-};
-namespace {
-
-struct NcclComm : CommBase {
-  void allreduce(pcgx_context c, int slot, int count) override {
-    PCGX_NCCL(nccl().AllReduce(c->S + slot, c->S + slot, count, ncclDouble, ncclSum, c->comm, c->s));
-  }
-  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override;
-  void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
-  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override;
-  void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
-                   double* const* gbuf) override;
-  bool graph_capturable() const override { return true; }
-};
-
-// LoopbackComm (measurement only): ONE process standing in for a rank of a P-rank
-// z-slab job on a single GPU. It owns its slab of the global grid and runs the whole
-// slab code path -- ghost planes, the exchange forked onto the comm stream, interior
-// launches meanwhile, boundary launches after the join, per-iteration all-reduce
-// points -- but its neighbours' planes are its OWN opposite boundary planes, copied
-// device-to-device with the real exchange's sizes, and an all-reduce keeps the local
-// value. What it solves is the slab with periodic ghosts in z (still SPD: Dirichlet in
-// x and y), so a PCG solve converges and its per-iteration time is that of a rank with
-// two neighbours minus the link: the slab path's own overhead, measurable on one GPU
-// (tools/slab_overhead.py). Not a product communicator.
-struct LoopbackComm : CommBase {
-  void allreduce(pcgx_context, int, int) override {}
-  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override {
-    const long long nxy = op->nx * op->ny, nzl = op->nzl;
-    const size_t pb = sizeof(double) * (size_t)nxy;
-    PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
-    PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
-    for (int v = 0; v < nv; ++v) {
-      double* glo = v ? op->ghost_lo2 : op->ghost_lo;
-      double* ghi = v ? op->ghost_hi2 : op->ghost_hi;
-      if (glo) PCGX_CUDA(cudaMemcpyAsync(glo, xs[v] + (nzl - 1) * nxy, pb, cudaMemcpyDeviceToDevice, c->cs));
-      if (ghi) PCGX_CUDA(cudaMemcpyAsync(ghi, xs[v], pb, cudaMemcpyDeviceToDevice, c->cs));
-    }
-    PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
-  }
-  void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
-  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override {
-    const bool lo = op->ghost_lo != nullptr, hi = op->ghost_hi != nullptr;
-    PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
-    PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
-    for (int i = 0; i < n; ++i) {
-      const PlaneX& it = items[i];
-      const size_t bytes = sizeof(double) * (size_t)it.count;
-      if (lo) PCGX_CUDA(cudaMemcpyAsync(it.recv_lo, it.send_hi, bytes, cudaMemcpyDeviceToDevice, c->cs));
-      if (hi) PCGX_CUDA(cudaMemcpyAsync(it.recv_hi, it.send_lo, bytes, cudaMemcpyDeviceToDevice, c->cs));
-    }
-    PCGX_CUDA(cudaEventRecord(c->ev_join, c->cs));
-  }
-  void sparse_xchg(pcgx_context, pcgx_operator, int, const double* const*, double* const*) override {
-    fail(PCGX_ERR_UNSUPPORTED, "loopback context: matrix-free stencil operators only");
-  }
-  bool graph_capturable() const override { return false; }
-};
-
-class HostBarrier {
- public:
-  explicit HostBarrier(int n) : n_(n) {}
-  void wait() {
-    std::unique_lock<std::mutex> lk(m_);
-    const long gen = gen_;
-    if (++count_ == n_) {
-      count_ = 0;
-      ++gen_;
-      cv_.notify_all();
-    } else {
-      cv_.wait(lk, [&] { return gen != gen_; });
-    }
-  }
-
- private:
-  std::mutex m_;
-  std::condition_variable cv_;
-  int n_, count_ = 0;
-  long gen_ = 0;
-};
-
-// rank-ordered sum of the group's contributions into every rank's slots
-__global__ void group_sum_kernel(const double* contrib, int nranks, int slot, int count, double* S) {
-  const int i = threadIdx.x;
-  if (i < count) {
-    double s = 0.0;
-    for (int q = 0; q < nranks; ++q) s += contrib[q * kSlots + slot + i];
-    S[slot + i] = s;
-  }
-}
-
-struct LocalGroup {
-  int nranks;
-  HostBarrier bar;
-  std::vector<pcgx_context> ctx;
-  std::vector<double*> ghost_lo, ghost_hi, ghost_lo2, ghost_hi2;
-  std::vector<std::vector<double*>> xrecv_lo, xrecv_hi;  // per rank, per xchg item
-  std::vector<std::vector<double*>> srecv;               // [rank][v * nranks + src] ghost destination
-  std::vector<cudaEvent_t> ev_ar;   // rank's contribution copied
-  std::vector<cudaEvent_t> ev_done; // rank finished reading contributions
-  double* contrib = nullptr;        // nranks * kSlots doubles on the first rank's device
-  std::atomic<int> refs{0};
-  explicit LocalGroup(int n)
-      : nranks(n), bar(n), ctx(n), ghost_lo(n), ghost_hi(n), ghost_lo2(n), ghost_hi2(n),
-        xrecv_lo(n), xrecv_hi(n), srecv(n), ev_ar(n), ev_done(n) {}
-};
-
-struct LocalComm : CommBase {
-  std::shared_ptr<LocalGroup> g;
-  int rank;
-  LocalComm(std::shared_ptr<LocalGroup> grp, int r) : g(std::move(grp)), rank(r) {}
-  void allreduce(pcgx_context c, int slot, int count) override {
-    // previous allreduce fully consumed by every rank before contrib is reused
-    for (int q = 0; q < g->nranks; ++q) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ev_done[q], 0));
-    PCGX_CUDA(cudaMemcpyAsync(g->contrib + rank * kSlots + slot, c->S + slot, sizeof(double) * count,
-                              cudaMemcpyDefault, c->s));
-    PCGX_CUDA(cudaEventRecord(g->ev_ar[rank], c->s));
-    g->bar.wait();
-    for (int q = 0; q < g->nranks; ++q) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ev_ar[q], 0));
-    group_sum_kernel<<<1, 32, 0, c->s>>>(g->contrib, g->nranks, slot, count, c->S);
-    check_launch();
-    PCGX_CUDA(cudaEventRecord(g->ev_done[rank], c->s));
-    g->bar.wait();
-  }
-  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override;
-  void halo_wait(pcgx_context c) override {  // my ghosts are written by the other ranks' copies
-    for (int q = 0; q < g->nranks; ++q)
-      if (q != rank) PCGX_CUDA(cudaStreamWaitEvent(c->s, g->ctx[q]->ev_join, 0));
-  }
-  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override;
-  void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
-                   double* const* gbuf) override;
-  bool graph_capturable() const override { return false; }
-};
-
-// ---------------------------------------------------------------- host-staged comm
-// HostComm: P ranks in P processes on one host (any devices, also all on ONE GPU)
-// exchanging through a POSIX shared-memory segment: every plane / segment / scalar
-// is copied device -> shared memory -> device by the host, synchronously, with a
-// process-shared barrier between the write and read phases. No kernel and no
-// stream ever waits on another rank, so ranks that share a GPU cannot deadlock
-// it. It exists to run the multi-process slab / block-row algorithm (the same
-// CommBase calls NCCL serves) where there is one GPU: bitwise the LocalGroup
-// results (scalars are summed in rank order, like group_sum_kernel).
-struct ShmHeader {
-  std::atomic<uint64_t> magic;
-  std::atomic<int> count;  // barrier arrivals of the current generation
-  std::atomic<int> gen;    // barrier generation
-  std::atomic<int> abort;  // a rank gave up (timeout): the others fail instead of waiting
-  int nranks;
-  size_t cap;
-};
-static_assert(std::atomic<int>::is_always_lock_free && std::atomic<uint64_t>::is_always_lock_free,
-              "host comm: atomics in shared memory must be address-free (lock-free)");
-constexpr uint64_t kShmMagic = 0x70636778686f7374ull;  // "pcgxhost"
-constexpr size_t kShmHdr = 4096;
-
-struct HostComm : CommBase {
-  int rank = 0, nranks = 1;
-  std::string name;
-  unsigned char* base = nullptr;
-  size_t total = 0, cap = 0;
-  ShmHeader* hdr() const { return reinterpret_cast<ShmHeader*>(base); }
-  double* box(int r) const { return reinterpret_cast<double*>(base + kShmHdr + (size_t)r * cap); }
-  // Counter barrier on lock-free atomics in the shared segment (release / acquire
-  // orders each rank's outbox writes before the peers' reads). A rank that waits
-  // longer than PCGX_HOSTCOMM_TIMEOUT seconds (default 600) marks the job aborted
-  // and fails; every waiting rank then fails too instead of hanging.
-  void barrier() const {
-    ShmHeader* h = hdr();
-    if (h->abort.load(std::memory_order_acquire)) fail(PCGX_ERR_NCCL, "host comm: a peer rank gave up");
-    const int g = h->gen.load(std::memory_order_acquire);
-    if (h->count.fetch_add(1, std::memory_order_acq_rel) + 1 == nranks) {
-      h->count.store(0, std::memory_order_relaxed);
-      h->gen.store(g + 1, std::memory_order_release);
-      return;
-    }
-    const double limit = (double)std::max(1, env_int("PCGX_HOSTCOMM_TIMEOUT", 600));
-    const auto t0 = std::chrono::steady_clock::now();
-    for (long spins = 0; h->gen.load(std::memory_order_acquire) == g; ++spins) {
-      if (h->abort.load(std::memory_order_acquire)) fail(PCGX_ERR_NCCL, "host comm: a peer rank gave up");
-      if (spins > 2000) {
-        usleep(20);
-        if ((spins & 1023) == 0 &&
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
-          h->abort.store(1, std::memory_order_release);
-          fail(PCGX_ERR_NCCL, "host comm: barrier timed out (a peer rank is gone)");
-        }
-      }
-    }
-  }
-  // A rank that cannot continue marks the job aborted first, so the peers fail at
-  // their next barrier instead of waiting out the timeout.
-  void give_up() const { hdr()->abort.store(1, std::memory_order_release); }
-  void need(size_t bytes) const {
-    if (bytes > cap) {
-      give_up();
-      fail(PCGX_ERR_UNSUPPORTED, "host comm: message of " + std::to_string(bytes) + " bytes exceeds the " +
-                                     std::to_string(cap) + "-byte mailbox");
-    }
-  }
-  ~HostComm() override {
-    if (!base) return;
-    try {
-      barrier();
-    } catch (...) {
-    }
-    munmap(base, total);
-    if (rank == 0) shm_unlink(name.c_str());
-  }
-  void allreduce(pcgx_context c, int slot, int count) override {
-    PCGX_CUDA(cudaStreamSynchronize(c->s));
-    PCGX_CUDA(cudaMemcpy(box(rank), c->S + slot, sizeof(double) * count, cudaMemcpyDeviceToHost));
-    barrier();
-    double sum[kSlots];
-    for (int i = 0; i < count; ++i) {
-      double v = 0.0;
-      for (int q = 0; q < nranks; ++q) v += box(q)[i];
-      sum[i] = v;
-    }
-    barrier();
-    PCGX_CUDA(cudaMemcpyAsync(c->S + slot, sum, sizeof(double) * count, cudaMemcpyHostToDevice, c->s));
-    PCGX_CUDA(cudaStreamSynchronize(c->s));
-  }
-  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override {
-    (void)op;
-    PCGX_CUDA(cudaStreamSynchronize(c->s));
-    size_t off = 0;
-    for (int i = 0; i < n; ++i) off += 2 * (size_t)items[i].count;
-    need(sizeof(double) * off);
-    off = 0;
-    for (int i = 0; i < n; ++i) {  // my outbox: [lo part | hi part] per item
-      const size_t b = sizeof(double) * (size_t)items[i].count;
-      if (rank > 0) PCGX_CUDA(cudaMemcpy(box(rank) + off, items[i].send_lo, b, cudaMemcpyDeviceToHost));
-      if (rank < nranks - 1)
-        PCGX_CUDA(cudaMemcpy(box(rank) + off + items[i].count, items[i].send_hi, b, cudaMemcpyDeviceToHost));
-      off += 2 * (size_t)items[i].count;
-    }
-    barrier();
-    off = 0;
-    for (int i = 0; i < n; ++i) {  // rank-1's top -> my recv_lo, rank+1's bottom -> my recv_hi
-      const size_t b = sizeof(double) * (size_t)items[i].count;
-      if (rank > 0 && items[i].recv_lo)
-        PCGX_CUDA(cudaMemcpyAsync(items[i].recv_lo, box(rank - 1) + off + items[i].count, b,
-                                  cudaMemcpyHostToDevice, c->s));
-      if (rank < nranks - 1 && items[i].recv_hi)
-        PCGX_CUDA(cudaMemcpyAsync(items[i].recv_hi, box(rank + 1) + off, b, cudaMemcpyHostToDevice, c->s));
-      off += 2 * (size_t)items[i].count;
-    }
-    PCGX_CUDA(cudaStreamSynchronize(c->s));  // the peers may refill their outboxes after the barrier
-    barrier();
-  }
-  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override {
-    const long long nxy = op->nx * op->ny, nzl = op->nzl;
-    PlaneX items[2];
-    for (int v = 0; v < nv && v < 2; ++v)
-      items[v] = {xs[v], v ? op->ghost_lo2 : op->ghost_lo, xs[v] + (nzl - 1) * nxy,
-                  v ? op->ghost_hi2 : op->ghost_hi, nxy};
-    xchg(c, op, items, std::min(nv, 2));
-  }
-  void halo_wait(pcgx_context c) override { (void)c; }  // the exchange completed synchronously
-  void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
-                   double* const* gbuf) override {
-    PCGX_CUDA(cudaStreamSynchronize(c->s));
-    const int P = nranks;
-    // my outbox: a directory (offset, count) per destination rank, then the data
-    int64_t* dir = reinterpret_cast<int64_t*>(box(rank));
-    for (int q = 0; q < 2 * P; ++q) dir[q] = 0;
-    size_t off = 2 * (size_t)P;  // in doubles (int64 and double are both 8 bytes)
-    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
-      const int q = op->nb_rank[i];
-      dir[q] = (int64_t)off;
-      dir[P + q] = op->send_cnt[i];
-      need(sizeof(double) * (off + (size_t)nv * op->send_cnt[i]));
-      for (int v = 0; v < nv; ++v) {
-        if (op->send_cnt[i])
-          PCGX_CUDA(cudaMemcpy(box(rank) + off, sbuf[v] + op->send_off[i], sizeof(double) * op->send_cnt[i],
-                               cudaMemcpyDeviceToHost));
-        off += (size_t)op->send_cnt[i];
-      }
-    }
-    barrier();
-    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
-      const int q = op->nb_rank[i];
-      const int64_t* qd = reinterpret_cast<const int64_t*>(box(q));
-      const int64_t qoff = qd[rank], qcnt = qd[P + rank];
-      if (qcnt != op->recv_cnt[i]) fail(PCGX_ERR_NCCL, "host comm: block-row segment size mismatch");
-      for (int v = 0; v < nv; ++v)
-        if (qcnt)
-          PCGX_CUDA(cudaMemcpyAsync(gbuf[v] + op->recv_off[i], box(q) + qoff + (size_t)v * qcnt,
-                                    sizeof(double) * qcnt, cudaMemcpyHostToDevice, c->s));
-    }
-    PCGX_CUDA(cudaStreamSynchronize(c->s));
-    barrier();
-  }
-  bool graph_capturable() const override { return false; }
-};
-
-HostComm* host_comm_open(int nranks, int rank, const std::string& name, size_t cap) {
-  auto hc = std::make_unique<HostComm>();
-  hc->rank = rank;
-  hc->nranks = nranks;
-  hc->name = name;
-  hc->cap = (cap + 4095) / 4096 * 4096;
-  hc->total = kShmHdr + (size_t)nranks * hc->cap;
-  int fd = -1;
-  if (rank == 0) {
-    shm_unlink(name.c_str());  // a stale segment of a crashed job
-    fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
-    if (fd < 0) fail(PCGX_ERR_NCCL, "host comm: shm_open(" + name + ") failed");
-    if (ftruncate(fd, (off_t)hc->total) != 0) {
-      close(fd);
-      fail(PCGX_ERR_NCCL, "host comm: ftruncate failed");
-    }
-  } else {
-    for (int tries = 0; fd < 0; ++tries) {  // rank 0 creates it; up to 120 s
-      fd = shm_open(name.c_str(), O_RDWR, 0600);
-      struct stat st;
-      if (fd >= 0 && (fstat(fd, &st) != 0 || (size_t)st.st_size < hc->total)) {
-        close(fd);
-        fd = -1;
-      }
-      if (fd < 0) {
-        if (tries > 120000) fail(PCGX_ERR_NCCL, "host comm: segment " + name + " never appeared");
-        usleep(1000);
-      }
-    }
-  }
-  void* m = mmap(nullptr, hc->total, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
-  close(fd);
-  if (m == MAP_FAILED) fail(PCGX_ERR_NCCL, "host comm: mmap failed");
-  hc->base = static_cast<unsigned char*>(m);
-  ShmHeader* h = hc->hdr();
-  if (rank == 0) {
-    h->count.store(0, std::memory_order_relaxed);
-    h->gen.store(0, std::memory_order_relaxed);
-    h->abort.store(0, std::memory_order_relaxed);
-    h->nranks = nranks;
-    h->cap = hc->cap;
-    h->magic.store(kShmMagic, std::memory_order_release);
-  } else {
-    for (int tries = 0; h->magic.load(std::memory_order_acquire) != kShmMagic; ++tries) {
-      if (tries > 120000) fail(PCGX_ERR_NCCL, "host comm: segment " + name + " never initialised");
-      usleep(1000);
-    }
-    if (h->nranks != nranks || h->cap != hc->cap) fail(PCGX_ERR_INVALID, "host comm: ranks disagree on the job shape");
-  }
-  hc->barrier();  // everyone attached
-  return hc.release();
-}
-
-// ---------------------------------------------------------------- peer-memory comm
-// IpcComm: P ranks in P processes on one node (one GPU each over NVLink / NVSwitch,
-// or sharing a GPU) exchanging through DEVICE memory: each rank exports a device
-// mailbox (two parity areas) and four events by CUDA IPC; every exchange is
-// stream-ordered -- the sender's stream copies its planes / segments / scalars
-// into its own mailbox and records `ready`, the receivers' streams wait on that
-// event and pull straight from the peer's mailbox into their ghost buffers (a
-// peer-to-peer copy over NVLink between GPUs), then record `done`. The host only
-// meets the peers at one shared-memory barrier per exchange (so each wait is
-// issued after the record it waits for); no host-side stream synchronisation, no
-// host staging, and the halo copies overlap the interior kernels like NCCL's.
-// No kernel ever waits on another rank (only streams wait on recorded events),
-// so ranks that share a GPU cannot deadlock it. Parity areas: an exchange reuses
-// the area of two exchanges ago only after every peer's `done` of that exchange
-// (the barrier in between orders the host calls). Scalars are summed in rank
-// order by peer_sum_kernel (bitwise the LocalGroup / HostComm sums).
-__global__ void peer_sum_kernel(const double* const* boxes, long long area_off, int nranks, int slot, int count,
-                                double* S) {
-  const int i = threadIdx.x;
-  if (i < count) {
-    double s = 0.0;
-    for (int q = 0; q < nranks; ++q) s += boxes[q][area_off + i];
-    S[slot + i] = s;
-  }
-}
-
-struct IpcExport {
-  cudaIpcMemHandle_t box;
-  cudaIpcEventHandle_t ready[2], done[2];
-  int device;
-  long long cap;
-};
-
-struct IpcComm : CommBase {
-  std::unique_ptr<HostComm> hc;  // barrier + setup exchange + block-row directories
-  int rank = 0, nranks = 1, device = 0;
-  long long capd = 0;                    // doubles per parity area (kSlots scalars + data)
-  double* box = nullptr;                 // my mailbox: 2 parity areas
-  std::vector<double*> peer;             // every rank's mailbox as mapped here (peer[rank] = box)
-  const double** d_peer = nullptr;       // the same table on the device (peer_sum_kernel)
-  cudaEvent_t ready[2] = {}, done[2] = {};
-  std::vector<std::array<cudaEvent_t, 2>> pready, pdone;  // the peers' events, opened here
-  uint64_t seq = 0;
-
-  double* area(int q, int par) const { return peer[(size_t)q] + (size_t)par * capd; }
-  // host-side block-row directory of rank q for parity par (offset, count per rank)
-  int64_t* dir(int q, int par) const { return reinterpret_cast<int64_t*>(hc->box(q)) + (size_t)par * 2 * nranks; }
-  void need(long long doubles) const {
-    if (doubles > capd - kSlots) {
-      hc->give_up();
-      fail(PCGX_ERR_UNSUPPORTED, "ipc comm: message of " + std::to_string(8 * doubles) + " bytes exceeds the " +
-                                     std::to_string(8 * (capd - kSlots)) + "-byte mailbox");
-    }
-  }
-  // Start exchange `seq` on stream st: the parity area is free once every peer has
-  // finished reading it (their `done` of two exchanges ago).
-  int begin(cudaStream_t st) {
-    const int par = (int)(seq++ & 1);
-    for (int q = 0; q < nranks; ++q)
-      if (q != rank) PCGX_CUDA(cudaStreamWaitEvent(st, pdone[(size_t)q][par], 0));
-    return par;
-  }
-  void publish(cudaStream_t st, int par) {
-    PCGX_CUDA(cudaEventRecord(ready[par], st));
-    hc->barrier();  // every rank's `ready` recorded before anyone waits on it
-  }
-  void finish(pcgx_context c, cudaStream_t st, int par, bool join) {
-    PCGX_CUDA(cudaEventRecord(done[par], st));
-    if (join) PCGX_CUDA(cudaEventRecord(c->ev_join, st));
-  }
-  void copy(double* dst, const double* src, long long count, cudaStream_t st) {
-    if (count > 0) PCGX_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * (size_t)count, cudaMemcpyDefault, st));
-  }
-
-  ~IpcComm() override {
-    if (!hc) return;
-    cudaSetDevice(device);
-    cudaDeviceSynchronize();  // my streams no longer touch the peers' mailboxes
-    try {
-      hc->barrier();
-    } catch (...) {
-    }
-    for (int q = 0; q < nranks; ++q) {
-      if (q == rank) continue;
-      if (peer[(size_t)q]) cudaIpcCloseMemHandle(peer[(size_t)q]);
-      for (int par = 0; par < 2; ++par) {
-        if (pready[(size_t)q][par]) cudaEventDestroy(pready[(size_t)q][par]);
-        if (pdone[(size_t)q][par]) cudaEventDestroy(pdone[(size_t)q][par]);
-      }
-    }
-    try {
-      hc->barrier();  // nobody maps my mailbox any more
-    } catch (...) {
-    }
-    for (int par = 0; par < 2; ++par) {
-      if (ready[par]) cudaEventDestroy(ready[par]);
-      if (done[par]) cudaEventDestroy(done[par]);
-    }
-    if (d_peer) cudaFree(d_peer);
-    if (box) cudaFree(box);
-  }
-
-  void allreduce(pcgx_context c, int slot, int count) override {
-    cudaStream_t st = c->s;
-    const int par = begin(st);
-    copy(area(rank, par), c->S + slot, count, st);
-    publish(st, par);
-    for (int q = 0; q < nranks; ++q)
-      if (q != rank) PCGX_CUDA(cudaStreamWaitEvent(st, pready[(size_t)q][par], 0));
-    peer_sum_kernel<<<1, 32, 0, st>>>(d_peer, (long long)par * capd, nranks, slot, count, c->S);
-    check_launch();
-    finish(c, st, par, false);
-  }
-  void xchg(pcgx_context c, pcgx_operator op, const PlaneX* items, int n) override {
-    (void)op;
-    long long tot = 0;
-    for (int i = 0; i < n; ++i) tot += 2 * items[i].count;
-    need(tot);
-    PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
-    PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
-    cudaStream_t st = c->cs;
-    const int par = begin(st);
-    double* mine = area(rank, par) + kSlots;
-    long long off = 0;
-    for (int i = 0; i < n; ++i) {  // my area: [bottom planes | top planes] per item
-      if (rank > 0) copy(mine + off, items[i].send_lo, items[i].count, st);
-      if (rank < nranks - 1) copy(mine + off + items[i].count, items[i].send_hi, items[i].count, st);
-      off += 2 * items[i].count;
-    }
-    publish(st, par);
-    if (rank > 0) PCGX_CUDA(cudaStreamWaitEvent(st, pready[(size_t)rank - 1][par], 0));
-    if (rank < nranks - 1) PCGX_CUDA(cudaStreamWaitEvent(st, pready[(size_t)rank + 1][par], 0));
-    off = 0;
-    for (int i = 0; i < n; ++i) {  // rank-1's top -> my recv_lo, rank+1's bottom -> my recv_hi
-      if (rank > 0 && items[i].recv_lo)
-        copy(items[i].recv_lo, area(rank - 1, par) + kSlots + off + items[i].count, items[i].count, st);
-      if (rank < nranks - 1 && items[i].recv_hi)
-        copy(items[i].recv_hi, area(rank + 1, par) + kSlots + off, items[i].count, st);
-      off += 2 * items[i].count;
-    }
-    finish(c, st, par, true);
-  }
-  void halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) override {
-    const long long nxy = op->nx * op->ny, nzl = op->nzl;
-    PlaneX items[2];
-    for (int v = 0; v < nv && v < 2; ++v)
-      items[v] = {xs[v], v ? op->ghost_lo2 : op->ghost_lo, xs[v] + (nzl - 1) * nxy,
-                  v ? op->ghost_hi2 : op->ghost_hi, nxy};
-    xchg(c, op, items, std::min(nv, 2));
-  }
-  void halo_wait(pcgx_context c) override { PCGX_CUDA(cudaStreamWaitEvent(c->s, c->ev_join, 0)); }
-  void sparse_xchg(pcgx_context c, pcgx_operator op, int nv, const double* const* sbuf,
-                   double* const* gbuf) override {
-    const int P = nranks;
-    long long tot = 0;
-    for (size_t i = 0; i < op->nb_rank.size(); ++i) tot += (long long)nv * op->send_cnt[i];
-    need(tot);
-    PCGX_CUDA(cudaEventRecord(c->ev_fork, c->s));
-    PCGX_CUDA(cudaStreamWaitEvent(c->cs, c->ev_fork, 0));
-    cudaStream_t st = c->cs;
-    const int par = begin(st);
-    int64_t* d = dir(rank, par);  // host directory: where my segment for rank q starts, its length
-    for (int q = 0; q < 2 * P; ++q) d[q] = 0;
-    double* mine = area(rank, par) + kSlots;
-    long long off = 0;
-    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
-      const int q = op->nb_rank[i];
-      d[q] = off;
-      d[P + q] = op->send_cnt[i];
-      for (int v = 0; v < nv; ++v) {
-        copy(mine + off, sbuf[v] + op->send_off[i], op->send_cnt[i], st);
-        off += op->send_cnt[i];
-      }
-    }
-    publish(st, par);
-    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
-      const int q = op->nb_rank[i];
-      const int64_t* qd = dir(q, par);
-      const int64_t qoff = qd[rank], qcnt = qd[P + rank];
-      if (qcnt != op->recv_cnt[i]) fail(PCGX_ERR_NCCL, "ipc comm: block-row segment size mismatch");
-      if (!qcnt) continue;
-      PCGX_CUDA(cudaStreamWaitEvent(st, pready[(size_t)q][par], 0));
-      for (int v = 0; v < nv; ++v)
-        copy(gbuf[v] + op->recv_off[i], area(q, par) + kSlots + qoff + (long long)v * qcnt, qcnt, st);
-    }
-    finish(c, st, par, true);
-  }
-  bool graph_capturable() const override { return false; }
-};
-
-IpcComm* ipc_comm_open(pcgx_context c, const std::string& name, size_t mailbox_bytes) {
-  auto ic = std::make_unique<IpcComm>();
-  const int P = c->nranks;
-  ic->rank = c->rank;
-  ic->nranks = P;
-  ic->device = c->device;
-  // the shared-memory segment holds the setup exports and two block-row directories
-  const size_t hbox = std::max(sizeof(IpcExport), (size_t)4 * P * sizeof(int64_t));
-  ic->hc.reset(host_comm_open(P, c->rank, name, hbox));
-  ic->capd = (long long)((mailbox_bytes + 127) / 128 * 16) + kSlots;  // 128-byte aligned areas
-  PCGX_CUDA(cudaMalloc(&ic->box, sizeof(double) * 2 * (size_t)ic->capd));
-  IpcExport ex{};
-  PCGX_CUDA(cudaIpcGetMemHandle(&ex.box, ic->box));
-  for (int par = 0; par < 2; ++par) {
-    PCGX_CUDA(cudaEventCreateWithFlags(&ic->ready[par], cudaEventDisableTiming | cudaEventInterprocess));
-    PCGX_CUDA(cudaEventCreateWithFlags(&ic->done[par], cudaEventDisableTiming | cudaEventInterprocess));
-    PCGX_CUDA(cudaIpcGetEventHandle(&ex.ready[par], ic->ready[par]));
-    PCGX_CUDA(cudaIpcGetEventHandle(&ex.done[par], ic->done[par]));
-  }
-  ex.device = c->device;
-  ex.cap = ic->capd;
-  std::memcpy(ic->hc->box(c->rank), &ex, sizeof ex);
-  ic->hc->barrier();
-  ic->peer.assign((size_t)P, nullptr);
-  ic->pready.assign((size_t)P, {nullptr, nullptr});
-  ic->pdone.assign((size_t)P, {nullptr, nullptr});
-  ic->peer[(size_t)c->rank] = ic->box;
-  for (int q = 0; q < P; ++q) {
-    if (q == c->rank) continue;
-    IpcExport qe;
-    std::memcpy(&qe, ic->hc->box(q), sizeof qe);
-    if (qe.cap != ic->capd) fail(PCGX_ERR_INVALID, "ipc comm: ranks disagree on the mailbox size");
-    if (qe.device != c->device) {
-      int can = 0;
-      PCGX_CUDA(cudaDeviceCanAccessPeer(&can, c->device, qe.device));
-      if (!can)
-        fail(PCGX_ERR_UNSUPPORTED, "ipc comm: device " + std::to_string(c->device) + " cannot access device " +
-                                       std::to_string(qe.device) + " (peer access)");
-    }
-    void* m = nullptr;
-    PCGX_CUDA(cudaIpcOpenMemHandle(&m, qe.box, cudaIpcMemLazyEnablePeerAccess));
-    ic->peer[(size_t)q] = static_cast<double*>(m);
-    for (int par = 0; par < 2; ++par) {
-      PCGX_CUDA(cudaIpcOpenEventHandle(&ic->pready[(size_t)q][par], qe.ready[par]));
-      PCGX_CUDA(cudaIpcOpenEventHandle(&ic->pdone[(size_t)q][par], qe.done[par]));
-    }
-  }
-  PCGX_CUDA(cudaMalloc(&ic->d_peer, sizeof(double*) * (size_t)P));
-  PCGX_CUDA(cudaMemcpy(ic->d_peer, ic->peer.data(), sizeof(double*) * (size_t)P, cudaMemcpyHostToDevice));
-  ic->hc->barrier();  // every rank has read the exports: the segment's boxes become directories
-  return ic.release();
-}
-
-void allreduce(pcgx_context c, int slot, int count) {
-  if (!c->cm) return;
-  c->cm->allreduce(c, slot, count);
-  c->cur_allreduce++;
-}
-
-// Sum k <= 5 host doubles over the ranks through the scratch slots S_DOT..S_E2 (setup
-// checks), stream-ordered on c->s: the comms' all-reduces are asynchronous there.
-void allreduce_host(pcgx_context c, const double* in, double* out, int k) {
-  PCGX_CUDA(cudaMemcpyAsync(c->S + S_DOT, in, sizeof(double) * k, cudaMemcpyHostToDevice, c->s));
-  allreduce(c, S_DOT, k);
-  PCGX_CUDA(cudaMemcpyAsync(out, c->S + S_DOT, sizeof(double) * k, cudaMemcpyDeviceToHost, c->s));
-  PCGX_CUDA(cudaStreamSynchronize(c->s));
-}
-
+#include "host_comm.cuh"
 // ---------------------------------------------------------------- operator launch
 
 void NcclComm::halo_begin(pcgx_context c, pcgx_operator op, const double* const* xs, int nv) {
@@ -2628,573 +1985,7 @@ void enqueue_prec(pcgx_context c, pcgx_operator op, const Prec& P, const double*
   else enqueue_newton(c, op, P.newton, r, out, rz_slot);
 }
 
-// ---------------------------------------------------------------- PCG
-
-template <class F>
-void capture(pcgx_context c, Graph& g, F&& body) {
-  const int64_t before = c->cur_launches;
-  const int64_t before_ar = c->cur_allreduce;
-  PCGX_CUDA(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
-  c->capturing = true;
-  try {
-    body();
-    c->capturing = false;
-  } catch (...) {
-    c->capturing = false;
-    cudaGraph_t tmp;
-    cudaStreamEndCapture(c->s, &tmp);
-    if (tmp) cudaGraphDestroy(tmp);
-    throw;
-  }
-  cudaGraph_t graph;
-  PCGX_CUDA(cudaStreamEndCapture(c->s, &graph));
-  PCGX_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
-  cudaGraphDestroy(graph);
-  g.kernels = c->cur_launches - before;
-  c->cur_launches = before;  // counted per replay instead
-  c->launches -= g.kernels;
-  g.allreduces = c->cur_allreduce - before_ar;
-  c->cur_allreduce = before_ar;
-}
-
-// Capture of a PCG segment whose tail runs only while the solve has not
-// converged: body() enqueues the head, calls cond_split(c) once (after the kernel
-// that writes the convergence flag), then the tail. The head is captured into the
-// root graph, the tail into the body graph of an IF node that follows it, so at
-// convergence the device skips the tail (the speculative P r and A p of the
-// reference's stopping iteration, pcg.cpp:89-95) instead of computing and
-// discarding it.
-template <class F>
-void capture_cond(pcgx_context c, Graph& g, F&& body) {
-  const int64_t before = c->cur_launches;
-  const int64_t before_ar = c->cur_allreduce;
-  cudaGraph_t root = nullptr;
-  PCGX_CUDA(cudaGraphCreate(&root, 0));
-  c->cond_root = root;
-  c->cond_split = false;
-  c->cond_mark = 0;
-  try {
-    PCGX_CUDA(cudaGraphConditionalHandleCreate(&c->cond_h, root, 1u, cudaGraphCondAssignDefault));
-    PCGX_CUDA(cudaStreamBeginCaptureToGraph(c->s, root, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    c->capturing = true;
-    body();
-    c->capturing = false;
-    cudaGraph_t tmp = nullptr;
-    PCGX_CUDA(cudaStreamEndCapture(c->s, &tmp));
-    if (!c->cond_split) fail(PCGX_ERR_CUDA, "capture_cond: the segment never split");
-    PCGX_CUDA(cudaGraphInstantiate(&g.exec, root, 0));
-  } catch (...) {
-    c->capturing = false;
-    cudaStreamCaptureStatus st;
-    if (cudaStreamIsCapturing(c->s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
-      cudaGraph_t tmp = nullptr;
-      cudaStreamEndCapture(c->s, &tmp);
-    }
-    cudaGetLastError();
-    cudaGraphDestroy(root);
-    c->cond_root = nullptr;
-    throw;
-  }
-  cudaGraphDestroy(root);
-  c->cond_root = nullptr;
-  g.kernels = c->cur_launches - before;
-  g.body_kernels = c->cur_launches - c->cond_mark;
-  c->cur_launches = before;
-  c->launches -= g.kernels;
-  g.allreduces = c->cur_allreduce - before_ar;
-  c->cur_allreduce = before_ar;
-}
-
-__global__ void cond_kernel(cudaGraphConditionalHandle h, const double* S, int slot_rr, int slot_bnorm,
-                            int slot_tol) {
-  // the host's test, same operations: rel_res = sqrt(r'r) / ||b||; stop iff <= tol
-  const double rel = sqrt(S[slot_rr]) / S[slot_bnorm];
-  cudaGraphSetConditional(h, rel <= S[slot_tol] ? 0u : 1u);
-}
-
-// Inside capture_cond's body: the convergence flag from S[slot_rr], then the IF
-// node; everything enqueued after this runs only if the solve goes on.
-// with_kernel = false: the reducing block of the preceding launch already set the
-// condition (Reduce::cond_bt, the fused first pass's r'r)
-void cond_split(pcgx_context c, int slot_rr, bool with_kernel = true) {
-  if (with_kernel) {
-    cond_kernel<<<1, 1, 0, c->s>>>(c->cond_h, c->S, slot_rr, S_BNORM, S_TOL);
-    check_launch();
-    count_launch(c);
-  }
-  cudaStreamCaptureStatus st;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t nd = 0;
-  PCGX_CUDA(cudaStreamGetCaptureInfo(c->s, &st, nullptr, nullptr, &deps, &nd));
-  std::vector<cudaGraphNode_t> dv(deps, deps + nd);
-  cudaGraphNodeParams cp{};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = c->cond_h;
-  cp.conditional.type = cudaGraphCondTypeIf;
-  cp.conditional.size = 1;
-  cudaGraphNode_t node;
-  PCGX_CUDA(cudaGraphAddNode(&node, c->cond_root, dv.data(), dv.size(), &cp));
-  cudaGraph_t tmp = nullptr;
-  PCGX_CUDA(cudaStreamEndCapture(c->s, &tmp));
-  PCGX_CUDA(cudaStreamBeginCaptureToGraph(c->s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                          cudaStreamCaptureModeThreadLocal));
-  c->cond_split = true;
-  c->cond_mark = c->cur_launches;
-}
-
-void replay(pcgx_context c, Graph& g) {
-  PCGX_CUDA(cudaGraphLaunch(g.exec, c->s));
-  c->cur_launches += g.kernels;
-  c->launches += g.kernels;
-  c->cur_allreduce += g.allreduces;
-}
-
-std::string fmt_double(double v) { return std::to_string(v); }
-
-// Matrix bytes of one pass in the device storage: int32 CSR 12 nnz + 4 (n+1);
-// BSR-3 8 nnz + 4 per block + 4 per block row; stencil none.
-double matrix_bytes(pcgx_operator op) {
-  if (op->kind == 0) return 0.0;
-  // the grid copy the regular steps stream (bsr3t_kernel): every slot of every node
-  // (absent blocks as zeros) + the masks; the other launches' SELL arrays are ~4% larger
-  if (op->b3g_val && op->tune.bsr3t != 0)
-    return 8.0 * 243.0 * (double)(op->n_local / 3) + 4.0 * (double)(op->n_local / 3);
-  if (op->bsr_ptr)
-    return 8.0 * (double)op->nnz + 4.0 * (double)op->bsr_blocks + 4.0 * (double)(op->n_local / 3 + 1);
-  if (op->dia_val) return 8.0 * (double)op->dia_k * (double)op->n_local + 4.0 * (double)op->n_local;
-  return 12.0 * (double)op->nnz + 4.0 * (double)(op->n_local + 1);
-}
-// SpMV-equivalent bytes, the BASELINE metric's numerator: stencil
-// 16 B/unknown (read x, write y); CSR 12 nnz + 4 (n+1) + 16 n whatever the storage.
-double spmv_equiv_bytes(pcgx_operator op) {
-  if (op->kind == 0) return 16.0 * (double)op->n_local;
-  return 12.0 * (double)op->nnz + 4.0 * (double)(op->n_local + 1) + 16.0 * (double)op->n_local;
-}
-// Algorithmic bytes of one SpMV pass in the actual storage (read x, write y).
-double spmv_alg_bytes(pcgx_operator op) { return matrix_bytes(op) + 16.0 * (double)op->n_local; }
-// Fused Chebyshev middle step: stencil 32 B/unknown; CSR / BSR matrix bytes + 32 n
-// (+ 8 n for the inv_sqrt_diag vector read with the row).
-double cheb_step_bytes(pcgx_operator op) {
-  if (op->kind == 0) return 32.0 * (double)op->n_local;
-  return matrix_bytes(op) + 40.0 * (double)op->n_local;
-}
-
-void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const double* b,
-                      double* x, const pcgx_solve_opts* o, pcgx_report* rep) {
-  NvtxRange nvtx_solve("pcgx::pcg_solve");
-  if (op->ctx != c) fail(PCGX_ERR_INVALID, "pcg_solve: operator belongs to another context");
-  pcgx_solve_opts opts;
-  pcgx_solve_opts_default(&opts);
-  if (o) opts = *o;
-  if (!(opts.tol > 0.0)) fail(PCGX_ERR_INVALID, "pcg_solve: tol must be positive");
-  if (opts.maxit < 1) fail(PCGX_ERR_INVALID, "pcg_solve: maxit must be >= 1");
-  const bool have_prec = prec.kind != 0;
-  const Cheb& P = prec.cheb;
-  const int m = prec.degree();
-  const long long n = op->n_local;
-  ensure_workspace(c, n, ws_pad_of(op));
-  // CUDA graphs on one GPU; multi-rank solves launch directly by default (the
-  // speculative schedule hides the launches either way; PCGX_GRAPH_MULTI=1 captures
-  // the NCCL plane exchanges and all-reduces into the graphs too)
-  const bool use_graph = !(opts.flags & PCGX_FLAG_NO_GRAPH) && op->tune.no_graph == 0 &&
-                         (!c->cm || (c->cm->graph_capturable() && op->tune.graph_multi != 0));
-  // one GPU: snapshot r'r right after the update and overlap the host check with
-  // the speculative P r; multi-GPU: merge [r'r, r'z] into one all-reduce after P r
-  // (PCGX_MERGED=1 forces the multi-GPU schedule on one GPU, for tests)
-  const bool spec_after_update = !c->cm && op->tune.merged == 0;
-  // one GPU with graphs: the speculative tail of each segment (P r and A p of the
-  // next iteration) sits in a conditional IF node that a device-side convergence
-  // test closes, so nothing is computed and discarded at convergence
-  // (degree >= tune.cond_graph, default 10: below it the IF node's per-iteration
-  // cost outweighs the one skipped tail per solve; m = 0 / plain CG never)
-  const bool use_cond = use_graph && spec_after_update && op->tune.cond_graph > 0 && prec.kind != 0 &&
-                        m >= op->tune.cond_graph;
-
-  std::memset(rep, 0, sizeof *rep);
-  c->cur_launches = 0;
-  c->cur_allreduce = 0;
-  c->cur_halo_bytes = 0;
-  double* r = c->r;
-  double* z = c->z;
-  double* p = c->p;
-  double* q = c->q;
-
-  PCGX_CUDA(cudaEventRecord(c->ev_t0, c->s));
-  auto finish = [&]() {
-    PCGX_CUDA(cudaEventRecord(c->ev_t1, c->s));
-    PCGX_CUDA(cudaEventSynchronize(c->ev_t1));
-    float ms = 0.f;
-    PCGX_CUDA(cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1));
-    rep->wall_time = ms * 1e-3;
-    rep->kernel_launches = c->cur_launches;
-    rep->allreduces = c->cur_allreduce;
-    rep->halo_bytes = c->cur_halo_bytes;
-    rep->spmv_equiv_bytes = (double)rep->matvec * spmv_equiv_bytes(op);
-  };
-  double alg = 0.0;  // algorithmic bytes, accumulated per enqueued pass
-  const double N8 = 8.0 * (double)n;
-  auto cheb_bytes = [&]() -> double {  // one preconditioner application incl. r.z
-    if (!have_prec) return 2 * N8;
-    if (prec.kind == 2) return newton_bytes(op, prec.newton.nlev, true);
-    if (m == 0) return 2 * N8;
-    const double spmv_extra = matrix_bytes(op);
-    if (m == 1) return spmv_extra + 2 * N8;
-    if (op->kind == 0 && op->cheb2)  // (1,2): read r, write x1 x2; pairs: 3 reads 2 writes; odd tail: 4
-      return 3 * N8 + (double)((m - 2) / 2) * 5 * N8 + ((m % 2) ? 4 * N8 : 0.0);
-    return (spmv_extra + 2 * N8) + (spmv_extra + 3 * N8) + (double)(m - 2) * (spmv_extra + 4 * N8);
-  };
-
-  // ||b|| (pcg.cpp:32)
-  auto nvtx_setup = std::make_unique<NvtxRange>("pcgx::pcg_solve setup");
-  launch_dot(c, n, b, b, S_BB);
-  allreduce(c, S_BB, 1);
-  fetch_scalars(c);
-  alg += N8;
-  const double bnorm = std::sqrt(c->hS[S_BB]);
-  rep->ddot++;
-  if (use_cond) {  // ||b|| and tol for the device convergence test (cond_kernel)
-    const double bt[2] = {bnorm, opts.tol};
-    static_assert(S_TOL == S_BNORM + 1, "adjacent slots");
-    PCGX_CUDA(cudaMemcpyAsync(c->S + S_BNORM, bt, sizeof bt, cudaMemcpyHostToDevice, c->s));
-  }
-  if (bnorm == 0.0) {
-    launch_fill(c, n, x, 0.0);
-    rep->converged = 1;
-    finish();
-    rep->alg_bytes = alg;
-    return;
-  }
-  if (opts.x0) {
-    copy_d2d(c, x, opts.x0, n);
-    op_launch<EpiResid, true>(c, op, x, EpiResid{b, r}, S_RR0);  // r = b - A x0
-    allreduce(c, S_RR0, 1);
-    fetch_scalars(c);
-    alg += spmv_alg_bytes(op) + 2 * N8;
-    rep->matvec++;
-    const double rnorm = std::sqrt(c->hS[S_RR0]);
-    rep->ddot++;
-    rep->rel_res = rnorm / bnorm;
-    if (rep->rel_res <= opts.tol) {
-      rep->converged = 1;
-      rep->true_rel_res = rep->rel_res;
-      finish();
-      rep->alg_bytes = alg;
-      return;
-    }
-  } else {
-    copy_d2d(c, r, b, n);
-    launch_fill(c, n, x, 0.0);
-    alg += 3 * N8;
-    rep->rel_res = 1.0;
-  }
-
-  // zmode: 0 = Chebyshev m >= 1 (z from the fused recurrence), 1 = m == 0 (z = r/theta
-  // written by the update kernel), 2 = no preconditioner (z is r itself).
-  const int zm = !have_prec ? 2 : (prec.kind == 1 && m == 0 ? 1 : 0);
-  double* Pd[2] = {p, c->p2};  // direction ping-pong: p(it) lives in Pd[it & 1]
-  const bool fuse = fuses_dir_update(op) && op->tune.no_fuse_p == 0;
-  // m = 0 on the TMA direction step: z = r / theta is formed there from r, never
-  // stored (the update kernel only reduces r'z): 8 B less per unknown and iteration
-  const bool zdiv = zm == 1 && fuse && dir_tma_ok(op) && op->tune.zdiv != 0;
-  const double* zvec = (zm == 2 || zdiv) ? r : z;
-  // single-rank stencil: x += alpha p moves from the update kernel into the next
-  // direction step, which reads p_old anyway (8 B less per unknown and iteration)
-  // (not with on_iterate: x must be current at every iteration's callback)
-  const bool cb = opts.on_iterate != nullptr;
-  const bool defer_x = fuse && dir_tma_ok(op) && op->tune.defer_x != 0 && !cb;
-  // one GPU, Chebyshev m >= 3 on the stencil: the update r -= alpha q, r'r rides in
-  // the first two-step pass of P r (cheb2f_upd_launch); r(it) lives in Rb[it & 1]
-  const bool fuse_upd = zm == 0 && prec.kind == 1 && (spec_after_update || c->cm != nullptr) && defer_x &&
-                        cheb_upd_ok(c, op, m);
-  double* Rb[2] = {r, fuse_upd ? c->r2 : r};
-
-  // dir_spmv(it): p(it) = z + beta p(it-1) (p(1) = z), q = A p(it), p'q -> pq(par); the
-  // direction update is fused into the SpMV's input (InComb) where the kernels allow it.
-  auto enqueue_dir_spmv = [&](int it) {
-    const int par = it & 1;
-    double* pnew = Pd[par];
-    const double* pold = Pd[par ^ 1];
-    const int first = (it == 1) ? 1 : 0;
-    if (fuse && dir_tma_ok(op)) {
-      // the previous iteration's x += alpha p_old rides along (defer_x)
-      dir_tma_launch(c, op, zvec, pold, pnew, q, slot_rz(par ^ 1), slot_rz(par), first, slot_pq(par),
-                     defer_x ? x : nullptr, slot_pq(par ^ 1), zdiv ? P.theta : 0.0);
-    } else if (fuse) {
-      op_launch_in<InComb, EpiStoreP, true>(
-          c, op, in_of(op, zvec, pold, c->S, slot_rz(par ^ 1), slot_rz(par), first, true),
-          EpiStoreP{q, pnew}, slot_pq(par));
-    } else {
-      pupdate_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, pnew, pold, zvec, c->S,
-                                                                slot_rz(par ^ 1), slot_rz(par), first);
-      check_launch();
-      count_launch(c);
-      op_launch<EpiStore, true>(c, op, pnew, EpiStore{q}, slot_pq(par));
-    }
-    allreduce(c, slot_pq(par), 1);
-  };
-  const double bytes_dir = fuse ? spmv_alg_bytes(op) + 2 * N8 : spmv_alg_bytes(op) + 3 * N8;
-  // one rank: every scalar the host checks reached hS from its reducing kernel
-  // (Reduce::mirror); several ranks: the all-reduced slots are copied
-  const bool snap_copy = c->cm != nullptr || op->tune.snap_memcpy != 0;
-  auto snapshot = [&]() {  // External: when captured, the graph records ev_sync on every replay
-    if (snap_copy)
-      PCGX_CUDA(cudaMemcpyAsync(c->hS, c->S, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->s));
-    if (c->capturing) PCGX_CUDA(cudaEventRecordWithFlags(c->ev_sync, c->s, cudaEventRecordExternal));
-    else PCGX_CUDA(cudaEventRecord(c->ev_sync, c->s));
-  };
-  // snapshot right after the update when r'r (and r'z for zmode > 0) are final there
-  const bool snap_after_update = spec_after_update || zm > 0;
-  // B(it): [prec(it) -> z, r'z ; multi-GPU: all-reduce (r'r, r'z) + snapshot] ; dir_spmv(it+1)
-  auto enqueue_B = [&](int it) {
-    const int par = it & 1;
-    if (fuse_upd) {
-      // r(it) = r(it-1) - alpha(it) q(it) inside P r(it)'s first pass; the scalar
-      // snapshot (r'r(it), p'q(it)) is taken right after that pass (and, with the
-      // conditional graph, the convergence test: the rest runs only if not converged)
-      const CgUpd u{Rb[par ^ 1], q, Rb[par], slot_rz(par ^ 1), slot_pq(par), slot_rr(par)};
-      if (spec_after_update) {
-        enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u, [&] {
-          snapshot();
-          if (use_cond) cond_split(c, slot_rr(par), false);  // the first pass set the condition
-        });
-      } else {
-        // several ranks: the pass reduced this rank's share of r'r; [r'r, r'z] are
-        // all-reduced together after P r, as without the fusion
-        enqueue_cheb(c, op, P, Rb[par], z, slot_rz(par), &u);
-        allreduce(c, slot_rr(par), 2);
-        snapshot();
-      }
-    } else if (use_cond) {
-      cond_split(c, slot_rr(par));  // r'r(it) came from the update kernel before this segment
-      if (zm == 0) enqueue_prec(c, op, prec, r, z, slot_rz(par));
-    } else if (zm == 0) {
-      enqueue_prec(c, op, prec, r, z, slot_rz(par));
-      if (!spec_after_update) {
-        allreduce(c, slot_rr(par), 2);
-        snapshot();
-      }
-    }
-    enqueue_dir_spmv(it + 1);
-  };
-  // setup: z_0 = P r_0 and rho_0 = r'z -> rz(0) (pcg.cpp:57-64)
-  if (zm == 0) enqueue_prec(c, op, prec, r, z, slot_rz(0));
-  else if (zm == 1) launch_zr(c, n, z, r, P.theta, 1, slot_rz(0));
-  else launch_dot(c, n, r, r, slot_rz(0));
-  // the two segment graphs (iteration parity 1, 0): cached across solves; a new
-  // one is captured here, on the host, while the device works on the setup P r
-  Graph* gB[2] = {nullptr, nullptr};
-  if (use_graph) {
-    std::string key;
-    auto add = [&](const void* v, size_t bytes) { key.append((const char*)v, bytes); };
-    const uint64_t ids[3] = {op->uid, c->ws_gen, defer_x ? (uint64_t)(uintptr_t)x : 0};
-    add(ids, sizeof ids);
-    const int flags[8] = {prec.kind, m,        zm, fuse ? 1 : 0, spec_after_update ? 1 : 0, fuse_upd ? 1 : 0,
-                          snap_copy ? 1 : 0, use_cond ? 1 : 0};
-    add(flags, sizeof flags);
-    if (prec.kind == 1) {
-      const double t[3] = {P.theta, P.delta, P.sigma};
-      add(t, sizeof t);
-      add(P.rho.data(), sizeof(double) * P.rho.size());
-    } else if (prec.kind == 2) {
-      add(prec.newton.zeta.data(), sizeof(double) * prec.newton.zeta.size());
-    }
-    for (int par = 0; par < 2; ++par) {
-      const std::string k = key + (par ? "1" : "0");
-      auto hit = c->gcache.find(k);
-      if (hit == c->gcache.end()) {
-        if (c->gcache.size() >= 64) c->gcache.clear();
-        auto g = std::make_unique<Graph>();
-        if (use_cond) capture_cond(c, *g, [&] { enqueue_B(par ? 1 : 2); });
-        else capture(c, *g, [&] { enqueue_B(par ? 1 : 2); });
-        hit = c->gcache.emplace(k, std::move(g)).first;
-      }
-      gB[par] = hit->second.get();
-    }
-  }
-  allreduce(c, slot_rz(0), 1);
-  alg += cheb_bytes();
-  if (have_prec) {
-    rep->prec_applies++;
-    rep->matvec += m;
-  }
-  rep->ddot++;
-  fetch_scalars(c);
-  {
-    const double rho = c->hS[slot_rz(0)];
-    if (!std::isfinite(rho) || rho <= 0.0)
-      fail(PCGX_ERR_NUMERICAL,
-           "pcg_solve: r'z = " + fmt_double(rho) + " at setup (preconditioner not SPD?)");
-  }
-
-  // fused: the first pass also reads q and writes r (+16 B), the update (24 B) is gone
-  const double bytes_B = (zm == 0 ? cheb_bytes() : 0.0) + bytes_dir + (defer_x ? 2 * N8 : 0.0) +
-                         (fuse_upd ? 2 * N8 : 0.0);
-  const double bytes_update = (defer_x ? 3 : 6) * N8 + (zm == 1 && !zdiv ? N8 : 0.0);
-  bool x_pending = false;  // a deferred x update no direction step has applied yet
-  int x_par = 0;
-
-  enqueue_dir_spmv(1);
-  alg += bytes_dir;
-  nvtx_setup.reset();
-  auto nvtx_iter = std::make_unique<NvtxRange>("pcgx::pcg_solve iterations");
-  for (int it = 1; it <= opts.maxit; ++it) {
-    const int par = it & 1;
-    const bool more = it < opts.maxit;
-    const bool upd_in_B = fuse_upd && more;  // else a standalone update (in place)
-    if (!upd_in_B) {
-      launch_update(c, n, defer_x ? nullptr : x, Rb[par ^ 1], Pd[par], q, slot_rz(par ^ 1), slot_pq(par),
-                    slot_rr(par), zm, zm == 1 ? P.theta : 1.0, zdiv ? nullptr : z);
-      check_launch();
-      count_launch(c);
-      alg += bytes_update;
-    }
-    x_pending = defer_x;
-    x_par = par;
-    rep->matvec++;  // q = A p of this iteration
-    if (!spec_after_update && (zm > 0 || !more)) allreduce(c, slot_rr(par), zm > 0 ? 2 : 1);
-    if ((snap_after_update && !upd_in_B) || !more) snapshot();
-    if (more) {
-      if (use_graph) {
-        replay(c, *gB[par]);
-      } else {
-        enqueue_B(it);
-      }
-      alg += bytes_B;
-      x_pending = false;  // dir_spmv(it+1) applies it
-    }
-    PCGX_CUDA(cudaEventSynchronize(c->ev_sync));
-    const double* hs = c->hS;
-    // checks in the reference's order: r'z(it-1) [pcg.cpp:103-106], p'Ap [:76-79], ||r|| [:85]
-    const bool rz_now = !spec_after_update || zm > 0;  // r'z(it) is in this snapshot
-    if (it >= 2 && !rz_now) {
-      const double rho_prev = hs[slot_rz(par ^ 1)];
-      if (!std::isfinite(rho_prev) || rho_prev <= 0.0)
-        fail(PCGX_ERR_NUMERICAL,
-             "pcg_solve: r'z = " + fmt_double(rho_prev) + " (preconditioner not SPD?)");
-    }
-    const double pq = hs[slot_pq(par)];
-    rep->ddot++;
-    if (!std::isfinite(pq) || pq <= 0.0)
-      fail(PCGX_ERR_NUMERICAL, "pcg_solve: p'Ap = " + fmt_double(pq) + " (operator not SPD?)");
-    const double rnorm = std::sqrt(hs[slot_rr(par)]);
-    rep->ddot++;
-    if (!std::isfinite(rnorm)) fail(PCGX_ERR_NUMERICAL, "pcg_solve: residual norm is not finite");
-    rep->iters = it;
-    rep->rel_res = rnorm / bnorm;
-    if (cb) {  // opts.on_iterate(it, x) (pcg.cpp:88): x(it) was final before the snapshot
-      c->hx.resize((size_t)n);
-      PCGX_CUDA(cudaMemcpyAsync(c->hx.data(), x, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->s));
-      PCGX_CUDA(cudaStreamSynchronize(c->s));
-      if (opts.on_iterate(it, c->hx.data(), n, opts.on_iterate_user) != 0)
-        fail(PCGX_ERR_CALLBACK, "pcg_solve: on_iterate stopped the solve at iteration " + std::to_string(it));
-    }
-    if (rep->rel_res <= opts.tol) {
-      rep->converged = 1;
-      if (more && use_cond) {
-        // the device skipped the segment's tail (IF node): only a fused first pass
-        // of P r ran; the direction step that would apply x += alpha p did not
-        rep->wasted_matvec = fuse_upd ? 2 : 0;
-        c->cur_launches -= gB[par]->body_kernels;
-        c->launches -= gB[par]->body_kernels;
-        alg -= bytes_B - (fuse_upd ? 5 * N8 : 0.0);
-        x_pending = defer_x;
-        x_par = par;
-      } else if (more) {
-        rep->wasted_matvec = (zm == 0 ? m : 0) + 1;  // speculative P r and A p
-      }
-      break;
-    }
-    if (!more) break;
-    if (have_prec) {
-      rep->prec_applies++;
-      rep->matvec += m;
-    }
-    rep->ddot++;  // r'z
-    if (rz_now) {
-      const double rz = hs[slot_rz(par)];
-      if (!std::isfinite(rz) || rz <= 0.0)
-        fail(PCGX_ERR_NUMERICAL, "pcg_solve: r'z = " + fmt_double(rz) + " (preconditioner not SPD?)");
-    }
-  }
-  if (x_pending) {  // the iteration limit ended the loop before the next direction step
-    xupd_kernel<<<vec_grid(c, n), kVecThreads, 0, c->s>>>(n, x, Pd[x_par], c->S, slot_rz(x_par ^ 1),
-                                                          slot_pq(x_par));
-    check_launch();
-    count_launch(c);
-    alg += 3 * N8;
-  }
-  // true residual (pcg.cpp:112-115)
-  nvtx_iter.reset();
-  NvtxRange nvtx_exit("pcgx::pcg_solve true residual");
-  op_launch<EpiResid, true>(c, op, x, EpiResid{b, nullptr}, S_EE);
-  allreduce(c, S_EE, 1);
-  fetch_scalars(c);
-  alg += spmv_alg_bytes(op) + N8;
-  rep->matvec++;
-  rep->true_rel_res = std::sqrt(c->hS[S_EE]) / bnorm;
-  rep->ddot++;
-  finish();
-  rep->alg_bytes = alg;
-  rep->step_bytes = cheb_step_bytes(op);
-
-  // Optional: time the dominant kernel with CUDA events on the compute stream, on
-  // this solve's operator and buffers: the two-step pass (stencil, cheb2) or the
-  // fused single middle step.
-  if ((opts.flags & PCGX_FLAG_TIME_KERNELS) && prec.kind == 1 && m >= 4) {
-    const int reps = std::max(3, op->tune.step_reps);
-    const bool two = (op->kind == 0 && op->cheb2);
-    Cheb2Params q{};
-    if (two) {
-      q.nx = (int)op->nx;
-      q.ny = (int)op->ny;
-      q.nzl = (int)op->nzl;
-      q.nxy = op->nx * op->ny;
-      q.d = op->d;
-      q.theta = P.theta;
-      q.c2 = 2.0 / P.delta;
-      q.c3 = 2.0 * P.sigma;
-      q.rk1 = P.rho[3];
-      q.rk1m1 = P.rho[2];
-      q.rk2 = P.rho[4];
-      q.rk2m1 = P.rho[3];
-      q.outC = c->w2;
-      q.outE = c->w3;
-    }
-    EpiChebStep e{r, c->w0, c->w0, P.rho[3], P.rho[2], 2.0 / P.delta, 2.0 * P.sigma, P.theta, 0,
-                  1.0 / P.theta};
-    const bool three = two && cheb3_ok(c, op) && op->tune.cheb3 == 1 && m >= 5;
-    Cheb3Params q3{};
-    q3.c2 = 2.0 / P.delta;
-    q3.c3 = 2.0 * P.sigma;
-    q3.rk1 = P.rho[3];
-    q3.rk1m1 = P.rho[2];
-    q3.rk2 = P.rho[4];
-    q3.rk2m1 = P.rho[3];
-    q3.rk3 = P.rho[5];
-    q3.rk3m1 = P.rho[4];
-    q3.outE = c->w2;
-    q3.outF = c->w3;
-    auto launch = [&] {
-      if (three) cheb3_pass<false>(c, op, c->w1, c->w0, r, q3, -1);
-      else if (two) cheb2_pass<false, false>(c, op, c->w1, c->w0, r, q, -1);
-      else op_launch<EpiChebStep, false>(c, op, c->w1, e, -1);
-    };
-    const uint64_t mv0 = op->matvecs.load();
-    launch();  // warm
-    PCGX_CUDA(cudaEventRecord(c->ev_t0, c->s));
-    for (int i = 0; i < reps; ++i) launch();
-    PCGX_CUDA(cudaEventRecord(c->ev_t1, c->s));
-    PCGX_CUDA(cudaEventSynchronize(c->ev_t1));
-    op->matvecs.store(mv0);
-    float ms = 0.f;
-    PCGX_CUDA(cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1));
-    rep->step_ms = ms;
-    rep->step_launches = reps;
-    rep->step_bytes = two ? 40.0 * (double)op->n_local : cheb_step_bytes(op);
-    rep->step_steps = three ? 3 : (two ? 2 : 1);
-  }
-}
-
+#include "host_solve.cuh"
 // ---------------------------------------------------------------- power method / DACG
 // Device restatements of the reference's bound estimators (eigenest.cpp:35-167):
 // same iteration, same elementwise rounding, deterministic tree reductions; the
@@ -3422,998 +2213,7 @@ void lanczos_device(pcgx_context c, pcgx_operator op, int steps_hi, int steps, u
   *lo = l2;
 }
 
-// ---------------------------------------------------------------- operator creation
-
-void init_stencil_ghosts(pcgx_context c, pcgx_operator op) {
-  const size_t pb = sizeof(double) * (size_t)(op->nx * op->ny);
-  if (c->nranks > 1) {
-    if (c->rank > 0) {
-      PCGX_CUDA(cudaMalloc(&op->ghost_lo, pb));
-      PCGX_CUDA(cudaMalloc(&op->ghost_lo2, pb));
-    }
-    if (c->rank < c->nranks - 1) {
-      PCGX_CUDA(cudaMalloc(&op->ghost_hi, pb));
-      PCGX_CUDA(cudaMalloc(&op->ghost_hi2, pb));
-    }
-  }
-}
-
-int default_kz(pcgx_context c, long long nx, long long ny, long long nzl) {
-  (void)0;
-  (void)c;
-  (void)nx;
-  (void)ny;
-  (void)nzl;
-  return 16;
-}
-
-void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
-                const std::vector<int>& ci32, const double* va);
-void build_bsr3(pcgx_operator op, long long n, const std::vector<int>& rp32,
-                const std::vector<int>& ci32, const double* va);
-bool is_bsr3(long long n, const std::vector<int>& rp, const std::vector<int>& ci);
-bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>& ci, std::vector<int>& off,
-                 long long row_base = 0);
-template <int P>
-bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vector<int>& ci,
-                const std::vector<int>& off, long long row_base = 0);
-
-// Offset storage of one plane-aligned z-slab of a 27-point-box matrix on an nx^3
-// grid (multi-rank cfg3): the rank owns node planes [z0, z0 + nzl) (pcgx_slab_partition
-// of the nx planes), its rows' values by offset as build_dia lays them out, the
-// Jacobi values of its rows and of the neighbours' boundary planes (from the full
-// matrix: no exchange), and x-ghost planes the stencil slab machinery fills before
-// each SpMV (dia3_kernel reads them as planes -1 and nzl).
-// local: rp32 / va / dv hold this rank's rows only (rp32 from 0, ci32 global); the
-// neighbours' boundary-plane Jacobi values then come through the plane exchange.
-void dia_slab_upload(pcgx_context c, pcgx_operator op, long long n, int nx, const std::vector<int>& rp32,
-                     const std::vector<int>& ci32, const double* va, const std::vector<double>& dv,
-                     const std::vector<int>& off, bool local = false) {
-  const int P = c->nranks, me = c->rank;
-  int64_t z0 = 0, nzl = 0;
-  pcgx_slab_partition(nx, P, me, &z0, &nzl);
-  const long long nxy = (long long)nx * nx, r0 = z0 * nxy, nloc = nzl * nxy;
-  const long long rb = local ? r0 : 0;  // rp32 / dv index of global row g: g - rb
-  const int K = (int)off.size();
-  const long long ld = (nloc + 31) / 32 * 32;
-  std::vector<double> val((size_t)(ld * K), 0.0);
-  std::vector<unsigned> mask((size_t)nloc, 0u);
-#pragma omp parallel for schedule(static)
-  for (long long i = 0; i < nloc; ++i) {
-    const long long g = r0 + i;
-    int q = 0;
-    for (int k = rp32[(size_t)(g - rb)]; k < rp32[(size_t)(g - rb) + 1]; ++k) {
-      const int o = (int)((long long)ci32[(size_t)k] - g);
-      while (off[(size_t)q] != o) ++q;  // both ascending
-      val[(size_t)(q * ld + i)] = va[k];
-      mask[(size_t)i] |= 1u << q;
-    }
-  }
-  op->kind = 1;
-  op->n_global = n;
-  op->nnz = (long long)rp32[(size_t)(r0 - rb + nloc)] - rp32[(size_t)(r0 - rb)];
-  op->row0 = r0;
-  op->n_local = nloc;
-  op->dia_k = K;
-  op->dia_ld = ld;
-  for (int k = 0; k < K; ++k) op->dia_off[k] = off[(size_t)k];
-  op->dia3_pat = 27;
-  op->dia3_nx = nx;
-  op->dia3_nzl = (int)nzl;
-  op->nx = op->ny = nx;
-  op->nz = nx;
-  op->z0 = z0;
-  op->nzl = nzl;
-  PCGX_CUDA(cudaMalloc(&op->dia_val, sizeof(double) * val.size()));
-  PCGX_CUDA(cudaMalloc(&op->dia_mask, sizeof(unsigned) * std::max<size_t>(mask.size(), 1)));
-  PCGX_CUDA(cudaMemcpy(op->dia_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMemcpy(op->dia_mask, mask.data(), sizeof(unsigned) * mask.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * (size_t)std::max(nloc, 1LL)));
-  PCGX_CUDA(cudaMemcpy(op->dvec, dv.data() + (r0 - rb), sizeof(double) * (size_t)nloc, cudaMemcpyHostToDevice));
-  if (me > 0) PCGX_CUDA(cudaMalloc(&op->dia3_dlo, sizeof(double) * (size_t)nxy));
-  if (me < P - 1) PCGX_CUDA(cudaMalloc(&op->dia3_dhi, sizeof(double) * (size_t)nxy));
-  init_stencil_ghosts(c, op);  // x / p ghost planes (nx * nx) for the plane exchange
-  if (!local) {
-    if (me > 0)
-      PCGX_CUDA(cudaMemcpy(op->dia3_dlo, dv.data() + r0 - nxy, sizeof(double) * (size_t)nxy, cudaMemcpyHostToDevice));
-    if (me < P - 1)
-      PCGX_CUDA(cudaMemcpy(op->dia3_dhi, dv.data() + r0 + nloc, sizeof(double) * (size_t)nxy, cudaMemcpyHostToDevice));
-    return;
-  }
-  // the neighbours' boundary planes of d, once, through the operator's own plane exchange
-  PCGX_CUDA(cudaDeviceSynchronize());  // legacy-stream uploads before the compute / comm streams
-  const double* xs[1] = {op->dvec};
-  c->cm->halo_begin(c, op, xs, 1);
-  c->cm->halo_wait(c);
-  if (me > 0)
-    PCGX_CUDA(cudaMemcpyAsync(op->dia3_dlo, op->ghost_lo, sizeof(double) * (size_t)nxy, cudaMemcpyDeviceToDevice, c->s));
-  if (me < P - 1)
-    PCGX_CUDA(cudaMemcpyAsync(op->dia3_dhi, op->ghost_hi, sizeof(double) * (size_t)nxy, cudaMemcpyDeviceToDevice, c->s));
-  PCGX_CUDA(cudaStreamSynchronize(c->s));
-}
-
-// CSR block rows (the paper's MPI block-row SpMV): this rank
-// keeps rows [row0, row0 + nloc) with columns remapped to the local space:
-// owned columns -> [0, nloc), others -> nloc + (position in the ascending list
-// of ghost columns). Entries keep their order (the reference's summation order).
-// Each rank holds the full matrix on the host, so the send lists (the rows of
-// mine other ranks' rows reference) are computed without communication.
-void csr_upload_block(pcgx_context c, pcgx_operator op, long long n, const std::vector<int>& rp32,
-                      const std::vector<int>& ci32, const double* va, const std::vector<double>& dv) {
-  const int P = c->nranks, me = c->rank;
-  // a matrix of aligned 3 x 3 blocks keeps BSR-3 on every rank: rows split in whole
-  // block rows (the balanced partition of the n/3 block rows), the local columns
-  // remapped to [local | ghost] stay aligned triples, and bsr3_kernel reads the
-  // ghost columns through the same exchange as SELL
-  const bool bsr = op->tune.bsr != 0 && n % 3 == 0 && n >= 3LL * P && is_bsr3(n, rp32, ci32);
-  // offset storage on a cubic grid with the 27-point box (cfg3): plane-aligned
-  // z-slabs and the grid-tile kernel with the neighbours' boundary planes as ghosts
-  if (!bsr && op->tune.dia != 0 && op->tune.dia3 != 0) {
-    std::vector<int> doff;
-    const long long nnz_all = rp32[(size_t)n];
-    int nx = (int)std::llround(std::cbrt((double)n));
-    while ((long long)nx * nx * nx > n) --nx;
-    while ((long long)(nx + 1) * (nx + 1) * (nx + 1) <= n) ++nx;
-    if ((long long)nx * nx * nx == n && nx >= 3 && nx >= P && dia_offsets(n, rp32, ci32, doff) &&
-        (double)doff.size() * (double)n <= 1.5 * (double)nnz_all && dia3_match<27>(n, nx, rp32, ci32, doff)) {
-      dia_slab_upload(c, op, n, nx, rp32, ci32, va, dv, doff);
-      return;
-    }
-  }
-  std::vector<long long> start(P + 1);
-  for (int q = 0; q < P; ++q) {
-    int64_t z0, nl;
-    if (bsr) {
-      pcgx_slab_partition(n / 3, P, q, &z0, &nl);
-      z0 *= 3;
-    } else {
-      pcgx_slab_partition(n, P, q, &z0, &nl);
-    }
-    start[(size_t)q] = z0;
-  }
-  start[(size_t)P] = n;
-  const long long r0 = start[(size_t)me], r1 = start[(size_t)me + 1], nloc = r1 - r0;
-  if (nloc < 1) fail(PCGX_ERR_INVALID, "csr_create: fewer rows than ranks");
-  // ghost columns of my rows, ascending (hence grouped by owner)
-  std::vector<int> ghosts;
-  for (long long i = r0; i < r1; ++i)
-    for (int k = rp32[(size_t)i]; k < rp32[(size_t)i + 1]; ++k) {
-      const int col = ci32[(size_t)k];
-      if (col < r0 || col >= r1) ghosts.push_back(col);
-    }
-  std::sort(ghosts.begin(), ghosts.end());
-  ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
-  // local CSR
-  const long long k0 = rp32[(size_t)r0];
-  std::vector<int> lrp((size_t)nloc + 1), lci((size_t)(rp32[(size_t)r1] - k0));
-  for (long long i = r0; i <= r1; ++i) lrp[(size_t)(i - r0)] = (int)(rp32[(size_t)i] - k0);
-  for (long long k = k0; k < rp32[(size_t)r1]; ++k) {
-    const int col = ci32[(size_t)k];
-    lci[(size_t)(k - k0)] = (col >= r0 && col < r1)
-                                ? (int)(col - r0)
-                                : (int)(nloc + (std::lower_bound(ghosts.begin(), ghosts.end(), col) -
-                                                ghosts.begin()));
-  }
-  // per-neighbour traffic: recv = my ghosts owned by q; send = my rows q's rows reference
-  op->nb_rank.clear();
-  op->send_off.clear();
-  op->send_cnt.clear();
-  op->recv_off.clear();
-  op->recv_cnt.clear();
-  std::vector<int> send_idx;
-  for (int q = 0; q < P; ++q) {
-    if (q == me) continue;
-    const long long lo = std::lower_bound(ghosts.begin(), ghosts.end(), (int)start[(size_t)q]) - ghosts.begin();
-    const long long hi = std::lower_bound(ghosts.begin(), ghosts.end(), (int)start[(size_t)q + 1]) - ghosts.begin();
-    std::vector<int> need;  // rows of mine referenced by q's rows, ascending
-    for (long long i = start[(size_t)q]; i < start[(size_t)q + 1]; ++i)
-      for (int k = rp32[(size_t)i]; k < rp32[(size_t)i + 1]; ++k) {
-        const int col = ci32[(size_t)k];
-        if (col >= r0 && col < r1) need.push_back(col);
-      }
-    std::sort(need.begin(), need.end());
-    need.erase(std::unique(need.begin(), need.end()), need.end());
-    if (hi == lo && need.empty()) continue;
-    op->nb_rank.push_back(q);
-    op->recv_off.push_back(lo);
-    op->recv_cnt.push_back(hi - lo);
-    op->send_off.push_back((long long)send_idx.size());
-    op->send_cnt.push_back((long long)need.size());
-    for (int col : need) send_idx.push_back((int)(col - r0));
-  }
-  op->row0 = r0;
-  op->n_local = nloc;
-  op->nghost = (long long)ghosts.size();
-  op->nsend = (long long)send_idx.size();
-  std::vector<double> dext((size_t)(nloc + op->nghost));
-  for (long long i = 0; i < nloc; ++i) dext[(size_t)i] = dv[(size_t)(r0 + i)];
-  for (long long g = 0; g < op->nghost; ++g) dext[(size_t)(nloc + g)] = dv[(size_t)ghosts[(size_t)g]];
-  PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * dext.size()));
-  PCGX_CUDA(cudaMemcpy(op->dvec, dext.data(), sizeof(double) * dext.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMalloc(&op->rp, sizeof(int) * lrp.size()));
-  PCGX_CUDA(cudaMemcpy(op->rp, lrp.data(), sizeof(int) * lrp.size(), cudaMemcpyHostToDevice));
-  const size_t ng = (size_t)std::max(op->nghost, 1LL), nsd = (size_t)std::max(op->nsend, 1LL);
-  PCGX_CUDA(cudaMalloc(&op->send_idx, sizeof(int) * nsd));
-  if (op->nsend)
-    PCGX_CUDA(cudaMemcpy(op->send_idx, send_idx.data(), sizeof(int) * send_idx.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMalloc(&op->sbuf_z, sizeof(double) * nsd));
-  PCGX_CUDA(cudaMalloc(&op->sbuf_p, sizeof(double) * nsd));
-  PCGX_CUDA(cudaMalloc(&op->ghost_z, sizeof(double) * ng));
-  PCGX_CUDA(cudaMalloc(&op->ghost_p, sizeof(double) * ng));
-  if (bsr && is_bsr3(nloc, lrp, lci)) build_bsr3(op, nloc, lrp, lci, va + k0);
-  else build_sell(op, nloc, lrp, lci, va + k0);
-}
-
-// Block-row CSR from THIS rank's rows only (the paper's distributed matrix,
-// PAPER.md:683-685): rows [row0, row0 + nloc) of a symmetric n x n matrix with
-// global column indices, the balanced row partition pcgx_slab_partition gives.
-// No rank holds the full matrix. The halo lists need no communication because the
-// pattern is symmetric (a_ic != 0 <=> a_ci != 0): rank q needs my x_c exactly when
-// my row c has a column in q's rows, and I receive my ghost columns from their
-// owners -- both sides list them in ascending column order. The Jacobi values of
-// the ghost columns (other ranks' diagonals) travel once through the operator's own
-// block-row exchange. Values are uploaded as given: bitwise the rows the full-matrix
-// path uploads, so every SpMV / Chebyshev step equals the single-domain result.
-template <class I>
-void csr_upload_local(pcgx_context c, pcgx_operator op, long long n, long long r0, long long nloc, const I* rp,
-                      const I* ci, const double* va, const double* isd) {
-  const int P = c->nranks, me = c->rank;
-  if (!rp || !ci || !va) fail(PCGX_ERR_INVALID, "CsrMatrix: null array");
-  // The rows may follow one of three balanced partitions (the ones pcgx_csr_create
-  // cuts a full matrix by): plain rows; whole 3 x 3 block rows (n % 3 == 0: keeps
-  // BSR-3); whole node planes of an nx^3 grid (keeps the offset storage on z-slabs).
-  // Every rank reports which ones its [row0, row0 + n_local) matches and the job
-  // takes the first that all ranks match -- rows, block rows, planes.
-  int nxg = (int)std::llround(std::cbrt((double)n));
-  while ((long long)nxg * nxg * nxg > n) --nxg;
-  while ((long long)(nxg + 1) * (nxg + 1) * (nxg + 1) <= n) ++nxg;
-  const bool cube = (long long)nxg * nxg * nxg == n && nxg >= 3 && nxg >= P;
-  auto part_start = [&](int kind, int q) -> long long {  // first row of rank q (q == P: n)
-    if (q == P) return n;
-    int64_t z0, nl;
-    if (kind == 1) {
-      pcgx_slab_partition(n / 3, P, q, &z0, &nl);
-      return 3 * z0;
-    }
-    if (kind == 2) {
-      pcgx_slab_partition(nxg, P, q, &z0, &nl);
-      return z0 * (long long)nxg * nxg;
-    }
-    pcgx_slab_partition(n, P, q, &z0, &nl);
-    return z0;
-  };
-  auto matches = [&](int kind) {
-    if (kind == 1 && (n % 3 != 0 || n < 3LL * P)) return false;
-    if (kind == 2 && !cube) return false;
-    return r0 == part_start(kind, me) && r0 + nloc == part_start(kind, me + 1);
-  };
-  // local int32 arrays (rp from 0, global columns) for the pattern checks of the
-  // plane partition; validated below like every other path
-  int kind = -1;
-  bool slab = false;
-  std::vector<int> doff;
-  {
-    double f[4] = {matches(0) ? 1.0 : 0.0, matches(1) ? 1.0 : 0.0, matches(2) ? 1.0 : 0.0, 0.0};
-    std::vector<int> grp, gci;
-    if (f[2] > 0.0 && op->tune.dia != 0 && op->tune.dia3 != 0 && nloc >= 1 && n < (1LL << 31) &&
-        (long long)rp[nloc] - (long long)rp[0] < (1LL << 31)) {
-      const long long base0 = (long long)rp[0], nz = (long long)rp[nloc] - base0;
-      grp.resize((size_t)nloc + 1);
-      gci.resize((size_t)nz);
-      bool sane = true;
-      for (long long i = 0; i <= nloc; ++i) {
-        grp[(size_t)i] = (int)((long long)rp[i] - base0);
-        if (i && grp[(size_t)i] < grp[(size_t)i - 1]) sane = false;
-      }
-      for (long long k = 0; k < nz && sane; ++k) {
-        gci[(size_t)k] = (int)ci[k];
-        if ((long long)ci[k] < 0 || (long long)ci[k] >= n) sane = false;
-      }
-      if (sane && dia_offsets(nloc, grp, gci, doff, r0) && dia3_match<27>(nloc, nxg, grp, gci, doff, r0)) f[3] = 1.0;
-    }
-    double g[4];
-    allreduce_host(c, f, g, 4);
-    if (g[2] == (double)P && g[3] == (double)P) {
-      kind = 2;
-      slab = true;
-    } else if (g[0] == (double)P) {
-      kind = 0;
-    } else if (g[1] == (double)P) {
-      kind = 1;
-    } else if (g[2] == (double)P) {
-      kind = 2;
-    } else {
-      fail(PCGX_ERR_INVALID, "csr_create_local: rank " + std::to_string(me) + " must own rows [" +
-                                 std::to_string(part_start(0, me)) + ", " + std::to_string(part_start(0, me + 1)) +
-                                 ") (pcgx_slab_partition of the rows; or, on every rank, of the 3 x 3 block rows "
-                                 "or of the node planes of a cubic grid)");
-    }
-  }
-  std::vector<long long> start(P + 1);
-  for (int q = 0; q <= P; ++q) start[(size_t)q] = part_start(kind, q);
-  if (nloc < 1) fail(PCGX_ERR_INVALID, "csr_create: fewer rows than ranks");
-  const long long base = (long long)rp[0], nnz = (long long)rp[nloc] - base;
-  if (nnz >= (1LL << 31) || n >= (1LL << 31))
-    fail(PCGX_ERR_OVERFLOW, "csr_create: nnz " + std::to_string(nnz) + " does not fit the int32 device CSR");
-  const long long r1 = r0 + nloc;
-  std::vector<int> ghosts;
-  std::vector<double> dv((size_t)nloc);
-  long long bad = -1;
-  for (long long i = 0; i < nloc; ++i) {
-    if (rp[i + 1] < rp[i]) fail(PCGX_ERR_INVALID, "CsrMatrix: row_ptr not nondecreasing");
-    double diag = 0.0;
-    for (long long k = (long long)rp[i] - base; k < (long long)rp[i + 1] - base; ++k) {
-      const long long col = (long long)ci[k];
-      if (col < 0 || col >= n)
-        fail(PCGX_ERR_INVALID, "CsrMatrix: column index out of range in row " + std::to_string(r0 + i));
-      if (k > (long long)rp[i] - base && col <= (long long)ci[k - 1])
-        fail(PCGX_ERR_INVALID, "CsrMatrix: columns not strictly increasing in row " + std::to_string(r0 + i));
-      if (col == r0 + i) diag = va[k];
-      if (col < r0 || col >= r1) ghosts.push_back((int)col);
-    }
-    if (isd) dv[(size_t)i] = isd[i];
-    else if (!(diag > 0.0)) {
-      if (bad < 0) bad = r0 + i;
-    } else {
-      dv[(size_t)i] = 1.0 / std::sqrt(diag);  // jacobi_scale (linop.cpp:340-351)
-    }
-  }
-  // every rank learns whether any rank's diagonal is nonpositive (no rank may be
-  // left waiting in the exchange below)
-  {
-    const double flag = bad >= 0 ? 1.0 : 0.0;
-    double any = 0.0;
-    allreduce_host(c, &flag, &any, 1);
-    if (bad >= 0) fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry at index " + std::to_string(bad));
-    if (any > 0.0) fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry on another rank");
-  }
-  if (slab) {
-    // 27-point box on plane-aligned slabs: the offset storage, ghost planes through
-    // the stencil's plane exchange (as pcgx_csr_create keeps it for a full matrix)
-    std::vector<int> grp((size_t)nloc + 1), gci((size_t)nnz);
-    for (long long i = 0; i <= nloc; ++i) grp[(size_t)i] = (int)((long long)rp[i] - base);
-    for (long long k = 0; k < nnz; ++k) gci[(size_t)k] = (int)ci[k];
-    dia_slab_upload(c, op, n, nxg, grp, gci, va, dv, doff, true);
-    return;
-  }
-  std::sort(ghosts.begin(), ghosts.end());
-  ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
-  std::vector<int> lrp((size_t)nloc + 1), lci((size_t)nnz);
-  for (long long i = 0; i <= nloc; ++i) lrp[(size_t)i] = (int)((long long)rp[i] - base);
-  for (long long k = 0; k < nnz; ++k) {
-    const long long col = (long long)ci[k];
-    lci[(size_t)k] = (col >= r0 && col < r1)
-                         ? (int)(col - r0)
-                         : (int)(nloc + (std::lower_bound(ghosts.begin(), ghosts.end(), (int)col) - ghosts.begin()));
-  }
-  op->nb_rank.clear();
-  op->send_off.clear();
-  op->send_cnt.clear();
-  op->recv_off.clear();
-  op->recv_cnt.clear();
-  std::vector<int> send_idx;
-  for (int q = 0; q < P; ++q) {
-    if (q == me) continue;
-    const long long lo = std::lower_bound(ghosts.begin(), ghosts.end(), (int)start[(size_t)q]) - ghosts.begin();
-    const long long hi = std::lower_bound(ghosts.begin(), ghosts.end(), (int)start[(size_t)q + 1]) - ghosts.begin();
-    std::vector<int> need;  // my rows with a column in q's rows (= the rows of mine q's rows reference)
-    for (long long i = 0; i < nloc; ++i)
-      for (long long k = lrp[(size_t)i]; k < lrp[(size_t)i + 1]; ++k) {
-        const long long col = (long long)ci[k];
-        if (col >= start[(size_t)q] && col < start[(size_t)q + 1]) {
-          need.push_back((int)i);
-          break;
-        }
-      }
-    if (hi == lo && need.empty()) continue;
-    op->nb_rank.push_back(q);
-    op->recv_off.push_back(lo);
-    op->recv_cnt.push_back(hi - lo);
-    op->send_off.push_back((long long)send_idx.size());
-    op->send_cnt.push_back((long long)need.size());
-    for (int r : need) send_idx.push_back(r);
-  }
-  // The lists are consistent only if the pattern is symmetric across ranks: check
-  // it before any point-to-point exchange (a mismatch would hang NCCL). Every rank
-  // contributes its row of the P x P "receive from" and "send to" count matrices;
-  // after the all-reduce recv[a][b] must equal send[b][a] everywhere.
-  {
-    std::vector<double> cnt(2 * (size_t)P * P, 0.0);
-    for (size_t i = 0; i < op->nb_rank.size(); ++i) {
-      cnt[(size_t)me * P + op->nb_rank[i]] = (double)op->recv_cnt[i];
-      cnt[(size_t)P * P + (size_t)me * P + op->nb_rank[i]] = (double)op->send_cnt[i];
-    }
-    const int chunk = S_E2 - S_DOT + 1;  // scratch slots S_DOT .. S_E2
-    for (size_t b0 = 0; b0 < cnt.size(); b0 += (size_t)chunk) {
-      const int k = (int)std::min<size_t>((size_t)chunk, cnt.size() - b0);
-      allreduce_host(c, cnt.data() + b0, cnt.data() + b0, k);
-    }
-    for (int a = 0; a < P; ++a)
-      for (int q = 0; q < P; ++q)
-        if (cnt[(size_t)a * P + q] != cnt[(size_t)P * P + (size_t)q * P + a])
-          fail(PCGX_ERR_INVALID, "CsrMatrix: block rows are not symmetric: rank " + std::to_string(a) +
-                                     " needs " + std::to_string((long long)cnt[(size_t)a * P + q]) +
-                                     " values of rank " + std::to_string(q) + ", which would send " +
-                                     std::to_string((long long)cnt[(size_t)P * P + (size_t)q * P + a]));
-  }
-  op->kind = 1;
-  op->n_global = n;
-  op->nnz = nnz;  // this rank's rows
-  op->row0 = r0;
-  op->n_local = nloc;
-  op->nghost = (long long)ghosts.size();
-  op->nsend = (long long)send_idx.size();
-  PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * (size_t)(nloc + std::max(op->nghost, 1LL))));
-  PCGX_CUDA(cudaMemcpy(op->dvec, dv.data(), sizeof(double) * (size_t)nloc, cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMalloc(&op->rp, sizeof(int) * lrp.size()));
-  PCGX_CUDA(cudaMemcpy(op->rp, lrp.data(), sizeof(int) * lrp.size(), cudaMemcpyHostToDevice));
-  const size_t ng = (size_t)std::max(op->nghost, 1LL), nsd = (size_t)std::max(op->nsend, 1LL);
-  PCGX_CUDA(cudaMalloc(&op->send_idx, sizeof(int) * nsd));
-  if (op->nsend)
-    PCGX_CUDA(cudaMemcpy(op->send_idx, send_idx.data(), sizeof(int) * send_idx.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMalloc(&op->sbuf_z, sizeof(double) * nsd));
-  PCGX_CUDA(cudaMalloc(&op->sbuf_p, sizeof(double) * nsd));
-  PCGX_CUDA(cudaMalloc(&op->ghost_z, sizeof(double) * ng));
-  PCGX_CUDA(cudaMalloc(&op->ghost_p, sizeof(double) * ng));
-  PCGX_CUDA(cudaDeviceSynchronize());  // legacy-stream uploads before the compute stream
-  // the ghost columns' Jacobi values from their owners, through the block-row exchange
-  if (op->nsend)
-    pack_kernel<<<vec_grid(c, op->nsend), kVecThreads, 0, c->s>>>(op->nsend, op->send_idx, op->dvec,
-                                                                   op->sbuf_z);
-  check_launch();
-  const double* sb[1] = {op->sbuf_z};
-  double* gb[1] = {op->ghost_z};
-  c->cm->sparse_xchg(c, op, 1, sb, gb);
-  c->cm->halo_wait(c);
-  if (op->nghost)
-    PCGX_CUDA(cudaMemcpyAsync(op->dvec + nloc, op->ghost_z, sizeof(double) * (size_t)op->nghost,
-                              cudaMemcpyDeviceToDevice, c->s));
-  PCGX_CUDA(cudaStreamSynchronize(c->s));
-  // whole 3 x 3 block rows with block-aligned ghost columns keep BSR-3 (a per-rank
-  // choice: the exchange lists do not depend on the storage)
-  if (op->tune.bsr != 0 && r0 % 3 == 0 && is_bsr3(nloc, lrp, lci)) build_bsr3(op, nloc, lrp, lci, va);
-  else build_sell(op, nloc, lrp, lci, va);
-}
-
-// SELL-32 arrays of an int32 CSR (n rows, local column space) -> op (see sell_kernel).
-void build_sell(pcgx_operator op, long long n, const std::vector<int>& rp32,
-                const std::vector<int>& ci32, const double* va) {
-  const long long ns = (n + 31) / 32;
-  std::vector<long long> sp((size_t)ns + 1, 0);
-  std::vector<int> rl((size_t)std::max(n, 1LL));
-  for (long long sI = 0; sI < ns; ++sI) {
-    int L = 0;
-    for (long long r = sI * 32; r < std::min(n, sI * 32 + 32); ++r) {
-      rl[(size_t)r] = rp32[(size_t)r + 1] - rp32[(size_t)r];
-      L = std::max(L, rl[(size_t)r]);
-    }
-    sp[(size_t)sI + 1] = sp[(size_t)sI] + 32LL * L;
-  }
-  const long long tot = sp[(size_t)ns];
-  std::vector<int> scol((size_t)std::max(tot, 1LL), 0);
-  std::vector<double> sval((size_t)std::max(tot, 1LL), 0.0);
-#pragma omp parallel for schedule(static)
-  for (long long sI = 0; sI < ns; ++sI)
-    for (long long r = sI * 32; r < std::min(n, sI * 32 + 32); ++r) {
-      const long long lane = r - sI * 32;
-      for (int k = 0; k < rl[(size_t)r]; ++k) {
-        const long long src = rp32[(size_t)r] + k;
-        const long long dst = sp[(size_t)sI] + 32LL * k + lane;
-        scol[(size_t)dst] = ci32[(size_t)src];
-        sval[(size_t)dst] = va[src];
-      }
-    }
-  op->nslices = (int)ns;
-  PCGX_CUDA(cudaMalloc(&op->sell_ptr, sizeof(long long) * sp.size()));
-  PCGX_CUDA(cudaMalloc(&op->sell_len, sizeof(int) * rl.size()));
-  PCGX_CUDA(cudaMalloc(&op->sell_col, sizeof(int) * scol.size()));
-  PCGX_CUDA(cudaMalloc(&op->sell_val, sizeof(double) * sval.size()));
-  PCGX_CUDA(cudaMemcpy(op->sell_ptr, sp.data(), sizeof(long long) * sp.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMemcpy(op->sell_len, rl.data(), sizeof(int) * rl.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMemcpy(op->sell_col, scol.data(), sizeof(int) * scol.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMemcpy(op->sell_val, sval.data(), sizeof(double) * sval.size(), cudaMemcpyHostToDevice));
-  op->sell_padded = tot;
-  // slices that touch no ghost column (local columns are < n): run while the halo travels
-  int b0 = (int)ns, b1 = 0;
-  for (long long sI = 0; sI < ns; ++sI) {
-    bool ghost = false;
-    for (long long r = sI * 32; r < std::min(n, sI * 32 + 32) && !ghost; ++r)
-      for (int k = rp32[(size_t)r]; k < rp32[(size_t)r + 1]; ++k)
-        if (ci32[(size_t)k] >= n) {
-          ghost = true;
-          break;
-        }
-    if (ghost) {
-      b0 = std::min(b0, (int)sI);
-      b1 = std::max(b1, (int)sI + 1);
-    }
-  }
-  if (b0 >= b1) {  // no ghost anywhere
-    op->sl_b0 = 0;
-    op->sl_b1 = (int)ns;
-  } else {  // ghost slices are a prefix and a suffix for block rows: interior in between
-    int lead = 0;
-    while (lead < (int)ns) {
-      bool ghost = false;
-      for (long long r = (long long)lead * 32; r < std::min(n, (long long)lead * 32 + 32) && !ghost; ++r)
-        for (int k = rp32[(size_t)r]; k < rp32[(size_t)r + 1]; ++k)
-          if (ci32[(size_t)k] >= n) {
-            ghost = true;
-            break;
-          }
-      if (!ghost) break;
-      ++lead;
-    }
-    int trail = (int)ns;
-    while (trail > lead) {
-      bool ghost = false;
-      const long long sI = trail - 1;
-      for (long long r = sI * 32; r < std::min(n, sI * 32 + 32) && !ghost; ++r)
-        for (int k = rp32[(size_t)r]; k < rp32[(size_t)r + 1]; ++k)
-          if (ci32[(size_t)k] >= n) {
-            ghost = true;
-            break;
-          }
-      if (!ghost) break;
-      --trail;
-    }
-    // any ghost slice strictly inside [lead, trail) forces the whole range after the halo
-    bool inner_ghost = false;
-    for (long long sI = lead; sI < trail && !inner_ghost; ++sI)
-      for (long long r = sI * 32; r < std::min(n, sI * 32 + 32) && !inner_ghost; ++r)
-        for (int k = rp32[(size_t)r]; k < rp32[(size_t)r + 1]; ++k)
-          if (ci32[(size_t)k] >= n) {
-            inner_ghost = true;
-            break;
-          }
-    op->sl_b0 = inner_ghost ? 0 : lead;
-    op->sl_b1 = inner_ghost ? 0 : trail;
-  }
-}
-
-// Rows in aligned triples (3I, 3I+1, 3I+2) sharing one pattern of full 3x3 blocks
-// (columns 3J, 3J+1, 3J+2 consecutive): the 3-dof-per-node block structure.
-bool is_bsr3(long long n, const std::vector<int>& rp, const std::vector<int>& ci) {
-  if (n <= 0 || n % 3) return false;
-  const long long nb = n / 3;
-  int ok = 1;
-#pragma omp parallel for schedule(static) reduction(&& : ok)
-  for (long long I = 0; I < nb; ++I) {
-    if (!ok) continue;
-    const long long a = 3 * I;
-    const int len = rp[(size_t)a + 1] - rp[(size_t)a];
-    bool good = len % 3 == 0;
-    for (int c = 1; c < 3 && good; ++c) good = rp[(size_t)a + c + 1] - rp[(size_t)a + c] == len;
-    for (int k = 0; k < len && good; k += 3) {
-      const int c0 = ci[(size_t)rp[(size_t)a] + k];
-      good = c0 % 3 == 0;
-      for (int c = 0; c < 3 && good; ++c)
-        for (int d = 0; d < 3 && good; ++d) good = ci[(size_t)rp[(size_t)a + c] + k + d] == c0 + d;
-    }
-    ok = ok && good;
-  }
-  return ok != 0;
-}
-
-// The sorted set of column offsets (col - row) if it has at most kDiaMax members.
-// (rows [row_base, row_base + n) of a larger matrix: rp is local, ci global)
-bool dia_offsets(long long n, const std::vector<int>& rp, const std::vector<int>& ci,
-                 std::vector<int>& off, long long row_base) {
-  off.clear();
-  // rows mostly repeat their neighbour's offset pattern: only new patterns are merged
-  int pa = 0, pb = 0;  // previous row's entries [pa, pb) and its row index
-  long long prow = -1;
-  for (long long i = 0; i < n; ++i) {
-    const int a = rp[(size_t)i], b = rp[(size_t)i + 1];
-    bool same = prow >= 0 && b - a == pb - pa;
-    for (int k = 0; k < b - a && same; ++k)
-      same = (long long)ci[(size_t)(a + k)] - i == (long long)ci[(size_t)(pa + k)] - prow;
-    if (!same)
-      for (int k = a; k < b; ++k) {
-        const long long o = (long long)ci[(size_t)k] - (i + row_base);
-        if (std::find(off.begin(), off.end(), (int)o) == off.end()) {
-          if ((int)off.size() == kDiaMax) return false;
-          off.push_back((int)o);
-        }
-      }
-    pa = a;
-    pb = b;
-    prow = i;
-  }
-  std::sort(off.begin(), off.end());
-  return !off.empty();
-}
-
-// dia3_kernel applies when the matrix lives on a cubic nx^3 grid in the
-// reference's index order, its column offsets are exactly DiaPat<P>'s (slot s =
-// grid neighbour s) and no coupling wraps across a grid face.
-template <int P>
-bool dia3_match(long long n, int nx, const std::vector<int>& rp, const std::vector<int>& ci,
-                const std::vector<int>& off, long long row_base) {
-  using Pat = DiaPat<P>;
-  if ((int)off.size() != Pat::K) return false;
-  const long long nxy = (long long)nx * nx;
-  for (int s = 0; s < Pat::K; ++s)
-    if ((long long)off[(size_t)s] != Pat::dz(s) * nxy + Pat::dy(s) * (long long)nx + Pat::dx(s)) return false;
-  int ok = 1;
-#pragma omp parallel for schedule(static) reduction(&& : ok)
-  for (long long rl = 0; rl < n; ++rl) {
-    const long long r = rl + row_base;
-    const int a = (int)(r % nx), b = (int)((r / nx) % nx), c = (int)(r / nxy);
-    for (int k = rp[(size_t)rl]; k < rp[(size_t)rl + 1]; ++k) {
-      const long long o = (long long)ci[(size_t)k] - r;
-      int s = 0;
-      while (s < Pat::K && off[(size_t)s] != o) ++s;
-      const int aa = a + Pat::dx(s), bb = b + Pat::dy(s), cc = c + Pat::dz(s);
-      if (aa < 0 || aa >= nx || bb < 0 || bb >= nx || cc < 0 || cc >= nx) ok = 0;
-    }
-  }
-  return ok != 0;
-}
-
-void dia3_detect(pcgx_operator op, long long n, const std::vector<int>& rp, const std::vector<int>& ci,
-                 const std::vector<int>& off) {
-  op->dia3_pat = 0;
-  int nx = (int)std::llround(std::cbrt((double)n));
-  while ((long long)nx * nx * nx > n) --nx;
-  while ((long long)(nx + 1) * (nx + 1) * (nx + 1) <= n) ++nx;
-  if (nx < 3 || (long long)nx * nx * nx != n) return;
-  if (dia3_match<27>(n, nx, rp, ci, off)) op->dia3_pat = 27;
-  else if (dia3_match<7>(n, nx, rp, ci, off)) op->dia3_pat = 7;
-  op->dia3_nx = nx;
-}
-
-// Offset-storage arrays (see dia_kernel).
-void build_dia(pcgx_operator op, long long n, const std::vector<int>& rp32,
-               const std::vector<int>& ci32, const double* va, const std::vector<int>& off) {
-  const int K = (int)off.size();
-  const long long ld = (n + 31) / 32 * 32;  // rows incl. the last slice's padding
-  std::vector<double> val((size_t)(ld * K), 0.0);
-  std::vector<unsigned> mask((size_t)n, 0u);
-#pragma omp parallel for schedule(static)
-  for (long long i = 0; i < n; ++i) {
-    int q = 0;
-    for (int k = rp32[(size_t)i]; k < rp32[(size_t)i + 1]; ++k) {
-      const int o = (int)((long long)ci32[(size_t)k] - i);
-      while (off[(size_t)q] != o) ++q;  // both ascending
-      val[(size_t)(q * ld + i)] = va[k];
-      mask[(size_t)i] |= 1u << q;
-    }
-  }
-  op->dia_k = K;
-  op->dia_ld = ld;
-  dia3_detect(op, n, rp32, ci32, off);
-  for (int k = 0; k < K; ++k) op->dia_off[k] = off[(size_t)k];
-  PCGX_CUDA(cudaMalloc(&op->dia_val, sizeof(double) * val.size()));
-  PCGX_CUDA(cudaMalloc(&op->dia_mask, sizeof(unsigned) * mask.size()));
-  PCGX_CUDA(cudaMemcpy(op->dia_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMemcpy(op->dia_mask, mask.data(), sizeof(unsigned) * mask.size(), cudaMemcpyHostToDevice));
-}
-
-// The bsr3t_kernel's grid copy of a BSR-3 matrix whose nodes form a cubic nx^3
-// grid (nx % 4 == 0, nx >= 36: TMA strides and boxes) and whose blocks lie in the
-// 27-point box without wrapping across a face; built slot by slot (one 9 ldn
-// host buffer at a time) so the host never holds a second full copy.
-void bsr3_grid_build(pcgx_operator op, long long n, const std::vector<int>& rp32,
-                     const std::vector<int>& ci32, const double* va) {
-  if (op->tune.bsr3t == 0) return;
-  const long long nb = n / 3;
-  long long nx = (long long)std::llround(std::cbrt((double)nb));
-  while (nx * nx * nx > nb) --nx;
-  while ((nx + 1) * (nx + 1) * (nx + 1) <= nb) ++nx;
-  if (nx * nx * nx != nb || nx % 4 != 0 || nx < kB3PX / 3) return;
-  const long long nxy = nx * nx;
-  std::vector<signed char> pos((size_t)nb * 27, (signed char)-1);  // block index of slot s
-  int ok = 1;
-#pragma omp parallel for schedule(static) reduction(&& : ok)
-  for (long long b = 0; b < nb; ++b) {
-    const int a = (int)(b % nx), bb = (int)((b / nx) % nx), cc = (int)(b / nxy);
-    const int len = (rp32[(size_t)(3 * b + 1)] - rp32[(size_t)(3 * b)]) / 3;
-    for (int k = 0; k < len && ok; ++k) {
-      const long long o = (long long)(ci32[(size_t)rp32[(size_t)(3 * b)] + 3 * k] / 3) - b;
-      int s = -1;
-      for (int q = 0; q < 27; ++q)
-        if (o == (q / 9 - 1) * nxy + ((q / 3) % 3 - 1) * nx + (q % 3 - 1)) s = q;
-      if (s < 0) { ok = 0; break; }
-      const int x2 = a + s % 3 - 1, y2 = bb + (s / 3) % 3 - 1, z2 = cc + s / 9 - 1;
-      if (x2 < 0 || x2 >= nx || y2 < 0 || y2 >= nx || z2 < 0 || z2 >= nx) { ok = 0; break; }
-      pos[(size_t)(b * 27 + s)] = (signed char)k;
-    }
-  }
-  if (!ok) return;
-  const long long ldn = (nb + 31) / 32 * 32;
-  std::vector<unsigned> mask((size_t)nb, 0u);
-#pragma omp parallel for schedule(static)
-  for (long long b = 0; b < nb; ++b)
-    for (int s = 0; s < 27; ++s)
-      if (pos[(size_t)(b * 27 + s)] >= 0) mask[(size_t)b] |= 1u << s;
-  PCGX_CUDA(cudaMalloc(&op->b3g_val, sizeof(double) * (size_t)(243 * ldn)));
-  PCGX_CUDA(cudaMalloc(&op->b3g_mask, sizeof(unsigned) * (size_t)nb));
-  PCGX_CUDA(cudaMemcpy(op->b3g_mask, mask.data(), sizeof(unsigned) * (size_t)nb, cudaMemcpyHostToDevice));
-  std::vector<double> buf((size_t)(9 * ldn));
-  for (int s = 0; s < 27; ++s) {
-#pragma omp parallel for schedule(static)
-    for (long long b = 0; b < ldn; ++b) {
-      const int k = b < nb ? pos[(size_t)(b * 27 + s)] : -1;
-      for (int c = 0; c < 3; ++c)
-        for (int d = 0; d < 3; ++d)
-          buf[(size_t)((3 * c + d) * ldn + b)] = k >= 0 ? va[(size_t)rp32[(size_t)(3 * b + c)] + 3 * k + d] : 0.0;
-    }
-    PCGX_CUDA(cudaMemcpy(op->b3g_val + (size_t)(9 * s * ldn), buf.data(), sizeof(double) * buf.size(),
-                         cudaMemcpyHostToDevice));
-  }
-  op->b3g_ld = ldn;
-  op->b3g_nx = (int)nx;
-}
-
-// BSR-3 / SELL-32 arrays (see bsr3_kernel) of an int32 CSR with is_bsr3 structure.
-void build_bsr3(pcgx_operator op, long long n, const std::vector<int>& rp32,
-                const std::vector<int>& ci32, const double* va) {
-  const long long nb = n / 3;
-  const long long ns = (nb + 31) / 32;
-  std::vector<long long> sp((size_t)ns + 1, 0);
-  std::vector<int> bl((size_t)nb);
-  for (long long sI = 0; sI < ns; ++sI) {
-    int L = 0;
-    for (long long b = sI * 32; b < std::min(nb, sI * 32 + 32); ++b) {
-      bl[(size_t)b] = (rp32[(size_t)(3 * b + 1)] - rp32[(size_t)(3 * b)]) / 3;
-      L = std::max(L, bl[(size_t)b]);
-    }
-    sp[(size_t)sI + 1] = sp[(size_t)sI] + 32LL * L;
-  }
-  const long long tot = sp[(size_t)ns];
-  std::vector<int> bcol((size_t)std::max(tot, 1LL), 0);
-  std::vector<double> bval((size_t)std::max(tot, 1LL) * 9, 0.0);
-#pragma omp parallel for schedule(static)
-  for (long long sI = 0; sI < ns; ++sI)
-    for (long long b = sI * 32; b < std::min(nb, sI * 32 + 32); ++b) {
-      const long long lane = b - sI * 32;
-      for (int k = 0; k < bl[(size_t)b]; ++k) {
-        const long long slot = sp[(size_t)sI] + 32LL * k;
-        bcol[(size_t)(slot + lane)] = ci32[(size_t)rp32[(size_t)(3 * b)] + 3 * k] / 3;
-        for (int c = 0; c < 3; ++c)
-          for (int d = 0; d < 3; ++d)
-            bval[(size_t)(slot * 9 + 32 * (3 * c + d) + lane)] =
-                va[(size_t)rp32[(size_t)(3 * b + c)] + 3 * k + d];
-      }
-    }
-  op->bsr_slices = (int)ns;
-  op->bsr_blocks = (long long)rp32[(size_t)n] / 9;
-  op->bsr_padded = tot;
-  PCGX_CUDA(cudaMalloc(&op->bsr_ptr, sizeof(long long) * sp.size()));
-  PCGX_CUDA(cudaMalloc(&op->bsr_len, sizeof(int) * bl.size()));
-  PCGX_CUDA(cudaMalloc(&op->bsr_col, sizeof(int) * bcol.size()));
-  PCGX_CUDA(cudaMalloc(&op->bsr_val, sizeof(double) * bval.size()));
-  PCGX_CUDA(cudaMemcpy(op->bsr_ptr, sp.data(), sizeof(long long) * sp.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMemcpy(op->bsr_len, bl.data(), sizeof(int) * bl.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMemcpy(op->bsr_col, bcol.data(), sizeof(int) * bcol.size(), cudaMemcpyHostToDevice));
-  PCGX_CUDA(cudaMemcpy(op->bsr_val, bval.data(), sizeof(double) * bval.size(), cudaMemcpyHostToDevice));
-  bsr3_grid_build(op, n, rp32, ci32, va);
-}
-
-template <class IdxT>
-void csr_upload(pcgx_context c, pcgx_operator op, long long n, const IdxT* rp, const IdxT* ci,
-                const double* va, const double* inv_sqrt) {
-  if (n < 0) fail(PCGX_ERR_INVALID, "LinearOperator: negative dimension");
-  if (!rp || (n > 0 && (!ci || !va)) ) fail(PCGX_ERR_INVALID, "CsrMatrix: null array");
-  if (rp[0] != 0) fail(PCGX_ERR_INVALID, "CsrMatrix: row_ptr must have length n+1 and start at 0");
-  const long long nnz = (long long)rp[n];
-  if (nnz >= (1LL << 31) || n >= (1LL << 31))
-    fail(PCGX_ERR_OVERFLOW, "csr_create: nnz " + std::to_string(nnz) +
-                                " does not fit the int32 device CSR");
-  std::vector<int> rp32((size_t)n + 1);
-  std::vector<int> ci32((size_t)nnz);
-  std::vector<double> dv((size_t)std::max(n, 1LL));
-  for (long long i = 0; i < n; ++i) {
-    if (rp[i + 1] < rp[i]) fail(PCGX_ERR_INVALID, "CsrMatrix: row_ptr not nondecreasing");
-    double diag = 0.0;
-    for (long long k = rp[i]; k < rp[i + 1]; ++k) {
-      const long long col = (long long)ci[k];
-      if (col < 0 || col >= n)
-        fail(PCGX_ERR_INVALID, "CsrMatrix: column index out of range in row " + std::to_string(i));
-      if (k > rp[i] && col <= (long long)ci[k - 1])
-        fail(PCGX_ERR_INVALID, "CsrMatrix: columns not strictly increasing in row " + std::to_string(i));
-      if (col == i) diag = va[k];
-      ci32[(size_t)k] = (int)col;
-    }
-    rp32[(size_t)i + 1] = (int)rp[i + 1];
-    if (inv_sqrt) {
-      dv[(size_t)i] = inv_sqrt[i];
-    } else {  // jacobi_scale (linop.cpp:340-351)
-      if (!(diag > 0.0))
-        fail(PCGX_ERR_NUMERICAL, "jacobi_scale: nonpositive diagonal entry at index " +
-                                     std::to_string(i) + " (" + std::to_string(diag) + ")");
-      dv[(size_t)i] = 1.0 / std::sqrt(diag);
-    }
-  }
-  op->kind = 1;
-  op->n_global = n;
-  op->nnz = nnz;
-  if (c->nranks > 1) {
-    csr_upload_block(c, op, n, rp32, ci32, va, dv);
-    return;
-  }
-  op->n_local = n;
-  PCGX_CUDA(cudaMalloc(&op->rp, sizeof(int) * (size_t)(n + 1)));
-  // +8 entries of padding: the TMA tile copies round their length up to 4 entries
-  PCGX_CUDA(cudaMalloc(&op->ci, sizeof(int) * (size_t)(nnz + 8)));
-  PCGX_CUDA(cudaMalloc(&op->va, sizeof(double) * (size_t)(nnz + 8)));
-  PCGX_CUDA(cudaMemset(op->ci, 0, sizeof(int) * (size_t)(nnz + 8)));
-  PCGX_CUDA(cudaMemset(op->va, 0, sizeof(double) * (size_t)(nnz + 8)));
-  PCGX_CUDA(cudaMalloc(&op->dvec, sizeof(double) * (size_t)std::max(n, 1LL)));
-  PCGX_CUDA(cudaMemcpy(op->rp, rp32.data(), sizeof(int) * (size_t)(n + 1), cudaMemcpyHostToDevice));
-  if (nnz) {
-    PCGX_CUDA(cudaMemcpy(op->ci, ci32.data(), sizeof(int) * (size_t)nnz, cudaMemcpyHostToDevice));
-    PCGX_CUDA(cudaMemcpy(op->va, va, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice));
-  }
-  if (n) PCGX_CUDA(cudaMemcpy(op->dvec, dv.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice));
-  std::vector<int> doff;
-  // offset storage moves fewer bytes than int32 CSR while 8 K n + 4 n < 12 nnz + 4 n
-  const bool dia = n > 0 && op->tune.dia != 0 && dia_offsets(n, rp32, ci32, doff) &&
-                   (double)doff.size() * (double)n <= 1.5 * (double)nnz;
-  if (dia) {
-    build_dia(op, n, rp32, ci32, va, doff);
-    cudaFree(op->ci);
-    cudaFree(op->va);
-    op->ci = nullptr;
-    op->va = nullptr;
-  } else if (n > 0 && op->tune.bsr != 0 && is_bsr3(n, rp32, ci32)) {
-    build_bsr3(op, n, rp32, ci32, va);
-    cudaFree(op->ci);
-    cudaFree(op->va);
-    op->ci = nullptr;
-    op->va = nullptr;
-  } else if (n > 0) {
-    build_sell(op, n, rp32, ci32, va);
-    // the SELL copy replaces the CSR value/index arrays on the device
-    cudaFree(op->ci);
-    cudaFree(op->va);
-    op->ci = nullptr;
-    op->va = nullptr;
-  }
-}
-
-void free_op(pcgx_operator op) {
-  if (!op) return;
-  cudaFree(op->ghost_lo);
-  cudaFree(op->ghost_hi);
-  cudaFree(op->ghost_lo2);
-  cudaFree(op->ghost_hi2);
-  cudaFree(op->rp);
-  cudaFree(op->ci);
-  cudaFree(op->va);
-  cudaFree(op->dvec);
-  cudaFree(op->sell_ptr);
-  cudaFree(op->sell_len);
-  cudaFree(op->sell_col);
-  cudaFree(op->sell_val);
-  cudaFree(op->bsr_ptr);
-  cudaFree(op->bsr_len);
-  cudaFree(op->bsr_col);
-  cudaFree(op->bsr_val);
-  cudaFree(op->b3g_val);
-  cudaFree(op->b3g_mask);
-  cudaFree(op->dia_val);
-  cudaFree(op->dia_mask);
-  cudaFree(op->dia3_dlo);
-  cudaFree(op->dia3_dhi);
-  cudaFree(op->send_idx);
-  cudaFree(op->sbuf_z);
-  cudaFree(op->sbuf_p);
-  cudaFree(op->ghost_z);
-  cudaFree(op->ghost_p);
-  delete op;
-}
-
-void ctx_init(pcgx_context c) {
-  c->tune = Tuning::from_env();
-  PCGX_CUDA(cudaSetDevice(c->device));
-  PCGX_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
-  PCGX_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
-  PCGX_CUDA(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
-  PCGX_CUDA(cudaMalloc(&c->S, sizeof(double) * kSlots));
-  PCGX_CUDA(cudaMemset(c->S, 0, sizeof(double) * kSlots));
-  PCGX_CUDA(cudaHostAlloc(&c->hS, sizeof(double) * kSlots, cudaHostAllocMapped));
-  PCGX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dS_map), c->hS, 0));
-  PCGX_CUDA(cudaMalloc(&c->partials, sizeof(double) * kMaxBlocks));
-  PCGX_CUDA(cudaMalloc(&c->counter, sizeof(unsigned) * 4));
-  PCGX_CUDA(cudaMemset(c->counter, 0, sizeof(unsigned) * 4));
-  PCGX_CUDA(cudaEventCreate(&c->ev_t0));
-  PCGX_CUDA(cudaEventCreate(&c->ev_t1));
-  PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming));
-  PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-  PCGX_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-  // the legacy-stream memsets above are unordered with the non-blocking streams
-  PCGX_CUDA(cudaDeviceSynchronize());
-}
-
-// The matrix-free 7-point operator's fields (frees op on failure).
-void stencil_setup(pcgx_context c, pcgx_operator op, int64_t nx, int64_t ny, int64_t nz, double inv_sqrt_diag) {
-  {
-    op->kind = 0;
-    op->nx = nx;
-    op->ny = ny;
-    op->nz = nz;
-    int64_t z0 = 0, nzl = 0;
-    pcgx_slab_partition(nz, c->nranks, c->rank, &z0, &nzl);
-    op->nzl = nzl;
-    op->z0 = z0;
-    op->n_global = nx * ny * nz;
-    op->n_local = nx * ny * op->nzl;
-    op->nnz = 7 * op->n_global - 2 * (ny * nz + nx * nz + nx * ny);
-    op->d = inv_sqrt_diag > 0.0 ? inv_sqrt_diag : 1.0 / std::sqrt(6.0);
-    op->kz = default_kz(c, nx, ny, op->nzl);
-    op->vec2 = (nx % 2 == 0);
-    op->pfd = op->tune.pfd;
-    op->cheb2 = op->vec2 && op->tune.cheb2 != 0;
-    op->kz2 = op->tune.kz2;
-    op->c2plan = op->tune.c2plan;
-    try {
-      init_stencil_ghosts(c, op);
-      if (c->nranks > 1 && op->nzl < 2) op->cheb2 = false;  // 2-plane halos need >= 2 planes
-      op->zpad = (op->cheb2 && c->nranks > 1) ? 2 : 0;
-      op->cheb3 = op->cheb2 && c->nranks == 1 && op->tune.cheb3 != 0;
-    } catch (...) {
-      free_op(op);
-      throw;
-    }
-  }
-}
-
-// Whether a CSR matrix is exactly assemble_laplacian(lap3d, nx) (linop.cpp:299-331):
-// cubic n = nx^3, every row the 7-point star in ascending columns with the
-// Dirichlet neighbours omitted, diagonal 6 and off-diagonals -1, and (if given) the
-// Jacobi vector 1/sqrt(6). Its scaled apply is then bitwise the StencilOperator's
-// (test_linop.cpp:67-79), so the matrix-free kernels can serve it. Opt-in
-// (PCGX_CSR_STENCIL=1): a CsrMatrix input is benchmarked as CSR (config 1 keeps its
-// offset storage and reads its values), this is a user-side shortcut.
-template <class I>
-bool csr_is_lap3d(int64_t n, const I* rp, const I* ci, const double* va, const double* isd, int64_t* nx_out) {
-  if (n < 8) return false;
-  int64_t nx = (int64_t)std::llround(std::cbrt((double)n));
-  while (nx * nx * nx > n) --nx;
-  while ((nx + 1) * (nx + 1) * (nx + 1) <= n) ++nx;
-  if (nx * nx * nx != n || nx < 2) return false;
-  const int64_t nxy = nx * nx;
-  const double d6 = 1.0 / std::sqrt(6.0);
-  int ok = 1;
-#pragma omp parallel for schedule(static) reduction(&& : ok)
-  for (int64_t r = 0; r < n; ++r) {
-    if (!ok) continue;
-    const int64_t i = r % nx, j = (r / nx) % nx, k = r / nxy;
-    const int64_t off[7] = {-nxy, -nx, -1, 0, 1, nx, nxy};
-    const bool on[7] = {k > 0, j > 0, i > 0, true, i < nx - 1, j < nx - 1, k < nx - 1};
-    int64_t p = (int64_t)rp[r];
-    for (int s = 0; s < 7 && ok; ++s) {
-      if (!on[s]) continue;
-      if (p >= (int64_t)rp[r + 1] || (int64_t)ci[p] != r + off[s] || va[p] != (s == 3 ? 6.0 : -1.0)) ok = 0;
-      ++p;
-    }
-    if (p != (int64_t)rp[r + 1]) ok = 0;
-    if (isd && isd[r] != d6) ok = 0;
-  }
-  if (ok) *nx_out = nx;
-  return ok != 0;
-}
-
-template <class I>
-void csr_create_any(pcgx_context c, pcgx_operator op, int64_t n, const I* rp, const I* ci, const double* va,
-                    const double* isd) {
-  int64_t nx = 0;
-  if (c->nranks == 1 && rp && ci && va && op->tune.csr_stencil != 0 &&
-      csr_is_lap3d(n, rp, ci, va, isd, &nx)) {
-    stencil_setup(c, op, nx, nx, nx, 1.0 / std::sqrt(6.0));
-    op->nnz = (int64_t)rp[n];
-    return;
-  }
-  try {
-    csr_upload(c, op, n, rp, ci, va, isd);
-  } catch (...) {
-    free_op(op);
-    throw;
-  }
-}
-
+#include "host_create.cuh"
 }  // namespace
 
 // ============================================================================ C ABI
