@@ -273,13 +273,14 @@ void pcg_solve_device(pcgx_context c, pcgx_operator op, const Prec& prec, const 
   // stored (the update kernel only reduces r'z): 8 B less per unknown and iteration
   const bool zdiv = zm == 1 && fuse && dir_tma_ok(op) && op->tune.zdiv != 0;
   const double* zvec = (zm == 2 || zdiv) ? r : z;
-  // single-rank stencil: x += alpha p moves from the update kernel into the next
+  // TMA direction step (stencil): x += alpha p moves from the update kernel into the next
   // direction step, which reads p_old anyway (8 B less per unknown and iteration)
   // (not with on_iterate: x must be current at every iteration's callback)
   const bool cb = opts.on_iterate != nullptr;
   const bool defer_x = fuse && dir_tma_ok(op) && op->tune.defer_x != 0 && !cb;
-  // one GPU, Chebyshev m >= 3 on the stencil: the update r -= alpha q, r'r rides in
-  // the first two-step pass of P r (cheb2f_upd_launch); r(it) lives in Rb[it & 1]
+  // Chebyshev m >= 3 on the stencil (one GPU, or z-slab ranks with two ghost planes):
+  // the update r -= alpha q, r'r rides in the first two-step pass of P r
+  // (cheb2f_upd_launch); r(it) lives in Rb[it & 1]
   const bool fuse_upd = zm == 0 && prec.kind == 1 && (spec_after_update || c->cm != nullptr) && defer_x &&
                         cheb_upd_ok(c, op, m);
   double* Rb[2] = {r, fuse_upd ? c->r2 : r};

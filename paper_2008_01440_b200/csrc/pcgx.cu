@@ -1497,7 +1497,7 @@ void cheb2_pass(pcgx_context c, pcgx_operator op, const double* A, const double*
 }
 
 // The PCG update r(it) = r(it-1) - alpha q(it) and r'r fused into the first
-// two-step pass of P r(it) (pipelined kernel, single rank): the pass reads r(it-1)
+// two-step pass of P r(it) (pipelined kernel; one GPU or a z-slab rank): the pass reads r(it-1)
 // and q(it) through TMA, forms r(it) in shared memory (bitwise the update kernel's
 // element operations), writes it to rnew and reduces r'r into s_rr. Saves the
 // update launch and 8 B per unknown and iteration.
