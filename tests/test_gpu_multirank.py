@@ -230,3 +230,35 @@ def test_slab_fused_update_matches_update_kernel(pcgx, nranks, dims, m, monkeypa
     assert (rf.ddot, rf.matvec) == (ru.ddot, ru.matvec)
     assert rel_norm(xf, xu) <= 1e-12
     assert rf.kernel_launches < ru.kernel_launches
+
+
+@pytest.mark.parametrize("nranks,m", [(3, 6), (2, 5)])
+def test_slab_solve_stopped_by_maxit_matches_oracle(pcgx, oracle, nranks, m):
+    """An iteration-limited solve on slab ranks (fused update in P r's first pass,
+    the last iteration's update as a kernel of its own, the deferred x update flushed
+    at the exit): x and the residuals after exactly maxit iterations match the
+    single-domain oracle stopped at the same iteration."""
+    P = pcgx
+    nx, ny, nz, maxit = 66, 24, 23, 7
+    a, b = P.analytic_extremes_box(nx, ny, nz)
+    opo = OracleOp("lap3d", nx=nx, ny=ny, nz=nz)
+    b_full = oracle.apply(opo, oracle.random_uniform(nx * ny * nz, SEED))
+    x_o, rep_o = oracle.pcg_solve(opo, oracle.cheb_params(a, b, m, 1.001), b_full, tol=1e-30, maxit=maxit)
+    ctxs = P.Context.local_group(nranks)
+
+    def rank(r, ctx):
+        op, _ = P.jacobi_scale(P.StencilOperator(nx, ny, nz), ctx)
+        lo = op.row0()
+        x, rep = P.pcg_solve(op, b_full[lo:lo + op.local_size()], P.SolveOptions(tol=1e-30, maxit=maxit),
+                             P.ChebyshevPreconditioner(P.cheb_params(a, b, m, 1.001)))
+        return x, rep
+
+    outs = run_ranks(ctxs, rank)
+    for c in ctxs:
+        c.close()
+    rep = outs[0][1]
+    assert rep.iters == maxit == rep_o["iters"] and not rep.converged
+    assert (rep.ddot, rep.matvec) == (rep_o["ddot"], rep_o["matvec"])
+    assert rel_norm(np.concatenate([o[0] for o in outs]), x_o) <= 1e-11
+    assert abs(rep.rel_res - rep_o["rel_res"]) <= 1e-12 * max(1.0, rep_o["rel_res"])
+    assert abs(rep.true_rel_res - rep_o["true_rel_res"]) <= 1e-12 * max(1.0, rep_o["true_rel_res"])
