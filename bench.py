@@ -641,7 +641,9 @@ def run_reference_cfg5(args, config, ws):
     for _ in range(args.warmup):
         sample(0, 1)
     step_t, mv, samples = [], [], []
-    for _ in range(max(1, args.steps)):
+    # at most five timed samples (each ~20 s of host work) however many steps are asked
+    # for, so the arm ends within a few minutes; ms_per_step is their mean
+    for _ in range(max(1, min(args.steps, 5))):
         rep = sample(k, 1)
         step_t.append(rep["wall_time"])
         mv.append(rep["matvec"])
@@ -658,7 +660,7 @@ def run_reference_cfg5(args, config, ws):
                    "sample": (f"bounded sample of the workload's operator and preconditioner: the reference's "
                               f"pcg_solve, k={k}, maxit=1 on a {nx}^3 cube (its StencilOperator is cubic; one "
                               f"SpMV of the full grid takes seconds on the host); value = matvecs x 16 B x "
-                              f"n_sample / time, the metric's size-independent part")},
+                              f"n_sample / time, the metric's size-independent part; at most five timed samples")},
         "samples": samples,
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": kind,
                          "sample": f"{config}: k={k}, maxit=1 on a {nx}^3 cube per step (see config)"},
